@@ -1,0 +1,146 @@
+/* foundry_b200.h — C-ABI of the B200-native Foundry LOAD path.
+ *
+ * Plain C: opaque handles, pointers and sizes; no C++ or torch types. This is
+ * the drop-in boundary a foreign binding (ctypes / cgo / JNI / N-API) binds,
+ * exported by paper_2604_06664_b200/libfoundry_b200.so. INTEGRATION.md shows
+ * the reference-side bindings.
+ *
+ * Two layers:
+ *
+ *  1. Session API — the reference's public LOAD surface, one call per
+ *     reference entry point (reference proj/bindings/module.cpp:53-60,102-134
+ *     and proj/include/foundry/pipeline.hpp:80-119):
+ *       fdy_load                 <- foundry::load(archive, LoadOptions)      pipeline.hpp:116-119
+ *       fdy_serving_replay       <- ServingContext::replay(batch)            pipeline.hpp:94
+ *                                   + LaunchTrace::to_text                   sim_driver.cpp:21-38
+ *       fdy_serving_batches      <- ServingContext::batches()                pipeline.hpp:95
+ *       fdy_serving_counter(s)   <- ServingContext::counters()               pipeline.hpp:100
+ *       fdy_serving_template_count <- ServingHandle.template_count           module.cpp:32
+ *       fdy_serving_close        <- ~ServingContext
+ *
+ *  2. Kernel API — the per-member work of the reference PrepareFn
+ *     (pipeline.cpp:506-514: parse_graph_at graph_model.cpp:295-303 +
+ *     apply_rank_patches rank_forge.cpp:132-152) and the archive integrity
+ *     pass (verify_archive_integrity pipeline.cpp:411-417), moved onto the GPU:
+ *       fdy_device_open / fdy_device_close
+ *       fdy_store_upload      pinned/pageable host -> HBM DMA of a template store
+ *       fdy_store_fanout      GPU -> GPU copy of a resident store (NVLink P2P)
+ *       fdy_materialize       K2 diff expansion + K1 relocation + K3 rank patch
+ *       fdy_members_download  HBM -> host copy of member images
+ *       fdy_crc64_segments    CRC-64/XZ of byte ranges, computed on the GPU
+ *       fdy_sync, fdy_last_error
+ *
+ * Return codes: 0 on success, otherwise 1 + the reference Errc value
+ * (errors.hpp:9-23: 1 invalid-argument ... 13 schema-violation), plus
+ * FDY_ERR_CUDA and FDY_ERR_NO_DEVICE. fdy_last_error() returns the message of
+ * the calling thread's last failure, formatted like foundry::Error::what()
+ * ("<code-name>: <step>: <detail>").
+ */
+#ifndef FOUNDRY_B200_H
+#define FOUNDRY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    FDY_OK = 0,
+    FDY_ERR_INVALID_ARGUMENT = 1,
+    FDY_ERR_SPEC_VIOLATION = 2,
+    FDY_ERR_BINARY_FORMAT = 3,
+    FDY_ERR_UNRESOLVED_KERNEL = 4,
+    FDY_ERR_UNMAPPED_ADDRESS = 5,
+    FDY_ERR_TOPOLOGY_MISMATCH = 6,
+    FDY_ERR_LAYOUT_DIVERGENCE = 7,
+    FDY_ERR_ARCHIVE_CORRUPTION = 8,
+    FDY_ERR_OUT_OF_REGION = 9,
+    FDY_ERR_UNKNOWN_ADDRESS = 10,
+    FDY_ERR_DEVICE_STATE_UNINITIALIZED = 11,
+    FDY_ERR_UNPATCHABLE_COMM = 12,
+    FDY_ERR_SCHEMA_VIOLATION = 13,
+    FDY_ERR_CUDA = 14,
+    FDY_ERR_NO_DEVICE = 15,
+};
+
+typedef struct fdy_device fdy_device;
+typedef struct fdy_store fdy_store;
+typedef struct fdy_members fdy_members;
+typedef struct fdy_serving fdy_serving;
+
+/* ---------------------------------------------------------------- misc */
+const char* fdy_last_error(void);
+const char* fdy_version(void);
+int fdy_device_count(void);
+
+/* ---------------------------------------------------------------- kernel API */
+int fdy_device_open(int ordinal, fdy_device** out);
+void fdy_device_close(fdy_device* dev);
+int fdy_sync(fdy_device* dev);
+
+/* Copies `bytes` of an FNDT template store (foundry/store_format.h) into HBM. */
+int fdy_store_upload(fdy_device* dev, const void* host_blob, size_t bytes, fdy_store** out);
+/* Copies a resident store to another device (peer copy over NVLink when the
+ * devices can access each other; staged otherwise). */
+int fdy_store_fanout(const fdy_store* src, fdy_device* dst_dev, fdy_store** out);
+void fdy_store_free(fdy_store* store);
+size_t fdy_store_members_bytes(const fdy_store* store);
+
+typedef struct {
+    uint32_t rank;
+    uint32_t world;
+    uint64_t new_base;        /* 0: keep the captured VA base (no relocation) */
+    const uint64_t* values;   /* optional per-rank value table (comm handles, peer buffers) */
+    uint32_t n_values;
+    int32_t grid;             /* 0: persistent grid = SMs x resident CTAs */
+} fdy_materialize_desc;
+
+/* Launches the fused materialization on the device stream. kernel_ms (may be
+ * NULL) receives the kernel's CUDA-event duration (this call then blocks). */
+int fdy_materialize(fdy_device* dev, const fdy_store* store, const fdy_materialize_desc* desc,
+                    fdy_members** out, float* kernel_ms);
+/* Reuses an existing output arena (same store) instead of allocating. */
+int fdy_materialize_into(fdy_device* dev, const fdy_store* store,
+                         const fdy_materialize_desc* desc, fdy_members* members,
+                         float* kernel_ms);
+size_t fdy_members_bytes(const fdy_members* members);
+int fdy_members_download(fdy_members* members, void* host_dst, size_t offset, size_t bytes);
+void fdy_members_free(fdy_members* members);
+
+/* CRC-64/XZ of n byte ranges of a host buffer, computed on the GPU after one
+ * H2D copy (ranges need not be aligned). digests receives n values. */
+int fdy_crc64_segments(fdy_device* dev, const void* host, size_t bytes,
+                       const uint64_t* offsets, const uint64_t* lengths, uint32_t n,
+                       uint64_t* digests, float* kernel_ms);
+
+/* ---------------------------------------------------------------- session API */
+typedef struct {
+    uint32_t rank;           /* LoadOptions.rank */
+    uint32_t world;          /* LoadOptions.world */
+    int32_t preallocate;     /* LoadOptions.preallocate (bool) */
+    uint32_t prepare_lanes;  /* LoadOptions.prepare_lanes: host threads for file staging */
+    int32_t device;          /* B200: CUDA device ordinal */
+    int32_t relocate;        /* B200: rebase embedded addresses if the VA region moves */
+    /* FaultInjection (pipeline.hpp:73-78) */
+    int32_t skip_binary_restore;
+    int32_t skip_device_init;
+    int64_t base_shift_granules;
+    int32_t extra_prewindow_alloc;
+} fdy_load_options;
+
+void fdy_load_options_init(fdy_load_options* opts);
+int fdy_load(const char* archive, const fdy_load_options* opts, fdy_serving** out);
+int fdy_serving_replay(fdy_serving* s, uint32_t batch, char* buf, size_t cap, size_t* len);
+int fdy_serving_batches(fdy_serving* s, uint32_t* out, size_t cap, size_t* count);
+int fdy_serving_counter(fdy_serving* s, const char* key, uint64_t* value);
+/* "key=value\n" lines, sorted by key. */
+int fdy_serving_counters(fdy_serving* s, char* buf, size_t cap, size_t* len);
+uint32_t fdy_serving_template_count(const fdy_serving* s);
+void fdy_serving_close(fdy_serving* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

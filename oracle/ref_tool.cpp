@@ -1,0 +1,186 @@
+// ref_tool — a thin command-line driver over the UNMODIFIED reference library
+// (/root/reference/proj, compiled by oracle/Makefile into oracle/_ref/).
+//
+// TEST INFRASTRUCTURE ONLY. Nothing in the product path links or executes
+// this; it exists so tests/ and bench.py's CPU-baseline leg can ask the
+// reference itself for ground truth:
+//
+//   save <preset|spec-file> <out-dir> [traces-file]
+//        foundry::save (pipeline.cpp:249-405); writes the SAVE self-replay
+//        traces (pipeline.cpp:326-327) to traces-file.
+//   prepare <archive> <rank> <world> <out.fndg>
+//        the reference PrepareFn for every member (pipeline.cpp:506-514):
+//        parse_graph_at (graph_model.cpp:295-303) + apply_rank_patches
+//        (rank_forge.cpp:132-152), re-serialized with serialize_graphs
+//        (graph_model.cpp:244-269) in graphs.bin locator order.
+//   replay <archive> <graphs.fndg> <delta-hex> <traces-out>
+//        replays externally materialized graphs on the reference simulated
+//        driver with the region mapped at base+delta (det_alloc.cpp:169-181,
+//        sim_driver.cpp:402-479): the reference's own hidden offsets decide
+//        whether every embedded address is live.
+//   time-load <archive> <rank> <world> <lanes> <reps> [replay]
+//        best-of-reps wall time of foundry::load (pipeline.cpp:447-557),
+//        optionally followed by serve+replay of every batch; prints JSON.
+//   crc <file>   CRC-64/XZ (hash.cpp:53-69) of a file, hex.
+//   diff <a.fndg> <b.fndg>   reference diff() text per graph pair.
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <iostream>
+#include <string>
+#include <thread>
+
+#include "foundry/binary_catalog.hpp"
+#include "foundry/det_alloc.hpp"
+#include "foundry/graph_model.hpp"
+#include "foundry/hash.hpp"
+#include "foundry/io.hpp"
+#include "foundry/pipeline.hpp"
+#include "foundry/rank_forge.hpp"
+#include "foundry/sim_driver.hpp"
+#include "foundry/workload_gen.hpp"
+
+using namespace foundry;
+namespace fs = std::filesystem;
+
+static int usage() {
+    std::fprintf(stderr,
+                 "usage: ref_tool save|prepare|replay|time-load|crc|diff ...\n");
+    return 64;
+}
+
+static int cmd_save(int argc, char** argv) {
+    if (argc < 4) return usage();
+    const WorkloadSpec spec = resolve_workload(argv[2]);
+    SaveResult result = save(spec, argv[3]);
+    if (argc >= 5) {
+        write_file(argv[4], traces_to_text(result.traces));
+    }
+    std::printf("{\"graphs\": %u, \"templates\": %u}\n", result.manifest.grouping.total_graphs,
+                result.manifest.grouping.template_count);
+    return 0;
+}
+
+static int cmd_prepare(int argc, char** argv) {
+    if (argc < 6) return usage();
+    const fs::path archive = argv[2];
+    const uint32_t rank = static_cast<uint32_t>(std::stoul(argv[3]));
+    const uint32_t world = static_cast<uint32_t>(std::stoul(argv[4]));
+    ArchivePaths paths{archive};
+    const auto manifest_bytes = read_file(paths.manifest());
+    const Manifest manifest =
+        parse_manifest(std::string(manifest_bytes.begin(), manifest_bytes.end()));
+    const PatchTable table = parse_patch_table(read_file(paths.patch_table()));
+    const auto graphs_bin = read_file(paths.graphs());
+    std::vector<CapturedGraph> out;
+    for (const auto& loc : parse_graph_locators(graphs_bin)) {
+        CapturedGraph g = parse_graph_at(graphs_bin, loc);
+        auto it = table.per_graph.find(loc.label);
+        if (it != table.per_graph.end()) {
+            apply_rank_patches(g, it->second, manifest.comm_real_hash, rank, world);
+        }
+        out.push_back(std::move(g));
+    }
+    write_file(argv[5], serialize_graphs(out));
+    return 0;
+}
+
+static int cmd_replay(int argc, char** argv) {
+    if (argc < 6) return usage();
+    const fs::path archive = argv[2];
+    ArchivePaths paths{archive};
+    const auto manifest_bytes = read_file(paths.manifest());
+    const Manifest manifest =
+        parse_manifest(std::string(manifest_bytes.begin(), manifest_bytes.end()));
+    const uint64_t delta = parse_hex_u64(argv[4]);
+    const auto graphs = parse_graphs(read_file(argv[3]));
+
+    SimDriver driver;
+    DeviceContext& ctx = driver.create_context();
+    const Catalog catalog = parse_catalog(read_file(paths.catalog()));
+    restore_binaries(ctx, catalog, [&](uint64_t hash) { return read_file(paths.binary(hash)); });
+    RegionConfig config = manifest.allocator;
+    config.base += delta;
+    VirtualRegion region(ctx, config, Phase::load);
+    region.preallocate(manifest.final_offset);
+
+    std::map<uint32_t, LaunchTrace> traces;
+    try {
+        for (const auto& g : graphs) {
+            const GraphHandle handle = ctx.build_graph(g);
+            const ExecHandle exec = ctx.instantiate(handle);
+            traces.emplace(g.label, ctx.replay(exec));
+        }
+    } catch (const Error& e) {
+        std::fprintf(stderr, "%s\n", e.what());
+        return 3;
+    }
+    write_file(argv[5], traces_to_text(traces));
+    return 0;
+}
+
+static int cmd_time_load(int argc, char** argv) {
+    if (argc < 7) return usage();
+    const fs::path archive = argv[2];
+    LoadOptions options;
+    options.rank = static_cast<uint32_t>(std::stoul(argv[3]));
+    options.world = static_cast<uint32_t>(std::stoul(argv[4]));
+    options.prepare_lanes = static_cast<unsigned>(std::stoul(argv[5]));
+    const int reps = std::stoi(argv[6]);
+    const bool replay = argc >= 8 && std::string(argv[7]) == "replay";
+    using clock = std::chrono::steady_clock;
+    double best = 1e300, total = 0.0;
+    size_t graphs = 0;
+    for (int i = 0; i < reps + 1; ++i) {  // one warm-up (page cache), then reps
+        const auto t0 = clock::now();
+        ServingContext sc = load(archive, options);
+        if (replay) {
+            for (uint32_t b : sc.batches()) sc.replay(b);
+        }
+        const auto t1 = clock::now();
+        graphs = sc.batches().size();
+        const double ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        if (i > 0) {
+            best = std::min(best, ms);
+            total += ms;
+        }
+    }
+    std::printf("{\"best_ms\": %.6f, \"mean_ms\": %.6f, \"reps\": %d, \"graphs\": %zu, "
+                "\"lanes\": %u, \"hw_threads\": %u}\n",
+                best, total / reps, reps, graphs, options.prepare_lanes,
+                std::thread::hardware_concurrency());
+    return 0;
+}
+
+static int cmd_crc(int argc, char** argv) {
+    if (argc < 3) return usage();
+    std::printf("%s\n", to_hex(crc64(read_file(argv[2]))).c_str());
+    return 0;
+}
+
+static int cmd_diff(int argc, char** argv) {
+    if (argc < 4) return usage();
+    const auto a = parse_graphs(read_file(argv[2]));
+    const auto b = parse_graphs(read_file(argv[3]));
+    for (size_t i = 0; i < std::min(a.size(), b.size()); ++i) {
+        std::printf("# graph %u\n%s", a[i].label, diff(a[i], b[i]).to_text().c_str());
+    }
+    return 0;
+}
+
+int main(int argc, char** argv) {
+    if (argc < 2) return usage();
+    const std::string cmd = argv[1];
+    try {
+        if (cmd == "save") return cmd_save(argc, argv);
+        if (cmd == "prepare") return cmd_prepare(argc, argv);
+        if (cmd == "replay") return cmd_replay(argc, argv);
+        if (cmd == "time-load") return cmd_time_load(argc, argv);
+        if (cmd == "crc") return cmd_crc(argc, argv);
+        if (cmd == "diff") return cmd_diff(argc, argv);
+    } catch (const Error& e) {
+        std::fprintf(stderr, "%s\n", e.what());
+        return 2;
+    }
+    return usage();
+}

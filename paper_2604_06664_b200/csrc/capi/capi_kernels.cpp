@@ -1,0 +1,187 @@
+// C-ABI, kernel layer (declarations and reference anchors: include/foundry_b200.h).
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "capi_common.hpp"
+#include "foundry/device.hpp"
+#include "foundry_b200.h"
+
+using namespace foundry;
+
+struct fdy_device {
+    std::unique_ptr<Device> dev;
+};
+
+struct fdy_store {
+    fdy_device* owner = nullptr;
+    DeviceStore store;
+};
+
+struct fdy_members {
+    fdy_device* owner = nullptr;
+    DeviceBuffer out;
+    DeviceBuffer values;
+};
+
+extern "C" {
+
+int fdy_device_count(void) { return cuda_device_count(); }
+
+int fdy_device_open(int ordinal, fdy_device** out) {
+    return fdy_guard([&] {
+        require(out != nullptr, Errc::invalid_argument, "fdy_device_open: null out");
+        auto d = std::make_unique<fdy_device>();
+        d->dev = std::make_unique<Device>(ordinal);
+        *out = d.release();
+    });
+}
+
+void fdy_device_close(fdy_device* dev) { delete dev; }
+
+int fdy_sync(fdy_device* dev) {
+    return fdy_guard([&] {
+        require(dev != nullptr, Errc::invalid_argument, "fdy_sync: null device");
+        dev->dev->sync();
+    });
+}
+
+int fdy_store_upload(fdy_device* dev, const void* host_blob, size_t bytes, fdy_store** out) {
+    return fdy_guard([&] {
+        require(dev && host_blob && out, Errc::invalid_argument, "fdy_store_upload: null argument");
+        auto s = std::make_unique<fdy_store>();
+        s->owner = dev;
+        s->store = upload_store(*dev->dev, host_blob, bytes);
+        *out = s.release();
+    });
+}
+
+int fdy_store_fanout(const fdy_store* src, fdy_device* dst_dev, fdy_store** out) {
+    return fdy_guard([&] {
+        require(src && dst_dev && out, Errc::invalid_argument, "fdy_store_fanout: null argument");
+        Device& d = *dst_dev->dev;
+        Device& s = *src->owner->dev;
+        DeviceBuffer buf(d, src->store.bytes);
+        src->owner->dev->sync();  // the source upload must have landed
+        d.make_current();
+        int can = 0;
+        if (d.ordinal() != s.ordinal()) {
+            cuda_check(cudaDeviceCanAccessPeer(&can, d.ordinal(), s.ordinal()), "cudaDeviceCanAccessPeer");
+            if (can) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(s.ordinal(), 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else cuda_check(e, "cudaDeviceEnablePeerAccess");
+            }
+        }
+        // peer copy: NVLink when P2P is enabled, otherwise the driver stages it
+        cuda_check(cudaMemcpyPeerAsync(buf.data(), d.ordinal(), src->store.data, s.ordinal(),
+                                       src->store.bytes, d.stream()),
+                   "cudaMemcpyPeerAsync(store fan-out)");
+        auto o = std::make_unique<fdy_store>();
+        o->owner = dst_dev;
+        o->store = adopt_store(d, buf.data(), src->store.bytes, src->store.header);
+        o->store.blob = std::move(buf);
+        *out = o.release();
+    });
+}
+
+void fdy_store_free(fdy_store* store) { delete store; }
+
+size_t fdy_store_members_bytes(const fdy_store* store) {
+    return store ? store->store.header.members_image_bytes : 0;
+}
+
+static void materialize_into(fdy_device* dev, const fdy_store* store,
+                             const fdy_materialize_desc* desc, fdy_members* m, float* kernel_ms) {
+    require(dev && store && desc && m, Errc::invalid_argument, "fdy_materialize: null argument");
+    require(store->owner == dev, Errc::invalid_argument, "fdy_materialize: store lives on another device");
+    MaterializeRequest req;
+    req.rank = desc->rank;
+    req.world = desc->world;
+    req.new_base = desc->new_base;
+    const uint64_t* d_values = nullptr;
+    if (desc->n_values) {
+        require(desc->values != nullptr, Errc::invalid_argument, "fdy_materialize: null value table");
+        req.values.assign(desc->values, desc->values + desc->n_values);
+        if (m->values.size() < desc->n_values * 8) m->values = DeviceBuffer(*dev->dev, desc->n_values * 8);
+        cuda_check(cudaMemcpyAsync(m->values.data(), desc->values, desc->n_values * 8,
+                                   cudaMemcpyHostToDevice, dev->dev->stream()),
+                   "cudaMemcpyAsync(value table)");
+        d_values = reinterpret_cast<const uint64_t*>(m->values.data());
+    }
+    MaterializeTiming t;
+    launch_materialize(*dev->dev, store->store, req, m->out.data(), kernel_ms ? &t : nullptr,
+                       desc->grid, d_values);
+    if (kernel_ms) *kernel_ms = t.kernel_ms;
+}
+
+int fdy_materialize(fdy_device* dev, const fdy_store* store, const fdy_materialize_desc* desc,
+                    fdy_members** out, float* kernel_ms) {
+    return fdy_guard([&] {
+        require(dev && store && out, Errc::invalid_argument, "fdy_materialize: null argument");
+        auto m = std::make_unique<fdy_members>();
+        m->owner = dev;
+        m->out = DeviceBuffer(*dev->dev, store->store.header.members_image_bytes);
+        materialize_into(dev, store, desc, m.get(), kernel_ms);
+        *out = m.release();
+    });
+}
+
+int fdy_materialize_into(fdy_device* dev, const fdy_store* store, const fdy_materialize_desc* desc,
+                         fdy_members* members, float* kernel_ms) {
+    return fdy_guard([&] {
+        require(members && store, Errc::invalid_argument, "fdy_materialize_into: null argument");
+        require(members->out.size() >= store->store.header.members_image_bytes,
+                Errc::invalid_argument, "fdy_materialize_into: arena too small for this store");
+        materialize_into(dev, store, desc, members, kernel_ms);
+    });
+}
+
+size_t fdy_members_bytes(const fdy_members* m) { return m ? m->out.size() : 0; }
+
+int fdy_members_download(fdy_members* m, void* host_dst, size_t offset, size_t bytes) {
+    return fdy_guard([&] {
+        require(m && host_dst, Errc::invalid_argument, "fdy_members_download: null argument");
+        require(offset <= m->out.size() && bytes <= m->out.size() - offset, Errc::invalid_argument,
+                "fdy_members_download: range outside the arena");
+        Device& d = *m->owner->dev;
+        d.make_current();
+        cuda_check(cudaMemcpyAsync(host_dst, m->out.data() + offset, bytes, cudaMemcpyDeviceToHost,
+                                   d.stream()),
+                   "cudaMemcpyAsync(members D2H)");
+        cuda_check(cudaStreamSynchronize(d.stream()), "cudaStreamSynchronize");
+    });
+}
+
+void fdy_members_free(fdy_members* m) { delete m; }
+
+int fdy_crc64_segments(fdy_device* dev, const void* host, size_t bytes, const uint64_t* offsets,
+                       const uint64_t* lengths, uint32_t n, uint64_t* digests, float* kernel_ms) {
+    return fdy_guard([&] {
+        require(dev && (host || !bytes) && (offsets || !n) && (lengths || !n) && (digests || !n),
+                Errc::invalid_argument, "fdy_crc64_segments: null argument");
+        // pack every range at a 16-byte aligned offset of one device buffer
+        std::vector<Segment> segs(n);
+        uint64_t total = 0;
+        for (uint32_t i = 0; i < n; ++i) {
+            require(offsets[i] <= bytes && lengths[i] <= bytes - offsets[i], Errc::invalid_argument,
+                    "fdy_crc64_segments: range outside the buffer");
+            segs[i] = {total, lengths[i]};
+            total += (lengths[i] + 255) / 256 * 256;
+        }
+        Device& d = *dev->dev;
+        DeviceBuffer buf(d, total);
+        for (uint32_t i = 0; i < n; ++i)
+            if (lengths[i])
+                cuda_check(cudaMemcpyAsync(buf.data() + segs[i].offset,
+                                           static_cast<const unsigned char*>(host) + offsets[i],
+                                           lengths[i], cudaMemcpyHostToDevice, d.stream()),
+                           "cudaMemcpyAsync(crc H2D)");
+        const auto out = crc64_device(d, buf.data(), segs, kernel_ms);
+        std::memcpy(digests, out.data(), n * sizeof(uint64_t));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,451 @@
+// Archive side-file codecs (anchors in foundry/archive.hpp).
+#include "foundry/archive.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <unordered_map>
+#include <unordered_set>
+
+#include <json.hpp>
+
+#include "foundry/bytes.hpp"
+
+namespace foundry {
+
+using nlohmann::json;
+
+// ------------------------------------------------------------ memlayout
+
+std::vector<uint8_t> serialize_event_log(const MemoryEventLog& log) {
+    Sink s;
+    for (uint64_t v : {log.config.base, log.config.capacity, log.config.granularity,
+                       log.starting_offset, log.final_offset, uint64_t(log.records.size())})
+        s.u64(v);
+    for (const auto& r : log.records) {
+        s.u64(r.sequence);
+        s.u64(r.size);
+        s.u64(r.address);
+        s.u64(r.length);
+        s.u8(static_cast<uint8_t>(r.window));
+    }
+    return s.release();
+}
+
+MemoryEventLog parse_event_log(std::span<const uint8_t> bytes) {
+    Cursor c(bytes, Errc::archive_corruption);
+    MemoryEventLog log;
+    log.config.base = c.u64();
+    log.config.capacity = c.u64();
+    log.config.granularity = c.u64();
+    log.starting_offset = c.u64();
+    log.final_offset = c.u64();
+    const uint64_t n = c.u64();
+    require(n <= bytes.size() / 33, Errc::archive_corruption, "truncated input");
+    log.records.resize(n);
+    for (auto& r : log.records) {
+        r.sequence = c.u64();
+        r.size = c.u64();
+        r.address = c.u64();
+        r.length = c.u64();
+        r.window = static_cast<AllocWindow>(c.u8());
+    }
+    require(c.at_end(), Errc::archive_corruption, "trailing bytes in event log");
+    return log;
+}
+
+// ------------------------------------------------------------ grouping
+
+GroupingManifest group_graphs(const std::vector<CapturedGraph>& graphs) {
+    struct KeyHash {
+        size_t operator()(const TopologyKey& k) const {
+            return size_t(k.digest.hi ^ (k.digest.lo * 0x9E3779B97F4A7C15ull));
+        }
+    };
+    GroupingManifest m;
+    std::unordered_map<TopologyKey, size_t, KeyHash> slot;
+    std::unordered_set<uint32_t> labels;
+    for (const auto& g : graphs) {
+        require(labels.insert(g.label).second, Errc::invalid_argument,
+                "duplicate graph label " + std::to_string(g.label));
+        const TopologyKey key = topology_key(g);
+        auto [it, fresh] = slot.try_emplace(key, m.groups.size());
+        if (fresh) {
+            TemplateGroup grp;
+            grp.key = key;
+            m.groups.push_back(std::move(grp));
+        }
+        m.groups[it->second].members.push_back(g.label);
+    }
+    for (auto& grp : m.groups) {
+        std::sort(grp.members.begin(), grp.members.end());
+        grp.representative = grp.members.front();
+    }
+    std::sort(m.groups.begin(), m.groups.end(),
+              [](const TemplateGroup& a, const TemplateGroup& b) {
+                  return a.representative < b.representative;
+              });
+    m.total_graphs = static_cast<uint32_t>(graphs.size());
+    m.template_count = static_cast<uint32_t>(m.groups.size());
+    return m;
+}
+
+void attach_locators(GroupingManifest& m, const std::vector<GraphLocator>& locators) {
+    std::unordered_map<uint32_t, GraphLocator> by_label;
+    for (const auto& l : locators) by_label[l.label] = l;
+    for (auto& grp : m.groups) {
+        grp.locators.clear();
+        for (uint32_t label : grp.members) {
+            auto it = by_label.find(label);
+            require(it != by_label.end(), Errc::archive_corruption,
+                    "container has no record for graph " + std::to_string(label));
+            grp.locators.push_back(it->second);
+        }
+    }
+}
+
+// ------------------------------------------------------------ manifest
+
+std::string serialize_manifest(const Manifest& m) {
+    json groups = json::array();
+    for (const auto& g : m.grouping.groups) {
+        json locs = json::array();
+        for (const auto& l : g.locators) locs.push_back({l.label, l.offset, l.length, l.checksum});
+        groups.push_back(json{{"key", g.key.hex()},
+                              {"representative", g.representative},
+                              {"members", g.members},
+                              {"locators", std::move(locs)}});
+    }
+    json root;
+    root["format_version"] = m.format_version;
+    root["hash_algorithm"] = m.hash_algorithm;
+    root["workload_digest"] = m.workload_digest;
+    root["workload"] = m.workload_text;
+    root["allocator"] = {{"base", m.allocator.base},
+                         {"capacity", m.allocator.capacity},
+                         {"granularity", m.allocator.granularity},
+                         {"final_offset", m.final_offset}};
+    root["kv_cache_bytes"] = m.kv_cache_bytes;
+    root["comm"] = {{"world_placeholder", m.comm_world_placeholder},
+                    {"real_binary_hash", m.comm_real_hash}};
+    root["grouping"] = {{"total", m.grouping.total_graphs},
+                        {"templates", m.grouping.template_count},
+                        {"groups", std::move(groups)}};
+    root["memlayout"] = m.memlayout_ref;
+    root["catalog"] = m.catalog_ref;
+    root["patch_table"] = m.patch_table_ref;
+    root["files"] = m.file_digests;
+    return root.dump(2) + "\n";
+}
+
+Manifest parse_manifest(const std::string& text) {
+    json root;
+    try {
+        root = json::parse(text);
+    } catch (const json::exception& e) {
+        raise(Errc::archive_corruption, std::string("manifest is not valid JSON: ") + e.what());
+    }
+    try {
+        Manifest m;
+        m.format_version = root.at("format_version").get<uint32_t>();
+        require(m.format_version == Manifest::kFormatVersion, Errc::archive_corruption,
+                "unsupported archive format version " + std::to_string(m.format_version));
+        m.hash_algorithm = root.at("hash_algorithm").get<uint8_t>();
+        require(m.hash_algorithm == kContentHashAlgorithm, Errc::archive_corruption,
+                "archive pins hash algorithm " + std::to_string(m.hash_algorithm) +
+                    ", this build implements " + std::to_string(kContentHashAlgorithm));
+        m.workload_digest = root.at("workload_digest").get<uint64_t>();
+        m.workload_text = root.at("workload").get<std::string>();
+        const json& a = root.at("allocator");
+        m.allocator.base = a.at("base").get<uint64_t>();
+        m.allocator.capacity = a.at("capacity").get<uint64_t>();
+        m.allocator.granularity = a.at("granularity").get<uint64_t>();
+        m.final_offset = a.at("final_offset").get<uint64_t>();
+        m.kv_cache_bytes = root.at("kv_cache_bytes").get<uint64_t>();
+        m.comm_world_placeholder = root.at("comm").at("world_placeholder").get<uint64_t>();
+        m.comm_real_hash = root.at("comm").at("real_binary_hash").get<uint64_t>();
+        const json& gr = root.at("grouping");
+        m.grouping.total_graphs = gr.at("total").get<uint32_t>();
+        m.grouping.template_count = gr.at("templates").get<uint32_t>();
+        for (const json& gj : gr.at("groups")) {
+            TemplateGroup g;
+            const std::string key = gj.at("key").get<std::string>();
+            require(key.size() == 32, Errc::archive_corruption, "bad topology key literal");
+            g.key.digest.hi = parse_hex(key.substr(0, 16));
+            g.key.digest.lo = parse_hex(key.substr(16));
+            g.representative = gj.at("representative").get<uint32_t>();
+            g.members = gj.at("members").get<std::vector<uint32_t>>();
+            for (const json& lj : gj.at("locators")) {
+                GraphLocator l;
+                l.label = lj.at(0).get<uint32_t>();
+                l.offset = lj.at(1).get<uint64_t>();
+                l.length = lj.at(2).get<uint64_t>();
+                l.checksum = lj.at(3).get<uint64_t>();
+                g.locators.push_back(l);
+            }
+            m.grouping.groups.push_back(std::move(g));
+        }
+        m.memlayout_ref = root.at("memlayout").get<std::string>();
+        m.catalog_ref = root.at("catalog").get<std::string>();
+        m.patch_table_ref = root.at("patch_table").get<std::string>();
+        m.file_digests = root.at("files").get<std::map<std::string, uint64_t>>();
+        return m;
+    } catch (const json::exception& e) {
+        raise(Errc::archive_corruption, std::string("manifest field error: ") + e.what());
+    }
+}
+
+// ------------------------------------------------------------ FNDB
+
+namespace {
+constexpr uint8_t kImgRelocatable = 0x01;
+constexpr uint8_t kImgDeviceInit = 0x02;
+
+void put_fattrs(Sink& s, const FuncAttrs& f) {
+    for (int32_t v : {f.max_dynamic_shared_size_bytes, f.preferred_shared_memory_carveout,
+                      f.cluster_scheduling_policy_preference, f.required_cluster_width,
+                      f.required_cluster_height, f.required_cluster_depth})
+        s.i32(v);
+}
+
+FuncAttrs get_fattrs(Cursor& c) {
+    FuncAttrs f;
+    f.max_dynamic_shared_size_bytes = c.i32();
+    f.preferred_shared_memory_carveout = c.i32();
+    f.cluster_scheduling_policy_preference = c.i32();
+    f.required_cluster_width = c.i32();
+    f.required_cluster_height = c.i32();
+    f.required_cluster_depth = c.i32();
+    return f;
+}
+}  // namespace
+
+std::vector<uint8_t> encode_kernel_image(const KernelImage& img) {
+    Sink s;
+    s.raw("FNDB", 4);
+    s.u16(1);
+    s.u8((img.relocatable ? kImgRelocatable : 0) | (img.requires_device_init ? kImgDeviceInit : 0));
+    s.u32(img.link_tag);
+    s.u32(static_cast<uint32_t>(img.entrypoints.size()));
+    for (const auto& e : img.entrypoints) {
+        s.str(e.name);
+        s.u32(e.arg_buffer_size);
+        s.u32(static_cast<uint32_t>(e.hidden_offsets.size()));
+        for (uint32_t o : e.hidden_offsets) s.u32(o);
+        put_fattrs(s, e.attrs);
+    }
+    s.u32(static_cast<uint32_t>(img.aux.size()));
+    s.raw(img.aux);
+    return s.release();
+}
+
+KernelImage parse_kernel_image(std::span<const uint8_t> payload) {
+    Cursor c(payload, Errc::binary_format);
+    c.magic("FNDB");
+    const uint16_t version = c.u16();
+    require(version == 1, Errc::binary_format, "unsupported image version " + std::to_string(version));
+    KernelImage img;
+    const uint8_t flags = c.u8();
+    img.relocatable = flags & kImgRelocatable;
+    img.requires_device_init = flags & kImgDeviceInit;
+    img.link_tag = c.u32();
+    const uint32_t n = c.u32();
+    std::unordered_set<std::string> seen;
+    for (uint32_t i = 0; i < n; ++i) {
+        KernelEntry e;
+        e.name = c.str();
+        require(!e.name.empty(), Errc::binary_format, "empty entrypoint name");
+        require(seen.insert(e.name).second, Errc::binary_format,
+                "duplicate entrypoint '" + e.name + "'");
+        e.arg_buffer_size = c.u32();
+        const uint32_t k = c.u32();
+        for (uint32_t j = 0; j < k; ++j) {
+            const uint32_t off = c.u32();
+            require(uint64_t(off) + 8 <= e.arg_buffer_size, Errc::binary_format,
+                    "hidden offset " + std::to_string(off) + " out of range in '" + e.name + "'");
+            e.hidden_offsets.push_back(off);
+        }
+        e.attrs = get_fattrs(c);
+        img.entrypoints.push_back(std::move(e));
+    }
+    const uint32_t aux = c.u32();
+    const uint8_t* p = c.take(aux);
+    img.aux.assign(p, p + aux);
+    require(c.at_end(), Errc::binary_format, "trailing bytes after image");
+    return img;
+}
+
+std::vector<uint8_t> link_segments(const std::vector<std::vector<uint8_t>>& segments) {
+    require(!segments.empty(), Errc::invalid_argument, "no segments to link");
+    KernelImage out;
+    std::unordered_set<std::string> names;
+    for (size_t i = 0; i < segments.size(); ++i) {
+        KernelImage seg = parse_kernel_image(segments[i]);
+        if (i == 0) {
+            out.link_tag = seg.link_tag;
+            out.requires_device_init = seg.requires_device_init;
+        } else {
+            require(seg.link_tag == out.link_tag, Errc::binary_format,
+                    "link tag mismatch across segments");
+            out.requires_device_init = out.requires_device_init || seg.requires_device_init;
+        }
+        for (auto& e : seg.entrypoints) {
+            require(names.insert(e.name).second, Errc::binary_format,
+                    "conflicting entrypoint '" + e.name + "' across segments");
+            out.entrypoints.push_back(std::move(e));
+        }
+    }
+    out.relocatable = false;
+    return encode_kernel_image(out);
+}
+
+// ------------------------------------------------------------ catalog
+
+namespace {
+constexpr uint8_t kCatInit = 0x01, kCatStub = 0x02, kCatReal = 0x04;
+}
+
+std::vector<uint8_t> serialize_catalog(const Catalog& cat) {
+    Sink s;
+    s.raw("FNDC", 4);
+    s.u16(1);
+    s.u8(kContentHashAlgorithm);
+    s.u32(static_cast<uint32_t>(cat.binaries.size()));
+    for (const auto& [hash, r] : cat.binaries) {
+        s.u64(hash);
+        s.u8(static_cast<uint8_t>(r.variant));
+        s.u8((r.needs_device_init ? kCatInit : 0) | (r.is_stub ? kCatStub : 0) |
+             (r.is_comm_real ? kCatReal : 0));
+        s.u32(static_cast<uint32_t>(r.load_options.size()));
+        s.raw(r.load_options);
+        s.u32(static_cast<uint32_t>(r.entrypoints.size()));
+        for (size_t i = 0; i < r.entrypoints.size(); ++i) {
+            s.str(r.entrypoints[i]);
+            put_fattrs(s, r.entrypoint_attrs[i]);
+        }
+    }
+    return s.release();
+}
+
+Catalog parse_catalog(std::span<const uint8_t> bytes) {
+    Cursor c(bytes, Errc::archive_corruption);
+    c.magic("FNDC");
+    const uint16_t version = c.u16();
+    require(version == 1, Errc::archive_corruption,
+            "unsupported catalog version " + std::to_string(version));
+    const uint8_t algo = c.u8();
+    require(algo == kContentHashAlgorithm, Errc::archive_corruption,
+            "archive uses hash algorithm " + std::to_string(algo) + ", this build implements " +
+                std::to_string(kContentHashAlgorithm));
+    Catalog cat;
+    const uint32_t n = c.u32();
+    for (uint32_t i = 0; i < n; ++i) {
+        KernelBinaryRecord r;
+        r.hash = c.u64();
+        r.variant = static_cast<LoadVariant>(c.u8());
+        const uint8_t f = c.u8();
+        r.needs_device_init = f & kCatInit;
+        r.is_stub = f & kCatStub;
+        r.is_comm_real = f & kCatReal;
+        const uint32_t no = c.u32();
+        const uint8_t* p = c.take(no);
+        r.load_options.assign(p, p + no);
+        const uint32_t ne = c.u32();
+        for (uint32_t j = 0; j < ne; ++j) {
+            r.entrypoints.push_back(c.str());
+            r.entrypoint_attrs.push_back(get_fattrs(c));
+        }
+        const uint64_t h = r.hash;
+        cat.binaries.emplace(h, std::move(r));
+    }
+    require(c.at_end(), Errc::archive_corruption, "trailing bytes in catalog");
+    return cat;
+}
+
+// ------------------------------------------------------------ patch table
+
+size_t PatchTable::total_entries() const {
+    size_t n = 0;
+    for (const auto& [label, entries] : per_graph) n += entries.size();
+    return n;
+}
+
+std::vector<uint8_t> serialize_patch_table(const PatchTable& t) {
+    Sink s;
+    s.raw("FNDP", 4);
+    s.u16(1);
+    s.u64(t.world_placeholder);
+    s.u32(static_cast<uint32_t>(t.per_graph.size()));
+    for (const auto& [label, entries] : t.per_graph) {
+        s.u32(label);
+        s.u32(static_cast<uint32_t>(entries.size()));
+        for (const auto& e : entries) {
+            s.u32(e.node_id);
+            s.u64(e.stub.binary_hash);
+            s.str(e.stub.name);
+            s.str(e.real_name);
+            s.u32(static_cast<uint32_t>(e.rank_offsets.size()));
+            for (uint32_t o : e.rank_offsets) s.u32(o);
+            s.u32(static_cast<uint32_t>(e.world_offsets.size()));
+            for (uint32_t o : e.world_offsets) s.u32(o);
+            s.u8(e.patch_width);
+        }
+    }
+    return s.release();
+}
+
+PatchTable parse_patch_table(std::span<const uint8_t> bytes) {
+    Cursor c(bytes, Errc::archive_corruption);
+    c.magic("FNDP");
+    const uint16_t version = c.u16();
+    require(version == 1, Errc::archive_corruption,
+            "unsupported patch table version " + std::to_string(version));
+    PatchTable t;
+    t.world_placeholder = c.u64();
+    const uint32_t ng = c.u32();
+    for (uint32_t g = 0; g < ng; ++g) {
+        const uint32_t label = c.u32();
+        const uint32_t n = c.u32();
+        std::vector<CommPatchEntry> entries;
+        for (uint32_t i = 0; i < n; ++i) {
+            CommPatchEntry e;
+            e.node_id = c.u32();
+            e.stub.binary_hash = c.u64();
+            e.stub.name = c.str();
+            e.real_name = c.str();
+            const uint32_t nr = c.u32();
+            for (uint32_t j = 0; j < nr; ++j) e.rank_offsets.push_back(c.u32());
+            const uint32_t nw = c.u32();
+            for (uint32_t j = 0; j < nw; ++j) e.world_offsets.push_back(c.u32());
+            e.patch_width = c.u8();
+            entries.push_back(std::move(e));
+        }
+        t.per_graph.emplace(label, std::move(entries));
+    }
+    require(c.at_end(), Errc::archive_corruption, "trailing bytes in patch table");
+    return t;
+}
+
+void apply_rank_patches(CapturedGraph& graph, std::span<const CommPatchEntry> entries,
+                        uint64_t real_comm_hash, uint32_t rank, uint32_t world) {
+    auto put = [](std::vector<uint8_t>& buf, uint32_t off, uint64_t v) {
+        require(uint64_t(off) + 8 <= buf.size(), Errc::invalid_argument,
+                "patch offset outside the argument buffer");
+        std::memcpy(buf.data() + off, &v, 8);
+    };
+    for (const auto& e : entries) {
+        require(e.node_id < graph.nodes.size(), Errc::archive_corruption,
+                "patch entry references missing node");
+        GraphNode& n = graph.nodes[e.node_id];
+        require(n.type == NodeType::Kernel, Errc::archive_corruption,
+                "patch entry references a non-kernel node");
+        auto& k = n.kernel_params();
+        require(k.kernel == e.stub, Errc::archive_corruption,
+                "node " + std::to_string(e.node_id) + " is not the recorded stub " +
+                    e.stub.describe());
+        k.kernel = KernelRef{real_comm_hash, e.real_name};
+        for (uint32_t o : e.rank_offsets) put(k.arg_buffer, o, rank);
+        for (uint32_t o : e.world_offsets) put(k.arg_buffer, o, world);
+    }
+}
+
+}  // namespace foundry

@@ -1,0 +1,280 @@
+// Device runtime: streams, HBM/pinned buffers, kernel launches (see device.hpp).
+#include "foundry/device.hpp"
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../kernels/fdy_kernels.h"
+#include "foundry/hash.hpp"
+
+namespace foundry {
+
+void cuda_check(int err, const char* what) {
+    if (err == cudaSuccess) return;
+    const auto e = static_cast<cudaError_t>(err);
+    const bool no_device = e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ||
+                           e == cudaErrorInitializationError;
+    raise(no_device ? Errc::device_unavailable : Errc::cuda_error,
+          std::string(what) + " failed: " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+
+int cuda_device_count() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();  // clear the sticky-free error state
+        return 0;
+    }
+    return n;
+}
+
+bool cuda_available() { return cuda_device_count() > 0; }
+
+namespace {
+std::once_flag g_const_once[64];
+}
+
+Device::Device(int ordinal) : ordinal_(ordinal) {
+    const int n = cuda_device_count();
+    require(n > 0, Errc::device_unavailable, "no CUDA device is visible (the B200 path has no CPU fallback)");
+    require(ordinal >= 0 && ordinal < n, Errc::invalid_argument,
+            "device ordinal " + std::to_string(ordinal) + " out of range (" + std::to_string(n) + " visible)");
+    cuda_check(cudaSetDevice(ordinal_), "cudaSetDevice");
+    cuda_check(cudaFree(nullptr), "cudaFree(0) context init");
+    cuda_check(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, ordinal_),
+               "cudaDeviceGetAttribute(SM count)");
+    cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    // per-device constant table of the CRC kernel: x^(2^k) mod P
+    std::call_once(g_const_once[ordinal_ & 63], [] {
+        cuda_check(fdy_crc64_set_constants(crc64_x2k_table()), "CRC constant upload");
+    });
+}
+
+Device::~Device() {
+    cudaSetDevice(ordinal_);
+    if (stream_) cudaStreamDestroy(stream_);
+    if (copy_stream_) cudaStreamDestroy(copy_stream_);
+}
+
+void Device::make_current() const { cuda_check(cudaSetDevice(ordinal_), "cudaSetDevice"); }
+
+void Device::sync() const {
+    cuda_check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+    cuda_check(cudaStreamSynchronize(copy_stream_), "cudaStreamSynchronize(copy)");
+}
+
+void* Device::alloc(size_t bytes) {
+    make_current();
+    void* p = nullptr;
+    if (bytes == 0) bytes = 16;
+    cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+    return p;
+}
+
+void Device::release(void* p) {
+    if (!p) return;
+    cudaSetDevice(ordinal_);
+    cudaFree(p);
+}
+
+void* Device::alloc_host_pinned(size_t bytes) {
+    make_current();
+    void* p = nullptr;
+    if (bytes == 0) bytes = 16;
+    cuda_check(cudaHostAlloc(&p, bytes, cudaHostAllocPortable), "cudaHostAlloc");
+    return p;
+}
+
+void Device::release_host_pinned(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+DeviceBuffer::DeviceBuffer(Device& dev, size_t bytes)
+    : dev_(&dev), p_(static_cast<unsigned char*>(dev.alloc(bytes))), n_(bytes) {}
+
+DeviceBuffer::~DeviceBuffer() {
+    if (dev_) dev_->release(p_);
+}
+
+DeviceBuffer& DeviceBuffer::operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) {
+        if (dev_) dev_->release(p_);
+        dev_ = o.dev_;
+        p_ = o.p_;
+        n_ = o.n_;
+        o.dev_ = nullptr;
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
+    return *this;
+}
+
+PinnedBuffer::PinnedBuffer(Device& dev, size_t bytes)
+    : dev_(&dev), p_(static_cast<unsigned char*>(dev.alloc_host_pinned(bytes))), n_(bytes) {}
+
+PinnedBuffer::~PinnedBuffer() {
+    if (dev_) dev_->release_host_pinned(p_);
+}
+
+PinnedBuffer& PinnedBuffer::operator=(PinnedBuffer&& o) noexcept {
+    if (this != &o) {
+        if (dev_) dev_->release_host_pinned(p_);
+        dev_ = o.dev_;
+        p_ = o.p_;
+        n_ = o.n_;
+        o.dev_ = nullptr;
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
+    return *this;
+}
+
+// ------------------------------------------------------------------ stores
+
+DeviceStore adopt_store(Device& dev, const unsigned char* d_blob, size_t bytes,
+                        const fdt_header& h) {
+    require(bytes >= sizeof(fdt_header) && std::memcmp(h.magic, "FNDT", 4) == 0,
+            Errc::archive_corruption, "template store: bad magic, expected 'FNDT'");
+    require(h.version == FDT_VERSION, Errc::archive_corruption,
+            "template store: unsupported version " + std::to_string(h.version));
+    for (int i = 0; i < FDT_NSEC; ++i)
+        require(h.sec[i].offset <= bytes && h.sec[i].bytes <= bytes - h.sec[i].offset,
+                Errc::archive_corruption, "template store: section overruns the blob");
+    require(h.tile_chunks == FDT_TILE_CHUNKS, Errc::archive_corruption,
+            "template store: tile size " + std::to_string(h.tile_chunks) + " unsupported");
+    DeviceStore s;
+    s.dev = &dev;
+    s.data = d_blob;
+    s.bytes = bytes;
+    s.header = h;
+    return s;
+}
+
+DeviceStore upload_store(Device& dev, const void* host_blob, size_t bytes) {
+    require(bytes >= sizeof(fdt_header), Errc::archive_corruption, "template store: truncated input");
+    fdt_header h;
+    std::memcpy(&h, host_blob, sizeof h);
+    DeviceBuffer buf(dev, bytes);
+    cuda_check(cudaMemcpyAsync(buf.data(), host_blob, bytes, cudaMemcpyHostToDevice, dev.stream()),
+               "cudaMemcpyAsync(store H2D)");
+    DeviceStore s = adopt_store(dev, buf.data(), bytes, h);
+    s.blob = std::move(buf);
+    return s;
+}
+
+void launch_materialize(Device& dev, const DeviceStore& store, const MaterializeRequest& req,
+                        unsigned char* out, MaterializeTiming* timing, int grid_override,
+                        const uint64_t* d_values) {
+    const fdt_header& h = store.header;
+    require(req.world >= 1 && req.rank < req.world, Errc::invalid_argument,
+            "rank " + std::to_string(req.rank) + " is outside world size " + std::to_string(req.world));
+    dev.make_current();
+    FdyMaterializeArgs a{};
+    const unsigned char* b = store.data;
+    a.store = b;
+    a.out = out;
+    a.tiles = reinterpret_cast<const fdt_tile*>(b + h.sec[FDT_SEC_TILES].offset);
+    a.cmeta = b + h.sec[FDT_SEC_CMETA].offset;
+    a.didx = reinterpret_cast<const uint32_t*>(b + h.sec[FDT_SEC_DIDX].offset);
+    a.dmeta = reinterpret_cast<const uint32_t*>(b + h.sec[FDT_SEC_DMETA].offset);
+    a.ddata = reinterpret_cast<const uint4*>(b + h.sec[FDT_SEC_DDATA].offset);
+    a.rops = reinterpret_cast<const fdt_rank_op*>(b + h.sec[FDT_SEC_ROPS].offset);
+    a.values = d_values;
+    a.n_values = d_values ? static_cast<uint32_t>(req.values.size()) : 0u;
+    a.timage_base = h.sec[FDT_SEC_TIMAGES].offset;
+    a.old_base = h.old_base;
+    a.span = h.final_offset;
+    a.delta = req.new_base ? req.new_base - h.old_base : 0;
+    a.rank = req.rank;
+    a.world = req.world;
+    a.n_tiles = h.n_tiles;
+
+    int per_sm = 0;
+    cuda_check(fdy_materialize_occupancy(&per_sm), "materialize occupancy query");
+    int grid = grid_override > 0 ? grid_override : dev.sm_count() * std::max(per_sm, 1);
+    grid = std::max(1, std::min<int>(grid, static_cast<int>(h.n_tiles)));
+
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing) {
+        cuda_check(cudaEventCreate(&e0), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&e1), "cudaEventCreate");
+        cuda_check(cudaEventRecord(e0, dev.stream()), "cudaEventRecord");
+    }
+    cuda_check(fdy_launch_materialize(&a, grid, dev.stream()), "materialize kernel launch");
+    if (timing) {
+        cuda_check(cudaEventRecord(e1, dev.stream()), "cudaEventRecord");
+        cuda_check(cudaEventSynchronize(e1), "cudaEventSynchronize");
+        cuda_check(cudaEventElapsedTime(&timing->kernel_ms, e0, e1), "cudaEventElapsedTime");
+        timing->grid = grid;
+        timing->blocks_per_sm = per_sm;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+}
+
+// ------------------------------------------------------------------ CRC
+
+std::vector<uint64_t> crc64_device(Device& dev, const unsigned char* d_base,
+                                   std::span<const Segment> segments, float* kernel_ms) {
+    dev.make_current();
+    std::vector<FdyCrcBlock> blocks;
+    std::vector<uint32_t> first(segments.size()), count(segments.size());
+    for (size_t s = 0; s < segments.size(); ++s) {
+        first[s] = static_cast<uint32_t>(blocks.size());
+        for (uint64_t off = 0; off < segments[s].length; off += kCrcBlockBytes) {
+            FdyCrcBlock b;
+            b.segment = static_cast<uint32_t>(s);
+            b.length = static_cast<uint32_t>(std::min<uint64_t>(kCrcBlockBytes, segments[s].length - off));
+            b.offset = segments[s].offset + off;
+            require(b.offset % 16 == 0, Errc::invalid_argument, "CRC segment must be 16-byte aligned");
+            blocks.push_back(b);
+        }
+        count[s] = static_cast<uint32_t>(blocks.size()) - first[s];
+    }
+    const size_t nb = blocks.size(), ns = segments.size();
+    // one scratch allocation: block table | first | count | crc | len | out
+    const size_t bytes = nb * sizeof(FdyCrcBlock) + 2 * ns * 4 + 2 * nb * 8 + ns * 8 + 64;
+    DeviceBuffer scratch(dev, bytes);
+    unsigned char* p = scratch.data();
+    auto* d_blocks = reinterpret_cast<FdyCrcBlock*>(p);
+    p += nb * sizeof(FdyCrcBlock);
+    auto* d_crc = reinterpret_cast<uint64_t*>(p);
+    p += nb * 8;
+    auto* d_len = reinterpret_cast<uint64_t*>(p);
+    p += nb * 8;
+    auto* d_out = reinterpret_cast<uint64_t*>(p);
+    p += ns * 8;
+    auto* d_first = reinterpret_cast<uint32_t*>(p);
+    p += ns * 4;
+    auto* d_count = reinterpret_cast<uint32_t*>(p);
+    cudaStream_t st = dev.stream();
+    if (nb) cuda_check(cudaMemcpyAsync(d_blocks, blocks.data(), nb * sizeof(FdyCrcBlock), cudaMemcpyHostToDevice, st), "H2D crc plan");
+    if (ns) {
+        cuda_check(cudaMemcpyAsync(d_first, first.data(), ns * 4, cudaMemcpyHostToDevice, st), "H2D crc plan");
+        cuda_check(cudaMemcpyAsync(d_count, count.data(), ns * 4, cudaMemcpyHostToDevice, st), "H2D crc plan");
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (kernel_ms) {
+        cuda_check(cudaEventCreate(&e0), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&e1), "cudaEventCreate");
+        cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
+    }
+    cuda_check(fdy_launch_crc64(d_base, d_blocks, static_cast<uint32_t>(nb), d_first, d_count,
+                                static_cast<uint32_t>(ns), d_crc, d_len, d_out, st),
+               "crc64 kernel launch");
+    if (kernel_ms) cuda_check(cudaEventRecord(e1, st), "cudaEventRecord");
+    std::vector<uint64_t> out(ns);
+    if (ns) cuda_check(cudaMemcpyAsync(out.data(), d_out, ns * 8, cudaMemcpyDeviceToHost, st), "D2H crc");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize(crc)");
+    if (kernel_ms) {
+        cuda_check(cudaEventElapsedTime(kernel_ms, e0, e1), "cudaEventElapsedTime");
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    return out;
+}
+
+}  // namespace foundry

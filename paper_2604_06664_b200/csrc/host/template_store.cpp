@@ -1,0 +1,542 @@
+// Template store packer + host view (format and semantics: store_format.h).
+#include "foundry/template_store.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <unordered_map>
+
+#include "foundry/bytes.hpp"
+#include "foundry/parallel.hpp"
+
+namespace foundry {
+
+namespace {
+
+constexpr uint32_t kNoKernel = 0xFFFFFFFFu;
+constexpr size_t kSectionAlign = 256;
+
+uint32_t round16(uint64_t v) { return static_cast<uint32_t>((v + 15) / 16 * 16); }
+
+uint32_t blob_len_of(const GraphNode& n) {
+    switch (n.type) {
+        case NodeType::Kernel: return static_cast<uint32_t>(n.kernel_params().arg_buffer.size());
+        case NodeType::Memcpy:
+        case NodeType::Memset: return 24;
+        default: return 0;
+    }
+}
+
+// Kernel table: unique (KernelRef, FuncAttrs) pairs.
+// Indices are assigned by a sequential pre-pass (intern) so the store is
+// deterministic; the parallel phases only call lookup() on a frozen table.
+class KernelTable {
+public:
+    uint32_t intern(const KernelRef& ref, const FuncAttrs& fa) {
+        auto [it, fresh] = index_.try_emplace(key(ref, fa), static_cast<uint32_t>(refs_.size()));
+        if (fresh) {
+            refs_.push_back(ref);
+            attrs_.push_back(fa);
+        }
+        return it->second;
+    }
+    uint32_t lookup(const KernelRef& ref, const FuncAttrs& fa) const {
+        auto it = index_.find(key(ref, fa));
+        require(it != index_.end(), Errc::invalid_argument, "kernel table: missing entry");
+        return it->second;
+    }
+    size_t size() const { return refs_.size(); }
+    const KernelRef& ref(size_t i) const { return refs_[i]; }
+    const FuncAttrs& attrs(size_t i) const { return attrs_[i]; }
+
+private:
+    static std::string key(const KernelRef& ref, const FuncAttrs& fa) {
+        std::string k(sizeof(uint64_t) + sizeof(FuncAttrs), '\0');
+        std::memcpy(k.data(), &ref.binary_hash, 8);
+        std::memcpy(k.data() + 8, &fa, sizeof(FuncAttrs));
+        return k + ref.name;
+    }
+    std::unordered_map<std::string, uint32_t> index_;
+    std::vector<KernelRef> refs_;
+    std::vector<FuncAttrs> attrs_;
+};
+
+struct GroupLayout {
+    uint32_t n_nodes = 0;
+    std::vector<uint32_t> blob_off;  // per node, from pool start
+    std::vector<uint32_t> cap;       // per node slot capacity (multiple of 16)
+    uint64_t pool_bytes = 0;
+    uint64_t image_bytes() const { return 48ull * n_nodes + pool_bytes; }
+    uint64_t desc_bytes() const { return 48ull * n_nodes; }
+};
+
+// Image of one graph under a group layout, plus per-chunk relocation meta.
+void build_image(const CapturedGraph& g, const GroupLayout& L, const KernelTable& kt,
+                 std::vector<uint8_t>& img, std::vector<uint8_t>& meta) {
+    img.assign(L.image_bytes(), 0);
+    meta.assign(L.image_bytes() / 16, 0);
+    uint8_t* pool = img.data() + L.desc_bytes();
+    const uint64_t pool_chunk0 = L.desc_bytes() / 16;
+    for (uint32_t i = 0; i < L.n_nodes; ++i) {
+        const GraphNode& n = g.nodes[i];
+        fdt_node d{};
+        d.type = static_cast<uint8_t>(n.type);
+        d.kernel = kNoKernel;
+        d.blob_off = L.blob_off[i];
+        d.blob_len = blob_len_of(n);
+        uint8_t* blob = pool + d.blob_off;
+        const uint64_t c0 = pool_chunk0 + d.blob_off / 16;
+        if (n.type == NodeType::Kernel) {
+            const auto& k = n.kernel_params();
+            d.kernel = kt.lookup(k.kernel, k.func_attrs);
+            d.grid[0] = k.grid.x, d.grid[1] = k.grid.y, d.grid[2] = k.grid.z;
+            d.block[0] = k.block.x, d.block[1] = k.block.y, d.block[2] = k.block.z;
+            d.shmem = k.shared_mem_bytes;
+            std::memcpy(blob, k.arg_buffer.data(), k.arg_buffer.size());
+            // every 8-aligned slot with o + 8 <= len is a relocation candidate
+            for (uint32_t o = 0; o + 8 <= d.blob_len; o += 8)
+                meta[c0 + o / 16] |= (o % 16 == 0) ? FDT_CMETA_LANE0 : FDT_CMETA_LANE1;
+        } else if (n.type == NodeType::Memcpy) {
+            const auto& m = std::get<MemcpyParams>(n.params);
+            std::memcpy(blob, &m.src, 8);
+            std::memcpy(blob + 8, &m.dst, 8);
+            std::memcpy(blob + 16, &m.length, 8);
+            meta[c0] |= FDT_CMETA_LANE0 | FDT_CMETA_LANE1;  // src, dst
+        } else if (n.type == NodeType::Memset) {
+            const auto& m = std::get<MemsetParams>(n.params);
+            std::memcpy(blob, &m.dst, 8);
+            std::memcpy(blob + 8, &m.value, 8);
+            std::memcpy(blob + 16, &m.length, 8);
+            meta[c0] |= FDT_CMETA_LANE0;  // dst only
+        }
+        std::memcpy(img.data() + 48ull * i, &d, sizeof d);
+    }
+}
+
+struct MemberOut {
+    std::vector<uint32_t> didx;
+    std::vector<uint32_t> dmeta;
+    std::vector<uint8_t> ddata;
+    std::vector<fdt_rank_op> rops;
+};
+
+// Splits a little-endian write of `width` bytes at image byte offset `at`
+// into per-chunk ops.
+void emit_write(std::vector<fdt_rank_op>& ops, uint64_t at, uint32_t width, uint8_t kind,
+                uint32_t aux) {
+    uint64_t b = at;
+    while (b < at + width) {
+        const uint64_t chunk = b / 16;
+        const uint64_t end = std::min<uint64_t>(at + width, (chunk + 1) * 16);
+        fdt_rank_op op{};
+        op.chunk = static_cast<uint32_t>(chunk);
+        op.kind = kind;
+        op.shift = static_cast<int8_t>(int64_t(at) - int64_t(chunk * 16));
+        for (uint64_t j = b; j < end; ++j) op.mask |= uint16_t(1u << (j - chunk * 16));
+        op.aux = aux;
+        ops.push_back(op);
+        b = end;
+    }
+}
+
+template <typename T>
+uint64_t put_section(Sink& s, fdt_header& h, int id, const T* data, size_t count) {
+    s.align(kSectionAlign);
+    h.sec[id].offset = s.size();
+    h.sec[id].bytes = count * sizeof(T);
+    s.raw(data, count * sizeof(T));
+    return h.sec[id].offset;
+}
+
+}  // namespace
+
+std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
+                                         std::span<const uint8_t> patch_bin,
+                                         const Manifest& manifest, unsigned threads,
+                                         PackStats* stats) {
+    const PatchTable patches = parse_patch_table(patch_bin);
+    KernelTable kt;
+    const bool has_patches = !patches.empty();
+    if (has_patches) {
+        require(manifest.comm_real_hash != 0, Errc::unresolved_kernel,
+                "archive carries comm patches but no real comm binary");
+    }
+
+    std::vector<fdt_group> groups;
+    std::vector<fdt_member> members;
+    std::vector<fdt_node_attrs> attrs;
+    std::vector<uint32_t> edges;
+    Sink timages;
+    std::vector<uint8_t> cmeta;
+    std::vector<uint32_t> didx, dmeta;
+    std::vector<uint8_t> ddata;
+    std::vector<fdt_rank_op> rops;
+    std::vector<fdt_tile> tiles;
+    uint64_t out_off = 0, total_nodes = 0;
+
+    for (const TemplateGroup& grp : manifest.grouping.groups) {
+        require(grp.locators.size() == grp.members.size() && !grp.members.empty(),
+                Errc::invalid_argument, "grouping manifest is missing member locators");
+        const size_t nm = grp.members.size();
+        std::vector<CapturedGraph> graphs(nm);
+        parallel_for(nm, threads, [&](size_t i) {
+            graphs[i] = parse_graph_at(graphs_bin, grp.locators[i]);
+        });
+        // representative = smallest label (templater.hpp:16); members ascending
+        size_t rep = 0;
+        for (size_t i = 0; i < nm; ++i)
+            if (graphs[i].label == grp.representative) rep = i;
+        const CapturedGraph& T = graphs[rep];
+        const TopologyKey tkey = topology_key(T);
+        parallel_for(nm, threads, [&](size_t i) {
+            if (i == rep) return;
+            const TopologyKey k = topology_key(graphs[i]);
+            require(k == tkey, Errc::topology_mismatch,
+                    "donor topology " + k.hex() + " does not match exec topology " + tkey.hex());
+        });
+
+        // deterministic kernel-table pre-pass (member order, then real comm kernels)
+        for (const auto& g : graphs) {
+            for (const auto& n : g.nodes)
+                if (n.type == NodeType::Kernel)
+                    kt.intern(n.kernel_params().kernel, n.kernel_params().func_attrs);
+            auto pit = patches.per_graph.find(g.label);
+            if (pit == patches.per_graph.end()) continue;
+            for (const CommPatchEntry& e : pit->second)
+                if (e.node_id < g.nodes.size() && g.nodes[e.node_id].type == NodeType::Kernel)
+                    kt.intern(KernelRef{manifest.comm_real_hash, e.real_name},
+                              g.nodes[e.node_id].kernel_params().func_attrs);
+        }
+
+        GroupLayout L;
+        L.n_nodes = static_cast<uint32_t>(T.nodes.size());
+        L.cap.assign(L.n_nodes, 0);
+        L.blob_off.assign(L.n_nodes, 0);
+        for (const auto& g : graphs)
+            for (uint32_t n = 0; n < L.n_nodes; ++n)
+                L.cap[n] = std::max(L.cap[n], round16(blob_len_of(g.nodes[n])));
+        for (uint32_t n = 0; n < L.n_nodes; ++n) {
+            L.blob_off[n] = static_cast<uint32_t>(L.pool_bytes);
+            L.pool_bytes += L.cap[n];
+        }
+
+        fdt_group G{};
+        G.image_bytes = L.image_bytes();
+        G.n_nodes = L.n_nodes;
+        G.n_edges = static_cast<uint32_t>(T.edges.size());
+        G.first_member = static_cast<uint32_t>(members.size());
+        G.n_members = static_cast<uint32_t>(nm);
+        G.representative = grp.representative;
+        G.attrs_first = static_cast<uint32_t>(attrs.size());
+        G.edges_off = edges.size() * sizeof(uint32_t);
+        G.key_hi = tkey.digest.hi;
+        G.key_lo = tkey.digest.lo;
+        for (const auto& n : T.nodes) {
+            fdt_node_attrs a{};
+            a.cluster[0] = n.attrs.cluster_dim.x;
+            a.cluster[1] = n.attrs.cluster_dim.y;
+            a.cluster[2] = n.attrs.cluster_dim.z;
+            a.sched_policy = n.attrs.cluster_scheduling_policy_preference;
+            a.sync_default = n.attrs.mem_sync_domain_map_default;
+            a.sync_remote = n.attrs.mem_sync_domain_map_remote;
+            a.attr_query = n.attrs.attr_query_available ? 1 : 0;
+            attrs.push_back(a);
+        }
+        for (const auto& e : T.edges) {
+            edges.push_back(e.from);
+            edges.push_back(e.to);
+        }
+
+        std::vector<uint8_t> timg, tmeta;
+        build_image(T, L, kt, timg, tmeta);
+        timages.align(16);
+        G.timage_off = timages.size();  // rebased onto the section below
+        timages.raw(timg);
+        cmeta.resize(timages.size() / 16, 0);
+        std::copy(tmeta.begin(), tmeta.end(), cmeta.begin() + G.timage_off / 16);
+
+        std::vector<MemberOut> outs(nm);
+        parallel_for(nm, threads, [&](size_t i) {
+            const CapturedGraph& g = graphs[i];
+            MemberOut& o = outs[i];
+            std::vector<uint8_t> img, meta;
+            build_image(g, L, kt, img, meta);
+            const size_t nchunks = img.size() / 16;
+            for (size_t c = 0; c < nchunks; ++c) {
+                uint32_t mask = 0;
+                for (int j = 0; j < 16; ++j)
+                    if (img[16 * c + j] != timg[16 * c + j]) mask |= 1u << j;
+                const bool meta_differs = meta[c] != tmeta[c];
+                if (!mask && !meta_differs) continue;
+                uint32_t dm = mask;
+                if (meta_differs) dm |= FDT_DMETA_RELOC_OVERRIDE | (uint32_t(meta[c]) << FDT_DMETA_RELOC_SHIFT);
+                o.didx.push_back(static_cast<uint32_t>(c));
+                o.dmeta.push_back(dm);
+                o.ddata.insert(o.ddata.end(), img.begin() + 16 * c, img.begin() + 16 * c + 16);
+            }
+            auto pit = patches.per_graph.find(g.label);
+            if (pit == patches.per_graph.end()) return;
+            for (const CommPatchEntry& e : pit->second) {
+                // the checks apply_rank_patches performs (rank_forge.cpp:136-150)
+                require(e.node_id < g.nodes.size(), Errc::archive_corruption,
+                        "patch entry references missing node");
+                const GraphNode& n = g.nodes[e.node_id];
+                require(n.type == NodeType::Kernel, Errc::archive_corruption,
+                        "patch entry references a non-kernel node");
+                const auto& kp = n.kernel_params();
+                require(kp.kernel == e.stub, Errc::archive_corruption,
+                        "node " + std::to_string(e.node_id) + " is not the recorded stub " +
+                            e.stub.describe());
+                const uint32_t real =
+                    kt.lookup(KernelRef{manifest.comm_real_hash, e.real_name}, kp.func_attrs);
+                emit_write(o.rops, 48ull * e.node_id + offsetof(fdt_node, kernel), 4,
+                           FDT_ROP_KERNEL, real);
+                const uint64_t blob = L.desc_bytes() + L.blob_off[e.node_id];
+                for (uint32_t off : e.rank_offsets) {
+                    require(uint64_t(off) + 8 <= kp.arg_buffer.size(), Errc::invalid_argument,
+                            "patch offset outside the argument buffer");
+                    emit_write(o.rops, blob + off, 8, FDT_ROP_RANK, 0);
+                }
+                for (uint32_t off : e.world_offsets) {
+                    require(uint64_t(off) + 8 <= kp.arg_buffer.size(), Errc::invalid_argument,
+                            "patch offset outside the argument buffer");
+                    emit_write(o.rops, blob + off, 8, FDT_ROP_WORLD, 0);
+                }
+            }
+            std::stable_sort(o.rops.begin(), o.rops.end(),
+                             [](const fdt_rank_op& a, const fdt_rank_op& b) { return a.chunk < b.chunk; });
+        });
+
+        for (size_t i = 0; i < nm; ++i) {
+            MemberOut& o = outs[i];
+            fdt_member M{};
+            M.label = graphs[i].label;
+            M.group = static_cast<uint32_t>(groups.size());
+            M.out_off = out_off;
+            M.n_nodes = L.n_nodes;
+            M.first_tile = static_cast<uint32_t>(tiles.size());
+            const uint64_t nchunks = L.image_bytes() / 16;
+            const uint64_t ntiles = (nchunks + FDT_TILE_CHUNKS - 1) / FDT_TILE_CHUNKS;
+            M.n_tiles = static_cast<uint32_t>(ntiles);
+            const uint32_t d0 = static_cast<uint32_t>(didx.size());
+            const uint32_t r0 = static_cast<uint32_t>(rops.size());
+            size_t dpos = 0, rpos = 0;
+            for (uint64_t t = 0; t < ntiles; ++t) {
+                const uint64_t cb = t * FDT_TILE_CHUNKS;
+                const uint64_t ce = std::min<uint64_t>(nchunks, cb + FDT_TILE_CHUNKS);
+                fdt_tile T{};
+                T.src_off = G.timage_off + 16 * cb;  // rebased below
+                T.dst_off = out_off + 16 * cb;
+                T.nchunks = static_cast<uint32_t>(ce - cb);
+                T.member = static_cast<uint32_t>(members.size());
+                T.chunk_base = static_cast<uint32_t>(cb);
+                T.diff_lo = d0 + static_cast<uint32_t>(dpos);
+                while (dpos < o.didx.size() && o.didx[dpos] < ce) ++dpos;
+                T.diff_hi = d0 + static_cast<uint32_t>(dpos);
+                T.rop_lo = r0 + static_cast<uint32_t>(rpos);
+                while (rpos < o.rops.size() && o.rops[rpos].chunk < ce) ++rpos;
+                T.rop_hi = r0 + static_cast<uint32_t>(rpos);
+                tiles.push_back(T);
+            }
+            didx.insert(didx.end(), o.didx.begin(), o.didx.end());
+            dmeta.insert(dmeta.end(), o.dmeta.begin(), o.dmeta.end());
+            ddata.insert(ddata.end(), o.ddata.begin(), o.ddata.end());
+            rops.insert(rops.end(), o.rops.begin(), o.rops.end());
+            members.push_back(M);
+            out_off += L.image_bytes();
+            total_nodes += L.n_nodes;
+        }
+        groups.push_back(G);
+    }
+
+    // kernel table + strings
+    std::vector<fdt_kernel> kernels(kt.size());
+    std::string strings;
+    for (size_t k = 0; k < kt.size(); ++k) {
+        kernels[k].binary_hash = kt.ref(k).binary_hash;
+        kernels[k].name_off = static_cast<uint32_t>(strings.size());
+        kernels[k].name_len = static_cast<uint32_t>(kt.ref(k).name.size());
+        std::memcpy(kernels[k].func_attrs, &kt.attrs(k), sizeof(FuncAttrs));
+        strings += kt.ref(k).name;
+    }
+
+    fdt_header h{};
+    std::memcpy(h.magic, "FNDT", 4);
+    h.version = FDT_VERSION;
+    h.header_bytes = sizeof(fdt_header);
+    h.n_groups = static_cast<uint32_t>(groups.size());
+    h.n_members = static_cast<uint32_t>(members.size());
+    h.n_kernels = static_cast<uint32_t>(kernels.size());
+    h.n_tiles = static_cast<uint32_t>(tiles.size());
+    h.tile_chunks = FDT_TILE_CHUNKS;
+    h.n_diffs = static_cast<uint32_t>(didx.size());
+    h.n_rank_ops = static_cast<uint32_t>(rops.size());
+    h.source_graphs_crc = crc64(graphs_bin);
+    h.source_patch_crc = crc64(patch_bin);
+    h.old_base = manifest.allocator.base;
+    h.final_offset = manifest.final_offset;
+    h.real_comm_hash = manifest.comm_real_hash;
+    h.members_image_bytes = out_off;
+    h.total_nodes = total_nodes;
+
+    Sink s;
+    s.zeros(sizeof(fdt_header));
+    // TIMAGES first so the group/tile offsets can be rebased before writing them.
+    s.align(kSectionAlign);
+    const uint64_t timg_base = s.size();
+    h.sec[FDT_SEC_TIMAGES] = {timg_base, timages.size()};
+    s.raw(timages.bytes());
+    for (auto& G : groups) G.timage_off += timg_base;
+    for (auto& T : tiles) T.src_off += timg_base;
+    put_section(s, h, FDT_SEC_GROUPS, groups.data(), groups.size());
+    put_section(s, h, FDT_SEC_CMETA, cmeta.data(), cmeta.size());
+    put_section(s, h, FDT_SEC_MEMBERS, members.data(), members.size());
+    put_section(s, h, FDT_SEC_TILES, tiles.data(), tiles.size());
+    put_section(s, h, FDT_SEC_DIDX, didx.data(), didx.size());
+    put_section(s, h, FDT_SEC_DMETA, dmeta.data(), dmeta.size());
+    put_section(s, h, FDT_SEC_DDATA, ddata.data(), ddata.size());
+    put_section(s, h, FDT_SEC_ROPS, rops.data(), rops.size());
+    put_section(s, h, FDT_SEC_KERNELS, kernels.data(), kernels.size());
+    put_section(s, h, FDT_SEC_NODEATTRS, attrs.data(), attrs.size());
+    put_section(s, h, FDT_SEC_EDGES, edges.data(), edges.size());
+    put_section(s, h, FDT_SEC_STRINGS, strings.data(), strings.size());
+    s.align(kSectionAlign);
+    s.poke(0, h);
+
+    if (stats) {
+        stats->template_bytes = timages.size();
+        stats->diff_entries = didx.size();
+        stats->rank_ops = rops.size();
+        stats->member_image_bytes = out_off;
+        stats->store_bytes = s.size();
+    }
+    return s.release();
+}
+
+PackStats pack_archive_store(const std::filesystem::path& archive, unsigned threads) {
+    ArchivePaths paths{archive};
+    const auto mtext = slurp(paths.manifest());
+    Manifest m = parse_manifest(std::string(mtext.begin(), mtext.end()));
+    const auto graphs = slurp(paths.graphs());
+    const auto patch = slurp(paths.patch_table());
+    PackStats st;
+    const auto store = pack_template_store(graphs, patch, m, threads, &st);
+    spit(paths.template_store(), store);
+    m.file_digests["templates.fdt"] = crc64(store);
+    spit(paths.manifest(), serialize_manifest(m));
+    return st;
+}
+
+// ------------------------------------------------------------------ StoreView
+
+StoreView::StoreView(std::span<const uint8_t> blob) : blob_(blob) {
+    require(blob.size() >= sizeof(fdt_header), Errc::archive_corruption,
+            "template store: truncated input");
+    std::memcpy(&h_, blob.data(), sizeof h_);
+    require(std::memcmp(h_.magic, "FNDT", 4) == 0, Errc::archive_corruption,
+            "template store: bad magic, expected 'FNDT'");
+    require(h_.version == FDT_VERSION, Errc::archive_corruption,
+            "template store: unsupported version " + std::to_string(h_.version));
+    for (int i = 0; i < FDT_NSEC; ++i)
+        require(h_.sec[i].offset <= blob.size() && h_.sec[i].bytes <= blob.size() - h_.sec[i].offset,
+                Errc::archive_corruption, "template store: section overruns the blob");
+    auto at = [&](int id) { return blob.data() + h_.sec[id].offset; };
+    require(h_.sec[FDT_SEC_GROUPS].bytes == h_.n_groups * sizeof(fdt_group) &&
+                h_.sec[FDT_SEC_MEMBERS].bytes == h_.n_members * sizeof(fdt_member) &&
+                h_.sec[FDT_SEC_KERNELS].bytes == h_.n_kernels * sizeof(fdt_kernel) &&
+                h_.sec[FDT_SEC_TILES].bytes == h_.n_tiles * sizeof(fdt_tile),
+            Errc::archive_corruption, "template store: section sizes disagree with the header");
+    groups_ = reinterpret_cast<const fdt_group*>(at(FDT_SEC_GROUPS));
+    members_ = reinterpret_cast<const fdt_member*>(at(FDT_SEC_MEMBERS));
+    kernels_ = reinterpret_cast<const fdt_kernel*>(at(FDT_SEC_KERNELS));
+    attrs_ = reinterpret_cast<const fdt_node_attrs*>(at(FDT_SEC_NODEATTRS));
+    edges_ = at(FDT_SEC_EDGES);
+    strings_ = reinterpret_cast<const char*>(at(FDT_SEC_STRINGS));
+    uint32_t max_label = 0;
+    for (uint32_t m = 0; m < h_.n_members; ++m) max_label = std::max(max_label, members_[m].label);
+    by_label_.assign(size_t(max_label) + 1, -1);
+    for (uint32_t m = 0; m < h_.n_members; ++m) by_label_[members_[m].label] = int32_t(m);
+}
+
+std::string_view StoreView::kernel_name(uint32_t k) const {
+    return {strings_ + kernels_[k].name_off, kernels_[k].name_len};
+}
+
+KernelRef StoreView::kernel_ref(uint32_t k) const {
+    return KernelRef{kernels_[k].binary_hash, std::string(kernel_name(k))};
+}
+
+FuncAttrs StoreView::kernel_func_attrs(uint32_t k) const {
+    FuncAttrs f;
+    std::memcpy(&f, kernels_[k].func_attrs, sizeof f);
+    return f;
+}
+
+const fdt_node_attrs& StoreView::node_attrs(uint32_t g, uint32_t n) const {
+    return attrs_[groups_[g].attrs_first + n];
+}
+
+std::span<const uint32_t> StoreView::edges(uint32_t g) const {
+    return {reinterpret_cast<const uint32_t*>(edges_ + groups_[g].edges_off),
+            size_t(groups_[g].n_edges) * 2};
+}
+
+int64_t StoreView::member_of(uint32_t label) const {
+    return label < by_label_.size() ? by_label_[label] : -1;
+}
+
+CapturedGraph StoreView::image_to_graph(uint32_t m, std::span<const uint8_t> image) const {
+    const fdt_member& M = members_[m];
+    const fdt_group& G = groups_[M.group];
+    require(image.size() >= G.image_bytes, Errc::invalid_argument, "member image too small");
+    CapturedGraph g;
+    g.label = M.label;
+    g.nodes.resize(G.n_nodes);
+    const uint8_t* pool = image.data() + 48ull * G.n_nodes;
+    for (uint32_t i = 0; i < G.n_nodes; ++i) {
+        fdt_node d;
+        std::memcpy(&d, image.data() + 48ull * i, sizeof d);
+        GraphNode& n = g.nodes[i];
+        n.id = i;
+        n.type = static_cast<NodeType>(d.type);
+        const uint8_t* blob = pool + d.blob_off;
+        if (n.type == NodeType::Kernel) {
+            const fdt_node_attrs& a = node_attrs(M.group, i);
+            n.attrs.cluster_dim = {a.cluster[0], a.cluster[1], a.cluster[2]};
+            n.attrs.cluster_scheduling_policy_preference = a.sched_policy;
+            n.attrs.mem_sync_domain_map_default = a.sync_default;
+            n.attrs.mem_sync_domain_map_remote = a.sync_remote;
+            n.attrs.attr_query_available = a.attr_query != 0;
+            KernelNodeParams k;
+            require(d.kernel < h_.n_kernels, Errc::archive_corruption,
+                    "template store: kernel index out of range");
+            k.kernel = kernel_ref(d.kernel);
+            k.func_attrs = kernel_func_attrs(d.kernel);
+            k.grid = {d.grid[0], d.grid[1], d.grid[2]};
+            k.block = {d.block[0], d.block[1], d.block[2]};
+            k.shared_mem_bytes = d.shmem;
+            k.arg_buffer.assign(blob, blob + d.blob_len);
+            n.params = std::move(k);
+        } else if (n.type == NodeType::Memcpy) {
+            MemcpyParams p;
+            std::memcpy(&p.src, blob, 8);
+            std::memcpy(&p.dst, blob + 8, 8);
+            std::memcpy(&p.length, blob + 16, 8);
+            n.params = p;
+        } else if (n.type == NodeType::Memset) {
+            MemsetParams p;
+            std::memcpy(&p.dst, blob, 8);
+            std::memcpy(&p.value, blob + 8, 8);
+            std::memcpy(&p.length, blob + 16, 8);
+            n.params = p;
+        } else {
+            n.params = EmptyParams{};
+        }
+    }
+    const auto e = edges(M.group);
+    g.edges.resize(G.n_edges);
+    for (uint32_t i = 0; i < G.n_edges; ++i) g.edges[i] = {e[2 * i], e[2 * i + 1]};
+    return g;
+}
+
+}  // namespace foundry

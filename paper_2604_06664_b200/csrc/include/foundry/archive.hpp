@@ -1,0 +1,187 @@
+// Archive side-files: manifest (JSON), catalog.bin (FNDC), patch.bin (FNDP),
+// memlayout.bin and the simulated device-binary format FNDB.
+//
+// Layouts and field names follow the reference so a reference-written archive
+// loads here unchanged (reference pipeline.hpp:17-48, pipeline.cpp:23-139;
+// binary_catalog.hpp:17-40, binary_catalog.cpp:33-105; rank_forge.hpp:19-38,
+// rank_forge.cpp:43-102; det_alloc.hpp:18-53, det_alloc.cpp:20-59;
+// kernel_image.hpp:11-61, kernel_image.cpp:14-117; templater.hpp:15-38).
+#pragma once
+
+#include <cstdint>
+#include <filesystem>
+#include <map>
+#include <optional>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "foundry/graph_model.hpp"
+
+namespace foundry {
+
+// ------------------------------------------------------------ allocator
+struct RegionConfig {
+    uint64_t base = 0x700000000000ull;
+    uint64_t capacity = 4ull << 30;
+    uint64_t granularity = 64ull << 10;
+    bool operator==(const RegionConfig&) const = default;
+};
+
+enum class AllocWindow : uint8_t { pre_capture = 0, capture_window = 1 };
+
+struct AllocationRecord {
+    uint64_t sequence = 0;
+    uint64_t size = 0;
+    uint64_t address = 0;
+    uint64_t length = 0;
+    AllocWindow window = AllocWindow::pre_capture;
+    bool operator==(const AllocationRecord&) const = default;
+};
+
+struct MemoryEventLog {
+    RegionConfig config;
+    uint64_t starting_offset = 0;
+    uint64_t final_offset = 0;
+    std::vector<AllocationRecord> records;
+    bool operator==(const MemoryEventLog&) const = default;
+};
+
+std::vector<uint8_t> serialize_event_log(const MemoryEventLog& log);
+MemoryEventLog parse_event_log(std::span<const uint8_t> bytes);
+
+// ------------------------------------------------------------ grouping
+struct TemplateGroup {
+    TopologyKey key;
+    uint32_t representative = 0;
+    std::vector<uint32_t> members;
+    std::vector<GraphLocator> locators;
+    bool operator==(const TemplateGroup&) const = default;
+};
+
+struct GroupingManifest {
+    std::vector<TemplateGroup> groups;
+    uint32_t total_graphs = 0;
+    uint32_t template_count = 0;
+    double update_served_fraction() const {
+        return total_graphs ? double(total_graphs - template_count) / total_graphs : 0.0;
+    }
+    bool operator==(const GroupingManifest&) const = default;
+};
+
+// Groups graphs by topology key; representative = smallest label
+// (reference templater.cpp:18-52).
+GroupingManifest group_graphs(const std::vector<CapturedGraph>& graphs);
+void attach_locators(GroupingManifest& m, const std::vector<GraphLocator>& locators);
+
+// ------------------------------------------------------------ manifest
+struct Manifest {
+    static constexpr uint32_t kFormatVersion = 1;
+    uint32_t format_version = kFormatVersion;
+    uint8_t hash_algorithm = kContentHashAlgorithm;
+    uint64_t workload_digest = 0;
+    std::string workload_text;
+    RegionConfig allocator;
+    uint64_t final_offset = 0;
+    uint64_t kv_cache_bytes = 0;
+    uint64_t comm_world_placeholder = 1;
+    uint64_t comm_real_hash = 0;
+    GroupingManifest grouping;
+    std::string memlayout_ref = "memlayout.bin";
+    std::string catalog_ref = "catalog.bin";
+    std::string patch_table_ref = "patch.bin";
+    std::map<std::string, uint64_t> file_digests;
+};
+
+std::string serialize_manifest(const Manifest& m);
+Manifest parse_manifest(const std::string& text);
+
+struct ArchivePaths {
+    std::filesystem::path root;
+    std::filesystem::path manifest() const { return root / "manifest"; }
+    std::filesystem::path graphs() const { return root / "graphs.bin"; }
+    std::filesystem::path memlayout() const { return root / "memlayout.bin"; }
+    std::filesystem::path catalog() const { return root / "catalog.bin"; }
+    std::filesystem::path patch_table() const { return root / "patch.bin"; }
+    std::filesystem::path binaries() const { return root / "binaries"; }
+    std::filesystem::path binary(uint64_t hash) const { return binaries() / (hex16(hash) + ".bin"); }
+    // B200 additions (ignored by the reference loader):
+    std::filesystem::path template_store() const { return root / "templates.fdt"; }
+    std::filesystem::path cubin(uint64_t hash) const {
+        return binaries() / (hex16(hash) + ".sm_100a.cubin");
+    }
+};
+
+// ------------------------------------------------------------ FNDB images
+struct KernelEntry {
+    std::string name;
+    uint32_t arg_buffer_size = 0;
+    std::vector<uint32_t> hidden_offsets;  // 8-byte device addresses the kernel dereferences
+    FuncAttrs attrs;
+    bool operator==(const KernelEntry&) const = default;
+};
+
+struct KernelImage {
+    bool relocatable = false;
+    bool requires_device_init = false;
+    uint32_t link_tag = 0;
+    std::vector<KernelEntry> entrypoints;
+    std::vector<uint8_t> aux;
+    bool operator==(const KernelImage&) const = default;
+};
+
+std::vector<uint8_t> encode_kernel_image(const KernelImage& image);
+KernelImage parse_kernel_image(std::span<const uint8_t> payload);
+std::vector<uint8_t> link_segments(const std::vector<std::vector<uint8_t>>& segments);
+
+// ------------------------------------------------------------ catalog
+enum class LoadVariant : uint8_t { data = 0, file = 1, with_options = 2 };
+
+struct KernelBinaryRecord {
+    uint64_t hash = 0;
+    LoadVariant variant = LoadVariant::data;
+    std::vector<uint8_t> load_options;
+    bool needs_device_init = false;
+    bool is_stub = false;
+    bool is_comm_real = false;
+    std::vector<std::string> entrypoints;
+    std::vector<FuncAttrs> entrypoint_attrs;
+    bool operator==(const KernelBinaryRecord&) const = default;
+};
+
+struct Catalog {
+    std::map<uint64_t, KernelBinaryRecord> binaries;
+    bool operator==(const Catalog&) const = default;
+};
+
+std::vector<uint8_t> serialize_catalog(const Catalog& c);
+Catalog parse_catalog(std::span<const uint8_t> bytes);
+
+// ------------------------------------------------------------ patch table
+struct CommPatchEntry {
+    uint32_t node_id = 0;
+    KernelRef stub;
+    std::string real_name;
+    std::vector<uint32_t> rank_offsets;
+    std::vector<uint32_t> world_offsets;
+    uint8_t patch_width = 8;
+    bool operator==(const CommPatchEntry&) const = default;
+};
+
+struct PatchTable {
+    uint64_t world_placeholder = 1;
+    std::map<uint32_t, std::vector<CommPatchEntry>> per_graph;
+    bool empty() const { return per_graph.empty(); }
+    size_t total_entries() const;
+    bool operator==(const PatchTable&) const = default;
+};
+
+std::vector<uint8_t> serialize_patch_table(const PatchTable& t);
+PatchTable parse_patch_table(std::span<const uint8_t> bytes);
+
+// Host reference of the K3 rewrite (reference rank_forge.cpp:132-152), kept for
+// the drop-in C++ surface; LOAD itself patches on the GPU.
+void apply_rank_patches(CapturedGraph& graph, std::span<const CommPatchEntry> entries,
+                        uint64_t real_comm_hash, uint32_t rank, uint32_t world);
+
+}  // namespace foundry

@@ -1,0 +1,134 @@
+// B200 device runtime: one CUDA device, its streams, HBM buffers, and the
+// launches of the sm_100a kernels (materialize, CRC-64). No CPU fallback:
+// every entry point raises Errc::device_unavailable when no GPU/driver exists.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <vector>
+
+#include "foundry/errors.hpp"
+#include "foundry/store_format.h"
+
+typedef struct CUstream_st* cudaStream_t;
+typedef struct CUevent_st* cudaEvent_t;
+
+namespace foundry {
+
+// Raises Errc::cuda_error (or device_unavailable) for a failed runtime call.
+void cuda_check(int err, const char* what);
+bool cuda_available();
+int cuda_device_count();
+
+class Device {
+public:
+    explicit Device(int ordinal);
+    ~Device();
+    Device(const Device&) = delete;
+    Device& operator=(const Device&) = delete;
+
+    int ordinal() const { return ordinal_; }
+    int sm_count() const { return sm_count_; }
+    cudaStream_t stream() const { return stream_; }
+    cudaStream_t copy_stream() const { return copy_stream_; }
+    void make_current() const;
+    void sync() const;
+
+    void* alloc(size_t bytes);
+    void release(void* p);
+    void* alloc_host_pinned(size_t bytes);
+    void release_host_pinned(void* p);
+
+private:
+    int ordinal_;
+    int sm_count_ = 0;
+    cudaStream_t stream_ = nullptr;
+    cudaStream_t copy_stream_ = nullptr;
+};
+
+// Device-resident buffer with RAII release.
+class DeviceBuffer {
+public:
+    DeviceBuffer() = default;
+    DeviceBuffer(Device& dev, size_t bytes);
+    ~DeviceBuffer();
+    DeviceBuffer(DeviceBuffer&& o) noexcept { *this = std::move(o); }
+    DeviceBuffer& operator=(DeviceBuffer&& o) noexcept;
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+
+    unsigned char* data() const { return p_; }
+    size_t size() const { return n_; }
+    Device* device() const { return dev_; }
+
+private:
+    Device* dev_ = nullptr;
+    unsigned char* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+class PinnedBuffer {
+public:
+    PinnedBuffer() = default;
+    PinnedBuffer(Device& dev, size_t bytes);
+    ~PinnedBuffer();
+    PinnedBuffer(PinnedBuffer&& o) noexcept { *this = std::move(o); }
+    PinnedBuffer& operator=(PinnedBuffer&& o) noexcept;
+    PinnedBuffer(const PinnedBuffer&) = delete;
+    PinnedBuffer& operator=(const PinnedBuffer&) = delete;
+
+    unsigned char* data() const { return p_; }
+    size_t size() const { return n_; }
+
+private:
+    Device* dev_ = nullptr;
+    unsigned char* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+// A template store resident in HBM (blob uploaded verbatim).
+struct DeviceStore {
+    Device* dev = nullptr;
+    DeviceBuffer blob;   // owning, unless `borrowed` is set
+    const unsigned char* data = nullptr;
+    size_t bytes = 0;
+    fdt_header header{};
+};
+
+struct MaterializeRequest {
+    uint32_t rank = 0;
+    uint32_t world = 1;
+    uint64_t new_base = 0;  // 0 = keep the captured base
+    std::vector<uint64_t> values;  // FDT_ROP_VALUE table
+};
+
+struct MaterializeTiming {
+    float kernel_ms = 0.f;  // CUDA-event time of the fused kernel, launching stream
+    int grid = 0;
+    int blocks_per_sm = 0;
+};
+
+// Checks a device-resident store blob's header (host copy) and prepares pointers.
+DeviceStore adopt_store(Device& dev, const unsigned char* d_blob, size_t bytes,
+                        const fdt_header& host_header);
+DeviceStore upload_store(Device& dev, const void* host_blob, size_t bytes);
+
+// Launches K2+K1+K3 into `out` (must hold header.members_image_bytes bytes).
+// Asynchronous on dev.stream(); timing (if non-null) is filled after a sync.
+void launch_materialize(Device& dev, const DeviceStore& store, const MaterializeRequest& req,
+                        unsigned char* out, MaterializeTiming* timing, int grid_override = 0,
+                        const uint64_t* d_values = nullptr);
+
+struct Segment {
+    uint64_t offset = 0;  // within the device buffer
+    uint64_t length = 0;
+};
+
+// GPU CRC-64/XZ of byte ranges in device memory; returns one digest per range.
+// Blocking (one small D2H of the digests).
+std::vector<uint64_t> crc64_device(Device& dev, const unsigned char* d_base,
+                                   std::span<const Segment> segments, float* kernel_ms = nullptr);
+
+}  // namespace foundry

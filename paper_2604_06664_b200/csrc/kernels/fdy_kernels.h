@@ -1,0 +1,54 @@
+// Internal interface between the sm_100a kernels and the host runtime.
+// (The public C-ABI is include/foundry_b200.h at the repository root.)
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "foundry/store_format.h"
+
+struct FdyMaterializeArgs {
+    const unsigned char* store;  // template store blob in HBM
+    unsigned char* out;          // member image arena in HBM
+    const fdt_tile* tiles;
+    const uint8_t* cmeta;
+    const uint32_t* didx;
+    const uint32_t* dmeta;
+    const uint4* ddata;
+    const fdt_rank_op* rops;
+    const uint64_t* values;  // FDT_ROP_VALUE table (may be null)
+    uint64_t timage_base;    // store offset of FDT_SEC_TIMAGES
+    uint64_t old_base;       // captured VA base
+    uint64_t span;           // final_offset
+    uint64_t delta;          // new_base - old_base (mod 2^64)
+    uint64_t rank;
+    uint64_t world;
+    uint32_t n_tiles;
+    uint32_t n_values;
+};
+
+struct FdyCrcBlock {
+    uint32_t segment;
+    uint32_t length;   // <= kCrcBlockBytes
+    uint64_t offset;   // absolute offset of the block in the device buffer
+};
+
+extern "C" {
+size_t fdy_materialize_smem_bytes();
+cudaError_t fdy_materialize_occupancy(int* blocks_per_sm);
+cudaError_t fdy_launch_materialize(const FdyMaterializeArgs* args, int grid, cudaStream_t stream);
+
+cudaError_t fdy_crc64_set_constants(const uint64_t* x2k64);  // per device
+// CRC-64/XZ of n_segments byte ranges already resident in device memory.
+// blocks: host-built table (see fdy_crc_plan) in device memory; partial /
+// lengths scratch: n_blocks entries each; out: n_segments digests (device).
+cudaError_t fdy_launch_crc64(const unsigned char* base, const FdyCrcBlock* blocks,
+                             uint32_t n_blocks, const uint32_t* seg_first_block,
+                             const uint32_t* seg_n_blocks, uint32_t n_segments,
+                             uint64_t* scratch_crc, uint64_t* scratch_len, uint64_t* out,
+                             cudaStream_t stream);
+}
+
+inline constexpr uint32_t kCrcBlockBytes = 65536;  // one CTA, 256 B per thread

@@ -1,0 +1,153 @@
+// fdy_tool — command-line front end to libfoundry_b200 (tooling + test driver).
+//
+//   pack <archive> [threads]                       write templates.fdt (+ manifest digest)
+//   gpu-materialize <archive> <rank> <world> <new_base_hex|0> <out.fndg> [reps] [device]
+//        DMA the store into HBM, run the fused K2+K1+K3 kernel, copy the member
+//        images back and re-encode them as an FNDG container in graphs.bin
+//        locator order (the layout of oracle/ref_tool `prepare`).
+//   gpu-crc <file>...                              CRC-64/XZ of files on the GPU
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "foundry/archive.hpp"
+#include "foundry/bytes.hpp"
+#include "foundry/template_store.hpp"
+#include "foundry_b200.h"
+
+using namespace foundry;
+
+static int die(const char* what) {
+    std::fprintf(stderr, "%s: %s\n", what, fdy_last_error());
+    return 2;
+}
+
+static int cmd_pack(int argc, char** argv) {
+    const unsigned threads = argc > 3 ? static_cast<unsigned>(std::stoul(argv[3])) : 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    const PackStats st = pack_archive_store(argv[2], threads);
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::printf("{\"store_bytes\": %llu, \"template_bytes\": %llu, \"diff_entries\": %llu, "
+                "\"rank_ops\": %llu, \"member_image_bytes\": %llu, \"pack_ms\": %.3f}\n",
+                (unsigned long long)st.store_bytes, (unsigned long long)st.template_bytes,
+                (unsigned long long)st.diff_entries, (unsigned long long)st.rank_ops,
+                (unsigned long long)st.member_image_bytes, ms);
+    return 0;
+}
+
+static int cmd_gpu_materialize(int argc, char** argv) {
+    if (argc < 7) return 64;
+    ArchivePaths paths{argv[2]};
+    const uint32_t rank = static_cast<uint32_t>(std::stoul(argv[3]));
+    const uint32_t world = static_cast<uint32_t>(std::stoul(argv[4]));
+    const uint64_t new_base = std::string(argv[5]) == "0" ? 0 : parse_hex(argv[5]);
+    const int reps = argc > 7 ? std::stoi(argv[7]) : 1;
+    const int ordinal = argc > 8 ? std::stoi(argv[8]) : 0;
+    const auto blob = slurp(paths.template_store());
+    StoreView view(blob);
+
+    fdy_device* dev = nullptr;
+    if (fdy_device_open(ordinal, &dev)) return die("fdy_device_open");
+    fdy_store* store = nullptr;
+    if (fdy_store_upload(dev, blob.data(), blob.size(), &store)) return die("fdy_store_upload");
+    fdy_materialize_desc d{};
+    d.rank = rank;
+    d.world = world;
+    d.new_base = new_base;
+    fdy_members* members = nullptr;
+    float ms = 0.f;
+    if (fdy_materialize(dev, store, &d, &members, &ms)) return die("fdy_materialize");
+    std::vector<float> times{ms};
+    for (int i = 1; i < reps; ++i) {
+        if (fdy_materialize_into(dev, store, &d, members, &ms)) return die("fdy_materialize_into");
+        times.push_back(ms);
+    }
+    std::vector<uint8_t> arena(fdy_members_bytes(members));
+    if (fdy_members_download(members, arena.data(), 0, arena.size())) return die("download");
+
+    const auto graphs_bin = slurp(paths.graphs());
+    std::vector<CapturedGraph> out;
+    for (const auto& loc : parse_graph_locators(graphs_bin)) {
+        const int64_t m = view.member_of(loc.label);
+        require(m >= 0, Errc::archive_corruption, "store has no member " + std::to_string(loc.label));
+        const auto& M = view.member(static_cast<uint32_t>(m));
+        const auto& G = view.group(M.group);
+        out.push_back(view.image_to_graph(static_cast<uint32_t>(m),
+                                          std::span<const uint8_t>(arena.data() + M.out_off, G.image_bytes)));
+    }
+    spit(argv[6], serialize_graphs(out));
+    float best = times[0];
+    for (float t : times) best = std::min(best, t);
+    std::printf("{\"kernel_ms_first\": %.6f, \"kernel_ms_best\": %.6f, \"reps\": %d, "
+                "\"members_bytes\": %zu, \"store_bytes\": %zu, \"tiles\": %u}\n",
+                times[0], best, reps, arena.size(), blob.size(), view.header().n_tiles);
+    fdy_members_free(members);
+    fdy_store_free(store);
+    fdy_device_close(dev);
+    return 0;
+}
+
+// decode an externally produced member-image arena (test emulator) to FNDG
+static int cmd_decode(int argc, char** argv) {
+    if (argc < 5) return 64;
+    ArchivePaths paths{argv[2]};
+    const auto blob = slurp(paths.template_store());
+    StoreView view(blob);
+    const auto arena = slurp(argv[3]);
+    const auto graphs_bin = slurp(paths.graphs());
+    std::vector<CapturedGraph> out;
+    for (const auto& loc : parse_graph_locators(graphs_bin)) {
+        const int64_t m = view.member_of(loc.label);
+        require(m >= 0, Errc::archive_corruption, "store has no member " + std::to_string(loc.label));
+        const auto& M = view.member(static_cast<uint32_t>(m));
+        out.push_back(view.image_to_graph(static_cast<uint32_t>(m),
+                                          std::span<const uint8_t>(arena.data() + M.out_off,
+                                                                   view.group(M.group).image_bytes)));
+    }
+    spit(argv[4], serialize_graphs(out));
+    return 0;
+}
+
+static int cmd_gpu_crc(int argc, char** argv) {
+    fdy_device* dev = nullptr;
+    if (fdy_device_open(0, &dev)) return die("fdy_device_open");
+    std::vector<uint8_t> all;
+    std::vector<uint64_t> off, len;
+    for (int i = 2; i < argc; ++i) {
+        const auto b = slurp(argv[i]);
+        off.push_back(all.size());
+        len.push_back(b.size());
+        all.insert(all.end(), b.begin(), b.end());
+    }
+    std::vector<uint64_t> dig(off.size());
+    float ms = 0;
+    if (fdy_crc64_segments(dev, all.data(), all.size(), off.data(), len.data(),
+                           static_cast<uint32_t>(off.size()), dig.data(), &ms))
+        return die("fdy_crc64_segments");
+    for (size_t i = 0; i < dig.size(); ++i) std::printf("%s %s\n", hex16(dig[i]).c_str(), argv[i + 2]);
+    std::fprintf(stderr, "kernel_ms %.6f\n", ms);
+    fdy_device_close(dev);
+    return 0;
+}
+
+int main(int argc, char** argv) {
+    if (argc < 3) {
+        std::fprintf(stderr, "usage: fdy_tool pack|gpu-materialize|gpu-crc ...\n");
+        return 64;
+    }
+    const std::string cmd = argv[1];
+    try {
+        if (cmd == "pack") return cmd_pack(argc, argv);
+        if (cmd == "gpu-materialize") return cmd_gpu_materialize(argc, argv);
+        if (cmd == "gpu-crc") return cmd_gpu_crc(argc, argv);
+        if (cmd == "decode") return cmd_decode(argc, argv);
+    } catch (const Error& e) {
+        std::fprintf(stderr, "%s\n", e.what());
+        return 2;
+    }
+    std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
+    return 64;
+}

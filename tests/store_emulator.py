@@ -1,0 +1,86 @@
+"""NumPy emulation of the fused materialize kernel over a packed FNDT store.
+
+TEST INFRASTRUCTURE: lets the CPU-only suite check the packer's diff/rank-op
+streams end to end (store -> member images -> FNDG records == oracle) without
+a GPU. It restates csrc/kernels/materialize.cu, not the reference; the GPU
+suite checks the kernel itself against the oracle.
+"""
+from __future__ import annotations
+
+import struct
+
+import numpy as np
+
+HEADER = struct.Struct("<4sHHIIIIIIII")  # up to n_rank_ops
+SEC_NAMES = ["groups", "timages", "cmeta", "members", "tiles", "didx", "dmeta", "ddata",
+             "rops", "kernels", "nodeattrs", "edges", "strings"]
+
+TILE_DT = np.dtype([("src_off", "<u8"), ("dst_off", "<u8"), ("nchunks", "<u4"), ("member", "<u4"),
+                    ("diff_lo", "<u4"), ("diff_hi", "<u4"), ("rop_lo", "<u4"), ("rop_hi", "<u4"),
+                    ("chunk_base", "<u4"), ("pad", "<u4")])
+ROP_DT = np.dtype([("chunk", "<u4"), ("kind", "u1"), ("shift", "i1"), ("mask", "<u2"),
+                   ("aux", "<u4"), ("pad", "<u4")])
+
+
+def parse_header(blob: bytes) -> dict:
+    f = HEADER.unpack_from(blob, 0)
+    h = dict(zip(["magic", "version", "flags", "header_bytes", "n_groups", "n_members",
+                  "n_kernels", "n_tiles", "tile_chunks", "n_diffs", "n_rank_ops"], f))
+    (h["source_graphs_crc"], h["source_patch_crc"], h["old_base"], h["final_offset"],
+     h["real_comm_hash"], h["members_image_bytes"], h["total_nodes"]) = struct.unpack_from("<7Q", blob, 40)
+    secs = struct.unpack_from("<%dQ" % (2 * len(SEC_NAMES)), blob, 96)
+    h["sec"] = {n: (secs[2 * i], secs[2 * i + 1]) for i, n in enumerate(SEC_NAMES)}
+    return h
+
+
+def expand(blob: bytes, rank: int, world: int, new_base: int = 0, values=()) -> bytes:
+    h = parse_header(blob)
+    assert h["magic"] == b"FNDT"
+    b = np.frombuffer(blob, dtype=np.uint8)
+
+    def sec(name, dtype):
+        off, n = h["sec"][name]
+        return b[off:off + n].view(dtype)
+
+    tiles = sec("tiles", TILE_DT)
+    cmeta = sec("cmeta", np.uint8)
+    didx = sec("didx", np.uint32)
+    dmeta = sec("dmeta", np.uint32)
+    ddata = sec("ddata", np.uint8).reshape(-1, 16)
+    rops = sec("rops", ROP_DT)
+    timg_base = h["sec"]["timages"][0]
+    old, span = h["old_base"], h["final_offset"]
+    delta = (new_base - old) % (1 << 64) if new_base else 0
+    out = np.zeros(h["members_image_bytes"], dtype=np.uint8)
+    for t in tiles:
+        n = int(t["nchunks"])
+        src = int(t["src_off"])
+        chunks = b[src:src + 16 * n].reshape(n, 16).copy()
+        meta = cmeta[(src - timg_base) // 16:(src - timg_base) // 16 + n].astype(np.uint32).copy()
+        lo, hi = int(t["diff_lo"]), int(t["diff_hi"])
+        if hi > lo:
+            rows = didx[lo:hi].astype(np.int64) - int(t["chunk_base"])
+            dm = dmeta[lo:hi]
+            bits = ((dm[:, None] >> np.arange(16, dtype=np.uint32)) & 1).astype(bool)
+            chunks[rows] = np.where(bits, ddata[lo:hi], chunks[rows])
+            ov = (dm & 0x10000) != 0
+            meta[rows[ov]] = (dm[ov] >> 17) & 3
+        if delta:
+            lanes = chunks.view("<u8").reshape(n, 2)
+            for lane, bit in ((0, 1), (1, 2)):
+                v = lanes[:, lane]
+                sel = ((meta & bit) != 0) & ((v - np.uint64(old)) < np.uint64(span))
+                v[sel] = v[sel] + np.uint64(delta)
+        flat = chunks.reshape(-1)
+        for op in rops[int(t["rop_lo"]):int(t["rop_hi"])]:
+            kind = int(op["kind"])
+            val = {0: rank, 1: world, 2: int(op["aux"])}.get(kind)
+            if val is None:
+                val = values[int(op["aux"])] if int(op["aux"]) < len(values) else 0
+            base = 16 * (int(op["chunk"]) - int(t["chunk_base"]))
+            for j in range(16):
+                if int(op["mask"]) >> j & 1:
+                    flat[base + j] = (val >> (8 * (j - int(op["shift"])))) & 0xFF
+        dst = int(t["dst_off"])
+        out[dst:dst + 16 * n] = flat
+    return out.tobytes()
