@@ -39,6 +39,9 @@ HOST_SRCS = [
     "host/archive.cpp",
     "host/template_store.cpp",
     "host/device.cpp",
+    "host/workload.cpp",
+    "host/save.cpp",
+    "host/trace_module.cpp",
     "capi/capi_misc.cpp",
     "capi/capi_kernels.cpp",
 ]
@@ -81,8 +84,11 @@ def _write_ninja() -> Path:
         "  deps = gcc",
         "  description = NVCC $in",
         "rule ptx",
-        "  command = $nvcc -std=c++17 -arch=sm_100a -rdc=true -ptx -O3 -lineinfo $in -o $out",
+        f"  command = $nvcc -std=c++17 -arch=sm_100a -rdc=true -ptx -O3 -lineinfo -I{CSRC}/include $in -o $out",
         "  description = PTX $in",
+        "rule embed",
+        f"  command = {sys.executable} {CSRC}/tools/embed_ptx.py $in $out",
+        "  description = EMBED $in",
         "rule link",
         f"  command = $cxx -shared -o $out $in {cudart} -ldl -lrt -lpthread "
         "-Wl,-soname,libfoundry_b200.so",
@@ -104,6 +110,11 @@ def _write_ninja() -> Path:
         obj = BUILD / (src.replace("/", "_") + ".o")
         lines.append(f"build {obj}: nvcc {CSRC / src}")
         objs.append(str(obj))
+    ptx = BUILD / "trace_body.ptx"
+    lines.append(f"build {ptx}: ptx {CSRC / 'kernels/trace_body.cu'}")
+    lines.append(f"build {BUILD / 'trace_body_ptx.cpp'}: embed {ptx}")
+    lines.append(f"build {BUILD / 'trace_body_ptx.o'}: cxx {BUILD / 'trace_body_ptx.cpp'}")
+    objs.append(str(BUILD / "trace_body_ptx.o"))
     lib = PKG / "libfoundry_b200.so"
     lines.append(f"build {lib}: link {' '.join(objs)}")
     lines.append(f"build {PKG / 'fdy_tool'}: exe {CSRC / 'tools/fdy_tool.cpp'} | {lib}")

@@ -1,0 +1,104 @@
+// Generation of per-binary trace cubins (see trace_module.hpp).
+#include "foundry/trace_module.hpp"
+
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <sstream>
+#include <unistd.h>
+
+#include "foundry/bytes.hpp"
+#include "foundry/parallel.hpp"
+
+namespace foundry {
+
+namespace fs = std::filesystem;
+
+std::string trace_module_ptx(const KernelImage& image, uint32_t ordinal, bool needs_init) {
+    std::ostringstream o;
+    o << ".version 8.8\n.target sm_100a\n.address_size 64\n\n";
+    // device body: strip its own module header
+    std::istringstream body(trace_body_ptx());
+    std::string line;
+    while (std::getline(body, line)) {
+        if (line.rfind(".version", 0) == 0 || line.rfind(".target", 0) == 0 ||
+            line.rfind(".address_size", 0) == 0)
+            continue;
+        o << line << "\n";
+    }
+    for (size_t i = 0; i < image.entrypoints.size(); ++i) {
+        const KernelEntry& e = image.entrypoints[i];
+        require(e.arg_buffer_size > 0 && e.arg_buffer_size <= 32764, Errc::binary_format,
+                "entrypoint '" + e.name + "' has an argument buffer the device ABI cannot carry");
+        const uint32_t entry_id = (ordinal << 16) | static_cast<uint32_t>(i);
+        const std::string h = "fdy_hidden_" + std::to_string(i);
+        if (!e.hidden_offsets.empty()) {
+            o << ".global .align 4 .u32 " << h << "[" << e.hidden_offsets.size() << "] = {";
+            for (size_t k = 0; k < e.hidden_offsets.size(); ++k) o << (k ? ", " : "") << e.hidden_offsets[k];
+            o << "};\n";
+        }
+        o << ".visible .entry " << e.name << "(\n\t.param .align 8 .b8 " << e.name << "_param_0["
+          << e.arg_buffer_size << "]\n)\n{\n"
+          << "\t.reg .b64 %rd<5>;\n"
+          << "\tmov.b64 %rd1, " << e.name << "_param_0;\n"
+          << "\tcvta.param.u64 %rd2, %rd1;\n";
+        if (!e.hidden_offsets.empty())
+            o << "\tmov.u64 %rd3, " << h << ";\n\tcvta.global.u64 %rd4, %rd3;\n";
+        else
+            o << "\tmov.u64 %rd4, 0;\n";
+        o << "\t{\n\t.param .b64 p0;\n\t.param .b32 p1;\n\t.param .b64 p2;\n\t.param .b32 p3;\n"
+          << "\t.param .b32 p4;\n\t.param .b32 p5;\n"
+          << "\tst.param.b64 [p0], %rd2;\n\tst.param.b32 [p1], " << e.arg_buffer_size << ";\n"
+          << "\tst.param.b64 [p2], %rd4;\n\tst.param.b32 [p3], " << e.hidden_offsets.size() << ";\n"
+          << "\tst.param.b32 [p4], " << entry_id << ";\n\tst.param.b32 [p5], " << (needs_init ? 1 : 0)
+          << ";\n\tcall.uni fdy_trace_body, (p0, p1, p2, p3, p4, p5);\n\t}\n\tret;\n}\n";
+    }
+    return o.str();
+}
+
+std::vector<uint8_t> compile_ptx_to_cubin(const std::string& ptx) {
+    const char* home = std::getenv("CUDA_HOME");
+    const std::string ptxas = std::string(home ? home : "/usr/local/cuda") + "/bin/ptxas";
+    char dir[] = "/tmp/fdy_ptx_XXXXXX";
+    require(mkdtemp(dir) != nullptr, Errc::invalid_argument, "cannot create a temp dir for ptxas");
+    const fs::path in = fs::path(dir) / "m.ptx", out = fs::path(dir) / "m.cubin",
+                   log = fs::path(dir) / "ptxas.log";
+    spit(in, ptx);
+    const std::string cmd = "'" + ptxas + "' -arch=sm_100a -O3 '" + in.string() + "' -o '" +
+                            out.string() + "' > '" + log.string() + "' 2>&1";
+    const int rc = std::system(cmd.c_str());
+    std::vector<uint8_t> cubin;
+    std::string err;
+    if (rc == 0 && fs::exists(out)) cubin = slurp(out);
+    else if (fs::exists(log)) {
+        const auto l = slurp(log);
+        err.assign(l.begin(), l.end());
+    }
+    std::error_code ec;
+    fs::remove_all(dir, ec);
+    require(!cubin.empty(), Errc::binary_format, "ptxas failed: " + err.substr(0, 2000));
+    return cubin;
+}
+
+void write_trace_cubins(const fs::path& archive, unsigned threads) {
+    ArchivePaths paths{archive};
+    const auto mt = slurp(paths.manifest());
+    Manifest m = parse_manifest(std::string(mt.begin(), mt.end()));
+    const Catalog cat = parse_catalog(slurp(paths.catalog()));
+    std::vector<const KernelBinaryRecord*> recs;
+    for (const auto& [hash, r] : cat.binaries) recs.push_back(&r);
+    std::vector<uint64_t> digests(recs.size());
+    parallel_for(recs.size(), threads ? threads : default_threads(), [&](size_t i) {
+        const KernelBinaryRecord& r = *recs[i];
+        const KernelImage img = parse_kernel_image(slurp(paths.binary(r.hash)));
+        const auto cubin = compile_ptx_to_cubin(
+            trace_module_ptx(img, static_cast<uint32_t>(i), r.needs_device_init));
+        spit(paths.cubin(r.hash), cubin);
+        digests[i] = crc64(cubin);
+    });
+    for (size_t i = 0; i < recs.size(); ++i)
+        m.file_digests["binaries/" + hex16(recs[i]->hash) + ".sm_100a.cubin"] = digests[i];
+    spit(paths.manifest(), serialize_manifest(m));
+}
+
+}  // namespace foundry

@@ -31,7 +31,7 @@ static_assert(FDT_TILE_CHUNKS % kThreads == 0, "tile must split evenly across th
 struct __align__(128) Smem {
     uint4 buf[2][FDT_TILE_CHUNKS];      // 2 x 16 KiB stages
     unsigned long long bar[2];          // mbarriers, one per stage
-    uint16_t slot[FDT_TILE_CHUNKS];     // chunk -> 1 + diff entry offset (0 = none)
+    uint8_t ometa[FDT_TILE_CHUNKS];     // relocation-meta overrides from diff entries (0x80 | lanes)
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -94,33 +94,67 @@ __device__ __forceinline__ uint64_t relocate_lane(uint64_t v, const FdyMateriali
     return (v - a.old_base < a.span) ? v + a.delta : v;
 }
 
-__device__ __forceinline__ uint4 merge_bytes(uint4 base, uint4 over, uint32_t mask) {
-    // expand a 16-bit byte mask into four 32-bit lane selectors
-    uint32_t w[4] = {base.x, base.y, base.z, base.w};
-    const uint32_t o[4] = {over.x, over.y, over.z, over.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint32_t m4 = (mask >> (4 * i)) & 0xFu;
-        // byte-select mask: 0x000000FF per set bit
-        const uint32_t sel = ((m4 & 1u) ? 0x000000FFu : 0u) | ((m4 & 2u) ? 0x0000FF00u : 0u) |
-                             ((m4 & 4u) ? 0x00FF0000u : 0u) | ((m4 & 8u) ? 0xFF000000u : 0u);
-        w[i] = (w[i] & ~sel) | (o[i] & sel);
-    }
-    return make_uint4(w[0], w[1], w[2], w[3]);
+// Expands 4 mask bits into a 32-bit byte-select word (bit i -> byte i = 0xFF).
+__device__ __forceinline__ uint32_t byte_select(uint32_t m4) {
+    return ((m4 * 0x00204081u) & 0x01010101u) * 0xFFu;
 }
 
+__device__ __forceinline__ uint4 merge_bytes(uint4 base, uint4 over, uint32_t mask) {
+    const uint32_t s0 = byte_select(mask & 0xFu), s1 = byte_select((mask >> 4) & 0xFu);
+    const uint32_t s2 = byte_select((mask >> 8) & 0xFu), s3 = byte_select((mask >> 12) & 0xFu);
+    return make_uint4((base.x & ~s0) | (over.x & s0), (base.y & ~s1) | (over.y & s1),
+                      (base.z & ~s2) | (over.z & s2), (base.w & ~s3) | (over.w & s3));
+}
+
+// 16-byte little-endian image of `value` placed so that byte j of the chunk
+// holds value byte (j - shift); bytes outside the value are zero.
+__device__ __forceinline__ uint4 place_value(uint64_t value, int shift) {
+    uint64_t lo, hi;
+    if (shift >= 0) {
+        const int s = 8 * shift;
+        lo = s < 64 ? value << s : 0ull;
+        hi = s == 0 ? 0ull : (s < 64 ? value >> (64 - s) : value << (s - 64));
+    } else {
+        lo = value >> (-8 * shift);
+        hi = 0ull;
+    }
+    return make_uint4(uint32_t(lo), uint32_t(lo >> 32), uint32_t(hi), uint32_t(hi >> 32));
+}
+
+__device__ __forceinline__ uint64_t rank_op_value(const fdt_rank_op& op, const FdyMaterializeArgs& a) {
+    switch (op.kind) {
+        case FDT_ROP_RANK: return a.rank;
+        case FDT_ROP_WORLD: return a.world;
+        case FDT_ROP_KERNEL: return op.aux;
+        default: return op.aux < a.n_values ? a.values[op.aux] : 0ull;
+    }
+}
+
+__device__ __forceinline__ void relocate_pair(uint32_t& lo, uint32_t& hi, bool flagged,
+                                              const FdyMaterializeArgs& a) {
+    const uint64_t x = (uint64_t(hi) << 32) | lo;
+    const uint64_t y = (flagged && x - a.old_base < a.span) ? x + a.delta : x;
+    lo = uint32_t(y);
+    hi = uint32_t(y >> 32);
+}
+
+// Phases per tile, each convergent across the CTA:
+//   B  diff-parallel: one thread per diff entry overlays its chunk in smem
+//   C  chunk-parallel relocation (skipped when delta == 0, a uniform branch)
+//   D  op-run-parallel rank patch: one thread per chunk's run of ops
 __global__ void __launch_bounds__(kThreads)
 fdy_materialize_kernel(const FdyMaterializeArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
     const int tid = threadIdx.x;
+    const bool relocating = a.delta != 0ull;
 
     if (tid == 0) {
         mbar_init(&s.bar[0], 1);
         mbar_init(&s.bar[1], 1);
         fence_mbar_init();
     }
-    for (int i = tid; i < FDT_TILE_CHUNKS; i += kThreads) s.slot[i] = 0;
+    for (int i = tid; i < FDT_TILE_CHUNKS; i += kThreads) s.ometa[i] = 0;
     __syncthreads();
 
     uint32_t t = blockIdx.x;
@@ -136,11 +170,6 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
     for (; t < a.n_tiles; t += gridDim.x) {
         const fdt_tile T = a.tiles[t];
         const uint32_t next = t + gridDim.x;
-
-        // K2 index: scatter this tile's diff entries into the chunk slot map
-        for (uint32_t e = T.diff_lo + tid; e < T.diff_hi; e += kThreads)
-            s.slot[a.didx[e] - T.chunk_base] = static_cast<uint16_t>(e - T.diff_lo + 1);
-
         // prefetch the next tile into the other stage once its store has drained
         if (tid == 0 && next < a.n_tiles) {
             bulk_wait_reads();
@@ -148,64 +177,55 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
             mbar_expect_tx(&s.bar[stage ^ 1], N.nchunks * 16u);
             bulk_load(s.buf[stage ^ 1], a.store + N.src_off, N.nchunks * 16u, &s.bar[stage ^ 1]);
         }
-        __syncthreads();
+        uint4* buf = s.buf[stage];
         mbar_wait(&s.bar[stage], (parity >> stage) & 1u);
         parity ^= 1u << stage;
 
-        const uint8_t* meta = a.cmeta + (T.src_off - a.timage_base) / 16;
-#pragma unroll
-        for (int k = 0; k < kChunksPerThread; ++k) {
-            const uint32_t c = tid + k * kThreads;
-            if (c >= T.nchunks) break;
-            uint4 v = s.buf[stage][c];
-            uint32_t m = meta[c];
-            const uint32_t sl = s.slot[c];
-            if (sl) {  // K2: overlay the member's bytes
-                const uint32_t e = T.diff_lo + sl - 1;
-                const uint32_t dm = __ldg(a.dmeta + e);
-                const uint4 d = __ldg(a.ddata + e);
-                v = merge_bytes(v, d, dm & FDT_DMETA_MASK);
-                if (dm & FDT_DMETA_RELOC_OVERRIDE) m = (dm >> FDT_DMETA_RELOC_SHIFT) & 3u;
-                s.slot[c] = 0;
-            }
-            if (m) {  // K1: relocate flagged lanes whose value is in the captured range
-                if (m & FDT_CMETA_LANE0) {
-                    uint64_t x = (uint64_t(v.y) << 32) | v.x;
-                    x = relocate_lane(x, a);
-                    v.x = uint32_t(x);
-                    v.y = uint32_t(x >> 32);
-                }
-                if (m & FDT_CMETA_LANE1) {
-                    uint64_t x = (uint64_t(v.w) << 32) | v.z;
-                    x = relocate_lane(x, a);
-                    v.z = uint32_t(x);
-                    v.w = uint32_t(x >> 32);
-                }
-            }
-            s.buf[stage][c] = v;
+        // B: K2 diff overlay
+        for (uint32_t e = T.diff_lo + tid; e < T.diff_hi; e += kThreads) {
+            const uint32_t c = __ldg(a.didx + e) - T.chunk_base;
+            const uint32_t dm = __ldg(a.dmeta + e);
+            buf[c] = merge_bytes(buf[c], __ldg(a.ddata + e), dm & FDT_DMETA_MASK);
+            if (relocating && (dm & FDT_DMETA_RELOC_OVERRIDE))
+                s.ometa[c] = static_cast<uint8_t>(0x80u | ((dm >> FDT_DMETA_RELOC_SHIFT) & 3u));
         }
         __syncthreads();
 
-        // K3: rank ops, in table order (ops on one chunk may overlap)
-        if (tid == 0) {
-            unsigned char* tile_bytes = reinterpret_cast<unsigned char*>(s.buf[stage]);
-            for (uint32_t i = T.rop_lo; i < T.rop_hi; ++i) {
-                const fdt_rank_op op = a.rops[i];
-                uint64_t value;
-                switch (op.kind) {
-                    case FDT_ROP_RANK: value = a.rank; break;
-                    case FDT_ROP_WORLD: value = a.world; break;
-                    case FDT_ROP_KERNEL: value = op.aux; break;
-                    default: value = op.aux < a.n_values ? a.values[op.aux] : 0ull; break;
+        // C: K1 relocation of flagged lanes whose value lies in the captured range
+        if (relocating) {
+            const uint8_t* meta = a.cmeta + (T.src_off - a.timage_base) / 16;
+            for (uint32_t c = tid; c < T.nchunks; c += kThreads) {
+                uint32_t m = __ldg(meta + c);
+                const uint32_t o = s.ometa[c];
+                if (o) {
+                    m = o & 3u;
+                    s.ometa[c] = 0;
                 }
-                unsigned char* chunk = tile_bytes + 16u * (op.chunk - T.chunk_base);
-                for (int j = 0; j < 16; ++j)
-                    if (op.mask & (1u << j)) chunk[j] = static_cast<unsigned char>(value >> (8 * (j - op.shift)));
+                if (m) {
+                    uint4 v = buf[c];
+                    relocate_pair(v.x, v.y, m & FDT_CMETA_LANE0, a);
+                    relocate_pair(v.z, v.w, m & FDT_CMETA_LANE1, a);
+                    buf[c] = v;
+                }
             }
+            __syncthreads();
+        }
+
+        // D: K3 rank ops; ops on one chunk are applied in table order by one thread
+        for (uint32_t i = T.rop_lo + tid; i < T.rop_hi; i += kThreads) {
+            const uint32_t ch = a.rops[i].chunk;
+            if (i != T.rop_lo && a.rops[i - 1].chunk == ch) continue;
+            uint4 v = buf[ch - T.chunk_base];
+            for (uint32_t j = i; j < T.rop_hi; ++j) {
+                const fdt_rank_op op = a.rops[j];
+                if (op.chunk != ch) break;
+                v = merge_bytes(v, place_value(rank_op_value(op, a), op.shift), op.mask);
+            }
+            buf[ch - T.chunk_base] = v;
         }
         fence_proxy_async_smem();
         __syncthreads();
-        if (tid == 0) bulk_store(a.out + T.dst_off, s.buf[stage], T.nchunks * 16u);
+        if (tid == 0) bulk_store(a.out + T.dst_off, buf, T.nchunks * 16u);
         stage ^= 1u;
     }
     if (tid == 0) bulk_wait_all();

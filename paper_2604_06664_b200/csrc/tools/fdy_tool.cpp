@@ -14,7 +14,9 @@
 
 #include "foundry/archive.hpp"
 #include "foundry/bytes.hpp"
+#include "foundry/save.hpp"
 #include "foundry/template_store.hpp"
+#include "foundry/workload.hpp"
 #include "foundry_b200.h"
 
 using namespace foundry;
@@ -111,6 +113,28 @@ static int cmd_decode(int argc, char** argv) {
     return 0;
 }
 
+// save <preset|spec> <out> [plain|b200] [traces-file]
+static int cmd_save(int argc, char** argv) {
+    if (argc < 4) return 64;
+    SaveOptions opt;
+    opt.b200_artifacts = !(argc > 4 && std::string(argv[4]) == "plain");
+    const auto t0 = std::chrono::steady_clock::now();
+    SaveResult r = save(resolve_workload(argv[2]), argv[3], opt);
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (argc > 5) spit(argv[5], traces_to_text(r.traces));
+    std::printf("{\"graphs\": %u, \"templates\": %u, \"save_ms\": %.3f}\n",
+                r.manifest.grouping.total_graphs, r.manifest.grouping.template_count, ms);
+    return 0;
+}
+
+// pack-cubins <archive>: trace cubins only (store via `pack`)
+static int cmd_pack_all(int argc, char** argv) {
+    (void)argc;
+    pack_archive(argv[2]);
+    return 0;
+}
+
 static int cmd_gpu_crc(int argc, char** argv) {
     fdy_device* dev = nullptr;
     if (fdy_device_open(0, &dev)) return die("fdy_device_open");
@@ -144,6 +168,8 @@ int main(int argc, char** argv) {
         if (cmd == "gpu-materialize") return cmd_gpu_materialize(argc, argv);
         if (cmd == "gpu-crc") return cmd_gpu_crc(argc, argv);
         if (cmd == "decode") return cmd_decode(argc, argv);
+        if (cmd == "save") return cmd_save(argc, argv);
+        if (cmd == "pack-all") return cmd_pack_all(argc, argv);
     } catch (const Error& e) {
         std::fprintf(stderr, "%s\n", e.what());
         return 2;
