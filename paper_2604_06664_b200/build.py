@@ -42,8 +42,13 @@ HOST_SRCS = [
     "host/workload.cpp",
     "host/save.cpp",
     "host/trace_module.cpp",
+    "host/driver_api.cpp",
+    "host/gpu_context.cpp",
+    "host/pipeline.cpp",
+    "host/tooling.cpp",
     "capi/capi_misc.cpp",
     "capi/capi_kernels.cpp",
+    "capi/capi_session.cpp",
 ]
 CU_SRCS = ["kernels/materialize.cu", "kernels/crc64.cu"]
 
@@ -118,6 +123,7 @@ def _write_ninja() -> Path:
     lib = PKG / "libfoundry_b200.so"
     lines.append(f"build {lib}: link {' '.join(objs)}")
     lines.append(f"build {PKG / 'fdy_tool'}: exe {CSRC / 'tools/fdy_tool.cpp'} | {lib}")
+    lines.append(f"build {PKG / ('_foundry' + ext)}: pymod {CSRC / 'bindings/module.cpp'} | {lib}")
     BUILD.mkdir(parents=True, exist_ok=True)
     path = BUILD / "build.ninja"
     text = "\n".join(lines) + "\n"

@@ -1,0 +1,185 @@
+// pybind11 module `_foundry`: the reference's Python surface (reference
+// proj/bindings/module.cpp:77-135, python/foundry/__init__.py:7-41) backed by
+// the B200 runtime. Names, argument names/defaults and return shapes match the
+// reference; B200-only knobs are extra keyword arguments with defaults that
+// keep reference behaviour.
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+#include <pybind11/stl/filesystem.h>
+
+#include <chrono>
+
+#include "foundry/pipeline.hpp"
+#include "foundry/save.hpp"
+#include "foundry/template_store.hpp"
+#include "foundry/tooling.hpp"
+#include "foundry/workload.hpp"
+
+namespace py = pybind11;
+using namespace foundry;
+
+namespace {
+
+struct SaveOutcome {
+    std::string archive_dir;
+    std::map<uint32_t, std::string> traces;
+    std::map<std::string, uint64_t> counters;
+    uint32_t total_graphs = 0;
+    uint32_t template_count = 0;
+    double update_served_fraction = 0.0;
+};
+
+struct ServingHandle {
+    explicit ServingHandle(ServingContext&& s) : sc(std::move(s)) {}
+    std::string replay(uint32_t batch) { return sc.replay(batch).to_text(); }
+    std::vector<uint32_t> batches() const { return sc.batches(); }
+    std::map<std::string, uint64_t> counters() const {
+        const auto c = sc.counters();
+        return {c.begin(), c.end()};
+    }
+    uint32_t template_count() const { return sc.template_count(); }
+    py::dict timings() const {
+        const LoadTimings& t = sc.timings();
+        py::dict d;
+        d["total_ms"] = t.total_ms;
+        d["manifest_ms"] = t.manifest_ms;
+        d["stage_ms"] = t.stage_ms;
+        d["integrity_ms"] = t.integrity_ms;
+        d["restore_ms"] = t.restore_ms;
+        d["region_ms"] = t.region_ms;
+        d["materialize_ms"] = t.materialize_ms;
+        d["download_ms"] = t.download_ms;
+        d["build_ms"] = t.build_ms;
+        d["instantiate_ms"] = t.instantiate_ms;
+        d["foreground_ms"] = t.foreground_ms;
+        d["crc_kernel_ms"] = t.crc_kernel_ms;
+        d["materialize_kernel_ms"] = t.materialize_kernel_ms;
+        d["h2d_bytes"] = t.h2d_bytes;
+        d["d2h_bytes"] = t.d2h_bytes;
+        d["member_bytes"] = t.member_bytes;
+        d["store_bytes"] = t.store_bytes;
+        d["graphs"] = t.graphs;
+        d["nodes"] = t.nodes;
+        d["templates"] = t.templates;
+        d["relocation_delta"] = t.relocation_delta;
+        return d;
+    }
+    py::bytes prepared_record(uint32_t batch) const {
+        const auto rec = encode_graph_record(sc.prepared_params(batch));
+        return py::bytes(reinterpret_cast<const char*>(rec.data()), rec.size());
+    }
+    uint64_t serve(uint32_t batch) { return sc.serve(batch); }
+    uint64_t region_base() { return sc.context().region_base(); }
+    ServingContext sc;
+};
+
+SaveOutcome do_save(const WorkloadSpec& spec, const std::string& out, bool emit_json_graphs,
+                    bool b200_artifacts) {
+    SaveOptions o;
+    o.b200_artifacts = b200_artifacts;
+    SaveResult r;
+    {
+        py::gil_scoped_release nogil;
+        r = save(spec, out, o);
+        if (emit_json_graphs) write_json_graphs(out);
+    }
+    SaveOutcome s;
+    s.archive_dir = r.archive_dir.string();
+    for (const auto& [b, t] : r.traces) s.traces.emplace(b, t.to_text());
+    s.counters = save_counters(spec);
+    s.total_graphs = r.manifest.grouping.total_graphs;
+    s.template_count = r.manifest.grouping.template_count;
+    s.update_served_fraction = r.manifest.grouping.update_served_fraction();
+    return s;
+}
+
+ServingHandle do_load(const std::string& archive, uint32_t rank, uint32_t world, bool preallocate,
+                      int device, bool relocate, unsigned prepare_lanes, bool skip_binary_restore,
+                      bool skip_device_init, int64_t base_shift_granules, bool extra_prewindow_alloc,
+                      bool verify_replay) {
+    LoadOptions o;
+    o.rank = rank;
+    o.world = world;
+    o.preallocate = preallocate;
+    o.device = device;
+    o.relocate = relocate;
+    o.prepare_lanes = prepare_lanes;
+    o.verify_replay = verify_replay;
+    o.faults.skip_binary_restore = skip_binary_restore;
+    o.faults.skip_device_init = skip_device_init;
+    o.faults.base_shift_granules = base_shift_granules;
+    o.faults.extra_prewindow_alloc = extra_prewindow_alloc;
+    py::gil_scoped_release nogil;
+    return ServingHandle(load(archive, o));
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_foundry, m) {
+    m.doc() = "B200-native LOAD of template-based CUDA graph archives (Foundry drop-in)";
+    m.attr("__version__") = "0.1.0";
+
+    py::register_exception<Error>(m, "FoundryError");
+
+    py::class_<WorkloadSpec>(m, "WorkloadSpec")
+        .def(py::init<>())
+        .def_readwrite("seed", &WorkloadSpec::seed)
+        .def_readwrite("batch_max", &WorkloadSpec::batch_max)
+        .def_readwrite("layers", &WorkloadSpec::layers)
+        .def_readwrite("kernels_per_layer", &WorkloadSpec::kernels_per_layer)
+        .def_readwrite("thresholds", &WorkloadSpec::thresholds)
+        .def_readwrite("collectives_per_layer", &WorkloadSpec::collectives_per_layer)
+        .def_readwrite("hidden_offset_density", &WorkloadSpec::hidden_offset_density)
+        .def("__repr__", [](const WorkloadSpec& s) {
+            return "<WorkloadSpec B=" + std::to_string(s.batch_max) + " L=" + std::to_string(s.layers) + ">";
+        });
+
+    py::class_<SaveOutcome>(m, "SaveOutcome")
+        .def_readonly("archive_dir", &SaveOutcome::archive_dir)
+        .def_readonly("traces", &SaveOutcome::traces)
+        .def_readonly("counters", &SaveOutcome::counters)
+        .def_readonly("total_graphs", &SaveOutcome::total_graphs)
+        .def_readonly("template_count", &SaveOutcome::template_count)
+        .def_readonly("update_served_fraction", &SaveOutcome::update_served_fraction);
+
+    py::class_<ServingHandle>(m, "ServingHandle")
+        .def("replay", &ServingHandle::replay, py::arg("batch"), py::call_guard<py::gil_scoped_release>())
+        .def("batches", &ServingHandle::batches)
+        .def("counters", &ServingHandle::counters)
+        .def("template_count", &ServingHandle::template_count)
+        .def("timings", &ServingHandle::timings)
+        .def("prepared_record", &ServingHandle::prepared_record, py::arg("batch"))
+        .def("serve", &ServingHandle::serve, py::arg("batch"), py::call_guard<py::gil_scoped_release>())
+        .def("region_base", &ServingHandle::region_base);
+
+    m.def("preset_names", &preset_names);
+    m.def("preset", &preset, py::arg("name"));
+    m.def("workload_from_text", [](const std::string& t) { return WorkloadSpec::parse_text(t); },
+          py::arg("text"));
+    m.def("spec_text", [](const WorkloadSpec& s) { return s.canonical_text(); }, py::arg("spec"));
+    m.def("save", &do_save, py::arg("spec"), py::arg("out"), py::arg("emit_json_graphs") = false,
+          py::arg("b200_artifacts") = true);
+    m.def("load", &do_load, py::arg("archive"), py::arg("rank") = 0, py::arg("world") = 1,
+          py::arg("preallocate") = true, py::arg("device") = 0, py::arg("relocate") = false,
+          py::arg("prepare_lanes") = 4, py::arg("skip_binary_restore") = false,
+          py::arg("skip_device_init") = false, py::arg("base_shift_granules") = 0,
+          py::arg("extra_prewindow_alloc") = false, py::arg("verify_replay") = true);
+    m.def("pack", [](const std::string& archive) {
+        py::gil_scoped_release nogil;
+        pack_archive(archive);
+    }, py::arg("archive"));
+    m.def("inspect_text", [](const std::string& a) { return inspect_text(a); }, py::arg("archive"));
+    m.def("inspect_graph_json", [](const std::string& a, uint32_t b) { return inspect_graph_json(a, b); },
+          py::arg("archive"), py::arg("batch"));
+    m.def("diff_archives",
+          [](const std::string& a, const std::string& b) {
+              const auto r = diff_archives(a, b);
+              return py::make_tuple(r.first, r.second);
+          },
+          py::arg("a"), py::arg("b"));
+    m.def("bench", [](const WorkloadSpec& spec, const std::string& mode) {
+        py::gil_scoped_release nogil;
+        return bench(spec, mode);
+    }, py::arg("spec"), py::arg("mode") = "load");
+    m.def("cuda_device_count", &cuda_device_count);
+}

@@ -1,0 +1,936 @@
+// LOAD orchestration on B200 (phase map and reference anchors: pipeline.hpp).
+#include "foundry/pipeline.hpp"
+
+#include <fcntl.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <exception>
+#include <thread>
+
+#include <cuda_runtime.h>
+
+#include "foundry/bytes.hpp"
+#include "foundry/parallel.hpp"
+#include "foundry/template_store.hpp"
+#include "foundry/trace_module.hpp"
+#include "foundry/workload.hpp"
+
+namespace foundry {
+
+namespace fs = std::filesystem;
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+constexpr uint32_t kNoMember = 0xFFFFFFFFu;
+constexpr size_t kStageAlign = 256;
+constexpr size_t kReadChunk = 8ull << 20;
+
+struct FileSeg {
+    std::string rel;
+    uint64_t offset = 0;  // in staging
+    uint64_t length = 0;
+};
+
+void read_range(const fs::path& p, uint8_t* dst, uint64_t off, uint64_t len) {
+    const int fd = ::open(p.c_str(), O_RDONLY | O_CLOEXEC);
+    require(fd >= 0, Errc::archive_corruption, "cannot open " + p.string());
+    uint64_t done = 0;
+    while (done < len) {
+        const ssize_t n = ::pread(fd, dst + done, len - done, static_cast<off_t>(off + done));
+        if (n <= 0) {
+            ::close(fd);
+            raise(Errc::archive_corruption, "short read on " + p.string());
+        }
+        done += static_cast<uint64_t>(n);
+    }
+    ::close(fd);
+}
+
+uint64_t rd64(const uint8_t* p) {
+    uint64_t v;
+    std::memcpy(&v, p, 8);
+    return v;
+}
+
+}  // namespace
+
+struct ServingContext::Impl {
+    std::unique_ptr<Device> owned_dev;
+    Device* dev = nullptr;
+    fs::path root;
+    std::unique_ptr<GpuContext> ctx;
+    LoadOptions opts;
+    LoadTimings t;
+    Manifest manifest;
+    Catalog catalog;
+
+    PinnedBuffer staging;
+    DeviceBuffer d_staging;
+    std::map<std::string, FileSeg> files;
+
+    std::vector<uint8_t> inline_store;  // reference archives without templates.fdt
+    DeviceBuffer d_inline_store;
+    std::span<const uint8_t> store_host;
+    std::unique_ptr<StoreView> view;
+    DeviceStore dstore;
+    DeviceBuffer d_members;
+    PinnedBuffer h_members;
+    std::vector<int32_t> kernel_of;  // store kernel index -> GpuContext kernel (or -1)
+
+    struct Group {
+        CUgraph graph = nullptr;
+        CUgraphExec exec = nullptr;
+        std::vector<CUgraphNode> nodes;
+        uint32_t applied = kNoMember;  // member index currently in the exec
+    };
+    std::vector<Group> groups;
+    std::vector<uint32_t> labels;
+    uint64_t lane_acquisitions = 0;
+    CUcontext cu_ctx = nullptr;
+
+    ~Impl() {
+        try {
+            const DriverApi& api = driver();
+            if (dev) dev->make_current();
+            for (auto& g : groups) {
+                if (g.exec) api.cuGraphExecDestroy(g.exec);
+                if (g.graph) api.cuGraphDestroy(g.graph);
+            }
+        } catch (...) {
+        }
+        ctx.reset();  // libraries, then VA (destroy order: execs -> graphs -> libraries -> VA)
+    }
+
+    std::span<const uint8_t> file_host(const std::string& rel) const {
+        auto it = files.find(rel);
+        require(it != files.end(), Errc::archive_corruption, "archive has no " + rel);
+        return {staging.data() + it->second.offset, it->second.length};
+    }
+
+    const uint8_t* member_image(uint32_t m) const { return h_members.data() + view->member(m).out_off; }
+
+    uint32_t member_for(uint32_t batch) const {
+        const int64_t m = view->member_of(batch);
+        require(m >= 0, Errc::invalid_argument,
+                "batch " + std::to_string(batch) + " is not a member of any group (routing bug)");
+        return static_cast<uint32_t>(m);
+    }
+
+    const GpuContext::Kernel& resolve(uint32_t store_kernel, uint32_t node) const {
+        const int32_t k = store_kernel < kernel_of.size() ? kernel_of[store_kernel] : -1;
+        if (k < 0) {
+            const KernelRef ref = view->kernel_ref(store_kernel);
+            raise(Errc::unresolved_kernel, "node " + std::to_string(node) + " references " + ref.describe());
+        }
+        return *ctx->kernel_by_entry_id(static_cast<uint32_t>(k));
+    }
+
+    void stage_files(const fs::path& root);
+    void restore_binaries();
+    void build_group(uint32_t g);
+    uint64_t build_graph_for(uint32_t g, uint32_t m, CUgraph& graph, std::vector<CUgraphNode>& nodes);
+    void kernel_params(const fdt_node& d, const uint8_t* blob, const GpuContext::Kernel& K,
+                       CUDA_KERNEL_NODE_PARAMS& p, void** extra, size_t* size) const;
+    CUDA_MEMCPY3D memcpy_params(const uint8_t* blob) const;
+    CUDA_MEMSET_NODE_PARAMS memset_params(const uint8_t* blob) const;
+    uint64_t safe(uint64_t addr) const;
+    uint64_t apply_member(uint32_t g, uint32_t m);
+    LaunchTrace replay(uint32_t batch);
+};
+
+// ---------------------------------------------------------------- staging
+
+void ServingContext::Impl::stage_files(const fs::path& root) {
+    uint64_t total = 0;
+    for (const auto& [rel, digest] : manifest.file_digests) {
+        (void)digest;
+        const fs::path p = root / rel;
+        std::error_code ec;
+        const uint64_t n = fs::file_size(p, ec);
+        require(!ec, Errc::archive_corruption, "cannot open " + p.string());
+        files[rel] = {rel, total, n};
+        total += (n + kStageAlign - 1) / kStageAlign * kStageAlign;
+    }
+    staging = PinnedBuffer(*dev, std::max<uint64_t>(total, 16));
+    struct Piece {
+        const FileSeg* f;
+        uint64_t off, len;
+    };
+    std::vector<Piece> pieces;
+    for (const auto& [rel, f] : files)
+        for (uint64_t o = 0; o < f.length || (o == 0 && f.length == 0); o += kReadChunk) {
+            pieces.push_back({&f, o, std::min<uint64_t>(kReadChunk, f.length - o)});
+            if (f.length == 0) break;
+        }
+    parallel_for(pieces.size(), std::max(1u, opts.prepare_lanes), [&](size_t i) {
+        const Piece& pc = pieces[i];
+        if (pc.len) read_range(root / pc.f->rel, staging.data() + pc.f->offset + pc.off, pc.off, pc.len);
+    });
+    d_staging = DeviceBuffer(*dev, std::max<uint64_t>(total, 16));
+    cuda_check(cudaMemcpyAsync(d_staging.data(), staging.data(), total, cudaMemcpyHostToDevice,
+                               dev->stream()),
+               "cudaMemcpyAsync(archive H2D)");
+    t.h2d_bytes += total;
+}
+
+// ---------------------------------------------------------------- restore
+
+void ServingContext::Impl::restore_binaries() {
+    uint32_t ordinal = 0;
+    for (const auto& [hash, rec] : catalog.binaries) {
+        const uint32_t ord = ordinal++;
+        if (ctx->has_library(hash)) continue;  // a second restore is a no-op
+        const std::string rel = "binaries/" + hex16(hash) + ".bin";
+        std::vector<uint8_t> fetched;
+        std::span<const uint8_t> payload;
+        uint64_t digest = 0;
+        if (files.count(rel)) {
+            payload = file_host(rel);
+            digest = manifest.file_digests.at(rel);  // verified on the GPU by stage 2
+        } else {
+            fetched = slurp(ArchivePaths{root}.binary(hash));
+            payload = fetched;
+            digest = crc64(fetched);
+        }
+        require(digest == hash, Errc::archive_corruption,
+                "binary " + hex16(hash) + " content does not match its hash");
+        const KernelImage image = parse_kernel_image(payload);
+        require(!image.relocatable, Errc::binary_format,
+                "relocatable segment must be pre-linked before loading");
+        const std::string crel = "binaries/" + hex16(hash) + ".sm_100a.cubin";
+        std::vector<uint8_t> built;
+        std::span<const uint8_t> cubin;
+        if (files.count(crel)) {
+            cubin = file_host(crel);
+        } else {  // reference-written archive: compile the trace module now
+            built = compile_ptx_to_cubin(trace_module_ptx(image, ord, rec.needs_device_init));
+            cubin = built;
+        }
+        const uint32_t lib = ctx->load_library(hash, image, cubin, ord, rec.needs_device_init);
+        if (rec.needs_device_init && !opts.faults.skip_device_init) ctx->run_device_init(lib);
+    }
+}
+
+// ---------------------------------------------------------------- graph params
+
+uint64_t ServingContext::Impl::safe(uint64_t addr) const {
+    // memop nodes are constructed with live addresses only; an address outside
+    // the mapping is reported at replay (unmapped-address) before any launch
+    return ctx->physically_backed(addr) ? addr : ctx->backing_base();
+}
+
+void ServingContext::Impl::kernel_params(const fdt_node& d, const uint8_t* blob,
+                                         const GpuContext::Kernel& K, CUDA_KERNEL_NODE_PARAMS& p,
+                                         void** extra, size_t* size) const {
+    std::memset(&p, 0, sizeof p);
+    p.func = K.fn;
+    p.gridDimX = d.grid[0];
+    p.gridDimY = d.grid[1];
+    p.gridDimZ = d.grid[2];
+    p.blockDimX = d.block[0];
+    p.blockDimY = d.block[1];
+    p.blockDimZ = d.block[2];
+    p.sharedMemBytes = d.shmem;
+    *size = K.arg_buffer_size;  // the device ABI of the entry; extra bytes stay host-side
+    extra[0] = CU_LAUNCH_PARAM_BUFFER_POINTER;
+    extra[1] = const_cast<uint8_t*>(blob);
+    extra[2] = CU_LAUNCH_PARAM_BUFFER_SIZE;
+    extra[3] = size;
+    extra[4] = CU_LAUNCH_PARAM_END;
+    p.extra = extra;
+}
+
+CUDA_MEMCPY3D ServingContext::Impl::memcpy_params(const uint8_t* blob) const {
+    CUDA_MEMCPY3D c;
+    std::memset(&c, 0, sizeof c);
+    c.srcMemoryType = CU_MEMORYTYPE_DEVICE;
+    c.srcDevice = safe(rd64(blob));
+    c.dstMemoryType = CU_MEMORYTYPE_DEVICE;
+    c.dstDevice = safe(rd64(blob + 8));
+    c.WidthInBytes = rd64(blob + 16);
+    c.Height = 1;
+    c.Depth = 1;
+    require(c.WidthInBytes > 0, Errc::invalid_argument, "memcpy node with zero length");
+    return c;
+}
+
+CUDA_MEMSET_NODE_PARAMS ServingContext::Impl::memset_params(const uint8_t* blob) const {
+    CUDA_MEMSET_NODE_PARAMS m;
+    std::memset(&m, 0, sizeof m);
+    m.dst = safe(rd64(blob));
+    const uint64_t value = rd64(blob + 8), len = rd64(blob + 16);
+    require(len > 0, Errc::invalid_argument, "memset node with zero length");
+    if (value <= 0xFF) {
+        m.elementSize = 1;
+        m.width = len;
+    } else {
+        require(value <= 0xFFFFFFFFull && len % 4 == 0, Errc::invalid_argument,
+                "memset value " + std::to_string(value) + " is not representable by a device memset");
+        m.elementSize = 4;
+        m.width = len / 4;
+    }
+    m.value = static_cast<unsigned int>(value);
+    m.height = 1;
+    m.pitch = 0;
+    return m;
+}
+
+uint64_t ServingContext::Impl::build_graph_for(uint32_t gi, uint32_t m, CUgraph& graph,
+                                               std::vector<CUgraphNode>& nodes) {
+    const DriverApi& api = driver();
+    dev->make_current();
+    const fdt_group& G = view->group(gi);
+    const uint8_t* img = member_image(m);
+    const uint8_t* pool = img + 48ull * G.n_nodes;
+    uint64_t calls = 0;
+
+    // validate every kernel node before touching the driver (sim_driver.cpp:295-305)
+    for (uint32_t n = 0; n < G.n_nodes; ++n) {
+        fdt_node d;
+        std::memcpy(&d, img + 48ull * n, sizeof d);
+        if (d.type != 0) continue;
+        const auto& K = resolve(d.kernel, n);
+        require(d.blob_len >= K.arg_buffer_size, Errc::invalid_argument,
+                "build_graph: argument buffer smaller than '" + K.name + "' declares (" +
+                    std::to_string(d.blob_len) + " < " + std::to_string(K.arg_buffer_size) + ")");
+        const FuncAttrs fa = view->kernel_func_attrs(d.kernel);
+        const int want = std::max<int>(fa.max_dynamic_shared_size_bytes, static_cast<int>(d.shmem));
+        if (want > 48 * 1024)
+            cu_check(api.cuFuncSetAttribute(K.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, want),
+                     "cuFuncSetAttribute(max dynamic smem)");
+        if (fa.preferred_shared_memory_carveout >= 0)
+            cu_check(api.cuFuncSetAttribute(K.fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT,
+                                            fa.preferred_shared_memory_carveout),
+                     "cuFuncSetAttribute(carveout)");
+    }
+
+    cu_check(api.cuGraphCreate(&graph, 0), "cuGraphCreate");
+    nodes.assign(G.n_nodes, nullptr);
+    for (uint32_t n = 0; n < G.n_nodes; ++n) {
+        fdt_node d;
+        std::memcpy(&d, img + 48ull * n, sizeof d);
+        const uint8_t* blob = pool + d.blob_off;
+        CUgraphNode& node = nodes[n];
+        switch (d.type) {
+            case 0: {
+                const auto& K = resolve(d.kernel, n);
+                CUDA_KERNEL_NODE_PARAMS p;
+                void* extra[5];
+                size_t size;
+                kernel_params(d, blob, K, p, extra, &size);
+                cu_check(api.cuGraphAddKernelNode(&node, graph, nullptr, 0, &p), "cuGraphAddKernelNode");
+                const fdt_node_attrs& a = view->node_attrs(gi, n);
+                const bool non_default = a.cluster[0] != 1 || a.cluster[1] != 1 || a.cluster[2] != 1 ||
+                                         a.sched_policy || a.sync_default || a.sync_remote || !a.attr_query;
+                if (non_default) {
+                    ++calls;
+                    const uint32_t csize = a.cluster[0] * a.cluster[1] * a.cluster[2];
+                    const bool cluster_ok = csize > 1 && csize <= 8 && d.grid[0] % a.cluster[0] == 0 &&
+                                            d.grid[1] % a.cluster[1] == 0 && d.grid[2] % a.cluster[2] == 0;
+                    if (cluster_ok) {
+                        CUkernelNodeAttrValue v{};
+                        v.clusterDim.x = a.cluster[0];
+                        v.clusterDim.y = a.cluster[1];
+                        v.clusterDim.z = a.cluster[2];
+                        cu_check(api.cuGraphKernelNodeSetAttribute(node, CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION, &v),
+                                 "cuGraphKernelNodeSetAttribute(cluster)");
+                    }
+                    if (a.sched_policy > 0 && a.sched_policy <= 2) {
+                        CUkernelNodeAttrValue v{};
+                        v.clusterSchedulingPolicyPreference =
+                            static_cast<CUclusterSchedulingPolicy>(a.sched_policy);
+                        cu_check(api.cuGraphKernelNodeSetAttribute(
+                                     node, CU_LAUNCH_ATTRIBUTE_CLUSTER_SCHEDULING_POLICY_PREFERENCE, &v),
+                                 "cuGraphKernelNodeSetAttribute(policy)");
+                    }
+                }
+                break;
+            }
+            case 1: {
+                const CUDA_MEMCPY3D c = memcpy_params(blob);
+                cu_check(api.cuGraphAddMemcpyNode(&node, graph, nullptr, 0, &c, cu_ctx), "cuGraphAddMemcpyNode");
+                break;
+            }
+            case 2: {
+                const CUDA_MEMSET_NODE_PARAMS s = memset_params(blob);
+                cu_check(api.cuGraphAddMemsetNode(&node, graph, nullptr, 0, &s, cu_ctx), "cuGraphAddMemsetNode");
+                break;
+            }
+            default:
+                cu_check(api.cuGraphAddEmptyNode(&node, graph, nullptr, 0), "cuGraphAddEmptyNode");
+        }
+        ++calls;
+    }
+    const auto e = view->edges(gi);
+    if (G.n_edges) {
+        std::vector<CUgraphNode> from(G.n_edges), to(G.n_edges);
+        for (uint32_t i = 0; i < G.n_edges; ++i) {
+            from[i] = nodes[e[2 * i]];
+            to[i] = nodes[e[2 * i + 1]];
+        }
+        cu_check(api.cuGraphAddDependencies(graph, from.data(), to.data(), G.n_edges),
+                 "cuGraphAddDependencies");
+        calls += G.n_edges;
+    }
+    return calls;
+}
+
+void ServingContext::Impl::build_group(uint32_t gi) {
+    const DriverApi& api = driver();
+    const fdt_group& G = view->group(gi);
+    Group& grp = groups[gi];
+    const uint32_t m = G.first_member;  // representative: the smallest label
+    const auto t0 = Clock::now();
+    build_graph_for(gi, m, grp.graph, grp.nodes);
+    const auto e = view->edges(gi);
+    (void)e;
+    // counters mirror the reference builder lane (sim_driver.cpp:307-313)
+    ctx->c_add_node.fetch_add(G.n_nodes);
+    ctx->c_add_edge.fetch_add(G.n_edges);
+    for (uint32_t n = 0; n < G.n_nodes; ++n) {
+        const fdt_node_attrs& a = view->node_attrs(gi, n);
+        fdt_node d;
+        std::memcpy(&d, member_image(m) + 48ull * n, sizeof d);
+        if (d.type == 0 && (a.cluster[0] != 1 || a.cluster[1] != 1 || a.cluster[2] != 1 ||
+                            a.sched_policy || a.sync_default || a.sync_remote || !a.attr_query))
+            ctx->c_set_attr.fetch_add(1);
+    }
+    ++lane_acquisitions;
+    const double build = ms_since(t0);
+    const auto t1 = Clock::now();
+    cu_check(api.cuGraphInstantiate(&grp.exec, grp.graph, 0), "cuGraphInstantiate");
+    ++lane_acquisitions;
+    ctx->c_instantiate.fetch_add(1);
+    t.build_ms += build;
+    t.instantiate_ms += ms_since(t1);
+    grp.applied = m;
+}
+
+// ---------------------------------------------------------------- serve
+
+uint64_t ServingContext::Impl::apply_member(uint32_t gi, uint32_t m) {
+    Group& grp = groups[gi];
+    if (grp.applied == m) return 0;
+    const DriverApi& api = driver();
+    dev->make_current();
+    const fdt_group& G = view->group(gi);
+    const uint8_t* img = member_image(m);
+    const uint8_t* pool = img + 48ull * G.n_nodes;
+    const uint8_t* cur = grp.applied == kNoMember ? nullptr : member_image(grp.applied);
+    uint64_t touched = 0;
+    for (uint32_t n = 0; n < G.n_nodes; ++n) {
+        fdt_node d;
+        std::memcpy(&d, img + 48ull * n, sizeof d);
+        const uint8_t* blob = pool + d.blob_off;
+        if (cur) {
+            const bool same = std::memcmp(cur + 48ull * n, img + 48ull * n, 48) == 0 &&
+                              std::memcmp(cur + 48ull * G.n_nodes + d.blob_off, blob, d.blob_len) == 0;
+            if (same) continue;
+        }
+        ++touched;
+        switch (d.type) {
+            case 0: {
+                const auto& K = resolve(d.kernel, n);
+                require(d.blob_len >= K.arg_buffer_size, Errc::invalid_argument,
+                        "exec_update: argument buffer smaller than '" + K.name + "' declares");
+                CUDA_KERNEL_NODE_PARAMS p;
+                void* extra[5];
+                size_t size;
+                kernel_params(d, blob, K, p, extra, &size);
+                cu_check(api.cuGraphExecKernelNodeSetParams(grp.exec, grp.nodes[n], &p),
+                         "cuGraphExecKernelNodeSetParams");
+                break;
+            }
+            case 1: {
+                const CUDA_MEMCPY3D c = memcpy_params(blob);
+                cu_check(api.cuGraphExecMemcpyNodeSetParams(grp.exec, grp.nodes[n], &c, cu_ctx),
+                         "cuGraphExecMemcpyNodeSetParams");
+                break;
+            }
+            case 2: {
+                const CUDA_MEMSET_NODE_PARAMS s = memset_params(blob);
+                cu_check(api.cuGraphExecMemsetNodeSetParams(grp.exec, grp.nodes[n], &s, cu_ctx),
+                         "cuGraphExecMemsetNodeSetParams");
+                break;
+            }
+            default: break;
+        }
+    }
+    grp.applied = m;
+    ++lane_acquisitions;
+    ctx->c_update.fetch_add(1);
+    ctx->c_update_touched.fetch_add(touched);
+    return touched;
+}
+
+// ---------------------------------------------------------------- replay
+
+LaunchTrace ServingContext::Impl::replay(uint32_t batch) {
+    const uint32_t m = member_for(batch);
+    const uint32_t gi = view->member(m).group;
+    apply_member(gi, m);
+    const fdt_group& G = view->group(gi);
+    const uint8_t* img = member_image(m);
+    const uint8_t* pool = img + 48ull * G.n_nodes;
+
+    // host pre-validation in node order (reference replay, sim_driver.cpp:423-470)
+    LaunchTrace trace;
+    trace.records.reserve(G.n_nodes);
+    struct Expect {
+        uint32_t node;
+        const GpuContext::Kernel* k;
+        const fdt_node* d;
+        const uint8_t* blob;
+    };
+    std::vector<fdt_node> descs(G.n_nodes);
+    std::vector<Expect> expect;
+    auto check_mapped = [&](uint32_t node, uint32_t off, uint64_t a) {
+        require(ctx->address_mapped(a), Errc::unmapped_address,
+                "node " + std::to_string(node) + " offset " + std::to_string(off) +
+                    " references unmapped address 0x" + hex16(a));
+    };
+    for (uint32_t n = 0; n < G.n_nodes; ++n) {
+        fdt_node& d = descs[n];
+        std::memcpy(&d, img + 48ull * n, sizeof d);
+        const uint8_t* blob = pool + d.blob_off;
+        TraceRecord r;
+        r.node_id = n;
+        r.type = static_cast<NodeType>(d.type);
+        if (d.type == 0) {
+            const auto& K = resolve(d.kernel, n);
+            require(!ctx->library_requires_init(K.library) || ctx->library_device_inited(K.library),
+                    Errc::device_state_uninitialized,
+                    "node " + std::to_string(n) + " kernel '" + K.name + "' used before device-side init");
+            require(d.blob_len >= K.arg_buffer_size, Errc::invalid_argument,
+                    "replay: argument buffer smaller than '" + K.name + "' declares (" +
+                        std::to_string(d.blob_len) + " < " + std::to_string(K.arg_buffer_size) + ")");
+            for (uint32_t off : K.hidden_offsets) {
+                const uint64_t a = rd64(blob + off);
+                check_mapped(n, off, a);
+                r.addresses.push_back(a);
+            }
+            r.kernel_name = K.name;
+            r.grid = {d.grid[0], d.grid[1], d.grid[2]};
+            r.block = {d.block[0], d.block[1], d.block[2]};
+            r.shared_mem_bytes = d.shmem;
+            r.arg_digest = crc64(blob, d.blob_len);
+            expect.push_back({n, &K, &descs[n], blob});
+        } else if (d.type == 1 || d.type == 2) {
+            const uint64_t a0 = rd64(blob), a1 = rd64(blob + 8);
+            check_mapped(n, 0, a0);
+            if (d.type == 1) {
+                check_mapped(n, 8, a1);
+                r.addresses = {a0, a1};
+            } else {
+                r.addresses = {a0};
+            }
+            r.arg_digest = crc64(blob, 24);
+        }
+        trace.records.push_back(std::move(r));
+    }
+
+    // launch the instantiated graph and verify the device-side trace
+    const DriverApi& api = driver();
+    dev->make_current();
+    ctx->reset_trace();
+    cu_check(api.cuGraphLaunch(groups[gi].exec, dev->stream()), "cuGraphLaunch");
+    ctx->c_replay.fetch_add(1);
+    if (!opts.verify_replay) {
+        dev->sync();
+        return trace;
+    }
+    const std::vector<uint8_t> recs = ctx->read_trace();
+    // index the expected launches by (entry id, parameter bytes)
+    std::multimap<std::pair<uint32_t, uint64_t>, const Expect*> want;
+    for (const auto& e : expect)
+        want.emplace(std::make_pair(e.k->entry_id, crc64(e.blob, e.k->arg_buffer_size)), &e);
+    size_t at = 0, seen = 0;
+    while (at + FDY_TRACE_HEADER_BYTES <= recs.size()) {
+        fdy_trace_header h;
+        std::memcpy(&h, recs.data() + at, sizeof h);
+        require(h.magic == FDY_TRACE_MAGIC, Errc::cuda_error, "replay verification: torn trace record");
+        const uint8_t* bytes = recs.data() + at + FDY_TRACE_HEADER_BYTES;
+        auto range = want.equal_range({h.entry_id, crc64(bytes, h.n_bytes)});
+        const Expect* hit = nullptr;
+        for (auto it = range.first; it != range.second; ++it) {
+            const Expect* e = it->second;
+            if (e->k->arg_buffer_size == h.n_bytes && std::memcmp(e->blob, bytes, h.n_bytes) == 0 &&
+                e->d->grid[0] == h.grid[0] && e->d->grid[1] == h.grid[1] && e->d->grid[2] == h.grid[2] &&
+                e->d->block[0] == h.block[0] && e->d->block[1] == h.block[1] &&
+                e->d->block[2] == h.block[2] && e->d->shmem == h.dyn_smem) {
+                hit = e;
+                want.erase(it);
+                break;
+            }
+        }
+        require(hit != nullptr, Errc::cuda_error,
+                "replay verification: device launch of entry " + std::to_string(h.entry_id) +
+                    " matches no expected node of batch " + std::to_string(batch));
+        require(!(h.flags & FDY_TRACE_FLAG_UNINIT), Errc::device_state_uninitialized,
+                "node " + std::to_string(hit->node) + " kernel '" + hit->k->name +
+                    "' used before device-side init");
+        require(!(h.flags & FDY_TRACE_FLAG_UNMAPPED), Errc::unmapped_address,
+                "node " + std::to_string(hit->node) + " dereferenced an unmapped address on the device");
+        at += FDY_TRACE_HEADER_BYTES + ((h.n_bytes + 15u) & ~15u);
+        ++seen;
+    }
+    require(seen == expect.size() && want.empty(), Errc::cuda_error,
+            "replay verification: " + std::to_string(seen) + " device launches recorded, " +
+                std::to_string(expect.size()) + " kernel nodes expected");
+    return trace;
+}
+
+// ---------------------------------------------------------------- load
+
+namespace {
+
+void verify_init_records(const std::vector<AllocationRecord>& actual, uint64_t actual_base,
+                         const MemoryEventLog& log) {
+    std::vector<AllocationRecord> expected;
+    for (const auto& r : log.records)
+        if (r.window == AllocWindow::pre_capture) expected.push_back(r);
+    require(actual.size() == expected.size(), Errc::layout_divergence,
+            "LOAD issued " + std::to_string(actual.size()) + " pre-window allocations, SAVE recorded " +
+                std::to_string(expected.size()));
+    for (size_t i = 0; i < expected.size(); ++i) {
+        const bool same = actual[i].sequence == expected[i].sequence &&
+                          actual[i].size == expected[i].size && actual[i].length == expected[i].length &&
+                          actual[i].address - actual_base == expected[i].address - log.config.base;
+        require(same, Errc::layout_divergence,
+                "allocation sequence diverged at record " + std::to_string(i) + " (requested " +
+                    std::to_string(actual[i].size) + " bytes at 0x" + hex16(actual[i].address) +
+                    ", SAVE recorded " + std::to_string(expected[i].size) + " at 0x" +
+                    hex16(expected[i].address) + ")");
+    }
+}
+
+}  // namespace
+
+ServingContext load(Device& device, const fs::path& archive, const LoadOptions& opts) {
+    const auto t_all = Clock::now();
+    require(opts.world >= 1 && opts.rank < opts.world, Errc::invalid_argument,
+            "rank " + std::to_string(opts.rank) + " is outside world size " + std::to_string(opts.world));
+    auto impl = std::make_unique<ServingContext::Impl>();
+    auto& I = *impl;
+    I.dev = &device;
+    I.opts = opts;
+    I.root = archive;
+    ArchivePaths paths{archive};
+    require(fs::exists(paths.manifest()), Errc::archive_corruption, "no manifest under " + archive.string());
+
+    auto t0 = Clock::now();
+    {
+        const auto mb = slurp(paths.manifest());
+        I.manifest = parse_manifest(std::string(mb.begin(), mb.end()));
+    }
+    I.t.manifest_ms = ms_since(t0);
+    device.make_current();
+    cu_check(driver().cuCtxGetCurrent(&I.cu_ctx), "cuCtxGetCurrent");
+    I.ctx = std::make_unique<GpuContext>(device);
+
+    // 1. stage every listed file into HBM, 2. verify digests on the GPU
+    t0 = Clock::now();
+    try {
+        I.stage_files(archive);
+    } catch (const Error&) {
+        rethrow_in_step("archive integrity");
+    }
+    I.t.stage_ms = ms_since(t0);
+    t0 = Clock::now();
+    {
+        std::vector<Segment> segs;
+        std::vector<const std::string*> names;
+        for (const auto& [rel, f] : I.files) {
+            segs.push_back({f.offset, f.length});
+            names.push_back(&f.rel);
+        }
+        const auto digests = crc64_device(device, I.d_staging.data(), segs, &I.t.crc_kernel_ms);
+        try {
+            for (size_t i = 0; i < names.size(); ++i)
+                require(digests[i] == I.manifest.file_digests.at(*names[i]), Errc::archive_corruption,
+                        "integrity check failed for " + *names[i]);
+        } catch (const Error&) {
+            rethrow_in_step("archive integrity");
+        }
+    }
+    I.t.integrity_ms = ms_since(t0);
+
+    const WorkloadSpec spec = WorkloadSpec::parse_text(I.manifest.workload_text);
+    require(spec.digest() == I.manifest.workload_digest, Errc::archive_corruption,
+            "embedded workload text does not match its recorded digest");
+    I.catalog = parse_catalog(I.file_host("catalog.bin"));
+    (void)parse_patch_table(I.file_host("patch.bin"));  // format check; the store carries the ops
+    const MemoryEventLog log = parse_event_log(I.file_host("memlayout.bin"));
+
+    // template store: packed offline (templates.fdt) or, for a reference-written
+    // archive, packed now from graphs.bin + patch.bin
+    if (I.files.count("templates.fdt")) {
+        const FileSeg& f = I.files.at("templates.fdt");
+        I.store_host = I.file_host("templates.fdt");
+        I.view = std::make_unique<StoreView>(I.store_host);
+        I.dstore = adopt_store(device, I.d_staging.data() + f.offset, f.length, I.view->header());
+    } else {
+        try {
+            I.inline_store = pack_template_store(I.file_host("graphs.bin"), I.file_host("patch.bin"),
+                                                 I.manifest, opts.prepare_lanes);
+        } catch (const Error&) {
+            rethrow_in_step("template construction");
+        }
+        I.store_host = I.inline_store;
+        I.view = std::make_unique<StoreView>(I.store_host);
+        I.dstore = upload_store(device, I.inline_store.data(), I.inline_store.size());
+        I.t.h2d_bytes += I.inline_store.size();
+    }
+    const fdt_header& H = I.view->header();
+    require(H.source_graphs_crc == I.manifest.file_digests.at("graphs.bin") &&
+                H.source_patch_crc == I.manifest.file_digests.at("patch.bin"),
+            Errc::archive_corruption, "template store was packed from a different graphs.bin/patch.bin");
+    if (H.n_rank_ops > 0)
+        require(I.manifest.comm_real_hash != 0, Errc::unresolved_kernel,
+                "archive carries comm patches but no real comm binary");
+
+    // 3. restore binaries (cuLibraryLoadData)
+    t0 = Clock::now();
+    if (!opts.faults.skip_binary_restore) {
+        try {
+            I.restore_binaries();
+        } catch (const Error&) {
+            rethrow_in_step("binary restore");
+        }
+    }
+    I.kernel_of.assign(H.n_kernels, -1);
+    for (uint32_t k = 0; k < H.n_kernels; ++k) {
+        const auto* K = I.ctx->find_kernel(I.view->kernel(k).binary_hash, I.view->kernel_name(k));
+        if (K) I.kernel_of[k] = static_cast<int32_t>(K->entry_id);
+    }
+    I.t.restore_ms = ms_since(t0);
+
+    // 4. region
+    t0 = Clock::now();
+    RegionConfig cfg = I.manifest.allocator;
+    cfg.base += static_cast<uint64_t>(opts.faults.base_shift_granules) * cfg.granularity;
+    I.ctx->reserve_region(cfg, I.manifest.final_offset + cfg.granularity, opts.relocate);
+    if (opts.preallocate) I.ctx->preallocate(I.manifest.final_offset);
+    if (opts.faults.extra_prewindow_alloc) I.ctx->allocate(1);
+    I.t.region_ms = ms_since(t0);
+
+    // 5. materialize every member for this rank: one fused kernel, then D2H
+    t0 = Clock::now();
+    MaterializeRequest req;
+    req.rank = opts.rank;
+    req.world = opts.world;
+    const uint64_t new_base = I.ctx->region_base();
+    req.new_base = (opts.relocate && new_base != I.manifest.allocator.base) ? new_base : 0;
+    I.t.relocation_delta = req.new_base ? req.new_base - I.manifest.allocator.base : 0;
+    I.d_members = DeviceBuffer(device, std::max<uint64_t>(H.members_image_bytes, 16));
+    I.h_members = PinnedBuffer(device, std::max<uint64_t>(H.members_image_bytes, 16));
+    MaterializeTiming mt;
+    launch_materialize(device, I.dstore, req, I.d_members.data(), &mt);
+    I.t.materialize_kernel_ms = mt.kernel_ms;
+    I.t.materialize_ms = ms_since(t0);
+    t0 = Clock::now();
+    cuda_check(cudaMemcpyAsync(I.h_members.data(), I.d_members.data(), H.members_image_bytes,
+                               cudaMemcpyDeviceToHost, device.stream()),
+               "cudaMemcpyAsync(member images D2H)");
+    cuda_check(cudaStreamSynchronize(device.stream()), "cudaStreamSynchronize");
+    I.t.download_ms = ms_since(t0);
+    I.t.d2h_bytes += H.members_image_bytes;
+    I.t.member_bytes = H.members_image_bytes;
+    I.t.store_bytes = I.dstore.bytes;
+
+    // 6. template construction (builder thread) || foreground init + window replay
+    I.groups.resize(H.n_groups);
+    std::exception_ptr builder_error, foreground_error;
+    std::thread builder([&] {
+        try {
+            for (uint32_t g = 0; g < H.n_groups; ++g) I.build_group(g);
+        } catch (...) {
+            builder_error = std::current_exception();
+        }
+    });
+    t0 = Clock::now();
+    try {
+        try {
+            std::vector<uint64_t> slot;
+            for (const InitStep& st : build_init_plan(spec)) {
+                if (st.kind == InitStep::Kind::alloc) {
+                    if (st.slot >= slot.size()) slot.resize(st.slot + 1, 0);
+                    slot[st.slot] = I.ctx->allocate(st.size);
+                } else {
+                    require(st.slot < slot.size(), Errc::invalid_argument, "init plan releases an unknown slot");
+                    I.ctx->free(slot[st.slot]);
+                }
+            }
+            verify_init_records(I.ctx->records(), cfg.base, log);
+        } catch (const Error&) {
+            rethrow_in_step("foreground init");
+        }
+        try {
+            I.ctx->replay_capture_window(log);
+        } catch (const Error&) {
+            rethrow_in_step("capture-window replay");
+        }
+    } catch (...) {
+        foreground_error = std::current_exception();
+    }
+    I.t.foreground_ms = ms_since(t0);
+    builder.join();
+    if (foreground_error) std::rethrow_exception(foreground_error);
+    if (builder_error) {
+        try {
+            std::rethrow_exception(builder_error);
+        } catch (const Error&) {
+            rethrow_in_step("template construction");
+        }
+    }
+
+    // trace arena: one record (64 B + parameter bytes) per kernel node
+    uint64_t arena = 1 << 16;
+    for (uint32_t g = 0; g < H.n_groups; ++g)
+        arena = std::max<uint64_t>(arena, I.view->group(g).image_bytes + 64ull * I.view->group(g).n_nodes);
+    I.ctx->ensure_trace_arena(arena);
+    I.ctx->sync_trace_state();
+
+    for (uint32_t m = 0; m < H.n_members; ++m) I.labels.push_back(I.view->member(m).label);
+    std::sort(I.labels.begin(), I.labels.end());
+    I.t.graphs = H.n_members;
+    I.t.nodes = H.total_nodes;
+    I.t.templates = H.n_groups;
+    I.t.total_ms = ms_since(t_all);
+    return ServingContext(std::move(impl));
+}
+
+ServingContext load(const fs::path& archive, const LoadOptions& opts) {
+    auto dev = std::make_unique<Device>(opts.device);
+    ServingContext sc = load(*dev, archive, opts);
+    sc.impl_->owned_dev = std::move(dev);
+    return sc;
+}
+
+// ---------------------------------------------------------------- ServingContext
+
+ServingContext::ServingContext(std::unique_ptr<Impl> impl) : impl_(std::move(impl)) {}
+ServingContext::ServingContext(ServingContext&&) noexcept = default;
+ServingContext& ServingContext::operator=(ServingContext&&) noexcept = default;
+ServingContext::~ServingContext() {
+    if (impl_) {
+        auto owned = std::move(impl_->owned_dev);
+        impl_.reset();  // graphs/libraries/VA go before the device they live on
+    }
+}
+
+LaunchTrace ServingContext::replay(uint32_t batch) { return impl_->replay(batch); }
+std::vector<uint32_t> ServingContext::batches() const { return impl_->labels; }
+const Manifest& ServingContext::manifest() const { return impl_->manifest; }
+std::vector<AllocationRecord> ServingContext::allocation_records() const { return impl_->ctx->records(); }
+GpuContext& ServingContext::context() { return *impl_->ctx; }
+const LoadTimings& ServingContext::timings() const { return impl_->t; }
+uint32_t ServingContext::template_count() const { return impl_->manifest.grouping.template_count; }
+
+CounterSnapshot ServingContext::counters() const {
+    CounterSnapshot s = impl_->ctx->counters();
+    s["driver.lane_acquisitions"] = impl_->lane_acquisitions;
+    s["driver.lane_contention_units"] = 0;
+    s["catalog.prelink_calls"] = 0;
+    s["catalog.linked_segments"] = 0;
+    return s;
+}
+
+CapturedGraph ServingContext::prepared_params(uint32_t batch) const {
+    const uint32_t m = impl_->member_for(batch);
+    const auto& G = impl_->view->group(impl_->view->member(m).group);
+    return impl_->view->image_to_graph(m, {impl_->member_image(m), G.image_bytes});
+}
+
+uint64_t ServingContext::serve(uint32_t batch) {
+    const uint32_t m = impl_->member_for(batch);
+    return impl_->apply_member(impl_->view->member(m).group, m);
+}
+
+uint64_t ServingContext::naive_rebuild_all() {
+    Impl& I = *impl_;
+    const DriverApi& api = driver();
+    uint64_t calls = 0;
+    for (uint32_t m = 0; m < I.view->n_members(); ++m) {
+        const uint32_t gi = I.view->member(m).group;
+        CUgraph g = nullptr;
+        CUgraphExec x = nullptr;
+        std::vector<CUgraphNode> nodes;
+        calls += I.build_graph_for(gi, m, g, nodes);
+        cu_check(api.cuGraphInstantiate(&x, g, 0), "cuGraphInstantiate");
+        ++calls;
+        cu_check(api.cuGraphLaunch(x, I.dev->stream()), "cuGraphLaunch");
+        I.dev->sync();
+        api.cuGraphExecDestroy(x);
+        api.cuGraphDestroy(g);
+    }
+    return calls;
+}
+
+void ServingContext::exec_update(uint32_t batch_in_group, const CapturedGraph& donor) {
+    Impl& I = *impl_;
+    const uint32_t m = I.member_for(batch_in_group);
+    const uint32_t gi = I.view->member(m).group;
+    const fdt_group& G = I.view->group(gi);
+    donor.validate();
+    for (const auto& n : donor.nodes) {
+        if (n.type != NodeType::Kernel) continue;
+        const auto& k = n.kernel_params();
+        const auto* K = I.ctx->find_kernel(k.kernel.binary_hash, k.kernel.name);
+        require(K != nullptr, Errc::unresolved_kernel,
+                "node " + std::to_string(n.id) + " references " + k.kernel.describe());
+        require(k.arg_buffer.size() >= K->arg_buffer_size, Errc::invalid_argument,
+                "exec_update: argument buffer smaller than '" + K->name + "' declares");
+    }
+    const TopologyKey want{Digest128{G.key_hi, G.key_lo}};
+    const TopologyKey got = topology_key(donor);
+    require(got == want, Errc::topology_mismatch,
+            "donor topology " + got.hex() + " does not match exec topology " + want.hex());
+    // donor parameters are applied node by node; the exec no longer holds a member
+    const DriverApi& api = driver();
+    I.dev->make_current();
+    Impl::Group& grp = I.groups[gi];
+    for (uint32_t n = 0; n < G.n_nodes; ++n) {
+        const GraphNode& node = donor.nodes[n];
+        if (node.type == NodeType::Kernel) {
+            const auto& k = node.kernel_params();
+            const auto* K = I.ctx->find_kernel(k.kernel.binary_hash, k.kernel.name);
+            fdt_node d{};
+            d.grid[0] = k.grid.x, d.grid[1] = k.grid.y, d.grid[2] = k.grid.z;
+            d.block[0] = k.block.x, d.block[1] = k.block.y, d.block[2] = k.block.z;
+            d.shmem = k.shared_mem_bytes;
+            CUDA_KERNEL_NODE_PARAMS p;
+            void* extra[5];
+            size_t size;
+            I.kernel_params(d, k.arg_buffer.data(), *K, p, extra, &size);
+            cu_check(api.cuGraphExecKernelNodeSetParams(grp.exec, grp.nodes[n], &p),
+                     "cuGraphExecKernelNodeSetParams");
+        } else if (node.type == NodeType::Memcpy) {
+            const auto& c = std::get<MemcpyParams>(node.params);
+            const uint64_t raw[3] = {c.src, c.dst, c.length};
+            const CUDA_MEMCPY3D cp = I.memcpy_params(reinterpret_cast<const uint8_t*>(raw));
+            cu_check(api.cuGraphExecMemcpyNodeSetParams(grp.exec, grp.nodes[n], &cp, I.cu_ctx),
+                     "cuGraphExecMemcpyNodeSetParams");
+        } else if (node.type == NodeType::Memset) {
+            const auto& s = std::get<MemsetParams>(node.params);
+            const uint64_t raw[3] = {s.dst, s.value, s.length};
+            const CUDA_MEMSET_NODE_PARAMS sp = I.memset_params(reinterpret_cast<const uint8_t*>(raw));
+            cu_check(api.cuGraphExecMemsetNodeSetParams(grp.exec, grp.nodes[n], &sp, I.cu_ctx),
+                     "cuGraphExecMemsetNodeSetParams");
+        }
+    }
+    grp.applied = kNoMember;
+    ++I.lane_acquisitions;
+    I.ctx->c_update.fetch_add(1);
+    I.ctx->c_update_touched.fetch_add(G.n_nodes);
+}
+
+}  // namespace foundry

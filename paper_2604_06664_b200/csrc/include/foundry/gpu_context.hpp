@@ -81,7 +81,11 @@ public:
     void replay_capture_window(const MemoryEventLog& log);
     uint64_t offset() const { return offset_; }
     std::vector<AllocationRecord> records() const { return records_; }
-    bool address_mapped(uint64_t addr) const;
+    bool address_mapped(uint64_t addr) const;  // logical (reference mapped_ ranges)
+    bool physically_backed(uint64_t addr) const {
+        return addr >= phys_at_ && addr < phys_at_ + phys_bytes_;
+    }
+    uint64_t backing_base() const { return phys_at_; }
     void zero_region();  // cuMemsetD8 over the backed range (deterministic replay outputs)
 
     // ------------------------------------------------------------ trace
