@@ -70,6 +70,19 @@ struct ServingHandle {
     }
     uint64_t serve(uint32_t batch) { return sc.serve(batch); }
     uint64_t region_base() { return sc.context().region_base(); }
+    py::tuple fresh_capture_check(uint32_t batch) {
+        std::string rep;
+        bool ok;
+        {
+            py::gil_scoped_release nogil;
+            ok = sc.fresh_capture_check(batch, &rep);
+        }
+        return py::make_tuple(ok, rep);
+    }
+    uint64_t naive_rebuild_all() {
+        py::gil_scoped_release nogil;
+        return sc.naive_rebuild_all();
+    }
     ServingContext sc;
 };
 
@@ -150,7 +163,9 @@ PYBIND11_MODULE(_foundry, m) {
         .def("timings", &ServingHandle::timings)
         .def("prepared_record", &ServingHandle::prepared_record, py::arg("batch"))
         .def("serve", &ServingHandle::serve, py::arg("batch"), py::call_guard<py::gil_scoped_release>())
-        .def("region_base", &ServingHandle::region_base);
+        .def("region_base", &ServingHandle::region_base)
+        .def("fresh_capture_check", &ServingHandle::fresh_capture_check, py::arg("batch"))
+        .def("naive_rebuild_all", &ServingHandle::naive_rebuild_all);
 
     m.def("preset_names", &preset_names);
     m.def("preset", &preset, py::arg("name"));

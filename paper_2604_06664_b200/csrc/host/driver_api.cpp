@@ -68,6 +68,9 @@ void load_all() {
     FDY_RESOLVE(cuGraphExecMemcpyNodeSetParams);
     FDY_RESOLVE(cuGraphExecMemsetNodeSetParams);
     FDY_RESOLVE(cuGraphLaunch);
+    FDY_RESOLVE(cuLaunchKernel);
+    FDY_RESOLVE(cuMemsetD8Async);
+    FDY_RESOLVE(cuMemsetD32Async);
 #undef FDY_RESOLVE
 }
 

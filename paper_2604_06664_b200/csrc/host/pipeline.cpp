@@ -855,6 +855,97 @@ uint64_t ServingContext::serve(uint32_t batch) {
     return impl_->apply_member(impl_->view->member(m).group, m);
 }
 
+namespace {
+// canonical form of a trace arena: records sorted by (entry id, bytes)
+std::vector<std::string> canonical_records(const std::vector<uint8_t>& recs) {
+    std::vector<std::string> out;
+    size_t at = 0;
+    while (at + FDY_TRACE_HEADER_BYTES <= recs.size()) {
+        fdy_trace_header h;
+        std::memcpy(&h, recs.data() + at, sizeof h);
+        const size_t len = FDY_TRACE_HEADER_BYTES + ((h.n_bytes + 15u) & ~15u);
+        out.emplace_back(reinterpret_cast<const char*>(recs.data() + at), std::min(len, recs.size() - at));
+        at += len;
+    }
+    std::sort(out.begin(), out.end());
+    return out;
+}
+}  // namespace
+
+bool ServingContext::fresh_capture_check(uint32_t batch, std::string* report) {
+    Impl& I = *impl_;
+    const DriverApi& api = driver();
+    const uint32_t m = I.member_for(batch);
+    const uint32_t gi = I.view->member(m).group;
+    GpuContext& ctx = *I.ctx;
+    Device& dev = *I.dev;
+    cudaStream_t st = dev.stream();
+    auto region_crc = [&]() {
+        const Segment seg{0, ctx.backed_bytes()};
+        return crc64_device(dev, reinterpret_cast<const unsigned char*>(ctx.backing_base()),
+                            std::span<const Segment>(&seg, 1))[0];
+    };
+    // (a) the materialized exec
+    I.replay(batch);  // validates addresses, applies member b
+    ctx.zero_region();
+    ctx.reset_trace();
+    cu_check(api.cuGraphLaunch(I.groups[gi].exec, st), "cuGraphLaunch");
+    dev.sync();
+    const auto trace_a = canonical_records(ctx.read_trace());
+    const uint64_t crc_a = region_crc();
+
+    // (b) a fresh stream capture of the same launches, in capture (node) order
+    const fdt_group& G = I.view->group(gi);
+    const uint8_t* img = I.member_image(m);
+    const uint8_t* pool = img + 48ull * G.n_nodes;
+    ctx.zero_region();
+    ctx.reset_trace();
+    dev.sync();
+    cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    for (uint32_t n = 0; n < G.n_nodes; ++n) {
+        fdt_node d;
+        std::memcpy(&d, img + 48ull * n, sizeof d);
+        const uint8_t* blob = pool + d.blob_off;
+        if (d.type == 0) {
+            const auto& K = I.resolve(d.kernel, n);
+            size_t size = K.arg_buffer_size;
+            void* extra[5] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<uint8_t*>(blob),
+                              CU_LAUNCH_PARAM_BUFFER_SIZE, &size, CU_LAUNCH_PARAM_END};
+            cu_check(api.cuLaunchKernel(K.fn, d.grid[0], d.grid[1], d.grid[2], d.block[0], d.block[1],
+                                        d.block[2], d.shmem, st, nullptr, extra),
+                     "cuLaunchKernel(capture)");
+        } else if (d.type == 1) {
+            cuda_check(cudaMemcpyAsync(reinterpret_cast<void*>(rd64(blob + 8)),
+                                       reinterpret_cast<const void*>(rd64(blob)), rd64(blob + 16),
+                                       cudaMemcpyDeviceToDevice, st),
+                       "cudaMemcpyAsync(capture)");
+        } else if (d.type == 2) {
+            const uint64_t value = rd64(blob + 8), len = rd64(blob + 16);
+            if (value <= 0xFF)
+                cu_check(api.cuMemsetD8Async(rd64(blob), static_cast<unsigned char>(value), len, st),
+                         "cuMemsetD8Async(capture)");
+            else
+                cu_check(api.cuMemsetD32Async(rd64(blob), static_cast<unsigned int>(value), len / 4, st),
+                         "cuMemsetD32Async(capture)");
+        }
+    }
+    cudaGraph_t g = nullptr;
+    cuda_check(cudaStreamEndCapture(st, &g), "cudaStreamEndCapture");
+    cudaGraphExec_t x = nullptr;
+    cuda_check(cudaGraphInstantiate(&x, g, 0), "cudaGraphInstantiate(capture)");
+    cuda_check(cudaGraphLaunch(x, st), "cudaGraphLaunch(capture)");
+    dev.sync();
+    const auto trace_b = canonical_records(ctx.read_trace());
+    const uint64_t crc_b = region_crc();
+    cudaGraphExecDestroy(x);
+    cudaGraphDestroy(g);
+    const bool ok = trace_a == trace_b && crc_a == crc_b && !trace_a.empty();
+    if (report)
+        *report = "records " + std::to_string(trace_a.size()) + "/" + std::to_string(trace_b.size()) +
+                  " region crc " + hex16(crc_a) + "/" + hex16(crc_b) + (ok ? " match" : " MISMATCH");
+    return ok;
+}
+
 uint64_t ServingContext::naive_rebuild_all() {
     Impl& I = *impl_;
     const DriverApi& api = driver();

@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <sstream>
+#include <cstring>
 #include <unistd.h>
 
 #include "foundry/bytes.hpp"
@@ -14,18 +15,16 @@ namespace foundry {
 
 namespace fs = std::filesystem;
 
-std::string trace_module_ptx(const KernelImage& image, uint32_t ordinal, bool needs_init) {
+namespace {
+
+// .entry wrappers only; the device body lives in a separately compiled object
+// that nvlink links in once (a whole-program compile would clone the body
+// into every entry and make large modules slow to build and load).
+std::string entries_ptx(const KernelImage& image, uint32_t ordinal, bool needs_init) {
     std::ostringstream o;
-    o << ".version 8.8\n.target sm_100a\n.address_size 64\n\n";
-    // device body: strip its own module header
-    std::istringstream body(trace_body_ptx());
-    std::string line;
-    while (std::getline(body, line)) {
-        if (line.rfind(".version", 0) == 0 || line.rfind(".target", 0) == 0 ||
-            line.rfind(".address_size", 0) == 0)
-            continue;
-        o << line << "\n";
-    }
+    o << ".version 8.8\n.target sm_100a\n.address_size 64\n\n"
+      << ".extern .func fdy_trace_body(.param .b64 a0, .param .b32 a1, .param .b64 a2, "
+         ".param .b32 a3, .param .b32 a4, .param .b32 a5);\n";
     for (size_t i = 0; i < image.entrypoints.size(); ++i) {
         const KernelEntry& e = image.entrypoints[i];
         require(e.arg_buffer_size > 0 && e.arg_buffer_size <= 32764, Errc::binary_format,
@@ -56,27 +55,88 @@ std::string trace_module_ptx(const KernelImage& image, uint32_t ordinal, bool ne
     return o.str();
 }
 
-std::vector<uint8_t> compile_ptx_to_cubin(const std::string& ptx) {
+std::string cuda_tool(const char* name) {
     const char* home = std::getenv("CUDA_HOME");
-    const std::string ptxas = std::string(home ? home : "/usr/local/cuda") + "/bin/ptxas";
-    char dir[] = "/tmp/fdy_ptx_XXXXXX";
-    require(mkdtemp(dir) != nullptr, Errc::invalid_argument, "cannot create a temp dir for ptxas");
-    const fs::path in = fs::path(dir) / "m.ptx", out = fs::path(dir) / "m.cubin",
-                   log = fs::path(dir) / "ptxas.log";
-    spit(in, ptx);
-    const std::string cmd = "'" + ptxas + "' -arch=sm_100a -O3 '" + in.string() + "' -o '" +
-                            out.string() + "' > '" + log.string() + "' 2>&1";
-    const int rc = std::system(cmd.c_str());
-    std::vector<uint8_t> cubin;
-    std::string err;
-    if (rc == 0 && fs::exists(out)) cubin = slurp(out);
-    else if (fs::exists(log)) {
-        const auto l = slurp(log);
-        err.assign(l.begin(), l.end());
+    return std::string(home ? home : "/usr/local/cuda") + "/bin/" + name;
+}
+
+struct TempDir {
+    fs::path path;
+    TempDir() {
+        char dir[] = "/tmp/fdy_ptx_XXXXXX";
+        require(mkdtemp(dir) != nullptr, Errc::invalid_argument, "cannot create a temp dir for ptxas");
+        path = dir;
     }
-    std::error_code ec;
-    fs::remove_all(dir, ec);
-    require(!cubin.empty(), Errc::binary_format, "ptxas failed: " + err.substr(0, 2000));
+    ~TempDir() {
+        std::error_code ec;
+        fs::remove_all(path, ec);
+    }
+};
+
+void run_tool(const std::string& cmd, const fs::path& log) {
+    if (std::system((cmd + " > '" + log.string() + "' 2>&1").c_str()) != 0) {
+        std::string err;
+        if (fs::exists(log)) {
+            const auto l = slurp(log);
+            err.assign(l.begin(), l.end());
+        }
+        raise(Errc::binary_format, "device code generation failed: " + err.substr(0, 2000));
+    }
+}
+
+// Relocatable object of the shared device body, built once per process.
+const fs::path& body_object() {
+    static std::once_flag once;
+    static fs::path obj;
+    static TempDir dir;
+    std::call_once(once, [] {
+        const fs::path ptx = dir.path / "body.ptx";
+        obj = dir.path / "body.o";
+        spit(ptx, std::string_view(trace_body_ptx()));
+        run_tool("'" + cuda_tool("ptxas") + "' -arch=sm_100a -O3 -c '" + ptx.string() + "' -o '" +
+                     obj.string() + "'",
+                 dir.path / "body.log");
+    });
+    return obj;
+}
+
+fs::path cache_dir() {
+    if (const char* env = std::getenv("FOUNDRY_CUBIN_CACHE")) return env;
+    return {};
+}
+
+}  // namespace
+
+std::string trace_module_ptx(const KernelImage& image, uint32_t ordinal, bool needs_init) {
+    return entries_ptx(image, ordinal, needs_init);
+}
+
+std::vector<uint8_t> compile_ptx_to_cubin(const std::string& entries) {
+    // content-addressed cache (optional): identical binaries compile once
+    const uint64_t key = crc64(entries.data(), entries.size()) ^
+                         (crc64(trace_body_ptx(), std::strlen(trace_body_ptx())) * 0x9E3779B97F4A7C15ull);
+    const fs::path cache = cache_dir();
+    if (!cache.empty()) {
+        const fs::path hit = cache / (hex16(key) + ".cubin");
+        if (fs::exists(hit)) return slurp(hit);
+    }
+    TempDir dir;
+    const fs::path in = dir.path / "m.ptx", obj = dir.path / "m.o", out = dir.path / "m.cubin";
+    spit(in, entries);
+    run_tool("'" + cuda_tool("ptxas") + "' -arch=sm_100a -O3 -c '" + in.string() + "' -o '" +
+                 obj.string() + "'",
+             dir.path / "ptxas.log");
+    run_tool("'" + cuda_tool("nvlink") + "' -arch=sm_100a '" + body_object().string() + "' '" +
+                 obj.string() + "' -o '" + out.string() + "'",
+             dir.path / "nvlink.log");
+    auto cubin = slurp(out);
+    if (!cache.empty()) {
+        std::error_code ec;
+        fs::create_directories(cache, ec);
+        const fs::path tmp = cache / (hex16(key) + ".tmp" + std::to_string(::getpid()));
+        spit(tmp, cubin);
+        fs::rename(tmp, cache / (hex16(key) + ".cubin"), ec);
+    }
     return cubin;
 }
 

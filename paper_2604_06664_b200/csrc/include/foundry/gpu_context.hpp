@@ -86,6 +86,7 @@ public:
         return addr >= phys_at_ && addr < phys_at_ + phys_bytes_;
     }
     uint64_t backing_base() const { return phys_at_; }
+    uint64_t backed_bytes() const { return phys_bytes_; }
     void zero_region();  // cuMemsetD8 over the backed range (deterministic replay outputs)
 
     // ------------------------------------------------------------ trace

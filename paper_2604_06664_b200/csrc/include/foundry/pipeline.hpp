@@ -100,6 +100,13 @@ public:
     // templates. Returns the construction calls issued (nodes+edges+attrs+inst).
     uint64_t naive_rebuild_all();
 
+    // "Replaying the materialized graphs must reproduce the outputs of freshly
+    // captured graphs": runs batch b once through the materialized exec and
+    // once through a graph stream-captured from the same launches, each from a
+    // zeroed region, and compares the device trace records and a GPU CRC-64 of
+    // the whole region. Returns true when both agree (details in *report).
+    bool fresh_capture_check(uint32_t batch, std::string* report = nullptr);
+
     struct Impl;
 
 private:

@@ -1,0 +1,149 @@
+"""Pure-Python readers for the archive formats (TEST INFRASTRUCTURE).
+
+Independent of the product's C++ codecs: FNDG graph containers (reference
+graph_model.cpp:96-303), FNDB kernel images (kernel_image.cpp:14-90) and the
+reference LaunchTrace text (sim_driver.cpp:21-38, replay :402-479), used to
+derive expected replay traces from oracle-materialized records.
+"""
+from __future__ import annotations
+
+import os
+import struct
+from dataclasses import dataclass, field
+
+TYPES = {0: "KernelNode", 1: "MemcpyNode", 2: "MemsetNode", 3: "EmptyNode"}
+
+
+@dataclass
+class Node:
+    id: int
+    type: int
+    attrs: bytes = b""
+    grid: tuple = (1, 1, 1)
+    block: tuple = (1, 1, 1)
+    shmem: int = 0
+    hash: int = 0
+    name: str = ""
+    fattrs: bytes = b""
+    args: bytes = b""
+    mem: tuple = (0, 0, 0)
+
+
+@dataclass
+class Graph:
+    label: int
+    nodes: list = field(default_factory=list)
+    edges: list = field(default_factory=list)
+
+
+def locators(buf: bytes):
+    assert buf[:4] == b"FNDG"
+    (ver,) = struct.unpack_from("<H", buf, 4)
+    (count,) = struct.unpack_from("<I", buf, 6)
+    out = []
+    for i in range(count):
+        out.append(struct.unpack_from("<IQQQ", buf, 10 + 28 * i))
+    return out
+
+
+def decode_record(rec: bytes) -> Graph:
+    label, nn, ne = struct.unpack_from("<III", rec, 0)
+    at = 12
+    g = Graph(label)
+    for i in range(nn):
+        t = rec[at]
+        at += 1
+        n = Node(i, t)
+        if t == 0:
+            n.attrs = rec[at:at + 25]
+            at += 25
+            dims = struct.unpack_from("<7I", rec, at)
+            at += 28
+            n.grid, n.block, n.shmem = dims[0:3], dims[3:6], dims[6]
+            (n.hash,) = struct.unpack_from("<Q", rec, at)
+            at += 8
+            (ln,) = struct.unpack_from("<I", rec, at)
+            at += 4
+            n.name = rec[at:at + ln].decode()
+            at += ln
+            n.fattrs = rec[at:at + 24]
+            at += 24
+            (al,) = struct.unpack_from("<I", rec, at)
+            at += 4
+            n.args = rec[at:at + al]
+            at += al
+        elif t in (1, 2):
+            n.mem = struct.unpack_from("<3Q", rec, at)
+            at += 24
+        g.nodes.append(n)
+    for i in range(ne):
+        g.edges.append(struct.unpack_from("<II", rec, at))
+        at += 8
+    assert at == len(rec)
+    return g
+
+
+def graphs(buf: bytes):
+    return [decode_record(buf[off:off + ln]) for (_, off, ln, _) in locators(buf)]
+
+
+def records(buf: bytes):
+    return {lab: buf[off:off + ln] for (lab, off, ln, _) in locators(buf)}
+
+
+def kernel_image(payload: bytes):
+    """FNDB -> {name: (arg_size, hidden_offsets)} (kernel_image.cpp:44-90)."""
+    assert payload[:4] == b"FNDB"
+    at = 7
+    _tag, count = struct.unpack_from("<II", payload, at)
+    at += 8
+    out = {}
+    for _ in range(count):
+        (ln,) = struct.unpack_from("<I", payload, at)
+        at += 4
+        name = payload[at:at + ln].decode()
+        at += ln
+        size, k = struct.unpack_from("<II", payload, at)
+        at += 8
+        hidden = list(struct.unpack_from("<%dI" % k, payload, at))
+        at += 4 * k + 24
+        out[name] = (size, hidden)
+    return out
+
+
+def hidden_map(archive: str):
+    """(hash, name) -> hidden offsets, for every binary of an archive."""
+    out = {}
+    bdir = os.path.join(archive, "binaries")
+    for f in os.listdir(bdir):
+        if f.endswith(".bin"):
+            h = int(f[:16], 16)
+            for name, (_, hidden) in kernel_image(open(os.path.join(bdir, f), "rb").read()).items():
+                out[(h, name)] = hidden
+    return out
+
+
+def trace_text(g: Graph, hidden, crc64) -> str:
+    """Expected replay trace of one prepared graph (sim_driver.cpp:21-38,402-479)."""
+    lines = []
+    for n in g.nodes:
+        s = "node=%d type=%s" % (n.id, TYPES[n.type])
+        addrs = []
+        if n.type == 0:
+            s += " name=%s grid=%d,%d,%d block=%d,%d,%d shmem=%d" % (
+                (n.name,) + tuple(n.grid) + tuple(n.block) + (n.shmem,))
+            for off in hidden[(n.hash, n.name)]:
+                (a,) = struct.unpack_from("<Q", n.args, off)
+                addrs.append(a)
+            digest = crc64(n.args)
+        elif n.type == 1:
+            addrs = [n.mem[0], n.mem[1]]
+            digest = crc64(struct.pack("<3Q", *n.mem))
+        elif n.type == 2:
+            addrs = [n.mem[0]]
+            digest = crc64(struct.pack("<3Q", *n.mem))
+        else:
+            digest = 0
+        s += " args=%016x addrs=%s" % (digest, ",".join("0x%016x" % a for a in addrs))
+        lines.append(s + "\n")
+    return "".join(lines)

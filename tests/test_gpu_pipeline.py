@@ -1,0 +1,170 @@
+"""GPU parity of the full LOAD path (reference pipeline.cpp:447-569 semantics).
+
+Every replayed trace is compared with the trace derived from the C oracle's
+materialization of the same member (parse_graph_at + relocation + rank patch),
+and the oracle itself is pinned to the reference in test_oracle.py.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+
+import pytest
+
+import fndg
+from conftest import manifest
+
+pytestmark = pytest.mark.gpu
+
+
+def expected_traces(oracle, archive, rank=0, world=1, delta=0):
+    container, _ = oracle.materialize_archive(archive, rank, world, delta)
+    hidden = fndg.hidden_map(archive)
+    return {g.label: fndg.trace_text(g, hidden, oracle.crc64) for g in fndg.graphs(container)}
+
+
+@pytest.mark.parametrize("name", ["micro", "llama3-8b", "moe-spmd"])
+def test_load_replays_every_batch_like_the_oracle(foundry, oracle, archives, name):
+    arch, outcome = archives(name)
+    h = foundry.load(arch)
+    assert h.batches() == list(range(1, outcome.total_graphs + 1))
+    want = expected_traces(oracle, arch)
+    for b in h.batches():
+        assert h.replay(b) == want[b], "batch %d" % b
+    c = h.counters()
+    assert c["exec.instantiate_calls"] == outcome.template_count
+    assert c["capture.begin_calls"] == 0
+    assert c["catalog.prelink_calls"] == 0
+    assert c["replay.launch_calls"] == outcome.total_graphs
+    # one on-demand update per non-template member (test_smoke.py:43, acceptance criterion 5)
+    assert c["exec.update_calls"] == outcome.total_graphs - outcome.template_count
+
+
+def test_save_traces_equal_load_traces_at_world_one(foundry, archives):
+    arch, outcome = archives("micro")
+    h = foundry.load(arch)
+    for b in h.batches():
+        assert h.replay(b) == outcome.traces[b]
+
+
+@pytest.mark.parametrize("rank,world", [(0, 2), (1, 2), (3, 4), (7, 8)])
+def test_rank_patching_matches_the_oracle(foundry, oracle, archives, rank, world):
+    arch, _ = archives("moe-spmd")
+    h = foundry.load(arch, rank=rank, world=world)
+    want = expected_traces(oracle, arch, rank, world)
+    for b in (1, 7, 16, 100, 255, 512):
+        text = h.replay(b)
+        assert text == want[b]
+        assert "stub_" not in text
+        assert "nccl_ring_allreduce" in text and "nvshmem_alltoall_ll" in text
+
+
+def test_ranks_share_one_device_with_relocation(foundry, oracle, archives):
+    """Several ranks on one GPU: only the first lands at the captured base; the
+    others are relocated (K1) onto wherever the driver placed their region."""
+    arch, _ = archives("moe-spmd")
+    base = manifest(arch)["allocator"]["base"]
+    handles = [foundry.load(arch, rank=r, world=4, relocate=True) for r in range(4)]
+    bases = [h.region_base() for h in handles]
+    assert len(set(bases)) == 4 and bases[0] == base
+    for r, h in enumerate(handles):
+        want = expected_traces(oracle, arch, r, 4, bases[r] - base)
+        for b in (1, 64, 333):
+            assert h.replay(b) == want[b]
+        assert h.timings()["relocation_delta"] == bases[r] - base
+    costs = [h.counters()["exec.instantiate_calls"] for h in handles]
+    assert len(set(costs)) == 1
+
+
+def test_shifted_base_without_relocation_fails_at_replay(foundry, archives):
+    arch, _ = archives("micro")
+    h = foundry.load(arch, base_shift_granules=1)
+    with pytest.raises(foundry.FoundryError, match="unmapped-address"):
+        h.replay(1)
+
+
+def test_shifted_base_with_relocation_replays(foundry, oracle, archives):
+    arch, _ = archives("micro")
+    h = foundry.load(arch, base_shift_granules=1, relocate=True)
+    want = expected_traces(oracle, arch, 0, 1, 0x10000)
+    for b in h.batches():
+        assert h.replay(b) == want[b]
+
+
+def test_skip_restore_is_an_unresolved_kernel(foundry, archives):
+    arch, _ = archives("micro")
+    with pytest.raises(foundry.FoundryError, match="unresolved-kernel: template construction"):
+        foundry.load(arch, skip_binary_restore=True)
+
+
+def test_extra_prewindow_alloc_is_a_layout_divergence(foundry, archives):
+    arch, _ = archives("micro")
+    with pytest.raises(foundry.FoundryError, match="layout-divergence: foreground init"):
+        foundry.load(arch, extra_prewindow_alloc=True)
+
+
+def test_skip_device_init_fails_on_comm_nodes(foundry, archives):
+    arch, _ = archives("moe-spmd")
+    h = foundry.load(arch, skip_device_init=True)
+    with pytest.raises(foundry.FoundryError, match="device-state-uninitialized"):
+        h.replay(1)
+
+
+def test_corrupt_graphs_bin_is_named(foundry, archives, tmp_path):
+    arch, _ = archives("micro")
+    bad = tmp_path / "bad"
+    shutil.copytree(arch, bad)
+    data = bytearray((bad / "graphs.bin").read_bytes())
+    data[len(data) // 2] ^= 1
+    (bad / "graphs.bin").write_bytes(bytes(data))
+    with pytest.raises(foundry.FoundryError, match="archive-corruption: archive integrity: integrity check failed for graphs.bin"):
+        foundry.load(str(bad))
+
+
+def test_prepared_params_equal_the_oracle_records(foundry, oracle, archives):
+    import fndg as F
+    arch, _ = archives("moe-spmd")
+    h = foundry.load(arch, rank=2, world=4)
+    container, _ = oracle.materialize_archive(arch, 2, 4)
+    recs = F.records(container)
+    for b in (1, 2, 31, 32, 511, 512):
+        assert h.prepared_record(b) == recs[b]
+
+
+def test_serve_touches_only_differing_nodes(foundry, archives):
+    arch, _ = archives("micro")
+    h = foundry.load(arch)
+    assert h.serve(1) == 0          # representative already applied
+    touched = h.serve(2)
+    assert touched > 0
+    assert h.serve(2) == 0          # serving the applied member is free
+    c = h.counters()
+    assert c["exec.update_calls"] == 1
+    assert c["exec.update_nodes_touched"] == touched
+
+
+@pytest.mark.parametrize("name,batch", [("micro", 5), ("moe-spmd", 200), ("llama3-8b", 35)])
+def test_materialized_graph_reproduces_a_fresh_capture(foundry, archives, name, batch):
+    arch, _ = archives(name)
+    h = foundry.load(arch)
+    ok, report = h.fresh_capture_check(batch)
+    assert ok, report
+
+
+def test_reference_written_archive_loads(foundry, oracle, archives, tmp_path):
+    """An archive without the B200 artefacts (as the reference writes it) is
+    packed in memory at LOAD and replays identically."""
+    arch, _ = archives("micro", b200=False)
+    h = foundry.load(arch)
+    want = expected_traces(oracle, arch)
+    for b in h.batches():
+        assert h.replay(b) == want[b]
+
+
+def test_naive_rebuild_costs_more_construction(foundry, archives):
+    arch, outcome = archives("micro")
+    h = foundry.load(arch)
+    naive = h.naive_rebuild_all()
+    c = h.counters()
+    templated = c["graph.add_node_calls"] + c["graph.add_edge_calls"] + c["graph.set_attr_calls"] + c["exec.instantiate_calls"]
+    assert naive / templated >= 8 / 3 - 0.01
