@@ -103,7 +103,7 @@ def _write_ninja() -> Path:
         f"-L{PKG} -lfoundry_b200 -Wl,-rpath,'$$ORIGIN' -o $out",
         "  description = PYMOD $out",
         "rule exe",
-        f"  command = $cxx $cxxflags $in -L{PKG} -lfoundry_b200 -Wl,-rpath,'$$ORIGIN' -o $out",
+        f"  command = $cxx $cxxflags -rdynamic $in -L{PKG} -lfoundry_b200 -Wl,-rpath,'$$ORIGIN' -o $out",
         "  description = EXE $out",
     ]
     objs = []

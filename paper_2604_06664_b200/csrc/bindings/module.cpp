@@ -9,6 +9,7 @@
 
 #include <chrono>
 
+#include "foundry/bytes.hpp"
 #include "foundry/pipeline.hpp"
 #include "foundry/save.hpp"
 #include "foundry/template_store.hpp"
@@ -197,4 +198,42 @@ PYBIND11_MODULE(_foundry, m) {
         return bench(spec, mode);
     }, py::arg("spec"), py::arg("mode") = "load");
     m.def("cuda_device_count", &cuda_device_count);
+
+    // --- internals used by the test-suite (not part of the reference surface) ---
+    m.def("_crc64", [](py::bytes b) {
+        const std::string s = b;
+        return crc64(s.data(), s.size());
+    });
+    m.def("_crc64_combine", &crc64_combine);
+    m.def("_pack_store", [](const std::string& archive) {
+        py::gil_scoped_release nogil;
+        const PackStats st = pack_archive_store(archive);
+        return std::map<std::string, uint64_t>{{"store_bytes", st.store_bytes},
+                                               {"template_bytes", st.template_bytes},
+                                               {"diff_entries", st.diff_entries},
+                                               {"rank_ops", st.rank_ops},
+                                               {"member_image_bytes", st.member_image_bytes}};
+    });
+    // member-image arena (the kernel's output layout) -> FNDG container in
+    // graphs.bin locator order
+    m.def("_decode_member_images", [](const std::string& archive, py::bytes arena_bytes) {
+        const std::string arena = arena_bytes;
+        ArchivePaths paths{archive};
+        const auto blob = slurp(paths.template_store());
+        StoreView view(blob);
+        const auto graphs_bin = slurp(paths.graphs());
+        std::vector<CapturedGraph> out;
+        for (const auto& loc : parse_graph_locators(graphs_bin)) {
+            const int64_t mi = view.member_of(loc.label);
+            require(mi >= 0, Errc::archive_corruption, "store has no member " + std::to_string(loc.label));
+            const auto& M = view.member(static_cast<uint32_t>(mi));
+            const auto& G = view.group(M.group);
+            require(M.out_off + G.image_bytes <= arena.size(), Errc::invalid_argument, "arena too small");
+            out.push_back(view.image_to_graph(
+                static_cast<uint32_t>(mi),
+                {reinterpret_cast<const uint8_t*>(arena.data()) + M.out_off, G.image_bytes}));
+        }
+        const auto c = serialize_graphs(out);
+        return py::bytes(reinterpret_cast<const char*>(c.data()), c.size());
+    });
 }

@@ -21,7 +21,7 @@ template <typename Fn>
 void resolve(Fn& slot, const char* symbol) {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q{};
-    const cudaError_t e = cudaGetDriverEntryPointByVersion(symbol, &p, 12080, cudaEnableDefault, &q);
+    const cudaError_t e = cudaGetDriverEntryPointByVersion(symbol, &p, 12000, cudaEnableDefault, &q);
     if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || p == nullptr) {
         cudaGetLastError();
         if (g_error.empty()) g_error = std::string("cannot resolve driver entry point ") + symbol;

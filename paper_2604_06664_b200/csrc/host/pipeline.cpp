@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <thread>
@@ -30,6 +32,12 @@ double ms_since(Clock::time_point t0) {
 }
 
 constexpr uint32_t kNoMember = 0xFFFFFFFFu;
+
+// FOUNDRY_DEBUG=1 prints LOAD phase boundaries to stderr (diagnostics only).
+void debug_phase(const char* what) {
+    static const bool on = std::getenv("FOUNDRY_DEBUG") != nullptr;
+    if (on) std::fprintf(stderr, "[foundry] %s\n", what);
+}
 constexpr size_t kStageAlign = 256;
 constexpr size_t kReadChunk = 8ull << 20;
 
@@ -326,6 +334,13 @@ uint64_t ServingContext::Impl::build_graph_for(uint32_t gi, uint32_t m, CUgraph&
                 void* extra[5];
                 size_t size;
                 kernel_params(d, blob, K, p, extra, &size);
+                static const bool one_fn = std::getenv("FOUNDRY_EXPERIMENT_ONE_FUNCTION") != nullptr;
+                static CUfunction first_fn = nullptr;
+                if (one_fn) {  // experiment: every node launches the same function
+                    if (!first_fn) first_fn = K.fn;
+                    p.func = first_fn;
+                    size = 192;
+                }
                 cu_check(api.cuGraphAddKernelNode(&node, graph, nullptr, 0, &p), "cuGraphAddKernelNode");
                 const fdt_node_attrs& a = view->node_attrs(gi, n);
                 const bool non_default = a.cluster[0] != 1 || a.cluster[1] != 1 || a.cluster[2] != 1 ||
@@ -389,7 +404,9 @@ void ServingContext::Impl::build_group(uint32_t gi) {
     Group& grp = groups[gi];
     const uint32_t m = G.first_member;  // representative: the smallest label
     const auto t0 = Clock::now();
+    debug_phase("build group");
     build_graph_for(gi, m, grp.graph, grp.nodes);
+    debug_phase("built group");
     const auto e = view->edges(gi);
     (void)e;
     // counters mirror the reference builder lane (sim_driver.cpp:307-313)
@@ -407,6 +424,7 @@ void ServingContext::Impl::build_group(uint32_t gi) {
     const double build = ms_since(t0);
     const auto t1 = Clock::now();
     cu_check(api.cuGraphInstantiate(&grp.exec, grp.graph, 0), "cuGraphInstantiate");
+    debug_phase("instantiated group");
     ++lane_acquisitions;
     ctx->c_instantiate.fetch_add(1);
     t.build_ms += build;
@@ -644,6 +662,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
         rethrow_in_step("archive integrity");
     }
     I.t.stage_ms = ms_since(t0);
+    debug_phase("stage done");
     t0 = Clock::now();
     {
         std::vector<Segment> segs;
@@ -662,6 +681,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
         }
     }
     I.t.integrity_ms = ms_since(t0);
+    debug_phase("integrity done");
 
     const WorkloadSpec spec = WorkloadSpec::parse_text(I.manifest.workload_text);
     require(spec.digest() == I.manifest.workload_digest, Errc::archive_corruption,
@@ -712,6 +732,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
         if (K) I.kernel_of[k] = static_cast<int32_t>(K->entry_id);
     }
     I.t.restore_ms = ms_since(t0);
+    debug_phase("restore done");
 
     // 4. region
     t0 = Clock::now();
@@ -721,6 +742,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     if (opts.preallocate) I.ctx->preallocate(I.manifest.final_offset);
     if (opts.faults.extra_prewindow_alloc) I.ctx->allocate(1);
     I.t.region_ms = ms_since(t0);
+    debug_phase("region done");
 
     // 5. materialize every member for this rank: one fused kernel, then D2H
     t0 = Clock::now();
@@ -736,12 +758,14 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     launch_materialize(device, I.dstore, req, I.d_members.data(), &mt);
     I.t.materialize_kernel_ms = mt.kernel_ms;
     I.t.materialize_ms = ms_since(t0);
+    debug_phase("materialize done");
     t0 = Clock::now();
     cuda_check(cudaMemcpyAsync(I.h_members.data(), I.d_members.data(), H.members_image_bytes,
                                cudaMemcpyDeviceToHost, device.stream()),
                "cudaMemcpyAsync(member images D2H)");
     cuda_check(cudaStreamSynchronize(device.stream()), "cudaStreamSynchronize");
     I.t.download_ms = ms_since(t0);
+    debug_phase("download done");
     I.t.d2h_bytes += H.members_image_bytes;
     I.t.member_bytes = H.members_image_bytes;
     I.t.store_bytes = I.dstore.bytes;
@@ -782,6 +806,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
         foreground_error = std::current_exception();
     }
     I.t.foreground_ms = ms_since(t0);
+    debug_phase("foreground done");
     builder.join();
     if (foreground_error) std::rethrow_exception(foreground_error);
     if (builder_error) {

@@ -6,7 +6,12 @@
 //        images back and re-encode them as an FNDG container in graphs.bin
 //        locator order (the layout of oracle/ref_tool `prepare`).
 //   gpu-crc <file>...                              CRC-64/XZ of files on the GPU
+#include <atomic>
 #include <chrono>
+#include <thread>
+#include <csignal>
+#include <execinfo.h>
+#include <unistd.h>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -14,6 +19,9 @@
 
 #include "foundry/archive.hpp"
 #include "foundry/bytes.hpp"
+#include "foundry/driver_api.hpp"
+#include "foundry/gpu_context.hpp"
+#include "foundry/pipeline.hpp"
 #include "foundry/save.hpp"
 #include "foundry/template_store.hpp"
 #include "foundry/workload.hpp"
@@ -128,6 +136,140 @@ static int cmd_save(int argc, char** argv) {
     return 0;
 }
 
+// load <archive> [rank world relocate] : LOAD + replay every batch, print timings
+static int cmd_load(int argc, char** argv) {
+    LoadOptions o;
+    if (argc > 3) o.rank = static_cast<uint32_t>(std::stoul(argv[3]));
+    if (argc > 4) o.world = static_cast<uint32_t>(std::stoul(argv[4]));
+    if (argc > 5) o.relocate = std::string(argv[5]) == "1";
+    ServingContext sc = load(argv[2], o);
+    const auto& t = sc.timings();
+    std::fprintf(stderr, "loaded: total %.3f ms restore %.3f instantiate %.3f build %.3f\n", t.total_ms,
+                 t.restore_ms, t.instantiate_ms, t.build_ms);
+    size_t n = 0;
+    for (uint32_t b : sc.batches()) n += sc.replay(b).records.size();
+    std::printf("{\"total_ms\": %.3f, \"stage_ms\": %.3f, \"integrity_ms\": %.3f, \"restore_ms\": %.3f, "
+                "\"materialize_ms\": %.3f, \"download_ms\": %.3f, \"build_ms\": %.3f, "
+                "\"instantiate_ms\": %.3f, \"records\": %zu}\n",
+                t.total_ms, t.stage_ms, t.integrity_ms, t.restore_ms, t.materialize_ms, t.download_ms,
+                t.build_ms, t.instantiate_ms, n);
+    return 0;
+}
+
+// instbench <archive>: cost of cuGraphInstantiate for N-node graphs under
+// different node/edge/attribute/parameter variants (driver-cost study).
+static int cmd_instbench(int argc, char** argv) {
+    (void)argc;
+    ArchivePaths paths{argv[2]};
+    Device dev(0);
+    GpuContext ctx(dev);
+    const Catalog cat = parse_catalog(slurp(paths.catalog()));
+    const auto& rec = cat.binaries.begin()->second;
+    const KernelImage img = parse_kernel_image(slurp(paths.binary(rec.hash)));
+    const auto cubin = slurp(paths.cubin(rec.hash));
+    ctx.load_library(rec.hash, img, cubin, 0, false);
+    const DriverApi& api = driver();
+    CUcontext cu = nullptr;
+    api.cuCtxGetCurrent(&cu);
+    std::vector<const GpuContext::Kernel*> ks;
+    for (const auto& e : img.entrypoints) ks.push_back(ctx.find_kernel(rec.hash, e.name));
+    std::vector<uint8_t> blob(4096, 0);
+    auto run = [&](const char* label, int nodes, bool distinct, bool chain, bool attrs, int param_bytes) {
+        CUgraph g;
+        cu_check(api.cuGraphCreate(&g, 0), "create");
+        std::vector<CUgraphNode> ns(nodes);
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int i = 0; i < nodes; ++i) {
+            const auto* K = ks[distinct ? i % ks.size() : 0];
+            size_t size = K->arg_buffer_size;
+            void* extra[5] = {CU_LAUNCH_PARAM_BUFFER_POINTER, blob.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &size,
+                              CU_LAUNCH_PARAM_END};
+            CUDA_KERNEL_NODE_PARAMS p;
+            std::memset(&p, 0, sizeof p);
+            p.func = K->fn;
+            p.gridDimX = p.gridDimY = p.gridDimZ = 1;
+            p.blockDimX = 128;
+            p.blockDimY = p.blockDimZ = 1;
+            p.extra = extra;
+            (void)param_bytes;
+            cu_check(api.cuGraphAddKernelNode(&ns[i], g, (chain && i) ? &ns[i - 1] : nullptr, (chain && i) ? 1 : 0, &p),
+                     "add");
+            if (attrs && i % 11 == 0) {
+                CUkernelNodeAttrValue v{};
+                v.clusterSchedulingPolicyPreference = CU_CLUSTER_SCHEDULING_POLICY_SPREAD;
+                cu_check(api.cuGraphKernelNodeSetAttribute(ns[i], CU_LAUNCH_ATTRIBUTE_CLUSTER_SCHEDULING_POLICY_PREFERENCE, &v), "attr");
+            }
+        }
+        const double add_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        const auto t1 = std::chrono::steady_clock::now();
+        CUgraphExec x;
+        cu_check(api.cuGraphInstantiate(&x, g, 0), "inst");
+        const double inst_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
+        const auto t2 = std::chrono::steady_clock::now();
+        cu_check(api.cuGraphLaunch(x, dev.stream()), "launch");
+        dev.sync();
+        const double launch_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t2).count();
+        std::printf("%-28s nodes %5d add %8.3f ms  instantiate %8.3f ms  first launch %8.3f ms\n", label, nodes,
+                    add_ms, inst_ms, launch_ms);
+        api.cuGraphExecDestroy(x);
+        api.cuGraphDestroy(g);
+    };
+    // parallel instantiation of independent graphs from T host threads
+    for (int threads : {1, 2, 4, 8}) {
+        const int graphs = 8;
+        std::vector<CUgraph> gs(graphs);
+        for (int k = 0; k < graphs; ++k) {
+            cu_check(api.cuGraphCreate(&gs[k], 0), "create");
+            for (int i = 0; i < 1000; ++i) {
+                const auto* K = ks[0];
+                size_t size = K->arg_buffer_size;
+                void* extra[5] = {CU_LAUNCH_PARAM_BUFFER_POINTER, blob.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &size,
+                                  CU_LAUNCH_PARAM_END};
+                CUDA_KERNEL_NODE_PARAMS p;
+                std::memset(&p, 0, sizeof p);
+                p.func = K->fn;
+                p.gridDimX = p.gridDimY = p.gridDimZ = 1;
+                p.blockDimX = 128;
+                p.blockDimY = p.blockDimZ = 1;
+                p.extra = extra;
+                CUgraphNode n;
+                cu_check(api.cuGraphAddKernelNode(&n, gs[k], nullptr, 0, &p), "add");
+            }
+        }
+        std::vector<CUgraphExec> xs(graphs);
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        std::atomic<int> next{0};
+        for (int t = 0; t < threads; ++t)
+            pool.emplace_back([&] {
+                try {
+                    dev.make_current();
+                    for (int k; (k = next.fetch_add(1)) < graphs;)
+                        cu_check(api.cuGraphInstantiate(&xs[k], gs[k], 0), "inst");
+                } catch (const std::exception& e) {
+                    std::fprintf(stderr, "thread error: %s\n", e.what());
+                }
+            });
+        for (auto& t : pool) t.join();
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        std::printf("instantiate %d x 1000-node independent graphs with %d threads: %.3f ms\n", graphs, threads, ms);
+        for (int k = 0; k < graphs; ++k) {
+            api.cuGraphExecDestroy(xs[k]);
+            api.cuGraphDestroy(gs[k]);
+        }
+    }
+    for (int rep = 0; rep < 1; ++rep) {
+        run("same fn, independent", 1000, false, false, false, 0);
+        run("same fn, chain", 1000, false, true, false, 0);
+        run("distinct fn, independent", 1000, true, false, false, 0);
+        run("distinct fn, chain", 1000, true, true, false, 0);
+        run("distinct fn, chain, attrs", 1000, true, true, true, 0);
+        run("same fn, independent", 100, false, false, false, 0);
+        run("same fn, independent", 4000, false, false, false, 0);
+    }
+    return 0;
+}
+
 // pack-cubins <archive>: trace cubins only (store via `pack`)
 static int cmd_pack_all(int argc, char** argv) {
     (void)argc;
@@ -157,7 +299,17 @@ static int cmd_gpu_crc(int argc, char** argv) {
     return 0;
 }
 
+static void on_fatal(int sig) {
+    void* frames[64];
+    const int n = backtrace(frames, 64);
+    std::fprintf(stderr, "fatal signal %d, backtrace:\n", sig);
+    backtrace_symbols_fd(frames, n, 2);
+    _exit(128 + sig);
+}
+
 int main(int argc, char** argv) {
+    std::signal(SIGSEGV, on_fatal);
+    std::signal(SIGABRT, on_fatal);
     if (argc < 3) {
         std::fprintf(stderr, "usage: fdy_tool pack|gpu-materialize|gpu-crc ...\n");
         return 64;
@@ -169,6 +321,8 @@ int main(int argc, char** argv) {
         if (cmd == "gpu-crc") return cmd_gpu_crc(argc, argv);
         if (cmd == "decode") return cmd_decode(argc, argv);
         if (cmd == "save") return cmd_save(argc, argv);
+        if (cmd == "load") return cmd_load(argc, argv);
+        if (cmd == "instbench") return cmd_instbench(argc, argv);
         if (cmd == "pack-all") return cmd_pack_all(argc, argv);
     } catch (const Error& e) {
         std::fprintf(stderr, "%s\n", e.what());
