@@ -31,16 +31,21 @@ struct SaveOutcome {
 };
 
 struct ServingHandle {
-    explicit ServingHandle(ServingContext&& s) : sc(std::move(s)) {}
-    std::string replay(uint32_t batch) { return sc.replay(batch).to_text(); }
-    std::vector<uint32_t> batches() const { return sc.batches(); }
+    explicit ServingHandle(ServingContext&& s) : sc(std::make_unique<ServingContext>(std::move(s))) {}
+    ServingContext& ctx() const {
+        require(sc != nullptr, Errc::invalid_argument, "serving handle is closed");
+        return *sc;
+    }
+    void close() { sc.reset(); }
+    std::string replay(uint32_t batch) { return ctx().replay(batch).to_text(); }
+    std::vector<uint32_t> batches() const { return ctx().batches(); }
     std::map<std::string, uint64_t> counters() const {
-        const auto c = sc.counters();
+        const auto c = ctx().counters();
         return {c.begin(), c.end()};
     }
-    uint32_t template_count() const { return sc.template_count(); }
+    uint32_t template_count() const { return ctx().template_count(); }
     py::dict timings() const {
-        const LoadTimings& t = sc.timings();
+        const LoadTimings& t = ctx().timings();
         py::dict d;
         d["total_ms"] = t.total_ms;
         d["manifest_ms"] = t.manifest_ms;
@@ -66,25 +71,25 @@ struct ServingHandle {
         return d;
     }
     py::bytes prepared_record(uint32_t batch) const {
-        const auto rec = encode_graph_record(sc.prepared_params(batch));
+        const auto rec = encode_graph_record(ctx().prepared_params(batch));
         return py::bytes(reinterpret_cast<const char*>(rec.data()), rec.size());
     }
-    uint64_t serve(uint32_t batch) { return sc.serve(batch); }
-    uint64_t region_base() { return sc.context().region_base(); }
+    uint64_t serve(uint32_t batch) { return ctx().serve(batch); }
+    uint64_t region_base() { return ctx().context().region_base(); }
     py::tuple fresh_capture_check(uint32_t batch) {
         std::string rep;
         bool ok;
         {
             py::gil_scoped_release nogil;
-            ok = sc.fresh_capture_check(batch, &rep);
+            ok = ctx().fresh_capture_check(batch, &rep);
         }
         return py::make_tuple(ok, rep);
     }
     uint64_t naive_rebuild_all() {
         py::gil_scoped_release nogil;
-        return sc.naive_rebuild_all();
+        return ctx().naive_rebuild_all();
     }
-    ServingContext sc;
+    std::unique_ptr<ServingContext> sc;
 };
 
 SaveOutcome do_save(const WorkloadSpec& spec, const std::string& out, bool emit_json_graphs,
@@ -166,7 +171,10 @@ PYBIND11_MODULE(_foundry, m) {
         .def("serve", &ServingHandle::serve, py::arg("batch"), py::call_guard<py::gil_scoped_release>())
         .def("region_base", &ServingHandle::region_base)
         .def("fresh_capture_check", &ServingHandle::fresh_capture_check, py::arg("batch"))
-        .def("naive_rebuild_all", &ServingHandle::naive_rebuild_all);
+        .def("naive_rebuild_all", &ServingHandle::naive_rebuild_all)
+        .def("close", &ServingHandle::close, "Release the rank's graphs, libraries and VA region now")
+        .def("__enter__", [](py::object self) { return self; })
+        .def("__exit__", [](ServingHandle& h, py::args) { h.close(); });
 
     m.def("preset_names", &preset_names);
     m.def("preset", &preset, py::arg("name"));

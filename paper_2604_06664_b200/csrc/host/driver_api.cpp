@@ -62,7 +62,7 @@ void load_all() {
     FDY_RESOLVE(cuGraphAddEmptyNode);
     FDY_RESOLVE(cuGraphAddDependencies);
     FDY_RESOLVE(cuGraphKernelNodeSetAttribute);
-    FDY_RESOLVE(cuGraphInstantiate);
+    resolve(g_api.cuGraphInstantiate, "cuGraphInstantiateWithFlags");  // not the legacy _v2 ABI
     FDY_RESOLVE(cuGraphExecDestroy);
     FDY_RESOLVE(cuGraphExecKernelNodeSetParams);
     FDY_RESOLVE(cuGraphExecMemcpyNodeSetParams);

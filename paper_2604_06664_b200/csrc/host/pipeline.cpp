@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -793,7 +794,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
                     I.ctx->free(slot[st.slot]);
                 }
             }
-            verify_init_records(I.ctx->records(), cfg.base, log);
+            verify_init_records(I.ctx->records(), I.ctx->region_base(), log);
         } catch (const Error&) {
             rethrow_in_step("foreground init");
         }
@@ -889,7 +890,11 @@ std::vector<std::string> canonical_records(const std::vector<uint8_t>& recs) {
         fdy_trace_header h;
         std::memcpy(&h, recs.data() + at, sizeof h);
         const size_t len = FDY_TRACE_HEADER_BYTES + ((h.n_bytes + 15u) & ~15u);
-        out.emplace_back(reinterpret_cast<const char*>(recs.data() + at), std::min(len, recs.size() - at));
+        // meaningful fields only: header words before the pad, then the parameter bytes
+        std::string r(reinterpret_cast<const char*>(recs.data() + at), offsetof(fdy_trace_header, magic));
+        r.append(reinterpret_cast<const char*>(recs.data() + at + FDY_TRACE_HEADER_BYTES),
+                 std::min<size_t>(h.n_bytes, recs.size() - at - FDY_TRACE_HEADER_BYTES));
+        out.push_back(std::move(r));
         at += len;
     }
     std::sort(out.begin(), out.end());

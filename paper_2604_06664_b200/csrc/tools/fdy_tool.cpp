@@ -323,6 +323,11 @@ int main(int argc, char** argv) {
         if (cmd == "save") return cmd_save(argc, argv);
         if (cmd == "load") return cmd_load(argc, argv);
         if (cmd == "instbench") return cmd_instbench(argc, argv);
+        if (cmd == "naive") {
+            ServingContext sc = load(argv[2], LoadOptions{});
+            std::printf("naive construction calls %llu\n", (unsigned long long)sc.naive_rebuild_all());
+            return 0;
+        }
         if (cmd == "pack-all") return cmd_pack_all(argc, argv);
     } catch (const Error& e) {
         std::fprintf(stderr, "%s\n", e.what());

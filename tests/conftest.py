@@ -103,3 +103,18 @@ def has_gpu() -> bool:
         return f.cuda_device_count() > 0
     except Exception:
         return False
+
+
+@pytest.fixture
+def load(foundry):
+    """foundry.load that closes every handle it returned at test teardown."""
+    handles = []
+
+    def _load(*args, **kwargs):
+        h = foundry.load(*args, **kwargs)
+        handles.append(h)
+        return h
+
+    yield _load
+    for h in handles:
+        h.close()

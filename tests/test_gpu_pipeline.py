@@ -17,6 +17,15 @@ from conftest import manifest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _release_handles():
+    """Handles own a VA reservation at the captured base; release every handle
+    a test created (even when it failed) before the next test loads."""
+    import gc
+    yield
+    gc.collect()
+
+
 def expected_traces(oracle, archive, rank=0, world=1, delta=0):
     container, _ = oracle.materialize_archive(archive, rank, world, delta)
     hidden = fndg.hidden_map(archive)
@@ -24,9 +33,9 @@ def expected_traces(oracle, archive, rank=0, world=1, delta=0):
 
 
 @pytest.mark.parametrize("name", ["micro", "llama3-8b", "moe-spmd"])
-def test_load_replays_every_batch_like_the_oracle(foundry, oracle, archives, name):
+def test_load_replays_every_batch_like_the_oracle(foundry, load, oracle, archives, name):
     arch, outcome = archives(name)
-    h = foundry.load(arch)
+    h = load(arch)
     assert h.batches() == list(range(1, outcome.total_graphs + 1))
     want = expected_traces(oracle, arch)
     for b in h.batches():
@@ -40,17 +49,17 @@ def test_load_replays_every_batch_like_the_oracle(foundry, oracle, archives, nam
     assert c["exec.update_calls"] == outcome.total_graphs - outcome.template_count
 
 
-def test_save_traces_equal_load_traces_at_world_one(foundry, archives):
+def test_save_traces_equal_load_traces_at_world_one(foundry, load, archives):
     arch, outcome = archives("micro")
-    h = foundry.load(arch)
+    h = load(arch)
     for b in h.batches():
         assert h.replay(b) == outcome.traces[b]
 
 
 @pytest.mark.parametrize("rank,world", [(0, 2), (1, 2), (3, 4), (7, 8)])
-def test_rank_patching_matches_the_oracle(foundry, oracle, archives, rank, world):
+def test_rank_patching_matches_the_oracle(foundry, load, oracle, archives, rank, world):
     arch, _ = archives("moe-spmd")
-    h = foundry.load(arch, rank=rank, world=world)
+    h = load(arch, rank=rank, world=world)
     want = expected_traces(oracle, arch, rank, world)
     for b in (1, 7, 16, 100, 255, 512):
         text = h.replay(b)
@@ -59,12 +68,12 @@ def test_rank_patching_matches_the_oracle(foundry, oracle, archives, rank, world
         assert "nccl_ring_allreduce" in text and "nvshmem_alltoall_ll" in text
 
 
-def test_ranks_share_one_device_with_relocation(foundry, oracle, archives):
+def test_ranks_share_one_device_with_relocation(foundry, load, oracle, archives):
     """Several ranks on one GPU: only the first lands at the captured base; the
     others are relocated (K1) onto wherever the driver placed their region."""
     arch, _ = archives("moe-spmd")
     base = manifest(arch)["allocator"]["base"]
-    handles = [foundry.load(arch, rank=r, world=4, relocate=True) for r in range(4)]
+    handles = [load(arch, rank=r, world=4, relocate=True) for r in range(4)]
     bases = [h.region_base() for h in handles]
     assert len(set(bases)) == 4 and bases[0] == base
     for r, h in enumerate(handles):
@@ -76,41 +85,41 @@ def test_ranks_share_one_device_with_relocation(foundry, oracle, archives):
     assert len(set(costs)) == 1
 
 
-def test_shifted_base_without_relocation_fails_at_replay(foundry, archives):
+def test_shifted_base_without_relocation_fails_at_replay(foundry, load, archives):
     arch, _ = archives("micro")
-    h = foundry.load(arch, base_shift_granules=1)
+    h = load(arch, base_shift_granules=1)
     with pytest.raises(foundry.FoundryError, match="unmapped-address"):
         h.replay(1)
 
 
-def test_shifted_base_with_relocation_replays(foundry, oracle, archives):
+def test_shifted_base_with_relocation_replays(foundry, load, oracle, archives):
     arch, _ = archives("micro")
-    h = foundry.load(arch, base_shift_granules=1, relocate=True)
+    h = load(arch, base_shift_granules=1, relocate=True)
     want = expected_traces(oracle, arch, 0, 1, 0x10000)
     for b in h.batches():
         assert h.replay(b) == want[b]
 
 
-def test_skip_restore_is_an_unresolved_kernel(foundry, archives):
+def test_skip_restore_is_an_unresolved_kernel(foundry, load, archives):
     arch, _ = archives("micro")
     with pytest.raises(foundry.FoundryError, match="unresolved-kernel: template construction"):
-        foundry.load(arch, skip_binary_restore=True)
+        load(arch, skip_binary_restore=True)
 
 
-def test_extra_prewindow_alloc_is_a_layout_divergence(foundry, archives):
+def test_extra_prewindow_alloc_is_a_layout_divergence(foundry, load, archives):
     arch, _ = archives("micro")
     with pytest.raises(foundry.FoundryError, match="layout-divergence: foreground init"):
-        foundry.load(arch, extra_prewindow_alloc=True)
+        load(arch, extra_prewindow_alloc=True)
 
 
-def test_skip_device_init_fails_on_comm_nodes(foundry, archives):
+def test_skip_device_init_fails_on_comm_nodes(foundry, load, archives):
     arch, _ = archives("moe-spmd")
-    h = foundry.load(arch, skip_device_init=True)
+    h = load(arch, skip_device_init=True)
     with pytest.raises(foundry.FoundryError, match="device-state-uninitialized"):
         h.replay(1)
 
 
-def test_corrupt_graphs_bin_is_named(foundry, archives, tmp_path):
+def test_corrupt_graphs_bin_is_named(foundry, load, archives, tmp_path):
     arch, _ = archives("micro")
     bad = tmp_path / "bad"
     shutil.copytree(arch, bad)
@@ -118,22 +127,22 @@ def test_corrupt_graphs_bin_is_named(foundry, archives, tmp_path):
     data[len(data) // 2] ^= 1
     (bad / "graphs.bin").write_bytes(bytes(data))
     with pytest.raises(foundry.FoundryError, match="archive-corruption: archive integrity: integrity check failed for graphs.bin"):
-        foundry.load(str(bad))
+        load(str(bad))
 
 
-def test_prepared_params_equal_the_oracle_records(foundry, oracle, archives):
+def test_prepared_params_equal_the_oracle_records(foundry, load, oracle, archives):
     import fndg as F
     arch, _ = archives("moe-spmd")
-    h = foundry.load(arch, rank=2, world=4)
+    h = load(arch, rank=2, world=4)
     container, _ = oracle.materialize_archive(arch, 2, 4)
     recs = F.records(container)
     for b in (1, 2, 31, 32, 511, 512):
         assert h.prepared_record(b) == recs[b]
 
 
-def test_serve_touches_only_differing_nodes(foundry, archives):
+def test_serve_touches_only_differing_nodes(foundry, load, archives):
     arch, _ = archives("micro")
-    h = foundry.load(arch)
+    h = load(arch)
     assert h.serve(1) == 0          # representative already applied
     touched = h.serve(2)
     assert touched > 0
@@ -144,26 +153,26 @@ def test_serve_touches_only_differing_nodes(foundry, archives):
 
 
 @pytest.mark.parametrize("name,batch", [("micro", 5), ("moe-spmd", 200), ("llama3-8b", 35)])
-def test_materialized_graph_reproduces_a_fresh_capture(foundry, archives, name, batch):
+def test_materialized_graph_reproduces_a_fresh_capture(foundry, load, archives, name, batch):
     arch, _ = archives(name)
-    h = foundry.load(arch)
+    h = load(arch)
     ok, report = h.fresh_capture_check(batch)
     assert ok, report
 
 
-def test_reference_written_archive_loads(foundry, oracle, archives, tmp_path):
+def test_reference_written_archive_loads(foundry, load, oracle, archives, tmp_path):
     """An archive without the B200 artefacts (as the reference writes it) is
     packed in memory at LOAD and replays identically."""
     arch, _ = archives("micro", b200=False)
-    h = foundry.load(arch)
+    h = load(arch)
     want = expected_traces(oracle, arch)
     for b in h.batches():
         assert h.replay(b) == want[b]
 
 
-def test_naive_rebuild_costs_more_construction(foundry, archives):
+def test_naive_rebuild_costs_more_construction(foundry, load, archives):
     arch, outcome = archives("micro")
-    h = foundry.load(arch)
+    h = load(arch)
     naive = h.naive_rebuild_all()
     c = h.counters()
     templated = c["graph.add_node_calls"] + c["graph.add_edge_calls"] + c["graph.set_attr_calls"] + c["exec.instantiate_calls"]
