@@ -1,0 +1,362 @@
+#!/usr/bin/env python3
+"""Benchmark: graph-set materialization on B200 (Foundry LOAD path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload qwen3-235b-a22b]
+
+One "step" = one graph-set materialization for one rank: every member graph
+of the archive (512 batch sizes, 1036 nodes each for the headline
+Qwen3-235B-A22B-shaped TP8 set) expanded from the HBM-resident template store
+by the fused K2 (diff) + K1 (relocation) + K3 (rank patch) kernel. Each process
+is one GPU and one TP rank (rank = global rank % 8 of world 8), so per-GPU work
+is fixed as N grows ("weak" scaling); there is no data-path collective.
+
+JSON keys beyond the base contract:
+  e2e          the same materialization measured through the public API
+               (`foundry.load(archive, rank, world)`): archive files on the host
+               -> GPU integrity CRC -> store DMA -> fused kernel -> cuLibrary
+               restore -> template graphs built+instantiated -> one verified
+               replay read back. Host<->device bytes are counted per step.
+  e2e.breakdown  per-phase wall times; `driver_bound_ms` (cuLibraryLoadData +
+               graph construction + cuGraphInstantiate) is reported separately.
+  roofline     HBM roofline of the fused kernel (algorithmic bytes / event time).
+  cpu_baseline the reference's own CPU path (oracle/_ref) on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+REF_TOOL = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TP_WORLD = 8  # the headline set is TP8: every GPU materializes one rank's graph set
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", default="qwen3-235b-a22b")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def prepare_archives(workload: str, rank: int, barrier) -> tuple[str, str]:
+    """Writes (once per node) the B200 archive and a reference-layout archive
+    (no B200 artefacts) of the same spec with this build's SAVE, which is
+    byte-identical to the reference's (tests/test_save.py)."""
+    import paper_2604_06664_b200 as foundry
+
+    root = os.path.join(tempfile.gettempdir(), "foundry_bench_" + workload)
+    ours, plain = os.path.join(root, "b200"), os.path.join(root, "plain")
+    done = os.path.join(root, "READY")
+    if rank == 0 and not os.path.exists(done):
+        shutil.rmtree(root, ignore_errors=True)
+        os.makedirs(root)
+        spec = foundry.workload_from_text(open(foundry.workload_path(workload)).read())
+        os.environ.setdefault("FOUNDRY_CUBIN_CACHE", os.path.join(root, "cubin_cache"))
+        foundry.save(spec, ours)
+        foundry.save(spec, plain, b200_artifacts=False)
+        open(done, "w").write("ok")
+    barrier()
+    return ours, plain
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + q, "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [int(r[0]) for r in self.rows if r[0].isdigit()]
+        busy = [int(r[0]) for r in self.rows if r[0].isdigit() and r[6].isdigit() and int(r[6]) > 0]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                "sw_power_cap"], r[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(busy or sm), "sm_max_mhz": int(self.rows[0][1]),
+                "samples": len(self.rows), "samples_busy": len(busy), "reasons": sorted(reasons)}
+
+
+def reference_load_ms(archive: str, rank: int, world: int, lanes: int, reps: int) -> dict | None:
+    if not os.path.exists(REF_TOOL):
+        return None
+    r = subprocess.run([REF_TOOL, "time-load", archive, str(rank), str(world), str(lanes), str(reps)],
+                       capture_output=True, text=True)
+    return json.loads(r.stdout) if r.returncode == 0 else None
+
+
+def reference_materialize_ms(archive: str, rank: int, world: int, lanes: int, reps: int) -> dict | None:
+    if not os.path.exists(REF_TOOL):
+        return None
+    r = subprocess.run([REF_TOOL, "time-materialize", archive, str(rank), str(world), str(lanes),
+                        str(reps)], capture_output=True, text=True)
+    return json.loads(r.stdout) if r.returncode == 0 else None
+
+
+def oracle_port_ms(archive: str, rank: int, world: int, lanes: int, reps: int) -> dict:
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle
+
+    orc = Oracle(os.path.join(ROOT, "oracle", "_build", "liboracle.so"))
+    times = []
+    for _ in range(reps + 1):
+        t0 = time.perf_counter()
+        orc.materialize_archive(archive, rank, world, 0x10000, lanes)
+        times.append((time.perf_counter() - t0) * 1e3)
+    return {"best_ms": min(times[1:]), "mean_ms": statistics.mean(times[1:]), "reps": reps,
+            "lanes": lanes}
+
+
+def run_reference(args, grank, gworld):
+    """--impl reference: the reference's own CPU load() of the same archive."""
+    if grank != 0:
+        return
+    lanes = os.cpu_count() or 1
+    _, plain = prepare_archives(args.workload, 0, lambda: None)
+    wrank = 0
+    res = reference_load_ms(plain, wrank, TP_WORLD, lanes, args.steps)
+    kind = "reference"
+    if res is None:
+        res = oracle_port_ms(plain, wrank, TP_WORLD, lanes, args.steps)
+        kind = "port"
+    value = res["mean_ms"]
+    line = {
+        "impl": "reference",
+        "metric": "graph-set materialization ms (cold start); relocation GB/s vs HBM peak",
+        "value": value, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps, "warmup": 1,
+        "ms_per_step": value, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic",
+        "config": {"workload": args.workload + "~ tier-R TP8 (rank 0 of 8)", "graphs": 512,
+                   "parallelism": "replicas"},
+        "cpu_baseline": {"value": value, "unit": "ms", "cores": lanes, "kind": kind,
+                         "sample": "full reference load() of the archive, %d reps after 1 warm-up" % args.steps},
+        "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    grank, gworld, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, grank, gworld)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_06664_b200 as foundry
+    from paper_2604_06664_b200 import capi
+
+    torch.cuda.set_device(local)
+    if gworld > 1:
+        dist.init_process_group("nccl", init_method="env://")
+
+    def barrier():
+        if gworld > 1:
+            dist.barrier()
+
+    def reduce_max(x: float) -> float:
+        if gworld == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    archive, plain = prepare_archives(args.workload, grank, barrier)
+    wrank = grank % TP_WORLD
+    with open(os.path.join(archive, "manifest")) as f:
+        manifest = json.load(f)
+    base = manifest["allocator"]["base"]
+    delta = 0x10000  # exercise K1: the region lands one granule away
+    blob = open(os.path.join(archive, "templates.fdt"), "rb").read()
+    hdr = capi.store_header(blob)
+    alg = capi.algorithmic_bytes(hdr)
+
+    # ---------------- device-resident materialization (value) ----------------
+    api = capi.CApi()
+    dev = api.device_open(local)
+    store = api.store_upload(dev, blob)
+    members, _ = api.materialize(dev, store, wrank, TP_WORLD, base + delta)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    for _ in range(args.warmup):
+        flush.zero_()
+        torch.cuda.synchronize()
+        api.materialize(dev, store, wrank, TP_WORLD, base + delta, members)
+    sampler = ClockSampler(local)
+    with sampler:
+        barrier()
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(args.steps):
+            flush.zero_()  # flush L2 between timed iterations (outside the events)
+            torch.cuda.synchronize()
+            _, ms = api.materialize(dev, store, wrank, TP_WORLD, base + delta, members)
+            times.append(ms)
+        torch.cuda.synchronize()
+        barrier()
+        kernel_ms = statistics.mean(times)
+        kernel_ms_max = reduce_max(kernel_ms)
+
+        # ---------------- end to end through the public API ----------------
+        e2e_times, breakdowns = [], []
+        h = foundry.load(archive, rank=wrank, world=TP_WORLD)  # warm-up (page cache, driver)
+        h.replay(1)
+        h.close()
+        for _ in range(args.e2e_steps):
+            barrier()
+            t0 = time.perf_counter()
+            h = foundry.load(archive, rank=wrank, world=TP_WORLD)
+            trace = h.replay(1)  # D2H of the verified device trace of batch 1
+            e2e_times.append((time.perf_counter() - t0) * 1e3)
+            breakdowns.append(h.timings())
+            h.close()
+        e2e_ms = reduce_max(statistics.mean(e2e_times))
+    clocks = sampler.summary()
+
+    api.lib.fdy_members_free(members)
+    api.lib.fdy_store_free(store)
+    api.lib.fdy_device_close(dev)
+
+    if grank != 0:
+        if gworld > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = hbm_peak()
+    achieved = alg["total"] / (kernel_ms * 1e-3) / 1e9
+    prof = os.path.join(ROOT, "profiles", "materialize_ncu_summary.json")
+    traffic = None
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    bd = {k: statistics.mean(b[k] for b in breakdowns) for k in breakdowns[0]} if breakdowns else {}
+    driver_bound = bd.get("restore_ms", 0) + bd.get("build_ms", 0) + bd.get("instantiate_ms", 0)
+
+    # ---------------- CPU baseline: the reference itself, rank 0, N=1 ----------------
+    cpu = None
+    if not args.no_cpu_baseline and gworld == 1:
+        lanes = os.cpu_count() or 1
+        ref = reference_load_ms(plain, wrank, TP_WORLD, lanes, 5)
+        refm = reference_materialize_ms(plain, wrank, TP_WORLD, lanes, 5)
+        if ref is not None:
+            cpu = {"value": ref["mean_ms"], "unit": "ms", "cores": lanes, "kind": "reference",
+                   "sample": "reference load() of the same graph set (rank 0 of 8), 5 reps after 1 warm-up",
+                   "reference_materialize_ms": refm["mean_ms"] if refm else None,
+                   "reference_integrity_ms": refm["integrity_best_ms"] if refm else None}
+        else:
+            port = oracle_port_ms(plain, wrank, TP_WORLD, lanes, 3)
+            cpu = {"value": port["mean_ms"], "unit": "ms", "cores": lanes, "kind": "port",
+                   "sample": "oracle/foundry_oracle.c materialization of every member, 3 reps"}
+
+    graphs = hdr["n_members"]
+    line = {
+        "metric": "graph-set materialization ms (cold start); relocation GB/s vs HBM peak",
+        "value": kernel_ms_max,
+        "unit": "ms",
+        "n_gpus": gworld,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": kernel_ms_max,
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic",
+        "config": {
+            "workload": args.workload + "~ tier-R decode graph set, TP8: rank %d of 8 per GPU" % wrank,
+            "graphs": graphs, "nodes": hdr["total_nodes"], "templates": hdr["n_groups"],
+            "store_bytes": len(blob), "member_image_bytes": hdr["members_image_bytes"],
+            "relocation_delta": delta, "parallelism": "replicas (one TP rank per GPU)",
+            "l2": "flushed between timed steps (256 MiB memset, outside the events)",
+        },
+        "graphs_per_s": gworld * graphs / (kernel_ms_max * 1e-3),
+        "nodes_per_s": gworld * hdr["total_nodes"] / (kernel_ms_max * 1e-3),
+        "relocation_gbps": achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes": alg["total"], "kernel": "fdy_materialize_kernel"},
+        "e2e": {"value": e2e_ms, "unit": "ms",
+                "h2d_bytes_per_step": int(bd.get("h2d_bytes", 0)),
+                "d2h_bytes_per_step": int(bd.get("d2h_bytes", 0)) + len(trace),
+                "steps": args.e2e_steps, "api": "paper_2604_06664_b200.load(...).replay(1)",
+                "driver_bound_ms": driver_bound,
+                "excluding_driver_bound_ms": e2e_ms - driver_bound,
+                "breakdown": {k: v for k, v in bd.items() if k.endswith("_ms")}},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "gpu_launches": args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    if gworld > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -21,8 +21,11 @@
 //   time-load <archive> <rank> <world> <lanes> <reps> [replay]
 //        best-of-reps wall time of foundry::load (pipeline.cpp:447-557),
 //        optionally followed by serve+replay of every batch; prints JSON.
+//   time-materialize <archive> <rank> <world> <lanes> <reps>
+//        integrity CRC of every file + PrepareFn of every member, timed.
 //   crc <file>   CRC-64/XZ (hash.cpp:53-69) of a file, hex.
 //   diff <a.fndg> <b.fndg>   reference diff() text per graph pair.
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -152,6 +155,63 @@ static int cmd_time_load(int argc, char** argv) {
     return 0;
 }
 
+// time-materialize <archive> <rank> <world> <lanes> <reps>
+//   the reference's share of LOAD that the GPU path replaces: the integrity
+//   CRC of every manifest-listed file, single-threaded as in
+//   verify_archive_integrity (pipeline.cpp:411-417), then the PrepareFn of
+//   every member (parse_graph_at + apply_rank_patches, pipeline.cpp:506-514)
+//   on `lanes` threads like the prepare lanes (templater.cpp:102-130).
+static int cmd_time_materialize(int argc, char** argv) {
+    if (argc < 7) return usage();
+    const fs::path archive = argv[2];
+    const uint32_t rank = static_cast<uint32_t>(std::stoul(argv[3]));
+    const uint32_t world = static_cast<uint32_t>(std::stoul(argv[4]));
+    const unsigned lanes = static_cast<unsigned>(std::stoul(argv[5]));
+    const int reps = std::stoi(argv[6]);
+    using clock = std::chrono::steady_clock;
+    double best = 1e300, total = 0.0, crc_best = 1e300;
+    for (int i = 0; i < reps + 1; ++i) {
+        const auto t0 = clock::now();
+        ArchivePaths paths{archive};
+        const auto mb = read_file(paths.manifest());
+        const Manifest m = parse_manifest(std::string(mb.begin(), mb.end()));
+        for (const auto& [rel, digest] : m.file_digests) {
+            if (crc64(read_file(archive / rel)) != digest) {
+                std::fprintf(stderr, "integrity check failed for %s\n", rel.c_str());
+                return 3;
+            }
+        }
+        const auto t1 = clock::now();
+        const PatchTable table = parse_patch_table(read_file(paths.patch_table()));
+        const auto graphs_bin = read_file(paths.graphs());
+        const auto locs = parse_graph_locators(graphs_bin);
+        std::atomic<size_t> next{0};
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < std::max(1u, lanes); ++t)
+            pool.emplace_back([&] {
+                for (size_t k; (k = next.fetch_add(1)) < locs.size();) {
+                    CapturedGraph g = parse_graph_at(graphs_bin, locs[k]);
+                    auto it = table.per_graph.find(locs[k].label);
+                    if (it != table.per_graph.end())
+                        apply_rank_patches(g, it->second, m.comm_real_hash, rank, world);
+                }
+            });
+        for (auto& t : pool) t.join();
+        const auto t2 = clock::now();
+        const double ms = std::chrono::duration<double, std::milli>(t2 - t0).count();
+        const double crc_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        if (i > 0) {
+            best = std::min(best, ms);
+            crc_best = std::min(crc_best, crc_ms);
+            total += ms;
+        }
+    }
+    std::printf("{\"best_ms\": %.6f, \"mean_ms\": %.6f, \"integrity_best_ms\": %.6f, \"reps\": %d, "
+                "\"lanes\": %u, \"hw_threads\": %u}\n",
+                best, total / reps, crc_best, reps, lanes, std::thread::hardware_concurrency());
+    return 0;
+}
+
 static int cmd_crc(int argc, char** argv) {
     if (argc < 3) return usage();
     std::printf("%s\n", to_hex(crc64(read_file(argv[2]))).c_str());
@@ -176,6 +236,7 @@ int main(int argc, char** argv) {
         if (cmd == "prepare") return cmd_prepare(argc, argv);
         if (cmd == "replay") return cmd_replay(argc, argv);
         if (cmd == "time-load") return cmd_time_load(argc, argv);
+        if (cmd == "time-materialize") return cmd_time_materialize(argc, argv);
         if (cmd == "crc") return cmd_crc(argc, argv);
         if (cmd == "diff") return cmd_diff(argc, argv);
     } catch (const Error& e) {

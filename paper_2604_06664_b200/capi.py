@@ -1,0 +1,168 @@
+"""ctypes binding of the C-ABI (include/foundry_b200.h).
+
+This is the binding a foreign host would write (INTEGRATION.md shows the same
+for cgo / JNI); bench.py uses it to drive the kernel layer directly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import struct
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfoundry_b200.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "foundry_b200.h")
+
+
+class MaterializeDesc(ctypes.Structure):
+    _fields_ = [
+        ("rank", ctypes.c_uint32),
+        ("world", ctypes.c_uint32),
+        ("new_base", ctypes.c_uint64),
+        ("values", ctypes.POINTER(ctypes.c_uint64)),
+        ("n_values", ctypes.c_uint32),
+        ("grid", ctypes.c_int32),
+    ]
+
+
+class LoadOptions(ctypes.Structure):
+    _fields_ = [
+        ("rank", ctypes.c_uint32),
+        ("world", ctypes.c_uint32),
+        ("preallocate", ctypes.c_int32),
+        ("prepare_lanes", ctypes.c_uint32),
+        ("device", ctypes.c_int32),
+        ("relocate", ctypes.c_int32),
+        ("skip_binary_restore", ctypes.c_int32),
+        ("skip_device_init", ctypes.c_int32),
+        ("base_shift_granules", ctypes.c_int64),
+        ("extra_prewindow_alloc", ctypes.c_int32),
+    ]
+
+
+class CApiError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+def declared_functions(header: str = HEADER) -> list[str]:
+    """Every fdy_* function the public header declares."""
+    text = open(header).read()
+    return sorted(set(re.findall(r"\b(fdy_[a-z0-9_]+)\s*\(", text)))
+
+
+class CApi:
+    def __init__(self, path: str = LIB_PATH):
+        self.lib = ctypes.CDLL(path)
+        L = self.lib
+        P = ctypes.c_void_p
+        L.fdy_last_error.restype = ctypes.c_char_p
+        L.fdy_version.restype = ctypes.c_char_p
+        L.fdy_device_count.restype = ctypes.c_int
+        L.fdy_device_open.argtypes = [ctypes.c_int, ctypes.POINTER(P)]
+        L.fdy_device_close.argtypes = [P]
+        L.fdy_sync.argtypes = [P]
+        L.fdy_store_upload.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(P)]
+        L.fdy_store_fanout.argtypes = [P, P, ctypes.POINTER(P)]
+        L.fdy_store_free.argtypes = [P]
+        L.fdy_store_members_bytes.argtypes = [P]
+        L.fdy_store_members_bytes.restype = ctypes.c_size_t
+        L.fdy_materialize.argtypes = [P, P, ctypes.POINTER(MaterializeDesc), ctypes.POINTER(P),
+                                      ctypes.POINTER(ctypes.c_float)]
+        L.fdy_materialize_into.argtypes = [P, P, ctypes.POINTER(MaterializeDesc), P,
+                                           ctypes.POINTER(ctypes.c_float)]
+        L.fdy_members_bytes.argtypes = [P]
+        L.fdy_members_bytes.restype = ctypes.c_size_t
+        L.fdy_members_download.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t]
+        L.fdy_members_free.argtypes = [P]
+        L.fdy_crc64_segments.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t,
+                                         ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
+                                         ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint64),
+                                         ctypes.POINTER(ctypes.c_float)]
+        L.fdy_load_options_init.argtypes = [ctypes.POINTER(LoadOptions)]
+        L.fdy_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(LoadOptions), ctypes.POINTER(P)]
+        L.fdy_serving_replay.argtypes = [P, ctypes.c_uint32, ctypes.c_char_p, ctypes.c_size_t,
+                                         ctypes.POINTER(ctypes.c_size_t)]
+        L.fdy_serving_close.argtypes = [P]
+
+    def check(self, rc: int) -> None:
+        if rc:
+            raise CApiError(rc, self.lib.fdy_last_error().decode())
+
+    # ---- kernel layer
+    def device_open(self, ordinal: int = 0):
+        h = ctypes.c_void_p()
+        self.check(self.lib.fdy_device_open(ordinal, ctypes.byref(h)))
+        return h
+
+    def store_upload(self, dev, blob: bytes):
+        h = ctypes.c_void_p()
+        self.check(self.lib.fdy_store_upload(dev, blob, len(blob), ctypes.byref(h)))
+        return h
+
+    def materialize(self, dev, store, rank: int, world: int, new_base: int = 0, members=None,
+                    values=()):
+        desc = MaterializeDesc(rank, world, new_base, None, 0, 0)
+        if values:
+            arr = (ctypes.c_uint64 * len(values))(*values)
+            desc.values = arr
+            desc.n_values = len(values)
+        ms = ctypes.c_float()
+        if members is None:
+            members = ctypes.c_void_p()
+            self.check(self.lib.fdy_materialize(dev, store, ctypes.byref(desc), ctypes.byref(members),
+                                                ctypes.byref(ms)))
+        else:
+            self.check(self.lib.fdy_materialize_into(dev, store, ctypes.byref(desc), members,
+                                                     ctypes.byref(ms)))
+        return members, ms.value
+
+    def members_download(self, members) -> bytes:
+        n = self.lib.fdy_members_bytes(members)
+        buf = ctypes.create_string_buffer(n)
+        self.check(self.lib.fdy_members_download(members, buf, 0, n))
+        return buf.raw
+
+    def crc64(self, dev, data: bytes, ranges):
+        n = len(ranges)
+        offs = (ctypes.c_uint64 * n)(*[r[0] for r in ranges])
+        lens = (ctypes.c_uint64 * n)(*[r[1] for r in ranges])
+        out = (ctypes.c_uint64 * n)()
+        ms = ctypes.c_float()
+        self.check(self.lib.fdy_crc64_segments(dev, data, len(data), offs, lens, n, out, ctypes.byref(ms)))
+        return list(out), ms.value
+
+
+# ---- FNDT store header (foundry/store_format.h) -----------------------------
+
+SECTIONS = ["groups", "timages", "cmeta", "members", "tiles", "didx", "dmeta", "ddata", "rops",
+            "kernels", "nodeattrs", "edges", "strings"]
+
+
+def store_header(blob: bytes) -> dict:
+    (magic, version, flags, header_bytes, n_groups, n_members, n_kernels, n_tiles, tile_chunks,
+     n_diffs, n_rank_ops) = struct.unpack_from("<4sHHIIIIIIII", blob, 0)
+    assert magic == b"FNDT", "not a template store"
+    u64 = struct.unpack_from("<7Q", blob, 40)
+    secs = struct.unpack_from("<%dQ" % (2 * len(SECTIONS)), blob, 96)
+    return {
+        "version": version, "n_groups": n_groups, "n_members": n_members, "n_kernels": n_kernels,
+        "n_tiles": n_tiles, "tile_chunks": tile_chunks, "n_diffs": n_diffs, "n_rank_ops": n_rank_ops,
+        "source_graphs_crc": u64[0], "source_patch_crc": u64[1], "old_base": u64[2],
+        "final_offset": u64[3], "real_comm_hash": u64[4], "members_image_bytes": u64[5],
+        "total_nodes": u64[6],
+        "sec": {n: (secs[2 * i], secs[2 * i + 1]) for i, n in enumerate(SECTIONS)},
+    }
+
+
+def algorithmic_bytes(h: dict) -> dict:
+    """Compulsory HBM traffic of one fused K2+K1+K3 launch:
+    templates + chunk meta read once, every diff / rank op / tile read once,
+    every member image written once."""
+    s = h["sec"]
+    read = (s["timages"][1] + s["cmeta"][1] + s["didx"][1] + s["dmeta"][1] + s["ddata"][1]
+            + s["rops"][1] + s["tiles"][1])
+    write = h["members_image_bytes"]
+    return {"read": read, "write": write, "total": read + write}
