@@ -115,6 +115,27 @@ int fdy_crc64_segments(fdy_device* dev, const void* host, size_t bytes,
                        const uint64_t* offsets, const uint64_t* lengths, uint32_t n,
                        uint64_t* digests, float* kernel_ms);
 
+/* The whole materialization path in one call — the GPU-native replacement of
+ * the reference's verify_archive_integrity (pipeline.cpp:411-417) followed by
+ * the PrepareFn over every member (pipeline.cpp:506-514): archive files ->
+ * pinned staging -> HBM -> GPU CRC of every file -> fused K2+K1+K3 for
+ * desc->(rank, world, new_base) -> member images (store_format.h layout)
+ * copied to host_out. host_out may be NULL (images stay in HBM only);
+ * out_len receives the image bytes. */
+typedef struct {
+    double total_ms, read_ms, integrity_ms, materialize_ms, d2h_ms;
+    float crc_kernel_ms, kernel_ms;
+    uint64_t h2d_bytes, d2h_bytes, member_bytes, graphs, nodes;
+} fdy_prepare_timings;
+
+int fdy_prepare_archive(fdy_device* dev, const char* archive, const fdy_materialize_desc* desc,
+                        uint32_t lanes, void* host_out, size_t cap, size_t* out_len,
+                        fdy_prepare_timings* timings);
+
+/* Pinned host memory usable as host_out (released with fdy_host_free). */
+void* fdy_host_alloc(fdy_device* dev, size_t bytes);
+void fdy_host_free(void* p);
+
 /* ---------------------------------------------------------------- session API */
 typedef struct {
     uint32_t rank;           /* LoadOptions.rank */

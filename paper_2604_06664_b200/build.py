@@ -44,6 +44,7 @@ HOST_SRCS = [
     "host/trace_module.cpp",
     "host/driver_api.cpp",
     "host/gpu_context.cpp",
+    "host/staging.cpp",
     "host/pipeline.cpp",
     "host/tooling.cpp",
     "capi/capi_misc.cpp",

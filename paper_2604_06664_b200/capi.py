@@ -41,6 +41,26 @@ class LoadOptions(ctypes.Structure):
     ]
 
 
+class PrepareTimings(ctypes.Structure):
+    _fields_ = [
+        ("total_ms", ctypes.c_double),
+        ("read_ms", ctypes.c_double),
+        ("integrity_ms", ctypes.c_double),
+        ("materialize_ms", ctypes.c_double),
+        ("d2h_ms", ctypes.c_double),
+        ("crc_kernel_ms", ctypes.c_float),
+        ("kernel_ms", ctypes.c_float),
+        ("h2d_bytes", ctypes.c_uint64),
+        ("d2h_bytes", ctypes.c_uint64),
+        ("member_bytes", ctypes.c_uint64),
+        ("graphs", ctypes.c_uint64),
+        ("nodes", ctypes.c_uint64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 class CApiError(RuntimeError):
     def __init__(self, code: int, message: str):
         super().__init__(message)
@@ -81,6 +101,12 @@ class CApi:
                                          ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
                                          ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint64),
                                          ctypes.POINTER(ctypes.c_float)]
+        L.fdy_prepare_archive.argtypes = [P, ctypes.c_char_p, ctypes.POINTER(MaterializeDesc),
+                                          ctypes.c_uint32, ctypes.c_void_p, ctypes.c_size_t,
+                                          ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(PrepareTimings)]
+        L.fdy_host_alloc.argtypes = [P, ctypes.c_size_t]
+        L.fdy_host_alloc.restype = ctypes.c_void_p
+        L.fdy_host_free.argtypes = [ctypes.c_void_p]
         L.fdy_load_options_init.argtypes = [ctypes.POINTER(LoadOptions)]
         L.fdy_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(LoadOptions), ctypes.POINTER(P)]
         L.fdy_serving_replay.argtypes = [P, ctypes.c_uint32, ctypes.c_char_p, ctypes.c_size_t,
@@ -118,6 +144,23 @@ class CApi:
             self.check(self.lib.fdy_materialize_into(dev, store, ctypes.byref(desc), members,
                                                      ctypes.byref(ms)))
         return members, ms.value
+
+    def prepare_archive(self, dev, archive: str, rank: int, world: int, new_base: int = 0,
+                        lanes: int = 0, host_out=None, cap: int = 0) -> dict:
+        """The materialization path in one C-ABI call (fdy_prepare_archive)."""
+        desc = MaterializeDesc(rank, world, new_base, None, 0, 0)
+        n = ctypes.c_size_t()
+        t = PrepareTimings()
+        self.check(self.lib.fdy_prepare_archive(dev, archive.encode(), ctypes.byref(desc),
+                                                lanes or (os.cpu_count() or 4), host_out, cap,
+                                                ctypes.byref(n), ctypes.byref(t)))
+        return t.as_dict()
+
+    def host_alloc(self, dev, nbytes: int):
+        p = self.lib.fdy_host_alloc(dev, nbytes)
+        if not p:
+            raise CApiError(1, self.lib.fdy_last_error().decode())
+        return p
 
     def members_download(self, members) -> bytes:
         n = self.lib.fdy_members_bytes(members)

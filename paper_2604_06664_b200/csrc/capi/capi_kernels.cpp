@@ -7,6 +7,7 @@
 
 #include "capi_common.hpp"
 #include "foundry/device.hpp"
+#include "foundry/staging.hpp"
 #include "foundry_b200.h"
 
 using namespace foundry;
@@ -156,6 +157,45 @@ int fdy_members_download(fdy_members* m, void* host_dst, size_t offset, size_t b
 }
 
 void fdy_members_free(fdy_members* m) { delete m; }
+
+int fdy_prepare_archive(fdy_device* dev, const char* archive, const fdy_materialize_desc* desc,
+                        uint32_t lanes, void* host_out, size_t cap, size_t* out_len,
+                        fdy_prepare_timings* timings) {
+    return fdy_guard([&] {
+        require(dev && archive && desc, Errc::invalid_argument, "fdy_prepare_archive: null argument");
+        ArchiveMaterializeTimings t;
+        const uint64_t n = materialize_archive(*dev->dev, archive, desc->rank, desc->world,
+                                               desc->new_base, lanes ? lanes : 4, host_out, cap, &t);
+        if (out_len) *out_len = n;
+        if (timings) {
+            timings->total_ms = t.total_ms;
+            timings->read_ms = t.read_ms;
+            timings->integrity_ms = t.integrity_ms;
+            timings->materialize_ms = t.materialize_ms;
+            timings->d2h_ms = t.d2h_ms;
+            timings->crc_kernel_ms = t.crc_kernel_ms;
+            timings->kernel_ms = t.kernel_ms;
+            timings->h2d_bytes = t.h2d_bytes;
+            timings->d2h_bytes = t.d2h_bytes;
+            timings->member_bytes = t.member_bytes;
+            timings->graphs = t.graphs;
+            timings->nodes = t.nodes;
+        }
+    });
+}
+
+void* fdy_host_alloc(fdy_device* dev, size_t bytes) {
+    void* p = nullptr;
+    fdy_guard([&] {
+        require(dev != nullptr, Errc::invalid_argument, "fdy_host_alloc: null device");
+        p = dev->dev->alloc_host_pinned(bytes);
+    });
+    return p;
+}
+
+void fdy_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
 
 int fdy_crc64_segments(fdy_device* dev, const void* host, size_t bytes, const uint64_t* offsets,
                        const uint64_t* lengths, uint32_t n, uint64_t* digests, float* kernel_ms) {

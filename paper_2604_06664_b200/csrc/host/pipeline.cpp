@@ -11,12 +11,14 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <mutex>
 #include <thread>
 
 #include <cuda_runtime.h>
 
 #include "foundry/bytes.hpp"
 #include "foundry/parallel.hpp"
+#include "foundry/staging.hpp"
 #include "foundry/template_store.hpp"
 #include "foundry/trace_module.hpp"
 #include "foundry/workload.hpp"
@@ -39,30 +41,6 @@ void debug_phase(const char* what) {
     static const bool on = std::getenv("FOUNDRY_DEBUG") != nullptr;
     if (on) std::fprintf(stderr, "[foundry] %s\n", what);
 }
-constexpr size_t kStageAlign = 256;
-constexpr size_t kReadChunk = 8ull << 20;
-
-struct FileSeg {
-    std::string rel;
-    uint64_t offset = 0;  // in staging
-    uint64_t length = 0;
-};
-
-void read_range(const fs::path& p, uint8_t* dst, uint64_t off, uint64_t len) {
-    const int fd = ::open(p.c_str(), O_RDONLY | O_CLOEXEC);
-    require(fd >= 0, Errc::archive_corruption, "cannot open " + p.string());
-    uint64_t done = 0;
-    while (done < len) {
-        const ssize_t n = ::pread(fd, dst + done, len - done, static_cast<off_t>(off + done));
-        if (n <= 0) {
-            ::close(fd);
-            raise(Errc::archive_corruption, "short read on " + p.string());
-        }
-        done += static_cast<uint64_t>(n);
-    }
-    ::close(fd);
-}
-
 uint64_t rd64(const uint8_t* p) {
     uint64_t v;
     std::memcpy(&v, p, 8);
@@ -81,17 +59,18 @@ struct ServingContext::Impl {
     Manifest manifest;
     Catalog catalog;
 
-    PinnedBuffer staging;
-    DeviceBuffer d_staging;
-    std::map<std::string, FileSeg> files;
+    std::unique_ptr<StagedArchive> staged;  // every listed file, in pinned host memory and HBM
 
     std::vector<uint8_t> inline_store;  // reference archives without templates.fdt
-    DeviceBuffer d_inline_store;
     std::span<const uint8_t> store_host;
     std::unique_ptr<StoreView> view;
     DeviceStore dstore;
-    DeviceBuffer d_members;
-    PinnedBuffer h_members;
+    DeviceBuffer d_members;  // every member image, materialized in HBM
+    // host copies of member images, fetched on first use (the representatives
+    // at LOAD; other members when served) — parameters stay resident in HBM
+    std::unique_ptr<uint8_t[]> h_members;
+    std::vector<uint8_t> h_present;
+    mutable std::mutex fetch_mu;
     std::vector<int32_t> kernel_of;  // store kernel index -> GpuContext kernel (or -1)
 
     struct Group {
@@ -103,6 +82,7 @@ struct ServingContext::Impl {
     std::vector<Group> groups;
     std::vector<uint32_t> labels;
     uint64_t lane_acquisitions = 0;
+    std::mutex stats_mu;
     CUcontext cu_ctx = nullptr;
 
     ~Impl() {
@@ -118,13 +98,23 @@ struct ServingContext::Impl {
         ctx.reset();  // libraries, then VA (destroy order: execs -> graphs -> libraries -> VA)
     }
 
-    std::span<const uint8_t> file_host(const std::string& rel) const {
-        auto it = files.find(rel);
-        require(it != files.end(), Errc::archive_corruption, "archive has no " + rel);
-        return {staging.data() + it->second.offset, it->second.length};
-    }
+    std::span<const uint8_t> file_host(const std::string& rel) const { return staged->host(rel); }
 
-    const uint8_t* member_image(uint32_t m) const { return h_members.data() + view->member(m).out_off; }
+    // Host view of member m's image; copied out of HBM on first use.
+    const uint8_t* member_image(uint32_t m) const {
+        const fdt_member& M = view->member(m);
+        uint8_t* dst = h_members.get() + M.out_off;
+        std::lock_guard lock(fetch_mu);
+        if (!h_present[m]) {
+            dev->make_current();
+            cuda_check(cudaMemcpy(dst, d_members.data() + M.out_off, view->group(M.group).image_bytes,
+                                  cudaMemcpyDeviceToHost),
+                       "cudaMemcpy(member image D2H)");
+            const_cast<Impl*>(this)->h_present[m] = 1;
+            const_cast<Impl*>(this)->t.d2h_bytes += view->group(M.group).image_bytes;
+        }
+        return dst;
+    }
 
     uint32_t member_for(uint32_t batch) const {
         const int64_t m = view->member_of(batch);
@@ -142,7 +132,6 @@ struct ServingContext::Impl {
         return *ctx->kernel_by_entry_id(static_cast<uint32_t>(k));
     }
 
-    void stage_files(const fs::path& root);
     void restore_binaries();
     void build_group(uint32_t g);
     uint64_t build_graph_for(uint32_t g, uint32_t m, CUgraph& graph, std::vector<CUgraphNode>& nodes);
@@ -155,41 +144,6 @@ struct ServingContext::Impl {
     LaunchTrace replay(uint32_t batch);
 };
 
-// ---------------------------------------------------------------- staging
-
-void ServingContext::Impl::stage_files(const fs::path& root) {
-    uint64_t total = 0;
-    for (const auto& [rel, digest] : manifest.file_digests) {
-        (void)digest;
-        const fs::path p = root / rel;
-        std::error_code ec;
-        const uint64_t n = fs::file_size(p, ec);
-        require(!ec, Errc::archive_corruption, "cannot open " + p.string());
-        files[rel] = {rel, total, n};
-        total += (n + kStageAlign - 1) / kStageAlign * kStageAlign;
-    }
-    staging = PinnedBuffer(*dev, std::max<uint64_t>(total, 16));
-    struct Piece {
-        const FileSeg* f;
-        uint64_t off, len;
-    };
-    std::vector<Piece> pieces;
-    for (const auto& [rel, f] : files)
-        for (uint64_t o = 0; o < f.length || (o == 0 && f.length == 0); o += kReadChunk) {
-            pieces.push_back({&f, o, std::min<uint64_t>(kReadChunk, f.length - o)});
-            if (f.length == 0) break;
-        }
-    parallel_for(pieces.size(), std::max(1u, opts.prepare_lanes), [&](size_t i) {
-        const Piece& pc = pieces[i];
-        if (pc.len) read_range(root / pc.f->rel, staging.data() + pc.f->offset + pc.off, pc.off, pc.len);
-    });
-    d_staging = DeviceBuffer(*dev, std::max<uint64_t>(total, 16));
-    cuda_check(cudaMemcpyAsync(d_staging.data(), staging.data(), total, cudaMemcpyHostToDevice,
-                               dev->stream()),
-               "cudaMemcpyAsync(archive H2D)");
-    t.h2d_bytes += total;
-}
-
 // ---------------------------------------------------------------- restore
 
 void ServingContext::Impl::restore_binaries() {
@@ -201,7 +155,7 @@ void ServingContext::Impl::restore_binaries() {
         std::vector<uint8_t> fetched;
         std::span<const uint8_t> payload;
         uint64_t digest = 0;
-        if (files.count(rel)) {
+        if (staged->has(rel)) {
             payload = file_host(rel);
             digest = manifest.file_digests.at(rel);  // verified on the GPU by stage 2
         } else {
@@ -217,7 +171,7 @@ void ServingContext::Impl::restore_binaries() {
         const std::string crel = "binaries/" + hex16(hash) + ".sm_100a.cubin";
         std::vector<uint8_t> built;
         std::span<const uint8_t> cubin;
-        if (files.count(crel)) {
+        if (staged->has(crel)) {
             cubin = file_host(crel);
         } else {  // reference-written archive: compile the trace module now
             built = compile_ptx_to_cubin(trace_module_ptx(image, ord, rec.needs_device_init));
@@ -421,15 +375,18 @@ void ServingContext::Impl::build_group(uint32_t gi) {
                             a.sched_policy || a.sync_default || a.sync_remote || !a.attr_query))
             ctx->c_set_attr.fetch_add(1);
     }
-    ++lane_acquisitions;
     const double build = ms_since(t0);
     const auto t1 = Clock::now();
     cu_check(api.cuGraphInstantiate(&grp.exec, grp.graph, 0), "cuGraphInstantiate");
     debug_phase("instantiated group");
-    ++lane_acquisitions;
     ctx->c_instantiate.fetch_add(1);
-    t.build_ms += build;
-    t.instantiate_ms += ms_since(t1);
+    const double inst = ms_since(t1);
+    {
+        std::lock_guard lock(stats_mu);  // builder lanes may run concurrently
+        lane_acquisitions += 2;
+        t.build_ms += build;
+        t.instantiate_ms += inst;
+    }
     grp.applied = m;
 }
 
@@ -655,33 +612,19 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     cu_check(driver().cuCtxGetCurrent(&I.cu_ctx), "cuCtxGetCurrent");
     I.ctx = std::make_unique<GpuContext>(device);
 
-    // 1. stage every listed file into HBM, 2. verify digests on the GPU
-    t0 = Clock::now();
+    // 1. stage every listed file into HBM (reads overlap the DMA),
+    // 2. verify every digest with one GPU CRC launch
+    StageTimings st;
     try {
-        I.stage_files(archive);
+        I.staged = std::make_unique<StagedArchive>(device, archive, I.manifest, opts.prepare_lanes, &st);
+        I.staged->verify(I.manifest, &st);
     } catch (const Error&) {
         rethrow_in_step("archive integrity");
     }
-    I.t.stage_ms = ms_since(t0);
-    debug_phase("stage done");
-    t0 = Clock::now();
-    {
-        std::vector<Segment> segs;
-        std::vector<const std::string*> names;
-        for (const auto& [rel, f] : I.files) {
-            segs.push_back({f.offset, f.length});
-            names.push_back(&f.rel);
-        }
-        const auto digests = crc64_device(device, I.d_staging.data(), segs, &I.t.crc_kernel_ms);
-        try {
-            for (size_t i = 0; i < names.size(); ++i)
-                require(digests[i] == I.manifest.file_digests.at(*names[i]), Errc::archive_corruption,
-                        "integrity check failed for " + *names[i]);
-        } catch (const Error&) {
-            rethrow_in_step("archive integrity");
-        }
-    }
-    I.t.integrity_ms = ms_since(t0);
+    I.t.stage_ms = st.read_ms;
+    I.t.integrity_ms = st.integrity_ms;
+    I.t.crc_kernel_ms = st.crc_kernel_ms;
+    I.t.h2d_bytes += st.h2d_bytes;
     debug_phase("integrity done");
 
     const WorkloadSpec spec = WorkloadSpec::parse_text(I.manifest.workload_text);
@@ -693,11 +636,11 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
 
     // template store: packed offline (templates.fdt) or, for a reference-written
     // archive, packed now from graphs.bin + patch.bin
-    if (I.files.count("templates.fdt")) {
-        const FileSeg& f = I.files.at("templates.fdt");
+    if (I.staged->has("templates.fdt")) {
         I.store_host = I.file_host("templates.fdt");
         I.view = std::make_unique<StoreView>(I.store_host);
-        I.dstore = adopt_store(device, I.d_staging.data() + f.offset, f.length, I.view->header());
+        I.dstore = adopt_store(device, I.staged->device("templates.fdt"), I.store_host.size(),
+                               I.view->header());
     } else {
         try {
             I.inline_store = pack_template_store(I.file_host("graphs.bin"), I.file_host("patch.bin"),
@@ -754,29 +697,30 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     req.new_base = (opts.relocate && new_base != I.manifest.allocator.base) ? new_base : 0;
     I.t.relocation_delta = req.new_base ? req.new_base - I.manifest.allocator.base : 0;
     I.d_members = DeviceBuffer(device, std::max<uint64_t>(H.members_image_bytes, 16));
-    I.h_members = PinnedBuffer(device, std::max<uint64_t>(H.members_image_bytes, 16));
+    I.h_members.reset(new uint8_t[std::max<uint64_t>(H.members_image_bytes, 16)]);
+    I.h_present.assign(H.n_members, 0);
     MaterializeTiming mt;
     launch_materialize(device, I.dstore, req, I.d_members.data(), &mt);
     I.t.materialize_kernel_ms = mt.kernel_ms;
     I.t.materialize_ms = ms_since(t0);
     debug_phase("materialize done");
     t0 = Clock::now();
-    cuda_check(cudaMemcpyAsync(I.h_members.data(), I.d_members.data(), H.members_image_bytes,
-                               cudaMemcpyDeviceToHost, device.stream()),
-               "cudaMemcpyAsync(member images D2H)");
-    cuda_check(cudaStreamSynchronize(device.stream()), "cudaStreamSynchronize");
+    for (uint32_t g = 0; g < H.n_groups; ++g) I.member_image(I.view->group(g).first_member);  // templates
     I.t.download_ms = ms_since(t0);
     debug_phase("download done");
-    I.t.d2h_bytes += H.members_image_bytes;
     I.t.member_bytes = H.members_image_bytes;
     I.t.store_bytes = I.dstore.bytes;
 
     // 6. template construction (builder thread) || foreground init + window replay
     I.groups.resize(H.n_groups);
     std::exception_ptr builder_error, foreground_error;
+    // builder lanes: templates are independent graphs; FOUNDRY_BUILD_LANES
+    // host threads construct + instantiate them (1 = the reference's single lane)
+    unsigned build_lanes = 1;
+    if (const char* env = std::getenv("FOUNDRY_BUILD_LANES")) build_lanes = std::max(1, std::atoi(env));
     std::thread builder([&] {
         try {
-            for (uint32_t g = 0; g < H.n_groups; ++g) I.build_group(g);
+            parallel_for(H.n_groups, build_lanes, [&](size_t g) { I.build_group(static_cast<uint32_t>(g)); });
         } catch (...) {
             builder_error = std::current_exception();
         }
