@@ -52,6 +52,7 @@ def parse_args():
     p.add_argument("--workload", default="qwen3-235b-a22b")
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--load-steps", type=int, default=2)
+    p.add_argument("--skip-load", action="store_true", help="skip the full-LOAD section (profiling)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -290,11 +291,12 @@ def main():
         api.lib.fdy_host_free(host_out)
 
         # ------- full LOAD through the Python API (adds driver-bound work) -------
-        load_times, breakdowns = [], []
-        h = foundry.load(archive, rank=wrank, world=TP_WORLD)  # warm-up (driver, page cache)
-        h.replay(1)
-        h.close()
-        for _ in range(args.load_steps):
+        load_times, breakdowns, trace = [], [], ""
+        if not args.skip_load:
+            h = foundry.load(archive, rank=wrank, world=TP_WORLD)  # warm-up (driver, page cache)
+            h.replay(1)
+            h.close()
+        for _ in range(0 if args.skip_load else args.load_steps):
             barrier()
             t0 = time.perf_counter()
             h = foundry.load(archive, rank=wrank, world=TP_WORLD)
@@ -302,7 +304,7 @@ def main():
             load_times.append((time.perf_counter() - t0) * 1e3)
             breakdowns.append(h.timings())
             h.close()
-        load_ms = reduce_max(statistics.mean(load_times))
+        load_ms = reduce_max(statistics.mean(load_times)) if load_times else None
     clocks = sampler.summary()
 
     api.lib.fdy_members_free(members)
@@ -381,7 +383,7 @@ def main():
                       "api": "paper_2604_06664_b200.load(archive, rank, world).replay(1)",
                       "driver_bound_ms": driver_bound,
                       "driver_bound": "cuLibraryLoadData x catalog + cuGraphAdd*/cuGraphInstantiate x templates",
-                      "excluding_driver_bound_ms": load_ms - driver_bound,
+                      "excluding_driver_bound_ms": (load_ms - driver_bound) if load_ms else None,
                       "h2d_bytes_per_step": int(bd.get("h2d_bytes", 0)),
                       "d2h_bytes_per_step": int(bd.get("d2h_bytes", 0)) + len(trace),
                       "breakdown": {k: v for k, v in bd.items() if k.endswith("_ms")}},
