@@ -53,6 +53,8 @@ def parse_args():
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--load-steps", type=int, default=2)
     p.add_argument("--skip-load", action="store_true", help="skip the full-LOAD section (profiling)")
+    p.add_argument("--fanout", choices=["host", "ipc"], default="ipc",
+                   help="N>1: how the store reaches every GPU (ipc = GPU0 -> peers over NVLink)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -215,28 +217,18 @@ def main():
         return
 
     import torch
-    import torch.distributed as dist
 
     import paper_2604_06664_b200 as foundry
     from paper_2604_06664_b200 import capi
+    from paper_2604_06664_b200.multirank import RankGroup, distribute_store, tp_rank
 
     torch.cuda.set_device(local)
-    if gworld > 1:
-        dist.init_process_group("nccl", init_method="env://")
-
-    def barrier():
-        if gworld > 1:
-            dist.barrier()
-
-    def reduce_max(x: float) -> float:
-        if gworld == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    group = RankGroup(grank, gworld, local)
+    group.init("nccl")
+    barrier, reduce_max = group.barrier, group.max
 
     archive, plain = prepare_archives(args.workload, grank, barrier)
-    wrank = grank % TP_WORLD
+    wrank = tp_rank(grank)
     with open(os.path.join(archive, "manifest")) as f:
         manifest = json.load(f)
     base = manifest["allocator"]["base"]
@@ -248,7 +240,9 @@ def main():
     # ---------------- device-resident materialization (value) ----------------
     api = capi.CApi()
     dev = api.device_open(local)
-    store = api.store_upload(dev, blob)
+    t_fan = time.perf_counter()
+    store = distribute_store(group, api, dev, blob, args.fanout)  # the one exchange step
+    fanout_ms = (time.perf_counter() - t_fan) * 1e3
     members, _ = api.materialize(dev, store, wrank, TP_WORLD, base + delta)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     for _ in range(args.warmup):
@@ -312,8 +306,7 @@ def main():
     api.lib.fdy_device_close(dev)
 
     if grank != 0:
-        if gworld > 1:
-            dist.destroy_process_group()
+        group.close()
         return
 
     peak, peak_src = hbm_peak()
@@ -390,10 +383,11 @@ def main():
         "cpu_baseline": cpu,
         "clocks": clocks,
         "gpu_launches": args.steps,
+        "fanout": {"mode": args.fanout if gworld > 1 else "none", "ms": fanout_ms,
+                   "store_bytes": len(blob)},
     }
     print(json.dumps(line), flush=True)
-    if gworld > 1:
-        dist.destroy_process_group()
+    group.close()
 
 
 if __name__ == "__main__":

@@ -85,6 +85,12 @@ int fdy_store_upload(fdy_device* dev, const void* host_blob, size_t bytes, fdy_s
 /* Copies a resident store to another device (peer copy over NVLink when the
  * devices can access each other; staged otherwise). */
 int fdy_store_fanout(const fdy_store* src, fdy_device* dst_dev, fdy_store** out);
+/* Cross-process fan-out (one process per GPU): the owner exports a CUDA IPC
+ * handle of its resident store; a peer process imports it, which pulls the
+ * bytes GPU->GPU (NVLink P2P) into its own HBM and closes the mapping. */
+int fdy_store_export(const fdy_store* store, unsigned char handle[64], uint64_t* bytes);
+int fdy_store_import(fdy_device* dev, const unsigned char handle[64], uint64_t bytes,
+                     fdy_store** out);
 void fdy_store_free(fdy_store* store);
 size_t fdy_store_members_bytes(const fdy_store* store);
 

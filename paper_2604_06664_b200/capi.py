@@ -87,6 +87,8 @@ class CApi:
         L.fdy_store_upload.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(P)]
         L.fdy_store_fanout.argtypes = [P, P, ctypes.POINTER(P)]
         L.fdy_store_free.argtypes = [P]
+        L.fdy_store_export.argtypes = [P, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64)]
+        L.fdy_store_import.argtypes = [P, ctypes.c_char_p, ctypes.c_uint64, ctypes.POINTER(P)]
         L.fdy_store_members_bytes.argtypes = [P]
         L.fdy_store_members_bytes.restype = ctypes.c_size_t
         L.fdy_materialize.argtypes = [P, P, ctypes.POINTER(MaterializeDesc), ctypes.POINTER(P),
@@ -126,6 +128,18 @@ class CApi:
     def store_upload(self, dev, blob: bytes):
         h = ctypes.c_void_p()
         self.check(self.lib.fdy_store_upload(dev, blob, len(blob), ctypes.byref(h)))
+        return h
+
+    def store_export(self, store) -> tuple[bytes, int]:
+        handle = ctypes.create_string_buffer(64)
+        n = ctypes.c_uint64()
+        self.check(self.lib.fdy_store_export(store, handle, ctypes.byref(n)))
+        return handle.raw, n.value
+
+    def store_import(self, dev, exported: tuple[bytes, int]):
+        handle, nbytes = exported
+        h = ctypes.c_void_p()
+        self.check(self.lib.fdy_store_import(dev, handle, nbytes, ctypes.byref(h)))
         return h
 
     def materialize(self, dev, store, rank: int, world: int, new_base: int = 0, members=None,

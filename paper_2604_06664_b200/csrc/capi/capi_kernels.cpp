@@ -88,6 +88,46 @@ int fdy_store_fanout(const fdy_store* src, fdy_device* dst_dev, fdy_store** out)
     });
 }
 
+int fdy_store_export(const fdy_store* store, unsigned char handle[64], uint64_t* bytes) {
+    return fdy_guard([&] {
+        require(store && handle && bytes, Errc::invalid_argument, "fdy_store_export: null argument");
+        require(store->store.blob.data() == store->store.data, Errc::invalid_argument,
+                "fdy_store_export: only stores uploaded with fdy_store_upload can be exported");
+        store->owner->dev->sync();  // the upload must have landed before a peer reads it
+        cudaIpcMemHandle_t h;
+        static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+        cuda_check(cudaIpcGetMemHandle(&h, const_cast<unsigned char*>(store->store.data)),
+                   "cudaIpcGetMemHandle");
+        std::memcpy(handle, &h, sizeof h);
+        *bytes = store->store.bytes;
+    });
+}
+
+int fdy_store_import(fdy_device* dev, const unsigned char handle[64], uint64_t bytes, fdy_store** out) {
+    return fdy_guard([&] {
+        require(dev && handle && out, Errc::invalid_argument, "fdy_store_import: null argument");
+        Device& d = *dev->dev;
+        d.make_current();
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        void* peer = nullptr;
+        cuda_check(cudaIpcOpenMemHandle(&peer, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        DeviceBuffer buf(d, bytes);
+        // GPU -> GPU pull; NVLink P2P between the two devices
+        const cudaError_t e = cudaMemcpyAsync(buf.data(), peer, bytes, cudaMemcpyDeviceToDevice, d.stream());
+        const cudaError_t s = e == cudaSuccess ? cudaStreamSynchronize(d.stream()) : e;
+        cudaIpcCloseMemHandle(peer);
+        cuda_check(s, "store fan-out copy");
+        fdt_header hdr;
+        cuda_check(cudaMemcpy(&hdr, buf.data(), sizeof hdr, cudaMemcpyDeviceToHost), "store header D2H");
+        auto o = std::make_unique<fdy_store>();
+        o->owner = dev;
+        o->store = adopt_store(d, buf.data(), bytes, hdr);
+        o->store.blob = std::move(buf);
+        *out = o.release();
+    });
+}
+
 void fdy_store_free(fdy_store* store) { delete store; }
 
 size_t fdy_store_members_bytes(const fdy_store* store) {

@@ -1,0 +1,84 @@
+"""N>1 host logic on CPU: two gloo processes run the bench orchestration
+(rank 0 writes the archive, barrier, each process materializes its own TP rank,
+max-over-ranks reduction, object broadcast of the store handle). The kernel is
+replaced by its NumPy emulation; each rank's graph set must equal the oracle's
+for that rank."""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank: int, world: int, port: int, workdir: str, queue) -> None:
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    try:
+        import json
+
+        import store_emulator as emu
+        from oracle_lib import Oracle
+        import paper_2604_06664_b200 as foundry
+        from paper_2604_06664_b200.multirank import RankGroup, TP_WORLD, tp_rank
+
+        g = RankGroup.from_env()
+        g.init("gloo")
+        arch = os.path.join(workdir, "moe")
+        if g.rank == 0:
+            spec = foundry.preset("moe-spmd")
+            spec.batch_max = 24
+            spec.thresholds = [5, 9, 17]
+            foundry.save(spec, arch)
+        g.barrier()
+        # the store bytes travel once from rank 0 (the handle/object broadcast path)
+        blob = open(os.path.join(arch, "templates.fdt"), "rb").read() if g.rank == 0 else None
+        blob = g.broadcast_object(blob, src=0)
+        r = tp_rank(g.rank + 5)  # ranks 5 and 6 of the TP-8 group
+        m = json.load(open(os.path.join(arch, "manifest")))
+        delta = 0x10000 * (g.rank + 1)
+        arena = emu.expand(blob, r, TP_WORLD, m["allocator"]["base"] + delta)
+        got = foundry._foundry._decode_member_images(arch, arena)
+        want, _ = Oracle(os.path.join(ROOT, "oracle", "_build", "liboracle.so")).materialize_archive(
+            arch, r, TP_WORLD, delta)
+        worst = g.max(float(g.rank + 1))
+        queue.put((g.rank, got == want, worst, r))
+        g.close()
+    except Exception as exc:  # surface worker failures to the parent
+        queue.put((rank, repr(exc), None, None))
+
+
+def test_two_rank_orchestration_over_gloo(tmp_path, native_build):
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, str(tmp_path), q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert [r[1] for r in results] == [True, True], results
+    assert all(r[2] == 2.0 for r in results)  # max over ranks
+    assert [r[3] for r in results] == [5, 6]
+
+
+def test_tp_rank_mapping():
+    from paper_2604_06664_b200.multirank import tp_rank
+
+    assert [tp_rank(r) for r in range(10)] == [0, 1, 2, 3, 4, 5, 6, 7, 0, 1]

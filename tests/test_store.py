@@ -1,0 +1,93 @@
+"""Template-store packer (FNDT) checked end to end on CPU: pack -> NumPy
+emulation of the fused kernel -> decode -> byte-identical to the oracle."""
+from __future__ import annotations
+
+import os
+import struct
+
+import pytest
+
+import store_emulator as emu
+from conftest import manifest
+
+
+def emulate(foundry, arch, rank, world, delta=0, values=()):
+    blob = open(os.path.join(arch, "templates.fdt"), "rb").read()
+    m = manifest(arch)
+    nb = m["allocator"]["base"] + delta if delta else 0
+    arena = emu.expand(blob, rank, world, nb, values)
+    return foundry._foundry._decode_member_images(arch, arena)
+
+
+@pytest.mark.parametrize("name,cases", [
+    ("micro", [(0, 1, 0), (0, 1, 0x10000)]),
+    ("llama3-8b", [(0, 1, 0), (0, 1, 0x123450000)]),
+    ("moe-spmd", [(0, 1, 0), (1, 4, 0), (7, 8, 0x10000000000), (2, 3, 0x10000)]),
+])
+def test_store_expansion_equals_oracle(foundry, oracle, archives, name, cases):
+    arch, _ = archives(name)
+    for rank, world, delta in cases:
+        want, _ = oracle.materialize_archive(arch, rank, world, delta)
+        assert emulate(foundry, arch, rank, world, delta) == want, (rank, world, hex(delta))
+
+
+def test_store_header_describes_the_archive(foundry, archives):
+    from paper_2604_06664_b200 import capi
+    arch, outcome = archives("moe-spmd")
+    m = manifest(arch)
+    h = capi.store_header(open(os.path.join(arch, "templates.fdt"), "rb").read())
+    assert h["n_members"] == outcome.total_graphs == 512
+    assert h["n_groups"] == outcome.template_count
+    assert h["old_base"] == m["allocator"]["base"]
+    assert h["final_offset"] == m["allocator"]["final_offset"]
+    assert h["real_comm_hash"] == m["comm"]["real_binary_hash"]
+    assert h["source_graphs_crc"] == m["files"]["graphs.bin"]
+    assert h["source_patch_crc"] == m["files"]["patch.bin"]
+    assert h["tile_chunks"] == 1024
+    # 12 layers x 2 collectives -> 24 patch entries per graph, each: kernel swap
+    # (one 4-byte op) + rank + world (one op each, 8-byte aligned inside a chunk)
+    assert h["n_rank_ops"] == 512 * 24 * 3
+    alg = capi.algorithmic_bytes(h)
+    assert alg["write"] == h["members_image_bytes"] and alg["read"] > 0
+
+
+def test_store_is_smaller_than_graphs_bin(archives):
+    arch, _ = archives("moe-spmd")
+    store = os.path.getsize(os.path.join(arch, "templates.fdt"))
+    graphs = os.path.getsize(os.path.join(arch, "graphs.bin"))
+    assert store < graphs / 3
+
+
+def test_repacking_is_deterministic(foundry, archives, tmp_path):
+    import shutil
+    arch, _ = archives("micro")
+    copy = tmp_path / "copy"
+    shutil.copytree(arch, copy)
+    foundry._foundry._pack_store(str(copy))
+    assert (copy / "templates.fdt").read_bytes() == open(os.path.join(arch, "templates.fdt"), "rb").read()
+
+
+def test_pack_rejects_a_patch_on_a_non_stub(foundry, archives, tmp_path):
+    """apply_rank_patches raises archive-corruption for a patch entry whose node
+    is not the recorded stub (rank_forge.cpp:141-143); the packer does too."""
+    import shutil
+    arch, _ = archives("moe-spmd", b200=False)
+    bad = tmp_path / "bad"
+    shutil.copytree(arch, bad)
+    patch = bytearray((bad / "patch.bin").read_bytes())
+    # first entry: magic(4) ver(2) placeholder(8) ngraphs(4) label(4) count(4) node_id(4)
+    struct.pack_into("<I", patch, 26, 1)  # point it at node 1 (a compute kernel)
+    (bad / "patch.bin").write_bytes(bytes(patch))
+    with pytest.raises(foundry.FoundryError, match="archive-corruption: node 1 is not the recorded stub"):
+        foundry._foundry._pack_store(str(bad))
+
+
+def test_crc64_host_matches_the_oracle_and_combines(foundry, oracle):
+    import random
+    rng = random.Random(3)
+    for n in (0, 1, 7, 8, 9, 100, 4096, 70001):
+        a = bytes(rng.randrange(256) for _ in range(n))
+        b = bytes(rng.randrange(256) for _ in range(n // 3 + 1))
+        assert foundry._foundry._crc64(a) == oracle.crc64(a)
+        combined = foundry._foundry._crc64_combine(oracle.crc64(a), oracle.crc64(b), len(b))
+        assert combined == oracle.crc64(a + b)
