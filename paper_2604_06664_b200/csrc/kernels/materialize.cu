@@ -3,14 +3,17 @@
 //
 // Work unit: a tile = up to FDT_TILE_CHUNKS (1024) 16-byte chunks of one
 // member image (layout: foundry/store_format.h). Each persistent CTA walks the
-// tile list with a 2-stage TMA bulk-copy pipeline:
+// tile list software-pipelined one tile ahead:
 //
-//   cp.async.bulk  global -> smem   template chunk tile (mbarrier complete_tx)
-//   overlay        diff chunks (byte masks) from the member's diff stream
-//   relocate       8-byte lanes flagged by the chunk meta whose value lies in
-//                  [old_base, old_base + span): v += delta
-//   patch          the tile's rank ops (rank/world u64, stub->real kernel
-//                  index, per-rank value table) on the smem tile
+//   cp.async.bulk  global -> smem   template tile t+1 (mbarrier complete_tx)
+//   registers      tile t+1's diff entries + chunk meta (plain loads, consumed
+//                  an iteration later, so no phase waits on global memory)
+//   cp.async       tile t+1's rank ops -> smem
+//   ---- tile t, all operands already on chip ----
+//   B  (K2)        one thread per diff entry overlays its chunk (byte masks)
+//   C  (K1)        one thread per chunk: flagged 8-byte lanes whose value is in
+//                  [old_base, old_base + span) get += delta (skipped if delta = 0)
+//   D  (K3)        one thread per chunk-run of rank ops, table order
 //   cp.async.bulk  smem -> global   member image tile (bulk_group)
 //
 // The reference does this work per node on CPU prepare lanes: parse_graph_at
@@ -25,13 +28,25 @@
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kChunksPerThread = FDT_TILE_CHUNKS / kThreads;
+constexpr int kChunksPerThread = FDT_TILE_CHUNKS / kThreads;  // 4
+constexpr int kDiffRegs = 2;    // diff entries per thread held in registers
+constexpr int kOpSlots = 256;   // rank ops per tile staged in shared memory
 static_assert(FDT_TILE_CHUNKS % kThreads == 0, "tile must split evenly across the CTA");
+static_assert(kChunksPerThread == 4, "chunk meta prefetch packs 4 bytes per thread");
 
 struct __align__(128) Smem {
-    uint4 buf[2][FDT_TILE_CHUNKS];      // 2 x 16 KiB stages
+    uint4 buf[2][FDT_TILE_CHUNKS];      // 2 x 16 KiB template/member tile stages
+    fdt_rank_op ops[kOpSlots];          // rank ops of the tile being processed (4 KiB)
     unsigned long long bar[2];          // mbarriers, one per stage
     uint8_t ometa[FDT_TILE_CHUNKS];     // relocation-meta overrides from diff entries (0x80 | lanes)
+};
+
+// Per-thread operands of one tile, loaded one iteration ahead.
+struct Prefetch {
+    uint32_t didx[kDiffRegs];  // chunk index within the tile
+    uint32_t dmeta[kDiffRegs];
+    uint4 ddata[kDiffRegs];
+    uint32_t cmeta;  // meta bytes of chunks tid + 256 k, k = 0..3
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -90,8 +105,17 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-__device__ __forceinline__ uint64_t relocate_lane(uint64_t v, const FdyMaterializeArgs& a) {
-    return (v - a.old_base < a.span) ? v + a.delta : v;
+__device__ __forceinline__ void cp_async16(void* dst_smem, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst_smem)), "l"(src)
+                 : "memory");
+}
+
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // Expands 4 mask bits into a 32-bit byte-select word (bit i -> byte i = 0xFF).
@@ -138,16 +162,46 @@ __device__ __forceinline__ void relocate_pair(uint32_t& lo, uint32_t& hi, bool f
     hi = uint32_t(y >> 32);
 }
 
-// Phases per tile, each convergent across the CTA:
-//   B  diff-parallel: one thread per diff entry overlays its chunk in smem
-//   C  chunk-parallel relocation (skipped when delta == 0, a uniform branch)
-//   D  op-run-parallel rank patch: one thread per chunk's run of ops
+__device__ __forceinline__ fdt_tile load_tile(const FdyMaterializeArgs& a, uint32_t t) {
+    if (t < a.n_tiles) return a.tiles[t];
+    fdt_tile z{};
+    return z;
+}
+
+// Issues the loads of tile T's per-thread operands (registers) and rank ops
+// (cp.async into smem); nothing here waits on memory.
+__device__ __forceinline__ void prefetch_tile(const FdyMaterializeArgs& a, const fdt_tile& T,
+                                              bool relocating, Smem& s, Prefetch& p, int tid) {
+#pragma unroll
+    for (int j = 0; j < kDiffRegs; ++j) {
+        const uint32_t e = T.diff_lo + tid + j * kThreads;
+        if (e < T.diff_hi) {
+            p.didx[j] = __ldg(a.didx + e) - T.chunk_base;
+            p.dmeta[j] = __ldg(a.dmeta + e);
+            p.ddata[j] = __ldg(a.ddata + e);
+        }
+    }
+    p.cmeta = 0;
+    if (relocating) {
+        const uint8_t* meta = a.cmeta + (T.src_off - a.timage_base) / 16;
+#pragma unroll
+        for (int k = 0; k < kChunksPerThread; ++k) {
+            const uint32_t c = tid + k * kThreads;
+            if (c < T.nchunks) p.cmeta |= uint32_t(__ldg(meta + c)) << (8 * k);
+        }
+    }
+    const uint32_t nops = min(T.rop_hi - T.rop_lo, uint32_t(kOpSlots));
+    for (uint32_t i = tid; i < nops; i += kThreads) cp_async16(&s.ops[i], a.rops + T.rop_lo + i);
+    cp_async_commit();
+}
+
 __global__ void __launch_bounds__(kThreads)
 fdy_materialize_kernel(const FdyMaterializeArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
     const int tid = threadIdx.x;
     const bool relocating = a.delta != 0ull;
+    const uint32_t G = gridDim.x;
 
     if (tid == 0) {
         mbar_init(&s.bar[0], 1);
@@ -159,43 +213,57 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
 
     uint32_t t = blockIdx.x;
     if (t >= a.n_tiles) return;
+    fdt_tile T = a.tiles[t];
+    fdt_tile Tn = load_tile(a, t + G);
     if (tid == 0) {
-        const fdt_tile& first = a.tiles[t];
-        mbar_expect_tx(&s.bar[0], first.nchunks * 16u);
-        bulk_load(s.buf[0], a.store + first.src_off, first.nchunks * 16u, &s.bar[0]);
+        mbar_expect_tx(&s.bar[0], T.nchunks * 16u);
+        bulk_load(s.buf[0], a.store + T.src_off, T.nchunks * 16u, &s.bar[0]);
     }
+    Prefetch cur;
+    prefetch_tile(a, T, relocating, s, cur, tid);
 
     uint32_t stage = 0;
     uint32_t parity = 0u;  // bit s = expected phase parity of stage s
-    for (; t < a.n_tiles; t += gridDim.x) {
-        const fdt_tile T = a.tiles[t];
-        const uint32_t next = t + gridDim.x;
-        // prefetch the next tile into the other stage once its store has drained
-        if (tid == 0 && next < a.n_tiles) {
-            bulk_wait_reads();
-            const fdt_tile& N = a.tiles[next];
-            mbar_expect_tx(&s.bar[stage ^ 1], N.nchunks * 16u);
-            bulk_load(s.buf[stage ^ 1], a.store + N.src_off, N.nchunks * 16u, &s.bar[stage ^ 1]);
+    for (; t < a.n_tiles; t += G) {
+        const bool has_next = t + G < a.n_tiles;
+        // stage s^1 <- tile t+G: its descriptor is already in registers
+        if (tid == 0 && has_next) {
+            bulk_wait_reads();  // the previous store out of stage s^1 has drained
+            mbar_expect_tx(&s.bar[stage ^ 1], Tn.nchunks * 16u);
+            bulk_load(s.buf[stage ^ 1], a.store + Tn.src_off, Tn.nchunks * 16u, &s.bar[stage ^ 1]);
         }
+        const fdt_tile Tnn = load_tile(a, t + 2 * G);  // consumed next iteration
         uint4* buf = s.buf[stage];
         mbar_wait(&s.bar[stage], (parity >> stage) & 1u);
         parity ^= 1u << stage;
 
-        // B: K2 diff overlay
-        for (uint32_t e = T.diff_lo + tid; e < T.diff_hi; e += kThreads) {
-            const uint32_t c = __ldg(a.didx + e) - T.chunk_base;
+        // B: K2 diff overlay (operands in registers)
+#pragma unroll
+        for (int j = 0; j < kDiffRegs; ++j) {
+            if (T.diff_lo + tid + j * kThreads < T.diff_hi) {
+                const uint32_t c = cur.didx[j], dm = cur.dmeta[j];
+                buf[c] = merge_bytes(buf[c], cur.ddata[j], dm & FDT_DMETA_MASK);
+                if (relocating && (dm & FDT_DMETA_RELOC_OVERRIDE))
+                    s.ometa[c] = static_cast<uint8_t>(0x80u | ((dm >> FDT_DMETA_RELOC_SHIFT) & 3u));
+            }
+        }
+        for (uint32_t e = T.diff_lo + kDiffRegs * kThreads + tid; e < T.diff_hi; e += kThreads) {
+            const uint32_t c = __ldg(a.didx + e) - T.chunk_base;  // dense tiles only
             const uint32_t dm = __ldg(a.dmeta + e);
             buf[c] = merge_bytes(buf[c], __ldg(a.ddata + e), dm & FDT_DMETA_MASK);
             if (relocating && (dm & FDT_DMETA_RELOC_OVERRIDE))
                 s.ometa[c] = static_cast<uint8_t>(0x80u | ((dm >> FDT_DMETA_RELOC_SHIFT) & 3u));
         }
+        cp_async_wait_all();  // this tile's rank ops are in smem
         __syncthreads();
 
         // C: K1 relocation of flagged lanes whose value lies in the captured range
         if (relocating) {
-            const uint8_t* meta = a.cmeta + (T.src_off - a.timage_base) / 16;
-            for (uint32_t c = tid; c < T.nchunks; c += kThreads) {
-                uint32_t m = __ldg(meta + c);
+#pragma unroll
+            for (int k = 0; k < kChunksPerThread; ++k) {
+                const uint32_t c = tid + k * kThreads;
+                if (c >= T.nchunks) break;
+                uint32_t m = (cur.cmeta >> (8 * k)) & 0xFFu;
                 const uint32_t o = s.ometa[c];
                 if (o) {
                     m = o & 3u;
@@ -212,20 +280,26 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
         }
 
         // D: K3 rank ops; ops on one chunk are applied in table order by one thread
-        for (uint32_t i = T.rop_lo + tid; i < T.rop_hi; i += kThreads) {
-            const uint32_t ch = a.rops[i].chunk;
-            if (i != T.rop_lo && a.rops[i - 1].chunk == ch) continue;
-            uint4 v = buf[ch - T.chunk_base];
-            for (uint32_t j = i; j < T.rop_hi; ++j) {
-                const fdt_rank_op op = a.rops[j];
-                if (op.chunk != ch) break;
+        const uint32_t nops = T.rop_hi - T.rop_lo;
+        for (uint32_t i = tid; i < nops; i += kThreads) {
+            auto op_at = [&](uint32_t k) { return k < kOpSlots ? s.ops[k] : a.rops[T.rop_lo + k]; };
+            const fdt_rank_op first = op_at(i);
+            if (i != 0 && op_at(i - 1).chunk == first.chunk) continue;
+            const uint32_t c = first.chunk - T.chunk_base;
+            uint4 v = buf[c];
+            for (uint32_t j = i; j < nops; ++j) {
+                const fdt_rank_op op = op_at(j);
+                if (op.chunk != first.chunk) break;
                 v = merge_bytes(v, place_value(rank_op_value(op, a), op.shift), op.mask);
             }
-            buf[ch - T.chunk_base] = v;
+            buf[c] = v;
         }
         fence_proxy_async_smem();
-        __syncthreads();
+        __syncthreads();  // member tile complete; ops / ometa free for the next tile
         if (tid == 0) bulk_store(a.out + T.dst_off, buf, T.nchunks * 16u);
+        if (has_next) prefetch_tile(a, Tn, relocating, s, cur, tid);
+        T = Tn;
+        Tn = Tnn;
         stage ^= 1u;
     }
     if (tid == 0) bulk_wait_all();
