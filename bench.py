@@ -25,6 +25,7 @@ JSON keys beyond the base contract:
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import shutil
@@ -83,14 +84,18 @@ def prepare_archives(workload: str, rank: int, barrier) -> tuple[str, str]:
     root = os.path.join(tempfile.gettempdir(), "foundry_bench_" + workload)
     ours, plain = os.path.join(root, "b200"), os.path.join(root, "plain")
     done = os.path.join(root, "READY")
-    if rank == 0 and not os.path.exists(done):
+    # the cache is only reused by the exact build + spec that wrote it
+    stamp = hashlib.sha1(open(foundry._foundry.__file__, "rb").read()
+                         + open(foundry.workload_path(workload), "rb").read()).hexdigest()
+    fresh = os.path.exists(done) and open(done).read() == stamp
+    if rank == 0 and not fresh:
         shutil.rmtree(root, ignore_errors=True)
         os.makedirs(root)
         spec = foundry.workload_from_text(open(foundry.workload_path(workload)).read())
         os.environ.setdefault("FOUNDRY_CUBIN_CACHE", os.path.join(root, "cubin_cache"))
         foundry.save(spec, ours)
         foundry.save(spec, plain, b200_artifacts=False)
-        open(done, "w").write("ok")
+        open(done, "w").write(stamp)
     barrier()
     return ours, plain
 

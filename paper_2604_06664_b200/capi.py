@@ -194,7 +194,7 @@ class CApi:
 
 # ---- FNDT store header (foundry/store_format.h) -----------------------------
 
-SECTIONS = ["groups", "timages", "cmeta", "members", "tiles", "didx", "dmeta", "ddata", "rops",
+SECTIONS = ["groups", "timages", "cmeta", "members", "tiles", "didx", "ddata", "rops",
             "kernels", "nodeattrs", "edges", "strings"]
 
 
@@ -219,7 +219,7 @@ def algorithmic_bytes(h: dict) -> dict:
     templates + chunk meta read once, every diff / rank op / tile read once,
     every member image written once."""
     s = h["sec"]
-    read = (s["timages"][1] + s["cmeta"][1] + s["didx"][1] + s["dmeta"][1] + s["ddata"][1]
+    read = (s["timages"][1] + s["cmeta"][1] + s["didx"][1] + s["ddata"][1]
             + s["rops"][1] + s["tiles"][1])
     write = h["members_image_bytes"]
     return {"read": read, "write": write, "total": read + write}

@@ -150,6 +150,7 @@ DeviceStore adopt_store(Device& dev, const unsigned char* d_blob, size_t bytes,
     s.data = d_blob;
     s.bytes = bytes;
     s.header = h;
+    if (h.sec[FDT_SEC_TIMAGES].bytes) s.rtimages = DeviceBuffer(dev, h.sec[FDT_SEC_TIMAGES].bytes);
     return s;
 }
 
@@ -176,21 +177,26 @@ void launch_materialize(Device& dev, const DeviceStore& store, const Materialize
     const unsigned char* b = store.data;
     a.store = b;
     a.out = out;
+    a.rtimg = store.rtimages.data();
     a.tiles = reinterpret_cast<const fdt_tile*>(b + h.sec[FDT_SEC_TILES].offset);
     a.cmeta = b + h.sec[FDT_SEC_CMETA].offset;
     a.didx = reinterpret_cast<const uint32_t*>(b + h.sec[FDT_SEC_DIDX].offset);
-    a.dmeta = reinterpret_cast<const uint32_t*>(b + h.sec[FDT_SEC_DMETA].offset);
     a.ddata = reinterpret_cast<const uint4*>(b + h.sec[FDT_SEC_DDATA].offset);
     a.rops = reinterpret_cast<const fdt_rank_op*>(b + h.sec[FDT_SEC_ROPS].offset);
     a.values = d_values;
     a.n_values = d_values ? static_cast<uint32_t>(req.values.size()) : 0u;
     a.timage_base = h.sec[FDT_SEC_TIMAGES].offset;
+    a.timage_bytes = h.sec[FDT_SEC_TIMAGES].bytes;
     a.old_base = h.old_base;
     a.span = h.final_offset;
     a.delta = req.new_base ? req.new_base - h.old_base : 0;
     a.rank = req.rank;
     a.world = req.world;
     a.n_tiles = h.n_tiles;
+    // the kernel reads template chunks at tsrc + tile.src_off (a store offset)
+    a.tsrc = a.delta && a.rtimg ? reinterpret_cast<const unsigned char*>(
+                                      reinterpret_cast<uintptr_t>(a.rtimg) - a.timage_base)
+                                : b;
 
     int per_sm = 0;
     cuda_check(fdy_materialize_occupancy(&per_sm), "materialize occupancy query");

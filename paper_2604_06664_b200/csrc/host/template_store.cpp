@@ -114,8 +114,8 @@ void build_image(const CapturedGraph& g, const GroupLayout& L, const KernelTable
 }
 
 struct MemberOut {
-    std::vector<uint32_t> didx;
-    std::vector<uint32_t> dmeta;
+    std::vector<uint32_t> didx;   // chunk index (lanes packed in when merged)
+    std::vector<uint8_t> dlanes;  // the member chunk's relocation lanes
     std::vector<uint8_t> ddata;
     std::vector<fdt_rank_op> rops;
 };
@@ -168,7 +168,7 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
     std::vector<uint32_t> edges;
     Sink timages;
     std::vector<uint8_t> cmeta;
-    std::vector<uint32_t> didx, dmeta;
+    std::vector<uint32_t> didx;
     std::vector<uint8_t> ddata;
     std::vector<fdt_rank_op> rops;
     std::vector<fdt_tile> tiles;
@@ -262,16 +262,16 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
             std::vector<uint8_t> img, meta;
             build_image(g, L, kt, img, meta);
             const size_t nchunks = img.size() / 16;
+            require(nchunks <= FDT_DIDX_CHUNK_MASK, Errc::invalid_argument,
+                    "graph image exceeds the store's 2^30-chunk limit");
+            // A chunk whose bytes or relocation lanes differ from the template's
+            // is carried whole, with the member's lanes (store_format.h).
             for (size_t c = 0; c < nchunks; ++c) {
-                uint32_t mask = 0;
-                for (int j = 0; j < 16; ++j)
-                    if (img[16 * c + j] != timg[16 * c + j]) mask |= 1u << j;
-                const bool meta_differs = meta[c] != tmeta[c];
-                if (!mask && !meta_differs) continue;
-                uint32_t dm = mask;
-                if (meta_differs) dm |= FDT_DMETA_RELOC_OVERRIDE | (uint32_t(meta[c]) << FDT_DMETA_RELOC_SHIFT);
+                if (meta[c] == tmeta[c] &&
+                    std::memcmp(img.data() + 16 * c, timg.data() + 16 * c, 16) == 0)
+                    continue;
                 o.didx.push_back(static_cast<uint32_t>(c));
-                o.dmeta.push_back(dm);
+                o.dlanes.push_back(meta[c]);
                 o.ddata.insert(o.ddata.end(), img.begin() + 16 * c, img.begin() + 16 * c + 16);
             }
             auto pit = patches.per_graph.find(g.label);
@@ -338,8 +338,8 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
                 T.rop_hi = r0 + static_cast<uint32_t>(rpos);
                 tiles.push_back(T);
             }
-            didx.insert(didx.end(), o.didx.begin(), o.didx.end());
-            dmeta.insert(dmeta.end(), o.dmeta.begin(), o.dmeta.end());
+            for (size_t k = 0; k < o.didx.size(); ++k)
+                didx.push_back(o.didx[k] | uint32_t(o.dlanes[k]) << FDT_DIDX_LANE_SHIFT);
             ddata.insert(ddata.end(), o.ddata.begin(), o.ddata.end());
             rops.insert(rops.end(), o.rops.begin(), o.rops.end());
             members.push_back(M);
@@ -393,7 +393,6 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
     put_section(s, h, FDT_SEC_MEMBERS, members.data(), members.size());
     put_section(s, h, FDT_SEC_TILES, tiles.data(), tiles.size());
     put_section(s, h, FDT_SEC_DIDX, didx.data(), didx.size());
-    put_section(s, h, FDT_SEC_DMETA, dmeta.data(), dmeta.size());
     put_section(s, h, FDT_SEC_DDATA, ddata.data(), ddata.size());
     put_section(s, h, FDT_SEC_ROPS, rops.data(), rops.size());
     put_section(s, h, FDT_SEC_KERNELS, kernels.data(), kernels.size());

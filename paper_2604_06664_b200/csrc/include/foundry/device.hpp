@@ -95,6 +95,9 @@ struct DeviceStore {
     const unsigned char* data = nullptr;
     size_t bytes = 0;
     fdt_header header{};
+    // Relocated template images of the launch in flight (delta != 0); one per
+    // store, so materializations of a store are ordered on its device stream.
+    DeviceBuffer rtimages;
 };
 
 struct MaterializeRequest {

@@ -19,12 +19,17 @@
  * un-rank-patched (the captured state).
  *
  * Materialization of member m for (rank, world, new_base) =
- *   K2  copy the template image, overlay the member's diff chunks;
- *   K1  for every 8-byte lane marked relocatable (chunk meta, possibly
- *       overridden by the diff entry) whose value v is in
+ *   K2  copy the template image, replace the member's diff chunks;
+ *   K1  for every 8-byte lane marked relocatable (template chunk meta, or the
+ *       lane bits of the diff entry for a replaced chunk) whose value v is in
  *       [old_base, old_base + final_offset): v += new_base - old_base;
  *   K3  apply the member's rank ops (rank / world u64 writes, stub->real
  *       kernel index swap, per-rank value-table writes).
+ * A diff entry exists for every chunk whose bytes OR relocation lanes differ
+ * from the template's, and carries the member's whole chunk, so K1 commutes
+ * with K2: relocating the template images once per launch (3 MB) and the
+ * diff chunks in registers gives the per-member result, and the per-member
+ * pass is copy + scatter + rank ops.
  * The kernel works tile by tile: a tile is up to tile_chunks consecutive
  * 16-byte chunks of one member image; the packer precomputes each tile's
  * diff and rank-op ranges so a CTA needs one descriptor load to start.
@@ -34,7 +39,7 @@
 
 #include <stdint.h>
 
-#define FDT_VERSION 1u
+#define FDT_VERSION 2u
 #define FDT_TILE_CHUNKS 1024u /* 16 KiB of member image per tile */
 
 enum fdt_section_id {
@@ -43,9 +48,8 @@ enum fdt_section_id {
     FDT_SEC_CMETA,       /* 1 byte per 16-B chunk of TIMAGES            (device)      */
     FDT_SEC_MEMBERS,     /* fdt_member[n_members]                       (host+device) */
     FDT_SEC_TILES,       /* fdt_tile[n_tiles]                           (device)      */
-    FDT_SEC_DIDX,        /* u32 chunk index per diff entry              (device)      */
-    FDT_SEC_DMETA,       /* u32 per diff entry (see FDT_DMETA_*)        (device)      */
-    FDT_SEC_DDATA,       /* 16 B per diff entry                         (device)      */
+    FDT_SEC_DIDX,        /* u32 per diff entry: chunk | lanes << 30     (device)      */
+    FDT_SEC_DDATA,       /* 16 B per diff entry: the member chunk       (device)      */
     FDT_SEC_ROPS,        /* fdt_rank_op[n_rank_ops]                     (device)      */
     FDT_SEC_KERNELS,     /* fdt_kernel[n_kernels]                       (host)        */
     FDT_SEC_NODEATTRS,   /* fdt_node_attrs per template node            (host)        */
@@ -129,9 +133,10 @@ typedef struct {
     uint32_t pad;
 } fdt_tile;
 
-#define FDT_DMETA_MASK 0xFFFFu           /* bytes taken from the diff data */
-#define FDT_DMETA_RELOC_OVERRIDE 0x10000u /* bits 17-18 replace the chunk meta */
-#define FDT_DMETA_RELOC_SHIFT 17
+/* Diff entry index word: the chunk index within the member image (< 2^30)
+ * and, in the top two bits, the member chunk's relocation lanes (FDT_CMETA_*). */
+#define FDT_DIDX_CHUNK_MASK 0x3FFFFFFFu
+#define FDT_DIDX_LANE_SHIFT 30
 
 #define FDT_CMETA_LANE0 0x1u /* bytes 0-7 of the chunk are a relocatable slot */
 #define FDT_CMETA_LANE1 0x2u /* bytes 8-15 */

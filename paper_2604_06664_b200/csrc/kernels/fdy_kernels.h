@@ -10,16 +10,19 @@
 #include "foundry/store_format.h"
 
 struct FdyMaterializeArgs {
-    const unsigned char* store;  // template store blob in HBM
+    const unsigned char* store;  // template store blob in HBM (never written)
+    const unsigned char* tsrc;   // template source: tsrc + tile.src_off = the tile's
+                                 // template chunks (store, or rtimg rebased by timage_base)
     unsigned char* out;          // member image arena in HBM
+    unsigned char* rtimg;        // relocated-template scratch (timage_bytes), delta != 0
     const fdt_tile* tiles;
     const uint8_t* cmeta;
     const uint32_t* didx;
-    const uint32_t* dmeta;
     const uint4* ddata;
     const fdt_rank_op* rops;
     const uint64_t* values;  // FDT_ROP_VALUE table (may be null)
     uint64_t timage_base;    // store offset of FDT_SEC_TIMAGES
+    uint64_t timage_bytes;
     uint64_t old_base;       // captured VA base
     uint64_t span;           // final_offset
     uint64_t delta;          // new_base - old_base (mod 2^64)
@@ -38,6 +41,8 @@ struct FdyCrcBlock {
 extern "C" {
 size_t fdy_materialize_smem_bytes();
 cudaError_t fdy_materialize_occupancy(int* blocks_per_sm);
+// delta == 0: one grid. Otherwise the template relocation grid, then the
+// member grid under programmatic dependent launch (both on `stream`).
 cudaError_t fdy_launch_materialize(const FdyMaterializeArgs* args, int grid, cudaStream_t stream);
 
 cudaError_t fdy_crc64_set_constants(const uint64_t* x2k64);  // per device

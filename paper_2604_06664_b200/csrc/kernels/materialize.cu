@@ -1,18 +1,29 @@
 // Fused graph-set materialization for sm_100a: K2 (template diff expansion)
 // -> K1 (VA relocation) -> K3 (rank / comm-state patch), one pass over HBM.
 //
-// Work unit: a tile = up to FDT_TILE_CHUNKS (1024) 16-byte chunks of one
-// member image (layout: foundry/store_format.h). Each persistent CTA walks the
-// tile list software-pipelined one tile ahead:
+// K1 commutes with K2 by construction of the store (foundry/store_format.h):
+// a diff entry carries the member's whole 16-byte chunk plus its relocation
+// lanes. So a launch with delta != 0 is two grids on one stream:
 //
-//   cp.async.bulk  global -> smem   template tile t+1 (mbarrier complete_tx)
-//   registers      tile t+1's diff entries + chunk meta (plain loads, consumed
-//                  an iteration later, so no phase waits on global memory)
+//   fdy_relocate_templates   template images (3 MB for the 512-graph set)
+//                            -> relocated copy in the store's scratch, once
+//   fdy_materialize          per member tile, started early under programmatic
+//                            dependent launch; its prologue (descriptors,
+//                            diff + rank-op prefetch) overlaps the first grid
+//                            and griddepcontrol.wait gates only the first
+//                            template read.
+//
+// Work unit of the second grid: a tile = up to FDT_TILE_CHUNKS (1024) 16-byte
+// chunks of one member image. Each persistent CTA walks the tile list
+// software-pipelined one tile ahead:
+//
+//   cp.async.bulk  global -> smem   template tile t+1 (16 KiB, mbarrier complete_tx)
+//   registers      tile t+1's diff entries (plain loads, consumed an
+//                  iteration later, so no phase waits on global memory)
 //   cp.async       tile t+1's rank ops -> smem
 //   ---- tile t, all operands already on chip ----
-//   B  (K2)        one thread per diff entry overlays its chunk (byte masks)
-//   C  (K1)        one thread per chunk: flagged 8-byte lanes whose value is in
-//                  [old_base, old_base + span) get += delta (skipped if delta = 0)
+//   B  (K2+K1)     one thread per diff entry: relocate its lanes in registers,
+//                  store the chunk over the template chunk
 //   D  (K3)        one thread per chunk-run of rank ops, table order
 //   cp.async.bulk  smem -> global   member image tile (bulk_group)
 //
@@ -20,6 +31,7 @@
 // (graph_model.cpp:295-303) + apply_rank_patches (rank_forge.cpp:132-152);
 // relocation has no reference function (SURVEY.md §8c rule). Pure integer
 // streaming: no tensor-core work exists here, the bound is HBM bandwidth.
+#include <algorithm>
 #include <cstdint>
 
 #include "foundry/store_format.h"
@@ -28,25 +40,21 @@
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kChunksPerThread = FDT_TILE_CHUNKS / kThreads;  // 4
 constexpr int kDiffRegs = 2;    // diff entries per thread held in registers
 constexpr int kOpSlots = 256;   // rank ops per tile staged in shared memory
+constexpr int kRelocThreads = 256;
 static_assert(FDT_TILE_CHUNKS % kThreads == 0, "tile must split evenly across the CTA");
-static_assert(kChunksPerThread == 4, "chunk meta prefetch packs 4 bytes per thread");
 
 struct __align__(128) Smem {
     uint4 buf[2][FDT_TILE_CHUNKS];      // 2 x 16 KiB template/member tile stages
     fdt_rank_op ops[kOpSlots];          // rank ops of the tile being processed (4 KiB)
     unsigned long long bar[2];          // mbarriers, one per stage
-    uint8_t ometa[FDT_TILE_CHUNKS];     // relocation-meta overrides from diff entries (0x80 | lanes)
 };
 
 // Per-thread operands of one tile, loaded one iteration ahead.
 struct Prefetch {
-    uint32_t didx[kDiffRegs];  // chunk index within the tile
-    uint32_t dmeta[kDiffRegs];
+    uint32_t didx[kDiffRegs];  // chunk index within the tile | lanes << 30
     uint4 ddata[kDiffRegs];
-    uint32_t cmeta;  // meta bytes of chunks tid + 256 k, k = 0..3
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -118,6 +126,17 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// Programmatic dependent launch (sm_90+): the primary grid lets the dependent
+// grid start; the dependent blocks in wait until the primary has completed
+// and its writes are visible. Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ void pdl_wait_primary() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // Expands 4 mask bits into a 32-bit byte-select word (bit i -> byte i = 0xFF).
 __device__ __forceinline__ uint32_t byte_select(uint32_t m4) {
     return ((m4 * 0x00204081u) & 0x01010101u) * 0xFFu;
@@ -162,6 +181,13 @@ __device__ __forceinline__ void relocate_pair(uint32_t& lo, uint32_t& hi, bool f
     hi = uint32_t(y >> 32);
 }
 
+// K1 on one chunk: lanes bit 0 = bytes 0-7, bit 1 = bytes 8-15.
+__device__ __forceinline__ uint4 relocate_chunk(uint4 v, uint32_t lanes, const FdyMaterializeArgs& a) {
+    relocate_pair(v.x, v.y, lanes & FDT_CMETA_LANE0, a);
+    relocate_pair(v.z, v.w, lanes & FDT_CMETA_LANE1, a);
+    return v;
+}
+
 __device__ __forceinline__ fdt_tile load_tile(const FdyMaterializeArgs& a, uint32_t t) {
     if (t < a.n_tiles) return a.tiles[t];
     fdt_tile z{};
@@ -171,28 +197,41 @@ __device__ __forceinline__ fdt_tile load_tile(const FdyMaterializeArgs& a, uint3
 // Issues the loads of tile T's per-thread operands (registers) and rank ops
 // (cp.async into smem); nothing here waits on memory.
 __device__ __forceinline__ void prefetch_tile(const FdyMaterializeArgs& a, const fdt_tile& T,
-                                              bool relocating, Smem& s, Prefetch& p, int tid) {
+                                              Smem& s, Prefetch& p, int tid) {
 #pragma unroll
     for (int j = 0; j < kDiffRegs; ++j) {
         const uint32_t e = T.diff_lo + tid + j * kThreads;
         if (e < T.diff_hi) {
-            p.didx[j] = __ldg(a.didx + e) - T.chunk_base;
-            p.dmeta[j] = __ldg(a.dmeta + e);
+            p.didx[j] = __ldg(a.didx + e);
             p.ddata[j] = __ldg(a.ddata + e);
-        }
-    }
-    p.cmeta = 0;
-    if (relocating) {
-        const uint8_t* meta = a.cmeta + (T.src_off - a.timage_base) / 16;
-#pragma unroll
-        for (int k = 0; k < kChunksPerThread; ++k) {
-            const uint32_t c = tid + k * kThreads;
-            if (c < T.nchunks) p.cmeta |= uint32_t(__ldg(meta + c)) << (8 * k);
         }
     }
     const uint32_t nops = min(T.rop_hi - T.rop_lo, uint32_t(kOpSlots));
     for (uint32_t i = tid; i < nops; i += kThreads) cp_async16(&s.ops[i], a.rops + T.rop_lo + i);
     cp_async_commit();
+}
+
+// B: one diff entry -> its chunk of the staged tile, relocated in registers.
+__device__ __forceinline__ void apply_diff(uint4* buf, uint32_t word, uint4 v, const fdt_tile& T,
+                                           bool relocating, const FdyMaterializeArgs& a) {
+    if (relocating) v = relocate_chunk(v, word >> FDT_DIDX_LANE_SHIFT, a);
+    buf[(word & FDT_DIDX_CHUNK_MASK) - T.chunk_base] = v;
+}
+
+// K1 over the template images, once per launch: store -> scratch.
+__global__ void __launch_bounds__(kRelocThreads)
+fdy_relocate_templates_kernel(const FdyMaterializeArgs a) {
+    pdl_launch_dependents();  // the member grid's prologue may start now
+    const uint4* src = reinterpret_cast<const uint4*>(a.store + a.timage_base);
+    uint4* dst = reinterpret_cast<uint4*>(a.rtimg);
+    const uint64_t n = a.timage_bytes / 16;
+    for (uint64_t i = uint64_t(blockIdx.x) * kRelocThreads + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * kRelocThreads) {
+        const uint32_t lanes = __ldg(a.cmeta + i);
+        uint4 v = __ldg(src + i);
+        if (lanes) v = relocate_chunk(v, lanes, a);
+        dst[i] = v;
+    }
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -208,19 +247,19 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
         mbar_init(&s.bar[1], 1);
         fence_mbar_init();
     }
-    for (int i = tid; i < FDT_TILE_CHUNKS; i += kThreads) s.ometa[i] = 0;
     __syncthreads();
 
     uint32_t t = blockIdx.x;
     if (t >= a.n_tiles) return;
     fdt_tile T = a.tiles[t];
     fdt_tile Tn = load_tile(a, t + G);
+    Prefetch cur;
+    prefetch_tile(a, T, s, cur, tid);  // the store itself is never written
+    if (relocating) pdl_wait_primary();  // templates come from the relocated copy
     if (tid == 0) {
         mbar_expect_tx(&s.bar[0], T.nchunks * 16u);
-        bulk_load(s.buf[0], a.store + T.src_off, T.nchunks * 16u, &s.bar[0]);
+        bulk_load(s.buf[0], a.tsrc + T.src_off, T.nchunks * 16u, &s.bar[0]);
     }
-    Prefetch cur;
-    prefetch_tile(a, T, relocating, s, cur, tid);
 
     uint32_t stage = 0;
     uint32_t parity = 0u;  // bit s = expected phase parity of stage s
@@ -230,54 +269,22 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
         if (tid == 0 && has_next) {
             bulk_wait_reads();  // the previous store out of stage s^1 has drained
             mbar_expect_tx(&s.bar[stage ^ 1], Tn.nchunks * 16u);
-            bulk_load(s.buf[stage ^ 1], a.store + Tn.src_off, Tn.nchunks * 16u, &s.bar[stage ^ 1]);
+            bulk_load(s.buf[stage ^ 1], a.tsrc + Tn.src_off, Tn.nchunks * 16u, &s.bar[stage ^ 1]);
         }
         const fdt_tile Tnn = load_tile(a, t + 2 * G);  // consumed next iteration
         uint4* buf = s.buf[stage];
         mbar_wait(&s.bar[stage], (parity >> stage) & 1u);
         parity ^= 1u << stage;
 
-        // B: K2 diff overlay (operands in registers)
+        // B: K2 + K1 for the member's own chunks (operands in registers)
 #pragma unroll
-        for (int j = 0; j < kDiffRegs; ++j) {
-            if (T.diff_lo + tid + j * kThreads < T.diff_hi) {
-                const uint32_t c = cur.didx[j], dm = cur.dmeta[j];
-                buf[c] = merge_bytes(buf[c], cur.ddata[j], dm & FDT_DMETA_MASK);
-                if (relocating && (dm & FDT_DMETA_RELOC_OVERRIDE))
-                    s.ometa[c] = static_cast<uint8_t>(0x80u | ((dm >> FDT_DMETA_RELOC_SHIFT) & 3u));
-            }
-        }
-        for (uint32_t e = T.diff_lo + kDiffRegs * kThreads + tid; e < T.diff_hi; e += kThreads) {
-            const uint32_t c = __ldg(a.didx + e) - T.chunk_base;  // dense tiles only
-            const uint32_t dm = __ldg(a.dmeta + e);
-            buf[c] = merge_bytes(buf[c], __ldg(a.ddata + e), dm & FDT_DMETA_MASK);
-            if (relocating && (dm & FDT_DMETA_RELOC_OVERRIDE))
-                s.ometa[c] = static_cast<uint8_t>(0x80u | ((dm >> FDT_DMETA_RELOC_SHIFT) & 3u));
-        }
+        for (int j = 0; j < kDiffRegs; ++j)
+            if (T.diff_lo + tid + j * kThreads < T.diff_hi)
+                apply_diff(buf, cur.didx[j], cur.ddata[j], T, relocating, a);
+        for (uint32_t e = T.diff_lo + kDiffRegs * kThreads + tid; e < T.diff_hi; e += kThreads)
+            apply_diff(buf, __ldg(a.didx + e), __ldg(a.ddata + e), T, relocating, a);  // dense tiles only
         cp_async_wait_all();  // this tile's rank ops are in smem
         __syncthreads();
-
-        // C: K1 relocation of flagged lanes whose value lies in the captured range
-        if (relocating) {
-#pragma unroll
-            for (int k = 0; k < kChunksPerThread; ++k) {
-                const uint32_t c = tid + k * kThreads;
-                if (c >= T.nchunks) break;
-                uint32_t m = (cur.cmeta >> (8 * k)) & 0xFFu;
-                const uint32_t o = s.ometa[c];
-                if (o) {
-                    m = o & 3u;
-                    s.ometa[c] = 0;
-                }
-                if (m) {
-                    uint4 v = buf[c];
-                    relocate_pair(v.x, v.y, m & FDT_CMETA_LANE0, a);
-                    relocate_pair(v.z, v.w, m & FDT_CMETA_LANE1, a);
-                    buf[c] = v;
-                }
-            }
-            __syncthreads();
-        }
 
         // D: K3 rank ops; ops on one chunk are applied in table order by one thread
         const uint32_t nops = T.rop_hi - T.rop_lo;
@@ -295,9 +302,9 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
             buf[c] = v;
         }
         fence_proxy_async_smem();
-        __syncthreads();  // member tile complete; ops / ometa free for the next tile
+        __syncthreads();  // member tile complete; ops free for the next tile
         if (tid == 0) bulk_store(a.out + T.dst_off, buf, T.nchunks * 16u);
-        if (has_next) prefetch_tile(a, Tn, relocating, s, cur, tid);
+        if (has_next) prefetch_tile(a, Tn, s, cur, tid);
         T = Tn;
         Tn = Tnn;
         stage ^= 1u;
@@ -313,11 +320,31 @@ extern "C" cudaError_t fdy_launch_materialize(const FdyMaterializeArgs* args, in
                                               cudaStream_t stream) {
     if (args->n_tiles == 0) return cudaSuccess;
     // per-device attribute; cheap enough to set on every launch
-    const cudaError_t e = cudaFuncSetAttribute(
+    cudaError_t e = cudaFuncSetAttribute(
         fdy_materialize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(Smem)));
     if (e != cudaSuccess) return e;
-    fdy_materialize_kernel<<<grid, kThreads, sizeof(Smem), stream>>>(*args);
-    return cudaGetLastError();
+    if (args->delta == 0ull) {
+        fdy_materialize_kernel<<<grid, kThreads, sizeof(Smem), stream>>>(*args);
+        return cudaGetLastError();
+    }
+    if (args->rtimg == nullptr) return cudaErrorInvalidValue;
+    const uint64_t n = args->timage_bytes / 16;
+    const int rgrid = int(std::min<uint64_t>((n + kRelocThreads - 1) / kRelocThreads, 4096));
+    if (rgrid > 0) {
+        fdy_relocate_templates_kernel<<<rgrid, kRelocThreads, 0, stream>>>(*args);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sizeof(Smem);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fdy_materialize_kernel, *args);
 }
 
 extern "C" cudaError_t fdy_materialize_occupancy(int* blocks_per_sm) {

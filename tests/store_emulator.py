@@ -12,7 +12,7 @@ import struct
 import numpy as np
 
 HEADER = struct.Struct("<4sHHIIIIIIII")  # up to n_rank_ops
-SEC_NAMES = ["groups", "timages", "cmeta", "members", "tiles", "didx", "dmeta", "ddata",
+SEC_NAMES = ["groups", "timages", "cmeta", "members", "tiles", "didx", "ddata",
              "rops", "kernels", "nodeattrs", "edges", "strings"]
 
 TILE_DT = np.dtype([("src_off", "<u8"), ("dst_off", "<u8"), ("nchunks", "<u4"), ("member", "<u4"),
@@ -45,32 +45,37 @@ def expand(blob: bytes, rank: int, world: int, new_base: int = 0, values=()) -> 
     tiles = sec("tiles", TILE_DT)
     cmeta = sec("cmeta", np.uint8)
     didx = sec("didx", np.uint32)
-    dmeta = sec("dmeta", np.uint32)
     ddata = sec("ddata", np.uint8).reshape(-1, 16)
     rops = sec("rops", ROP_DT)
     timg_base = h["sec"]["timages"][0]
     old, span = h["old_base"], h["final_offset"]
     delta = (new_base - old) % (1 << 64) if new_base else 0
+
+    def relocate(chunks, lanes_of):
+        lanes = chunks.view("<u8").reshape(-1, 2)
+        for lane, bit in ((0, 1), (1, 2)):
+            v = lanes[:, lane]
+            sel = ((lanes_of & bit) != 0) & ((v - np.uint64(old)) < np.uint64(span))
+            v[sel] = v[sel] + np.uint64(delta)
+
+    # K1 once over the template images (the kernel's first grid)
+    toff, tn = h["sec"]["timages"]
+    timg = b[toff:toff + tn].copy().reshape(-1, 16)
+    if delta:
+        relocate(timg, cmeta.astype(np.uint32))
     out = np.zeros(h["members_image_bytes"], dtype=np.uint8)
     for t in tiles:
         n = int(t["nchunks"])
-        src = int(t["src_off"])
-        chunks = b[src:src + 16 * n].reshape(n, 16).copy()
-        meta = cmeta[(src - timg_base) // 16:(src - timg_base) // 16 + n].astype(np.uint32).copy()
+        first = (int(t["src_off"]) - timg_base) // 16
+        chunks = timg[first:first + n].copy()
         lo, hi = int(t["diff_lo"]), int(t["diff_hi"])
         if hi > lo:
-            rows = didx[lo:hi].astype(np.int64) - int(t["chunk_base"])
-            dm = dmeta[lo:hi]
-            bits = ((dm[:, None] >> np.arange(16, dtype=np.uint32)) & 1).astype(bool)
-            chunks[rows] = np.where(bits, ddata[lo:hi], chunks[rows])
-            ov = (dm & 0x10000) != 0
-            meta[rows[ov]] = (dm[ov] >> 17) & 3
-        if delta:
-            lanes = chunks.view("<u8").reshape(n, 2)
-            for lane, bit in ((0, 1), (1, 2)):
-                v = lanes[:, lane]
-                sel = ((meta & bit) != 0) & ((v - np.uint64(old)) < np.uint64(span))
-                v[sel] = v[sel] + np.uint64(delta)
+            words = didx[lo:hi]
+            rows = (words & 0x3FFFFFFF).astype(np.int64) - int(t["chunk_base"])
+            data = ddata[lo:hi].copy()
+            if delta:
+                relocate(data, words >> 30)
+            chunks[rows] = data
         flat = chunks.reshape(-1)
         for op in rops[int(t["rop_lo"]):int(t["rop_hi"])]:
             kind = int(op["kind"])
