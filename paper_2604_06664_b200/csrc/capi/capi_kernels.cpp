@@ -64,7 +64,7 @@ int fdy_store_fanout(const fdy_store* src, fdy_device* dst_dev, fdy_store** out)
         require(src && dst_dev && out, Errc::invalid_argument, "fdy_store_fanout: null argument");
         Device& d = *dst_dev->dev;
         Device& s = *src->owner->dev;
-        DeviceBuffer buf(d, src->store.bytes);
+        DeviceBuffer buf(d, src->store.bytes, /*shareable=*/true);
         src->owner->dev->sync();  // the source upload must have landed
         d.make_current();
         int can = 0;

@@ -34,6 +34,7 @@ bool cuda_available() { return cuda_device_count() > 0; }
 
 namespace {
 std::once_flag g_const_once[64];
+std::once_flag g_pool_once[64];
 }
 
 Device::Device(int ordinal) : ordinal_(ordinal) {
@@ -51,6 +52,14 @@ Device::Device(int ordinal) : ordinal_(ordinal) {
     std::call_once(g_const_once[ordinal_ & 63], [] {
         cuda_check(fdy_crc64_set_constants(crc64_x2k_table()), "CRC constant upload");
     });
+    // the default pool keeps what it is given back (see alloc())
+    std::call_once(g_pool_once[ordinal_ & 63], [this] {
+        cudaMemPool_t pool;
+        cuda_check(cudaDeviceGetDefaultMemPool(&pool, ordinal_), "cudaDeviceGetDefaultMemPool");
+        uint64_t keep = UINT64_MAX;
+        cuda_check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep),
+                   "cudaMemPoolSetAttribute(release threshold)");
+    });
 }
 
 Device::~Device() {
@@ -66,18 +75,24 @@ void Device::sync() const {
     cuda_check(cudaStreamSynchronize(copy_stream_), "cudaStreamSynchronize(copy)");
 }
 
-void* Device::alloc(size_t bytes) {
+void* Device::alloc(size_t bytes, bool shareable) {
     make_current();
     void* p = nullptr;
     if (bytes == 0) bytes = 16;
-    cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+    if (shareable)
+        cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+    else
+        cuda_check(cudaMallocAsync(&p, bytes, stream_), "cudaMallocAsync");
     return p;
 }
 
-void Device::release(void* p) {
+void Device::release(void* p, bool shareable) {
     if (!p) return;
     cudaSetDevice(ordinal_);
-    cudaFree(p);
+    if (shareable)
+        cudaFree(p);
+    else
+        cudaFreeAsync(p, stream_);
 }
 
 void* Device::alloc_host_pinned(size_t bytes) {
@@ -92,19 +107,21 @@ void Device::release_host_pinned(void* p) {
     if (p) cudaFreeHost(p);
 }
 
-DeviceBuffer::DeviceBuffer(Device& dev, size_t bytes)
-    : dev_(&dev), p_(static_cast<unsigned char*>(dev.alloc(bytes))), n_(bytes) {}
+DeviceBuffer::DeviceBuffer(Device& dev, size_t bytes, bool shareable)
+    : dev_(&dev), p_(static_cast<unsigned char*>(dev.alloc(bytes, shareable))), n_(bytes),
+      shareable_(shareable) {}
 
 DeviceBuffer::~DeviceBuffer() {
-    if (dev_) dev_->release(p_);
+    if (dev_) dev_->release(p_, shareable_);
 }
 
 DeviceBuffer& DeviceBuffer::operator=(DeviceBuffer&& o) noexcept {
     if (this != &o) {
-        if (dev_) dev_->release(p_);
+        if (dev_) dev_->release(p_, shareable_);
         dev_ = o.dev_;
         p_ = o.p_;
         n_ = o.n_;
+        shareable_ = o.shareable_;
         o.dev_ = nullptr;
         o.p_ = nullptr;
         o.n_ = 0;
@@ -158,7 +175,7 @@ DeviceStore upload_store(Device& dev, const void* host_blob, size_t bytes) {
     require(bytes >= sizeof(fdt_header), Errc::archive_corruption, "template store: truncated input");
     fdt_header h;
     std::memcpy(&h, host_blob, sizeof h);
-    DeviceBuffer buf(dev, bytes);
+    DeviceBuffer buf(dev, bytes, /*shareable=*/true);  // fdy_store_export may hand it to peers
     cuda_check(cudaMemcpyAsync(buf.data(), host_blob, bytes, cudaMemcpyHostToDevice, dev.stream()),
                "cudaMemcpyAsync(store H2D)");
     DeviceStore s = adopt_store(dev, buf.data(), bytes, h);
@@ -180,8 +197,8 @@ void launch_materialize(Device& dev, const DeviceStore& store, const Materialize
     a.rtimg = store.rtimages.data();
     a.tiles = reinterpret_cast<const fdt_tile*>(b + h.sec[FDT_SEC_TILES].offset);
     a.cmeta = b + h.sec[FDT_SEC_CMETA].offset;
-    a.didx = reinterpret_cast<const uint32_t*>(b + h.sec[FDT_SEC_DIDX].offset);
-    a.ddata = reinterpret_cast<const uint4*>(b + h.sec[FDT_SEC_DDATA].offset);
+    a.didx = reinterpret_cast<const uint16_t*>(b + h.sec[FDT_SEC_DIDX].offset);
+    a.ddata = reinterpret_cast<const uint64_t*>(b + h.sec[FDT_SEC_DDATA].offset);
     a.rops = reinterpret_cast<const fdt_rank_op*>(b + h.sec[FDT_SEC_ROPS].offset);
     a.values = d_values;
     a.n_values = d_values ? static_cast<uint32_t>(req.values.size()) : 0u;

@@ -121,6 +121,13 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const Manifest& 
     // read a piece, then queue its DMA right away: reads and H2D overlap
     dev.make_current();
     cudaStream_t copy = dev.copy_stream();
+    {  // device_ is stream-ordered on dev.stream(): the copies start after its allocation
+        cudaEvent_t allocated;
+        cuda_check(cudaEventCreateWithFlags(&allocated, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventRecord(allocated, dev.stream()), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(copy, allocated, 0), "cudaStreamWaitEvent");
+        cudaEventDestroy(allocated);
+    }
     parallel_for(pieces.size(), std::max(1u, lanes), [&](size_t i) {
         const Piece& pc = pieces[i];
         unsigned char* h = host_.data() + pc.f->offset + pc.off;

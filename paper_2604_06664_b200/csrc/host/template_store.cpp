@@ -114,11 +114,15 @@ void build_image(const CapturedGraph& g, const GroupLayout& L, const KernelTable
 }
 
 struct MemberOut {
-    std::vector<uint32_t> didx;   // chunk index (lanes packed in when merged)
-    std::vector<uint8_t> dlanes;  // the member chunk's relocation lanes
-    std::vector<uint8_t> ddata;
+    std::vector<uint32_t> dlane;  // 8-byte lane index within the member image
+    std::vector<uint8_t> dreloc;  // the lane's relocation flag in the member
+    std::vector<uint64_t> dval;   // the member's lane value
     std::vector<fdt_rank_op> rops;
 };
+
+bool lane_flag(const std::vector<uint8_t>& meta, uint64_t lane) {
+    return (meta[lane / 2] >> (lane % 2)) & 1u;
+}
 
 // Splits a little-endian write of `width` bytes at image byte offset `at`
 // into per-chunk ops.
@@ -148,6 +152,44 @@ uint64_t put_section(Sink& s, fdt_header& h, int id, const T* data, size_t count
     return h.sec[id].offset;
 }
 
+// apply_rank_patches (rank_forge.cpp:132-152) for graph g, split by what it
+// depends on: the stub -> real kernel swap is rank-independent, so it is
+// written into g's image here (and so lands in the template / diffs); the
+// rank and world writes become rank ops, in table order.
+void patch_graph(const CapturedGraph& g, const PatchTable& patches, const GroupLayout& L,
+                 const KernelTable& kt, uint64_t comm_real_hash, std::vector<uint8_t>& img,
+                 std::vector<fdt_rank_op>* rops) {
+    auto pit = patches.per_graph.find(g.label);
+    if (pit == patches.per_graph.end()) return;
+    for (const CommPatchEntry& e : pit->second) {
+        // the checks apply_rank_patches performs (rank_forge.cpp:136-150)
+        require(e.node_id < g.nodes.size(), Errc::archive_corruption,
+                "patch entry references missing node");
+        const GraphNode& n = g.nodes[e.node_id];
+        require(n.type == NodeType::Kernel, Errc::archive_corruption,
+                "patch entry references a non-kernel node");
+        const auto& kp = n.kernel_params();
+        require(kp.kernel == e.stub, Errc::archive_corruption,
+                "node " + std::to_string(e.node_id) + " is not the recorded stub " + e.stub.describe());
+        const uint32_t real = kt.lookup(KernelRef{comm_real_hash, e.real_name}, kp.func_attrs);
+        std::memcpy(img.data() + 48ull * e.node_id + offsetof(fdt_node, kernel), &real, 4);
+        const uint64_t blob = L.desc_bytes() + L.blob_off[e.node_id];
+        for (uint32_t off : e.rank_offsets) {
+            require(uint64_t(off) + 8 <= kp.arg_buffer.size(), Errc::invalid_argument,
+                    "patch offset outside the argument buffer");
+            if (rops) emit_write(*rops, blob + off, 8, FDT_ROP_RANK, 0);
+        }
+        for (uint32_t off : e.world_offsets) {
+            require(uint64_t(off) + 8 <= kp.arg_buffer.size(), Errc::invalid_argument,
+                    "patch offset outside the argument buffer");
+            if (rops) emit_write(*rops, blob + off, 8, FDT_ROP_WORLD, 0);
+        }
+    }
+    if (rops)
+        std::stable_sort(rops->begin(), rops->end(),
+                         [](const fdt_rank_op& a, const fdt_rank_op& b) { return a.chunk < b.chunk; });
+}
+
 }  // namespace
 
 std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
@@ -168,8 +210,8 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
     std::vector<uint32_t> edges;
     Sink timages;
     std::vector<uint8_t> cmeta;
-    std::vector<uint32_t> didx;
-    std::vector<uint8_t> ddata;
+    std::vector<uint16_t> didx;
+    std::vector<uint64_t> ddata;
     std::vector<fdt_rank_op> rops;
     std::vector<fdt_tile> tiles;
     uint64_t out_off = 0, total_nodes = 0;
@@ -249,6 +291,7 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
 
         std::vector<uint8_t> timg, tmeta;
         build_image(T, L, kt, timg, tmeta);
+        patch_graph(T, patches, L, kt, manifest.comm_real_hash, timg, nullptr);
         timages.align(16);
         G.timage_off = timages.size();  // rebased onto the section below
         timages.raw(timg);
@@ -261,52 +304,25 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
             MemberOut& o = outs[i];
             std::vector<uint8_t> img, meta;
             build_image(g, L, kt, img, meta);
-            const size_t nchunks = img.size() / 16;
-            require(nchunks <= FDT_DIDX_CHUNK_MASK, Errc::invalid_argument,
-                    "graph image exceeds the store's 2^30-chunk limit");
-            // A chunk whose bytes or relocation lanes differ from the template's
-            // is carried whole, with the member's lanes (store_format.h).
-            for (size_t c = 0; c < nchunks; ++c) {
-                if (meta[c] == tmeta[c] &&
-                    std::memcmp(img.data() + 16 * c, timg.data() + 16 * c, 16) == 0)
+            patch_graph(g, patches, L, kt, manifest.comm_real_hash, img, &o.rops);
+            // every 8-byte lane whose bytes or relocation flag differ from the
+            // template's becomes a diff entry (store_format.h)
+            const uint64_t nlanes = img.size() / 8;
+            for (uint64_t l = 0; l < nlanes; ++l) {
+                const bool f = lane_flag(meta, l);
+                if (f == lane_flag(tmeta, l) && std::memcmp(img.data() + 8 * l, timg.data() + 8 * l, 8) == 0)
                     continue;
-                o.didx.push_back(static_cast<uint32_t>(c));
-                o.dlanes.push_back(meta[c]);
-                o.ddata.insert(o.ddata.end(), img.begin() + 16 * c, img.begin() + 16 * c + 16);
+                uint64_t v;
+                std::memcpy(&v, img.data() + 8 * l, 8);
+                o.dlane.push_back(static_cast<uint32_t>(l));
+                o.dreloc.push_back(f ? 1 : 0);
+                o.dval.push_back(v);
             }
-            auto pit = patches.per_graph.find(g.label);
-            if (pit == patches.per_graph.end()) return;
-            for (const CommPatchEntry& e : pit->second) {
-                // the checks apply_rank_patches performs (rank_forge.cpp:136-150)
-                require(e.node_id < g.nodes.size(), Errc::archive_corruption,
-                        "patch entry references missing node");
-                const GraphNode& n = g.nodes[e.node_id];
-                require(n.type == NodeType::Kernel, Errc::archive_corruption,
-                        "patch entry references a non-kernel node");
-                const auto& kp = n.kernel_params();
-                require(kp.kernel == e.stub, Errc::archive_corruption,
-                        "node " + std::to_string(e.node_id) + " is not the recorded stub " +
-                            e.stub.describe());
-                const uint32_t real =
-                    kt.lookup(KernelRef{manifest.comm_real_hash, e.real_name}, kp.func_attrs);
-                emit_write(o.rops, 48ull * e.node_id + offsetof(fdt_node, kernel), 4,
-                           FDT_ROP_KERNEL, real);
-                const uint64_t blob = L.desc_bytes() + L.blob_off[e.node_id];
-                for (uint32_t off : e.rank_offsets) {
-                    require(uint64_t(off) + 8 <= kp.arg_buffer.size(), Errc::invalid_argument,
-                            "patch offset outside the argument buffer");
-                    emit_write(o.rops, blob + off, 8, FDT_ROP_RANK, 0);
-                }
-                for (uint32_t off : e.world_offsets) {
-                    require(uint64_t(off) + 8 <= kp.arg_buffer.size(), Errc::invalid_argument,
-                            "patch offset outside the argument buffer");
-                    emit_write(o.rops, blob + off, 8, FDT_ROP_WORLD, 0);
-                }
-            }
-            std::stable_sort(o.rops.begin(), o.rops.end(),
-                             [](const fdt_rank_op& a, const fdt_rank_op& b) { return a.chunk < b.chunk; });
         });
 
+        // members of a group whose rank ops for a tile are identical share
+        // one stored range (tile index -> op bytes -> range)
+        std::vector<std::map<std::string, std::pair<uint32_t, uint32_t>>> shared_ops;
         for (size_t i = 0; i < nm; ++i) {
             MemberOut& o = outs[i];
             fdt_member M{};
@@ -318,8 +334,9 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
             const uint64_t nchunks = L.image_bytes() / 16;
             const uint64_t ntiles = (nchunks + FDT_TILE_CHUNKS - 1) / FDT_TILE_CHUNKS;
             M.n_tiles = static_cast<uint32_t>(ntiles);
-            const uint32_t d0 = static_cast<uint32_t>(didx.size());
-            const uint32_t r0 = static_cast<uint32_t>(rops.size());
+            require(ntiles <= UINT32_MAX && L.image_bytes() / 8 <= UINT32_MAX, Errc::invalid_argument,
+                    "graph image exceeds the store's 32 GiB limit");
+            shared_ops.resize(std::max<size_t>(shared_ops.size(), ntiles));
             size_t dpos = 0, rpos = 0;
             for (uint64_t t = 0; t < ntiles; ++t) {
                 const uint64_t cb = t * FDT_TILE_CHUNKS;
@@ -330,18 +347,28 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
                 T.nchunks = static_cast<uint32_t>(ce - cb);
                 T.member = static_cast<uint32_t>(members.size());
                 T.chunk_base = static_cast<uint32_t>(cb);
-                T.diff_lo = d0 + static_cast<uint32_t>(dpos);
-                while (dpos < o.didx.size() && o.didx[dpos] < ce) ++dpos;
-                T.diff_hi = d0 + static_cast<uint32_t>(dpos);
-                T.rop_lo = r0 + static_cast<uint32_t>(rpos);
+                T.diff_lo = static_cast<uint32_t>(didx.size());
+                for (; dpos < o.dlane.size() && o.dlane[dpos] < 2 * ce; ++dpos) {
+                    didx.push_back(static_cast<uint16_t>((o.dlane[dpos] - 2 * cb) |
+                                                         (o.dreloc[dpos] ? FDT_DIDX_RELOC : 0u)));
+                    ddata.push_back(o.dval[dpos]);
+                }
+                T.diff_hi = static_cast<uint32_t>(didx.size());
+                const size_t r_begin = rpos;
                 while (rpos < o.rops.size() && o.rops[rpos].chunk < ce) ++rpos;
-                T.rop_hi = r0 + static_cast<uint32_t>(rpos);
+                const std::string key(reinterpret_cast<const char*>(o.rops.data() + r_begin),
+                                      (rpos - r_begin) * sizeof(fdt_rank_op));
+                auto [it, fresh] = shared_ops[t].try_emplace(key);
+                if (fresh) {
+                    it->second.first = static_cast<uint32_t>(rops.size());
+                    rops.insert(rops.end(), o.rops.begin() + static_cast<long>(r_begin),
+                                o.rops.begin() + static_cast<long>(rpos));
+                    it->second.second = static_cast<uint32_t>(rops.size());
+                }
+                T.rop_lo = it->second.first;
+                T.rop_hi = it->second.second;
                 tiles.push_back(T);
             }
-            for (size_t k = 0; k < o.didx.size(); ++k)
-                didx.push_back(o.didx[k] | uint32_t(o.dlanes[k]) << FDT_DIDX_LANE_SHIFT);
-            ddata.insert(ddata.end(), o.ddata.begin(), o.ddata.end());
-            rops.insert(rops.end(), o.rops.begin(), o.rops.end());
             members.push_back(M);
             out_off += L.image_bytes();
             total_nodes += L.n_nodes;

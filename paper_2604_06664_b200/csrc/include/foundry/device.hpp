@@ -36,8 +36,12 @@ public:
     void make_current() const;
     void sync() const;
 
-    void* alloc(size_t bytes);
-    void release(void* p);
+    // HBM. Ordinary buffers come from the device's stream-ordered pool
+    // (cudaMallocAsync on stream(); the pool keeps freed memory, so a second
+    // LOAD / prepare in the process does not pay cudaMalloc + cudaFree of
+    // ~400 MB again). `shareable` buffers (CUDA IPC export) use cudaMalloc.
+    void* alloc(size_t bytes, bool shareable = false);
+    void release(void* p, bool shareable = false);
     void* alloc_host_pinned(size_t bytes);
     void release_host_pinned(void* p);
 
@@ -52,7 +56,7 @@ private:
 class DeviceBuffer {
 public:
     DeviceBuffer() = default;
-    DeviceBuffer(Device& dev, size_t bytes);
+    DeviceBuffer(Device& dev, size_t bytes, bool shareable = false);
     ~DeviceBuffer();
     DeviceBuffer(DeviceBuffer&& o) noexcept { *this = std::move(o); }
     DeviceBuffer& operator=(DeviceBuffer&& o) noexcept;
@@ -67,6 +71,7 @@ private:
     Device* dev_ = nullptr;
     unsigned char* p_ = nullptr;
     size_t n_ = 0;
+    bool shareable_ = false;
 };
 
 class PinnedBuffer {

@@ -19,17 +19,20 @@
  * un-rank-patched (the captured state).
  *
  * Materialization of member m for (rank, world, new_base) =
- *   K2  copy the template image, replace the member's diff chunks;
+ *   K2  copy the template image, replace the member's diff lanes;
  *   K1  for every 8-byte lane marked relocatable (template chunk meta, or the
- *       lane bits of the diff entry for a replaced chunk) whose value v is in
+ *       flag of the diff entry for a replaced lane) whose value v is in
  *       [old_base, old_base + final_offset): v += new_base - old_base;
- *   K3  apply the member's rank ops (rank / world u64 writes, stub->real
- *       kernel index swap, per-rank value-table writes).
- * A diff entry exists for every chunk whose bytes OR relocation lanes differ
- * from the template's, and carries the member's whole chunk, so K1 commutes
- * with K2: relocating the template images once per launch (3 MB) and the
- * diff chunks in registers gives the per-member result, and the per-member
- * pass is copy + scatter + rank ops.
+ *   K3  apply the member's rank ops (rank / world u64 writes, per-rank
+ *       value-table writes).
+ * A diff entry exists for every 8-byte lane whose bytes OR relocation flag
+ * differ from the template's, and carries the member's whole lane, so K1
+ * commutes with K2: relocating the template images once per launch (3 MB)
+ * and the diff lanes in registers gives the per-member result, and the
+ * per-member pass is copy + scatter + rank ops.
+ * The rank-independent part of apply_rank_patches (the stub -> real kernel
+ * index swap) is applied at pack time, so it lives in the images; members of
+ * a group whose rank ops for a tile are identical share one op range.
  * The kernel works tile by tile: a tile is up to tile_chunks consecutive
  * 16-byte chunks of one member image; the packer precomputes each tile's
  * diff and rank-op ranges so a CTA needs one descriptor load to start.
@@ -39,7 +42,7 @@
 
 #include <stdint.h>
 
-#define FDT_VERSION 2u
+#define FDT_VERSION 3u
 #define FDT_TILE_CHUNKS 1024u /* 16 KiB of member image per tile */
 
 enum fdt_section_id {
@@ -48,8 +51,8 @@ enum fdt_section_id {
     FDT_SEC_CMETA,       /* 1 byte per 16-B chunk of TIMAGES            (device)      */
     FDT_SEC_MEMBERS,     /* fdt_member[n_members]                       (host+device) */
     FDT_SEC_TILES,       /* fdt_tile[n_tiles]                           (device)      */
-    FDT_SEC_DIDX,        /* u32 per diff entry: chunk | lanes << 30     (device)      */
-    FDT_SEC_DDATA,       /* 16 B per diff entry: the member chunk       (device)      */
+    FDT_SEC_DIDX,        /* u16 per diff entry: lane in tile | reloc    (device)      */
+    FDT_SEC_DDATA,       /* u64 per diff entry: the member's lane value (device)      */
     FDT_SEC_ROPS,        /* fdt_rank_op[n_rank_ops]                     (device)      */
     FDT_SEC_KERNELS,     /* fdt_kernel[n_kernels]                       (host)        */
     FDT_SEC_NODEATTRS,   /* fdt_node_attrs per template node            (host)        */
@@ -133,10 +136,10 @@ typedef struct {
     uint32_t pad;
 } fdt_tile;
 
-/* Diff entry index word: the chunk index within the member image (< 2^30)
- * and, in the top two bits, the member chunk's relocation lanes (FDT_CMETA_*). */
-#define FDT_DIDX_CHUNK_MASK 0x3FFFFFFFu
-#define FDT_DIDX_LANE_SHIFT 30
+/* Diff entry index: the 8-byte lane's index within its tile (< 2 x
+ * FDT_TILE_CHUNKS) and, in bit 15, the member lane's relocation flag. */
+#define FDT_DIDX_LANE_MASK 0x7FFFu
+#define FDT_DIDX_RELOC 0x8000u
 
 #define FDT_CMETA_LANE0 0x1u /* bytes 0-7 of the chunk are a relocatable slot */
 #define FDT_CMETA_LANE1 0x2u /* bytes 8-15 */
@@ -144,7 +147,9 @@ typedef struct {
 enum fdt_rank_op_kind {
     FDT_ROP_RANK = 0,   /* u64 rank   (CommPatchEntry.rank_offsets)  */
     FDT_ROP_WORLD = 1,  /* u64 world  (CommPatchEntry.world_offsets) */
-    FDT_ROP_KERNEL = 2, /* u32 kernel index = aux (stub -> real comm kernel) */
+    FDT_ROP_KERNEL = 2, /* u32 kernel index = aux (the packer folds the stub ->
+                           real swap into the images instead; kept for stores
+                           whose swap is rank-dependent) */
     FDT_ROP_VALUE = 3,  /* u64 per-rank value table[aux] (comm handles, peer buffers) */
 };
 
@@ -174,5 +179,9 @@ typedef struct {
     int32_t sync_remote;
     uint32_t attr_query; /* bool */
 } fdt_node_attrs;
+
+#if FDT_TILE_CHUNKS * 2 > FDT_DIDX_LANE_MASK + 1
+#error "tile lanes must fit the diff index"
+#endif
 
 #endif

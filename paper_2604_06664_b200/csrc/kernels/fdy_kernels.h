@@ -17,8 +17,8 @@ struct FdyMaterializeArgs {
     unsigned char* rtimg;        // relocated-template scratch (timage_bytes), delta != 0
     const fdt_tile* tiles;
     const uint8_t* cmeta;
-    const uint32_t* didx;
-    const uint4* ddata;
+    const uint16_t* didx;
+    const uint64_t* ddata;
     const fdt_rank_op* rops;
     const uint64_t* values;  // FDT_ROP_VALUE table (may be null)
     uint64_t timage_base;    // store offset of FDT_SEC_TIMAGES

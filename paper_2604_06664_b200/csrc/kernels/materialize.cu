@@ -2,8 +2,8 @@
 // -> K1 (VA relocation) -> K3 (rank / comm-state patch), one pass over HBM.
 //
 // K1 commutes with K2 by construction of the store (foundry/store_format.h):
-// a diff entry carries the member's whole 16-byte chunk plus its relocation
-// lanes. So a launch with delta != 0 is two grids on one stream:
+// a diff entry carries the member's whole 8-byte lane plus its relocation
+// flag. So a launch with delta != 0 is two grids on one stream:
 //
 //   fdy_relocate_templates   template images (3 MB for the 512-graph set)
 //                            -> relocated copy in the store's scratch, once
@@ -22,8 +22,8 @@
 //                  iteration later, so no phase waits on global memory)
 //   cp.async       tile t+1's rank ops -> smem
 //   ---- tile t, all operands already on chip ----
-//   B  (K2+K1)     one thread per diff entry: relocate its lanes in registers,
-//                  store the chunk over the template chunk
+//   B  (K2+K1)     one thread per diff entry: relocate its lane in registers,
+//                  store it over the template lane
 //   D  (K3)        one thread per chunk-run of rank ops, table order
 //   cp.async.bulk  smem -> global   member image tile (bulk_group)
 //
@@ -53,8 +53,8 @@ struct __align__(128) Smem {
 
 // Per-thread operands of one tile, loaded one iteration ahead.
 struct Prefetch {
-    uint32_t didx[kDiffRegs];  // chunk index within the tile | lanes << 30
-    uint4 ddata[kDiffRegs];
+    uint32_t didx[kDiffRegs];  // lane within the tile | FDT_DIDX_RELOC
+    uint64_t ddata[kDiffRegs];
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -203,7 +203,7 @@ __device__ __forceinline__ void prefetch_tile(const FdyMaterializeArgs& a, const
         const uint32_t e = T.diff_lo + tid + j * kThreads;
         if (e < T.diff_hi) {
             p.didx[j] = __ldg(a.didx + e);
-            p.ddata[j] = __ldg(a.ddata + e);
+            p.ddata[j] = __ldg(reinterpret_cast<const unsigned long long*>(a.ddata) + e);
         }
     }
     const uint32_t nops = min(T.rop_hi - T.rop_lo, uint32_t(kOpSlots));
@@ -211,11 +211,11 @@ __device__ __forceinline__ void prefetch_tile(const FdyMaterializeArgs& a, const
     cp_async_commit();
 }
 
-// B: one diff entry -> its chunk of the staged tile, relocated in registers.
-__device__ __forceinline__ void apply_diff(uint4* buf, uint32_t word, uint4 v, const fdt_tile& T,
-                                           bool relocating, const FdyMaterializeArgs& a) {
-    if (relocating) v = relocate_chunk(v, word >> FDT_DIDX_LANE_SHIFT, a);
-    buf[(word & FDT_DIDX_CHUNK_MASK) - T.chunk_base] = v;
+// B: one diff entry -> its lane of the staged tile, relocated in registers.
+__device__ __forceinline__ void apply_diff(uint4* buf, uint32_t word, uint64_t v, bool relocating,
+                                           const FdyMaterializeArgs& a) {
+    if (relocating && (word & FDT_DIDX_RELOC) && v - a.old_base < a.span) v += a.delta;
+    reinterpret_cast<uint64_t*>(buf)[word & FDT_DIDX_LANE_MASK] = v;
 }
 
 // K1 over the template images, once per launch: store -> scratch.
@@ -280,9 +280,11 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
 #pragma unroll
         for (int j = 0; j < kDiffRegs; ++j)
             if (T.diff_lo + tid + j * kThreads < T.diff_hi)
-                apply_diff(buf, cur.didx[j], cur.ddata[j], T, relocating, a);
+                apply_diff(buf, cur.didx[j], cur.ddata[j], relocating, a);
         for (uint32_t e = T.diff_lo + kDiffRegs * kThreads + tid; e < T.diff_hi; e += kThreads)
-            apply_diff(buf, __ldg(a.didx + e), __ldg(a.ddata + e), T, relocating, a);  // dense tiles only
+            apply_diff(buf, __ldg(a.didx + e),
+                       __ldg(reinterpret_cast<const unsigned long long*>(a.ddata) + e), relocating,
+                       a);  // dense tiles only
         cp_async_wait_all();  // this tile's rank ops are in smem
         __syncthreads();
 

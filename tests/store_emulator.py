@@ -44,8 +44,8 @@ def expand(blob: bytes, rank: int, world: int, new_base: int = 0, values=()) -> 
 
     tiles = sec("tiles", TILE_DT)
     cmeta = sec("cmeta", np.uint8)
-    didx = sec("didx", np.uint32)
-    ddata = sec("ddata", np.uint8).reshape(-1, 16)
+    didx = sec("didx", np.uint16)
+    ddata = sec("ddata", np.uint64)
     rops = sec("rops", ROP_DT)
     timg_base = h["sec"]["timages"][0]
     old, span = h["old_base"], h["final_offset"]
@@ -69,13 +69,13 @@ def expand(blob: bytes, rank: int, world: int, new_base: int = 0, values=()) -> 
         first = (int(t["src_off"]) - timg_base) // 16
         chunks = timg[first:first + n].copy()
         lo, hi = int(t["diff_lo"]), int(t["diff_hi"])
-        if hi > lo:
-            words = didx[lo:hi]
-            rows = (words & 0x3FFFFFFF).astype(np.int64) - int(t["chunk_base"])
-            data = ddata[lo:hi].copy()
+        if hi > lo:  # K2 + K1 on the member's own lanes
+            words = didx[lo:hi].astype(np.uint32)
+            vals = ddata[lo:hi].copy()
             if delta:
-                relocate(data, words >> 30)
-            chunks[rows] = data
+                sel = ((words & 0x8000) != 0) & ((vals - np.uint64(old)) < np.uint64(span))
+                vals[sel] = vals[sel] + np.uint64(delta)
+            chunks.view("<u8").reshape(-1)[(words & 0x7FFF).astype(np.int64)] = vals
         flat = chunks.reshape(-1)
         for op in rops[int(t["rop_lo"]):int(t["rop_hi"])]:
             kind = int(op["kind"])

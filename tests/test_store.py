@@ -5,6 +5,7 @@ from __future__ import annotations
 import os
 import struct
 
+import numpy as np
 import pytest
 
 import store_emulator as emu
@@ -44,9 +45,15 @@ def test_store_header_describes_the_archive(foundry, archives):
     assert h["source_graphs_crc"] == m["files"]["graphs.bin"]
     assert h["source_patch_crc"] == m["files"]["patch.bin"]
     assert h["tile_chunks"] == 1024
-    # 12 layers x 2 collectives -> 24 patch entries per graph, each: kernel swap
-    # (one 4-byte op) + rank + world (one op each, 8-byte aligned inside a chunk)
-    assert h["n_rank_ops"] == 512 * 24 * 3
+    # 12 layers x 2 collectives -> 24 patch entries per graph, each: rank + world
+    # (one op each, 8-byte aligned inside a chunk); the kernel swap is folded
+    # into the images. Every member of a group patches the same offsets, so a
+    # group's op ranges are stored once and shared by its members' tiles.
+    assert h["n_rank_ops"] == h["n_groups"] * 24 * 2
+    blob = open(os.path.join(arch, "templates.fdt"), "rb").read()
+    off, n = h["sec"]["tiles"]
+    tiles = np.frombuffer(blob, emu.TILE_DT, n // emu.TILE_DT.itemsize, off)
+    assert int((tiles["rop_hi"] - tiles["rop_lo"]).sum()) == 512 * 24 * 2
     alg = capi.algorithmic_bytes(h)
     assert alg["write"] == h["members_image_bytes"] and alg["read"] > 0
 
