@@ -289,13 +289,6 @@ uint64_t ServingContext::Impl::build_graph_for(uint32_t gi, uint32_t m, CUgraph&
                 void* extra[5];
                 size_t size;
                 kernel_params(d, blob, K, p, extra, &size);
-                static const bool one_fn = std::getenv("FOUNDRY_EXPERIMENT_ONE_FUNCTION") != nullptr;
-                static CUfunction first_fn = nullptr;
-                if (one_fn) {  // experiment: every node launches the same function
-                    if (!first_fn) first_fn = K.fn;
-                    p.func = first_fn;
-                    size = 192;
-                }
                 cu_check(api.cuGraphAddKernelNode(&node, graph, nullptr, 0, &p), "cuGraphAddKernelNode");
                 const fdt_node_attrs& a = view->node_attrs(gi, n);
                 const bool non_default = a.cluster[0] != 1 || a.cluster[1] != 1 || a.cluster[2] != 1 ||

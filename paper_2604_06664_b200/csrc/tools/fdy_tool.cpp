@@ -258,6 +258,119 @@ static int cmd_instbench(int argc, char** argv) {
             api.cuGraphDestroy(gs[k]);
         }
     }
+    // layered DAGs: `levels` levels of `width` nodes, node (l, i) depends on
+    // (l-1, i) and, when `fan` is set, on (l-1, 0) too; instantiated with `flags`
+    auto layered = [&](int levels, int width, bool fan, unsigned long long flags) {
+        CUgraph g;
+        cu_check(api.cuGraphCreate(&g, 0), "create");
+        std::vector<CUgraphNode> prev, cur;
+        for (int l = 0; l < levels; ++l) {
+            cur.assign(width, nullptr);
+            for (int i = 0; i < width; ++i) {
+                const auto* K = ks[(l * width + i) % ks.size()];
+                size_t size = K->arg_buffer_size;
+                void* extra[5] = {CU_LAUNCH_PARAM_BUFFER_POINTER, blob.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &size,
+                                  CU_LAUNCH_PARAM_END};
+                CUDA_KERNEL_NODE_PARAMS p;
+                std::memset(&p, 0, sizeof p);
+                p.func = K->fn;
+                p.gridDimX = p.gridDimY = p.gridDimZ = 1;
+                p.blockDimX = 128;
+                p.blockDimY = p.blockDimZ = 1;
+                p.extra = extra;
+                CUgraphNode deps[2];
+                size_t nd = 0;
+                if (l) {
+                    deps[nd++] = prev[i];
+                    if (fan && i) deps[nd++] = prev[0];
+                }
+                cu_check(api.cuGraphAddKernelNode(&cur[i], g, deps, nd, &p), "add");
+            }
+            prev = cur;
+        }
+        const auto t1 = std::chrono::steady_clock::now();
+        CUgraphExec x;
+        const CUresult r = api.cuGraphInstantiate(&x, g, flags);
+        const double inst_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
+        std::printf("layered %4d x %d fan %d flags %llu: instantiate %8.3f ms%s\n", levels, width, fan ? 1 : 0, flags,
+                    inst_ms, r ? " (failed)" : "");
+        if (!r) api.cuGraphExecDestroy(x);
+        api.cuGraphDestroy(g);
+    };
+    // the archive's own template topology (group 0) with one dummy kernel per
+    // node: edges added in bulk after the nodes vs inline at node creation
+    {
+        const auto store_blob = slurp(paths.root / "templates.fdt");
+        const StoreView view(store_blob);
+        const fdt_group& G = view.group(0);
+        const auto E = view.edges(0);
+        std::vector<std::vector<uint32_t>> preds(G.n_nodes);
+        for (uint32_t i = 0; i < G.n_edges; ++i) preds[E[2 * i + 1]].push_back(E[2 * i]);
+        // transitive reduction size (edges implied by another path)
+        size_t redundant = 0;
+        {
+            std::vector<std::vector<uint8_t>> reach(G.n_nodes, std::vector<uint8_t>(G.n_nodes, 0));
+            for (uint32_t v = 0; v < G.n_nodes; ++v)
+                for (uint32_t u : preds[v]) {
+                    reach[v][u] = 1;
+                    for (uint32_t w = 0; w < G.n_nodes; ++w) reach[v][w] |= reach[u][w];
+                }
+            for (uint32_t v = 0; v < G.n_nodes; ++v)
+                for (uint32_t u : preds[v])
+                    for (uint32_t u2 : preds[v])
+                        if (u2 != u && reach[u2][u]) {
+                            ++redundant;
+                            break;
+                        }
+        }
+        std::printf("template 0: %u nodes, %u edges, %zu implied by another path\n", G.n_nodes, G.n_edges,
+                    redundant);
+        for (int inline_deps = 0; inline_deps < 2; ++inline_deps) {
+            CUgraph g;
+            cu_check(api.cuGraphCreate(&g, 0), "create");
+            std::vector<CUgraphNode> ns(G.n_nodes);
+            for (uint32_t n = 0; n < G.n_nodes; ++n) {
+                const auto* K = ks[0];
+                size_t size = K->arg_buffer_size;
+                void* extra[5] = {CU_LAUNCH_PARAM_BUFFER_POINTER, blob.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &size,
+                                  CU_LAUNCH_PARAM_END};
+                CUDA_KERNEL_NODE_PARAMS p;
+                std::memset(&p, 0, sizeof p);
+                p.func = K->fn;
+                p.gridDimX = p.gridDimY = p.gridDimZ = 1;
+                p.blockDimX = 128;
+                p.blockDimY = p.blockDimZ = 1;
+                p.extra = extra;
+                std::vector<CUgraphNode> d;
+                if (inline_deps)
+                    for (uint32_t u : preds[n]) d.push_back(ns[u]);
+                cu_check(api.cuGraphAddKernelNode(&ns[n], g, d.data(), d.size(), &p), "add");
+            }
+            if (!inline_deps) {
+                std::vector<CUgraphNode> from(G.n_edges), to(G.n_edges);
+                for (uint32_t i = 0; i < G.n_edges; ++i) {
+                    from[i] = ns[E[2 * i]];
+                    to[i] = ns[E[2 * i + 1]];
+                }
+                cu_check(api.cuGraphAddDependencies(g, from.data(), to.data(), G.n_edges), "deps");
+            }
+            for (int rep = 0; rep < 2; ++rep) {
+                const auto t1 = std::chrono::steady_clock::now();
+                CUgraphExec x;
+                cu_check(api.cuGraphInstantiate(&x, g, 0), "inst");
+                const double ms =
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
+                std::printf("template 0 topology, %s edges: instantiate %8.3f ms\n",
+                            inline_deps ? "inline" : "bulk", ms);
+                api.cuGraphExecDestroy(x);
+            }
+            api.cuGraphDestroy(g);
+        }
+    }
+    layered(1000, 1, false, 0);  // warm-up
+    for (int width : {1, 2, 4, 7})
+        for (bool fan : {false, true}) layered(1036 / width, width, fan, 0);
+    for (unsigned long long flags : {1ull, 2ull, 4ull, 8ull}) layered(148, 7, true, flags);
     for (int rep = 0; rep < 1; ++rep) {
         run("same fn, independent", 1000, false, false, false, 0);
         run("same fn, chain", 1000, false, true, false, 0);
