@@ -398,7 +398,7 @@ def main():
                       "breakdown": {k: v for k, v in bd.items() if k.endswith("_ms")}},
         "cpu_baseline": cpu,
         "clocks": clocks,
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * (2 if delta else 1),  # relocation grid + member grid
         "fanout": {"mode": args.fanout if gworld > 1 else "none", "ms": fanout_ms,
                    "store_bytes": len(blob)},
     }

@@ -54,6 +54,8 @@ void load_all() {
     FDY_RESOLVE(cuKernelGetFunction);
     FDY_RESOLVE(cuFuncSetAttribute);
     FDY_RESOLVE(cuFuncGetAttribute);
+    FDY_RESOLVE(cuKernelSetAttribute);
+    FDY_RESOLVE(cuCtxGetDevice);
     FDY_RESOLVE(cuGraphCreate);
     FDY_RESOLVE(cuGraphDestroy);
     FDY_RESOLVE(cuGraphAddKernelNode);

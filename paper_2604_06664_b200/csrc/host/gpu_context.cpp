@@ -14,7 +14,13 @@ uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 std::string key_of(uint64_t hash, std::string_view name) { return hex16(hash) + "|" + std::string(name); }
 }  // namespace
 
-GpuContext::GpuContext(Device& dev) : dev_(dev) { driver(); }
+GpuContext::GpuContext(Device& dev) : dev_(dev) {
+    const DriverApi& api = driver();
+    dev_.make_current();
+    CUdevice d = 0;
+    cu_check(api.cuCtxGetDevice(&d), "cuCtxGetDevice");
+    cu_device_ = d;
+}
 
 GpuContext::~GpuContext() {
     const DriverApi* api = nullptr;
@@ -34,29 +40,78 @@ GpuContext::~GpuContext() {
 
 // ------------------------------------------------------------------ libraries
 
+GpuContext::OpenedLibrary GpuContext::open_library(const KernelImage& image,
+                                                   std::span<const uint8_t> cubin) const {
+    const DriverApi& api = driver();
+    dev_.make_current();
+    OpenedLibrary o;
+    cu_check(api.cuLibraryLoadData(&o.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
+             "cuLibraryLoadData");
+    try {
+        size_t sz = 0;
+        cu_check(api.cuLibraryGetGlobal(&o.ctx_global, &sz, o.lib, "fdy_trace_context"),
+                 "cuLibraryGetGlobal(fdy_trace_context)");
+        cu_check(api.cuLibraryGetGlobal(&o.init_global, &sz, o.lib, "fdy_device_inited"),
+                 "cuLibraryGetGlobal(fdy_device_inited)");
+        o.kernels.resize(image.entrypoints.size());
+        for (size_t i = 0; i < image.entrypoints.size(); ++i)
+            cu_check(api.cuLibraryGetKernel(&o.kernels[i], o.lib, image.entrypoints[i].name.c_str()),
+                     "cuLibraryGetKernel");
+    } catch (...) {
+        api.cuLibraryUnload(o.lib);
+        throw;
+    }
+    return o;
+}
+
 uint32_t GpuContext::load_library(uint64_t hash, const KernelImage& image,
                                   std::span<const uint8_t> cubin, uint32_t ordinal,
                                   bool requires_init) {
-    const DriverApi& api = driver();
-    dev_.make_current();
+    return register_library(hash, image, open_library(image, cubin), ordinal, requires_init);
+}
+
+CUfunction GpuContext::function(const Kernel& k) const {
+    std::lock_guard lock(fn_mu_);
+    if (!k.fn) {
+        dev_.make_current();
+        cu_check(driver().cuKernelGetFunction(&k.fn, k.kern), "cuKernelGetFunction");
+    }
+    return k.fn;
+}
+
+void GpuContext::set_kernel_attribute(const Kernel& k, CUfunction_attribute attr, int value) const {
+    cu_check(driver().cuKernelSetAttribute(attr, value, k.kern, cu_device_), "cuKernelSetAttribute");
+}
+
+void GpuContext::require_dynamic_smem(const Kernel& k, int bytes) const {
+    std::lock_guard lock(fn_mu_);
+    if (bytes <= k.max_dynamic_smem) return;
+    set_kernel_attribute(k, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, bytes);
+    k.max_dynamic_smem = bytes;
+}
+
+void GpuContext::set_carveout(const Kernel& k, int percent) const {
+    std::lock_guard lock(fn_mu_);
+    if (percent == k.carveout) return;
+    set_kernel_attribute(k, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, percent);
+    k.carveout = percent;
+}
+
+uint32_t GpuContext::register_library(uint64_t hash, const KernelImage& image, OpenedLibrary&& o,
+                                      uint32_t ordinal, bool requires_init) {
     Library L;
     L.hash = hash;
     L.requires_init = requires_init;
-    cu_check(api.cuLibraryLoadData(&L.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
-             "cuLibraryLoadData");
-    size_t sz = 0;
-    cu_check(api.cuLibraryGetGlobal(&L.ctx_global, &sz, L.lib, "fdy_trace_context"),
-             "cuLibraryGetGlobal(fdy_trace_context)");
-    cu_check(api.cuLibraryGetGlobal(&L.init_global, &sz, L.lib, "fdy_device_inited"),
-             "cuLibraryGetGlobal(fdy_device_inited)");
+    L.lib = o.lib;
+    L.ctx_global = o.ctx_global;
+    L.init_global = o.init_global;
+    o.lib = nullptr;
     const uint32_t li = static_cast<uint32_t>(libs_.size());
     libs_.push_back(L);
     for (uint32_t i = 0; i < image.entrypoints.size(); ++i) {
         const KernelEntry& e = image.entrypoints[i];
         Kernel k;
-        CUkernel ck = nullptr;
-        cu_check(api.cuLibraryGetKernel(&ck, L.lib, e.name.c_str()), "cuLibraryGetKernel");
-        cu_check(api.cuKernelGetFunction(&k.fn, ck), "cuKernelGetFunction");
+        k.kern = o.kernels[i];
         k.library = li;
         k.entry_index = i;
         k.entry_id = (ordinal << 16) | i;

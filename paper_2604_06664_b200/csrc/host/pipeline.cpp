@@ -5,6 +5,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstddef>
 #include <cstdio>
@@ -133,6 +134,8 @@ struct ServingContext::Impl {
     }
 
     void restore_binaries();
+    void open_binary(uint64_t hash, const KernelBinaryRecord& rec, uint32_t ordinal, KernelImage& image,
+                     GpuContext::OpenedLibrary& opened);
     void build_group(uint32_t g);
     uint64_t build_graph_for(uint32_t g, uint32_t m, CUgraph& graph, std::vector<CUgraphNode>& nodes);
     void kernel_params(const fdt_node& d, const uint8_t* blob, const GpuContext::Kernel& K,
@@ -146,11 +149,51 @@ struct ServingContext::Impl {
 
 // ---------------------------------------------------------------- restore
 
+// restore_binaries (binary_catalog.cpp:200-227): every cataloged binary is
+// checked, parsed and opened (cuLibraryLoadData + cuLibraryGetKernel) on
+// `prepare_lanes` host threads — the driver's library load scales with
+// threads — then registered and device-inited in catalog order on this one.
 void ServingContext::Impl::restore_binaries() {
+    struct Item {
+        uint64_t hash;
+        const KernelBinaryRecord* rec;
+        uint32_t ordinal;
+        KernelImage image;
+        GpuContext::OpenedLibrary opened;
+    };
+    std::vector<Item> items;
     uint32_t ordinal = 0;
     for (const auto& [hash, rec] : catalog.binaries) {
         const uint32_t ord = ordinal++;
         if (ctx->has_library(hash)) continue;  // a second restore is a no-op
+        items.push_back(Item{hash, &rec, ord, {}, {}});
+    }
+    const unsigned lanes = std::max(1u, std::min(opts.prepare_lanes, 8u));
+    std::vector<std::exception_ptr> failed(items.size());
+    parallel_for(items.size(), lanes, [&](size_t i) {
+        try {
+            open_binary(items[i].hash, *items[i].rec, items[i].ordinal, items[i].image, items[i].opened);
+        } catch (...) {
+            failed[i] = std::current_exception();
+        }
+    });
+    // the first failure in catalog order is the one reported, as sequentially
+    for (size_t i = 0; i < items.size(); ++i) {
+        if (!failed[i]) continue;
+        for (Item& it : items)
+            if (it.opened.lib) driver().cuLibraryUnload(it.opened.lib);
+        std::rethrow_exception(failed[i]);
+    }
+    for (Item& it : items) {
+        const uint32_t lib = ctx->register_library(it.hash, it.image, std::move(it.opened), it.ordinal,
+                                                   it.rec->needs_device_init);
+        if (it.rec->needs_device_init && !opts.faults.skip_device_init) ctx->run_device_init(lib);
+    }
+}
+
+void ServingContext::Impl::open_binary(uint64_t hash, const KernelBinaryRecord& rec, uint32_t ord,
+                                       KernelImage& image_out, GpuContext::OpenedLibrary& opened) {
+    {
         const std::string rel = "binaries/" + hex16(hash) + ".bin";
         std::vector<uint8_t> fetched;
         std::span<const uint8_t> payload;
@@ -177,8 +220,8 @@ void ServingContext::Impl::restore_binaries() {
             built = compile_ptx_to_cubin(trace_module_ptx(image, ord, rec.needs_device_init));
             cubin = built;
         }
-        const uint32_t lib = ctx->load_library(hash, image, cubin, ord, rec.needs_device_init);
-        if (rec.needs_device_init && !opts.faults.skip_device_init) ctx->run_device_init(lib);
+        opened = ctx->open_library(image, cubin);
+        image_out = std::move(image);
     }
 }
 
@@ -194,7 +237,7 @@ void ServingContext::Impl::kernel_params(const fdt_node& d, const uint8_t* blob,
                                          const GpuContext::Kernel& K, CUDA_KERNEL_NODE_PARAMS& p,
                                          void** extra, size_t* size) const {
     std::memset(&p, 0, sizeof p);
-    p.func = K.fn;
+    p.kern = K.kern;  // func = null: the driver resolves the kernel in the current context
     p.gridDimX = d.grid[0];
     p.gridDimY = d.grid[1];
     p.gridDimZ = d.grid[2];
@@ -266,13 +309,8 @@ uint64_t ServingContext::Impl::build_graph_for(uint32_t gi, uint32_t m, CUgraph&
                     std::to_string(d.blob_len) + " < " + std::to_string(K.arg_buffer_size) + ")");
         const FuncAttrs fa = view->kernel_func_attrs(d.kernel);
         const int want = std::max<int>(fa.max_dynamic_shared_size_bytes, static_cast<int>(d.shmem));
-        if (want > 48 * 1024)
-            cu_check(api.cuFuncSetAttribute(K.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, want),
-                     "cuFuncSetAttribute(max dynamic smem)");
-        if (fa.preferred_shared_memory_carveout >= 0)
-            cu_check(api.cuFuncSetAttribute(K.fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT,
-                                            fa.preferred_shared_memory_carveout),
-                     "cuFuncSetAttribute(carveout)");
+        if (want > 48 * 1024) ctx->require_dynamic_smem(K, want);
+        if (fa.preferred_shared_memory_carveout >= 0) ctx->set_carveout(K, fa.preferred_shared_memory_carveout);
     }
 
     cu_check(api.cuGraphCreate(&graph, 0), "cuGraphCreate");
@@ -711,6 +749,9 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     // host threads construct + instantiate them (1 = the reference's single lane)
     unsigned build_lanes = 1;
     if (const char* env = std::getenv("FOUNDRY_BUILD_LANES")) build_lanes = std::max(1, std::atoi(env));
+    // (the driver loads each kernel's function lazily when its first node is
+    // added; a separate loader thread ahead of the builder measured no gain:
+    // function loads and instantiation serialize inside the driver)
     std::thread builder([&] {
         try {
             parallel_for(H.n_groups, build_lanes, [&](size_t g) { I.build_group(static_cast<uint32_t>(g)); });
@@ -878,7 +919,7 @@ bool ServingContext::fresh_capture_check(uint32_t batch, std::string* report) {
             size_t size = K.arg_buffer_size;
             void* extra[5] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<uint8_t*>(blob),
                               CU_LAUNCH_PARAM_BUFFER_SIZE, &size, CU_LAUNCH_PARAM_END};
-            cu_check(api.cuLaunchKernel(K.fn, d.grid[0], d.grid[1], d.grid[2], d.block[0], d.block[1],
+            cu_check(api.cuLaunchKernel(ctx.function(K), d.grid[0], d.grid[1], d.grid[2], d.block[0], d.block[1],
                                         d.block[2], d.shmem, st, nullptr, extra),
                      "cuLaunchKernel(capture)");
         } else if (d.type == 1) {

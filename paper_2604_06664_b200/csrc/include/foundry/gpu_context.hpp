@@ -49,7 +49,10 @@ public:
 
     // ------------------------------------------------------------ libraries
     struct Kernel {
-        CUfunction fn = nullptr;
+        CUkernel kern = nullptr;           // context-independent handle (graph nodes use this)
+        mutable CUfunction fn = nullptr;   // loaded on demand, see function()
+        mutable int max_dynamic_smem = 0;  // attribute values already applied
+        mutable int carveout = -1;
         uint32_t library = 0;
         uint32_t entry_index = 0;
         uint32_t entry_id = 0;
@@ -58,9 +61,31 @@ public:
         std::string name;
         uint64_t binary_hash = 0;
     };
-    // Loads one cataloged binary (its sm_100a cubin) and registers its entrypoints.
+    // A loaded library before registration: only driver calls, so several
+    // host threads may open libraries concurrently (cuLibraryLoadData scales
+    // with threads). Entry functions are not forced into the context here:
+    // graph nodes reference the CUkernel and the driver loads each function
+    // when a graph is instantiated (lazy loading).
+    struct OpenedLibrary {
+        CUlibrary lib = nullptr;
+        CUdeviceptr ctx_global = 0;
+        CUdeviceptr init_global = 0;
+        std::vector<CUkernel> kernels;  // image.entrypoints order
+    };
+    OpenedLibrary open_library(const KernelImage& image, std::span<const uint8_t> cubin) const;
+    // Registers an opened library and its entrypoints (single thread).
+    uint32_t register_library(uint64_t hash, const KernelImage& image, OpenedLibrary&& opened,
+                              uint32_t ordinal, bool requires_device_init);
+    // open_library + register_library.
     uint32_t load_library(uint64_t hash, const KernelImage& image, std::span<const uint8_t> cubin,
                           uint32_t ordinal, bool requires_device_init);
+    // The kernel's CUfunction in this context (cuKernelGetFunction on first use).
+    CUfunction function(const Kernel& k) const;
+    void set_kernel_attribute(const Kernel& k, CUfunction_attribute attr, int value) const;
+    // Per-kernel launch attributes, applied once: the dynamic shared memory
+    // limit only ever grows (every node of the kernel must fit).
+    void require_dynamic_smem(const Kernel& k, int bytes) const;
+    void set_carveout(const Kernel& k, int percent) const;
     void run_device_init(uint32_t library);
     bool library_device_inited(uint32_t library) const;
     bool library_requires_init(uint32_t library) const;
@@ -115,6 +140,8 @@ private:
     void mark(uint64_t addr, uint64_t len, bool on);
 
     Device& dev_;
+    int cu_device_ = 0;
+    mutable std::mutex fn_mu_;
     std::vector<Library> libs_;
     std::unordered_map<std::string, uint32_t> kernel_index_;  // hash|name -> kernels_
     std::vector<Kernel> kernels_;

@@ -156,6 +156,62 @@ static int cmd_load(int argc, char** argv) {
     return 0;
 }
 
+// restorebench <archive>: where the binary-restore time goes (driver-cost
+// study): cuLibraryLoadData alone, + cuLibraryGetKernel, + cuKernelGetFunction,
+// sequential and from T host threads.
+static int cmd_restorebench(int argc, char** argv) {
+    (void)argc;
+    ArchivePaths paths{argv[2]};
+    Device dev(0);
+    const DriverApi& api = driver();
+    const Catalog cat = parse_catalog(slurp(paths.catalog()));
+    struct Bin {
+        std::vector<uint8_t> cubin;
+        std::vector<std::string> names;
+    };
+    std::vector<Bin> bins;
+    for (const auto& [hash, rec] : cat.binaries) {
+        Bin b;
+        b.cubin = slurp(paths.cubin(hash));
+        for (const auto& e : parse_kernel_image(slurp(paths.binary(hash))).entrypoints) b.names.push_back(e.name);
+        bins.push_back(std::move(b));
+    }
+    auto run = [&](const char* label, int stage, int threads) {
+        std::vector<CUlibrary> libs(bins.size(), nullptr);
+        std::atomic<size_t> next{0};
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (int t = 0; t < threads; ++t)
+            pool.emplace_back([&] {
+                dev.make_current();
+                for (size_t i; (i = next.fetch_add(1)) < bins.size();) {
+                    cu_check(api.cuLibraryLoadData(&libs[i], bins[i].cubin.data(), nullptr, nullptr, 0, nullptr,
+                                                   nullptr, 0),
+                             "load");
+                    if (stage < 1) continue;
+                    for (const auto& n : bins[i].names) {
+                        CUkernel k;
+                        cu_check(api.cuLibraryGetKernel(&k, libs[i], n.c_str()), "getkernel");
+                        if (stage < 2) continue;
+                        CUfunction f;
+                        cu_check(api.cuKernelGetFunction(&f, k), "getfunction");
+                    }
+                }
+            });
+        for (auto& t : pool) t.join();
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        std::printf("%-40s threads %2d: %8.3f ms for %zu libraries\n", label, threads, ms, bins.size());
+        for (CUlibrary l : libs) api.cuLibraryUnload(l);
+    };
+    run("warm-up", 2, 1);
+    for (int threads : {1, 4, 16}) {
+        run("cuLibraryLoadData", 0, threads);
+        run("+ cuLibraryGetKernel", 1, threads);
+        run("+ cuKernelGetFunction", 2, threads);
+    }
+    return 0;
+}
+
 // instbench <archive>: cost of cuGraphInstantiate for N-node graphs under
 // different node/edge/attribute/parameter variants (driver-cost study).
 static int cmd_instbench(int argc, char** argv) {
@@ -186,7 +242,7 @@ static int cmd_instbench(int argc, char** argv) {
                               CU_LAUNCH_PARAM_END};
             CUDA_KERNEL_NODE_PARAMS p;
             std::memset(&p, 0, sizeof p);
-            p.func = K->fn;
+            p.func = ctx.function(*K);
             p.gridDimX = p.gridDimY = p.gridDimZ = 1;
             p.blockDimX = 128;
             p.blockDimY = p.blockDimZ = 1;
@@ -227,7 +283,7 @@ static int cmd_instbench(int argc, char** argv) {
                                   CU_LAUNCH_PARAM_END};
                 CUDA_KERNEL_NODE_PARAMS p;
                 std::memset(&p, 0, sizeof p);
-                p.func = K->fn;
+                p.func = ctx.function(*K);
                 p.gridDimX = p.gridDimY = p.gridDimZ = 1;
                 p.blockDimX = 128;
                 p.blockDimY = p.blockDimZ = 1;
@@ -273,7 +329,7 @@ static int cmd_instbench(int argc, char** argv) {
                                   CU_LAUNCH_PARAM_END};
                 CUDA_KERNEL_NODE_PARAMS p;
                 std::memset(&p, 0, sizeof p);
-                p.func = K->fn;
+                p.func = ctx.function(*K);
                 p.gridDimX = p.gridDimY = p.gridDimZ = 1;
                 p.blockDimX = 128;
                 p.blockDimY = p.blockDimZ = 1;
@@ -336,7 +392,7 @@ static int cmd_instbench(int argc, char** argv) {
                                   CU_LAUNCH_PARAM_END};
                 CUDA_KERNEL_NODE_PARAMS p;
                 std::memset(&p, 0, sizeof p);
-                p.func = K->fn;
+                p.func = ctx.function(*K);
                 p.gridDimX = p.gridDimY = p.gridDimZ = 1;
                 p.blockDimX = 128;
                 p.blockDimY = p.blockDimZ = 1;
@@ -436,6 +492,7 @@ int main(int argc, char** argv) {
         if (cmd == "save") return cmd_save(argc, argv);
         if (cmd == "load") return cmd_load(argc, argv);
         if (cmd == "instbench") return cmd_instbench(argc, argv);
+        if (cmd == "restorebench") return cmd_restorebench(argc, argv);
         if (cmd == "naive") {
             ServingContext sc = load(argv[2], LoadOptions{});
             std::printf("naive construction calls %llu\n", (unsigned long long)sc.naive_rebuild_all());
