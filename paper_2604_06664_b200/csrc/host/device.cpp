@@ -224,6 +224,9 @@ void launch_materialize(Device& dev, const DeviceStore& store, const Materialize
     if (timing) {
         cuda_check(cudaEventCreate(&e0), "cudaEventCreate");
         cuda_check(cudaEventCreate(&e1), "cudaEventCreate");
+        // hold the stream while the launches are submitted: the events then
+        // bracket device time only (the host's launch latency is not in it)
+        cuda_check(fdy_launch_gate(dev.stream(), 50000), "gate kernel launch");
         cuda_check(cudaEventRecord(e0, dev.stream()), "cudaEventRecord");
     }
     cuda_check(fdy_launch_materialize(&a, grid, dev.stream()), "materialize kernel launch");

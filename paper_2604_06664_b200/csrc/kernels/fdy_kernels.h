@@ -40,6 +40,8 @@ struct FdyCrcBlock {
 
 extern "C" {
 size_t fdy_materialize_smem_bytes();
+// A one-thread kernel that holds `stream` for `ns` ns (see materialize.cu).
+cudaError_t fdy_launch_gate(cudaStream_t stream, uint64_t ns);
 cudaError_t fdy_materialize_occupancy(int* blocks_per_sm);
 // delta == 0: one grid. Otherwise the template relocation grid, then the
 // member grid under programmatic dependent launch (both on `stream`).

@@ -33,6 +33,7 @@
 // streaming: no tensor-core work exists here, the bound is HBM bandwidth.
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
 
 #include "foundry/store_format.h"
 #include "fdy_kernels.h"
@@ -314,16 +315,45 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
     if (tid == 0) bulk_wait_all();
 }
 
+// Holds the stream for `ns` nanoseconds (globaltimer). Timed launches queue
+// behind it, so the CUDA events around them measure device time only, not
+// the host's submission of the launches.
+__global__ void fdy_gate_kernel(uint64_t ns) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        __nanosleep(1000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+
+cudaError_t set_smem_attribute_once() {
+    static std::once_flag once[64];
+    static cudaError_t result[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::call_once(once[dev & 63], [&] {
+        result[dev & 63] = cudaFuncSetAttribute(fdy_materialize_kernel,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(sizeof(Smem)));
+    });
+    return result[dev & 63];
+}
+
 }  // namespace
+
+extern "C" cudaError_t fdy_launch_gate(cudaStream_t stream, uint64_t ns) {
+    fdy_gate_kernel<<<1, 1, 0, stream>>>(ns);
+    return cudaGetLastError();
+}
 
 extern "C" size_t fdy_materialize_smem_bytes() { return sizeof(Smem); }
 
 extern "C" cudaError_t fdy_launch_materialize(const FdyMaterializeArgs* args, int grid,
                                               cudaStream_t stream) {
     if (args->n_tiles == 0) return cudaSuccess;
-    // per-device attribute; cheap enough to set on every launch
-    cudaError_t e = cudaFuncSetAttribute(
-        fdy_materialize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(Smem)));
+    cudaError_t e = set_smem_attribute_once();  // per device
     if (e != cudaSuccess) return e;
     if (args->delta == 0ull) {
         fdy_materialize_kernel<<<grid, kThreads, sizeof(Smem), stream>>>(*args);
@@ -350,9 +380,7 @@ extern "C" cudaError_t fdy_launch_materialize(const FdyMaterializeArgs* args, in
 }
 
 extern "C" cudaError_t fdy_materialize_occupancy(int* blocks_per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(fdy_materialize_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(sizeof(Smem)));
+    const cudaError_t e = set_smem_attribute_once();
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fdy_materialize_kernel,
                                                          kThreads, sizeof(Smem));
