@@ -112,7 +112,7 @@ int fdy_store_import(fdy_device* dev, const unsigned char handle[64], uint64_t b
         std::memcpy(&h, handle, sizeof h);
         void* peer = nullptr;
         cuda_check(cudaIpcOpenMemHandle(&peer, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-        DeviceBuffer buf(d, bytes);
+        DeviceBuffer buf(d, bytes, /*shareable=*/true);  // may be exported onwards
         // GPU -> GPU pull; NVLink P2P between the two devices
         const cudaError_t e = cudaMemcpyAsync(buf.data(), peer, bytes, cudaMemcpyDeviceToDevice, d.stream());
         const cudaError_t s = e == cudaSuccess ? cudaStreamSynchronize(d.stream()) : e;

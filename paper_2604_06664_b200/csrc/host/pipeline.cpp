@@ -731,6 +731,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     I.h_members.reset(new uint8_t[std::max<uint64_t>(H.members_image_bytes, 16)]);
     I.h_present.assign(H.n_members, 0);
     MaterializeTiming mt;
+    mt.gate = false;  // inside LOAD: no stream hold for the events
     launch_materialize(device, I.dstore, req, I.d_members.data(), &mt);
     I.t.materialize_kernel_ms = mt.kernel_ms;
     I.t.materialize_ms = ms_since(t0);

@@ -33,6 +33,7 @@ public:
     int sm_count() const { return sm_count_; }
     cudaStream_t stream() const { return stream_; }
     cudaStream_t copy_stream() const { return copy_stream_; }
+    cudaStream_t side_stream() const { return side_stream_; }  // integrity CRC work
     void make_current() const;
     void sync() const;
 
@@ -50,6 +51,7 @@ private:
     int sm_count_ = 0;
     cudaStream_t stream_ = nullptr;
     cudaStream_t copy_stream_ = nullptr;
+    cudaStream_t side_stream_ = nullptr;
 };
 
 // Device-resident buffer with RAII release.
@@ -113,6 +115,7 @@ struct MaterializeRequest {
 };
 
 struct MaterializeTiming {
+    bool gate = true;       // hold the stream while submitting (events = device time only)
     float kernel_ms = 0.f;  // CUDA-event time of the fused kernel, launching stream
     int grid = 0;
     int blocks_per_sm = 0;

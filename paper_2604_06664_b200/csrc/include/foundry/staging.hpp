@@ -49,6 +49,9 @@ struct StagedFile {
     std::string rel;
     uint64_t offset = 0;  // in host staging and in device staging
     uint64_t length = 0;
+    uint32_t segment = 0;      // index in staging order
+    uint32_t first_block = 0;  // CRC block table range
+    uint32_t n_blocks = 0;
 };
 
 struct StageTimings {
@@ -57,28 +60,59 @@ struct StageTimings {
     uint64_t h2d_bytes = 0;
 };
 
-// All manifest-listed files, resident both in pinned host memory and in HBM.
+// All manifest-listed files, resident both in pinned host memory and in HBM,
+// with their GPU CRC-64/XZ computed while they stream in:
+//
+//   reader lanes (host threads) take 8 MiB pieces in order — `first` files'
+//   pieces before the rest — pread each into leased pinned staging, then on
+//   the copy stream queue its H2D copy and the CRC of its 64 KiB blocks
+//   (fdy_launch_crc64_blocks). The lane that submits a file's last piece
+//   queues that file's fold and digest D2H (a `first` file) — the other
+//   files fold in one batch after the last piece of all — and records the
+//   file's event. So CRC overlaps the reads and the DMA; what is left when
+//   the reads end is the last piece's copy + CRC and the folds.
+//
+// The constructor returns once the lanes are started; host(), device() and
+// verify_*() wait for what they need.
 class StagedArchive {
 public:
     StagedArchive(Device& dev, const std::filesystem::path& root, const Manifest& manifest,
-                  unsigned lanes, StageTimings* timings);
+                  unsigned lanes, StageTimings* timings, std::vector<std::string> first = {});
+    ~StagedArchive();
+    StagedArchive(const StagedArchive&) = delete;
+    StagedArchive& operator=(const StagedArchive&) = delete;
+
     // GPU CRC of every staged file against the manifest; raises
     // archive_corruption "integrity check failed for <rel>" on the first
     // mismatch in manifest order (caller adds the "archive integrity" step).
     void verify(const Manifest& manifest, StageTimings* timings);
+    // The same for one file, without waiting for the others; on a mismatch
+    // it reports the first failing file in manifest order, as verify() does.
+    void verify_file(const Manifest& manifest, const std::string& rel, StageTimings* timings);
+    // Makes `stream` wait until rel's bytes are in HBM and CRCed.
+    void order_after(const std::string& rel, cudaStream_t stream);
 
     bool has(const std::string& rel) const { return files_.count(rel) != 0; }
-    std::span<const uint8_t> host(const std::string& rel) const;
+    std::span<const uint8_t> host(const std::string& rel) const;  // waits for rel's reads
     const unsigned char* device(const std::string& rel) const;
     uint64_t size(const std::string& rel) const;
     uint64_t total_bytes() const { return total_; }
 
 private:
+    struct Shared;
+    const StagedFile& file(const std::string& rel) const;
+    void wait_submitted(const StagedFile& f) const;  // all of f's pieces queued (rethrows read errors)
+    void join();
+
     Device& dev_;
     std::map<std::string, StagedFile> files_;
+    std::vector<const StagedFile*> order_;  // staging order
     PinnedLease host_;
     DeviceBuffer device_;
+    DeviceBuffer crc_;  // block table | block crc | block len | seg first | seg count | digests
+    PinnedLease digests_;
     uint64_t total_ = 0;
+    std::unique_ptr<Shared> sh_;
 };
 
 struct ArchiveMaterializeTimings {

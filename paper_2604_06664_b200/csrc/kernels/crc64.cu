@@ -126,6 +126,22 @@ extern "C" cudaError_t fdy_crc64_set_constants(const uint64_t* x2k64) {
     return cudaMemcpyToSymbol(c_x2k, x2k64, sizeof(uint64_t) * 64);
 }
 
+extern "C" cudaError_t fdy_launch_crc64_blocks(const unsigned char* base, const FdyCrcBlock* blocks,
+                                               uint32_t n_blocks, uint64_t* block_crc,
+                                               uint64_t* block_len, cudaStream_t stream) {
+    if (n_blocks) crc_blocks_kernel<<<n_blocks, kThreads, 0, stream>>>(base, blocks, block_crc, block_len);
+    return cudaGetLastError();
+}
+
+extern "C" cudaError_t fdy_launch_crc64_fold(const uint32_t* seg_first_block, const uint32_t* seg_n_blocks,
+                                             uint32_t n_segments, uint64_t* block_crc, uint64_t* block_len,
+                                             uint64_t* out, cudaStream_t stream) {
+    if (n_segments)
+        crc_fold_kernel<<<n_segments, 1024, 0, stream>>>(seg_first_block, seg_n_blocks, block_crc, block_len,
+                                                         out);
+    return cudaGetLastError();
+}
+
 extern "C" cudaError_t fdy_launch_crc64(const unsigned char* base, const FdyCrcBlock* blocks,
                                         uint32_t n_blocks, const uint32_t* seg_first_block,
                                         const uint32_t* seg_n_blocks, uint32_t n_segments,

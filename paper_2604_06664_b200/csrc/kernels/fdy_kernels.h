@@ -51,6 +51,15 @@ cudaError_t fdy_crc64_set_constants(const uint64_t* x2k64);  // per device
 // CRC-64/XZ of n_segments byte ranges already resident in device memory.
 // blocks: host-built table (see fdy_crc_plan) in device memory; partial /
 // lengths scratch: n_blocks entries each; out: n_segments digests (device).
+// The two halves of fdy_launch_crc64, for callers that CRC blocks as their
+// bytes land (block i of the table -> block_crc[i], block_len[i]) and fold
+// segments later. Block / segment pointers may be offset into larger tables.
+cudaError_t fdy_launch_crc64_blocks(const unsigned char* base, const FdyCrcBlock* blocks,
+                                    uint32_t n_blocks, uint64_t* block_crc, uint64_t* block_len,
+                                    cudaStream_t stream);
+cudaError_t fdy_launch_crc64_fold(const uint32_t* seg_first_block, const uint32_t* seg_n_blocks,
+                                  uint32_t n_segments, uint64_t* block_crc, uint64_t* block_len,
+                                  uint64_t* out, cudaStream_t stream);
 cudaError_t fdy_launch_crc64(const unsigned char* base, const FdyCrcBlock* blocks,
                              uint32_t n_blocks, const uint32_t* seg_first_block,
                              const uint32_t* seg_n_blocks, uint32_t n_segments,

@@ -1,0 +1,224 @@
+"""GPU parity through the C-ABI (include/foundry_b200.h) — the boundary a
+foreign host binds. Every materialized member-image arena is
+decoded back to FNDG records and compared byte for byte with the C oracle's
+materialization of the same archive (parse_graph_at + relocation + rank
+patch), which test_oracle.py pins to the reference.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import shutil
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT, manifest
+
+pytestmark = pytest.mark.gpu
+
+ERR_INVALID_ARGUMENT = 1
+ERR_ARCHIVE_CORRUPTION = 8
+
+# deltas {0, one granule, 0x7000.. -> 0x7100.., a SplitMix64 draw}
+DELTAS = [0, 0x10000, 0x10000000000, 0x5A3F2B0000]
+
+
+@pytest.fixture(scope="module")
+def api(foundry):
+    from paper_2604_06664_b200 import capi
+    return capi.CApi()
+
+
+@pytest.fixture(scope="module")
+def dev(api):
+    d = api.device_open(0)
+    yield d
+    api.lib.fdy_device_close(d)
+
+
+def decode(foundry, arch, arena: bytes) -> bytes:
+    return foundry._foundry._decode_member_images(arch, arena)
+
+
+@pytest.mark.parametrize("name,rank,world,delta", [
+    ("micro", 0, 1, 0),
+    ("llama3-8b", 0, 1, DELTAS[1]),
+    ("moe-spmd", 3, 8, DELTAS[2]),
+    ("moe-spmd", 7, 8, DELTAS[3]),
+])
+def test_materialize_equals_the_oracle(foundry, oracle, archives, api, dev, name, rank, world, delta):
+    arch, _ = archives(name)
+    blob = open(os.path.join(arch, "templates.fdt"), "rb").read()
+    base = manifest(arch)["allocator"]["base"]
+    store = api.store_upload(dev, blob)
+    try:
+        members, ms = api.materialize(dev, store, rank, world, base + delta if delta else 0)
+        assert ms > 0
+        got = decode(foundry, arch, api.members_download(members))
+        api.lib.fdy_members_free(members)
+    finally:
+        api.lib.fdy_store_free(store)
+    want, _ = oracle.materialize_archive(arch, rank, world, delta)
+    assert got == want
+
+
+def test_materialize_into_reuses_the_arena(foundry, oracle, archives, api, dev):
+    """fdy_materialize_into overwrites every byte: ranks alternate in one arena."""
+    arch, _ = archives("moe-spmd")
+    blob = open(os.path.join(arch, "templates.fdt"), "rb").read()
+    base = manifest(arch)["allocator"]["base"]
+    store = api.store_upload(dev, blob)
+    members, _ = api.materialize(dev, store, 0, 4)
+    try:
+        for rank, delta in ((1, DELTAS[1]), (2, 0), (3, DELTAS[3])):
+            api.materialize(dev, store, rank, 4, base + delta if delta else 0, members)
+            want, _ = oracle.materialize_archive(arch, rank, 4, delta)
+            assert decode(foundry, arch, api.members_download(members)) == want, (rank, hex(delta))
+    finally:
+        api.lib.fdy_members_free(members)
+        api.lib.fdy_store_free(store)
+
+
+def test_rank_outside_world_is_invalid_argument(archives, api, dev):
+    from paper_2604_06664_b200.capi import CApiError
+    arch, _ = archives("micro")
+    store = api.store_upload(dev, open(os.path.join(arch, "templates.fdt"), "rb").read())
+    try:
+        with pytest.raises(CApiError, match="outside world size") as e:
+            api.materialize(dev, store, 4, 4)
+        assert e.value.code == ERR_INVALID_ARGUMENT
+    finally:
+        api.lib.fdy_store_free(store)
+
+
+def test_store_fanout_to_the_same_device(foundry, oracle, archives, api, dev):
+    """fdy_store_fanout (GPU -> GPU copy); on one GPU the copy is device-local."""
+    arch, _ = archives("moe-spmd")
+    blob = open(os.path.join(arch, "templates.fdt"), "rb").read()
+    src = api.store_upload(dev, blob)
+    out = ctypes.c_void_p()
+    api.check(api.lib.fdy_store_fanout(src, dev, ctypes.byref(out)))
+    api.lib.fdy_store_free(src)  # the copy must stand alone
+    try:
+        members, _ = api.materialize(dev, out, 5, 8)
+        got = decode(foundry, arch, api.members_download(members))
+        api.lib.fdy_members_free(members)
+    finally:
+        api.lib.fdy_store_free(out)
+    want, _ = oracle.materialize_archive(arch, 5, 8, 0)
+    assert got == want
+
+
+@pytest.mark.parametrize("b200", [True, False])
+@pytest.mark.parametrize("rank,world,delta", [(0, 1, 0), (6, 8, DELTAS[2])])
+def test_prepare_archive_equals_the_oracle(foundry, oracle, archives, api, dev, b200, rank, world, delta):
+    """fdy_prepare_archive: files -> GPU integrity -> fused kernel -> host memory,
+    for a B200 archive (store on disk) and a reference-written one (packed on the fly)."""
+    from paper_2604_06664_b200 import capi
+    arch, _ = archives("moe-spmd", b200=b200)
+    base = manifest(arch)["allocator"]["base"]
+    size = capi.store_header(open(os.path.join(archives("moe-spmd")[0], "templates.fdt"), "rb").read())[
+        "members_image_bytes"]  # same spec, same member images
+    host = api.host_alloc(dev, size)
+    try:
+        t = api.prepare_archive(dev, arch, rank, world, base + delta if delta else 0, 4, host, size)
+        arena = ctypes.string_at(host, t["member_bytes"])
+    finally:
+        api.lib.fdy_host_free(host)
+    assert t["graphs"] == 512 and t["d2h_bytes"] == t["member_bytes"]
+    want, _ = oracle.materialize_archive(arch, rank, world, delta)
+    # decoded with the B200 archive's store: packing is deterministic, so the
+    # store packed on the fly from the plain archive has the same layout
+    assert decode(foundry, archives("moe-spmd")[0], arena) == want
+
+
+@pytest.mark.parametrize("victim", ["graphs.bin", "templates.fdt", "catalog.bin"])
+def test_prepare_archive_names_the_corrupt_file(archives, api, dev, tmp_path, victim):
+    from paper_2604_06664_b200.capi import CApiError
+    arch, _ = archives("micro")
+    bad = tmp_path / "bad"
+    shutil.copytree(arch, bad)
+    data = bytearray((bad / victim).read_bytes())
+    data[len(data) // 3] ^= 0x40
+    (bad / victim).write_bytes(bytes(data))
+    host = api.host_alloc(dev, 64 << 20)
+    try:
+        with pytest.raises(CApiError, match="archive integrity: integrity check failed for " + victim) as e:
+            api.prepare_archive(dev, str(bad), 0, 1, 0, 4, host, 64 << 20)
+        assert e.value.code == ERR_ARCHIVE_CORRUPTION
+    finally:
+        api.lib.fdy_host_free(host)
+
+
+def test_prepare_archive_reports_the_first_corrupt_file_in_manifest_order(archives, api, dev, tmp_path):
+    """Two corrupt files: the one earlier in manifest order is named (as the
+    reference's verify_archive_integrity walk would), even though the store
+    is verified first."""
+    from paper_2604_06664_b200.capi import CApiError
+    arch, _ = archives("micro")
+    bad = tmp_path / "bad2"
+    shutil.copytree(arch, bad)
+    for victim in ("graphs.bin", "templates.fdt"):
+        data = bytearray((bad / victim).read_bytes())
+        data[7] ^= 1
+        (bad / victim).write_bytes(bytes(data))
+    host = api.host_alloc(dev, 64 << 20)
+    try:
+        with pytest.raises(CApiError, match="integrity check failed for graphs.bin"):
+            api.prepare_archive(dev, str(bad), 0, 1, 0, 4, host, 64 << 20)
+    finally:
+        api.lib.fdy_host_free(host)
+
+
+@pytest.mark.parametrize("sizes", [
+    [0], [1], [15, 16, 17], [65535, 65536, 65537], [3 * 65536 + 5, 0, 999_999], [8 << 20],
+])
+def test_crc64_segments_match_the_oracle(oracle, api, dev, sizes):
+    import random
+    rng = random.Random(sum(sizes) + len(sizes))
+    parts, ranges, off = [], [], 0
+    for n in sizes:
+        data = bytes(rng.getrandbits(8) for _ in range(min(n, 4096))) * (n // 4096 + 1)
+        data = data[:n]
+        parts.append(data + b"\0" * ((-len(data)) % 16))  # segments start 16-byte aligned
+        ranges.append((off, n))
+        off += len(parts[-1])
+    digests, _ = api.crc64(dev, b"".join(parts), ranges)
+    assert digests == [oracle.crc64(p[:n]) for p, (_, n) in zip(parts, ranges)]
+
+
+def test_crc64_known_answer(api, dev):
+    """crc64("123456789") == 0x995DC9BBDF1939FA (test_hash.cpp:13-16)."""
+    digests, _ = api.crc64(dev, b"123456789", [(0, 9)])
+    assert digests == [0x995DC9BBDF1939FA]
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_ipc_fanout_between_two_processes(foundry, oracle, archives, tmp_path):
+    """The N>1 exchange step on one GPU: rank 0 uploads + exports the store
+    (CUDA IPC), rank 1 imports it GPU -> GPU; each materializes its own TP
+    rank and must equal the oracle's graph set for that rank."""
+    arch, _ = archives("moe-spmd")
+    port = _free_port()
+    procs = []
+    for rank in range(2):
+        env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                   WORLD_SIZE="2", LOCAL_RANK="0")
+        procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "ipc_worker.py"), arch,
+                                       str(tmp_path)], env=env))
+    for p in procs:
+        assert p.wait(timeout=600) == 0
+    for rank in range(2):
+        got = (tmp_path / ("rank%d.fndg" % rank)).read_bytes()
+        want, _ = oracle.materialize_archive(arch, 2 + rank, 8, 0x10000 * (rank + 1))
+        assert got == want, rank
