@@ -644,10 +644,16 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     I.ctx = std::make_unique<GpuContext>(device);
 
     // 1. stage every listed file into HBM (reads overlap the DMA),
-    // 2. verify every digest with one GPU CRC launch
+    // 2. stage + verify every digest: the store goes to HBM (GPU CRC as it
+    //    lands); files LOAD parses stay in host memory; graphs.bin is only
+    //    hashed when the store replaces it
     StageTimings st;
     try {
-        I.staged = std::make_unique<StagedArchive>(device, archive, I.manifest, opts.prepare_lanes, &st);
+        StagePlan plan;
+        const bool has_store = I.manifest.file_digests.count("templates.fdt") != 0;
+        if (has_store) plan.device = {"templates.fdt"};
+        plan.keep_host = [has_store](const std::string& rel) { return !(has_store && rel == "graphs.bin"); };
+        I.staged = std::make_unique<StagedArchive>(device, archive, I.manifest, opts.prepare_lanes, &st, plan);
         I.staged->verify(I.manifest, &st);
     } catch (const Error&) {
         rethrow_in_step("archive integrity");

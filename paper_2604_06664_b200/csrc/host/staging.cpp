@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include "foundry/bytes.hpp"
+#include "foundry/hash.hpp"
 #include "foundry/parallel.hpp"
 #include "../kernels/fdy_kernels.h"
 
@@ -102,21 +103,28 @@ PinnedLease& PinnedLease::operator=(PinnedLease&& o) noexcept {
 
 // ------------------------------------------------------------------ staging
 
+namespace {
+constexpr size_t kScratch = 1 << 20;  // hash-only reads: per-lane, stays in cache
+}
+
 struct StagedArchive::Shared {
     std::mutex mu;
     std::condition_variable cv;
-    std::vector<uint32_t> pieces_left;       // per segment
-    std::vector<cudaEvent_t> done;           // per segment, recorded after its fold
-    std::vector<uint8_t> submitted;          // per segment
-    std::exception_ptr error;                // first reader failure
-    size_t remaining = 0;                    // pieces not yet submitted
+    std::vector<uint32_t> pieces_left;  // per segment
+    std::vector<uint8_t> ready;         // per segment: every piece read (and queued / CRCed)
+    std::vector<cudaEvent_t> done;      // per device segment, recorded after its fold
+    std::vector<uint64_t> piece_crc;    // host / hash files
+    std::vector<uint64_t> piece_len;
+    std::vector<uint64_t> cpu_digest;   // per segment (host / hash files)
+    std::exception_ptr error;           // first reader failure
+    size_t remaining = 0;               // pieces not yet done
     std::vector<std::thread> lanes;
     Clock::time_point t0;
     double read_ms = 0;
 };
 
 StagedArchive::StagedArchive(Device& dev, const fs::path& root, const Manifest& manifest,
-                             unsigned lanes, StageTimings* t, std::vector<std::string> first)
+                             unsigned lanes, StageTimings* t, StagePlan plan)
     : dev_(dev), sh_(std::make_unique<Shared>()) {
     sh_->t0 = Clock::now();
     for (const auto& [rel, digest] : manifest.file_digests) {
@@ -124,135 +132,182 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const Manifest& 
         std::error_code ec;
         const uint64_t n = fs::file_size(root / rel, ec);
         require(!ec, Errc::archive_corruption, "cannot open " + (root / rel).string());
-        files_[rel] = {rel, 0, n};
+        StagedFile f;
+        f.rel = rel;
+        f.length = n;
+        f.placement = plan.keep_host && plan.keep_host(rel) ? Placement::host : Placement::hash;
+        files_[rel] = f;
     }
-    // staging order: the `first` files, then the rest in manifest order
-    std::vector<uint8_t> is_first(files_.size(), 0);
-    for (const auto& rel : first)
-        if (files_.count(rel)) order_.push_back(&files_.at(rel));
-    for (const auto& [rel, f] : files_)
-        if (std::find(order_.begin(), order_.end(), &f) == order_.end()) order_.push_back(&f);
-    const size_t n_first = std::min(first.size(), order_.size());
+    for (const auto& rel : plan.device)
+        if (files_.count(rel) && files_.at(rel).placement != Placement::device) {
+            files_.at(rel).placement = Placement::device;
+            order_.push_back(&files_.at(rel));
+        }
+    for (Placement pl : {Placement::host, Placement::hash})
+        for (const auto& [rel, f] : files_)
+            if (f.placement == pl) order_.push_back(&f);
+
+    // layout: device + host files in staging memory; device files' CRC plan
     std::vector<FdyCrcBlock> blocks;
     std::vector<uint32_t> seg_first, seg_count;
+    uint32_t n_pieces = 0;
     for (size_t i = 0; i < order_.size(); ++i) {
         StagedFile& f = files_.at(order_[i]->rel);
-        f.offset = total_;
         f.segment = static_cast<uint32_t>(i);
-        f.first_block = static_cast<uint32_t>(blocks.size());
-        for (uint64_t o = 0; o < f.length; o += kCrcBlockBytes)
-            blocks.push_back({f.segment, static_cast<uint32_t>(std::min<uint64_t>(kCrcBlockBytes, f.length - o)),
-                              f.offset + o});
-        f.n_blocks = static_cast<uint32_t>(blocks.size()) - f.first_block;
-        seg_first.push_back(f.first_block);
-        seg_count.push_back(f.n_blocks);
-        total_ += (f.length + kAlign - 1) / kAlign * kAlign;
+        if (f.placement != Placement::hash) {
+            f.offset = total_;
+            total_ += (f.length + kAlign - 1) / kAlign * kAlign;
+        }
+        if (f.placement == Placement::device) {
+            f.dseg = static_cast<uint32_t>(seg_first.size());
+            f.first_block = static_cast<uint32_t>(blocks.size());
+            for (uint64_t o = 0; o < f.length; o += kCrcBlockBytes)
+                blocks.push_back({f.dseg, static_cast<uint32_t>(std::min<uint64_t>(kCrcBlockBytes, f.length - o)),
+                                  f.offset + o});
+            f.n_blocks = static_cast<uint32_t>(blocks.size()) - f.first_block;
+            seg_first.push_back(f.first_block);
+            seg_count.push_back(f.n_blocks);
+            device_bytes_ = total_;
+        } else {
+            f.first_piece = n_pieces;
+            f.n_pieces = static_cast<uint32_t>((f.length + kPiece - 1) / kPiece);
+            n_pieces += f.n_pieces;
+        }
     }
-    const size_t nb = blocks.size(), ns = order_.size();
+    const size_t nb = blocks.size(), nd = seg_first.size(), ns = order_.size();
     host_ = PinnedLease(dev, std::max<uint64_t>(total_, 16));
-    device_ = DeviceBuffer(dev, std::max<uint64_t>(total_, 16));
-    // CRC scratch: block table | crc | len | first | count | digests
-    const size_t table = nb * sizeof(FdyCrcBlock), plan = table + 2 * ns * 4;
-    crc_ = DeviceBuffer(dev, plan + 2 * nb * 8 + ns * 8 + 64);
-    digests_ = PinnedLease(dev, std::max<size_t>(plan, ns * 8) + 64);
+    device_ = DeviceBuffer(dev, std::max<uint64_t>(device_bytes_, 16));
+    // GPU CRC scratch: block table | first | count | (align 8) crc | len | digests
+    const size_t table = nb * sizeof(FdyCrcBlock), plan_bytes = table + 2 * nd * 4;
+    crc_ = DeviceBuffer(dev, plan_bytes + 2 * nb * 8 + nd * 8 + 64);
+    digests_ = PinnedLease(dev, std::max<size_t>(plan_bytes, nd * 8) + 64);
     std::memcpy(digests_.data(), blocks.data(), table);
-    std::memcpy(digests_.data() + table, seg_first.data(), ns * 4);
-    std::memcpy(digests_.data() + table + ns * 4, seg_count.data(), ns * 4);
+    std::memcpy(digests_.data() + table, seg_first.data(), nd * 4);
+    std::memcpy(digests_.data() + table + nd * 4, seg_count.data(), nd * 4);
     auto* d_blocks = reinterpret_cast<FdyCrcBlock*>(crc_.data());
     auto* d_first = reinterpret_cast<uint32_t*>(crc_.data() + table);
-    auto* d_count = d_first + ns;
-    auto* d_crc = reinterpret_cast<uint64_t*>(crc_.data() + (plan + 7) / 8 * 8);
+    auto* d_count = d_first + nd;
+    auto* d_crc = reinterpret_cast<uint64_t*>(crc_.data() + (plan_bytes + 7) / 8 * 8);
     auto* d_len = d_crc + nb;
     auto* d_out = d_len + nb;
 
     dev.make_current();
     cudaStream_t copy = dev.copy_stream();
+    cudaStream_t side = dev.side_stream();
     {  // device buffers are stream-ordered on dev.stream(): copies start after the allocations
         cudaEvent_t allocated;
         cuda_check(cudaEventCreateWithFlags(&allocated, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventRecord(allocated, dev.stream()), "cudaEventRecord");
         cuda_check(cudaStreamWaitEvent(copy, allocated, 0), "cudaStreamWaitEvent");
+        cuda_check(cudaStreamWaitEvent(side, allocated, 0), "cudaStreamWaitEvent");
         cudaEventDestroy(allocated);
     }
-    cuda_check(cudaMemcpyAsync(crc_.data(), digests_.data(), plan, cudaMemcpyHostToDevice, copy),
-               "cudaMemcpyAsync(CRC plan H2D)");
-    // the plan must land before the digest slots (same pinned buffer) are reused
-    cuda_check(cudaStreamSynchronize(copy), "cudaStreamSynchronize(CRC plan)");
+    if (plan_bytes) {
+        cuda_check(cudaMemcpyAsync(crc_.data(), digests_.data(), plan_bytes, cudaMemcpyHostToDevice, copy),
+                   "cudaMemcpyAsync(CRC plan H2D)");
+        // the plan must land before the digest slots (same pinned buffer) are reused
+        cuda_check(cudaStreamSynchronize(copy), "cudaStreamSynchronize(CRC plan)");
+    }
 
     struct Piece {
         const StagedFile* f;
         uint64_t off, len;
+        uint32_t slot;  // host / hash: per-piece CRC slot
     };
     auto pieces = std::make_shared<std::vector<Piece>>();
     for (const StagedFile* f : order_)
-        for (uint64_t o = 0; o < f->length; o += kPiece)
-            pieces->push_back({f, o, std::min<uint64_t>(kPiece, f->length - o)});
+        for (uint64_t o = 0, k = 0; o < f->length; o += kPiece, ++k)
+            pieces->push_back({f, o, std::min<uint64_t>(kPiece, f->length - o), f->first_piece + static_cast<uint32_t>(k)});
     sh_->pieces_left.assign(ns, 0);
     for (const Piece& pc : *pieces) ++sh_->pieces_left[pc.f->segment];
-    sh_->submitted.assign(ns, 0);
-    sh_->done.assign(ns, nullptr);
+    sh_->ready.assign(ns, 0);
+    sh_->cpu_digest.assign(ns, 0);
+    sh_->piece_crc.assign(n_pieces, 0);
+    sh_->piece_len.assign(n_pieces, 0);
+    sh_->done.assign(nd, nullptr);
     for (auto& e : sh_->done) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     sh_->remaining = pieces->size();
-    uint64_t* h_digest = reinterpret_cast<uint64_t*>(digests_.data());  // plan is no longer needed
+    uint64_t* h_digest = reinterpret_cast<uint64_t*>(digests_.data());  // the plan has landed
 
-    // folds one segment range and copies its digests to the pinned slots
-    // CRC work runs on the side stream, each piece's blocks gated by an event
-    // on its copy, so the copy engine streams pieces back to back
-    cudaStream_t side = dev.side_stream();
-    auto fold = [=](uint32_t s0, uint32_t n) {
-        cuda_check(fdy_launch_crc64_fold(d_first + s0, d_count + s0, n, d_crc, d_len, d_out + s0, side),
-                   "CRC fold launch");
-        cuda_check(cudaMemcpyAsync(h_digest + s0, d_out + s0, 8ull * n, cudaMemcpyDeviceToHost, side),
-                   "cudaMemcpyAsync(digest D2H)");
-    };
-    // empty files: fold + event right away (no pieces)
-    for (uint32_t s = 0; s < ns; ++s)
-        if (sh_->pieces_left[s] == 0 && s < n_first) {
-            fold(s, 1);
-            cuda_check(cudaEventRecord(sh_->done[s], side), "cudaEventRecord");
-            sh_->submitted[s] = 1;
-        }
-    auto next = std::make_shared<std::atomic<size_t>>(0);
     Shared* sh = sh_.get();
+    // finishes a file whose pieces are all done (called with sh->mu held)
+    auto complete = [=](const StagedFile& f) {
+        if (f.placement == Placement::device) {
+            cuda_check(fdy_launch_crc64_fold(d_first + f.dseg, d_count + f.dseg, 1, d_crc, d_len,
+                                             d_out + f.dseg, side),
+                       "CRC fold launch");
+            cuda_check(cudaMemcpyAsync(h_digest + f.dseg, d_out + f.dseg, 8, cudaMemcpyDeviceToHost, side),
+                       "cudaMemcpyAsync(digest D2H)");
+            cuda_check(cudaEventRecord(sh->done[f.dseg], side), "cudaEventRecord");
+        } else {
+            uint64_t c = 0;  // CRC of the empty string
+            for (uint32_t k = 0; k < f.n_pieces; ++k)
+                c = k ? crc64_combine(c, sh->piece_crc[f.first_piece + k], sh->piece_len[f.first_piece + k])
+                      : sh->piece_crc[f.first_piece];
+            sh->cpu_digest[f.segment] = c;
+        }
+        sh->ready[f.segment] = 1;
+    };
+    for (const StagedFile* f : order_)  // empty files
+        if (sh_->pieces_left[f->segment] == 0) complete(*f);
+
+    auto next = std::make_shared<std::atomic<size_t>>(0);
     unsigned char* hbase = host_.data();
     unsigned char* dbase = device_.data();
     const int ordinal = dev.ordinal();
     const fs::path dir = root;  // the lanes outlive this constructor
     auto body = [=]() {
         cudaSetDevice(ordinal);
+        std::unique_ptr<uint8_t[]> scratch;
         for (;;) {
             const size_t i = next->fetch_add(1);
             if (i >= pieces->size()) return;
             const Piece& pc = (*pieces)[i];
             try {
-                unsigned char* h = hbase + pc.f->offset + pc.off;
-                read_range(dir / pc.f->rel, h, pc.off, pc.len);
-                const uint32_t b0 = pc.f->first_block + static_cast<uint32_t>(pc.off / kCrcBlockBytes);
-                const uint32_t nblk = static_cast<uint32_t>((pc.len + kCrcBlockBytes - 1) / kCrcBlockBytes);
-                std::lock_guard lock(sh->mu);  // one submission order on the copy stream
-                cuda_check(cudaMemcpyAsync(dbase + pc.f->offset + pc.off, h, pc.len, cudaMemcpyHostToDevice, copy),
-                           "cudaMemcpyAsync(archive H2D)");
-                cudaEvent_t landed;
-                cuda_check(cudaEventCreateWithFlags(&landed, cudaEventDisableTiming), "cudaEventCreate");
-                cuda_check(cudaEventRecord(landed, copy), "cudaEventRecord");
-                cuda_check(cudaStreamWaitEvent(side, landed, 0), "cudaStreamWaitEvent");
-                cudaEventDestroy(landed);
-                cuda_check(fdy_launch_crc64_blocks(dbase, d_blocks + b0, nblk, d_crc + b0, d_len + b0, side),
-                           "CRC block launch");
-                const uint32_t s = pc.f->segment;
-                if (--sh->pieces_left[s] == 0 && s < n_first) {
-                    fold(s, 1);
-                    cuda_check(cudaEventRecord(sh->done[s], side), "cudaEventRecord");
-                    sh->submitted[s] = 1;
-                }
-                if (--sh->remaining == 0) {  // the rest fold in one launch
-                    if (ns > n_first) fold(static_cast<uint32_t>(n_first), static_cast<uint32_t>(ns - n_first));
-                    for (size_t k = n_first; k < ns; ++k) {
-                        cuda_check(cudaEventRecord(sh->done[k], side), "cudaEventRecord");
-                        sh->submitted[k] = 1;
+                const StagedFile& f = *pc.f;
+                uint64_t piece_crc = 0;
+                if (f.placement == Placement::hash) {
+                    if (!scratch) scratch.reset(new uint8_t[kScratch]);
+                    Crc64 c;
+                    const int fd = ::open((dir / f.rel).c_str(), O_RDONLY | O_CLOEXEC);
+                    require(fd >= 0, Errc::archive_corruption, "cannot open " + (dir / f.rel).string());
+                    for (uint64_t done = 0; done < pc.len;) {
+                        const ssize_t n = ::pread(fd, scratch.get(), std::min<uint64_t>(kScratch, pc.len - done),
+                                                  static_cast<off_t>(pc.off + done));
+                        if (n <= 0) {
+                            ::close(fd);
+                            raise(Errc::archive_corruption, "short read on " + (dir / f.rel).string());
+                        }
+                        c.update(scratch.get(), static_cast<size_t>(n));
+                        done += static_cast<uint64_t>(n);
                     }
-                    sh->read_ms = ms_since(sh->t0);
+                    ::close(fd);
+                    piece_crc = c.value();
+                } else {
+                    unsigned char* h = hbase + f.offset + pc.off;
+                    read_range(dir / f.rel, h, pc.off, pc.len);
+                    if (f.placement == Placement::host) piece_crc = crc64(h, pc.len);
                 }
+                std::lock_guard lock(sh->mu);  // one submission order on the streams
+                if (f.placement == Placement::device) {
+                    const uint32_t b0 = f.first_block + static_cast<uint32_t>(pc.off / kCrcBlockBytes);
+                    const uint32_t nblk = static_cast<uint32_t>((pc.len + kCrcBlockBytes - 1) / kCrcBlockBytes);
+                    cuda_check(cudaMemcpyAsync(dbase + f.offset + pc.off, hbase + f.offset + pc.off, pc.len,
+                                               cudaMemcpyHostToDevice, copy),
+                               "cudaMemcpyAsync(archive H2D)");
+                    cudaEvent_t landed;
+                    cuda_check(cudaEventCreateWithFlags(&landed, cudaEventDisableTiming), "cudaEventCreate");
+                    cuda_check(cudaEventRecord(landed, copy), "cudaEventRecord");
+                    cuda_check(cudaStreamWaitEvent(side, landed, 0), "cudaStreamWaitEvent");
+                    cudaEventDestroy(landed);
+                    cuda_check(fdy_launch_crc64_blocks(dbase, d_blocks + b0, nblk, d_crc + b0, d_len + b0, side),
+                               "CRC block launch");
+                } else {
+                    sh->piece_crc[pc.slot] = piece_crc;
+                    sh->piece_len[pc.slot] = pc.len;
+                }
+                if (--sh->pieces_left[f.segment] == 0) complete(f);
+                if (--sh->remaining == 0) sh->read_ms = ms_since(sh->t0);
             } catch (...) {
                 std::lock_guard lock(sh->mu);
                 if (!sh->error) sh->error = std::current_exception();
@@ -261,16 +316,9 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const Manifest& 
             sh->cv.notify_all();
         }
     };
-    if (pieces->empty()) {
-        for (size_t k = n_first; k < ns; ++k) {
-            fold(static_cast<uint32_t>(k), 1);
-            cuda_check(cudaEventRecord(sh_->done[k], side), "cudaEventRecord");
-            sh_->submitted[k] = 1;
-        }
-    }
     const unsigned nl = static_cast<unsigned>(std::min<size_t>(std::max(1u, lanes), std::max<size_t>(1, pieces->size())));
     for (unsigned l = 0; l < nl; ++l) sh_->lanes.emplace_back(body);
-    if (t) t->h2d_bytes += total_;
+    if (t) t->h2d_bytes += device_bytes_;
 }
 
 StagedArchive::~StagedArchive() {
@@ -297,24 +345,30 @@ const StagedFile& StagedArchive::file(const std::string& rel) const {
     return it->second;
 }
 
-void StagedArchive::wait_submitted(const StagedFile& f) const {
+void StagedArchive::wait_ready(const StagedFile& f) const {
     std::unique_lock lock(sh_->mu);
-    sh_->cv.wait(lock, [&] { return sh_->error || sh_->submitted[f.segment]; });
+    sh_->cv.wait(lock, [&] { return sh_->error || sh_->ready[f.segment]; });
     if (sh_->error) std::rethrow_exception(sh_->error);
+}
+
+uint64_t StagedArchive::digest_of(const StagedFile& f) const {
+    if (f.placement != Placement::device) return sh_->cpu_digest[f.segment];
+    cuda_check(cudaEventSynchronize(sh_->done[f.dseg]), "cudaEventSynchronize(CRC)");
+    return reinterpret_cast<const uint64_t*>(digests_.data())[f.dseg];
 }
 
 void StagedArchive::order_after(const std::string& rel, cudaStream_t stream) {
     const StagedFile& f = file(rel);
-    wait_submitted(f);
-    cuda_check(cudaStreamWaitEvent(stream, sh_->done[f.segment], 0), "cudaStreamWaitEvent");
+    require(f.placement == Placement::device, Errc::invalid_argument, rel + " is not staged in HBM");
+    wait_ready(f);
+    cuda_check(cudaStreamWaitEvent(stream, sh_->done[f.dseg], 0), "cudaStreamWaitEvent");
 }
 
 void StagedArchive::verify_file(const Manifest& manifest, const std::string& rel, StageTimings* t) {
     const auto t0 = Clock::now();
     const StagedFile& f = file(rel);
-    wait_submitted(f);
-    cuda_check(cudaEventSynchronize(sh_->done[f.segment]), "cudaEventSynchronize(CRC)");
-    const uint64_t got = reinterpret_cast<const uint64_t*>(digests_.data())[f.segment];
+    wait_ready(f);
+    const uint64_t got = digest_of(f);
     if (t) t->integrity_ms += ms_since(t0);
     if (got != manifest.file_digests.at(rel)) verify(manifest, t);  // reports in manifest order
     require(got == manifest.file_digests.at(rel), Errc::archive_corruption, "integrity check failed for " + rel);
@@ -325,21 +379,22 @@ void StagedArchive::verify(const Manifest& manifest, StageTimings* t) {
     join();
     if (sh_->error) std::rethrow_exception(sh_->error);
     if (t) t->read_ms += sh_->read_ms;
-    cuda_check(cudaStreamSynchronize(dev_.side_stream()), "cudaStreamSynchronize(CRC)");
-    const auto* got = reinterpret_cast<const uint64_t*>(digests_.data());
     for (const auto& [rel, digest] : manifest.file_digests)
-        require(got[file(rel).segment] == digest, Errc::archive_corruption, "integrity check failed for " + rel);
+        require(digest_of(file(rel)) == digest, Errc::archive_corruption, "integrity check failed for " + rel);
     if (t) t->integrity_ms += ms_since(t0);
 }
 
 std::span<const uint8_t> StagedArchive::host(const std::string& rel) const {
     const StagedFile& f = file(rel);
-    wait_submitted(f);
+    require(f.placement != Placement::hash, Errc::invalid_argument, rel + " was hashed, not kept in host memory");
+    wait_ready(f);
     return {host_.data() + f.offset, f.length};
 }
 
 const unsigned char* StagedArchive::device(const std::string& rel) const {
-    return device_.data() + file(rel).offset;
+    const StagedFile& f = file(rel);
+    require(f.placement == Placement::device, Errc::invalid_argument, rel + " is not staged in HBM");
+    return device_.data() + f.offset;
 }
 
 uint64_t StagedArchive::size(const std::string& rel) const { return file(rel).length; }
@@ -363,10 +418,19 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
     // the D2H of the result then overlap the reads of the remaining files,
     // whose verification still gates the return
     const bool has_store = manifest.file_digests.count("templates.fdt") != 0;
-    const std::vector<std::string> first =
-        has_store ? std::vector<std::string>{"templates.fdt"} : std::vector<std::string>{"graphs.bin", "patch.bin"};
+    // the store goes to HBM; a reference-written archive keeps the two files
+    // it is packed from in host memory; every other file is only hashed
+    StagePlan plan;
+    std::vector<std::string> first;
+    if (has_store) {
+        plan.device = {"templates.fdt"};
+        first = plan.device;
+    } else {
+        first = {"graphs.bin", "patch.bin"};
+        plan.keep_host = [](const std::string& rel) { return rel == "graphs.bin" || rel == "patch.bin"; };
+    }
     try {
-        staged = std::make_unique<StagedArchive>(dev, root, manifest, lanes, &st, first);
+        staged = std::make_unique<StagedArchive>(dev, root, manifest, lanes, &st, plan);
         for (const auto& rel : first) staged->verify_file(manifest, rel, &st);
     } catch (const Error&) {
         rethrow_in_step("archive integrity");

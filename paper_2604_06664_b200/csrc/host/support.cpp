@@ -1,5 +1,7 @@
 // errors, file I/O and host hashes (see the headers for the reference anchors).
 #include <array>
+#include <cstring>
+#include <immintrin.h>
 #include <cstdio>
 #include <fstream>
 
@@ -94,12 +96,89 @@ const SliceTables& tables() {
     return s;
 }
 
+// ---- carry-less multiply folding (PCLMULQDQ) for long inputs
+//
+// In the reflected representation (x^0 is bit 63 of a u64; a 16-byte LE
+// load has x^127 in bit 0), clmul(a, b) of two reflected 64-bit operands is
+// the reflected 128-bit form of a(x) b(x) x. A 128-bit state X = Xh x^64 + Xl
+// (Xh = low lane) moves d bits further down the message as
+//     X x^d == clmul(Xh, x^(d+63) mod P) ^ clmul(Xl, x^(d-1) mod P)   (mod P),
+// and a final 128-bit state reduces to the CRC register by feeding its 16
+// bytes through the table walk from a zero register (register = W x^64 mod P).
+// Four accumulators fold 64 bytes per step.
+
+uint64_t x_pow_mod(unsigned n) {  // x^n mod P, reflected
+    uint64_t p = 1ull << 63;
+    while (n--) p = (p & 1) ? (p >> 1) ^ kCrc64Poly : p >> 1;
+    return p;
+}
+
+struct FoldConstants {
+    uint64_t k[4][2];  // fold distances 128, 256, 384, 512 bits: {x^(d+63), x^(d-1)}
+    FoldConstants() {
+        for (int i = 0; i < 4; ++i) {
+            const unsigned d = 128u * static_cast<unsigned>(i + 1);
+            k[i][0] = x_pow_mod(d + 63);
+            k[i][1] = x_pow_mod(d - 1);
+        }
+    }
+};
+
+const FoldConstants& fold_constants() {
+    static const FoldConstants f;
+    return f;
+}
+
+bool have_pclmul() {
+    static const bool ok = __builtin_cpu_supports("pclmul") && __builtin_cpu_supports("sse4.1");
+    return ok;
+}
+
+__attribute__((target("pclmul,sse4.1"))) inline __m128i fold128(__m128i x, const uint64_t* k) {
+    const __m128i kk = _mm_set_epi64x(static_cast<long long>(k[1]), static_cast<long long>(k[0]));
+    return _mm_xor_si128(_mm_clmulepi64_si128(x, kk, 0x00), _mm_clmulepi64_si128(x, kk, 0x11));
+}
+
+// Consumes floor(len / 64) * 64 bytes (len >= 64); returns the register.
+__attribute__((target("pclmul,sse4.1"))) uint64_t fold_blocks(uint64_t c, const uint8_t* p, size_t n64) {
+    const FoldConstants& K = fold_constants();
+    __m128i x0 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(p));
+    __m128i x1 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(p + 16));
+    __m128i x2 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(p + 32));
+    __m128i x3 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(p + 48));
+    x0 = _mm_xor_si128(x0, _mm_set_epi64x(0, static_cast<long long>(c)));  // register into the first 8 bytes
+    for (size_t i = 1; i < n64; ++i) {
+        const uint8_t* q = p + 64 * i;
+        x0 = _mm_xor_si128(fold128(x0, K.k[3]), _mm_loadu_si128(reinterpret_cast<const __m128i*>(q)));
+        x1 = _mm_xor_si128(fold128(x1, K.k[3]), _mm_loadu_si128(reinterpret_cast<const __m128i*>(q + 16)));
+        x2 = _mm_xor_si128(fold128(x2, K.k[3]), _mm_loadu_si128(reinterpret_cast<const __m128i*>(q + 32)));
+        x3 = _mm_xor_si128(fold128(x3, K.k[3]), _mm_loadu_si128(reinterpret_cast<const __m128i*>(q + 48)));
+    }
+    __m128i x = _mm_xor_si128(_mm_xor_si128(fold128(x0, K.k[2]), fold128(x1, K.k[1])),
+                              _mm_xor_si128(fold128(x2, K.k[0]), x3));
+    // 16 bytes through the table walk from a zero register
+    const auto& T = tables().t;
+    uint64_t r = 0;
+    for (int lane = 0; lane < 2; ++lane) {
+        r ^= static_cast<uint64_t>(lane ? _mm_extract_epi64(x, 1) : _mm_cvtsi128_si64(x));
+        r = T[7][r & 0xFF] ^ T[6][(r >> 8) & 0xFF] ^ T[5][(r >> 16) & 0xFF] ^ T[4][(r >> 24) & 0xFF] ^
+            T[3][(r >> 32) & 0xFF] ^ T[2][(r >> 40) & 0xFF] ^ T[1][(r >> 48) & 0xFF] ^ T[0][r >> 56];
+    }
+    return r;
+}
+
 }  // namespace
 
 void Crc64::update(const void* data, size_t len) {
     const auto& T = tables().t;
     const auto* p = static_cast<const uint8_t*>(data);
     uint64_t c = state_;
+    if (len >= 256 && have_pclmul()) {
+        const size_t n64 = len / 64;
+        c = fold_blocks(c, p, n64);
+        p += 64 * n64;
+        len -= 64 * n64;
+    }
     while (len >= 8) {
         uint64_t w;
         std::memcpy(&w, p, 8);

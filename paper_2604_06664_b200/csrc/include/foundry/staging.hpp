@@ -15,6 +15,7 @@
 
 #include <cstdint>
 #include <filesystem>
+#include <functional>
 #include <map>
 #include <memory>
 #include <span>
@@ -45,63 +46,83 @@ private:
     int device_ = -1;
 };
 
+// Where a staged file goes. Every file is CRC-64/XZ-checked against the
+// manifest; only the template store needs to be in HBM.
+enum class Placement : uint8_t {
+    device,  // pinned host copy + DMA to HBM; CRC on the GPU as its pieces land
+    host,    // pinned host copy (the caller parses it); CRC on the host per piece
+    hash,    // not kept: read through a per-lane scratch, CRC on the host
+};
+
+struct StagePlan {
+    std::vector<std::string> device;                   // staged first, in this order
+    std::function<bool(const std::string&)> keep_host;  // Placement::host files (others: hash)
+};
+
 struct StagedFile {
     std::string rel;
-    uint64_t offset = 0;  // in host staging and in device staging
+    uint64_t offset = 0;  // in host staging and in device staging (device / host files)
     uint64_t length = 0;
-    uint32_t segment = 0;      // index in staging order
-    uint32_t first_block = 0;  // CRC block table range
+    uint32_t segment = 0;  // index in staging order
+    Placement placement = Placement::hash;
+    uint32_t dseg = 0;         // device files: index of the GPU digest
+    uint32_t first_block = 0;  // device files: CRC block table range
     uint32_t n_blocks = 0;
+    uint32_t first_piece = 0;  // host / hash files: per-piece CRC slots
+    uint32_t n_pieces = 0;
 };
 
 struct StageTimings {
-    double read_ms = 0, integrity_ms = 0;  // integrity: wait for DMA + CRC kernel + compare
+    double read_ms = 0, integrity_ms = 0;  // integrity: waits for CRC results + compare
     float crc_kernel_ms = 0;
     uint64_t h2d_bytes = 0;
 };
 
-// All manifest-listed files, resident both in pinned host memory and in HBM,
-// with their GPU CRC-64/XZ computed while they stream in:
+// All manifest-listed files, CRC-checked while they stream in:
 //
-//   reader lanes (host threads) take 8 MiB pieces in order — `first` files'
-//   pieces before the rest — pread each into leased pinned staging, then on
-//   the copy stream queue its H2D copy and the CRC of its 64 KiB blocks
-//   (fdy_launch_crc64_blocks). The lane that submits a file's last piece
-//   queues that file's fold and digest D2H (a `first` file) — the other
-//   files fold in one batch after the last piece of all — and records the
-//   file's event. So CRC overlaps the reads and the DMA; what is left when
-//   the reads end is the last piece's copy + CRC and the folds.
+//   reader lanes (host threads) take 8 MiB pieces in order — device files'
+//   pieces first, then host-kept files, then hash-only ones. A device piece
+//   is pread into leased pinned staging, then (in one submission order) its
+//   H2D copy goes on the copy stream and the CRC of its 64 KiB blocks on the
+//   side stream behind the copy (fdy_launch_crc64_blocks); the lane that
+//   submits a device file's last piece queues its fold + digest D2H and
+//   records the file's event. Host and hash pieces are CRCed on the lane
+//   right after the read, while the bytes are still in cache (PCLMUL
+//   folding, hash.hpp), and combined per file — bytes only the host needs
+//   never cross PCIe.
 //
 // The constructor returns once the lanes are started; host(), device() and
 // verify_*() wait for what they need.
 class StagedArchive {
 public:
     StagedArchive(Device& dev, const std::filesystem::path& root, const Manifest& manifest,
-                  unsigned lanes, StageTimings* timings, std::vector<std::string> first = {});
+                  unsigned lanes, StageTimings* timings, StagePlan plan);
     ~StagedArchive();
     StagedArchive(const StagedArchive&) = delete;
     StagedArchive& operator=(const StagedArchive&) = delete;
 
-    // GPU CRC of every staged file against the manifest; raises
-    // archive_corruption "integrity check failed for <rel>" on the first
-    // mismatch in manifest order (caller adds the "archive integrity" step).
+    // CRC of every staged file against the manifest; raises archive_corruption
+    // "integrity check failed for <rel>" on the first mismatch in manifest
+    // order (caller adds the "archive integrity" step).
     void verify(const Manifest& manifest, StageTimings* timings);
     // The same for one file, without waiting for the others; on a mismatch
     // it reports the first failing file in manifest order, as verify() does.
     void verify_file(const Manifest& manifest, const std::string& rel, StageTimings* timings);
-    // Makes `stream` wait until rel's bytes are in HBM and CRCed.
+    // Makes `stream` wait until a device file's bytes are in HBM and CRCed.
     void order_after(const std::string& rel, cudaStream_t stream);
 
     bool has(const std::string& rel) const { return files_.count(rel) != 0; }
-    std::span<const uint8_t> host(const std::string& rel) const;  // waits for rel's reads
-    const unsigned char* device(const std::string& rel) const;
+    // Host bytes of a device or host-kept file (waits for its reads).
+    std::span<const uint8_t> host(const std::string& rel) const;
+    const unsigned char* device(const std::string& rel) const;  // device files
     uint64_t size(const std::string& rel) const;
     uint64_t total_bytes() const { return total_; }
 
 private:
     struct Shared;
     const StagedFile& file(const std::string& rel) const;
-    void wait_submitted(const StagedFile& f) const;  // all of f's pieces queued (rethrows read errors)
+    void wait_ready(const StagedFile& f) const;  // all of f's pieces done (rethrows read errors)
+    uint64_t digest_of(const StagedFile& f) const;
     void join();
 
     Device& dev_;
@@ -111,7 +132,8 @@ private:
     DeviceBuffer device_;
     DeviceBuffer crc_;  // block table | block crc | block len | seg first | seg count | digests
     PinnedLease digests_;
-    uint64_t total_ = 0;
+    uint64_t total_ = 0;         // staged (device + host) bytes
+    uint64_t device_bytes_ = 0;  // of which DMAed to HBM
     std::unique_ptr<Shared> sh_;
 };
 
