@@ -8,6 +8,8 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -31,7 +33,15 @@ double ms_since(Clock::time_point t0) {
 }
 
 constexpr size_t kAlign = 256;
-constexpr size_t kPiece = 8ull << 20;
+
+// FOUNDRY_DEBUG=1: timeline of the end-to-end path on stderr (diagnostics)
+void trace_point(const char* what, Clock::time_point t0) {
+    static const bool on = std::getenv("FOUNDRY_DEBUG") != nullptr;
+    if (on) std::fprintf(stderr, "[foundry] %8.3f ms  %s\n", ms_since(t0), what);
+}
+// 2 MiB: one pread of it takes ~1 ms on a lane, so the store (read first)
+// is spread over every lane and the last pieces balance across lanes
+constexpr size_t kPiece = 2ull << 20;
 
 struct PoolEntry {
     int device;
@@ -175,6 +185,7 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const Manifest& 
         }
     }
     const size_t nb = blocks.size(), nd = seg_first.size(), ns = order_.size();
+    trace_point("  staging: layout", sh_->t0);
     host_ = PinnedLease(dev, std::max<uint64_t>(total_, 16));
     device_ = DeviceBuffer(dev, std::max<uint64_t>(device_bytes_, 16));
     // GPU CRC scratch: block table | first | count | (align 8) crc | len | digests
@@ -251,6 +262,7 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const Manifest& 
     for (const StagedFile* f : order_)  // empty files
         if (sh_->pieces_left[f->segment] == 0) complete(*f);
 
+    trace_point("  staging: buffers + CRC plan", sh_->t0);
     auto next = std::make_shared<std::atomic<size_t>>(0);
     unsigned char* hbase = host_.data();
     unsigned char* dbase = device_.data();
@@ -318,6 +330,7 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const Manifest& 
     };
     const unsigned nl = static_cast<unsigned>(std::min<size_t>(std::max(1u, lanes), std::max<size_t>(1, pieces->size())));
     for (unsigned l = 0; l < nl; ++l) sh_->lanes.emplace_back(body);
+    trace_point("  staging: lanes started", sh_->t0);
     if (t) t->h2d_bytes += device_bytes_;
 }
 
@@ -411,6 +424,7 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
     require(fs::exists(paths.manifest()), Errc::archive_corruption, "no manifest under " + root.string());
     const auto mb = slurp(paths.manifest());
     const Manifest manifest = parse_manifest(std::string(mb.begin(), mb.end()));
+    trace_point("manifest parsed", t_all);
     StageTimings st;
     std::unique_ptr<StagedArchive> staged;
     // the store (or, for a reference-written archive, the files it is packed
@@ -431,7 +445,9 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
     }
     try {
         staged = std::make_unique<StagedArchive>(dev, root, manifest, lanes, &st, plan);
+        trace_point("staging started", t_all);
         for (const auto& rel : first) staged->verify_file(manifest, rel, &st);
+        trace_point("store verified", t_all);
     } catch (const Error&) {
         rethrow_in_step("archive integrity");
     }
@@ -473,6 +489,7 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
     mt.gate = false;  // part of a pipeline: no stream hold for the events
     launch_materialize(dev, store, req, out.data(), &mt);
     const auto t2 = Clock::now();
+    trace_point("kernel launched", t_all);
     if (host_out) {
         dev.make_current();
         cuda_check(cudaMemcpyAsync(host_out, out.data(), H.members_image_bytes, cudaMemcpyDeviceToHost,
@@ -481,6 +498,7 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
     }
     try {
         staged->verify(manifest, &st);  // every file, while the D2H runs
+        trace_point("all files verified", t_all);
     } catch (const Error&) {
         cudaStreamSynchronize(dev.stream());
         rethrow_in_step("archive integrity");

@@ -3,7 +3,7 @@
 // (pipeline.cpp:411-417) and the PrepareFn over every member
 // (pipeline.cpp:506-514) — as one host->HBM->host pipeline.
 //
-//   read   every manifest-listed file, `lanes` host threads, 8 MiB pieces,
+//   read   every manifest-listed file, `lanes` host threads, 2 MiB pieces,
 //          into leased pinned staging; each piece is DMAed to HBM as soon as
 //          it is read (reads and H2D overlap)
 //   verify one GPU CRC-64/XZ launch over all files vs the manifest digests
@@ -80,7 +80,7 @@ struct StageTimings {
 
 // All manifest-listed files, CRC-checked while they stream in:
 //
-//   reader lanes (host threads) take 8 MiB pieces in order — device files'
+//   reader lanes (host threads) take 2 MiB pieces in order — device files'
 //   pieces first, then host-kept files, then hash-only ones. A device piece
 //   is pread into leased pinned staging, then (in one submission order) its
 //   H2D copy goes on the copy stream and the CRC of its 64 KiB blocks on the
