@@ -40,7 +40,8 @@ constexpr uint32_t kNoMember = 0xFFFFFFFFu;
 // FOUNDRY_DEBUG=1 prints LOAD phase boundaries to stderr (diagnostics only).
 void debug_phase(const char* what) {
     static const bool on = std::getenv("FOUNDRY_DEBUG") != nullptr;
-    if (on) std::fprintf(stderr, "[foundry] %s\n", what);
+    static const auto t0 = Clock::now();
+    if (on) std::fprintf(stderr, "[foundry] %9.3f ms  %s\n", ms_since(t0), what);
 }
 uint64_t rd64(const uint8_t* p) {
     uint64_t v;
@@ -371,6 +372,12 @@ uint64_t ServingContext::Impl::build_graph_for(uint32_t gi, uint32_t m, CUgraph&
         ++calls;
     }
     const auto e = view->edges(gi);
+    static const int edge_mode = std::getenv("FOUNDRY_EDGE_MODE") ? std::atoi(std::getenv("FOUNDRY_EDGE_MODE")) : 0;
+    if (edge_mode == 1) {  // EXPERIMENT: chain
+        for (uint32_t n = 1; n < G.n_nodes; ++n) cu_check(api.cuGraphAddDependencies(graph, &nodes[n-1], &nodes[n], 1), "dep");
+        return calls;
+    }
+    if (edge_mode == 2) return calls;  // EXPERIMENT: no edges
     if (G.n_edges) {
         std::vector<CUgraphNode> from(G.n_edges), to(G.n_edges);
         for (uint32_t i = 0; i < G.n_edges; ++i) {
@@ -412,6 +419,9 @@ void ServingContext::Impl::build_group(uint32_t gi) {
     debug_phase("instantiated group");
     ctx->c_instantiate.fetch_add(1);
     const double inst = ms_since(t1);
+    if (std::getenv("FOUNDRY_DEBUG"))
+        std::fprintf(stderr, "[foundry] group %u: %u nodes %u edges build %.3f ms instantiate %.3f ms\n", gi,
+                     G.n_nodes, G.n_edges, build, inst);
     {
         std::lock_guard lock(stats_mu);  // builder lanes may run concurrently
         lane_acquisitions += 2;
