@@ -262,6 +262,7 @@ std::vector<uint64_t> crc64_device(Device& dev, const unsigned char* d_base,
             blocks.push_back(b);
         }
         count[s] = static_cast<uint32_t>(blocks.size()) - first[s];
+        require(count[s] <= kCrcMaxSegmentBlocks, Errc::invalid_argument, "CRC segment longer than 64 GiB");
     }
     const size_t nb = blocks.size(), ns = segments.size();
     // one scratch allocation: block table | first | count | crc | len | out

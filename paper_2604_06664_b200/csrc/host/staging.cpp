@@ -175,6 +175,7 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const Manifest& 
                 blocks.push_back({f.dseg, static_cast<uint32_t>(std::min<uint64_t>(kCrcBlockBytes, f.length - o)),
                                   f.offset + o});
             f.n_blocks = static_cast<uint32_t>(blocks.size()) - f.first_block;
+            require(f.n_blocks <= kCrcMaxSegmentBlocks, Errc::invalid_argument, f.rel + ": longer than 64 GiB");
             seg_first.push_back(f.first_block);
             seg_count.push_back(f.n_blocks);
             device_bytes_ = total_;

@@ -47,7 +47,8 @@ cudaError_t fdy_materialize_occupancy(int* blocks_per_sm);
 // member grid under programmatic dependent launch (both on `stream`).
 cudaError_t fdy_launch_materialize(const FdyMaterializeArgs* args, int grid, cudaStream_t stream);
 
-cudaError_t fdy_crc64_set_constants(const uint64_t* x2k64);  // per device
+// per device: x^(2^k) mod P and the constant-multiplier nibble tables built from them
+cudaError_t fdy_crc64_set_constants(const uint64_t* x2k64);
 // CRC-64/XZ of n_segments byte ranges already resident in device memory.
 // blocks: host-built table (see fdy_crc_plan) in device memory; partial /
 // lengths scratch: n_blocks entries each; out: n_segments digests (device).
@@ -67,4 +68,5 @@ cudaError_t fdy_launch_crc64(const unsigned char* base, const FdyCrcBlock* block
                              cudaStream_t stream);
 }
 
-inline constexpr uint32_t kCrcBlockBytes = 65536;  // one CTA, 256 B per thread
+inline constexpr uint32_t kCrcBlockBytes = 65536;  // one CTA, 8 KiB per warp
+inline constexpr uint32_t kCrcMaxSegmentBlocks = (1u << 20) + 1;  // fold tables: 64 GiB per segment
