@@ -1,15 +1,19 @@
 #!/bin/bash
-# ncu evidence for the bench command (1 GPU): launch list + full sets of the two
-# kernels on the LOAD path. Results land in gpurun_out/; summaries go to profiles/.
+# ncu evidence for the bench command (1 GPU): launch list + full sets of the
+# kernels on the path. Results land in gpurun_out/; summaries go to profiles/.
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-B="python bench.py --steps 3 --warmup 1 --e2e-steps 1 --skip-load --no-cpu-baseline"
+B="python bench.py --steps 3 --warmup 3 --e2e-steps 1 --skip-load --no-cpu-baseline"
 $B > /dev/null 2>&1   # writes the archive once (not under the profiler)
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file gpurun_out/launches_bench.csv $B > gpurun_out/launches_bench.stdout 2>&1
-ncu --set full --clock-control none --import-source on -k regex:fdy_materialize -s 2 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"fdy_(materialize|relocate)" -s 6 -c 2 \
     -o gpurun_out/prof_materialize -f $B > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:crc_blocks -s 1 -c 1 \
-    -o gpurun_out/prof_crc -f $B > /dev/null 2>&1
+# GPU CRC-64 at archive scale (277 MB in 3 segments)
+ncu --set full --clock-control none --import-source on -k regex:crc_ -s 2 -c 2 \
+    -o gpurun_out/prof_crc -f python tools/gpu_crc_bench.py > /dev/null 2>&1
+python tools/gpu_crc_bench.py > gpurun_out/crc_bench.json
+python tools/gpu_floor.py > gpurun_out/gpu_floor.json 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/write_ceiling tools/write_ceiling.cu && /tmp/write_ceiling > gpurun_out/write_ceiling.jsonl
 echo PROFILE-DONE

@@ -43,14 +43,14 @@ def unit_scale(unit: str) -> float:
             "Ghz": 1e9, "Mhz": 1e6, "hz": 1}.get(unit, 1)
 
 
-def raw_page(rep: str) -> dict:
+def raw_page(rep: str, kernel: str = "fdy_materialize_kernel") -> dict:
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], check=True,
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     res = {}
     for row in rows[2:]:
-        if "fdy_materialize_kernel" not in ",".join(row):
+        if kernel not in ",".join(row):
             continue
         for m, key in METRICS.items():
             if m in hdr:
@@ -81,13 +81,14 @@ def launch_list(path: str) -> dict:
 
 def main() -> None:
     rep, launches, out = sys.argv[1:4]
-    full = raw_page(rep)
+    kernel = sys.argv[4] if len(sys.argv) > 4 else "fdy_materialize_kernel"
+    full = raw_page(rep, kernel)
     ll = launch_list(launches)
     mat = ll.get("fdy_materialize_kernel", {}).get("mean_ns", 0.0)
     rel = ll.get("fdy_relocate_templates_kernel", {}).get("mean_ns", 0.0)
     summary = {
-        "kernel": "fdy_materialize_kernel (K2+K1+K3 fused member pass)",
-        "command": "python bench.py --steps 3 --warmup 1 --e2e-steps 1 --skip-load --no-cpu-baseline",
+        "kernel": kernel,
+        "command": "python bench.py --steps 3 --warmup 3 --e2e-steps 1 --skip-load --no-cpu-baseline (tools/gpu_profile_bench.sh)",
         "source": {"full_set": rep, "launch_list": launches},
         **{k: v for k, v in full.items()},
         # one fdy_materialize launch = the template relocation grid (delta != 0,
