@@ -227,9 +227,15 @@ def main():
     from paper_2604_06664_b200 import capi
     from paper_2604_06664_b200.multirank import RankGroup, distribute_store, tp_rank
 
+    # FOUNDRY_BENCH_SHARED_GPU=1 (testing the N>1 path on a one-GPU box): every
+    # rank runs on cuda:0 and the plumbing goes over gloo (NCCL refuses two
+    # ranks on one device). The driver's runs never set it.
+    shared = os.environ.get("FOUNDRY_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     group = RankGroup(grank, gworld, local)
-    group.init("nccl")
+    group.init("gloo" if shared else "nccl")
     barrier, reduce_max = group.barrier, group.max
 
     archive, plain = prepare_archives(args.workload, grank, barrier)
