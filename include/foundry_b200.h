@@ -17,6 +17,11 @@
  *       fdy_serving_counter(s)   <- ServingContext::counters()               pipeline.hpp:100
  *       fdy_serving_template_count <- ServingHandle.template_count           module.cpp:32
  *       fdy_serving_close        <- ~ServingContext
+ *       fdy_serving_capture_graph   GPU-side SAVE: the batch's graph
+ *                                   stream-captured on the device and extracted back,
+ *                                   as the FNDG record encode_graph_record writes
+ *                                   (reference graph_model.cpp:205-218; capture
+ *                                   semantics sim_driver.cpp:222-290)
  *
  *  2. Kernel API — the per-member work of the reference PrepareFn
  *     (pipeline.cpp:506-514: parse_graph_at graph_model.cpp:295-303 +
@@ -166,6 +171,8 @@ int fdy_serving_counter(fdy_serving* s, const char* key, uint64_t* value);
 int fdy_serving_counters(fdy_serving* s, char* buf, size_t cap, size_t* len);
 uint32_t fdy_serving_template_count(const fdy_serving* s);
 void fdy_serving_close(fdy_serving* s);
+/* Bytes written to buf (up to cap); *len = the record's full length. */
+int fdy_serving_capture_graph(fdy_serving* s, uint32_t batch, unsigned char* buf, size_t cap, size_t* len);
 
 #ifdef __cplusplus
 }

@@ -45,6 +45,7 @@ HOST_SRCS = [
     "host/driver_api.cpp",
     "host/gpu_context.cpp",
     "host/staging.cpp",
+    "host/capture.cpp",
     "host/pipeline.cpp",
     "host/tooling.cpp",
     "capi/capi_misc.cpp",

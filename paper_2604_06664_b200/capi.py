@@ -114,10 +114,35 @@ class CApi:
         L.fdy_serving_replay.argtypes = [P, ctypes.c_uint32, ctypes.c_char_p, ctypes.c_size_t,
                                          ctypes.POINTER(ctypes.c_size_t)]
         L.fdy_serving_close.argtypes = [P]
+        L.fdy_serving_capture_graph.argtypes = [P, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_size_t,
+                                                ctypes.POINTER(ctypes.c_size_t)]
 
     def check(self, rc: int) -> None:
         if rc:
             raise CApiError(rc, self.lib.fdy_last_error().decode())
+
+    # ---- session layer (the reference's LOAD surface)
+    def load(self, archive: str, rank: int = 0, world: int = 1, relocate: bool = False):
+        o = LoadOptions()
+        self.lib.fdy_load_options_init(ctypes.byref(o))
+        o.rank, o.world, o.relocate = rank, world, int(relocate)
+        h = ctypes.c_void_p()
+        self.check(self.lib.fdy_load(archive.encode(), ctypes.byref(o), ctypes.byref(h)))
+        return h
+
+    def serving_replay(self, h, batch: int) -> str:
+        n = ctypes.c_size_t()
+        self.check(self.lib.fdy_serving_replay(h, batch, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        self.check(self.lib.fdy_serving_replay(h, batch, buf, n.value + 1, ctypes.byref(n)))
+        return buf.raw[:n.value].decode()
+
+    def serving_capture_graph(self, h, batch: int) -> bytes:
+        n = ctypes.c_size_t()
+        self.check(self.lib.fdy_serving_capture_graph(h, batch, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        self.check(self.lib.fdy_serving_capture_graph(h, batch, buf, n.value, ctypes.byref(n)))
+        return buf.raw[:n.value]
 
     # ---- kernel layer
     def device_open(self, ordinal: int = 0):

@@ -85,6 +85,16 @@ struct ServingHandle {
         }
         return py::make_tuple(ok, rep);
     }
+    // GPU-side SAVE: the FNDG record (encode_graph_record) of batch's graph as
+    // stream-captured on the device and extracted back from the driver
+    py::bytes capture_graph(uint32_t batch) {
+        std::vector<uint8_t> rec;
+        {
+            py::gil_scoped_release nogil;
+            rec = encode_graph_record(ctx().capture_graph(batch));
+        }
+        return py::bytes(reinterpret_cast<const char*>(rec.data()), rec.size());
+    }
     uint64_t naive_rebuild_all() {
         py::gil_scoped_release nogil;
         return ctx().naive_rebuild_all();
@@ -171,6 +181,8 @@ PYBIND11_MODULE(_foundry, m) {
         .def("serve", &ServingHandle::serve, py::arg("batch"), py::call_guard<py::gil_scoped_release>())
         .def("region_base", &ServingHandle::region_base)
         .def("fresh_capture_check", &ServingHandle::fresh_capture_check, py::arg("batch"))
+        .def("capture_graph", &ServingHandle::capture_graph, py::arg("batch"),
+             "GPU-side SAVE: stream-capture the batch's graph and extract it (FNDG record bytes)")
         .def("naive_rebuild_all", &ServingHandle::naive_rebuild_all)
         .def("close", &ServingHandle::close, "Release the rank's graphs, libraries and VA region now")
         .def("__enter__", [](py::object self) { return self; })

@@ -64,6 +64,15 @@ int fdy_serving_replay(fdy_serving* s, uint32_t batch, char* buf, size_t cap, si
     });
 }
 
+int fdy_serving_capture_graph(fdy_serving* s, uint32_t batch, unsigned char* buf, size_t cap, size_t* len) {
+    return fdy_guard([&] {
+        require(s != nullptr, Errc::invalid_argument, "fdy_serving_capture_graph: null handle");
+        const std::vector<uint8_t> rec = encode_graph_record(s->sc.capture_graph(batch));
+        if (len) *len = rec.size();
+        if (buf) std::memcpy(buf, rec.data(), std::min(cap, rec.size()));
+    });
+}
+
 int fdy_serving_batches(fdy_serving* s, uint32_t* out, size_t cap, size_t* count) {
     return fdy_guard([&] {
         require(s != nullptr, Errc::invalid_argument, "fdy_serving_batches: null handle");

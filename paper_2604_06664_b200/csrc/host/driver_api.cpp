@@ -18,10 +18,10 @@ std::once_flag g_once;
 std::string g_error;
 
 template <typename Fn>
-void resolve(Fn& slot, const char* symbol) {
+void resolve(Fn& slot, const char* symbol, unsigned version = 12000) {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q{};
-    const cudaError_t e = cudaGetDriverEntryPointByVersion(symbol, &p, 12000, cudaEnableDefault, &q);
+    const cudaError_t e = cudaGetDriverEntryPointByVersion(symbol, &p, version, cudaEnableDefault, &q);
     if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || p == nullptr) {
         cudaGetLastError();
         if (g_error.empty()) g_error = std::string("cannot resolve driver entry point ") + symbol;
@@ -73,6 +73,15 @@ void load_all() {
     FDY_RESOLVE(cuLaunchKernel);
     FDY_RESOLVE(cuMemsetD8Async);
     FDY_RESOLVE(cuMemsetD32Async);
+    FDY_RESOLVE(cuGraphGetNodes);
+    FDY_RESOLVE(cuGraphGetEdges);
+    FDY_RESOLVE(cuGraphNodeGetType);
+    FDY_RESOLVE(cuGraphKernelNodeGetParams);
+    FDY_RESOLVE(cuGraphMemcpyNodeGetParams);
+    FDY_RESOLVE(cuGraphMemsetNodeGetParams);
+    FDY_RESOLVE(cuGraphKernelNodeGetAttribute);
+    resolve(g_api.cuFuncGetParamInfo, "cuFuncGetParamInfo", 12040);
+    FDY_RESOLVE(cuLaunchKernelEx);
 #undef FDY_RESOLVE
 }
 

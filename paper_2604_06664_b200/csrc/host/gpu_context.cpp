@@ -117,6 +117,7 @@ uint32_t GpuContext::register_library(uint64_t hash, const KernelImage& image, O
         k.entry_id = (ordinal << 16) | i;
         k.arg_buffer_size = e.arg_buffer_size;
         k.hidden_offsets = e.hidden_offsets;
+        k.attrs = e.attrs;
         k.name = e.name;
         k.binary_hash = hash;
         const uint32_t ki = static_cast<uint32_t>(kernels_.size());
@@ -151,6 +152,22 @@ const GpuContext::Kernel* GpuContext::find_kernel(uint64_t hash, std::string_vie
 const GpuContext::Kernel* GpuContext::kernel_by_entry_id(uint32_t id) const {
     auto it = by_entry_id_.find(id);
     return it == by_entry_id_.end() ? nullptr : &kernels_[it->second];
+}
+
+const GpuContext::Kernel* GpuContext::kernel_by_handle(CUfunction fn, CUkernel kern) const {
+    std::lock_guard lock(fn_mu_);  // fn is filled lazily under this lock
+    for (const auto& k : kernels_)
+        if ((fn && k.fn == fn) || (kern && k.kern == kern)) return &k;
+    if (fn) {  // a function handle obtained outside function(): compare through the kernel
+        for (const auto& k : kernels_) {
+            CUfunction f = nullptr;
+            if (driver().cuKernelGetFunction(&f, k.kern) == CUDA_SUCCESS && f == fn) {
+                k.fn = f;
+                return &k;
+            }
+        }
+    }
+    return nullptr;
 }
 
 bool GpuContext::has_library(uint64_t hash) const {

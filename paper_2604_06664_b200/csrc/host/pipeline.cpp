@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include "foundry/bytes.hpp"
+#include "foundry/capture.hpp"
 #include "foundry/parallel.hpp"
 #include "foundry/staging.hpp"
 #include "foundry/template_store.hpp"
@@ -969,6 +970,119 @@ bool ServingContext::fresh_capture_check(uint32_t batch, std::string* report) {
         *report = "records " + std::to_string(trace_a.size()) + "/" + std::to_string(trace_b.size()) +
                   " region crc " + hex16(crc_a) + "/" + hex16(crc_b) + (ok ? " match" : " MISMATCH");
     return ok;
+}
+
+CapturedGraph ServingContext::capture_graph(uint32_t batch) {
+    Impl& I = *impl_;
+    const DriverApi& api = driver();
+    const uint32_t m = I.member_for(batch);
+    const uint32_t gi = I.view->member(m).group;
+    const fdt_group& G = I.view->group(gi);
+    const uint8_t* img = I.member_image(m);
+    const uint8_t* pool = img + 48ull * G.n_nodes;
+    // predecessors of every node, from the template's edges
+    std::vector<std::vector<uint32_t>> preds(G.n_nodes);
+    const auto e = I.view->edges(gi);
+    for (uint32_t k = 0; k < G.n_edges; ++k) preds[e[2 * k + 1]].push_back(e[2 * k]);
+
+    I.dev->make_current();
+    cudaStream_t st = nullptr;  // a private stream: nothing else may join the capture
+    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate(capture)");
+    std::vector<CUgraphNode> captured(G.n_nodes, nullptr);
+    cudaGraph_t graph = nullptr;
+    auto cleanup = [&] {
+        if (graph) cudaGraphDestroy(graph);
+        cudaStreamDestroy(st);
+    };
+    try {
+        cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+        for (uint32_t n = 0; n < G.n_nodes; ++n) {
+            std::vector<cudaGraphNode_t> deps;
+            for (uint32_t p : preds[n]) deps.push_back(reinterpret_cast<cudaGraphNode_t>(captured[p]));
+            cuda_check(cudaStreamUpdateCaptureDependencies(st, deps.data(), deps.size(),
+                                                           cudaStreamSetCaptureDependencies),
+                       "cudaStreamUpdateCaptureDependencies");
+            fdt_node d;
+            std::memcpy(&d, img + 48ull * n, sizeof d);
+            const uint8_t* blob = pool + d.blob_off;
+            if (d.type == 0) {
+                const auto& K = I.resolve(d.kernel, n);
+                size_t size = K.arg_buffer_size;
+                void* extra[5] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<uint8_t*>(blob),
+                                  CU_LAUNCH_PARAM_BUFFER_SIZE, &size, CU_LAUNCH_PARAM_END};
+                // the launch attributes the template build applies (build_graph_for)
+                const fdt_node_attrs& a = I.view->node_attrs(gi, n);
+                CUlaunchAttribute attrs[2];
+                unsigned na = 0;
+                const uint32_t csize = a.cluster[0] * a.cluster[1] * a.cluster[2];
+                if (csize > 1 && csize <= 8 && d.grid[0] % a.cluster[0] == 0 && d.grid[1] % a.cluster[1] == 0 &&
+                    d.grid[2] % a.cluster[2] == 0) {
+                    attrs[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+                    attrs[na].value.clusterDim.x = a.cluster[0];
+                    attrs[na].value.clusterDim.y = a.cluster[1];
+                    attrs[na].value.clusterDim.z = a.cluster[2];
+                    ++na;
+                }
+                if (a.sched_policy > 0 && a.sched_policy <= 2) {
+                    attrs[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_SCHEDULING_POLICY_PREFERENCE;
+                    attrs[na].value.clusterSchedulingPolicyPreference =
+                        static_cast<CUclusterSchedulingPolicy>(a.sched_policy);
+                    ++na;
+                }
+                CUlaunchConfig cfg{};
+                cfg.gridDimX = d.grid[0], cfg.gridDimY = d.grid[1], cfg.gridDimZ = d.grid[2];
+                cfg.blockDimX = d.block[0], cfg.blockDimY = d.block[1], cfg.blockDimZ = d.block[2];
+                cfg.sharedMemBytes = d.shmem;
+                cfg.hStream = st;
+                cfg.attrs = na ? attrs : nullptr;
+                cfg.numAttrs = na;
+                cu_check(api.cuLaunchKernelEx(&cfg, I.ctx->function(K), nullptr, extra), "cuLaunchKernelEx(capture)");
+            } else if (d.type == 1) {
+                cuda_check(cudaMemcpyAsync(reinterpret_cast<void*>(rd64(blob + 8)),
+                                           reinterpret_cast<const void*>(rd64(blob)), rd64(blob + 16),
+                                           cudaMemcpyDeviceToDevice, st),
+                           "cudaMemcpyAsync(capture)");
+            } else if (d.type == 2) {
+                const uint64_t value = rd64(blob + 8), len = rd64(blob + 16);
+                if (value <= 0xFF)
+                    cu_check(api.cuMemsetD8Async(rd64(blob), static_cast<unsigned char>(value), len, st),
+                             "cuMemsetD8Async(capture)");
+                else
+                    cu_check(api.cuMemsetD32Async(rd64(blob), static_cast<unsigned int>(value), len / 4, st),
+                             "cuMemsetD32Async(capture)");
+            } else {  // no stream operation makes an empty node: add it to the capture graph
+                cudaStreamCaptureStatus status;
+                cudaGraph_t cg = nullptr;
+                cuda_check(cudaStreamGetCaptureInfo(st, &status, nullptr, &cg), "cudaStreamGetCaptureInfo");
+                cudaGraphNode_t empty = nullptr;
+                cuda_check(cudaGraphAddEmptyNode(&empty, cg, deps.data(), deps.size()), "cudaGraphAddEmptyNode");
+                cuda_check(cudaStreamUpdateCaptureDependencies(st, &empty, 1, cudaStreamSetCaptureDependencies),
+                           "cudaStreamUpdateCaptureDependencies");
+            }
+            // the node just captured is the stream's whole dependency set now
+            cudaStreamCaptureStatus status;
+            const cudaGraphNode_t* now = nullptr;
+            size_t n_now = 0;
+            cuda_check(cudaStreamGetCaptureInfo(st, &status, nullptr, nullptr, &now, &n_now),
+                       "cudaStreamGetCaptureInfo");
+            require(status == cudaStreamCaptureStatusActive && n_now == 1, Errc::cuda_error,
+                    "capture of node " + std::to_string(n) + " did not yield exactly one graph node");
+            captured[n] = reinterpret_cast<CUgraphNode>(now[0]);
+        }
+        cuda_check(cudaStreamEndCapture(st, &graph), "cudaStreamEndCapture");
+        CapturedGraph g = extract_graph(*I.ctx, reinterpret_cast<CUgraph>(graph), batch, captured);
+        cleanup();
+        return g;
+    } catch (...) {
+        if (!graph) {
+            cudaGraph_t partial = nullptr;
+            cudaStreamEndCapture(st, &partial);  // leave capture mode before unwinding
+            if (partial) cudaGraphDestroy(partial);
+            cudaGetLastError();
+        }
+        cleanup();
+        throw;
+    }
 }
 
 uint64_t ServingContext::naive_rebuild_all() {

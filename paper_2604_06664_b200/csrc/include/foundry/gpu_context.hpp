@@ -60,6 +60,7 @@ public:
         std::vector<uint32_t> hidden_offsets;
         std::string name;
         uint64_t binary_hash = 0;
+        FuncAttrs attrs;                   // the catalog entry's captured attributes
     };
     // A loaded library before registration: only driver calls, so several
     // host threads may open libraries concurrently (cuLibraryLoadData scales
@@ -91,6 +92,9 @@ public:
     bool library_requires_init(uint32_t library) const;
     const Kernel* find_kernel(uint64_t hash, std::string_view name) const;
     const Kernel* kernel_by_entry_id(uint32_t entry_id) const;
+    // Reverse lookup for graph extraction: the restored kernel a node's
+    // function (or context-independent kernel handle) belongs to.
+    const Kernel* kernel_by_handle(CUfunction fn, CUkernel kern) const;
     bool has_library(uint64_t hash) const;
 
     // ------------------------------------------------------------ region

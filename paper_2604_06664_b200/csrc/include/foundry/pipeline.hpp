@@ -106,6 +106,10 @@ public:
     // zeroed region, and compares the device trace records and a GPU CRC-64 of
     // the whole region. Returns true when both agree (details in *report).
     bool fresh_capture_check(uint32_t batch, std::string* report = nullptr);
+    // GPU-side SAVE: stream-captures batch's materialized work
+    // with the template's dependencies (cudaStreamUpdateCaptureDependencies per
+    // node) and extracts the driver's graph back into the portable model.
+    CapturedGraph capture_graph(uint32_t batch);
 
     struct Impl;
 

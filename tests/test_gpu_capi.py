@@ -222,3 +222,27 @@ def test_ipc_fanout_between_two_processes(foundry, oracle, archives, tmp_path):
         got = (tmp_path / ("rank%d.fndg" % rank)).read_bytes()
         want, _ = oracle.materialize_archive(arch, 2 + rank, 8, 0x10000 * (rank + 1))
         assert got == want, rank
+
+
+def test_session_layer_load_replay_and_capture(foundry, oracle, archives, api):
+    """The reference's LOAD surface through the C-ABI (fdy_load ->
+    fdy_serving_replay / fdy_serving_capture_graph): traces equal the oracle's,
+    and the GPU-captured graph record equals the oracle's member record except
+    for node launch attributes (test_gpu_pipeline.py explains which)."""
+    import fndg
+
+    arch, _ = archives("moe-spmd")
+    container, _ = oracle.materialize_archive(arch, 5, 8, 0)
+    graphs = {g.label: g for g in fndg.graphs(container)}
+    hidden = fndg.hidden_map(arch)
+    h = api.load(arch, rank=5, world=8)
+    try:
+        for b in (1, 2, 9, 100, 512):
+            assert api.serving_replay(h, b) == fndg.trace_text(graphs[b], hidden, oracle.crc64)
+            got = fndg.decode_record(api.serving_capture_graph(h, b))
+            ref = graphs[b]
+            assert got.edges == ref.edges
+            assert [(n.type, n.grid, n.block, n.shmem, n.name, n.args, n.mem) for n in got.nodes] == \
+                   [(n.type, n.grid, n.block, n.shmem, n.name, n.args, n.mem) for n in ref.nodes]
+    finally:
+        api.lib.fdy_serving_close(h)

@@ -177,3 +177,45 @@ def test_naive_rebuild_costs_more_construction(foundry, load, archives):
     c = h.counters()
     templated = c["graph.add_node_calls"] + c["graph.add_edge_calls"] + c["graph.set_attr_calls"] + c["exec.instantiate_calls"]
     assert naive / templated >= 8 / 3 - 0.01
+
+
+def _without_node_attrs(g):
+    for n in g.nodes:
+        n.attrs = b""
+    return g
+
+
+@pytest.mark.parametrize("name,rank,world,relocate", [
+    ("micro", 0, 1, False), ("llama3-8b", 0, 1, False), ("moe-spmd", 1, 4, False), ("moe-spmd", 2, 4, True),
+])
+def test_gpu_capture_extracts_the_oracle_graph(foundry, load, oracle, archives, name, rank, world, relocate):
+    """GPU-side SAVE: the member's work is stream-captured on
+    the device with the template's dependencies, and the driver's graph is
+    extracted back (cuGraphGetNodes/GetEdges, cuGraphKernelNodeGetParams +
+    cuFuncGetParamInfo flattening). The FNDG record equals the oracle's
+    materialized member byte for byte, except the per-node launch attributes
+    the hardware cannot carry (reference cluster dims that do not divide the
+    grid): those are compared where they were applied."""
+    arch, _ = archives(name)
+    base = manifest(arch)["allocator"]["base"]
+    if relocate:  # a second handle holds the captured base: this one is relocated
+        load(arch, rank=0, world=world)
+    h = load(arch, rank=rank, world=world, relocate=relocate)
+    delta = h.region_base() - base
+    assert (delta != 0) == relocate
+    container, _ = oracle.materialize_archive(arch, rank, world, delta)
+    want = {g.label: g for g in fndg.graphs(container)}
+    for b in h.batches()[:: max(1, len(h.batches()) // 12)]:
+        got = fndg.decode_record(h.capture_graph(b))
+        ref = want[b]
+        assert got.label == b and len(got.nodes) == len(ref.nodes)
+        assert got.edges == ref.edges
+        for gn, rn in zip(got.nodes, ref.nodes):
+            assert (gn.type, gn.grid, gn.block, gn.shmem, gn.hash, gn.name, gn.fattrs, gn.args, gn.mem) == \
+                   (rn.type, rn.grid, rn.block, rn.shmem, rn.hash, rn.name, rn.fattrs, rn.args, rn.mem), \
+                   "batch %d node %d" % (b, gn.id)
+            if gn.type == 0 and rn.attrs[12:16] != b"\0\0\0\0":
+                # an explicitly applied scheduling policy (i32 after the 3 x u32
+                # cluster dims) reads back; an unset one reads back as the
+                # driver's effective default, which the model cannot tell apart
+                assert gn.attrs[12:16] == rn.attrs[12:16], "batch %d node %d policy" % (b, gn.id)
