@@ -317,6 +317,18 @@ def main():
             breakdowns.append(h.timings())
             h.close()
         load_ms = reduce_max(statistics.mean(load_times)) if load_times else None
+        # the same LOAD with LoadOptions.share_execs (one cuGraphInstantiate per graph shape)
+        shared_times, shared_bd = [], []
+        for _ in range(0 if args.skip_load else args.load_steps):
+            barrier()
+            t0 = time.perf_counter()
+            h = foundry.load(archive, rank=wrank, world=TP_WORLD, share_execs=True)
+            trace_s = h.replay(1)
+            shared_times.append((time.perf_counter() - t0) * 1e3)
+            shared_bd.append(dict(h.timings(), instantiate_calls=h.counters()["exec.instantiate_calls"]))
+            assert trace_s == trace, "share_execs replay differs"
+            h.close()
+        shared_ms = reduce_max(statistics.mean(shared_times)) if shared_times else None
     clocks = sampler.summary()
 
     api.lib.fdy_members_free(members)
@@ -338,6 +350,8 @@ def main():
             traffic = None
     bd = {k: statistics.mean(b[k] for b in breakdowns) for k in breakdowns[0]} if breakdowns else {}
     driver_bound = bd.get("restore_ms", 0) + bd.get("build_ms", 0) + bd.get("instantiate_ms", 0)
+    sbd = {k: statistics.mean(b[k] for b in shared_bd) for k in shared_bd[0]} if shared_bd else {}
+    shared_driver = sum(sbd.get(k, 0) for k in ("restore_ms", "build_ms", "instantiate_ms", "function_load_ms"))
     ep = {k: statistics.mean(p[k] for p in e2e_parts) for k in e2e_parts[0]}
 
     # ---------------- CPU baseline: the reference itself, rank 0, N=1 ----------------
@@ -405,6 +419,14 @@ def main():
                       "d2h_bytes_per_step": int(bd.get("d2h_bytes", 0)) + len(trace),
                       "breakdown": {k: v for k, v in bd.items()
                                     if k.endswith("_ms") and k != "crc_kernel_ms"}},
+        "full_load_shared_execs": None if shared_ms is None else {
+            "value": shared_ms, "unit": "ms", "steps": args.load_steps,
+            "api": "paper_2604_06664_b200.load(archive, rank, world, share_execs=True).replay(1)",
+            "instantiate_calls": shared_bd[0]["instantiate_calls"],
+            "driver_bound_ms": shared_driver,
+            "driver_bound": "cuLibraryLoadData + cuFuncLoad of every template's functions + "
+                            "cuGraphAdd*/cuGraphInstantiate per graph shape",
+            "breakdown": {k: v for k, v in sbd.items() if k.endswith("_ms") and k != "crc_kernel_ms"}},
         "cpu_baseline": cpu,
         "clocks": clocks,
         "gpu_launches": args.steps * (2 if delta else 1),  # relocation grid + member grid

@@ -160,6 +160,7 @@ typedef struct {
     int32_t skip_device_init;
     int64_t base_shift_granules;
     int32_t extra_prewindow_alloc;
+    int32_t share_execs;     /* B200: one instantiated exec per graph shape (LoadOptions.share_execs) */
 } fdy_load_options;
 
 void fdy_load_options_init(fdy_load_options* opts);

@@ -38,6 +38,7 @@ class LoadOptions(ctypes.Structure):
         ("skip_device_init", ctypes.c_int32),
         ("base_shift_granules", ctypes.c_int64),
         ("extra_prewindow_alloc", ctypes.c_int32),
+        ("share_execs", ctypes.c_int32),
     ]
 
 
@@ -122,10 +123,11 @@ class CApi:
             raise CApiError(rc, self.lib.fdy_last_error().decode())
 
     # ---- session layer (the reference's LOAD surface)
-    def load(self, archive: str, rank: int = 0, world: int = 1, relocate: bool = False):
+    def load(self, archive: str, rank: int = 0, world: int = 1, relocate: bool = False,
+             share_execs: bool = False):
         o = LoadOptions()
         self.lib.fdy_load_options_init(ctypes.byref(o))
-        o.rank, o.world, o.relocate = rank, world, int(relocate)
+        o.rank, o.world, o.relocate, o.share_execs = rank, world, int(relocate), int(share_execs)
         h = ctypes.c_void_p()
         self.check(self.lib.fdy_load(archive.encode(), ctypes.byref(o), ctypes.byref(h)))
         return h

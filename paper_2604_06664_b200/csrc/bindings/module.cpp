@@ -56,6 +56,7 @@ struct ServingHandle {
         d["materialize_ms"] = t.materialize_ms;
         d["download_ms"] = t.download_ms;
         d["build_ms"] = t.build_ms;
+        d["function_load_ms"] = t.function_load_ms;
         d["instantiate_ms"] = t.instantiate_ms;
         d["foreground_ms"] = t.foreground_ms;
         d["crc_kernel_ms"] = t.crc_kernel_ms;
@@ -125,7 +126,7 @@ SaveOutcome do_save(const WorkloadSpec& spec, const std::string& out, bool emit_
 ServingHandle do_load(const std::string& archive, uint32_t rank, uint32_t world, bool preallocate,
                       int device, bool relocate, unsigned prepare_lanes, bool skip_binary_restore,
                       bool skip_device_init, int64_t base_shift_granules, bool extra_prewindow_alloc,
-                      bool verify_replay) {
+                      bool verify_replay, bool share_execs) {
     LoadOptions o;
     o.rank = rank;
     o.world = world;
@@ -134,6 +135,7 @@ ServingHandle do_load(const std::string& archive, uint32_t rank, uint32_t world,
     o.relocate = relocate;
     o.prepare_lanes = prepare_lanes;
     o.verify_replay = verify_replay;
+    o.share_execs = share_execs;
     o.faults.skip_binary_restore = skip_binary_restore;
     o.faults.skip_device_init = skip_device_init;
     o.faults.base_shift_granules = base_shift_granules;
@@ -199,7 +201,8 @@ PYBIND11_MODULE(_foundry, m) {
           py::arg("preallocate") = true, py::arg("device") = 0, py::arg("relocate") = false,
           py::arg("prepare_lanes") = 4, py::arg("skip_binary_restore") = false,
           py::arg("skip_device_init") = false, py::arg("base_shift_granules") = 0,
-          py::arg("extra_prewindow_alloc") = false, py::arg("verify_replay") = true);
+          py::arg("extra_prewindow_alloc") = false, py::arg("verify_replay") = true,
+          py::arg("share_execs") = false);
     m.def("pack", [](const std::string& archive) {
         py::gil_scoped_release nogil;
         pack_archive(archive);

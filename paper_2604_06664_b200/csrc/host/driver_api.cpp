@@ -82,6 +82,7 @@ void load_all() {
     FDY_RESOLVE(cuGraphKernelNodeGetAttribute);
     resolve(g_api.cuFuncGetParamInfo, "cuFuncGetParamInfo", 12040);
     FDY_RESOLVE(cuLaunchKernelEx);
+    resolve(g_api.cuFuncLoad, "cuFuncLoad", 12040);
 #undef FDY_RESOLVE
 }
 

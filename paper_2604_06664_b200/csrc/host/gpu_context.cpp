@@ -79,6 +79,14 @@ CUfunction GpuContext::function(const Kernel& k) const {
     return k.fn;
 }
 
+void GpuContext::ensure_loaded(const Kernel& k) const {
+    const CUfunction f = function(k);
+    std::lock_guard lock(fn_mu_);
+    if (k.loaded) return;
+    if (driver().cuFuncLoad) cu_check(driver().cuFuncLoad(f), "cuFuncLoad");
+    k.loaded = true;
+}
+
 void GpuContext::set_kernel_attribute(const Kernel& k, CUfunction_attribute attr, int value) const {
     cu_check(driver().cuKernelSetAttribute(attr, value, k.kern, cu_device_), "cuKernelSetAttribute");
 }

@@ -81,8 +81,12 @@ struct ServingContext::Impl {
         CUgraphExec exec = nullptr;
         std::vector<CUgraphNode> nodes;
         uint32_t applied = kNoMember;  // member index currently in the exec
+        uint32_t bound = kNoMember;    // group whose member that is (share_execs: any of the shape)
     };
     std::vector<Group> groups;
+    // share_execs: the group whose graph/exec serves group g (itself otherwise)
+    std::vector<uint32_t> owner;
+    Group& exec_of(uint32_t g) { return groups[owner.empty() ? g : owner[g]]; }
     std::vector<uint32_t> labels;
     uint64_t lane_acquisitions = 0;
     std::mutex stats_mu;
@@ -139,6 +143,8 @@ struct ServingContext::Impl {
     void open_binary(uint64_t hash, const KernelBinaryRecord& rec, uint32_t ordinal, KernelImage& image,
                      GpuContext::OpenedLibrary& opened);
     void build_group(uint32_t g);
+    void prepare_kernels(uint32_t g, uint32_t m, bool load_functions = false);
+    std::string shape_key(uint32_t g);
     uint64_t build_graph_for(uint32_t g, uint32_t m, CUgraph& graph, std::vector<CUgraphNode>& nodes);
     void kernel_params(const fdt_node& d, const uint8_t* blob, const GpuContext::Kernel& K,
                        CUDA_KERNEL_NODE_PARAMS& p, void** extra, size_t* size) const;
@@ -291,16 +297,11 @@ CUDA_MEMSET_NODE_PARAMS ServingContext::Impl::memset_params(const uint8_t* blob)
     return m;
 }
 
-uint64_t ServingContext::Impl::build_graph_for(uint32_t gi, uint32_t m, CUgraph& graph,
-                                               std::vector<CUgraphNode>& nodes) {
-    const DriverApi& api = driver();
-    dev->make_current();
+// validate every kernel node before touching the driver (sim_driver.cpp:295-305)
+// and apply the per-function launch limits its nodes need
+void ServingContext::Impl::prepare_kernels(uint32_t gi, uint32_t m, bool load_functions) {
     const fdt_group& G = view->group(gi);
     const uint8_t* img = member_image(m);
-    const uint8_t* pool = img + 48ull * G.n_nodes;
-    uint64_t calls = 0;
-
-    // validate every kernel node before touching the driver (sim_driver.cpp:295-305)
     for (uint32_t n = 0; n < G.n_nodes; ++n) {
         fdt_node d;
         std::memcpy(&d, img + 48ull * n, sizeof d);
@@ -313,7 +314,48 @@ uint64_t ServingContext::Impl::build_graph_for(uint32_t gi, uint32_t m, CUgraph&
         const int want = std::max<int>(fa.max_dynamic_shared_size_bytes, static_cast<int>(d.shmem));
         if (want > 48 * 1024) ctx->require_dynamic_smem(K, want);
         if (fa.preferred_shared_memory_carveout >= 0) ctx->set_carveout(K, fa.preferred_shared_memory_carveout);
+        if (load_functions) ctx->ensure_loaded(K);
     }
+}
+
+// What an instantiated exec fixes: node count and types, edges, and the launch
+// attributes the template build applies. Groups with equal keys can share one
+// exec (everything else is per-node parameters: cuGraphExec*NodeSetParams).
+std::string ServingContext::Impl::shape_key(uint32_t gi) {
+    const fdt_group& G = view->group(gi);
+    const uint8_t* img = member_image(G.first_member);
+    std::string key;
+    auto put = [&](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
+    put(&G.n_nodes, 4);
+    for (uint32_t n = 0; n < G.n_nodes; ++n) {
+        fdt_node d;
+        std::memcpy(&d, img + 48ull * n, sizeof d);
+        put(&d.type, 1);
+        if (d.type != 0) continue;
+        const fdt_node_attrs& a = view->node_attrs(gi, n);
+        const uint32_t csize = a.cluster[0] * a.cluster[1] * a.cluster[2];
+        const bool cluster_ok = csize > 1 && csize <= 8 && d.grid[0] % a.cluster[0] == 0 &&
+                                d.grid[1] % a.cluster[1] == 0 && d.grid[2] % a.cluster[2] == 0;
+        const uint32_t applied[4] = {cluster_ok ? a.cluster[0] : 1u, cluster_ok ? a.cluster[1] : 1u,
+                                     cluster_ok ? a.cluster[2] : 1u,
+                                     (a.sched_policy > 0 && a.sched_policy <= 2) ? uint32_t(a.sched_policy) : 0u};
+        put(applied, sizeof applied);
+    }
+    const auto e = view->edges(gi);
+    put(e.data(), size_t(G.n_edges) * 2 * sizeof(uint32_t));
+    return key;
+}
+
+uint64_t ServingContext::Impl::build_graph_for(uint32_t gi, uint32_t m, CUgraph& graph,
+                                               std::vector<CUgraphNode>& nodes) {
+    const DriverApi& api = driver();
+    dev->make_current();
+    const fdt_group& G = view->group(gi);
+    const uint8_t* img = member_image(m);
+    const uint8_t* pool = img + 48ull * G.n_nodes;
+    uint64_t calls = 0;
+
+    prepare_kernels(gi, m);
 
     cu_check(api.cuGraphCreate(&graph, 0), "cuGraphCreate");
     nodes.assign(G.n_nodes, nullptr);
@@ -430,27 +472,34 @@ void ServingContext::Impl::build_group(uint32_t gi) {
         t.instantiate_ms += inst;
     }
     grp.applied = m;
+    grp.bound = gi;
 }
 
 // ---------------------------------------------------------------- serve
 
 uint64_t ServingContext::Impl::apply_member(uint32_t gi, uint32_t m) {
-    Group& grp = groups[gi];
+    Group& grp = exec_of(gi);
     if (grp.applied == m) return 0;
     const DriverApi& api = driver();
     dev->make_current();
     const fdt_group& G = view->group(gi);
     const uint8_t* img = member_image(m);
     const uint8_t* pool = img + 48ull * G.n_nodes;
+    // what the exec holds now: a member of this group, or (share_execs) of
+    // another group of the same shape, whose image layout may differ
     const uint8_t* cur = grp.applied == kNoMember ? nullptr : member_image(grp.applied);
+    const uint8_t* cur_pool = cur ? cur + 48ull * view->group(grp.bound).n_nodes : nullptr;
     uint64_t touched = 0;
     for (uint32_t n = 0; n < G.n_nodes; ++n) {
         fdt_node d;
         std::memcpy(&d, img + 48ull * n, sizeof d);
         const uint8_t* blob = pool + d.blob_off;
         if (cur) {
-            const bool same = std::memcmp(cur + 48ull * n, img + 48ull * n, 48) == 0 &&
-                              std::memcmp(cur + 48ull * G.n_nodes + d.blob_off, blob, d.blob_len) == 0;
+            fdt_node c;
+            std::memcpy(&c, cur + 48ull * n, sizeof c);
+            // descriptor up to blob_off (type, kernel, dims, shmem, blob_len), then the bytes
+            const bool same = std::memcmp(&c, &d, offsetof(fdt_node, blob_off)) == 0 &&
+                              std::memcmp(cur_pool + c.blob_off, blob, d.blob_len) == 0;
             if (same) continue;
         }
         ++touched;
@@ -483,6 +532,7 @@ uint64_t ServingContext::Impl::apply_member(uint32_t gi, uint32_t m) {
         }
     }
     grp.applied = m;
+    grp.bound = gi;
     ++lane_acquisitions;
     ctx->c_update.fetch_add(1);
     ctx->c_update_touched.fetch_add(touched);
@@ -559,7 +609,7 @@ LaunchTrace ServingContext::Impl::replay(uint32_t batch) {
     const DriverApi& api = driver();
     dev->make_current();
     ctx->reset_trace();
-    cu_check(api.cuGraphLaunch(groups[gi].exec, dev->stream()), "cuGraphLaunch");
+    cu_check(api.cuGraphLaunch(exec_of(gi).exec, dev->stream()), "cuGraphLaunch");
     ctx->c_replay.fetch_add(1);
     if (!opts.verify_replay) {
         dev->sync();
@@ -770,9 +820,26 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     // (the driver loads each kernel's function lazily when its first node is
     // added; a separate loader thread ahead of the builder measured no gain:
     // function loads and instantiation serialize inside the driver)
+    if (opts.share_execs) {  // one exec per graph shape; the first group of a shape owns it
+        std::map<std::string, uint32_t> first_of_shape;
+        I.owner.resize(H.n_groups);
+        for (uint32_t g = 0; g < H.n_groups; ++g)
+            I.owner[g] = first_of_shape.emplace(I.shape_key(g), g).first->second;
+    }
     std::thread builder([&] {
         try {
-            parallel_for(H.n_groups, build_lanes, [&](size_t g) { I.build_group(static_cast<uint32_t>(g)); });
+            parallel_for(H.n_groups, build_lanes, [&](size_t g) {
+                const uint32_t gi = static_cast<uint32_t>(g);
+                if (I.owner.empty() || I.owner[gi] == gi)
+                    I.build_group(gi);
+                else
+                    // served through the owner's exec: its functions are loaded now, as
+                    // a build would (every template is servable when LOAD returns)
+                    const auto tf = Clock::now();
+                    I.prepare_kernels(gi, I.view->group(gi).first_member, /*load_functions=*/true);
+                    std::lock_guard lock(I.stats_mu);
+                    I.t.function_load_ms += ms_since(tf);
+            });
         } catch (...) {
             builder_error = std::current_exception();
         }
@@ -915,7 +982,7 @@ bool ServingContext::fresh_capture_check(uint32_t batch, std::string* report) {
     I.replay(batch);  // validates addresses, applies member b
     ctx.zero_region();
     ctx.reset_trace();
-    cu_check(api.cuGraphLaunch(I.groups[gi].exec, st), "cuGraphLaunch");
+    cu_check(api.cuGraphLaunch(I.exec_of(gi).exec, st), "cuGraphLaunch");
     dev.sync();
     const auto trace_a = canonical_records(ctx.read_trace());
     const uint64_t crc_a = region_crc();
@@ -1127,7 +1194,7 @@ void ServingContext::exec_update(uint32_t batch_in_group, const CapturedGraph& d
     // donor parameters are applied node by node; the exec no longer holds a member
     const DriverApi& api = driver();
     I.dev->make_current();
-    Impl::Group& grp = I.groups[gi];
+    Impl::Group& grp = I.exec_of(gi);
     for (uint32_t n = 0; n < G.n_nodes; ++n) {
         const GraphNode& node = donor.nodes[n];
         if (node.type == NodeType::Kernel) {
@@ -1158,6 +1225,7 @@ void ServingContext::exec_update(uint32_t batch_in_group, const CapturedGraph& d
         }
     }
     grp.applied = kNoMember;
+    grp.bound = gi;
     ++I.lane_acquisitions;
     I.ctx->c_update.fetch_add(1);
     I.ctx->c_update_touched.fetch_add(G.n_nodes);

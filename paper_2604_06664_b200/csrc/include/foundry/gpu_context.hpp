@@ -53,6 +53,7 @@ public:
         mutable CUfunction fn = nullptr;   // loaded on demand, see function()
         mutable int max_dynamic_smem = 0;  // attribute values already applied
         mutable int carveout = -1;
+        mutable bool loaded = false;       // function forced into the context (ensure_loaded)
         uint32_t library = 0;
         uint32_t entry_index = 0;
         uint32_t entry_id = 0;
@@ -82,6 +83,9 @@ public:
                           uint32_t ordinal, bool requires_device_init);
     // The kernel's CUfunction in this context (cuKernelGetFunction on first use).
     CUfunction function(const Kernel& k) const;
+    // Forces the (lazily loaded) function into the context now (cuFuncLoad),
+    // so a later graph update or launch of it does not stall on the load.
+    void ensure_loaded(const Kernel& k) const;
     void set_kernel_attribute(const Kernel& k, CUfunction_attribute attr, int value) const;
     // Per-kernel launch attributes, applied once: the dynamic shared memory
     // limit only ever grows (every node of the kernel must fit).

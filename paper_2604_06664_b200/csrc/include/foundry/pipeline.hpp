@@ -58,13 +58,21 @@ struct LoadOptions {
     int device = 0;
     bool relocate = false;       // rebase embedded addresses if the VA region moves
     bool verify_replay = true;   // check on-device trace records at replay
+    // Templates whose CUDA graphs have the same shape (node types, edges and the
+    // launch attributes the build applies) share ONE instantiated exec; serve()
+    // switches it between them with cuGraphExec*NodeSetParams on the nodes that
+    // differ. Cold start pays one cuGraphInstantiate per shape instead of one per
+    // template (the driver-bound part of LOAD); a serve that crosses templates
+    // pays a larger update. Off = the reference's one exec per template.
+    bool share_execs = false;
 };
 
 // Wall/kernel time of each LOAD phase (milliseconds) and the DMA volume.
 struct LoadTimings {
     double total_ms = 0, manifest_ms = 0, stage_ms = 0, integrity_ms = 0, restore_ms = 0,
            region_ms = 0, materialize_ms = 0, download_ms = 0, build_ms = 0, instantiate_ms = 0,
-           foreground_ms = 0;
+           foreground_ms = 0,
+           function_load_ms = 0;  // share_execs: loading the functions of exec-sharing templates
     float crc_kernel_ms = 0, materialize_kernel_ms = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0, member_bytes = 0, store_bytes = 0;
     uint64_t graphs = 0, nodes = 0, templates = 0;

@@ -195,6 +195,8 @@ static int cmd_restorebench(int argc, char** argv) {
                         if (stage < 2) continue;
                         CUfunction f;
                         cu_check(api.cuKernelGetFunction(&f, k), "getfunction");
+                        if (stage < 3) continue;
+                        cu_check(api.cuFuncLoad(f), "funcload");
                     }
                 }
             });
@@ -208,6 +210,7 @@ static int cmd_restorebench(int argc, char** argv) {
         run("cuLibraryLoadData", 0, threads);
         run("+ cuLibraryGetKernel", 1, threads);
         run("+ cuKernelGetFunction", 2, threads);
+        run("+ cuFuncLoad", 3, threads);
     }
     return 0;
 }

@@ -219,3 +219,20 @@ def test_gpu_capture_extracts_the_oracle_graph(foundry, load, oracle, archives, 
                 # cluster dims) reads back; an unset one reads back as the
                 # driver's effective default, which the model cannot tell apart
                 assert gn.attrs[12:16] == rn.attrs[12:16], "batch %d node %d policy" % (b, gn.id)
+
+
+@pytest.mark.parametrize("name,rank,world", [("llama3-8b", 0, 1), ("moe-spmd", 3, 4)])
+def test_shared_execs_serve_every_batch_like_the_oracle(foundry, load, oracle, archives, name, rank, world):
+    """LoadOptions.share_execs: templates of one graph shape share an exec, so
+    LOAD instantiates once per shape; serving still reproduces every member
+    (switching the exec between templates in both directions)."""
+    arch, outcome = archives(name)
+    h = load(arch, rank=rank, world=world, share_execs=True)
+    c = h.counters()
+    assert 1 <= c["exec.instantiate_calls"] < outcome.template_count
+    want = expected_traces(oracle, arch, rank, world)
+    order = h.batches() + h.batches()[::-1]  # crosses every template boundary both ways
+    for b in order:
+        assert h.replay(b) == want[b], "batch %d" % b
+    ok, report = h.fresh_capture_check(h.batches()[-1])
+    assert ok, report
