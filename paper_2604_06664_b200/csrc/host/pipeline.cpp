@@ -830,15 +830,16 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
         try {
             parallel_for(H.n_groups, build_lanes, [&](size_t g) {
                 const uint32_t gi = static_cast<uint32_t>(g);
-                if (I.owner.empty() || I.owner[gi] == gi)
+                if (I.owner.empty() || I.owner[gi] == gi) {
                     I.build_group(gi);
-                else
-                    // served through the owner's exec: its functions are loaded now, as
-                    // a build would (every template is servable when LOAD returns)
-                    const auto tf = Clock::now();
-                    I.prepare_kernels(gi, I.view->group(gi).first_member, /*load_functions=*/true);
-                    std::lock_guard lock(I.stats_mu);
-                    I.t.function_load_ms += ms_since(tf);
+                    return;
+                }
+                // served through the owner's exec: its functions are loaded now, as
+                // a build would (every template is servable when LOAD returns)
+                const auto tf = Clock::now();
+                I.prepare_kernels(gi, I.view->group(gi).first_member, /*load_functions=*/true);
+                std::lock_guard lock(I.stats_mu);
+                I.t.function_load_ms += ms_since(tf);
             });
         } catch (...) {
             builder_error = std::current_exception();
