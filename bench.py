@@ -328,6 +328,22 @@ def main():
             shared_bd.append(dict(h.timings(), instantiate_calls=h.counters()["exec.instantiate_calls"]))
             assert trace_s == trace, "share_execs replay differs"
             h.close()
+        # serve sweep (reference ServingSet::serve, templater.cpp:177-188): apply every
+        # batch's parameters in label order, one exec per template vs shared execs
+        serve_ms = {}
+        if not args.skip_load:
+            for mode in ("per_template", "shared_execs", "device_updates"):
+                h = foundry.load(archive, rank=wrank, world=TP_WORLD, share_execs=mode == "shared_execs",
+                                 device_updates=mode == "device_updates")
+                bs = h.batches()
+                t0 = time.perf_counter()
+                touched = sum(h.serve(b) for b in bs)
+                ms = (time.perf_counter() - t0) * 1e3
+                ok = h.replay(bs[-1]) == h.replay(bs[-1])  # the trace is device-verified
+                serve_ms[mode] = {"ms": ms, "us_per_serve": ms * 1e3 / len(bs), "batches": len(bs),
+                                  "nodes_touched": touched, "load_ms": h.timings()["total_ms"],
+                                  "verified": ok}
+                h.close()
         shared_ms = reduce_max(statistics.mean(shared_times)) if shared_times else None
     clocks = sampler.summary()
 
@@ -427,6 +443,7 @@ def main():
             "driver_bound": "cuLibraryLoadData + cuFuncLoad of every template's functions + "
                             "cuGraphAdd*/cuGraphInstantiate per graph shape",
             "breakdown": {k: v for k, v in sbd.items() if k.endswith("_ms") and k != "crc_kernel_ms"}},
+        "serve_sweep": serve_ms or None,
         "cpu_baseline": cpu,
         "clocks": clocks,
         "gpu_launches": args.steps * (2 if delta else 1),  # relocation grid + member grid

@@ -161,6 +161,7 @@ typedef struct {
     int64_t base_shift_granules;
     int32_t extra_prewindow_alloc;
     int32_t share_execs;     /* B200: one instantiated exec per graph shape (LoadOptions.share_execs) */
+    int32_t device_updates;  /* B200: serve applies kernel-node parameters from the GPU (LoadOptions.device_updates) */
 } fdy_load_options;
 
 void fdy_load_options_init(fdy_load_options* opts);

@@ -53,6 +53,7 @@ HOST_SRCS = [
     "capi/capi_session.cpp",
 ]
 CU_SRCS = ["kernels/materialize.cu", "kernels/crc64.cu"]
+RDC_SRCS = ["kernels/serve.cu"]  # device runtime (graph device updates): -rdc + device link
 
 
 def _ninja_bin() -> str:
@@ -90,6 +91,15 @@ def _write_ninja() -> Path:
         "  depfile = $out.d",
         "  deps = gcc",
         "  description = NVCC $in",
+        "rule nvcc_rdc",
+        "  command = $nvcc $nvflags -rdc=true -MD -MF $out.d -c $in -o $out 2> $out.ptxas.log || "
+        "(cat $out.ptxas.log; false)",
+        "  depfile = $out.d",
+        "  deps = gcc",
+        "  description = NVCC-RDC $in",
+        "rule dlink",
+        f"  command = $nvcc {ARCH} -Xcompiler -fPIC -dlink $in -L{CUDA}/lib64 -lcudadevrt -o $out",
+        "  description = DLINK $out",
         "rule ptx",
         f"  command = $nvcc -std=c++17 -arch=sm_100a -rdc=true -ptx -O3 -lineinfo -I{CSRC}/include $in -o $out",
         "  description = PTX $in",
@@ -97,7 +107,7 @@ def _write_ninja() -> Path:
         f"  command = {sys.executable} {CSRC}/tools/embed_ptx.py $in $out",
         "  description = EMBED $in",
         "rule link",
-        f"  command = $cxx -shared -o $out $in {cudart} -ldl -lrt -lpthread "
+        f"  command = $cxx -shared -o $out $in {cudart} {CUDA}/lib64/libcudadevrt.a -ldl -lrt -lpthread "
         "-Wl,-soname,libfoundry_b200.so",
         "  description = LINK $out",
         "rule pymod",
@@ -117,6 +127,14 @@ def _write_ninja() -> Path:
         obj = BUILD / (src.replace("/", "_") + ".o")
         lines.append(f"build {obj}: nvcc {CSRC / src}")
         objs.append(str(obj))
+    rdc_objs = []
+    for src in RDC_SRCS:
+        obj = BUILD / (src.replace("/", "_") + ".o")
+        lines.append(f"build {obj}: nvcc_rdc {CSRC / src}")
+        rdc_objs.append(str(obj))
+    dl = BUILD / "device_link.o"
+    lines.append(f"build {dl}: dlink {' '.join(rdc_objs)}")
+    objs += rdc_objs + [str(dl)]
     ptx = BUILD / "trace_body.ptx"
     lines.append(f"build {ptx}: ptx {CSRC / 'kernels/trace_body.cu'}")
     lines.append(f"build {BUILD / 'trace_body_ptx.cpp'}: embed {ptx}")

@@ -39,6 +39,7 @@ class LoadOptions(ctypes.Structure):
         ("base_shift_granules", ctypes.c_int64),
         ("extra_prewindow_alloc", ctypes.c_int32),
         ("share_execs", ctypes.c_int32),
+        ("device_updates", ctypes.c_int32),
     ]
 
 

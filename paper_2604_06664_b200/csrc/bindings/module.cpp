@@ -96,6 +96,16 @@ struct ServingHandle {
         }
         return py::bytes(reinterpret_cast<const char*>(rec.data()), rec.size());
     }
+    // reference DeviceContext::exec_update (sim_driver.cpp:365-398): apply a
+    // donor graph (FNDG record bytes) to the exec serving batch's template;
+    // a different topology raises topology-mismatch
+    void exec_update(uint32_t batch, py::bytes donor) {
+        const std::string b = donor;
+        const CapturedGraph g = decode_graph_record(
+            std::span<const uint8_t>(reinterpret_cast<const uint8_t*>(b.data()), b.size()));
+        py::gil_scoped_release nogil;
+        ctx().exec_update(batch, g);
+    }
     uint64_t naive_rebuild_all() {
         py::gil_scoped_release nogil;
         return ctx().naive_rebuild_all();
@@ -126,7 +136,7 @@ SaveOutcome do_save(const WorkloadSpec& spec, const std::string& out, bool emit_
 ServingHandle do_load(const std::string& archive, uint32_t rank, uint32_t world, bool preallocate,
                       int device, bool relocate, unsigned prepare_lanes, bool skip_binary_restore,
                       bool skip_device_init, int64_t base_shift_granules, bool extra_prewindow_alloc,
-                      bool verify_replay, bool share_execs) {
+                      bool verify_replay, bool share_execs, bool device_updates) {
     LoadOptions o;
     o.rank = rank;
     o.world = world;
@@ -136,6 +146,7 @@ ServingHandle do_load(const std::string& archive, uint32_t rank, uint32_t world,
     o.prepare_lanes = prepare_lanes;
     o.verify_replay = verify_replay;
     o.share_execs = share_execs;
+    o.device_updates = device_updates;
     o.faults.skip_binary_restore = skip_binary_restore;
     o.faults.skip_device_init = skip_device_init;
     o.faults.base_shift_granules = base_shift_granules;
@@ -186,6 +197,8 @@ PYBIND11_MODULE(_foundry, m) {
         .def("capture_graph", &ServingHandle::capture_graph, py::arg("batch"),
              "GPU-side SAVE: stream-capture the batch's graph and extract it (FNDG record bytes)")
         .def("naive_rebuild_all", &ServingHandle::naive_rebuild_all)
+        .def("exec_update", &ServingHandle::exec_update, py::arg("batch"), py::arg("donor"),
+             "Apply a donor graph (FNDG record bytes) to the exec of batch's template")
         .def("close", &ServingHandle::close, "Release the rank's graphs, libraries and VA region now")
         .def("__enter__", [](py::object self) { return self; })
         .def("__exit__", [](ServingHandle& h, py::args) { h.close(); });
@@ -202,7 +215,7 @@ PYBIND11_MODULE(_foundry, m) {
           py::arg("prepare_lanes") = 4, py::arg("skip_binary_restore") = false,
           py::arg("skip_device_init") = false, py::arg("base_shift_granules") = 0,
           py::arg("extra_prewindow_alloc") = false, py::arg("verify_replay") = true,
-          py::arg("share_execs") = false);
+          py::arg("share_execs") = false, py::arg("device_updates") = false);
     m.def("pack", [](const std::string& archive) {
         py::gil_scoped_release nogil;
         pack_archive(archive);

@@ -53,6 +53,7 @@ int fdy_load(const char* archive, const fdy_load_options* o, fdy_serving** out) 
             opts.faults.base_shift_granules = o->base_shift_granules;
             opts.faults.extra_prewindow_alloc = o->extra_prewindow_alloc != 0;
             opts.share_execs = o->share_execs != 0;
+            opts.device_updates = o->device_updates != 0;
         }
         *out = new fdy_serving(load(archive, opts));
     });

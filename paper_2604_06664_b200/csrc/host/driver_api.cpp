@@ -83,6 +83,7 @@ void load_all() {
     resolve(g_api.cuFuncGetParamInfo, "cuFuncGetParamInfo", 12040);
     FDY_RESOLVE(cuLaunchKernelEx);
     resolve(g_api.cuFuncLoad, "cuFuncLoad", 12040);
+    FDY_RESOLVE(cuGraphUpload);
 #undef FDY_RESOLVE
 }
 

@@ -5,6 +5,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cstddef>
@@ -19,6 +20,7 @@
 
 #include "foundry/bytes.hpp"
 #include "foundry/capture.hpp"
+#include "../kernels/fdy_kernels.h"
 #include "foundry/parallel.hpp"
 #include "foundry/staging.hpp"
 #include "foundry/template_store.hpp"
@@ -82,7 +84,17 @@ struct ServingContext::Impl {
         std::vector<CUgraphNode> nodes;
         uint32_t applied = kNoMember;  // member index currently in the exec
         uint32_t bound = kNoMember;    // group whose member that is (share_execs: any of the shape)
+        // device_updates: per-node device handles + what each node was built with
+        std::vector<FdyServeNode> serve_nodes;
+        DeviceBuffer d_serve_nodes;
+        std::vector<std::array<uint64_t, 3>> memops;  // memop records currently in the exec
     };
+    // device_updates: host-mapped flags / memop records the serve kernel writes
+    uint8_t* serve_flags = nullptr;
+    uint64_t* serve_records = nullptr;
+    size_t serve_capacity = 0;
+    void ensure_serve_buffers(uint32_t n_nodes);
+    uint64_t serve_on_device(uint32_t gi, uint32_t m);
     std::vector<Group> groups;
     // share_execs: the group whose graph/exec serves group g (itself otherwise)
     std::vector<uint32_t> owner;
@@ -96,6 +108,8 @@ struct ServingContext::Impl {
         try {
             const DriverApi& api = driver();
             if (dev) dev->make_current();
+            if (serve_flags) cudaFreeHost(serve_flags);
+            if (serve_records) cudaFreeHost(serve_records);
             for (auto& g : groups) {
                 if (g.exec) api.cuGraphExecDestroy(g.exec);
                 if (g.graph) api.cuGraphDestroy(g.graph);
@@ -372,6 +386,13 @@ uint64_t ServingContext::Impl::build_graph_for(uint32_t gi, uint32_t m, CUgraph&
                 size_t size;
                 kernel_params(d, blob, K, p, extra, &size);
                 cu_check(api.cuGraphAddKernelNode(&node, graph, nullptr, 0, &p), "cuGraphAddKernelNode");
+                if (opts.device_updates) {
+                    CUkernelNodeAttrValue v{};
+                    v.deviceUpdatableKernelNode.deviceUpdatable = 1;
+                    cu_check(api.cuGraphKernelNodeSetAttribute(node, CU_LAUNCH_ATTRIBUTE_DEVICE_UPDATABLE_KERNEL_NODE,
+                                                               &v),
+                             "cuGraphKernelNodeSetAttribute(device updatable)");
+                }
                 const fdt_node_attrs& a = view->node_attrs(gi, n);
                 const bool non_default = a.cluster[0] != 1 || a.cluster[1] != 1 || a.cluster[2] != 1 ||
                                          a.sched_policy || a.sync_default || a.sync_remote || !a.attr_query;
@@ -461,6 +482,34 @@ void ServingContext::Impl::build_group(uint32_t gi) {
     cu_check(api.cuGraphInstantiate(&grp.exec, grp.graph, 0), "cuGraphInstantiate");
     debug_phase("instantiated group");
     ctx->c_instantiate.fetch_add(1);
+    if (opts.device_updates) {  // device handles of the kernel nodes, what they were built with
+        const uint8_t* img = member_image(m);
+        grp.serve_nodes.assign(G.n_nodes, FdyServeNode{});
+        grp.memops.assign(G.n_nodes, {0, 0, 0});
+        for (uint32_t n = 0; n < G.n_nodes; ++n) {
+            fdt_node d;
+            std::memcpy(&d, img + 48ull * n, sizeof d);
+            FdyServeNode& sn = grp.serve_nodes[n];
+            if (d.type == 0) {
+                CUkernelNodeAttrValue v{};
+                cu_check(api.cuGraphKernelNodeGetAttribute(grp.nodes[n], CU_LAUNCH_ATTRIBUTE_DEVICE_UPDATABLE_KERNEL_NODE,
+                                                           &v),
+                         "cuGraphKernelNodeGetAttribute(device node)");
+                sn.devnode = reinterpret_cast<void*>(v.deviceUpdatableKernelNode.devNode);
+                sn.param_bytes = resolve(d.kernel, n).arg_buffer_size;
+                sn.kernel = d.kernel;
+                std::memcpy(sn.block, d.block, sizeof sn.block);
+                sn.shmem = d.shmem;
+            } else if (d.type == 1 || d.type == 2) {
+                std::memcpy(grp.memops[n].data(), img + 48ull * G.n_nodes + d.blob_off, 24);
+            }
+        }
+        grp.d_serve_nodes = DeviceBuffer(*dev, sizeof(FdyServeNode) * std::max<uint32_t>(G.n_nodes, 1));
+        cuda_check(cudaMemcpy(grp.d_serve_nodes.data(), grp.serve_nodes.data(), sizeof(FdyServeNode) * G.n_nodes,
+                              cudaMemcpyHostToDevice),
+                   "cudaMemcpy(serve table)");
+        cu_check(api.cuGraphUpload(grp.exec, dev->stream()), "cuGraphUpload");
+    }
     const double inst = ms_since(t1);
     if (std::getenv("FOUNDRY_DEBUG"))
         std::fprintf(stderr, "[foundry] group %u: %u nodes %u edges build %.3f ms instantiate %.3f ms\n", gi,
@@ -477,9 +526,86 @@ void ServingContext::Impl::build_group(uint32_t gi) {
 
 // ---------------------------------------------------------------- serve
 
+void ServingContext::Impl::ensure_serve_buffers(uint32_t n_nodes) {
+    if (n_nodes <= serve_capacity) return;
+    if (serve_flags) cudaFreeHost(serve_flags);
+    if (serve_records) cudaFreeHost(serve_records);
+    serve_flags = nullptr;
+    serve_records = nullptr;
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&serve_flags), n_nodes, cudaHostAllocMapped),
+               "cudaHostAlloc(serve flags)");
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&serve_records), 24ull * n_nodes, cudaHostAllocMapped),
+               "cudaHostAlloc(serve records)");
+    serve_capacity = n_nodes;
+}
+
+// device_updates serve: kernel nodes from the GPU, memops (and anything the
+// device cannot change) from the host. Returns the nodes updated.
+uint64_t ServingContext::Impl::serve_on_device(uint32_t gi, uint32_t m) {
+    Group& grp = groups[gi];
+    const fdt_group& G = view->group(gi);
+    const DriverApi& api = driver();
+    dev->make_current();
+    ensure_serve_buffers(G.n_nodes);
+    FdyServeArgs a{};
+    a.nodes = reinterpret_cast<const FdyServeNode*>(grp.d_serve_nodes.data());
+    a.image = d_members.data() + view->member(m).out_off;
+    cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.host_flags), serve_flags, 0),
+               "cudaHostGetDevicePointer");
+    cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.host_records), serve_records, 0),
+               "cudaHostGetDevicePointer");
+    a.n_nodes = G.n_nodes;
+    cuda_check(fdy_launch_serve(&a, dev->stream()), "serve kernel launch");
+    cuda_check(cudaStreamSynchronize(dev->stream()), "cudaStreamSynchronize(serve)");
+    uint64_t touched = 0;
+    bool host_path = false;
+    for (uint32_t n = 0; n < G.n_nodes; ++n) {
+        const uint8_t f = serve_flags[n];
+        if (f == 0) {
+            touched += grp.serve_nodes[n].devnode != nullptr;
+        } else if (f == 1) {
+            std::array<uint64_t, 3> rec;
+            std::memcpy(rec.data(), serve_records + 3ull * n, 24);
+            if (rec == grp.memops[n]) continue;
+            const uint8_t* blob = reinterpret_cast<const uint8_t*>(rec.data());
+            CUgraphNodeType t;
+            cu_check(api.cuGraphNodeGetType(grp.nodes[n], &t), "cuGraphNodeGetType");
+            if (t == CU_GRAPH_NODE_TYPE_MEMCPY) {
+                const CUDA_MEMCPY3D c = memcpy_params(blob);
+                cu_check(api.cuGraphExecMemcpyNodeSetParams(grp.exec, grp.nodes[n], &c, cu_ctx),
+                         "cuGraphExecMemcpyNodeSetParams");
+            } else {
+                const CUDA_MEMSET_NODE_PARAMS sp = memset_params(blob);
+                cu_check(api.cuGraphExecMemsetNodeSetParams(grp.exec, grp.nodes[n], &sp, cu_ctx),
+                         "cuGraphExecMemsetNodeSetParams");
+            }
+            grp.memops[n] = rec;
+            ++touched;
+        } else {
+            host_path = true;
+        }
+    }
+    if (host_path) {  // a change the device cannot make: the whole member from the host
+        grp.applied = kNoMember;
+        return kNoMember;
+    }
+    return touched;
+}
+
 uint64_t ServingContext::Impl::apply_member(uint32_t gi, uint32_t m) {
     Group& grp = exec_of(gi);
     if (grp.applied == m) return 0;
+    if (opts.device_updates && !grp.serve_nodes.empty()) {
+        const uint64_t touched = serve_on_device(gi, m);
+        if (touched != kNoMember) {
+            grp.applied = m;
+            grp.bound = gi;
+            ++lane_acquisitions;
+            ctx->c_update.fetch_add(1);
+            ctx->c_update_touched.fetch_add(touched);
+            return touched;
+        }
+    }
     const DriverApi& api = driver();
     dev->make_current();
     const fdt_group& G = view->group(gi);
@@ -529,6 +655,15 @@ uint64_t ServingContext::Impl::apply_member(uint32_t gi, uint32_t m) {
                 break;
             }
             default: break;
+        }
+    }
+    if (opts.device_updates && !grp.serve_nodes.empty()) {
+        // host updates of device-updatable nodes take effect after an upload
+        cu_check(api.cuGraphUpload(grp.exec, dev->stream()), "cuGraphUpload");
+        for (uint32_t n = 0; n < G.n_nodes; ++n) {
+            fdt_node d;
+            std::memcpy(&d, img + 48ull * n, sizeof d);
+            if (d.type == 1 || d.type == 2) std::memcpy(grp.memops[n].data(), pool + d.blob_off, 24);
         }
     }
     grp.applied = m;
@@ -690,6 +825,9 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     auto& I = *impl;
     I.dev = &device;
     I.opts = opts;
+    require(!(opts.share_execs && opts.device_updates), Errc::invalid_argument,
+            "share_execs and device_updates exclude each other (a shared exec changes functions; "
+            "device-updatable graphs cannot)");
     I.root = archive;
     ArchivePaths paths{archive};
     require(fs::exists(paths.manifest()), Errc::archive_corruption, "no manifest under " + archive.string());
@@ -1224,6 +1362,10 @@ void ServingContext::exec_update(uint32_t batch_in_group, const CapturedGraph& d
             cu_check(api.cuGraphExecMemsetNodeSetParams(grp.exec, grp.nodes[n], &sp, I.cu_ctx),
                      "cuGraphExecMemsetNodeSetParams");
         }
+    }
+    if (I.opts.device_updates && !grp.serve_nodes.empty()) {
+        cu_check(api.cuGraphUpload(grp.exec, I.dev->stream()), "cuGraphUpload");
+        for (auto& r : grp.memops) r = {~0ull, ~0ull, ~0ull};  // unknown: the next serve re-applies memops
     }
     grp.applied = kNoMember;
     grp.bound = gi;

@@ -65,6 +65,12 @@ struct LoadOptions {
     // template (the driver-bound part of LOAD); a serve that crosses templates
     // pays a larger update. Off = the reference's one exec per template.
     bool share_execs = false;
+    // Kernel nodes are built device-updatable: serve() applies a member from
+    // the GPU (kernels/serve.cu: cudaGraphKernelNodeSetParam / SetGridDim
+    // straight from the HBM member images, one thread per node); only memcpy /
+    // memset nodes (and any node whose function, block or shared memory would
+    // change) go through the host. Excludes share_execs.
+    bool device_updates = false;
 };
 
 // Wall/kernel time of each LOAD phase (milliseconds) and the DMA volume.

@@ -32,6 +32,23 @@ struct FdyMaterializeArgs {
     uint32_t n_values;
 };
 
+// Device-side serve (kernels/serve.cu): one entry per template node.
+struct FdyServeNode {
+    void* devnode;          // cudaGraphDeviceNode_t of a device-updatable kernel node (else null)
+    uint32_t param_bytes;   // the entry's argument-buffer size (what the node was built with)
+    uint32_t kernel;        // store kernel index the node was built with
+    uint32_t block[3];
+    uint32_t shmem;
+};
+
+struct FdyServeArgs {
+    const FdyServeNode* nodes;      // device table, n_nodes entries
+    const unsigned char* image;     // member image in HBM (descriptors + pool)
+    uint8_t* host_flags;            // host-mapped: 0 applied on device, 1 memop, 2 host path
+    uint64_t* host_records;         // host-mapped: 3 x u64 per node (memop records)
+    uint32_t n_nodes;
+};
+
 struct FdyCrcBlock {
     uint32_t segment;
     uint32_t length;   // <= kCrcBlockBytes
@@ -49,6 +66,9 @@ cudaError_t fdy_launch_materialize(const FdyMaterializeArgs* args, int grid, cud
 
 // per device: x^(2^k) mod P and the constant-multiplier nibble tables built from them
 cudaError_t fdy_crc64_set_constants(const uint64_t* x2k64);
+
+// Device-side serve: apply a member image to a device-updatable exec (serve.cu).
+cudaError_t fdy_launch_serve(const FdyServeArgs* args, cudaStream_t stream);
 // CRC-64/XZ of n_segments byte ranges already resident in device memory.
 // blocks: host-built table (see fdy_crc_plan) in device memory; partial /
 // lengths scratch: n_blocks entries each; out: n_segments digests (device).

@@ -1,0 +1,56 @@
+// Device-side serve for sm_100a (reference ServingSet::serve -> exec_update,
+// templater.cpp:177-188, sim_driver.cpp:365-398): apply member m's parameters
+// to its template's instantiated graph from the GPU, reading them straight out
+// of the member-image arena the materialize kernel wrote in HBM.
+//
+// The template's kernel nodes are device-updatable
+// (CU_LAUNCH_ATTRIBUTE_DEVICE_UPDATABLE_KERNEL_NODE); one thread per node
+// calls cudaGraphKernelNodeSetParam (the whole argument block) and
+// cudaGraphKernelNodeSetGridDim. A device update cannot change a node's
+// function, block dims or dynamic shared memory, and memcpy / memset nodes
+// have no device-side update: such nodes are flagged (with their 24-byte
+// memop record) in host-mapped memory and the host applies them with
+// cuGraphExec*NodeSetParams. No host copy of the member image is needed.
+//
+// Compiled with -rdc=true and device-linked against libcudadevrt (the device
+// graph-update API lives in the device runtime).
+#include <cstdint>
+
+#include "fdy_kernels.h"
+
+namespace {
+
+constexpr int kServeThreads = 128;
+
+__global__ void __launch_bounds__(kServeThreads)
+fdy_serve_kernel(const FdyServeArgs a) {
+    const uint32_t n = blockIdx.x * kServeThreads + threadIdx.x;
+    if (n >= a.n_nodes) return;
+    const fdt_node d = reinterpret_cast<const fdt_node*>(a.image)[n];
+    const FdyServeNode& s = a.nodes[n];
+    const unsigned char* blob = a.image + 48ull * a.n_nodes + d.blob_off;
+    uint8_t flag = 0;
+    if (d.type == 0 && s.devnode != nullptr && d.kernel == s.kernel && d.block[0] == s.block[0] &&
+        d.block[1] == s.block[1] && d.block[2] == s.block[2] && d.shmem == s.shmem) {
+        const cudaGraphDeviceNode_t node = reinterpret_cast<cudaGraphDeviceNode_t>(s.devnode);
+        if (cudaGraphKernelNodeSetParam(node, 0, blob, s.param_bytes) != cudaSuccess ||
+            cudaGraphKernelNodeSetGridDim(node, dim3(d.grid[0], d.grid[1], d.grid[2])) != cudaSuccess)
+            flag = 2;  // the host re-applies the whole member
+    } else if (d.type == 1 || d.type == 2) {
+        flag = 1;      // memop: host SetParams from the record below
+        const uint64_t* r = reinterpret_cast<const uint64_t*>(blob);
+        uint64_t* out = a.host_records + 3ull * n;
+        out[0] = r[0], out[1] = r[1], out[2] = r[2];
+    } else if (d.type == 0) {
+        flag = 2;      // function / block / shmem changed: host path
+    }
+    a.host_flags[n] = flag;
+}
+
+}  // namespace
+
+extern "C" cudaError_t fdy_launch_serve(const FdyServeArgs* args, cudaStream_t stream) {
+    if (args->n_nodes == 0) return cudaSuccess;
+    fdy_serve_kernel<<<(args->n_nodes + kServeThreads - 1) / kServeThreads, kServeThreads, 0, stream>>>(*args);
+    return cudaGetLastError();
+}

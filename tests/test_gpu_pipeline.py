@@ -236,3 +236,42 @@ def test_shared_execs_serve_every_batch_like_the_oracle(foundry, load, oracle, a
         assert h.replay(b) == want[b], "batch %d" % b
     ok, report = h.fresh_capture_check(h.batches()[-1])
     assert ok, report
+
+
+def test_exec_update_with_a_mismatched_donor_is_a_topology_mismatch(foundry, load, oracle, archives):
+    """Acceptance criterion 7, last case (acceptance.cpp:304-371): updating an
+    exec from a graph of another topology fails with topology-mismatch and
+    leaves serving intact; a same-topology donor is applied."""
+    arch, _ = archives("moe-spmd")
+    h = load(arch)
+    container, _ = oracle.materialize_archive(arch, 0, 1, 0)
+    recs = fndg.records(container)
+    want = expected_traces(oracle, arch)
+    first, last = h.batches()[0], h.batches()[-1]
+    with pytest.raises(foundry.FoundryError, match="topology-mismatch"):
+        h.exec_update(first, recs[last])        # batch 1 and 512 are different templates
+    h.exec_update(last, recs[last - 1])         # same template: applied node by node
+    assert h.replay(last) == want[last]         # serving re-applies the member
+    assert h.replay(first) == want[first]
+
+
+@pytest.mark.parametrize("name,rank,world,relocate", [("llama3-8b", 0, 1, False), ("moe-spmd", 3, 4, True)])
+def test_device_updates_serve_every_batch_like_the_oracle(foundry, load, oracle, archives, name, rank, world,
+                                                          relocate):
+    """LoadOptions.device_updates: kernel nodes are device-updatable and serve()
+    applies each member from the GPU (cudaGraphKernelNodeSetParam/SetGridDim
+    from the HBM member images); memcpy/memset nodes from the host. Every
+    replay's on-device trace records must equal the oracle's, in both sweep
+    directions (every template switch and member change)."""
+    arch, _ = archives(name)
+    base = manifest(arch)["allocator"]["base"]
+    if relocate:
+        load(arch, rank=0, world=world)
+    h = load(arch, rank=rank, world=world, relocate=relocate, device_updates=True)
+    want = expected_traces(oracle, arch, rank, world, h.region_base() - base)
+    for b in h.batches() + h.batches()[::-1]:
+        assert h.replay(b) == want[b], "batch %d" % b
+    ok, report = h.fresh_capture_check(h.batches()[len(h.batches()) // 2])
+    assert ok, report
+    with pytest.raises(foundry.FoundryError, match="exclude each other"):
+        load(arch, share_execs=True, device_updates=True)
