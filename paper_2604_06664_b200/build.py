@@ -8,6 +8,7 @@ snapshot to the GPU box and are what the tests/bench load):
   _foundry<EXT>               pybind11 module mirroring the reference bindings
   trace_body.ptx              device body of the generated trace kernels
   fdy_tool                    CLI: save / pack / load / bench helpers
+  foundry                     the reference's CLI (save/load/inspect/diff/bench)
 
 Kernels compile with -gencode arch=compute_100a,code=sm_100a -lineinfo; there
 is no other architecture and no JIT fallback.
@@ -100,8 +101,9 @@ def _write_ninja() -> Path:
         "rule dlink",
         f"  command = $nvcc {ARCH} -Xcompiler -fPIC -dlink $in -L{CUDA}/lib64 -lcudadevrt -o $out",
         "  description = DLINK $out",
+        # no -lineinfo: the PTX is embedded into SAVE output, which must not depend on paths
         "rule ptx",
-        f"  command = $nvcc -std=c++17 -arch=sm_100a -rdc=true -ptx -O3 -lineinfo -I{CSRC}/include $in -o $out",
+        f"  command = $nvcc -std=c++17 -arch=sm_100a -rdc=true -ptx -O3 -I{CSRC}/include $in -o $out",
         "  description = PTX $in",
         "rule embed",
         f"  command = {sys.executable} {CSRC}/tools/embed_ptx.py $in $out",
@@ -143,10 +145,15 @@ def _write_ninja() -> Path:
     lib = PKG / "libfoundry_b200.so"
     lines.append(f"build {lib}: link {' '.join(objs)}")
     lines.append(f"build {PKG / 'fdy_tool'}: exe {CSRC / 'tools/fdy_tool.cpp'} | {lib}")
+    lines.append(f"build {PKG / 'foundry'}: exe {CSRC / 'tools/foundry_cli.cpp'} | {lib}")
     lines.append(f"build {PKG / ('_foundry' + ext)}: pymod {CSRC / 'bindings/module.cpp'} | {lib}")
     BUILD.mkdir(parents=True, exist_ok=True)
     path = BUILD / "build.ninja"
-    text = "\n".join(lines) + "\n"
+    # in-tree paths relative to the build directory (ninja runs there): the
+    # same build.ninja, depfiles and PTX `.file` lines wherever the tree is
+    # checked out (the GPU box copies it to a scratch path), so a snapshot's
+    # up-to-date objects are not rebuilt and SAVE's cubins stay byte-identical
+    text = ("\n".join(lines) + "\n").replace(str(ROOT), os.path.relpath(ROOT, BUILD))
     if not path.exists() or path.read_text() != text:
         path.write_text(text)
     return path
