@@ -246,3 +246,53 @@ def test_session_layer_load_replay_and_capture(foundry, oracle, archives, api):
                    [(n.type, n.grid, n.block, n.shmem, n.name, n.args, n.mem) for n in ref.nodes]
     finally:
         api.lib.fdy_serving_close(h)
+
+
+# BASELINE.json configs at their full tier-R sizes: the
+# spec, then the (rank, world, delta) cases each config is quoted on.
+FULL_CONFIGS = [
+    ("llama3-8b", [(0, 1, 0x10000)]),                                   # config 1, TP=1
+    ("qwen3-8b", [(0, 1, 0x10000000000)]),                              # config 2, TP=1
+    ("qwen3-30b-a3b", [(0, 1, 0), (1, 2, 0x10000)]),                    # config 3, 1 and 2 GPUs
+    ("llama3-70b", [(3, 4, 0x10000), (7, 8, DELTAS[3])]),              # config 4, TP4 / TP8
+    ("qwen3-235b-a22b", [(0, 8, 0x10000), (5, 8, DELTAS[2])]),         # config 5, TP8 (headline)
+]
+
+
+@pytest.mark.parametrize("name,cases", FULL_CONFIGS, ids=[c[0] for c in FULL_CONFIGS])
+def test_baseline_configs_full_size_bit_exact(foundry, oracle, api, dev, tmp_path, name, cases):
+    """Every BASELINE config at full size through the C-ABI: the GPU-CRC'd
+    archive files equal their manifest digests, and every member graph of
+    every (rank, world, delta) case equals the oracle byte for byte."""
+    from conftest import spec_path
+
+    arch = str(tmp_path / name)
+    foundry.save(foundry.workload_from_text(open(spec_path(name)).read()), arch, b200_artifacts=False)
+    foundry._foundry._pack_store(arch)
+    m = manifest(arch)
+    files = sorted(f for f in m["files"] if f != "templates.fdt") + ["templates.fdt"]
+    parts, ranges, off = [], [], 0
+    for f in files:
+        d = open(os.path.join(arch, f), "rb").read()
+        parts.append(d + b"\0" * ((-len(d)) % 256))
+        ranges.append((off, len(d)))
+        off += len(parts[-1])
+    digests, _ = api.crc64(dev, b"".join(parts), ranges)
+    want_digests = dict(m["files"])
+    for f, dg in zip(files, digests):
+        if f in want_digests:
+            assert dg == want_digests[f], f
+    blob = open(os.path.join(arch, "templates.fdt"), "rb").read()
+    base = m["allocator"]["base"]
+    store = api.store_upload(dev, blob)
+    try:
+        for rank, world, delta in cases:
+            members, _ = api.materialize(dev, store, rank, world, base + delta if delta else 0)
+            try:
+                got = decode(foundry, arch, api.members_download(members))
+            finally:
+                api.lib.fdy_members_free(members)
+            want, _ = oracle.materialize_archive(arch, rank, world, delta)
+            assert got == want, (name, rank, world, hex(delta))
+    finally:
+        api.lib.fdy_store_free(store)

@@ -275,3 +275,17 @@ def test_device_updates_serve_every_batch_like_the_oracle(foundry, load, oracle,
     assert ok, report
     with pytest.raises(foundry.FoundryError, match="exclude each other"):
         load(arch, share_execs=True, device_updates=True)
+
+
+def test_headline_graph_set_replay_verified(foundry, load, oracle, archives):
+    """BASELINE config 5 at full size (qwen3-235b-a22b~ TP8, 512 graphs x 1036
+    nodes): LOAD rank 5 of 8 through the public API, replay batches across
+    every template against the oracle, and one fresh-capture equivalence."""
+    arch, outcome = archives("qwen3-235b-a22b")
+    h = load(arch, rank=5, world=8)
+    assert h.counters()["exec.instantiate_calls"] == outcome.template_count == 12
+    want = expected_traces(oracle, arch, 5, 8)
+    for b in (1, 15, 16, 31, 47, 63, 95, 127, 191, 255, 319, 383, 447, 511, 512):
+        assert h.replay(b) == want[b], "batch %d" % b
+    ok, report = h.fresh_capture_check(300)
+    assert ok, report
