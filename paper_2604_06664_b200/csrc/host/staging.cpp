@@ -8,6 +8,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <future>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -133,12 +134,24 @@ struct StagedArchive::Shared {
     double read_ms = 0;
 };
 
+namespace {
+std::vector<std::string> manifest_files(const Manifest& m) {
+    std::vector<std::string> out;
+    for (const auto& [rel, digest] : m.file_digests) out.push_back(rel);
+    return out;
+}
+}  // namespace
+
 StagedArchive::StagedArchive(Device& dev, const fs::path& root, const Manifest& manifest,
+                             unsigned lanes, StageTimings* t, StagePlan plan)
+    : StagedArchive(dev, root, manifest_files(manifest), lanes, t, std::move(plan)) {}
+
+StagedArchive::StagedArchive(Device& dev, const fs::path& root, const std::vector<std::string>& names,
                              unsigned lanes, StageTimings* t, StagePlan plan)
     : dev_(dev), sh_(std::make_unique<Shared>()) {
     sh_->t0 = Clock::now();
-    for (const auto& [rel, digest] : manifest.file_digests) {
-        (void)digest;
+    dev.make_current();  // may run on a helper thread (materialize_archive)
+    for (const auto& rel : names) {
         std::error_code ec;
         const uint64_t n = fs::file_size(root / rel, ec);
         require(!ec, Errc::archive_corruption, "cannot open " + (root / rel).string());
@@ -388,6 +401,18 @@ void StagedArchive::verify_file(const Manifest& manifest, const std::string& rel
     require(got == manifest.file_digests.at(rel), Errc::archive_corruption, "integrity check failed for " + rel);
 }
 
+uint64_t StagedArchive::digest(const std::string& rel) const {
+    const StagedFile& f = file(rel);
+    wait_ready(f);
+    return digest_of(f);
+}
+
+void StagedArchive::finish(StageTimings* t) {
+    join();
+    if (sh_->error) std::rethrow_exception(sh_->error);
+    if (t) t->read_ms = std::max(t->read_ms, sh_->read_ms);
+}
+
 void StagedArchive::verify(const Manifest& manifest, StageTimings* t) {
     const auto t0 = Clock::now();
     join();
@@ -415,6 +440,112 @@ uint64_t StagedArchive::size(const std::string& rel) const { return file(rel).le
 
 // ------------------------------------------------------------------ materialize
 
+namespace {
+
+// Launches the fused kernel over the store and queues the D2H of the result.
+struct Launched {
+    DeviceBuffer out;
+    MaterializeTiming mt;
+    Clock::time_point t1, t2;
+    uint64_t bytes = 0;
+};
+
+void launch_from_store(Device& dev, const Manifest& manifest, DeviceStore& store, uint32_t rank, uint32_t world,
+                       uint64_t new_base, void* host_out, uint64_t cap, Launched& L) {
+    const fdt_header& H = store.header;
+    require(H.source_graphs_crc == manifest.file_digests.at("graphs.bin") &&
+                H.source_patch_crc == manifest.file_digests.at("patch.bin"),
+            Errc::archive_corruption, "template store was packed from a different graphs.bin/patch.bin");
+    if (H.n_rank_ops > 0)
+        require(manifest.comm_real_hash != 0, Errc::unresolved_kernel,
+                "archive carries comm patches but no real comm binary");
+    if (host_out)
+        require(cap >= H.members_image_bytes, Errc::invalid_argument,
+                "output buffer holds " + std::to_string(cap) + " bytes, the member images need " +
+                    std::to_string(H.members_image_bytes));
+    L.out = DeviceBuffer(dev, std::max<uint64_t>(H.members_image_bytes, 16));
+    MaterializeRequest req;
+    req.rank = rank;
+    req.world = world;
+    req.new_base = new_base;
+    L.mt.gate = false;  // part of a pipeline: no stream hold for the events
+    launch_materialize(dev, store, req, L.out.data(), &L.mt);
+    L.t2 = Clock::now();
+    if (host_out) {
+        dev.make_current();
+        cuda_check(cudaMemcpyAsync(host_out, L.out.data(), H.members_image_bytes, cudaMemcpyDeviceToHost,
+                                   dev.stream()),
+                   "cudaMemcpyAsync(member images D2H)");
+    }
+    L.bytes = H.members_image_bytes;
+}
+
+}  // namespace
+
+static uint64_t materialize_archive_early(Device& dev, const fs::path& root, const Manifest& manifest,
+                                          std::unique_ptr<StagedArchive> early,
+                                          std::future<std::unique_ptr<StagedArchive>> rest_future, StageTimings& st,
+                                          Clock::time_point t_all, uint32_t rank, uint32_t world, uint64_t new_base,
+                                          void* host_out, uint64_t cap, ArchiveMaterializeTimings* t) {
+    std::unique_ptr<StagedArchive> rest;
+    auto others = [&]() -> StagedArchive& {
+        if (!rest) rest = rest_future.get();  // rethrows a listing / staging error
+        return *rest;
+    };
+    // reference verify_archive_integrity (pipeline.cpp:411-417): the first
+    // failing (or missing) file in manifest order names the error
+    auto verify_all = [&] {
+        for (const auto& [rel, digest] : manifest.file_digests) {
+            StagedArchive& s = early->has(rel) ? *early : others();
+            require(s.has(rel), Errc::archive_corruption, "cannot open " + (root / rel).string());
+            require(s.digest(rel) == digest, Errc::archive_corruption, "integrity check failed for " + rel);
+        }
+    };
+    Launched L;
+    try {
+        const auto ts = Clock::now();
+        if (early->digest("templates.fdt") != manifest.file_digests.at("templates.fdt")) verify_all();
+        st.integrity_ms += ms_since(ts);
+        trace_point("store verified", t_all);
+    } catch (const Error&) {
+        rethrow_in_step("archive integrity");
+    }
+    L.t1 = Clock::now();
+    const auto host = early->host("templates.fdt");
+    const StoreView view(host);
+    early->order_after("templates.fdt", dev.stream());
+    DeviceStore store = adopt_store(dev, early->device("templates.fdt"), host.size(), view.header());
+    launch_from_store(dev, manifest, store, rank, world, new_base, host_out, cap, L);
+    trace_point("kernel launched", t_all);
+    try {
+        const auto tv = Clock::now();
+        early->finish(&st);  // the kernel and the D2H are queued: the lanes hash the rest meanwhile
+        others().finish(&st);
+        verify_all();  // every file, while the D2H runs
+        st.integrity_ms += ms_since(tv);
+        trace_point("all files verified", t_all);
+    } catch (const Error&) {
+        cudaStreamSynchronize(dev.stream());
+        rethrow_in_step("archive integrity");
+    }
+    cuda_check(cudaStreamSynchronize(dev.stream()), "cudaStreamSynchronize");
+    if (t) {
+        t->read_ms = st.read_ms;
+        t->integrity_ms = st.integrity_ms;
+        t->crc_kernel_ms = st.crc_kernel_ms;
+        t->materialize_ms = std::chrono::duration<double, std::milli>(L.t2 - L.t1).count();
+        t->kernel_ms = L.mt.kernel_ms;
+        t->d2h_ms = ms_since(L.t2);
+        t->h2d_bytes = st.h2d_bytes;
+        t->d2h_bytes = host_out ? L.bytes : 0;
+        t->member_bytes = L.bytes;
+        t->graphs = store.header.n_members;
+        t->nodes = store.header.total_nodes;
+        t->total_ms = ms_since(t_all);
+    }
+    return L.bytes;
+}
+
 uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, uint32_t world,
                              uint64_t new_base, unsigned lanes, void* host_out, uint64_t cap,
                              ArchiveMaterializeTimings* t) {
@@ -422,11 +553,61 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
     require(world >= 1 && rank < world, Errc::invalid_argument,
             "rank " + std::to_string(rank) + " is outside world size " + std::to_string(world));
     ArchivePaths paths{root};
+    StageTimings st;
+    // The store and graphs.bin (the largest file, hashed only) start streaming
+    // before the manifest is parsed: the store -> kernel -> D2H chain and the
+    // host hashing both begin at t = 0. Their digests are checked once the
+    // manifest is known, in manifest order with every other file.
+    // The store (to HBM, then kernel, then D2H) and every other archive file
+    // (hashed on the host) start streaming before the manifest is parsed; the
+    // digests are checked once it is known, in manifest order.
+    std::unique_ptr<StagedArchive> early;
+    std::future<std::unique_ptr<StagedArchive>> rest;
+    {
+        std::error_code e1;
+        if (fs::is_regular_file(paths.template_store(), e1)) {
+            StagePlan p;
+            p.device = {"templates.fdt"};
+            try {
+                early = std::make_unique<StagedArchive>(dev, root, std::vector<std::string>{"templates.fdt"},
+                                                        std::max(1u, std::min(lanes, 4u)), &st, p);
+                // the rest: every other regular file under the archive directory
+                // (extra files are hashed for nothing; missing ones are reported
+                // against the manifest), listed and staged on a helper thread
+                const unsigned rest_lanes = std::max(1u, lanes > 4 ? lanes - 4 : lanes);
+                rest = std::async(std::launch::async, [&dev, root, rest_lanes] {
+                    std::vector<std::string> files;
+                    const std::string prefix = root.string() + "/";
+                    std::error_code ec;
+                    for (auto it = fs::recursive_directory_iterator(root, ec);
+                         !ec && it != fs::recursive_directory_iterator(); it.increment(ec)) {
+                        if (!it->is_regular_file(ec)) continue;
+                        const std::string full = it->path().string();
+                        std::string rel = full.compare(0, prefix.size(), prefix) == 0 ? full.substr(prefix.size()) : full;
+                        if (rel != "manifest" && rel != "templates.fdt") files.push_back(std::move(rel));
+                    }
+                    return std::make_unique<StagedArchive>(dev, root, files, rest_lanes, nullptr, StagePlan{});
+                });
+            } catch (const Error&) {
+                early.reset();  // the regular path reports it in manifest order
+            }
+        }
+    }
+    trace_point("early staging started", t_all);
     require(fs::exists(paths.manifest()), Errc::archive_corruption, "no manifest under " + root.string());
     const auto mb = slurp(paths.manifest());
     const Manifest manifest = parse_manifest(std::string(mb.begin(), mb.end()));
     trace_point("manifest parsed", t_all);
-    StageTimings st;
+    if (early && manifest.file_digests.count("templates.fdt"))
+        return materialize_archive_early(dev, root, manifest, std::move(early), std::move(rest), st, t_all, rank,
+                                         world, new_base, host_out, cap, t);
+    if (rest.valid()) {
+        try {
+            rest.get();
+        } catch (...) {
+        }
+    }
+    early.reset();
     std::unique_ptr<StagedArchive> staged;
     // the store (or, for a reference-written archive, the files it is packed
     // from) streams in first and is verified on its own; materialization and

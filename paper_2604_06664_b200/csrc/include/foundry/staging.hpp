@@ -97,6 +97,10 @@ class StagedArchive {
 public:
     StagedArchive(Device& dev, const std::filesystem::path& root, const Manifest& manifest,
                   unsigned lanes, StageTimings* timings, StagePlan plan);
+    // The same for an explicit file list (no manifest needed to start reading:
+    // materialize_archive streams the store before the manifest is parsed).
+    StagedArchive(Device& dev, const std::filesystem::path& root, const std::vector<std::string>& files,
+                  unsigned lanes, StageTimings* timings, StagePlan plan);
     ~StagedArchive();
     StagedArchive(const StagedArchive&) = delete;
     StagedArchive& operator=(const StagedArchive&) = delete;
@@ -112,6 +116,10 @@ public:
     void order_after(const std::string& rel, cudaStream_t stream);
 
     bool has(const std::string& rel) const { return files_.count(rel) != 0; }
+    // CRC-64 of one staged file (waits for its pieces / GPU fold).
+    uint64_t digest(const std::string& rel) const;
+    // Joins the reader lanes (rethrows a read error); adds the read time.
+    void finish(StageTimings* timings);
     // Host bytes of a device or host-kept file (waits for its reads).
     std::span<const uint8_t> host(const std::string& rel) const;
     const unsigned char* device(const std::string& rel) const;  // device files
