@@ -4,8 +4,8 @@
 // of the member-image arena the materialize kernel wrote in HBM.
 //
 // The template's kernel nodes are device-updatable
-// (CU_LAUNCH_ATTRIBUTE_DEVICE_UPDATABLE_KERNEL_NODE); one thread per node
-// calls cudaGraphKernelNodeSetParam (the whole argument block) and
+// (CU_LAUNCH_ATTRIBUTE_DEVICE_UPDATABLE_KERNEL_NODE); one warp per node
+// calls cudaGraphKernelNodeSetParam (16-byte slices of the argument block) and
 // cudaGraphKernelNodeSetGridDim. A device update cannot change a node's
 // function, block dims or dynamic shared memory, and memcpy / memset nodes
 // have no device-side update: such nodes are flagged (with their 24-byte
@@ -20,11 +20,16 @@
 
 namespace {
 
-constexpr int kServeThreads = 128;
+constexpr int kServeThreads = 128;  // 4 nodes per CTA: one warp per node
 
+// One warp per node: lane l writes argument bytes [16 l, 16 l + 16) with its
+// own cudaGraphKernelNodeSetParam (disjoint ranges of the node's parameter
+// block), lane 0 the grid; a single thread per node was latency-bound on the
+// device runtime's byte copy (20 us for 1036 nodes).
 __global__ void __launch_bounds__(kServeThreads)
 fdy_serve_kernel(const FdyServeArgs a) {
-    const uint32_t n = blockIdx.x * kServeThreads + threadIdx.x;
+    const uint32_t n = blockIdx.x * (kServeThreads / 32) + (threadIdx.x >> 5);
+    const uint32_t lane = threadIdx.x & 31;
     if (n >= a.n_nodes) return;
     const fdt_node d = reinterpret_cast<const fdt_node*>(a.image)[n];
     const FdyServeNode& s = a.nodes[n];
@@ -33,24 +38,25 @@ fdy_serve_kernel(const FdyServeArgs a) {
     if (d.type == 0 && s.devnode != nullptr && d.kernel == s.kernel && d.block[0] == s.block[0] &&
         d.block[1] == s.block[1] && d.block[2] == s.block[2] && d.shmem == s.shmem) {
         const cudaGraphDeviceNode_t node = reinterpret_cast<cudaGraphDeviceNode_t>(s.devnode);
-        if (cudaGraphKernelNodeSetParam(node, 0, blob, s.param_bytes) != cudaSuccess ||
-            cudaGraphKernelNodeSetGridDim(node, dim3(d.grid[0], d.grid[1], d.grid[2])) != cudaSuccess)
-            flag = 2;  // the host re-applies the whole member
+        bool ok = true;
+        for (uint32_t off = 16 * lane; off < s.param_bytes; off += 16 * 32)
+            ok &= cudaGraphKernelNodeSetParam(node, off, blob + off, min(16u, s.param_bytes - off)) == cudaSuccess;
+        if (lane == 0) ok &= cudaGraphKernelNodeSetGridDim(node, dim3(d.grid[0], d.grid[1], d.grid[2])) == cudaSuccess;
+        if (!__all_sync(0xFFFFFFFFu, ok)) flag = 2;  // the host re-applies the whole member
     } else if (d.type == 1 || d.type == 2) {
-        flag = 1;      // memop: host SetParams from the record below
-        const uint64_t* r = reinterpret_cast<const uint64_t*>(blob);
-        uint64_t* out = a.host_records + 3ull * n;
-        out[0] = r[0], out[1] = r[1], out[2] = r[2];
+        flag = 1;  // memop: host SetParams from the record below
+        if (lane < 3) a.host_records[3ull * n + lane] = reinterpret_cast<const uint64_t*>(blob)[lane];
     } else if (d.type == 0) {
-        flag = 2;      // function / block / shmem changed: host path
+        flag = 2;  // function / block / shmem changed: host path
     }
-    a.host_flags[n] = flag;
+    if (lane == 0) a.host_flags[n] = flag;
 }
 
 }  // namespace
 
 extern "C" cudaError_t fdy_launch_serve(const FdyServeArgs* args, cudaStream_t stream) {
     if (args->n_nodes == 0) return cudaSuccess;
-    fdy_serve_kernel<<<(args->n_nodes + kServeThreads - 1) / kServeThreads, kServeThreads, 0, stream>>>(*args);
+    const uint32_t per_cta = kServeThreads / 32;
+    fdy_serve_kernel<<<(args->n_nodes + per_cta - 1) / per_cta, kServeThreads, 0, stream>>>(*args);
     return cudaGetLastError();
 }
