@@ -158,11 +158,12 @@ def reference_load_ms(archive: str, rank: int, world: int, lanes: int, reps: int
     return json.loads(r.stdout) if r.returncode == 0 else None
 
 
-def reference_materialize_ms(archive: str, rank: int, world: int, lanes: int, reps: int) -> dict | None:
+def reference_materialize_ms(archive: str, rank: int, world: int, lanes: int, reps: int,
+                             warmup: int = 1) -> dict | None:
     if not os.path.exists(REF_TOOL):
         return None
     r = subprocess.run([REF_TOOL, "time-materialize", archive, str(rank), str(world), str(lanes),
-                        str(reps)], capture_output=True, text=True)
+                        str(reps), str(warmup)], capture_output=True, text=True)
     return json.loads(r.stdout) if r.returncode == 0 else None
 
 
@@ -180,16 +181,41 @@ def oracle_port_ms(archive: str, rank: int, world: int, lanes: int, reps: int) -
             "lanes": lanes}
 
 
+def reference_archive(workload: str) -> str | None:
+    """The workload's archive written by the reference itself (ref_tool save,
+    foundry::save pipeline.cpp:249-405), so the reference arm runs none of
+    this build's code. Byte-identical to this build's SAVE (tests/test_save.py)."""
+    if not os.path.exists(REF_TOOL):
+        return None
+    import paper_2604_06664_b200 as foundry  # only for the bundled spec path
+
+    spec = foundry.workload_path(workload)
+    root = os.path.join(tempfile.gettempdir(), "foundry_refarm_" + workload)
+    stamp = hashlib.sha1(open(REF_TOOL, "rb").read() + open(spec, "rb").read()).hexdigest()
+    done = os.path.join(root, "READY")
+    out = os.path.join(root, "archive")
+    if not (os.path.exists(done) and open(done).read() == stamp):
+        shutil.rmtree(root, ignore_errors=True)
+        os.makedirs(root)
+        r = subprocess.run([REF_TOOL, "save", spec, out], capture_output=True, text=True)
+        if r.returncode != 0:
+            return None
+        open(done, "w").write(stamp)
+    return out
+
+
 def run_reference(args, grank, gworld):
     """--impl reference: the reference's own CPU load() of the same archive."""
     if grank != 0:
         return
     lanes = os.cpu_count() or 1
-    _, plain = prepare_archives(args.workload, 0, lambda: None)
+    plain = reference_archive(args.workload)
+    if plain is None:  # no reference build: this build's byte-identical SAVE
+        _, plain = prepare_archives(args.workload, 0, lambda: None)
     wrank = 0
     # the reference's CPU implementation of the path: verify_archive_integrity +
     # PrepareFn over every member (oracle/_ref/ref_tool time-materialize)
-    res = reference_materialize_ms(plain, wrank, TP_WORLD, lanes, args.steps)
+    res = reference_materialize_ms(plain, wrank, TP_WORLD, lanes, args.steps, args.warmup)
     kind = "reference"
     if res is None:
         res = oracle_port_ms(plain, wrank, TP_WORLD, lanes, args.steps)
@@ -199,14 +225,16 @@ def run_reference(args, grank, gworld):
     line = {
         "impl": "reference",
         "metric": "graph-set materialization ms (cold start); relocation GB/s vs HBM peak",
-        "value": value, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps, "warmup": 1,
+        "value": value, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup if kind == "reference" else 1,
         "ms_per_step": value, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "u8", "data": "synthetic",
         "config": {"workload": args.workload + "~ tier-R TP8 (rank 0 of 8)", "graphs": 512,
                    "parallelism": "replicas"},
         "cpu_baseline": {"value": value, "unit": "ms", "cores": lanes, "kind": kind,
-                         "sample": "reference verify_archive_integrity + PrepareFn over all 512 "
-                                   "members, %d reps after 1 warm-up" % args.steps},
+                         "sample": "reference verify_archive_integrity + PrepareFn over all "
+                                   "member graphs (archive written by the reference's own save), %d reps "
+                                   "after %d warm-up" % (args.steps, args.warmup if kind == "reference" else 1)},
         "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "full_load": {"value": full["mean_ms"] if full else None, "unit": "ms",
                       "api": "reference foundry::load (pipeline.cpp:447-557)"},

@@ -155,7 +155,7 @@ static int cmd_time_load(int argc, char** argv) {
     return 0;
 }
 
-// time-materialize <archive> <rank> <world> <lanes> <reps>
+// time-materialize <archive> <rank> <world> <lanes> <reps> [warmup=1]
 //   the reference's share of LOAD that the GPU path replaces: the integrity
 //   CRC of every manifest-listed file, single-threaded as in
 //   verify_archive_integrity (pipeline.cpp:411-417), then the PrepareFn of
@@ -168,9 +168,10 @@ static int cmd_time_materialize(int argc, char** argv) {
     const uint32_t world = static_cast<uint32_t>(std::stoul(argv[4]));
     const unsigned lanes = static_cast<unsigned>(std::stoul(argv[5]));
     const int reps = std::stoi(argv[6]);
+    const int warmup = argc > 7 ? std::max(0, std::stoi(argv[7])) : 1;
     using clock = std::chrono::steady_clock;
     double best = 1e300, total = 0.0, crc_best = 1e300;
-    for (int i = 0; i < reps + 1; ++i) {
+    for (int i = 0; i < reps + warmup; ++i) {
         const auto t0 = clock::now();
         ArchivePaths paths{archive};
         const auto mb = read_file(paths.manifest());
@@ -200,7 +201,7 @@ static int cmd_time_materialize(int argc, char** argv) {
         const auto t2 = clock::now();
         const double ms = std::chrono::duration<double, std::milli>(t2 - t0).count();
         const double crc_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
-        if (i > 0) {
+        if (i >= warmup) {
             best = std::min(best, ms);
             crc_best = std::min(crc_best, crc_ms);
             total += ms;
