@@ -234,6 +234,14 @@ int main(int argc, char** argv) {
     const std::string cmd = argv[1];
     try {
         if (cmd == "save") return cmd_save(argc, argv);
+        if (cmd == "pack" && argc == 4) {  // reference pack_archive (pipeline.cpp:747-773)
+            pack_archive(argv[2], argv[3]);
+            return 0;
+        }
+        if (cmd == "unpack" && argc == 4) {  // reference unpack_archive (pipeline.cpp:775-817)
+            unpack_archive(argv[2], argv[3]);
+            return 0;
+        }
         if (cmd == "prepare") return cmd_prepare(argc, argv);
         if (cmd == "replay") return cmd_replay(argc, argv);
         if (cmd == "time-load") return cmd_time_load(argc, argv);

@@ -26,10 +26,12 @@ try:
         inspect_text,
         load,
         pack,
+        pack_archive,
         preset,
         preset_names,
         save,
         spec_text,
+        unpack_archive,
         workload_from_text,
     )
 except ImportError as exc:  # pragma: no cover - exercised only on a broken build
@@ -60,6 +62,8 @@ __all__ = [
     "inspect_text",
     "load",
     "pack",
+    "pack_archive",
+    "unpack_archive",
     "preset",
     "preset_names",
     "save",

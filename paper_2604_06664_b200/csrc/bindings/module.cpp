@@ -220,6 +220,14 @@ PYBIND11_MODULE(_foundry, m) {
         py::gil_scoped_release nogil;
         pack_archive(archive);
     }, py::arg("archive"));
+    m.def("pack_archive", [](const std::string& dir, const std::string& file) {
+        py::gil_scoped_release nogil;
+        pack_archive_file(dir, file);
+    }, py::arg("archive"), py::arg("file"), "Single-file FNDA archive (reference pack_archive)");
+    m.def("unpack_archive", [](const std::string& file, const std::string& dir) {
+        py::gil_scoped_release nogil;
+        unpack_archive_file(file, dir);
+    }, py::arg("file"), py::arg("archive"), "Inverse of pack_archive (reference unpack_archive)");
     m.def("inspect_text", [](const std::string& a) { return inspect_text(a); }, py::arg("archive"));
     m.def("inspect_graph_json", [](const std::string& a, uint32_t b) { return inspect_graph_json(a, b); },
           py::arg("archive"), py::arg("batch"));

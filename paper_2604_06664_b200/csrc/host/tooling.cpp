@@ -267,4 +267,63 @@ std::map<std::string, double> bench(const WorkloadSpec& spec, const std::string&
     return r;
 }
 
+// ---------------------------------------------------------------- FNDA
+
+void pack_archive_file(const fs::path& dir, const fs::path& file) {
+    require(fs::exists(ArchivePaths{dir}.manifest()), Errc::archive_corruption, "no manifest under " + dir.string());
+    std::map<std::string, std::vector<uint8_t>> files;  // sorted by relative path
+    for (const auto& e : fs::recursive_directory_iterator(dir))
+        if (e.is_regular_file()) files[fs::relative(e.path(), dir).generic_string()] = slurp(e.path());
+    Sink w;
+    w.raw("FNDA", 4);
+    w.u16(1);
+    w.u32(static_cast<uint32_t>(files.size()));
+    std::vector<size_t> at;
+    for (const auto& [rel, bytes] : files) {
+        w.str(rel);
+        at.push_back(w.size());
+        w.u64(0);  // offset: known once the table is complete
+        w.u64(bytes.size());
+        w.u64(crc64(bytes.data(), bytes.size()));
+    }
+    size_t k = 0;
+    for (const auto& [rel, bytes] : files) {
+        w.poke<uint64_t>(at[k++], w.size());
+        w.raw(bytes);
+    }
+    spit(file, w.bytes());
+}
+
+void unpack_archive_file(const fs::path& file, const fs::path& dir) {
+    const auto bytes = slurp(file);
+    Cursor r(bytes, Errc::archive_corruption);
+    r.magic("FNDA");
+    const uint16_t version = r.u16();
+    require(version == 1, Errc::archive_corruption, "unsupported packed archive version " + std::to_string(version));
+    struct Entry {
+        std::string rel;
+        uint64_t offset, length, checksum;
+    };
+    std::vector<Entry> entries(r.u32());
+    for (Entry& e : entries) {
+        e.rel = r.str();
+        e.offset = r.u64();
+        e.length = r.u64();
+        e.checksum = r.u64();
+        require(e.offset <= bytes.size() && e.length <= bytes.size() - e.offset, Errc::archive_corruption,
+                e.rel + " overruns the packed archive");
+        require(!e.rel.empty() && e.rel.find("..") == std::string::npos && e.rel.front() != '/',
+                Errc::archive_corruption, "packed entry path escapes the archive");
+    }
+    fs::create_directories(dir);
+    for (const Entry& e : entries) {
+        const std::span<const uint8_t> blob(bytes.data() + e.offset, e.length);
+        require(crc64(blob.data(), blob.size()) == e.checksum, Errc::archive_corruption,
+                "integrity check failed for " + e.rel);
+        const fs::path target = dir / e.rel;
+        fs::create_directories(target.parent_path());
+        spit(target, blob);
+    }
+}
+
 }  // namespace foundry

@@ -27,4 +27,10 @@ std::map<std::string, uint64_t> save_counters(const WorkloadSpec& spec);
 // update_served_fraction, construction_calls, update_calls, capture_calls.
 std::map<std::string, double> bench(const WorkloadSpec& spec, const std::string& mode);
 
+// Single-file archive "FNDA" (reference pack_archive / unpack_archive,
+// pipeline.cpp:740-817): u16 version 1, u32 count, then per file (sorted by
+// relative path) {str path, u64 offset, u64 length, u64 crc64}, then the bytes.
+void pack_archive_file(const std::filesystem::path& dir, const std::filesystem::path& file);
+void unpack_archive_file(const std::filesystem::path& file, const std::filesystem::path& dir);
+
 }  // namespace foundry

@@ -136,3 +136,29 @@ def test_inspect_matches_reference_text(foundry, ref_tool, tmp_path):
     ref_inspect, ref_json = json.loads(out)
     assert foundry.inspect_text(ours) == ref_inspect
     assert foundry.inspect_graph_json(ours, 37) == ref_json
+
+
+def test_pack_archive_matches_the_reference_and_round_trips(foundry, ref_tool, tmp_path):
+    """Single-file FNDA archive (reference pack_archive / unpack_archive,
+    pipeline.cpp:740-817): byte-identical to the reference's, and unpacking
+    restores the directory; corruption and path escapes are archive errors
+    (test_pipeline.cpp:360-385)."""
+    import filecmp
+    import subprocess
+
+    arch = tmp_path / "arch"
+    foundry.save(foundry.preset("micro"), str(arch))
+    foundry.pack_archive(str(arch), str(tmp_path / "ours.fnda"))
+    subprocess.run([ref_tool, "pack", str(arch), str(tmp_path / "ref.fnda")], check=True)
+    assert (tmp_path / "ours.fnda").read_bytes() == (tmp_path / "ref.fnda").read_bytes()
+    foundry.unpack_archive(str(tmp_path / "ours.fnda"), str(tmp_path / "back"))
+    cmp = filecmp.dircmp(arch, tmp_path / "back")
+    assert not cmp.left_only and not cmp.right_only and not cmp.diff_files
+    assert foundry.diff_archives(str(arch), str(tmp_path / "back"))[0]
+    data = bytearray((tmp_path / "ours.fnda").read_bytes())
+    data[-5] ^= 1
+    (tmp_path / "bad.fnda").write_bytes(bytes(data))
+    with pytest.raises(foundry.FoundryError, match="integrity check failed"):
+        foundry.unpack_archive(str(tmp_path / "bad.fnda"), str(tmp_path / "bad"))
+    with pytest.raises(foundry.FoundryError, match="bad magic"):
+        foundry.unpack_archive(str(arch / "graphs.bin"), str(tmp_path / "bad2"))
