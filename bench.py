@@ -314,7 +314,7 @@ def main():
         # fdy_prepare_archive = read every file, DMA to HBM, GPU CRC of every
         # file vs the manifest, fused kernel over every member, copy all member
         # images back to (pinned) host memory.
-        lanes = os.cpu_count() or 4
+        lanes = max(1, (os.cpu_count() or 4) // gworld)  # the host cores are shared by the ranks
         host_out = api.host_alloc(dev, hdr["members_image_bytes"])
         for _ in range(2):  # warm-up: page cache + pinned staging pool
             api.prepare_archive(dev, archive, wrank, TP_WORLD, base + delta, lanes, host_out,
