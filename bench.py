@@ -309,6 +309,16 @@ def main():
         barrier()
         kernel_ms = statistics.mean(times)
         kernel_ms_max = reduce_max(kernel_ms)
+        # the dominant kernel alone (roofline): the same materialization with the
+        # relocation grid and the member pass as separate launches, timed apart
+        split = []
+        for _ in range(args.steps):
+            flush_l2()
+            split.append(api.materialize_split(dev, store, wrank, TP_WORLD, base + delta, members))
+        torch.cuda.synchronize()
+        barrier()
+        reloc_ms = reduce_max(statistics.mean(r for r, _ in split))
+        member_ms = reduce_max(statistics.mean(m for _, m in split))
 
         # ------- end to end through the C-ABI: archive files -> host result -------
         # fdy_prepare_archive = read every file, DMA to HBM, GPU CRC of every
@@ -384,7 +394,8 @@ def main():
         return
 
     peak, peak_src = hbm_peak()
-    achieved = alg["total"] / (kernel_ms * 1e-3) / 1e9
+    achieved = alg["member_pass"] / (member_ms * 1e-3) / 1e9  # the dominant kernel
+    launch_gbps = alg["total"] / (kernel_ms_max * 1e-3) / 1e9     # the whole materialization
     prof = os.path.join(ROOT, "profiles", "materialize_ncu_summary.json")
     traffic = None
     if os.path.exists(prof):
@@ -438,13 +449,18 @@ def main():
         },
         "graphs_per_s": gworld * graphs / (kernel_ms_max * 1e-3),
         "nodes_per_s": gworld * hdr["total_nodes"] / (kernel_ms_max * 1e-3),
-        "relocation_gbps": achieved,
+        "relocation_gbps": launch_gbps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes": alg["total"],
-                     "kernel": "fdy_materialize launch = fdy_relocate_templates_kernel (3.4 MB "
-                               "of templates) + fdy_materialize_kernel (member pass), CUDA events "
-                               "around both"},
+                     "algorithmic_bytes": alg["member_pass"],
+                     "kernel": "fdy_materialize_kernel (member pass: K2 diff + K1 relocated lanes + "
+                               "K3 rank patch), CUDA events around it alone, L2 flushed",
+                     "kernel_ms": member_ms,
+                     "relocation_prepass": {"kernel": "fdy_relocate_templates_kernel (3.4 MB of "
+                                                      "templates, once per launch)", "ms": reloc_ms},
+                     "whole_launch": {"ms": kernel_ms_max, "algorithmic_bytes": alg["total"],
+                                      "achieved": launch_gbps, "frac": launch_gbps / peak,
+                                      "note": "both grids under programmatic dependent launch = value"}},
         "e2e": {"value": e2e_ms, "unit": "ms",
                 "h2d_bytes_per_step": int(ep["h2d_bytes"]),
                 "d2h_bytes_per_step": int(ep["d2h_bytes"]),

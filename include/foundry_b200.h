@@ -116,6 +116,11 @@ int fdy_materialize(fdy_device* dev, const fdy_store* store, const fdy_materiali
 int fdy_materialize_into(fdy_device* dev, const fdy_store* store,
                          const fdy_materialize_desc* desc, fdy_members* members,
                          float* kernel_ms);
+/* Measurement variant of fdy_materialize_into: the template relocation grid and
+ * the member pass run as separate launches and are timed separately (CUDA
+ * events on the device stream; blocks). Same output. */
+int fdy_materialize_timed_split(fdy_device* dev, const fdy_store* store, const fdy_materialize_desc* desc,
+                                fdy_members* members, float* reloc_ms, float* member_ms);
 size_t fdy_members_bytes(const fdy_members* members);
 int fdy_members_download(fdy_members* members, void* host_dst, size_t offset, size_t bytes);
 void fdy_members_free(fdy_members* members);

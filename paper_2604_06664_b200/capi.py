@@ -101,6 +101,8 @@ class CApi:
         L.fdy_members_bytes.restype = ctypes.c_size_t
         L.fdy_members_download.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t]
         L.fdy_members_free.argtypes = [P]
+        L.fdy_materialize_timed_split.argtypes = [P, P, ctypes.POINTER(MaterializeDesc), P,
+                                                  ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
         L.fdy_crc64_segments.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t,
                                          ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
                                          ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint64),
@@ -187,6 +189,14 @@ class CApi:
                                                      ctypes.byref(ms)))
         return members, ms.value
 
+    def materialize_split(self, dev, store, rank: int, world: int, new_base: int, members):
+        """(relocation ms, member-pass ms): the two grids timed apart."""
+        desc = MaterializeDesc(rank, world, new_base, None, 0, 0)
+        r, m = ctypes.c_float(), ctypes.c_float()
+        self.check(self.lib.fdy_materialize_timed_split(dev, store, ctypes.byref(desc), members,
+                                                        ctypes.byref(r), ctypes.byref(m)))
+        return r.value, m.value
+
     def prepare_archive(self, dev, archive: str, rank: int, world: int, new_base: int = 0,
                         lanes: int = 0, host_out=None, cap: int = 0) -> dict:
         """The materialization path in one C-ABI call (fdy_prepare_archive)."""
@@ -245,9 +255,11 @@ def store_header(blob: bytes) -> dict:
 def algorithmic_bytes(h: dict) -> dict:
     """Compulsory HBM traffic of one fused K2+K1+K3 launch:
     templates + chunk meta read once, every diff / rank op / tile read once,
-    every member image written once."""
+    every member image written once. `member_pass` is the fdy_materialize_kernel
+    grid's own share (it reads the relocated templates, not the chunk meta)."""
     s = h["sec"]
     read = (s["timages"][1] + s["cmeta"][1] + s["didx"][1] + s["ddata"][1]
             + s["rops"][1] + s["tiles"][1])
     write = h["members_image_bytes"]
-    return {"read": read, "write": write, "total": read + write}
+    return {"read": read, "write": write, "total": read + write,
+            "member_pass": read - s["cmeta"][1] + write}

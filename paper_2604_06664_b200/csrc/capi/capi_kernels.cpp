@@ -180,6 +180,25 @@ int fdy_materialize_into(fdy_device* dev, const fdy_store* store, const fdy_mate
     });
 }
 
+int fdy_materialize_timed_split(fdy_device* dev, const fdy_store* store, const fdy_materialize_desc* desc,
+                                fdy_members* m, float* reloc_ms, float* member_ms) {
+    return fdy_guard([&] {
+        require(dev && store && desc && m, Errc::invalid_argument, "fdy_materialize_timed_split: null argument");
+        require(store->owner == dev, Errc::invalid_argument, "fdy_materialize: store lives on another device");
+        require(m->out.size() >= store->store.header.members_image_bytes, Errc::invalid_argument,
+                "fdy_materialize_timed_split: arena too small for this store");
+        MaterializeRequest req;
+        req.rank = desc->rank;
+        req.world = desc->world;
+        req.new_base = desc->new_base;
+        MaterializeTiming t;
+        t.split = true;
+        launch_materialize(*dev->dev, store->store, req, m->out.data(), &t, desc->grid, nullptr);
+        if (reloc_ms) *reloc_ms = t.reloc_ms;
+        if (member_ms) *member_ms = t.member_ms;
+    });
+}
+
 size_t fdy_members_bytes(const fdy_members* m) { return m ? m->out.size() : 0; }
 
 int fdy_members_download(fdy_members* m, void* host_dst, size_t offset, size_t bytes) {

@@ -232,11 +232,22 @@ void launch_materialize(Device& dev, const DeviceStore& store, const Materialize
         if (timing->gate) cuda_check(fdy_launch_gate(dev.stream(), 50000), "gate kernel launch");
         cuda_check(cudaEventRecord(e0, dev.stream()), "cudaEventRecord");
     }
-    cuda_check(fdy_launch_materialize(&a, grid, dev.stream()), "materialize kernel launch");
+    cudaEvent_t em = nullptr;
+    if (timing && timing->split) {
+        cuda_check(cudaEventCreate(&em), "cudaEventCreate");
+        cuda_check(fdy_launch_materialize_split(&a, grid, dev.stream(), em), "materialize kernel launch");
+    } else {
+        cuda_check(fdy_launch_materialize(&a, grid, dev.stream()), "materialize kernel launch");
+    }
     if (timing) {
         cuda_check(cudaEventRecord(e1, dev.stream()), "cudaEventRecord");
         cuda_check(cudaEventSynchronize(e1), "cudaEventSynchronize");
         cuda_check(cudaEventElapsedTime(&timing->kernel_ms, e0, e1), "cudaEventElapsedTime");
+        if (em) {
+            cuda_check(cudaEventElapsedTime(&timing->reloc_ms, e0, em), "cudaEventElapsedTime");
+            cuda_check(cudaEventElapsedTime(&timing->member_ms, em, e1), "cudaEventElapsedTime");
+            cudaEventDestroy(em);
+        }
         timing->grid = grid;
         timing->blocks_per_sm = per_sm;
         cudaEventDestroy(e0);

@@ -116,7 +116,10 @@ struct MaterializeRequest {
 
 struct MaterializeTiming {
     bool gate = true;       // hold the stream while submitting (events = device time only)
+    bool split = false;     // time the relocation prepass and the member pass separately
     float kernel_ms = 0.f;  // CUDA-event time of the fused kernel, launching stream
+    float reloc_ms = 0.f;   // split: relocation grid (delta != 0)
+    float member_ms = 0.f;  // split: member pass alone
     int grid = 0;
     int blocks_per_sm = 0;
 };

@@ -60,6 +60,10 @@ size_t fdy_materialize_smem_bytes();
 // A one-thread kernel that holds `stream` for `ns` ns (see materialize.cu).
 cudaError_t fdy_launch_gate(cudaStream_t stream, uint64_t ns);
 cudaError_t fdy_materialize_occupancy(int* blocks_per_sm);
+// Measurement variant: relocation grid, then `between` recorded, then the member
+// grid as an ordinary launch (events time the member pass alone).
+cudaError_t fdy_launch_materialize_split(const FdyMaterializeArgs* args, int grid, cudaStream_t stream,
+                                         cudaEvent_t between);
 // delta == 0: one grid. Otherwise the template relocation grid, then the
 // member grid under programmatic dependent launch (both on `stream`).
 cudaError_t fdy_launch_materialize(const FdyMaterializeArgs* args, int grid, cudaStream_t stream);

@@ -379,6 +379,25 @@ extern "C" cudaError_t fdy_launch_materialize(const FdyMaterializeArgs* args, in
     return cudaLaunchKernelEx(&cfg, fdy_materialize_kernel, *args);
 }
 
+// The two grids of a relocating launch as separate stream operations (no
+// programmatic overlap), so events can time the member pass on its own.
+extern "C" cudaError_t fdy_launch_materialize_split(const FdyMaterializeArgs* args, int grid, cudaStream_t stream,
+                                                    cudaEvent_t between) {
+    if (args->n_tiles == 0) return cudaSuccess;
+    cudaError_t e = set_smem_attribute_once();
+    if (e != cudaSuccess) return e;
+    if (args->delta != 0ull) {
+        if (args->rtimg == nullptr) return cudaErrorInvalidValue;
+        const uint64_t n = args->timage_bytes / 16;
+        const int rgrid = int(std::min<uint64_t>((n + kRelocThreads - 1) / kRelocThreads, 4096));
+        if (rgrid > 0) fdy_relocate_templates_kernel<<<rgrid, kRelocThreads, 0, stream>>>(*args);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (between && (e = cudaEventRecord(between, stream)) != cudaSuccess) return e;
+    fdy_materialize_kernel<<<grid, kThreads, sizeof(Smem), stream>>>(*args);  // griddepcontrol.wait: no-op
+    return cudaGetLastError();
+}
+
 extern "C" cudaError_t fdy_materialize_occupancy(int* blocks_per_sm) {
     const cudaError_t e = set_smem_attribute_once();
     if (e != cudaSuccess) return e;
