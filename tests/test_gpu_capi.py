@@ -255,7 +255,7 @@ FULL_CONFIGS = [
     ("qwen3-8b", [(0, 1, 0x10000000000)]),                              # config 2, TP=1
     ("qwen3-30b-a3b", [(0, 1, 0), (1, 2, 0x10000)]),                    # config 3, 1 and 2 GPUs
     ("llama3-70b", [(3, 4, 0x10000), (7, 8, DELTAS[3])]),              # config 4, TP4 / TP8
-    ("qwen3-235b-a22b", [(0, 8, 0x10000), (5, 8, DELTAS[2])]),         # config 5, TP8 (headline)
+    ("qwen3-235b-a22b", [(r, 8, [0x10000, DELTAS[2], DELTAS[3], 0][r % 4]) for r in range(8)]),  # config 5: all 8 TP ranks
 ]
 
 
