@@ -436,12 +436,6 @@ uint64_t ServingContext::Impl::build_graph_for(uint32_t gi, uint32_t m, CUgraph&
         ++calls;
     }
     const auto e = view->edges(gi);
-    static const int edge_mode = std::getenv("FOUNDRY_EDGE_MODE") ? std::atoi(std::getenv("FOUNDRY_EDGE_MODE")) : 0;
-    if (edge_mode == 1) {  // EXPERIMENT: chain
-        for (uint32_t n = 1; n < G.n_nodes; ++n) cu_check(api.cuGraphAddDependencies(graph, &nodes[n-1], &nodes[n], 1), "dep");
-        return calls;
-    }
-    if (edge_mode == 2) return calls;  // EXPERIMENT: no edges
     if (G.n_edges) {
         std::vector<CUgraphNode> from(G.n_edges), to(G.n_edges);
         for (uint32_t i = 0; i < G.n_edges; ++i) {
