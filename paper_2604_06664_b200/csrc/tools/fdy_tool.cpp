@@ -273,13 +273,20 @@ static int cmd_instbench(int argc, char** argv) {
         api.cuGraphExecDestroy(x);
         api.cuGraphDestroy(g);
     };
-    // parallel instantiation of independent graphs from T host threads
-    for (int threads : {1, 2, 4, 8}) {
-        const int graphs = 8;
+    // parallel instantiation of 12 graphs with the archive's template-0
+    // topology (one dummy kernel per node) from T host threads; repeated so
+    // the first (cold) round does not bias the comparison
+    const auto tstore = slurp(paths.root / "templates.fdt");
+    const StoreView tview(tstore);
+    const fdt_group& TG = tview.group(0);
+    const auto TE = tview.edges(0);
+    for (int threads : {1, 2, 4, 1, 2, 4, 8}) {
+        const int graphs = 12;
         std::vector<CUgraph> gs(graphs);
         for (int k = 0; k < graphs; ++k) {
             cu_check(api.cuGraphCreate(&gs[k], 0), "create");
-            for (int i = 0; i < 1000; ++i) {
+            std::vector<CUgraphNode> ns(TG.n_nodes);
+            for (uint32_t i = 0; i < TG.n_nodes; ++i) {
                 const auto* K = ks[0];
                 size_t size = K->arg_buffer_size;
                 void* extra[5] = {CU_LAUNCH_PARAM_BUFFER_POINTER, blob.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &size,
@@ -291,9 +298,14 @@ static int cmd_instbench(int argc, char** argv) {
                 p.blockDimX = 128;
                 p.blockDimY = p.blockDimZ = 1;
                 p.extra = extra;
-                CUgraphNode n;
-                cu_check(api.cuGraphAddKernelNode(&n, gs[k], nullptr, 0, &p), "add");
+                cu_check(api.cuGraphAddKernelNode(&ns[i], gs[k], nullptr, 0, &p), "add");
             }
+            std::vector<CUgraphNode> from(TG.n_edges), to(TG.n_edges);
+            for (uint32_t i = 0; i < TG.n_edges; ++i) {
+                from[i] = ns[TE[2 * i]];
+                to[i] = ns[TE[2 * i + 1]];
+            }
+            cu_check(api.cuGraphAddDependencies(gs[k], from.data(), to.data(), TG.n_edges), "deps");
         }
         std::vector<CUgraphExec> xs(graphs);
         const auto t0 = std::chrono::steady_clock::now();
@@ -311,7 +323,8 @@ static int cmd_instbench(int argc, char** argv) {
             });
         for (auto& t : pool) t.join();
         const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-        std::printf("instantiate %d x 1000-node independent graphs with %d threads: %.3f ms\n", graphs, threads, ms);
+        std::printf("instantiate %d template-0-shaped graphs (%u nodes) with %d threads: %.3f ms\n", graphs,
+                    TG.n_nodes, threads, ms);
         for (int k = 0; k < graphs; ++k) {
             api.cuGraphExecDestroy(xs[k]);
             api.cuGraphDestroy(gs[k]);
