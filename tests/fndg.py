@@ -147,3 +147,38 @@ def trace_text(g: Graph, hidden, crc64) -> str:
         s += " args=%016x addrs=%s" % (digest, ",".join("0x%016x" % a for a in addrs))
         lines.append(s + "\n")
     return "".join(lines)
+
+
+# ---- writers (tier-S fixtures: model-shaped graphs the tier-R generator cannot express)
+
+def encode_record(g: Graph) -> bytes:
+    """Inverse of decode_record (graph_model.cpp:205-218 layout)."""
+    out = [struct.pack("<III", g.label, len(g.nodes), len(g.edges))]
+    for n in g.nodes:
+        out.append(bytes([n.type]))
+        if n.type == 0:
+            name = n.name.encode()
+            out.append(n.attrs)
+            out.append(struct.pack("<7I", *n.grid, *n.block, n.shmem))
+            out.append(struct.pack("<QI", n.hash, len(name)) + name)
+            out.append(n.fattrs)
+            out.append(struct.pack("<I", len(n.args)) + n.args)
+        elif n.type in (1, 2):
+            out.append(struct.pack("<3Q", *n.mem))
+    for e in g.edges:
+        out.append(struct.pack("<II", *e))
+    return b"".join(out)
+
+
+def write_container(graph_list, version: int, crc64) -> tuple[bytes, list]:
+    """FNDG container (graph_model.cpp:244-269): header, 28-byte locators
+    {u32 label, u64 offset, u64 length, u64 crc64(record)}, records.
+    Returns (bytes, locators)."""
+    recs = [encode_record(g) for g in graph_list]
+    at = 10 + 28 * len(recs)
+    locs = []
+    for g, r in zip(graph_list, recs):
+        locs.append((g.label, at, len(r), crc64(r)))
+        at += len(r)
+    head = b"FNDG" + struct.pack("<HI", version, len(recs))
+    return head + b"".join(struct.pack("<IQQQ", *l) for l in locs) + b"".join(recs), locs

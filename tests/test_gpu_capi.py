@@ -296,3 +296,26 @@ def test_baseline_configs_full_size_bit_exact(foundry, oracle, api, dev, tmp_pat
             assert got == want, (name, rank, world, hex(delta))
     finally:
         api.lib.fdy_store_free(store)
+
+
+@pytest.mark.parametrize("rank,world,delta", [(0, 1, 0), (3, 8, 0x10000), (5, 8, DELTAS[3])])
+def test_tier_s_graphs_on_the_gpu(foundry, oracle, archives, api, dev, tmp_path, rank, world, delta):
+    """Tier-S fixtures (tests/tier_s.py: 1720-byte argument blocks, unaligned
+    pointers, ragged sizes, member-varying grids) through the fused kernel."""
+    import tier_s
+    src, _ = archives("moe-spmd")
+    arch = tier_s.make_tier_s(src, str(tmp_path / "s"), oracle.crc64)
+    foundry._foundry._pack_store(arch)
+    blob = open(os.path.join(arch, "templates.fdt"), "rb").read()
+    base = manifest(arch)["allocator"]["base"]
+    store = api.store_upload(dev, blob)
+    try:
+        members, _ = api.materialize(dev, store, rank, world, base + delta if delta else 0)
+        try:
+            got = decode(foundry, arch, api.members_download(members))
+        finally:
+            api.lib.fdy_members_free(members)
+    finally:
+        api.lib.fdy_store_free(store)
+    want, _ = oracle.materialize_archive(arch, rank, world, delta)
+    assert got == want

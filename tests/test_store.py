@@ -98,3 +98,22 @@ def test_crc64_host_matches_the_oracle_and_combines(foundry, oracle):
         assert foundry._foundry._crc64(a) == oracle.crc64(a)
         combined = foundry._foundry._crc64_combine(oracle.crc64(a), oracle.crc64(b), len(b))
         assert combined == oracle.crc64(a + b)
+
+
+@pytest.fixture(scope="module")
+def tier_s_archive(foundry, oracle, archives, tmp_path_factory):
+    import tier_s
+    src, _ = archives("moe-spmd")
+    dst = str(tmp_path_factory.mktemp("tier_s") / "moe-s")
+    tier_s.make_tier_s(src, dst, oracle.crc64)
+    foundry._foundry._pack_store(dst)
+    return dst
+
+
+@pytest.mark.parametrize("rank,world,delta", [(0, 1, 0), (1, 4, 0x10000), (7, 8, 0x10000000000)])
+def test_tier_s_store_expansion_equals_oracle(foundry, oracle, tier_s_archive, rank, world, delta):
+    """Model-shaped graphs beyond tier R (1720-byte argument blocks with
+    pointers at aligned and unaligned offsets, ragged sizes, grid dims that vary
+    inside a template): pack + kernel emulation == oracle."""
+    want, _ = oracle.materialize_archive(tier_s_archive, rank, world, delta)
+    assert emulate(foundry, tier_s_archive, rank, world, delta) == want
