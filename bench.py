@@ -490,7 +490,9 @@ def main():
         "serve_sweep": serve_ms or None,
         "cpu_baseline": cpu,
         "clocks": clocks,
-        "gpu_launches": args.steps * (2 if delta else 1),  # relocation grid + member grid
+        # per timed step: the gate kernel that holds the stream while the launches are
+        # submitted (its hold ends before the start event), the relocation grid, the member grid
+        "gpu_launches": args.steps * (3 if delta else 2),
         "fanout": {"mode": args.fanout if gworld > 1 else "none", "ms": fanout_ms,
                    "store_bytes": len(blob)},
     }
