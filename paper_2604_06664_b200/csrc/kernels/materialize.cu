@@ -42,14 +42,18 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kDiffRegs = 2;    // diff entries per thread held in registers
+#ifndef FDY_STAGES
+#define FDY_STAGES 2
+#endif
+constexpr uint32_t kStages = FDY_STAGES;  // template/member tile buffers per CTA
 constexpr int kOpSlots = 256;   // rank ops per tile staged in shared memory
 constexpr int kRelocThreads = 256;
 static_assert(FDT_TILE_CHUNKS % kThreads == 0, "tile must split evenly across the CTA");
 
 struct __align__(128) Smem {
-    uint4 buf[2][FDT_TILE_CHUNKS];      // 2 x 16 KiB template/member tile stages
+    uint4 buf[kStages][FDT_TILE_CHUNKS];  // kStages x 16 KiB template/member tile stages
     fdt_rank_op ops[kOpSlots];          // rank ops of the tile being processed (4 KiB)
-    unsigned long long bar[2];          // mbarriers, one per stage
+    unsigned long long bar[kStages];    // mbarriers, one per stage
 };
 
 // Per-thread operands of one tile, loaded one iteration ahead.
@@ -102,8 +106,10 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
+// All but the newest kStages-2 bulk stores have finished reading shared memory
+// (the stage about to be refilled was stored kStages-1 tiles ago).
 __device__ __forceinline__ void bulk_wait_reads() {
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStages - 2) : "memory");
 }
 
 __device__ __forceinline__ void bulk_wait_all() {
@@ -244,8 +250,7 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
     const uint32_t G = gridDim.x;
 
     if (tid == 0) {
-        mbar_init(&s.bar[0], 1);
-        mbar_init(&s.bar[1], 1);
+        for (uint32_t i = 0; i < kStages; ++i) mbar_init(&s.bar[i], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -267,10 +272,11 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
     for (; t < a.n_tiles; t += G) {
         const bool has_next = t + G < a.n_tiles;
         // stage s^1 <- tile t+G: its descriptor is already in registers
+        const uint32_t nstage = stage + 1 == kStages ? 0 : stage + 1;
         if (tid == 0 && has_next) {
-            bulk_wait_reads();  // the previous store out of stage s^1 has drained
-            mbar_expect_tx(&s.bar[stage ^ 1], Tn.nchunks * 16u);
-            bulk_load(s.buf[stage ^ 1], a.tsrc + Tn.src_off, Tn.nchunks * 16u, &s.bar[stage ^ 1]);
+            bulk_wait_reads();  // the store that last used stage `nstage` has drained
+            mbar_expect_tx(&s.bar[nstage], Tn.nchunks * 16u);
+            bulk_load(s.buf[nstage], a.tsrc + Tn.src_off, Tn.nchunks * 16u, &s.bar[nstage]);
         }
         const fdt_tile Tnn = load_tile(a, t + 2 * G);  // consumed next iteration
         uint4* buf = s.buf[stage];
@@ -310,7 +316,7 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
         if (has_next) prefetch_tile(a, Tn, s, cur, tid);
         T = Tn;
         Tn = Tnn;
-        stage ^= 1u;
+        stage = nstage;
     }
     if (tid == 0) bulk_wait_all();
 }
