@@ -343,13 +343,13 @@ def main():
         # ------- full LOAD through the Python API (adds driver-bound work) -------
         load_times, breakdowns, trace = [], [], ""
         if not args.skip_load:
-            h = foundry.load(archive, rank=wrank, world=TP_WORLD)  # warm-up (driver, page cache)
+            h = foundry.load(archive, rank=wrank, world=TP_WORLD, prepare_lanes=lanes)  # warm-up (driver, page cache)
             h.replay(1)
             h.close()
         for _ in range(0 if args.skip_load else args.load_steps):
             barrier()
             t0 = time.perf_counter()
-            h = foundry.load(archive, rank=wrank, world=TP_WORLD)
+            h = foundry.load(archive, rank=wrank, world=TP_WORLD, prepare_lanes=lanes)
             trace = h.replay(1)  # D2H of the verified device trace of batch 1
             load_times.append((time.perf_counter() - t0) * 1e3)
             breakdowns.append(h.timings())
@@ -360,7 +360,7 @@ def main():
         for _ in range(0 if args.skip_load else args.load_steps):
             barrier()
             t0 = time.perf_counter()
-            h = foundry.load(archive, rank=wrank, world=TP_WORLD, share_execs=True)
+            h = foundry.load(archive, rank=wrank, world=TP_WORLD, share_execs=True, prepare_lanes=lanes)
             trace_s = h.replay(1)
             shared_times.append((time.perf_counter() - t0) * 1e3)
             shared_bd.append(dict(h.timings(), instantiate_calls=h.counters()["exec.instantiate_calls"]))
@@ -371,7 +371,7 @@ def main():
         serve_ms = {}
         if not args.skip_load:
             for mode in ("per_template", "shared_execs", "device_updates"):
-                h = foundry.load(archive, rank=wrank, world=TP_WORLD, share_execs=mode == "shared_execs",
+                h = foundry.load(archive, rank=wrank, world=TP_WORLD, prepare_lanes=lanes, share_execs=mode == "shared_execs",
                                  device_updates=mode == "device_updates")
                 bs = h.batches()
                 t0 = time.perf_counter()
@@ -471,7 +471,7 @@ def main():
                 # stream: no separate kernel time, see profiles/ for the launch list)
                 "breakdown": {k: v for k, v in ep.items() if k.endswith("_ms") and k != "crc_kernel_ms"}},
         "full_load": {"value": load_ms, "unit": "ms", "steps": args.load_steps,
-                      "api": "paper_2604_06664_b200.load(archive, rank, world).replay(1)",
+                      "api": "paper_2604_06664_b200.load(archive, rank, world, prepare_lanes=<host cores per rank>).replay(1)",
                       "driver_bound_ms": driver_bound,
                       "driver_bound": "cuLibraryLoadData x catalog + cuGraphAdd*/cuGraphInstantiate x templates",
                       "excluding_driver_bound_ms": (load_ms - driver_bound) if load_ms else None,
