@@ -28,7 +28,16 @@ struct SaveOutcome {
     uint32_t total_graphs = 0;
     uint32_t template_count = 0;
     double update_served_fraction = 0.0;
+    // (sequence, size, address, length, window) per allocation, SAVE's capture-time layout
+    std::vector<std::tuple<uint64_t, uint64_t, uint64_t, uint64_t, int>> allocation_records;
 };
+
+std::vector<std::tuple<uint64_t, uint64_t, uint64_t, uint64_t, int>> records_tuples(
+    const std::vector<AllocationRecord>& rs) {
+    std::vector<std::tuple<uint64_t, uint64_t, uint64_t, uint64_t, int>> out;
+    for (const auto& r : rs) out.emplace_back(r.sequence, r.size, r.address, r.length, static_cast<int>(r.window));
+    return out;
+}
 
 struct ServingHandle {
     explicit ServingHandle(ServingContext&& s) : sc(std::make_unique<ServingContext>(std::move(s))) {}
@@ -130,6 +139,7 @@ SaveOutcome do_save(const WorkloadSpec& spec, const std::string& out, bool emit_
     s.total_graphs = r.manifest.grouping.total_graphs;
     s.template_count = r.manifest.grouping.template_count;
     s.update_served_fraction = r.manifest.grouping.update_served_fraction();
+    s.allocation_records = records_tuples(r.allocation_records);
     return s;
 }
 
@@ -182,11 +192,15 @@ PYBIND11_MODULE(_foundry, m) {
         .def_readonly("counters", &SaveOutcome::counters)
         .def_readonly("total_graphs", &SaveOutcome::total_graphs)
         .def_readonly("template_count", &SaveOutcome::template_count)
-        .def_readonly("update_served_fraction", &SaveOutcome::update_served_fraction);
+        .def_readonly("update_served_fraction", &SaveOutcome::update_served_fraction)
+        .def_readonly("allocation_records", &SaveOutcome::allocation_records);
 
     py::class_<ServingHandle>(m, "ServingHandle")
         .def("replay", &ServingHandle::replay, py::arg("batch"), py::call_guard<py::gil_scoped_release>())
         .def("batches", &ServingHandle::batches)
+        .def("allocation_records",
+             [](ServingHandle& h) { return records_tuples(h.ctx().allocation_records()); },
+             "(sequence, size, address, length, window) per allocation of the rank's region")
         .def("counters", &ServingHandle::counters)
         .def("template_count", &ServingHandle::template_count)
         .def("timings", &ServingHandle::timings)

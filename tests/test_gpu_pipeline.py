@@ -289,3 +289,15 @@ def test_headline_graph_set_replay_verified(foundry, load, oracle, archives):
         assert h.replay(b) == want[b], "batch %d" % b
     ok, report = h.fresh_capture_check(300)
     assert ok, report
+
+
+@pytest.mark.parametrize("name", ["micro", "dense-small", "moe-spmd"])
+def test_layout_determinism_with_and_without_preallocation(foundry, load, archives, name):
+    """Acceptance criterion 2 (acceptance.cpp:143-161): LOAD reproduces SAVE's
+    allocation addresses, with the one-shot preallocation and without it."""
+    arch, outcome = archives(name)
+    assert outcome.allocation_records
+    for pre in (True, False):
+        h = load(arch, preallocate=pre)
+        assert h.allocation_records() == outcome.allocation_records, "preallocate=%s" % pre
+        h.close()
