@@ -301,3 +301,22 @@ def test_layout_determinism_with_and_without_preallocation(foundry, load, archiv
         h = load(arch, preallocate=pre)
         assert h.allocation_records() == outcome.allocation_records, "preallocate=%s" % pre
         h.close()
+
+
+def test_construction_reduction_on_dense_small(foundry, load, archives):
+    """Acceptance criterion 4 (acceptance.cpp:182-220) on real graphs: dense-small
+    has 20 templates; templated construction (graph mutation + instantiate)
+    times 512 stays within the naive rebuild times K+1, and with the
+    per-member updates of serving every batch the ratio is <= 0.10."""
+    arch, outcome = archives("dense-small")
+    assert outcome.template_count == 20
+    h = load(arch)
+    for b in h.batches():
+        h.serve(b)
+    c = h.counters()
+    templated = (c["graph.add_node_calls"] + c["graph.add_edge_calls"] + c["graph.set_attr_calls"]
+                 + c["exec.instantiate_calls"])
+    updates = c["exec.update_calls"]
+    naive = h.naive_rebuild_all()
+    assert templated * 512 <= naive * (outcome.template_count + 1)
+    assert (templated + updates) / naive <= 0.10
