@@ -320,3 +320,14 @@ def test_construction_reduction_on_dense_small(foundry, load, archives):
     naive = h.naive_rebuild_all()
     assert templated * 512 <= naive * (outcome.template_count + 1)
     assert (templated + updates) / naive <= 0.10
+
+
+@pytest.mark.parametrize("name", ["micro", "dense-small"])
+def test_replay_equivalence_at_world_four(foundry, load, oracle, archives, name):
+    """Acceptance criterion 1 (acceptance.cpp:108-141) at W=4: every batch of
+    rank 3 replays exactly the oracle's trace."""
+    arch, _ = archives(name)
+    h = load(arch, rank=3, world=4)
+    want = expected_traces(oracle, arch, 3, 4)
+    for b in h.batches():
+        assert h.replay(b) == want[b], "batch %d" % b
