@@ -204,6 +204,35 @@ def reference_archive(workload: str) -> str | None:
     return out
 
 
+def cold_process_load(args, local: int) -> dict:
+    """Wall clock of a fresh process from exec to every template servable:
+    `foundry load --archive <headline> --rank 0 --world 8` (CUDA context
+    creation + LOAD), per-template execs and share_execs, next to a fresh
+    process that only creates the CUDA context (`fdy_tool cuda-init`)."""
+    archive, _ = prepare_archives(args.workload, 0, lambda: None)
+    pkg = os.path.join(ROOT, "paper_2604_06664_b200")
+    runs = {"cuda_init": [os.path.join(pkg, "fdy_tool"), "cuda-init", str(local)]}
+    base = [os.path.join(pkg, "foundry"), "load", "--archive", archive, "--rank", "0", "--world",
+            str(TP_WORLD), "--device", str(local)]
+    runs["per_template"] = base
+    runs["share_execs"] = base + ["--share-execs"]
+    # one untimed fresh process first: the box's very first context creation after
+    # idle (driver / GPU wake-up) is not part of any load
+    subprocess.run(runs["cuda_init"], capture_output=True)
+    out = {}
+    for name, cmd in runs.items():
+        walls = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            walls.append((time.perf_counter() - t0) * 1e3)
+            if r.returncode != 0:
+                walls = []
+                break
+        out[name] = statistics.mean(walls) if walls else None
+    return out
+
+
 def run_reference(args, grank, gworld):
     """--impl reference: the reference's own CPU load() of the same archive."""
     if grank != 0:
@@ -261,6 +290,9 @@ def main():
     shared = os.environ.get("FOUNDRY_BENCH_SHARED_GPU") == "1"
     if shared:
         local = 0
+    # cold start as the paper measures it (N=1, before this process touches CUDA,
+    # so no other context shares the GPU): fresh `foundry load` processes
+    cold = cold_process_load(args, local) if gworld == 1 and not args.skip_load else {}
     torch.cuda.set_device(local)
     group = RankGroup(grank, gworld, local)
     group.init("gloo" if shared else "nccl")
@@ -488,6 +520,14 @@ def main():
                             "cuGraphAdd*/cuGraphInstantiate per graph shape",
             "breakdown": {k: v for k, v in sbd.items() if k.endswith("_ms") and k != "crc_kernel_ms"}},
         "serve_sweep": serve_ms or None,
+        "cold_process_load": None if not cold else {
+            "unit": "ms", "per_template": cold.get("per_template"), "share_execs": cold.get("share_execs"),
+            "cuda_init_only": cold.get("cuda_init"),
+            "what": "wall clock of `foundry load --archive <headline> --rank r --world 8` in a fresh "
+                    "process: CUDA context creation + LOAD to every template servable (the paper's "
+                    "cold start); cuda_init_only = a fresh process that only opens the device "
+                    "(CUDA context creation). The "
+                    "reference arm's simulated LOAD creates no CUDA context"},
         "cpu_baseline": cpu,
         "clocks": clocks,
         # per timed step: the gate kernel that holds the stream while the launches are

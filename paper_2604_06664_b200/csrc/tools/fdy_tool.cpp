@@ -508,6 +508,12 @@ int main(int argc, char** argv) {
         if (cmd == "save") return cmd_save(argc, argv);
         if (cmd == "load") return cmd_load(argc, argv);
         if (cmd == "instbench") return cmd_instbench(argc, argv);
+        if (cmd == "cuda-init") {  // fresh-process floor: create the device context, nothing else
+            fdy_device* d = nullptr;
+            if (fdy_device_open(argc > 2 ? std::atoi(argv[2]) : 0, &d)) return 1;
+            fdy_device_close(d);
+            return 0;
+        }
         if (cmd == "restorebench") return cmd_restorebench(argc, argv);
         if (cmd == "naive") {
             ServingContext sc = load(argv[2], LoadOptions{});
