@@ -406,8 +406,10 @@ def main():
                 h = foundry.load(archive, rank=wrank, world=TP_WORLD, prepare_lanes=lanes, share_execs=mode == "shared_execs",
                                  device_updates=mode == "device_updates")
                 bs = h.batches()
+                torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 touched = sum(h.serve(b) for b in bs)
+                torch.cuda.synchronize()  # device_updates queues its serve kernels: count them
                 ms = (time.perf_counter() - t0) * 1e3
                 ok = h.replay(bs[-1]) == h.replay(bs[-1])  # the trace is device-verified
                 serve_ms[mode] = {"ms": ms, "us_per_serve": ms * 1e3 / len(bs), "batches": len(bs),

@@ -88,12 +88,14 @@ struct ServingContext::Impl {
         std::vector<FdyServeNode> serve_nodes;
         DeviceBuffer d_serve_nodes;
         std::vector<std::array<uint64_t, 3>> memops;  // memop records currently in the exec
+        std::vector<uint32_t> memop_nodes;            // node index of memop slot k
+        uint32_t n_kernel_nodes = 0;
     };
-    // device_updates: host-mapped flags / memop records the serve kernel writes
-    uint8_t* serve_flags = nullptr;
-    uint64_t* serve_records = nullptr;
-    size_t serve_capacity = 0;
-    void ensure_serve_buffers(uint32_t n_nodes);
+    // device_updates serve plan (computed once at LOAD by fdy_serve_plan_kernel)
+    std::vector<uint8_t> serve_member_host;           // per member: host path needed
+    std::vector<uint32_t> serve_memop_base;           // per member: first slot in serve_plan_records
+    std::vector<std::array<uint64_t, 3>> serve_plan_records;
+    void build_serve_plan();
     uint64_t serve_on_device(uint32_t gi, uint32_t m);
     std::vector<Group> groups;
     // share_execs: the group whose graph/exec serves group g (itself otherwise)
@@ -108,8 +110,6 @@ struct ServingContext::Impl {
         try {
             const DriverApi& api = driver();
             if (dev) dev->make_current();
-            if (serve_flags) cudaFreeHost(serve_flags);
-            if (serve_records) cudaFreeHost(serve_records);
             for (auto& g : groups) {
                 if (g.exec) api.cuGraphExecDestroy(g.exec);
                 if (g.graph) api.cuGraphDestroy(g.graph);
@@ -496,7 +496,11 @@ void ServingContext::Impl::build_group(uint32_t gi) {
                 sn.shmem = d.shmem;
             } else if (d.type == 1 || d.type == 2) {
                 std::memcpy(grp.memops[n].data(), img + 48ull * G.n_nodes + d.blob_off, 24);
+                sn.memop_slot = static_cast<int32_t>(grp.memop_nodes.size());
+                grp.memop_nodes.push_back(n);
             }
+            if (d.type != 1 && d.type != 2) sn.memop_slot = -1;
+            if (d.type == 0) ++grp.n_kernel_nodes;
         }
         grp.d_serve_nodes = DeviceBuffer(*dev, sizeof(FdyServeNode) * std::max<uint32_t>(G.n_nodes, 1));
         cuda_check(cudaMemcpy(grp.d_serve_nodes.data(), grp.serve_nodes.data(), sizeof(FdyServeNode) * G.n_nodes,
@@ -520,68 +524,91 @@ void ServingContext::Impl::build_group(uint32_t gi) {
 
 // ---------------------------------------------------------------- serve
 
-void ServingContext::Impl::ensure_serve_buffers(uint32_t n_nodes) {
-    if (n_nodes <= serve_capacity) return;
-    if (serve_flags) cudaFreeHost(serve_flags);
-    if (serve_records) cudaFreeHost(serve_records);
-    serve_flags = nullptr;
-    serve_records = nullptr;
-    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&serve_flags), n_nodes, cudaHostAllocMapped),
-               "cudaHostAlloc(serve flags)");
-    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&serve_records), 24ull * n_nodes, cudaHostAllocMapped),
-               "cudaHostAlloc(serve records)");
-    serve_capacity = n_nodes;
+void ServingContext::Impl::build_serve_plan() {
+    const uint32_t nm = view->n_members(), ng = static_cast<uint32_t>(groups.size());
+    std::vector<uint64_t> off(nm);
+    std::vector<uint32_t> grp_of(nm), base(nm);
+    std::vector<const FdyServeNode*> tables(ng);
+    std::vector<uint32_t> nn(ng);
+    uint32_t slots = 0;
+    for (uint32_t m = 0; m < nm; ++m) {
+        const fdt_member& M = view->member(m);
+        off[m] = M.out_off;
+        grp_of[m] = M.group;
+        base[m] = slots;
+        slots += static_cast<uint32_t>(groups[M.group].memop_nodes.size());
+    }
+    for (uint32_t g = 0; g < ng; ++g) {
+        tables[g] = reinterpret_cast<const FdyServeNode*>(groups[g].d_serve_nodes.data());
+        nn[g] = view->group(g).n_nodes;
+    }
+    // one scratch buffer: offsets | groups | bases | tables | n_nodes | flags | records
+    const size_t bytes = 8ull * nm + 4ull * nm + 4ull * nm + 8ull * ng + 4ull * ng + nm + 24ull * slots + 64;
+    DeviceBuffer scratch(*dev, bytes);
+    unsigned char* p = scratch.data();
+    auto put = [&](const void* src, size_t n) {
+        unsigned char* at = p;
+        if (n) cuda_check(cudaMemcpyAsync(at, src, n, cudaMemcpyHostToDevice, dev->stream()), "serve plan H2D");
+        p += (n + 7) / 8 * 8;
+        return at;
+    };
+    FdyServePlanArgs a{};
+    a.arena = d_members.data();
+    a.member_off = reinterpret_cast<const uint64_t*>(put(off.data(), 8ull * nm));
+    a.member_group = reinterpret_cast<const uint32_t*>(put(grp_of.data(), 4ull * nm));
+    a.memop_base = reinterpret_cast<const uint32_t*>(put(base.data(), 4ull * nm));
+    a.group_nodes = reinterpret_cast<const FdyServeNode* const*>(put(tables.data(), 8ull * ng));
+    a.group_n_nodes = reinterpret_cast<const uint32_t*>(put(nn.data(), 4ull * ng));
+    a.member_host = p;
+    p += (nm + 7) / 8 * 8;
+    a.records = reinterpret_cast<uint64_t*>(p);
+    a.n_members = nm;
+    cuda_check(fdy_launch_serve_plan(&a, dev->stream()), "serve plan launch");
+    serve_member_host.assign(nm, 1);
+    serve_plan_records.assign(slots, {0, 0, 0});
+    if (nm) cuda_check(cudaMemcpyAsync(serve_member_host.data(), a.member_host, nm, cudaMemcpyDeviceToHost,
+                                       dev->stream()), "serve plan D2H");
+    if (slots) cuda_check(cudaMemcpyAsync(serve_plan_records.data(), a.records, 24ull * slots,
+                                          cudaMemcpyDeviceToHost, dev->stream()), "serve plan D2H");
+    cuda_check(cudaStreamSynchronize(dev->stream()), "cudaStreamSynchronize(serve plan)");
+    serve_memop_base = std::move(base);
 }
 
-// device_updates serve: kernel nodes from the GPU, memops (and anything the
-// device cannot change) from the host. Returns the nodes updated.
+// device_updates serve: kernel nodes from the GPU (asynchronous: the launch is
+// queued on the device stream ahead of the next graph launch), memop nodes from
+// the host out of the LOAD-time plan. No readback. Returns the nodes updated, or
+// kNoMember when the member needs the host path (function / block / shared
+// memory of a node differs from what its template was built with).
 uint64_t ServingContext::Impl::serve_on_device(uint32_t gi, uint32_t m) {
+    if (serve_member_host[m]) return kNoMember;
     Group& grp = groups[gi];
     const fdt_group& G = view->group(gi);
     const DriverApi& api = driver();
     dev->make_current();
-    ensure_serve_buffers(G.n_nodes);
     FdyServeArgs a{};
     a.nodes = reinterpret_cast<const FdyServeNode*>(grp.d_serve_nodes.data());
     a.image = d_members.data() + view->member(m).out_off;
-    cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.host_flags), serve_flags, 0),
-               "cudaHostGetDevicePointer");
-    cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.host_records), serve_records, 0),
-               "cudaHostGetDevicePointer");
-    a.n_nodes = G.n_nodes;
+    a.n_nodes = G.n_nodes;  // host_flags / host_records null: nothing comes back
     cuda_check(fdy_launch_serve(&a, dev->stream()), "serve kernel launch");
-    cuda_check(cudaStreamSynchronize(dev->stream()), "cudaStreamSynchronize(serve)");
-    uint64_t touched = 0;
-    bool host_path = false;
-    for (uint32_t n = 0; n < G.n_nodes; ++n) {
-        const uint8_t f = serve_flags[n];
-        if (f == 0) {
-            touched += grp.serve_nodes[n].devnode != nullptr;
-        } else if (f == 1) {
-            std::array<uint64_t, 3> rec;
-            std::memcpy(rec.data(), serve_records + 3ull * n, 24);
-            if (rec == grp.memops[n]) continue;
-            const uint8_t* blob = reinterpret_cast<const uint8_t*>(rec.data());
-            CUgraphNodeType t;
-            cu_check(api.cuGraphNodeGetType(grp.nodes[n], &t), "cuGraphNodeGetType");
-            if (t == CU_GRAPH_NODE_TYPE_MEMCPY) {
-                const CUDA_MEMCPY3D c = memcpy_params(blob);
-                cu_check(api.cuGraphExecMemcpyNodeSetParams(grp.exec, grp.nodes[n], &c, cu_ctx),
-                         "cuGraphExecMemcpyNodeSetParams");
-            } else {
-                const CUDA_MEMSET_NODE_PARAMS sp = memset_params(blob);
-                cu_check(api.cuGraphExecMemsetNodeSetParams(grp.exec, grp.nodes[n], &sp, cu_ctx),
-                         "cuGraphExecMemsetNodeSetParams");
-            }
-            grp.memops[n] = rec;
-            ++touched;
+    uint64_t touched = grp.n_kernel_nodes;
+    for (uint32_t k = 0; k < grp.memop_nodes.size(); ++k) {
+        const uint32_t n = grp.memop_nodes[k];
+        const std::array<uint64_t, 3>& rec = serve_plan_records[serve_memop_base[m] + k];
+        if (rec == grp.memops[n]) continue;
+        const uint8_t* blob = reinterpret_cast<const uint8_t*>(rec.data());
+        CUgraphNodeType t;
+        cu_check(api.cuGraphNodeGetType(grp.nodes[n], &t), "cuGraphNodeGetType");
+        if (t == CU_GRAPH_NODE_TYPE_MEMCPY) {
+            const CUDA_MEMCPY3D c = memcpy_params(blob);
+            cu_check(api.cuGraphExecMemcpyNodeSetParams(grp.exec, grp.nodes[n], &c, cu_ctx),
+                     "cuGraphExecMemcpyNodeSetParams");
         } else {
-            host_path = true;
+            const CUDA_MEMSET_NODE_PARAMS sp = memset_params(blob);
+            cu_check(api.cuGraphExecMemsetNodeSetParams(grp.exec, grp.nodes[n], &sp, cu_ctx),
+                     "cuGraphExecMemsetNodeSetParams");
         }
-    }
-    if (host_path) {  // a change the device cannot make: the whole member from the host
-        grp.applied = kNoMember;
-        return kNoMember;
+        grp.memops[n] = rec;
+        ++touched;
     }
     return touched;
 }
@@ -591,6 +618,7 @@ uint64_t ServingContext::Impl::apply_member(uint32_t gi, uint32_t m) {
     if (grp.applied == m) return 0;
     if (opts.device_updates && !grp.serve_nodes.empty()) {
         const uint64_t touched = serve_on_device(gi, m);
+        if (touched == kNoMember) grp.applied = kNoMember;  // the host path applies every node
         if (touched != kNoMember) {
             grp.applied = m;
             grp.bound = gi;
@@ -1013,6 +1041,8 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
             rethrow_in_step("template construction");
         }
     }
+
+    if (opts.device_updates) I.build_serve_plan();
 
     // trace arena: one record (64 B + parameter bytes) per kernel node
     uint64_t arena = 1 << 16;

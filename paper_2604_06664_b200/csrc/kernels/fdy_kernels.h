@@ -39,6 +39,23 @@ struct FdyServeNode {
     uint32_t kernel;        // store kernel index the node was built with
     uint32_t block[3];
     uint32_t shmem;
+    int32_t memop_slot;     // memcpy / memset node: its index among the group's memops, else -1
+    uint32_t pad;
+};
+
+// Serve plan, once per LOAD: for every member, whether the device can apply it
+// (no node's function / block / shared memory differs from what its template
+// was built with) and its memop records, so serve() needs no readback.
+struct FdyServePlanArgs {
+    const unsigned char* arena;              // member images in HBM
+    const uint64_t* member_off;              // per member: image offset in the arena
+    const uint32_t* member_group;            // per member: group index
+    const FdyServeNode* const* group_nodes;  // per group: device serve table
+    const uint32_t* group_n_nodes;
+    const uint32_t* memop_base;              // per member: first slot in records
+    uint8_t* member_host;                    // out, per member: 1 = host path needed
+    uint64_t* records;                       // out: 3 x u64 per (member, memop slot)
+    uint32_t n_members;
 };
 
 struct FdyServeArgs {
@@ -72,7 +89,9 @@ cudaError_t fdy_launch_materialize(const FdyMaterializeArgs* args, int grid, cud
 cudaError_t fdy_crc64_set_constants(const uint64_t* x2k64);
 
 // Device-side serve: apply a member image to a device-updatable exec (serve.cu).
+// host_flags / host_records may be null (then nothing is written back).
 cudaError_t fdy_launch_serve(const FdyServeArgs* args, cudaStream_t stream);
+cudaError_t fdy_launch_serve_plan(const FdyServePlanArgs* args, cudaStream_t stream);
 // CRC-64/XZ of n_segments byte ranges already resident in device memory.
 // blocks: host-built table (see fdy_crc_plan) in device memory; partial /
 // lengths scratch: n_blocks entries each; out: n_segments digests (device).

@@ -8,9 +8,10 @@
 // calls cudaGraphKernelNodeSetParam (16-byte slices of the argument block) and
 // cudaGraphKernelNodeSetGridDim. A device update cannot change a node's
 // function, block dims or dynamic shared memory, and memcpy / memset nodes
-// have no device-side update: such nodes are flagged (with their 24-byte
-// memop record) in host-mapped memory and the host applies them with
-// cuGraphExec*NodeSetParams. No host copy of the member image is needed.
+// have no device-side update: fdy_serve_plan_kernel records, once per LOAD,
+// which members need the host path and every member's memop records, so the
+// host applies memops with cuGraphExec*NodeSetParams without a readback and
+// serve() never waits on the device. No host copy of the member image is needed.
 //
 // Compiled with -rdc=true and device-linked against libcudadevrt (the device
 // graph-update API lives in the device runtime).
@@ -45,14 +46,48 @@ fdy_serve_kernel(const FdyServeArgs a) {
         if (!__all_sync(0xFFFFFFFFu, ok)) flag = 2;  // the host re-applies the whole member
     } else if (d.type == 1 || d.type == 2) {
         flag = 1;  // memop: host SetParams from the record below
-        if (lane < 3) a.host_records[3ull * n + lane] = reinterpret_cast<const uint64_t*>(blob)[lane];
+        if (lane < 3 && a.host_records) a.host_records[3ull * n + lane] = reinterpret_cast<const uint64_t*>(blob)[lane];
     } else if (d.type == 0) {
         flag = 2;  // function / block / shmem changed: host path
     }
-    if (lane == 0) a.host_flags[n] = flag;
+    if (lane == 0 && a.host_flags) a.host_flags[n] = flag;
+}
+
+// One CTA per member: device-applicability flag and memop records (see FdyServePlanArgs).
+__global__ void __launch_bounds__(kServeThreads)
+fdy_serve_plan_kernel(const FdyServePlanArgs a) {
+    __shared__ int needs_host;
+    const uint32_t m = blockIdx.x;
+    if (threadIdx.x == 0) needs_host = 0;
+    __syncthreads();
+    const uint32_t g = a.member_group[m];
+    const FdyServeNode* nodes = a.group_nodes[g];
+    const uint32_t nn = a.group_n_nodes[g];
+    const unsigned char* image = a.arena + a.member_off[m];
+    for (uint32_t n = threadIdx.x; n < nn; n += kServeThreads) {
+        const fdt_node d = reinterpret_cast<const fdt_node*>(image)[n];
+        const FdyServeNode& s = nodes[n];
+        if (d.type == 0) {
+            if (s.devnode == nullptr || d.kernel != s.kernel || d.block[0] != s.block[0] ||
+                d.block[1] != s.block[1] || d.block[2] != s.block[2] || d.shmem != s.shmem)
+                needs_host = 1;
+        } else if ((d.type == 1 || d.type == 2) && s.memop_slot >= 0) {
+            const uint64_t* r = reinterpret_cast<const uint64_t*>(image + 48ull * nn + d.blob_off);
+            uint64_t* out = a.records + 3ull * (a.memop_base[m] + uint32_t(s.memop_slot));
+            out[0] = r[0], out[1] = r[1], out[2] = r[2];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) a.member_host[m] = uint8_t(needs_host);
 }
 
 }  // namespace
+
+extern "C" cudaError_t fdy_launch_serve_plan(const FdyServePlanArgs* args, cudaStream_t stream) {
+    if (args->n_members == 0) return cudaSuccess;
+    fdy_serve_plan_kernel<<<args->n_members, kServeThreads, 0, stream>>>(*args);
+    return cudaGetLastError();
+}
 
 extern "C" cudaError_t fdy_launch_serve(const FdyServeArgs* args, cudaStream_t stream) {
     if (args->n_nodes == 0) return cudaSuccess;
