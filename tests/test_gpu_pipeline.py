@@ -331,3 +331,23 @@ def test_replay_equivalence_at_world_four(foundry, load, oracle, archives, name)
     want = expected_traces(oracle, arch, 3, 4)
     for b in h.batches():
         assert h.replay(b) == want[b], "batch %d" % b
+
+
+def test_device_updates_random_serve_order(foundry, load, oracle, archives):
+    """Asynchronous device serves in a random order, interleaved with serves
+    that are not replayed (queued updates overwritten by later ones) and
+    with repeated batches: every replay still matches the oracle."""
+    import random
+    arch, _ = archives("moe-spmd")
+    h = load(arch, rank=2, world=8, device_updates=True)
+    want = expected_traces(oracle, arch, 2, 8)
+    rng = random.Random(11)
+    bs = h.batches()
+    for i in range(150):
+        b = rng.choice(bs)
+        for _ in range(rng.randrange(3)):
+            h.serve(rng.choice(bs))  # queued, superseded
+        if i % 3 == 0:
+            h.serve(b)
+            h.serve(b)               # no-op: already applied
+        assert h.replay(b) == want[b], "step %d batch %d" % (i, b)
