@@ -9,7 +9,7 @@ base = json.load(open(A + "/manifest"))["allocator"]["base"]
 api = capi.CApi(); dev = api.device_open(0); store = api.store_upload(dev, blob)
 members, _ = api.materialize(dev, store, 0, 8, base + 0x10000)
 fw = torch.empty(256 << 20, dtype=torch.uint8, device="cuda"); fr = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
-for grid in [148, 296, 444, 592, 740, 888, 1036]:
+for grid in [int(g) for g in (sys.argv[1].split(",") if len(sys.argv) > 1 else "148,296,444,592,740,888,1036".split(","))]:
     ts = []
     for i in range(15):
         fw.zero_(); torch.count_nonzero(fr); torch.cuda.synchronize()
