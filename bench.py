@@ -57,6 +57,7 @@ def parse_args():
     p.add_argument("--fanout", choices=["host", "ipc"], default="ipc",
                    help="N>1: how the store reaches every GPU (ipc = GPU0 -> peers over NVLink)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--skip-tier-s", action="store_true", help="skip the model-shaped arena measurement")
     return p.parse_args()
 
 
@@ -98,6 +99,25 @@ def prepare_archives(workload: str, rank: int, barrier) -> tuple[str, str]:
         open(done, "w").write(stamp)
     barrier()
     return ours, plain
+
+
+def tier_s_archive(archive: str) -> str:
+    """The headline archive with model-shaped argument blocks (SURVEY §8(d) tier
+    S: every third kernel node a 1720-byte GEMM-like block with embedded device
+    pointers, ragged tails, member-varying grids; tests/tier_s.py), packed.
+    Cached next to the archive it is derived from."""
+    import paper_2604_06664_b200 as foundry
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import tier_s
+
+    out = os.path.join(os.path.dirname(archive), "tier_s")
+    done = os.path.join(os.path.dirname(archive), "TIER_S_READY")
+    if not os.path.exists(done):
+        shutil.rmtree(out, ignore_errors=True)
+        tier_s.make_tier_s(archive, out, foundry._foundry._crc64)
+        foundry._foundry._pack_store(out)
+        open(done, "w").write("ok")
+    return out
 
 
 class ClockSampler:
@@ -352,6 +372,41 @@ def main():
         reloc_ms = reduce_max(statistics.mean(r for r, _ in split))
         member_ms = reduce_max(statistics.mean(m for _, m in split))
 
+        # the same on a model-shaped (tier-S) arena of the headline set: 1720-byte
+        # GEMM-like argument blocks make the member images ~330 MB (SURVEY §8(d):
+        # GB/s is most meaningful on arenas of hundreds of MB)
+        ts = None
+        if not args.skip_tier_s:
+            ts_arch = tier_s_archive(archive) if grank == 0 else None
+            barrier()
+            ts_arch = ts_arch or os.path.join(os.path.dirname(archive), "tier_s")
+            ts_blob = open(os.path.join(ts_arch, "templates.fdt"), "rb").read()
+            ts_hdr = capi.store_header(ts_blob)
+            ts_alg = capi.algorithmic_bytes(ts_hdr)
+            ts_store = api.store_upload(dev, ts_blob)
+            ts_members, _ = api.materialize(dev, ts_store, wrank, TP_WORLD, base + delta)
+            ts_whole, ts_split = [], []
+            for _ in range(args.warmup):
+                flush_l2()
+                api.materialize(dev, ts_store, wrank, TP_WORLD, base + delta, ts_members)
+            for _ in range(args.steps):
+                flush_l2()
+                ts_whole.append(api.materialize(dev, ts_store, wrank, TP_WORLD, base + delta, ts_members)[1])
+                flush_l2()
+                ts_split.append(api.materialize_split(dev, ts_store, wrank, TP_WORLD, base + delta,
+                                                      ts_members)[1])
+            torch.cuda.synchronize()
+            ts_ms = reduce_max(statistics.mean(ts_whole))
+            ts_member_ms = reduce_max(statistics.mean(ts_split))
+            api.lib.fdy_members_free(ts_members)
+            api.lib.fdy_store_free(ts_store)
+            ts = {"workload": args.workload + "~ tier-S (model-shaped argument blocks), rank %d of 8" % wrank,
+                  "member_image_bytes": ts_hdr["members_image_bytes"], "store_bytes": len(ts_blob),
+                  "ms": ts_ms, "member_pass_ms": ts_member_ms,
+                  "member_pass_algorithmic_bytes": ts_alg["member_pass"],
+                  "member_pass_gbps": ts_alg["member_pass"] / (ts_member_ms * 1e-3) / 1e9,
+                  "whole_launch_gbps": ts_alg["total"] / (ts_ms * 1e-3) / 1e9}
+
         # ------- end to end through the C-ABI: archive files -> host result -------
         # fdy_prepare_archive = read every file, DMA to HBM, GPU CRC of every
         # file vs the manifest, fused kernel over every member, copy all member
@@ -521,6 +576,8 @@ def main():
             "driver_bound": "cuLibraryLoadData + cuFuncLoad of every template's functions + "
                             "cuGraphAdd*/cuGraphInstantiate per graph shape",
             "breakdown": {k: v for k, v in sbd.items() if k.endswith("_ms") and k != "crc_kernel_ms"}},
+        "tier_s": None if ts is None else dict(ts, member_pass_frac=ts["member_pass_gbps"] / peak,
+                                               whole_launch_frac=ts["whole_launch_gbps"] / peak),
         "serve_sweep": serve_ms or None,
         "cold_process_load": None if not cold else {
             "unit": "ms", "per_template": cold.get("per_template"), "share_execs": cold.get("share_execs"),

@@ -298,12 +298,15 @@ def test_baseline_configs_full_size_bit_exact(foundry, oracle, api, dev, tmp_pat
         api.lib.fdy_store_free(store)
 
 
-@pytest.mark.parametrize("rank,world,delta", [(0, 1, 0), (3, 8, 0x10000), (5, 8, DELTAS[3])])
-def test_tier_s_graphs_on_the_gpu(foundry, oracle, archives, api, dev, tmp_path, rank, world, delta):
+@pytest.mark.parametrize("name,rank,world,delta", [
+    ("moe-spmd", 0, 1, 0), ("moe-spmd", 3, 8, 0x10000), ("moe-spmd", 5, 8, DELTAS[3]),
+    ("qwen3-235b-a22b", 5, 8, 0x10000),  # the bench's tier-S arena (330 MB of member images)
+])
+def test_tier_s_graphs_on_the_gpu(foundry, oracle, archives, api, dev, tmp_path, name, rank, world, delta):
     """Tier-S fixtures (tests/tier_s.py: 1720-byte argument blocks, unaligned
     pointers, ragged sizes, member-varying grids) through the fused kernel."""
     import tier_s
-    src, _ = archives("moe-spmd")
+    src, _ = archives(name)
     arch = tier_s.make_tier_s(src, str(tmp_path / "s"), oracle.crc64)
     foundry._foundry._pack_store(arch)
     blob = open(os.path.join(arch, "templates.fdt"), "rb").read()

@@ -23,24 +23,31 @@ def make_tier_s(src: str, dst: str, crc64, seed: int = 7) -> str:
     raw = open(os.path.join(dst, "graphs.bin"), "rb").read()
     (version,) = struct.unpack_from("<H", raw, 4)
     graphs = fndg.graphs(raw)
+    ext_of = {}  # node id -> its GEMM-block extension (identical across members)
+    tail_of = {}
     for g in graphs:
         for n in g.nodes:
             if n.type != 0 or n.name.startswith("stub_"):
                 continue
-            r = random.Random(seed * 1_000_003 + n.id)  # same per node across members
             if n.id % 3 == 0:
-                # GEMM-like block: 1720 bytes (ragged: not a multiple of 16)
-                ext = bytearray(r.getrandbits(8) for _ in range(1720 - len(n.args)))
-                for off in range(0, len(ext) - 8, 24):  # device pointers, some unaligned
-                    p = base + r.randrange(0, span, 16)
-                    o = off + (off // 24) % 3  # 8-aligned in the block when (len+o) % 8 == 0
-                    struct.pack_into("<Q", ext, o, p)
+                key = (n.id, len(n.args))
+                if key not in ext_of:
+                    r = random.Random(seed * 1_000_003 + n.id)
+                    # GEMM-like block: 1720 bytes (ragged: not a multiple of 16)
+                    ext = bytearray(r.randbytes(1720 - len(n.args)))
+                    for off in range(0, len(ext) - 8, 24):  # device pointers, some unaligned
+                        o = off + (off // 24) % 3  # 8-aligned in the block when (len+o) % 8 == 0
+                        struct.pack_into("<Q", ext, o, base + r.randrange(0, span, 16))
+                    ext_of[key] = ext
+                ext = bytearray(ext_of[key])
                 # member-dependent bytes: batch label, a per-batch scratch pointer
                 struct.pack_into("<Q", ext, 40, g.label)
                 struct.pack_into("<Q", ext, 48, base + 0x10000 * (g.label % 7))
                 n.args = n.args + bytes(ext)
             elif n.id % 5 == 0:
-                n.args = n.args + bytes(r.getrandbits(8) for _ in range(13))  # ragged tail
+                if n.id not in tail_of:
+                    tail_of[n.id] = random.Random(seed * 1_000_003 + n.id).randbytes(13)
+                n.args = n.args + tail_of[n.id]  # ragged tail
             if n.id % 7 == 0:
                 n.grid = (n.grid[0], n.grid[1], 1 + g.label % 3)  # dims differ between members
     data, locs = fndg.write_container(graphs, version, crc64)
