@@ -227,8 +227,10 @@ def reference_archive(workload: str) -> str | None:
 def cold_process_load(args, local: int) -> dict:
     """Wall clock of a fresh process from exec to every template servable:
     `foundry load --archive <headline> --rank 0 --world 8` (CUDA context
-    creation + LOAD), per-template execs and share_execs, next to a fresh
-    process that only creates the CUDA context (`fdy_tool cuda-init`)."""
+    creation + LOAD, stamped when the CLI's "ready" line arrives), per-template
+    execs and share_execs, next to a fresh process that only creates the CUDA
+    context (`fdy_tool cuda-init`). `process_exit` adds the teardown (graphs,
+    libraries, context) until the process has exited."""
     archive, _ = prepare_archives(args.workload, 0, lambda: None)
     pkg = os.path.join(ROOT, "paper_2604_06664_b200")
     runs = {"cuda_init": [os.path.join(pkg, "fdy_tool"), "cuda-init", str(local)]}
@@ -240,16 +242,26 @@ def cold_process_load(args, local: int) -> dict:
     # idle (driver / GPU wake-up) is not part of any load
     subprocess.run(runs["cuda_init"], capture_output=True)
     out = {}
+    exits = {}
     for name, cmd in runs.items():
-        walls = []
+        walls, totals = [], []
         for _ in range(2):
             t0 = time.perf_counter()
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            walls.append((time.perf_counter() - t0) * 1e3)
-            if r.returncode != 0:
+            p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            t_ready = None
+            for line in p.stdout:  # the CLI flushes its "ready" line when LOAD returns
+                if t_ready is None and " ready: " in line:
+                    t_ready = time.perf_counter()
+            rc = p.wait()
+            t_exit = time.perf_counter()
+            if rc != 0:
                 walls = []
                 break
+            walls.append(((t_ready or t_exit) - t0) * 1e3)
+            totals.append((t_exit - t0) * 1e3)
         out[name] = statistics.mean(walls) if walls else None
+        exits[name] = statistics.mean(totals) if walls else None
+    out["process_exit"] = exits
     return out
 
 
@@ -581,11 +593,12 @@ def main():
         "serve_sweep": serve_ms or None,
         "cold_process_load": None if not cold else {
             "unit": "ms", "per_template": cold.get("per_template"), "share_execs": cold.get("share_execs"),
-            "cuda_init_only": cold.get("cuda_init"),
+            "cuda_init_only": cold.get("cuda_init"), "process_exit": cold.get("process_exit"),
             "what": "wall clock of `foundry load --archive <headline> --rank r --world 8` in a fresh "
-                    "process: CUDA context creation + LOAD to every template servable (the paper's "
-                    "cold start); cuda_init_only = a fresh process that only opens the device "
-                    "(CUDA context creation). The "
+                    "process from exec to its 'ready' line: CUDA context creation + LOAD to every "
+                    "template servable (the paper's cold start); cuda_init_only = a fresh process "
+                    "that only opens the device (CUDA context creation, until exit); process_exit = "
+                    "exec to exit, teardown included. The "
                     "reference arm's simulated LOAD creates no CUDA context"},
         "cpu_baseline": cpu,
         "clocks": clocks,

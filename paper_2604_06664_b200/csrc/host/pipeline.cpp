@@ -40,11 +40,12 @@ double ms_since(Clock::time_point t0) {
 
 constexpr uint32_t kNoMember = 0xFFFFFFFFu;
 
-// FOUNDRY_DEBUG=1 prints LOAD phase boundaries to stderr (diagnostics only).
+// FOUNDRY_DEBUG=1 prints LOAD phase boundaries to stderr (diagnostics only),
+// in ms since this library's static initialization (~process start for the CLI).
+const auto g_debug_t0 = Clock::now();
 void debug_phase(const char* what) {
     static const bool on = std::getenv("FOUNDRY_DEBUG") != nullptr;
-    static const auto t0 = Clock::now();
-    if (on) std::fprintf(stderr, "[foundry] %9.3f ms  %s\n", ms_since(t0), what);
+    if (on) std::fprintf(stderr, "[foundry] %9.3f ms  %s\n", ms_since(g_debug_t0), what);
 }
 uint64_t rd64(const uint8_t* p) {
     uint64_t v;
@@ -863,6 +864,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     device.make_current();
     cu_check(driver().cuCtxGetCurrent(&I.cu_ctx), "cuCtxGetCurrent");
     I.ctx = std::make_unique<GpuContext>(device);
+    debug_phase("gpu context ready");
 
     // 1. stage every listed file into HBM (reads overlap the DMA),
     // 2. stage + verify every digest: the store goes to HBM (GPU CRC as it
@@ -1033,6 +1035,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     I.t.foreground_ms = ms_since(t0);
     debug_phase("foreground done");
     builder.join();
+    debug_phase("templates servable");
     if (foreground_error) std::rethrow_exception(foreground_error);
     if (builder_error) {
         try {
@@ -1057,11 +1060,14 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     I.t.nodes = H.total_nodes;
     I.t.templates = H.n_groups;
     I.t.total_ms = ms_since(t_all);
+    debug_phase("load returns");
     return ServingContext(std::move(impl));
 }
 
 ServingContext load(const fs::path& archive, const LoadOptions& opts) {
+    debug_phase("open device");
     auto dev = std::make_unique<Device>(opts.device);
+    debug_phase("device open");
     ServingContext sc = load(*dev, archive, opts);
     sc.impl_->owned_dev = std::move(dev);
     return sc;

@@ -11,6 +11,7 @@
 //   foundry diff    <a> <b>
 //   foundry bench   --workload <preset|spec> [--mode save|load|naive]
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <filesystem>
@@ -109,9 +110,10 @@ int cmd_load(const Args& a) {
     o.share_execs = a.has("--share-execs");
     o.device_updates = a.has("--device-updates");
     o.device = std::stoi(a.get("--device", "0"));
-    ServingContext sc = load(a.get("--archive"), o);
+    std::optional<ServingContext> held(load(a.get("--archive"), o));
+    ServingContext& sc = *held;
     std::cout << "rank " << o.rank << "/" << o.world << " ready: " << sc.batches().size()
-              << " batch sizes servable\n";
+              << " batch sizes servable" << std::endl;  // flushed: callers time exec -> servable
     if (a.has("--replay-all")) {
         std::map<uint32_t, LaunchTrace> traces;
         for (uint32_t b : sc.batches()) traces.emplace(b, sc.replay(b));
@@ -119,6 +121,12 @@ int cmd_load(const Args& a) {
         if (a.has("--traces")) spit(a.get("--traces"), traces_to_text(traces));
     }
     for (const auto& [key, value] : sc.counters()) std::cout << "  " << key << " = " << value << "\n";
+    const auto t0 = std::chrono::steady_clock::now();
+    held.reset();  // graphs, libraries, VA and the device context
+    if (std::getenv("FOUNDRY_DEBUG"))
+        std::cerr << "[foundry] teardown "
+                  << std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count()
+                  << " ms\n";
     return 0;
 }
 
