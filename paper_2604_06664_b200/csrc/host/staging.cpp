@@ -116,7 +116,34 @@ PinnedLease& PinnedLease::operator=(PinnedLease&& o) noexcept {
 
 namespace {
 constexpr size_t kScratch = 1 << 20;  // hash-only reads: per-lane, stays in cache
-}
+
+// Hash-only read buffers outlive the lanes that use them: a fresh buffer per
+// lane per call would page-fault 256 times per MiB inside every LOAD.
+std::mutex g_scratch_mu;
+std::vector<std::unique_ptr<uint8_t[]>> g_scratch;
+
+struct ScratchLease {
+    std::unique_ptr<uint8_t[]> p;
+    uint8_t* get() {
+        if (!p) {
+            {
+                std::lock_guard lock(g_scratch_mu);
+                if (!g_scratch.empty()) {
+                    p = std::move(g_scratch.back());
+                    g_scratch.pop_back();
+                }
+            }
+            if (!p) p.reset(new uint8_t[kScratch]);
+        }
+        return p.get();
+    }
+    ~ScratchLease() {
+        if (!p) return;
+        std::lock_guard lock(g_scratch_mu);
+        g_scratch.push_back(std::move(p));
+    }
+};
+}  // namespace
 
 struct StagedArchive::Shared {
     std::mutex mu;
@@ -284,7 +311,7 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const std::vecto
     const fs::path dir = root;  // the lanes outlive this constructor
     auto body = [=]() {
         cudaSetDevice(ordinal);
-        std::unique_ptr<uint8_t[]> scratch;
+        ScratchLease scratch;
         for (;;) {
             const size_t i = next->fetch_add(1);
             if (i >= pieces->size()) return;
@@ -293,7 +320,6 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const std::vecto
                 const StagedFile& f = *pc.f;
                 uint64_t piece_crc = 0;
                 if (f.placement == Placement::hash) {
-                    if (!scratch) scratch.reset(new uint8_t[kScratch]);
                     Crc64 c;
                     const int fd = ::open((dir / f.rel).c_str(), O_RDONLY | O_CLOEXEC);
                     require(fd >= 0, Errc::archive_corruption, "cannot open " + (dir / f.rel).string());
@@ -529,6 +555,7 @@ static uint64_t materialize_archive_early(Device& dev, const fs::path& root, con
         rethrow_in_step("archive integrity");
     }
     cuda_check(cudaStreamSynchronize(dev.stream()), "cudaStreamSynchronize");
+    trace_point("member images on the host", t_all);
     if (t) {
         t->read_ms = st.read_ms;
         t->integrity_ms = st.integrity_ms;
@@ -686,6 +713,7 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
         rethrow_in_step("archive integrity");
     }
     cuda_check(cudaStreamSynchronize(dev.stream()), "cudaStreamSynchronize");
+    trace_point("member images on the host", t_all);
     if (t) {
         t->read_ms = st.read_ms;
         t->integrity_ms = st.integrity_ms;

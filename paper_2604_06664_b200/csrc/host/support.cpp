@@ -167,12 +167,86 @@ __attribute__((target("pclmul,sse4.1"))) uint64_t fold_blocks(uint64_t c, const 
     return r;
 }
 
+// ---- the same fold four 128-bit lanes at a time (VPCLMULQDQ on 512-bit
+// registers): four accumulators fold 256 bytes per step, then the 16 lanes
+// (lane i = bytes 16i..16i+15 of the last window) fold to the end of it.
+
+struct WideFoldConstants {
+    uint64_t step[2];      // d = 2048 bits
+    uint64_t tail[16][2];  // d = 128 * (15 - i) bits for lane i (lane 15: unused)
+    WideFoldConstants() {
+        step[0] = x_pow_mod(2048 + 63);
+        step[1] = x_pow_mod(2048 - 1);
+        for (int i = 0; i < 15; ++i) {
+            const unsigned d = 128u * static_cast<unsigned>(15 - i);
+            tail[i][0] = x_pow_mod(d + 63);
+            tail[i][1] = x_pow_mod(d - 1);
+        }
+    }
+};
+
+const WideFoldConstants& wide_fold_constants() {
+    static const WideFoldConstants f;
+    return f;
+}
+
+bool have_vpclmul() {
+    static const bool ok = __builtin_cpu_supports("vpclmulqdq") && __builtin_cpu_supports("avx512f") &&
+                           __builtin_cpu_supports("pclmul") && __builtin_cpu_supports("sse4.1");
+    return ok;
+}
+
+__attribute__((target("avx512f,vpclmulqdq"))) inline __m512i fold512(__m512i x, __m512i k) {
+    return _mm512_xor_si512(_mm512_clmulepi64_epi128(x, k, 0x00), _mm512_clmulepi64_epi128(x, k, 0x11));
+}
+
+// Consumes n256 * 256 bytes (n256 >= 1); returns the register.
+__attribute__((target("avx512f,vpclmulqdq,pclmul,sse4.1"))) uint64_t fold_blocks_wide(uint64_t c, const uint8_t* p,
+                                                                                       size_t n256) {
+    const WideFoldConstants& K = wide_fold_constants();
+    const __m512i k = _mm512_broadcast_i32x4(
+        _mm_set_epi64x(static_cast<long long>(K.step[1]), static_cast<long long>(K.step[0])));
+    __m512i x0 = _mm512_loadu_si512(p);
+    __m512i x1 = _mm512_loadu_si512(p + 64);
+    __m512i x2 = _mm512_loadu_si512(p + 128);
+    __m512i x3 = _mm512_loadu_si512(p + 192);
+    x0 = _mm512_xor_si512(x0, _mm512_set_epi64(0, 0, 0, 0, 0, 0, 0, static_cast<long long>(c)));
+    for (size_t i = 1; i < n256; ++i) {
+        const uint8_t* q = p + 256 * i;
+        x0 = _mm512_xor_si512(fold512(x0, k), _mm512_loadu_si512(q));
+        x1 = _mm512_xor_si512(fold512(x1, k), _mm512_loadu_si512(q + 64));
+        x2 = _mm512_xor_si512(fold512(x2, k), _mm512_loadu_si512(q + 128));
+        x3 = _mm512_xor_si512(fold512(x3, k), _mm512_loadu_si512(q + 192));
+    }
+    alignas(64) __m128i lane[16];
+    _mm512_store_si512(lane, x0);
+    _mm512_store_si512(lane + 4, x1);
+    _mm512_store_si512(lane + 8, x2);
+    _mm512_store_si512(lane + 12, x3);
+    __m128i x = lane[15];
+    for (int i = 0; i < 15; ++i) x = _mm_xor_si128(x, fold128(lane[i], K.tail[i]));
+    const auto& T = tables().t;
+    uint64_t r = 0;
+    for (int l = 0; l < 2; ++l) {
+        r ^= static_cast<uint64_t>(l ? _mm_extract_epi64(x, 1) : _mm_cvtsi128_si64(x));
+        r = T[7][r & 0xFF] ^ T[6][(r >> 8) & 0xFF] ^ T[5][(r >> 16) & 0xFF] ^ T[4][(r >> 24) & 0xFF] ^
+            T[3][(r >> 32) & 0xFF] ^ T[2][(r >> 40) & 0xFF] ^ T[1][(r >> 48) & 0xFF] ^ T[0][r >> 56];
+    }
+    return r;
+}
+
 }  // namespace
 
 void Crc64::update(const void* data, size_t len) {
     const auto& T = tables().t;
     const auto* p = static_cast<const uint8_t*>(data);
     uint64_t c = state_;
+    if (len >= 1024 && have_vpclmul()) {
+        const size_t n256 = len / 256;
+        c = fold_blocks_wide(c, p, n256);
+        p += 256 * n256;
+        len -= 256 * n256;
+    }
     if (len >= 256 && have_pclmul()) {
         const size_t n64 = len / 64;
         c = fold_blocks(c, p, n64);

@@ -100,6 +100,18 @@ def test_crc64_host_matches_the_oracle_and_combines(foundry, oracle):
         assert combined == oracle.crc64(a + b)
 
 
+def test_crc64_folding_paths_match_the_oracle(foundry, oracle):
+    # lengths around the 64-byte (PCLMULQDQ) and 256-byte (VPCLMULQDQ, >= 1 KiB)
+    # fold boundaries, unaligned starts, and a multi-MiB buffer
+    import random
+    rng = random.Random(11)
+    big = rng.randbytes(3 << 20)
+    for n in (255, 256, 257, 1023, 1024, 1025, 1279, 1280, 4095, 65536 + 17, 1 << 20, 3 << 20):
+        for off in (0, 1, 13):
+            a = big[off:off + n]
+            assert foundry._foundry._crc64(a) == oracle.crc64(a), (n, off)
+
+
 @pytest.fixture(scope="module")
 def tier_s_archive(foundry, oracle, archives, tmp_path_factory):
     import tier_s
