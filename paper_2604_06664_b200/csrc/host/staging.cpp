@@ -2,6 +2,8 @@
 #include "foundry/staging.hpp"
 
 #include <fcntl.h>
+#include <sys/resource.h>
+#include <sys/syscall.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -309,7 +311,9 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const std::vecto
     unsigned char* dbase = device_.data();
     const int ordinal = dev.ordinal();
     const fs::path dir = root;  // the lanes outlive this constructor
+    const int nice = plan.lane_nice;
     auto body = [=]() {
+        if (nice > 0) ::setpriority(PRIO_PROCESS, static_cast<id_t>(::syscall(SYS_gettid)), nice);
         cudaSetDevice(ordinal);
         ScratchLease scratch;
         for (;;) {
@@ -601,7 +605,12 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
                 // the rest: every other regular file under the archive directory
                 // (extra files are hashed for nothing; missing ones are reported
                 // against the manifest), listed and staged on a helper thread
-                const unsigned rest_lanes = std::max(1u, lanes > 4 ? lanes - 4 : lanes);
+                // on every lane, at the lowest CPU priority: while the store's
+                // pieces are in flight the host is oversubscribed and the store
+                // (the critical path: store -> kernel -> D2H) must win the cores
+                // (tools/_exp_e2e_lanes.sh: median 4.2-4.3 ms vs 4.6-4.75 ms with
+                // lanes - 4 at normal priority, and no 5.5-6 ms outliers)
+                const unsigned rest_lanes = std::max(1u, lanes);
                 rest = std::async(std::launch::async, [&dev, root, rest_lanes] {
                     std::vector<std::string> files;
                     const std::string prefix = root.string() + "/";
@@ -613,7 +622,9 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
                         std::string rel = full.compare(0, prefix.size(), prefix) == 0 ? full.substr(prefix.size()) : full;
                         if (rel != "manifest" && rel != "templates.fdt") files.push_back(std::move(rel));
                     }
-                    return std::make_unique<StagedArchive>(dev, root, files, rest_lanes, nullptr, StagePlan{});
+                    StagePlan background;
+                    background.lane_nice = 19;
+                    return std::make_unique<StagedArchive>(dev, root, files, rest_lanes, nullptr, background);
                 });
             } catch (const Error&) {
                 early.reset();  // the regular path reports it in manifest order

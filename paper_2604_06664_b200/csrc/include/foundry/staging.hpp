@@ -57,6 +57,8 @@ enum class Placement : uint8_t {
 struct StagePlan {
     std::vector<std::string> device;                   // staged first, in this order
     std::function<bool(const std::string&)> keep_host;  // Placement::host files (others: hash)
+    int lane_nice = 0;  // > 0: lanes run at this lower CPU priority (they yield to a concurrent
+                        // critical-path stager when the host's cores are oversubscribed)
 };
 
 struct StagedFile {

@@ -10,7 +10,7 @@ out = api.host_alloc(dev, h["members_image_bytes"])
 reps = int(os.environ.get("REPS", "4"))
 rows = [api.prepare_archive(dev, A, 0, 8, base + 0x10000, 16, out, h["members_image_bytes"]) for _ in range(reps + 1)][1:]
 med = {k: round(statistics.median(r[k] for r in rows), 3) for k in ("total_ms", "read_ms", "integrity_ms", "d2h_ms")}
-print(os.environ.get("TAG", ""), med, "min total %.3f" % min(r["total_ms"] for r in rows), file=sys.stderr)
+print(os.environ.get("TAG", ""), med, "min total %.3f max %.3f" % (min(r["total_ms"] for r in rows), max(r["total_ms"] for r in rows)), file=sys.stderr)
 if len(sys.argv) > 1:
     for f in sorted(os.listdir(A)):
         p = os.path.join(A, f)
