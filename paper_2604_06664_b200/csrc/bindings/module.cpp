@@ -263,6 +263,7 @@ PYBIND11_MODULE(_foundry, m) {
         return crc64(s.data(), s.size());
     });
     m.def("_crc64_combine", &crc64_combine);
+    m.def("_manifest_fast_path_agrees", [](const std::string& text) { return manifest_fast_path_agrees(text); });
     m.def("_pack_store", [](const std::string& archive) {
         py::gil_scoped_release nogil;
         const PackStats st = pack_archive_store(archive);

@@ -91,10 +91,14 @@ struct Manifest {
     std::string catalog_ref = "catalog.bin";
     std::string patch_table_ref = "patch.bin";
     std::map<std::string, uint64_t> file_digests;
+    bool operator==(const Manifest&) const = default;
 };
 
 std::string serialize_manifest(const Manifest& m);
 Manifest parse_manifest(const std::string& text);
+// tests: 1 = parse_manifest's fast reader took the text and agrees with the full
+// JSON parser, 0 = it took it and disagrees, -1 = it deferred to the full parser
+int manifest_fast_path_agrees(const std::string& text);
 
 struct ArchivePaths {
     std::filesystem::path root;

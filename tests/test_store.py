@@ -129,3 +129,32 @@ def test_tier_s_store_expansion_equals_oracle(foundry, oracle, tier_s_archive, r
     inside a template): pack + kernel emulation == oracle."""
     want, _ = oracle.materialize_archive(tier_s_archive, rank, world, delta)
     assert emulate(foundry, tier_s_archive, rank, world, delta) == want
+
+
+def test_manifest_fast_reader_agrees_or_defers(foundry, archives):
+    # parse_manifest reads the manifest with a minimal JSON reader first and hands
+    # anything outside its subset to the full JSON parser; it must never disagree
+    agrees = foundry._foundry._manifest_fast_path_agrees
+    texts = []
+    for name, b200 in (("micro", True), ("moe-spmd", True), ("moe-spmd", False)):
+        arch, _ = archives(name, b200=b200)
+        texts.append(open(os.path.join(arch, "manifest")).read())
+    for t in texts:
+        assert agrees(t) == 1  # every writer's manifest takes the fast path
+    t = texts[0]
+    variants = [
+        t.replace('"format_version": 1', '"format_version": 1.0', 1),
+        t.replace('"kv_cache_bytes": ', '"kv_cache_bytes": -', 1),
+        t.replace('{', '{"catalog": "x", ', 1),            # duplicate key
+        t.replace('"catalog.bin"', '"catalog\\u002ebin"', 1),  # \u escape
+        t.replace('"catalog.bin"', '"catalogé.bin"', 1),  # non-ASCII
+        t + " x",                                            # trailing garbage
+        t.replace('"patch_table"', '"patch_tablex"', 1),     # missing field
+        t.replace('"workload_digest": ', '"workload_digest": 0', 1),  # leading zero
+        " \n" + t + "\n ",                                    # whitespace only
+    ]
+    for v in variants:
+        assert agrees(v) in (-1, 1), v[:80]
+    assert agrees(variants[-1]) == 1
+    for v in variants[:8]:
+        assert agrees(v) == -1
