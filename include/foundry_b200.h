@@ -133,10 +133,13 @@ int fdy_crc64_segments(fdy_device* dev, const void* host, size_t bytes,
 
 /* The whole materialization path in one call — the GPU-native replacement of
  * the reference's verify_archive_integrity (pipeline.cpp:411-417) followed by
- * the PrepareFn over every member (pipeline.cpp:506-514): archive files ->
- * pinned staging -> HBM -> GPU CRC of every file -> fused K2+K1+K3 for
- * desc->(rank, world, new_base) -> member images (store_format.h layout)
- * copied to host_out. host_out may be NULL (images stay in HBM only);
+ * the PrepareFn over every member (pipeline.cpp:506-514): the template store
+ * -> pinned staging -> HBM with a GPU CRC of each piece as it lands -> fused
+ * K2+K1+K3 for desc->(rank, world, new_base) -> member images (store_format.h
+ * layout) copied to host_out; meanwhile every other archive file is CRCed on
+ * the host (`lanes` threads at the lowest CPU priority; the store uses up to 4
+ * lanes at normal priority) and all digests are checked against the manifest
+ * before the call returns. host_out may be NULL (images stay in HBM only);
  * out_len receives the image bytes. */
 typedef struct {
     double total_ms, read_ms, integrity_ms, materialize_ms, d2h_ms;
