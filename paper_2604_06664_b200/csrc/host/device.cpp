@@ -155,7 +155,7 @@ PinnedBuffer& PinnedBuffer::operator=(PinnedBuffer&& o) noexcept {
 // ------------------------------------------------------------------ stores
 
 DeviceStore adopt_store(Device& dev, const unsigned char* d_blob, size_t bytes,
-                        const fdt_header& h) {
+                        const fdt_header& h, const void* host_blob) {
     require(bytes >= sizeof(fdt_header) && std::memcmp(h.magic, "FNDT", 4) == 0,
             Errc::archive_corruption, "template store: bad magic, expected 'FNDT'");
     require(h.version == FDT_VERSION, Errc::archive_corruption,
@@ -171,6 +171,31 @@ DeviceStore adopt_store(Device& dev, const unsigned char* d_blob, size_t bytes,
     s.bytes = bytes;
     s.header = h;
     if (h.sec[FDT_SEC_TIMAGES].bytes) s.rtimages = DeviceBuffer(dev, h.sec[FDT_SEC_TIMAGES].bytes);
+    if (host_blob != nullptr && h.n_tiles != 0 &&
+        h.sec[FDT_SEC_TILES].bytes >= uint64_t(h.n_tiles) * sizeof(fdt_tile)) {
+        // tiles without a relocatable lane in their template chunks first
+        const auto* hb = static_cast<const unsigned char*>(host_blob);
+        const auto* tiles = reinterpret_cast<const fdt_tile*>(hb + h.sec[FDT_SEC_TILES].offset);
+        const unsigned char* cmeta = hb + h.sec[FDT_SEC_CMETA].offset;
+        const uint64_t tbase = h.sec[FDT_SEC_TIMAGES].offset, ncm = h.sec[FDT_SEC_CMETA].bytes;
+        std::vector<fdt_tile> plain, rest;
+        for (uint32_t i = 0; i < h.n_tiles; ++i) {
+            const fdt_tile& t = tiles[i];
+            const uint64_t c0 = (t.src_off - tbase) / 16;
+            bool reloc = t.src_off < tbase || c0 + t.nchunks > ncm;  // malformed: keep it behind the wait
+            for (uint64_t c = c0; !reloc && c < c0 + t.nchunks; ++c) reloc = cmeta[c] != 0;
+            (reloc ? rest : plain).push_back(t);
+        }
+        if (!plain.empty() && !rest.empty()) {
+            plain.insert(plain.end(), rest.begin(), rest.end());
+            s.planned_tiles = DeviceBuffer(dev, plain.size() * sizeof(fdt_tile));
+            cuda_check(cudaMemcpyAsync(s.planned_tiles.data(), plain.data(), plain.size() * sizeof(fdt_tile),
+                                       cudaMemcpyHostToDevice, dev.stream()),
+                       "cudaMemcpyAsync(tile plan H2D)");
+            cuda_check(cudaStreamSynchronize(dev.stream()), "cudaStreamSynchronize(tile plan)");
+            s.n_plain_tiles = static_cast<uint32_t>(h.n_tiles - rest.size());
+        }
+    }
     return s;
 }
 
@@ -181,7 +206,7 @@ DeviceStore upload_store(Device& dev, const void* host_blob, size_t bytes) {
     DeviceBuffer buf(dev, bytes, /*shareable=*/true);  // fdy_store_export may hand it to peers
     cuda_check(cudaMemcpyAsync(buf.data(), host_blob, bytes, cudaMemcpyHostToDevice, dev.stream()),
                "cudaMemcpyAsync(store H2D)");
-    DeviceStore s = adopt_store(dev, buf.data(), bytes, h);
+    DeviceStore s = adopt_store(dev, buf.data(), bytes, h, host_blob);
     s.blob = std::move(buf);
     return s;
 }
@@ -213,6 +238,10 @@ void launch_materialize(Device& dev, const DeviceStore& store, const Materialize
     a.rank = req.rank;
     a.world = req.world;
     a.n_tiles = h.n_tiles;
+    if (store.planned_tiles.data() != nullptr && a.delta != 0) {
+        a.tiles = reinterpret_cast<const fdt_tile*>(store.planned_tiles.data());
+        a.n_plain = store.n_plain_tiles;
+    }
     // the kernel reads template chunks at tsrc + tile.src_off (a store offset)
     a.tsrc = a.delta && a.rtimg ? reinterpret_cast<const unsigned char*>(
                                       reinterpret_cast<uintptr_t>(a.rtimg) - a.timage_base)

@@ -105,6 +105,12 @@ struct DeviceStore {
     // Relocated template images of the launch in flight (delta != 0); one per
     // store, so materializations of a store are ordered on its device stream.
     DeviceBuffer rtimages;
+    // Tile order of the launch (adopt_store with the host blob): tiles whose
+    // template chunks hold no relocatable lane first, so with delta != 0 the
+    // member grid's first tiles read the store itself and do not wait for the
+    // relocation grid. Empty = the store's own order.
+    DeviceBuffer planned_tiles;
+    uint32_t n_plain_tiles = 0;
 };
 
 struct MaterializeRequest {
@@ -126,7 +132,8 @@ struct MaterializeTiming {
 
 // Checks a device-resident store blob's header (host copy) and prepares pointers.
 DeviceStore adopt_store(Device& dev, const unsigned char* d_blob, size_t bytes,
-                        const fdt_header& host_header);
+                        const fdt_header& host_header,
+                        const void* host_blob = nullptr);
 DeviceStore upload_store(Device& dev, const void* host_blob, size_t bytes);
 
 // Launches K2+K1+K3 into `out` (must hold header.members_image_bytes bytes).

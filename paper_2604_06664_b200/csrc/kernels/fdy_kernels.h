@@ -30,6 +30,8 @@ struct FdyMaterializeArgs {
     uint64_t world;
     uint32_t n_tiles;
     uint32_t n_values;
+    uint32_t n_plain;  // tiles[0, n_plain) hold no relocatable template lane: read from the store
+    uint32_t pad_;
 };
 
 // Device-side serve (kernels/serve.cu): one entry per template node.

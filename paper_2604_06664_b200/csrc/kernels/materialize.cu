@@ -261,10 +261,22 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
     fdt_tile Tn = load_tile(a, t + G);
     Prefetch cur;
     prefetch_tile(a, T, s, cur, tid);  // the store itself is never written
-    if (relocating) pdl_wait_primary();  // templates come from the relocated copy
+    // Template source of tile t: the store for the first n_plain tiles (no
+    // relocatable lane), else the relocated copy. Only thread 0 reads
+    // templates (bulk loads), so only it waits for the relocation grid, and
+    // only once it reaches a tile that needs it.
+    bool waited = !relocating;
+    auto template_src = [&](uint32_t tile) {
+        if (tile < a.n_plain) return a.store;
+        if (!waited) {
+            pdl_wait_primary();
+            waited = true;
+        }
+        return a.tsrc;
+    };
     if (tid == 0) {
         mbar_expect_tx(&s.bar[0], T.nchunks * 16u);
-        bulk_load(s.buf[0], a.tsrc + T.src_off, T.nchunks * 16u, &s.bar[0]);
+        bulk_load(s.buf[0], template_src(t) + T.src_off, T.nchunks * 16u, &s.bar[0]);
     }
 
     uint32_t stage = 0;
@@ -276,7 +288,7 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
         if (tid == 0 && has_next) {
             bulk_wait_reads();  // the store that last used stage `nstage` has drained
             mbar_expect_tx(&s.bar[nstage], Tn.nchunks * 16u);
-            bulk_load(s.buf[nstage], a.tsrc + Tn.src_off, Tn.nchunks * 16u, &s.bar[nstage]);
+            bulk_load(s.buf[nstage], template_src(t + G) + Tn.src_off, Tn.nchunks * 16u, &s.bar[nstage]);
         }
         const fdt_tile Tnn = load_tile(a, t + 2 * G);  // consumed next iteration
         uint4* buf = s.buf[stage];
