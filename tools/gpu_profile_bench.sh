@@ -4,7 +4,7 @@
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-B="python bench.py --steps 3 --warmup 3 --e2e-steps 1 --skip-load --no-cpu-baseline"
+B="python bench.py --steps 3 --warmup 3 --e2e-steps 1 --skip-load --no-cpu-baseline --skip-tier-s"
 $B > /dev/null 2>&1   # writes the archive once (not under the profiler)
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file gpurun_out/launches_bench.csv $B > gpurun_out/launches_bench.stdout 2>&1

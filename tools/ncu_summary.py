@@ -88,7 +88,7 @@ def main() -> None:
     rel = ll.get("fdy_relocate_templates_kernel", {}).get("mean_ns", 0.0)
     summary = {
         "kernel": kernel,
-        "command": "python bench.py --steps 3 --warmup 3 --e2e-steps 1 --skip-load --no-cpu-baseline (tools/gpu_profile_bench.sh)",
+        "command": "python bench.py --steps 3 --warmup 3 --e2e-steps 1 --skip-load --no-cpu-baseline --skip-tier-s (tools/gpu_profile_bench.sh)",
         "source": {"full_set": rep, "launch_list": launches},
         **{k: v for k, v in full.items()},
         # one fdy_materialize launch = the template relocation grid (delta != 0,
