@@ -76,10 +76,11 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def prepare_archives(workload: str, rank: int, barrier) -> tuple[str, str]:
-    """Writes (once per node) the B200 archive and a reference-layout archive
-    (no B200 artefacts) of the same spec with this build's SAVE, which is
-    byte-identical to the reference's (tests/test_save.py)."""
+def prepare_archives(workload: str, local_rank: int, barrier) -> tuple[str, str]:
+    """Writes (once per node: local rank 0, into the node-local temp dir) the
+    B200 archive and a reference-layout archive (no B200 artefacts) of the same
+    spec with this build's SAVE, which is byte-identical to the reference's
+    (tests/test_save.py). Every rank waits at `barrier` for its node's writer."""
     import paper_2604_06664_b200 as foundry
 
     root = os.path.join(tempfile.gettempdir(), "foundry_bench_" + workload)
@@ -89,7 +90,7 @@ def prepare_archives(workload: str, rank: int, barrier) -> tuple[str, str]:
     stamp = hashlib.sha1(open(foundry._foundry.__file__, "rb").read()
                          + open(foundry.workload_path(workload), "rb").read()).hexdigest()
     fresh = os.path.exists(done) and open(done).read() == stamp
-    if rank == 0 and not fresh:
+    if local_rank == 0 and not fresh:
         shutil.rmtree(root, ignore_errors=True)
         os.makedirs(root)
         spec = foundry.workload_from_text(open(foundry.workload_path(workload)).read())
@@ -201,15 +202,19 @@ def oracle_port_ms(archive: str, rank: int, world: int, lanes: int, reps: int) -
             "lanes": lanes}
 
 
+def spec_path(workload: str) -> str:
+    """The bundled tier-R spec, resolved by path (the reference arm must not
+    import this build's package)."""
+    return os.path.join(ROOT, "paper_2604_06664_b200", "workloads", workload + ".spec")
+
+
 def reference_archive(workload: str) -> str | None:
     """The workload's archive written by the reference itself (ref_tool save,
     foundry::save pipeline.cpp:249-405), so the reference arm runs none of
     this build's code. Byte-identical to this build's SAVE (tests/test_save.py)."""
     if not os.path.exists(REF_TOOL):
         return None
-    import paper_2604_06664_b200 as foundry  # only for the bundled spec path
-
-    spec = foundry.workload_path(workload)
+    spec = spec_path(workload)
     root = os.path.join(tempfile.gettempdir(), "foundry_refarm_" + workload)
     stamp = hashlib.sha1(open(REF_TOOL, "rb").read() + open(spec, "rb").read()).hexdigest()
     done = os.path.join(root, "READY")
@@ -222,6 +227,57 @@ def reference_archive(workload: str) -> str | None:
             return None
         open(done, "w").write(stamp)
     return out
+
+
+def graph_counts(archive: str) -> tuple[int, int, int]:
+    """(graphs, templates, nodes) of an archive from its manifest and the FNDG
+    locator table of graphs.bin (graph_model.cpp:244-293) — plain file reads,
+    identical for both arms."""
+    import struct
+
+    with open(os.path.join(archive, "manifest")) as f:
+        grouping = json.load(f)["grouping"]
+    nodes = 0
+    with open(os.path.join(archive, "graphs.bin"), "rb") as f:
+        head = f.read(10)
+        (count,) = struct.unpack_from("<I", head, 6)
+        locs = f.read(28 * count)
+        for i in range(count):
+            (off,) = struct.unpack_from("<Q", locs, 28 * i + 4)
+            f.seek(off + 4)
+            nodes += struct.unpack("<I", f.read(4))[0]
+    return grouping["total"], grouping["templates"], nodes
+
+
+def bench_config(workload: str, archive: str, wrank: int) -> dict:
+    """The `config` both arms print (the driver compares them for equality)."""
+    graphs, templates, nodes = graph_counts(archive)
+    return {"workload": workload + "~ tier-R decode graph set, TP8: rank %d of 8 per GPU" % wrank,
+            "graphs": graphs, "templates": templates, "nodes": nodes, "rank": wrank, "world": TP_WORLD,
+            "parallelism": "replicas (one TP rank per GPU)",
+            "value": "graph-set materialization with the template store resident in HBM (ours) / "
+                     "the reference CPU path (reference)",
+            "e2e": "archive files -> integrity -> every member graph's parameters in host memory",
+            "l2": "flushed between timed device steps (256 MiB memset + 256 MiB read of unrelated "
+                  "buffers, outside the events)"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_serve_ms(archive: str, rank: int, world: int, lanes: int, reps: int) -> dict | None:
+    if not os.path.exists(REF_TOOL):
+        return None
+    r = subprocess.run([REF_TOOL, "time-serve", archive, str(rank), str(world), str(lanes), str(reps)],
+                       capture_output=True, text=True)
+    return json.loads(r.stdout) if r.returncode == 0 else None
 
 
 def cold_process_load(args, local: int) -> dict:
@@ -266,23 +322,30 @@ def cold_process_load(args, local: int) -> dict:
 
 
 def run_reference(args, grank, gworld):
-    """--impl reference: the reference's own CPU load() of the same archive."""
+    """--impl reference: the reference's own CPU implementation of the path on
+    this host's cores (oracle/_ref/ref_tool over the unmodified reference), on
+    an archive the reference's own save wrote. Imports nothing from this
+    build. value = e2e = verify_archive_integrity + PrepareFn of every member
+    on all host threads; the full load() and serve+replay sweep ride along."""
     if grank != 0:
         return
     lanes = os.cpu_count() or 1
     plain = reference_archive(args.workload)
-    if plain is None:  # no reference build: this build's byte-identical SAVE
-        _, plain = prepare_archives(args.workload, 0, lambda: None)
+    if plain is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_tool is not built "
+                          "(make -C oracle ref needs /root/reference)"}), flush=True)
+        return
     wrank = 0
-    # the reference's CPU implementation of the path: verify_archive_integrity +
-    # PrepareFn over every member (oracle/_ref/ref_tool time-materialize)
     res = reference_materialize_ms(plain, wrank, TP_WORLD, lanes, args.steps, args.warmup)
     kind = "reference"
     if res is None:
         res = oracle_port_ms(plain, wrank, TP_WORLD, lanes, args.steps)
         kind = "port"
     value = res["mean_ms"]
-    full = reference_load_ms(plain, wrank, TP_WORLD, lanes, min(args.steps, 3))
+    lanes4 = reference_materialize_ms(plain, wrank, TP_WORLD, 4, 3, 1)
+    full = reference_load_ms(plain, wrank, TP_WORLD, lanes, 3)
+    full4 = reference_load_ms(plain, wrank, TP_WORLD, 4, 3)
+    serve = reference_serve_ms(plain, wrank, TP_WORLD, lanes, 2)
     line = {
         "impl": "reference",
         "metric": "graph-set materialization ms (cold start); relocation GB/s vs HBM peak",
@@ -290,15 +353,22 @@ def run_reference(args, grank, gworld):
         "warmup": args.warmup if kind == "reference" else 1,
         "ms_per_step": value, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "u8", "data": "synthetic",
-        "config": {"workload": args.workload + "~ tier-R TP8 (rank 0 of 8)", "graphs": 512,
-                   "parallelism": "replicas"},
-        "cpu_baseline": {"value": value, "unit": "ms", "cores": lanes, "kind": kind,
-                         "sample": "reference verify_archive_integrity + PrepareFn over all "
-                                   "member graphs (archive written by the reference's own save), %d reps "
-                                   "after %d warm-up" % (args.steps, args.warmup if kind == "reference" else 1)},
+        "config": bench_config(args.workload, plain, wrank),
+        "cpu_baseline": {"value": value, "unit": "ms", "cores": lanes, "kind": kind, "cpu_model": cpu_model(),
+                         "sample": "reference verify_archive_integrity (single-threaded, pipeline.cpp:411-417) "
+                                   "+ PrepareFn over all member graphs on %d prepare lanes (archive written by "
+                                   "the reference's own save), %d reps after %d warm-up"
+                                   % (lanes, args.steps, args.warmup if kind == "reference" else 1),
+                         "integrity_ms": res.get("integrity_best_ms"),
+                         "prepare_lanes_4_ms": lanes4["mean_ms"] if lanes4 else None},
         "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "full_load": {"value": full["mean_ms"] if full else None, "unit": "ms",
-                      "api": "reference foundry::load (pipeline.cpp:447-557)"},
+        "full_load": {"value": full["mean_ms"] if full else None, "unit": "ms", "prepare_lanes": lanes,
+                      "prepare_lanes_4_ms": full4["mean_ms"] if full4 else None,
+                      "api": "reference foundry::load (pipeline.cpp:447-557), simulated driver"},
+        "serve_replay_all": None if serve is None else {
+            "ms": serve["mean_ms"], "us_per_batch": serve["us_per_batch"], "batches": serve["batches"],
+            "api": "reference ServingContext::replay of every batch in label order (serve + simulated "
+                   "launch, pipeline.cpp:566-569, 876-889)"},
     }
     print(json.dumps(line), flush=True)
 
@@ -330,7 +400,7 @@ def main():
     group.init("gloo" if shared else "nccl")
     barrier, reduce_max = group.barrier, group.max
 
-    archive, plain = prepare_archives(args.workload, grank, barrier)
+    archive, plain = prepare_archives(args.workload, local, barrier)
     wrank = tp_rank(grank)
     with open(os.path.join(archive, "manifest")) as f:
         manifest = json.load(f)
@@ -389,7 +459,7 @@ def main():
         # GB/s is most meaningful on arenas of hundreds of MB)
         ts = None
         if not args.skip_tier_s:
-            ts_arch = tier_s_archive(archive) if grank == 0 else None
+            ts_arch = tier_s_archive(archive) if local == 0 else None
             barrier()
             ts_arch = ts_arch or os.path.join(os.path.dirname(archive), "tier_s")
             ts_blob = open(os.path.join(ts_arch, "templates.fdt"), "rb").read()
@@ -540,14 +610,9 @@ def main():
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic",
-        "config": {
-            "workload": args.workload + "~ tier-R decode graph set, TP8: rank %d of 8 per GPU" % wrank,
-            "graphs": graphs, "nodes": hdr["total_nodes"], "templates": hdr["n_groups"],
-            "store_bytes": len(blob), "member_image_bytes": hdr["members_image_bytes"],
-            "relocation_delta": delta, "parallelism": "replicas (one TP rank per GPU)",
-            "l2": "flushed between timed steps (256 MiB memset + 256 MiB read of unrelated "
-                  "buffers, outside the events)",
-        },
+        "config": bench_config(args.workload, archive, wrank),
+        "store": {"store_bytes": len(blob), "member_image_bytes": hdr["members_image_bytes"],
+                  "relocation_delta": delta, "nodes": hdr["total_nodes"], "templates": hdr["n_groups"]},
         "graphs_per_s": gworld * graphs / (kernel_ms_max * 1e-3),
         "nodes_per_s": gworld * hdr["total_nodes"] / (kernel_ms_max * 1e-3),
         "relocation_gbps": launch_gbps,

@@ -23,6 +23,8 @@
 //        optionally followed by serve+replay of every batch; prints JSON.
 //   time-materialize <archive> <rank> <world> <lanes> <reps>
 //        integrity CRC of every file + PrepareFn of every member, timed.
+//   time-serve <archive> <rank> <world> <lanes> <reps>
+//        serve + replay of every batch after one load (pipeline.cpp:876-889).
 //   crc <file>   CRC-64/XZ (hash.cpp:53-69) of a file, hex.
 //   diff <a.fndg> <b.fndg>   reference diff() text per graph pair.
 #include <atomic>
@@ -155,6 +157,37 @@ static int cmd_time_load(int argc, char** argv) {
     return 0;
 }
 
+// time-serve <archive> <rank> <world> <lanes> <reps>
+//   one foundry::load, then `reps` sweeps of ServingContext::replay over every
+//   batch in label order (= ServingSet::serve + the simulated launch,
+//   pipeline.cpp:566-569, the loop of bench --mode load pipeline.cpp:876-889),
+//   after one untimed sweep.
+static int cmd_time_serve(int argc, char** argv) {
+    if (argc < 7) return usage();
+    LoadOptions options;
+    options.rank = static_cast<uint32_t>(std::stoul(argv[3]));
+    options.world = static_cast<uint32_t>(std::stoul(argv[4]));
+    options.prepare_lanes = static_cast<unsigned>(std::stoul(argv[5]));
+    const int reps = std::max(1, std::stoi(argv[6]));
+    using clock = std::chrono::steady_clock;
+    ServingContext sc = load(argv[2], options);
+    const auto batches = sc.batches();
+    double best = 1e300, total = 0.0;
+    for (int i = 0; i < reps + 1; ++i) {
+        const auto t0 = clock::now();
+        for (uint32_t b : batches) sc.replay(b);
+        const double ms = std::chrono::duration<double, std::milli>(clock::now() - t0).count();
+        if (i > 0) {
+            best = std::min(best, ms);
+            total += ms;
+        }
+    }
+    std::printf("{\"best_ms\": %.6f, \"mean_ms\": %.6f, \"reps\": %d, \"batches\": %zu, "
+                "\"us_per_batch\": %.3f}\n",
+                best, total / reps, reps, batches.size(), 1e3 * (total / reps) / batches.size());
+    return 0;
+}
+
 // time-materialize <archive> <rank> <world> <lanes> <reps> [warmup=1]
 //   the reference's share of LOAD that the GPU path replaces: the integrity
 //   CRC of every manifest-listed file, single-threaded as in
@@ -246,6 +279,7 @@ int main(int argc, char** argv) {
         if (cmd == "replay") return cmd_replay(argc, argv);
         if (cmd == "time-load") return cmd_time_load(argc, argv);
         if (cmd == "time-materialize") return cmd_time_materialize(argc, argv);
+        if (cmd == "time-serve") return cmd_time_serve(argc, argv);
         if (cmd == "crc") return cmd_crc(argc, argv);
         if (cmd == "diff") return cmd_diff(argc, argv);
     } catch (const Error& e) {

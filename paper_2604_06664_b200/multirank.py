@@ -71,6 +71,15 @@ class RankGroup:
         dist.broadcast_object_list(box, src=src)
         return box[0]
 
+    def all_gather_object(self, obj) -> list:
+        if self.world == 1:
+            return [obj]
+        import torch.distributed as dist
+
+        out = [None] * self.world
+        dist.all_gather_object(out, obj)
+        return out
+
     def close(self) -> None:
         if self.world > 1:
             import torch.distributed as dist
@@ -79,21 +88,33 @@ class RankGroup:
                 dist.destroy_process_group()
 
 
+def node_leader(group: RankGroup) -> int:
+    """Global rank of the first process on this rank's node (torchrun numbers
+    ranks node by node, so it is global rank - local rank)."""
+    return group.rank - group.local
+
+
 def distribute_store(group: RankGroup, api, dev, blob: bytes | None, mode: str = "host"):
     """Returns this rank's device-resident copy of the store.
 
     mode "host": each rank uploads `blob` itself (blob must be given on every rank).
-    mode "ipc":  rank 0 uploads and exports; the others import over NVLink.
+    mode "ipc":  local rank 0 of every node uploads and exports; the other ranks of
+                 that node import it over NVLink (CUDA IPC handles are node-local).
     """
     if mode == "host" or group.world == 1:
         return api.store_upload(dev, blob)
-    if group.rank == 0:
+    leader = node_leader(group)
+    if group.rank == leader:
         store = api.store_upload(dev, blob)
         handle = api.store_export(store)
     else:
         store, handle = None, None
-    handle = group.broadcast_object(handle, src=0)
-    if group.rank != 0:
-        store = api.store_import(dev, handle)
-    group.barrier()  # every peer has finished pulling before rank 0 may free
+    handles = group.all_gather_object((leader, handle) if group.rank == leader else None)
+    if group.rank != leader:
+        mine = [h for h in handles if h is not None and h[0] == leader]
+        if not mine:  # no exporter on this node: fall back to a host upload
+            store = api.store_upload(dev, blob)
+        else:
+            store = api.store_import(dev, mine[0][1])
+    group.barrier()  # every peer has finished pulling before a leader may free
     return store

@@ -82,3 +82,60 @@ def test_tp_rank_mapping():
     from paper_2604_06664_b200.multirank import tp_rank
 
     assert [tp_rank(r) for r in range(10)] == [0, 1, 2, 3, 4, 5, 6, 7, 0, 1]
+
+
+class _FakeApi:
+    """Records the store calls distribute_store makes (no GPU)."""
+
+    def __init__(self, rank):
+        self.rank, self.calls = rank, []
+
+    def store_upload(self, dev, blob):
+        self.calls.append(("upload", len(blob)))
+        return ("store", self.rank)
+
+    def store_export(self, store):
+        self.calls.append(("export",))
+        return "handle-of-%d" % self.rank
+
+    def store_import(self, dev, handle):
+        self.calls.append(("import", handle))
+        return ("imported", handle)
+
+
+def _fanout_worker(rank: int, world: int, local: int, port: int, queue) -> None:
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(local))
+    sys.path.insert(0, ROOT)
+    try:
+        from paper_2604_06664_b200.multirank import RankGroup, distribute_store
+
+        g = RankGroup.from_env()
+        g.init("gloo")
+        api = _FakeApi(rank)
+        distribute_store(g, api, None, b"x" * 64, "ipc")
+        queue.put((rank, api.calls))
+        g.close()
+    except Exception as exc:
+        queue.put((rank, repr(exc)))
+
+
+def test_ipc_fanout_has_one_exporter_per_node():
+    """Two 'nodes' of two ranks each (world 4, local ranks 0,1,0,1): each node's
+    local rank 0 uploads and exports; its peer imports that node's handle
+    (CUDA IPC handles do not cross nodes)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fanout_worker, args=(r, 4, r % 2, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert got[0] == [("upload", 64), ("export",)], got
+    assert got[2] == [("upload", 64), ("export",)], got
+    assert got[1] == [("import", "handle-of-0")], got
+    assert got[3] == [("import", "handle-of-2")], got
