@@ -390,12 +390,11 @@ def main():
     # rank runs on cuda:0 and the plumbing goes over gloo (NCCL refuses two
     # ranks on one device). The driver's runs never set it.
     shared = os.environ.get("FOUNDRY_BENCH_SHARED_GPU") == "1"
-    if shared:
-        local = 0
+    gpu = 0 if shared else local  # the device this rank drives; `local` still names the node-local rank
     # cold start as the paper measures it (N=1, before this process touches CUDA,
     # so no other context shares the GPU): fresh `foundry load` processes
-    cold = cold_process_load(args, local) if gworld == 1 and not args.skip_load else {}
-    torch.cuda.set_device(local)
+    cold = cold_process_load(args, gpu) if gworld == 1 and not args.skip_load else {}
+    torch.cuda.set_device(gpu)
     group = RankGroup(grank, gworld, local)
     group.init("gloo" if shared else "nccl")
     barrier, reduce_max = group.barrier, group.max
@@ -412,7 +411,7 @@ def main():
 
     # ---------------- device-resident materialization (value) ----------------
     api = capi.CApi()
-    dev = api.device_open(local)
+    dev = api.device_open(gpu)
     t_fan = time.perf_counter()
     store = distribute_store(group, api, dev, blob, args.fanout)  # the one exchange step
     fanout_ms = (time.perf_counter() - t_fan) * 1e3
@@ -430,7 +429,7 @@ def main():
     for _ in range(args.warmup):
         flush_l2()
         api.materialize(dev, store, wrank, TP_WORLD, base + delta, members)
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(gpu)
     with sampler:
         barrier()
         torch.cuda.synchronize()

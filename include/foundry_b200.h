@@ -170,6 +170,10 @@ typedef struct {
     int32_t extra_prewindow_alloc;
     int32_t share_execs;     /* B200: one instantiated exec per graph shape (LoadOptions.share_execs) */
     int32_t device_updates;  /* B200: serve applies kernel-node parameters from the GPU (LoadOptions.device_updates) */
+    /* B200: this rank's value table for the archive's comm slots (comm_slots.bin:
+     * comm handles, peer buffer addresses; LoadOptions.comm_values) */
+    const uint64_t* comm_values;
+    uint32_t n_comm_values;
 } fdy_load_options;
 
 void fdy_load_options_init(fdy_load_options* opts);

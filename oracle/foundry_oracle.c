@@ -16,6 +16,11 @@
  *   relocation rule ...... SURVEY.md §8(c) (no reference function; anchors det_alloc.cpp:152,
  *                          pipeline.cpp:434, range = manifest allocator.base + final_offset,
  *                          pipeline.hpp:38-39)
+ *   comm slots ........... B200 extension, no reference function (the stub layer authors
+ *                          the stub argument layout, rank_forge.cpp:18-22, and its patch
+ *                          entries, :132-152; slot format and rule: archive.hpp CommSlot).
+ *                          Pinned by property: the output equals ref_tool prepare's except
+ *                          at exactly the slot bytes, which hold the rank's values.
  */
 #define _GNU_SOURCE
 #include "foundry_oracle.h"
@@ -203,6 +208,83 @@ static void free_patch(patch_table_t* t) {
 }
 
 static const patch_graph_t* patch_for(const patch_table_t* t, uint32_t label) {
+    for (uint32_t g = 0; g < t->n_graphs; ++g)
+        if (t->graphs[g].label == label) return &t->graphs[g];
+    return NULL;
+}
+
+/* ----------------------------------------------------------- comm slots */
+
+typedef struct {
+    uint32_t node_id, offset, value_index;
+    uint8_t width;
+} slot_t;
+
+typedef struct {
+    uint32_t label, count;
+    slot_t* slots;
+} slot_graph_t;
+
+typedef struct {
+    uint32_t n_values, n_graphs;
+    slot_graph_t* graphs;
+} slot_table_t;
+
+/* "FNDS" u16 version=1 u32 n_values u32 n_graphs, per graph u32 label u32 count,
+ * per slot u32 node_id u32 offset u32 value_index u8 width (archive.hpp). */
+static int parse_slots(const uint8_t* p, size_t n, slot_table_t* t, err_t* e) {
+    memset(t, 0, sizeof *t);
+    if (n == 0) return 0; /* no comm_slots.bin */
+    rd_t r = {p, n, 0, 0};
+    const uint8_t* magic = rd_bytes(&r, 4);
+    if (!magic || memcmp(magic, "FNDS", 4) != 0)
+        return fail(e, FO_ARCHIVE_CORRUPTION, "archive-corruption: bad magic, expected 'FNDS'");
+    uint16_t ver = rd_u16(&r);
+    if (!r.err && ver != 1)
+        return fail(e, FO_ARCHIVE_CORRUPTION, "archive-corruption: unsupported comm slot table version %u", ver);
+    t->n_values = rd_u32(&r);
+    t->n_graphs = rd_u32(&r);
+    if (r.err) return fail(e, FO_ARCHIVE_CORRUPTION, "archive-corruption: truncated input");
+    if ((uint64_t)t->n_graphs * 8 > n) return fail(e, FO_ARCHIVE_CORRUPTION, "archive-corruption: truncated input");
+    t->graphs = (slot_graph_t*)calloc(t->n_graphs ? t->n_graphs : 1, sizeof(slot_graph_t));
+    for (uint32_t g = 0; g < t->n_graphs && !r.err; ++g) {
+        slot_graph_t* sg = &t->graphs[g];
+        sg->label = rd_u32(&r);
+        sg->count = rd_u32(&r);
+        if (r.err || (uint64_t)sg->count * 13 > n) { r.err = 1; break; }
+        sg->slots = (slot_t*)calloc(sg->count ? sg->count : 1, sizeof(slot_t));
+        for (uint32_t i = 0; i < sg->count && !r.err; ++i) {
+            slot_t* s = &sg->slots[i];
+            s->node_id = rd_u32(&r);
+            s->offset = rd_u32(&r);
+            s->value_index = rd_u32(&r);
+            s->width = rd_u8(&r);
+            if (r.err) break;
+            if (s->width < 1 || s->width > 8)
+                return fail(e, FO_ARCHIVE_CORRUPTION, "archive-corruption: comm slot width %u is not 1..8", s->width);
+            if (s->value_index >= t->n_values)
+                return fail(e, FO_ARCHIVE_CORRUPTION,
+                            "archive-corruption: comm slot value index %u is outside the %u-entry value table",
+                            s->value_index, t->n_values);
+        }
+        for (uint32_t h = 0; h < g && !r.err; ++h)
+            if (t->graphs[h].label == sg->label)
+                return fail(e, FO_ARCHIVE_CORRUPTION, "archive-corruption: comm slot table lists label %u twice",
+                            sg->label);
+    }
+    if (r.err) return fail(e, FO_ARCHIVE_CORRUPTION, "archive-corruption: truncated input");
+    if (r.pos != r.n) return fail(e, FO_ARCHIVE_CORRUPTION, "archive-corruption: trailing bytes in comm slot table");
+    return 0;
+}
+
+static void free_slots(slot_table_t* t) {
+    if (!t->graphs) return;
+    for (uint32_t g = 0; g < t->n_graphs; ++g) free(t->graphs[g].slots);
+    free(t->graphs);
+    t->graphs = NULL;
+}
+
+static const slot_graph_t* slots_for(const slot_table_t* t, uint32_t label) {
     for (uint32_t g = 0; g < t->n_graphs; ++g)
         if (t->graphs[g].label == label) return &t->graphs[g];
     return NULL;
@@ -411,6 +493,29 @@ static int rank_patch(graph_t* g, const patch_graph_t* pg, uint64_t real_hash, u
     return 0;
 }
 
+/* Comm slot writes of one (already rank-patched) graph, in table order: only
+ * nodes the graph's patch entries name; little-endian low `width` bytes. */
+static int apply_slots(graph_t* g, const slot_graph_t* sg, const patch_graph_t* pg, const uint64_t* values,
+                       uint32_t n_values, err_t* e) {
+    for (uint32_t i = 0; i < sg->count; ++i) {
+        const slot_t* s = &sg->slots[i];
+        int stub = 0;
+        for (uint32_t k = 0; pg && k < pg->count; ++k) stub |= pg->entries[k].node_id == s->node_id;
+        if (!stub || s->node_id >= g->n_nodes || g->nodes[s->node_id].type != NT_KERNEL)
+            return fail(e, FO_ARCHIVE_CORRUPTION,
+                        "archive-corruption: comm slot references node %u, which is not a patched comm node",
+                        s->node_id);
+        node_t* nd = &g->nodes[s->node_id];
+        if ((uint64_t)s->offset + s->width > nd->arg_len)
+            return fail(e, FO_INVALID_ARGUMENT, "invalid-argument: comm slot offset outside the argument buffer");
+        if (s->value_index >= n_values)
+            return fail(e, FO_INVALID_ARGUMENT, "invalid-argument: comm slot value index %u has no value",
+                        s->value_index);
+        for (uint32_t b = 0; b < s->width; ++b) nd->args[s->offset + b] = (uint8_t)(values[s->value_index] >> (8 * b));
+    }
+    return 0;
+}
+
 /* ------------------------------------------------------- container walk */
 
 typedef struct {
@@ -464,6 +569,9 @@ typedef struct {
     const loc_t* locs;
     uint32_t count;
     const patch_table_t* patch;
+    const slot_table_t* slots;
+    const uint64_t* values;
+    uint32_t n_values;
     uint64_t real_hash, lo, span, delta;
     uint32_t rank, world;
     wr_t* records;       /* per member encoded record */
@@ -493,6 +601,8 @@ static void do_member(job_t* j, uint32_t i) {
     j->relocated[i] = relocate(&g, j->lo, j->span, j->delta);
     const patch_graph_t* pg = patch_for(j->patch, loc->label);
     if (pg && rank_patch(&g, pg, j->real_hash, j->rank, j->world, e)) { free_graph(&g); return; }
+    const slot_graph_t* sg = slots_for(j->slots, loc->label);
+    if (sg && apply_slots(&g, sg, pg, j->values, j->n_values, e)) { free_graph(&g); return; }
     encode_record(&g, &j->records[i]);
     free_graph(&g);
 }
@@ -515,8 +625,22 @@ int fo_materialize_container(const uint8_t* graphs, size_t graphs_len,
                              uint64_t old_base, uint64_t final_offset, uint64_t new_base,
                              unsigned lanes, uint8_t** out, size_t* out_len,
                              uint64_t* n_relocated, char* err_msg, size_t err_cap) {
+    return fo_materialize_container_ex(graphs, graphs_len, patch, patch_len, NULL, 0, NULL, 0, real_comm_hash,
+                                       rank, world, old_base, final_offset, new_base, lanes, out, out_len,
+                                       n_relocated, err_msg, err_cap);
+}
+
+int fo_materialize_container_ex(const uint8_t* graphs, size_t graphs_len,
+                                const uint8_t* patch, size_t patch_len,
+                                const uint8_t* slots, size_t slots_len,
+                                const uint64_t* values, uint32_t n_values,
+                                uint64_t real_comm_hash, uint32_t rank, uint32_t world,
+                                uint64_t old_base, uint64_t final_offset, uint64_t new_base,
+                                unsigned lanes, uint8_t** out, size_t* out_len,
+                                uint64_t* n_relocated, char* err_msg, size_t err_cap) {
     err_t e = {0, {0}};
     patch_table_t pt = {0, NULL};
+    slot_table_t stab = {0, 0, NULL};
     loc_t* locs = NULL;
     uint32_t count = 0;
     int rc = 0;
@@ -528,6 +652,20 @@ int fo_materialize_container(const uint8_t* graphs, size_t graphs_len,
         goto done;
     }
     if ((rc = parse_patch(patch, patch_len, &pt, &e))) goto done;
+    if ((rc = parse_slots(slots, slots_len, &stab, &e))) goto done;
+    for (uint32_t g = 0; g < stab.n_graphs; ++g)
+        if (!patch_for(&pt, stab.graphs[g].label)) {
+            rc = fail(&e, FO_ARCHIVE_CORRUPTION,
+                      "archive-corruption: comm slot table lists graph %u, which has no comm patches",
+                      stab.graphs[g].label);
+            goto done;
+        }
+    if (stab.n_graphs && n_values < stab.n_values) {
+        rc = fail(&e, FO_INVALID_ARGUMENT,
+                  "invalid-argument: the archive's comm slots read %u per-rank values, %u given", stab.n_values,
+                  n_values);
+        goto done;
+    }
     if (pt.n_graphs > 0 && real_comm_hash == 0) {
         /* instantiate_rank rank_forge.cpp:162-163 */
         rc = fail(&e, FO_UNRESOLVED_KERNEL,
@@ -542,6 +680,9 @@ int fo_materialize_container(const uint8_t* graphs, size_t graphs_len,
     j.locs = locs;
     j.count = count;
     j.patch = &pt;
+    j.slots = &stab;
+    j.values = values;
+    j.n_values = n_values;
     j.real_hash = real_comm_hash;
     j.lo = old_base;
     j.span = final_offset;
@@ -596,6 +737,7 @@ int fo_materialize_container(const uint8_t* graphs, size_t graphs_len,
 done:
     free(locs);
     free_patch(&pt);
+    free_slots(&stab);
     if (rc && err_msg && err_cap) snprintf(err_msg, err_cap, "%s", e.msg);
     return rc;
 }

@@ -63,6 +63,18 @@ int fo_materialize_container(const uint8_t* graphs, size_t graphs_len,
                              unsigned lanes, uint8_t** out, size_t* out_len,
                              uint64_t* n_relocated, char* err_msg, size_t err_cap);
 
+/* The same with the archive's comm slots (comm_slots.bin; slots/slots_len
+ * 0 = none) applied after apply_rank_patches from the rank's value table
+ * (values[n_values]). Slot rule: archive.hpp CommSlot. */
+int fo_materialize_container_ex(const uint8_t* graphs, size_t graphs_len,
+                                const uint8_t* patch, size_t patch_len,
+                                const uint8_t* slots, size_t slots_len,
+                                const uint64_t* values, uint32_t n_values,
+                                uint64_t real_comm_hash, uint32_t rank, uint32_t world,
+                                uint64_t old_base, uint64_t final_offset, uint64_t new_base,
+                                unsigned lanes, uint8_t** out, size_t* out_len,
+                                uint64_t* n_relocated, char* err_msg, size_t err_cap);
+
 void fo_free(void* p);
 
 #ifdef __cplusplus

@@ -33,6 +33,7 @@ try:
         spec_text,
         unpack_archive,
         workload_from_text,
+        write_comm_slots,
     )
 except ImportError as exc:  # pragma: no cover - exercised only on a broken build
     raise ImportError(
@@ -70,5 +71,6 @@ __all__ = [
     "spec_text",
     "workload_from_text",
     "workload_path",
+    "write_comm_slots",
     "LIBRARY_PATH",
 ]

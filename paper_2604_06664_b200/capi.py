@@ -40,6 +40,8 @@ class LoadOptions(ctypes.Structure):
         ("extra_prewindow_alloc", ctypes.c_int32),
         ("share_execs", ctypes.c_int32),
         ("device_updates", ctypes.c_int32),
+        ("comm_values", ctypes.POINTER(ctypes.c_uint64)),
+        ("n_comm_values", ctypes.c_uint32),
     ]
 
 
@@ -127,10 +129,12 @@ class CApi:
 
     # ---- session layer (the reference's LOAD surface)
     def load(self, archive: str, rank: int = 0, world: int = 1, relocate: bool = False,
-             share_execs: bool = False):
+             share_execs: bool = False, comm_values=()):
         o = LoadOptions()
         self.lib.fdy_load_options_init(ctypes.byref(o))
         o.rank, o.world, o.relocate, o.share_execs = rank, world, int(relocate), int(share_execs)
+        vals = (ctypes.c_uint64 * max(1, len(comm_values)))(*comm_values)
+        o.comm_values, o.n_comm_values = vals, len(comm_values)
         h = ctypes.c_void_p()
         self.check(self.lib.fdy_load(archive.encode(), ctypes.byref(o), ctypes.byref(h)))
         return h
@@ -172,13 +176,19 @@ class CApi:
         self.check(self.lib.fdy_store_import(dev, handle, nbytes, ctypes.byref(h)))
         return h
 
-    def materialize(self, dev, store, rank: int, world: int, new_base: int = 0, members=None,
-                    values=()):
+    @staticmethod
+    def _desc(rank: int, world: int, new_base: int, values=()):
         desc = MaterializeDesc(rank, world, new_base, None, 0, 0)
         if values:
             arr = (ctypes.c_uint64 * len(values))(*values)
             desc.values = arr
             desc.n_values = len(values)
+            desc._keep = arr  # the table must outlive the call
+        return desc
+
+    def materialize(self, dev, store, rank: int, world: int, new_base: int = 0, members=None,
+                    values=()):
+        desc = self._desc(rank, world, new_base, values)
         ms = ctypes.c_float()
         if members is None:
             members = ctypes.c_void_p()
@@ -189,18 +199,18 @@ class CApi:
                                                      ctypes.byref(ms)))
         return members, ms.value
 
-    def materialize_split(self, dev, store, rank: int, world: int, new_base: int, members):
+    def materialize_split(self, dev, store, rank: int, world: int, new_base: int, members, values=()):
         """(relocation ms, member-pass ms): the two grids timed apart."""
-        desc = MaterializeDesc(rank, world, new_base, None, 0, 0)
+        desc = self._desc(rank, world, new_base, values)
         r, m = ctypes.c_float(), ctypes.c_float()
         self.check(self.lib.fdy_materialize_timed_split(dev, store, ctypes.byref(desc), members,
                                                         ctypes.byref(r), ctypes.byref(m)))
         return r.value, m.value
 
     def prepare_archive(self, dev, archive: str, rank: int, world: int, new_base: int = 0,
-                        lanes: int = 0, host_out=None, cap: int = 0) -> dict:
+                        lanes: int = 0, host_out=None, cap: int = 0, values=()) -> dict:
         """The materialization path in one C-ABI call (fdy_prepare_archive)."""
-        desc = MaterializeDesc(rank, world, new_base, None, 0, 0)
+        desc = self._desc(rank, world, new_base, values)
         n = ctypes.c_size_t()
         t = PrepareTimings()
         self.check(self.lib.fdy_prepare_archive(dev, archive.encode(), ctypes.byref(desc),
@@ -241,13 +251,15 @@ def store_header(blob: bytes) -> dict:
      n_diffs, n_rank_ops) = struct.unpack_from("<4sHHIIIIIIII", blob, 0)
     assert magic == b"FNDT", "not a template store"
     u64 = struct.unpack_from("<7Q", blob, 40)
-    secs = struct.unpack_from("<%dQ" % (2 * len(SECTIONS)), blob, 96)
+    n_plain, n_values, slots_crc = struct.unpack_from("<IIQ", blob, 96)
+    secs = struct.unpack_from("<%dQ" % (2 * len(SECTIONS)), blob, 112)
     return {
         "version": version, "n_groups": n_groups, "n_members": n_members, "n_kernels": n_kernels,
         "n_tiles": n_tiles, "tile_chunks": tile_chunks, "n_diffs": n_diffs, "n_rank_ops": n_rank_ops,
         "source_graphs_crc": u64[0], "source_patch_crc": u64[1], "old_base": u64[2],
         "final_offset": u64[3], "real_comm_hash": u64[4], "members_image_bytes": u64[5],
-        "total_nodes": u64[6],
+        "total_nodes": u64[6], "n_plain_tiles": n_plain, "n_values": n_values,
+        "source_slots_crc": slots_crc,
         "sec": {n: (secs[2 * i], secs[2 * i + 1]) for i, n in enumerate(SECTIONS)},
     }
 

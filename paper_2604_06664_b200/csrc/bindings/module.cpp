@@ -146,7 +146,8 @@ SaveOutcome do_save(const WorkloadSpec& spec, const std::string& out, bool emit_
 ServingHandle do_load(const std::string& archive, uint32_t rank, uint32_t world, bool preallocate,
                       int device, bool relocate, unsigned prepare_lanes, bool skip_binary_restore,
                       bool skip_device_init, int64_t base_shift_granules, bool extra_prewindow_alloc,
-                      bool verify_replay, bool share_execs, bool device_updates) {
+                      bool verify_replay, bool share_execs, bool device_updates,
+                      std::vector<uint64_t> comm_values) {
     LoadOptions o;
     o.rank = rank;
     o.world = world;
@@ -157,6 +158,7 @@ ServingHandle do_load(const std::string& archive, uint32_t rank, uint32_t world,
     o.verify_replay = verify_replay;
     o.share_execs = share_execs;
     o.device_updates = device_updates;
+    o.comm_values = std::move(comm_values);
     o.faults.skip_binary_restore = skip_binary_restore;
     o.faults.skip_device_init = skip_device_init;
     o.faults.base_shift_granules = base_shift_granules;
@@ -229,7 +231,20 @@ PYBIND11_MODULE(_foundry, m) {
           py::arg("prepare_lanes") = 4, py::arg("skip_binary_restore") = false,
           py::arg("skip_device_init") = false, py::arg("base_shift_granules") = 0,
           py::arg("extra_prewindow_alloc") = false, py::arg("verify_replay") = true,
-          py::arg("share_execs") = false, py::arg("device_updates") = false);
+          py::arg("share_execs") = false, py::arg("device_updates") = false,
+          py::arg("comm_values") = std::vector<uint64_t>{});
+    // The stub layer's comm-slot authoring (archive.hpp CommSlotTable): writes
+    // comm_slots.bin, records its digest in the manifest and re-packs the
+    // template store if the archive has one.
+    m.def("write_comm_slots", [](const std::string& archive, uint32_t n_values,
+                                 const std::map<uint32_t, std::vector<std::tuple<uint32_t, uint32_t, uint32_t, uint8_t>>>& slots) {
+        CommSlotTable t;
+        t.n_values = n_values;
+        for (const auto& [label, list] : slots)
+            for (const auto& [node, off, idx, width] : list) t.per_graph[label].push_back(CommSlot{node, off, idx, width});
+        py::gil_scoped_release nogil;
+        write_comm_slots(archive, t);
+    }, py::arg("archive"), py::arg("n_values"), py::arg("slots"));
     m.def("pack", [](const std::string& archive) {
         py::gil_scoped_release nogil;
         pack_archive(archive);

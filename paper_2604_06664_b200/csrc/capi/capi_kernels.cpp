@@ -24,7 +24,6 @@ struct fdy_store {
 struct fdy_members {
     fdy_device* owner = nullptr;
     DeviceBuffer out;
-    DeviceBuffer values;
 };
 
 extern "C" {
@@ -134,27 +133,27 @@ size_t fdy_store_members_bytes(const fdy_store* store) {
     return store ? store->store.header.members_image_bytes : 0;
 }
 
-static void materialize_into(fdy_device* dev, const fdy_store* store,
-                             const fdy_materialize_desc* desc, fdy_members* m, float* kernel_ms) {
-    require(dev && store && desc && m, Errc::invalid_argument, "fdy_materialize: null argument");
-    require(store->owner == dev, Errc::invalid_argument, "fdy_materialize: store lives on another device");
+// The request a descriptor describes; the value table (FDT_ROP_VALUE ops) is
+// part of it on every entry point.
+static MaterializeRequest request_of(const fdy_materialize_desc* desc) {
     MaterializeRequest req;
     req.rank = desc->rank;
     req.world = desc->world;
     req.new_base = desc->new_base;
-    const uint64_t* d_values = nullptr;
     if (desc->n_values) {
         require(desc->values != nullptr, Errc::invalid_argument, "fdy_materialize: null value table");
         req.values.assign(desc->values, desc->values + desc->n_values);
-        if (m->values.size() < desc->n_values * 8) m->values = DeviceBuffer(*dev->dev, desc->n_values * 8);
-        cuda_check(cudaMemcpyAsync(m->values.data(), desc->values, desc->n_values * 8,
-                                   cudaMemcpyHostToDevice, dev->dev->stream()),
-                   "cudaMemcpyAsync(value table)");
-        d_values = reinterpret_cast<const uint64_t*>(m->values.data());
     }
+    return req;
+}
+
+static void materialize_into(fdy_device* dev, const fdy_store* store,
+                             const fdy_materialize_desc* desc, fdy_members* m, float* kernel_ms) {
+    require(dev && store && desc && m, Errc::invalid_argument, "fdy_materialize: null argument");
+    require(store->owner == dev, Errc::invalid_argument, "fdy_materialize: store lives on another device");
+    const MaterializeRequest req = request_of(desc);
     MaterializeTiming t;
-    launch_materialize(*dev->dev, store->store, req, m->out.data(), kernel_ms ? &t : nullptr,
-                       desc->grid, d_values);
+    launch_materialize(*dev->dev, store->store, req, m->out.data(), kernel_ms ? &t : nullptr, desc->grid);
     if (kernel_ms) *kernel_ms = t.kernel_ms;
 }
 
@@ -187,13 +186,10 @@ int fdy_materialize_timed_split(fdy_device* dev, const fdy_store* store, const f
         require(store->owner == dev, Errc::invalid_argument, "fdy_materialize: store lives on another device");
         require(m->out.size() >= store->store.header.members_image_bytes, Errc::invalid_argument,
                 "fdy_materialize_timed_split: arena too small for this store");
-        MaterializeRequest req;
-        req.rank = desc->rank;
-        req.world = desc->world;
-        req.new_base = desc->new_base;
+        const MaterializeRequest req = request_of(desc);
         MaterializeTiming t;
         t.split = true;
-        launch_materialize(*dev->dev, store->store, req, m->out.data(), &t, desc->grid, nullptr);
+        launch_materialize(*dev->dev, store->store, req, m->out.data(), &t, desc->grid);
         if (reloc_ms) *reloc_ms = t.reloc_ms;
         if (member_ms) *member_ms = t.member_ms;
     });
@@ -223,8 +219,8 @@ int fdy_prepare_archive(fdy_device* dev, const char* archive, const fdy_material
     return fdy_guard([&] {
         require(dev && archive && desc, Errc::invalid_argument, "fdy_prepare_archive: null argument");
         ArchiveMaterializeTimings t;
-        const uint64_t n = materialize_archive(*dev->dev, archive, desc->rank, desc->world,
-                                               desc->new_base, lanes ? lanes : 4, host_out, cap, &t);
+        const MaterializeRequest req = request_of(desc);
+        const uint64_t n = materialize_archive(*dev->dev, archive, req, lanes ? lanes : 4, host_out, cap, &t);
         if (out_len) *out_len = n;
         if (timings) {
             timings->total_ms = t.total_ms;

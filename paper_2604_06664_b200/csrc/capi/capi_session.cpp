@@ -54,6 +54,10 @@ int fdy_load(const char* archive, const fdy_load_options* o, fdy_serving** out) 
             opts.faults.extra_prewindow_alloc = o->extra_prewindow_alloc != 0;
             opts.share_execs = o->share_execs != 0;
             opts.device_updates = o->device_updates != 0;
+            if (o->n_comm_values) {
+                require(o->comm_values != nullptr, Errc::invalid_argument, "fdy_load: null comm_values");
+                opts.comm_values.assign(o->comm_values, o->comm_values + o->n_comm_values);
+            }
         }
         *out = new fdy_serving(load(archive, opts));
     });

@@ -724,4 +724,75 @@ void apply_rank_patches(CapturedGraph& graph, std::span<const CommPatchEntry> en
     }
 }
 
+// ------------------------------------------------------------------ comm slots
+
+std::vector<uint8_t> serialize_comm_slots(const CommSlotTable& t) {
+    Sink s;
+    s.raw("FNDS", 4);
+    s.u16(1);
+    s.u32(t.n_values);
+    s.u32(static_cast<uint32_t>(t.per_graph.size()));
+    for (const auto& [label, slots] : t.per_graph) {
+        s.u32(label);
+        s.u32(static_cast<uint32_t>(slots.size()));
+        for (const CommSlot& c : slots) {
+            s.u32(c.node_id);
+            s.u32(c.offset);
+            s.u32(c.value_index);
+            s.u8(c.width);
+        }
+    }
+    return s.release();
+}
+
+CommSlotTable parse_comm_slots(std::span<const uint8_t> bytes) {
+    Cursor c(bytes, Errc::archive_corruption);
+    c.magic("FNDS");
+    const uint16_t version = c.u16();
+    require(version == 1, Errc::archive_corruption, "unsupported comm slot table version " + std::to_string(version));
+    CommSlotTable t;
+    t.n_values = c.u32();
+    const uint32_t graphs = c.u32();
+    for (uint32_t g = 0; g < graphs; ++g) {
+        const uint32_t label = c.u32();
+        const uint32_t count = c.u32();
+        std::vector<CommSlot> slots;
+        for (uint32_t i = 0; i < count; ++i) {  // one at a time: a short table is a cursor overrun
+            CommSlot s;
+            s.node_id = c.u32();
+            s.offset = c.u32();
+            s.value_index = c.u32();
+            s.width = c.u8();
+            require(s.width >= 1 && s.width <= 8, Errc::archive_corruption,
+                    "comm slot width " + std::to_string(s.width) + " is not 1..8");
+            require(s.value_index < t.n_values, Errc::archive_corruption,
+                    "comm slot value index " + std::to_string(s.value_index) + " is outside the " +
+                        std::to_string(t.n_values) + "-entry value table");
+            slots.push_back(s);
+        }
+        require(t.per_graph.emplace(label, std::move(slots)).second, Errc::archive_corruption,
+                "comm slot table lists label " + std::to_string(label) + " twice");
+    }
+    require(c.at_end(), Errc::archive_corruption, "trailing bytes in comm slot table");
+    return t;
+}
+
+void apply_comm_slots(CapturedGraph& graph, std::span<const CommSlot> slots,
+                      std::span<const CommPatchEntry> patches, std::span<const uint64_t> values) {
+    for (const CommSlot& s : slots) {
+        bool stub = false;
+        for (const auto& e : patches) stub = stub || e.node_id == s.node_id;
+        require(stub && s.node_id < graph.nodes.size() && graph.nodes[s.node_id].type == NodeType::Kernel,
+                Errc::archive_corruption,
+                "comm slot references node " + std::to_string(s.node_id) + ", which is not a patched comm node");
+        auto& args = graph.nodes[s.node_id].kernel_params().arg_buffer;
+        require(uint64_t(s.offset) + s.width <= args.size(), Errc::invalid_argument,
+                "comm slot offset outside the argument buffer");
+        require(s.value_index < values.size(), Errc::invalid_argument,
+                "comm slot value index " + std::to_string(s.value_index) + " has no value");
+        const uint64_t v = values[s.value_index];
+        std::memcpy(args.data() + s.offset, &v, s.width);
+    }
+}
+
 }  // namespace foundry

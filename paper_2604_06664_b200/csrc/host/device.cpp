@@ -154,8 +154,7 @@ PinnedBuffer& PinnedBuffer::operator=(PinnedBuffer&& o) noexcept {
 
 // ------------------------------------------------------------------ stores
 
-DeviceStore adopt_store(Device& dev, const unsigned char* d_blob, size_t bytes,
-                        const fdt_header& h, const void* host_blob) {
+DeviceStore adopt_store(Device& dev, const unsigned char* d_blob, size_t bytes, const fdt_header& h) {
     require(bytes >= sizeof(fdt_header) && std::memcmp(h.magic, "FNDT", 4) == 0,
             Errc::archive_corruption, "template store: bad magic, expected 'FNDT'");
     require(h.version == FDT_VERSION, Errc::archive_corruption,
@@ -171,31 +170,8 @@ DeviceStore adopt_store(Device& dev, const unsigned char* d_blob, size_t bytes,
     s.bytes = bytes;
     s.header = h;
     if (h.sec[FDT_SEC_TIMAGES].bytes) s.rtimages = DeviceBuffer(dev, h.sec[FDT_SEC_TIMAGES].bytes);
-    if (host_blob != nullptr && h.n_tiles != 0 &&
-        h.sec[FDT_SEC_TILES].bytes >= uint64_t(h.n_tiles) * sizeof(fdt_tile)) {
-        // tiles without a relocatable lane in their template chunks first
-        const auto* hb = static_cast<const unsigned char*>(host_blob);
-        const auto* tiles = reinterpret_cast<const fdt_tile*>(hb + h.sec[FDT_SEC_TILES].offset);
-        const unsigned char* cmeta = hb + h.sec[FDT_SEC_CMETA].offset;
-        const uint64_t tbase = h.sec[FDT_SEC_TIMAGES].offset, ncm = h.sec[FDT_SEC_CMETA].bytes;
-        std::vector<fdt_tile> plain, rest;
-        for (uint32_t i = 0; i < h.n_tiles; ++i) {
-            const fdt_tile& t = tiles[i];
-            const uint64_t c0 = (t.src_off - tbase) / 16;
-            bool reloc = t.src_off < tbase || c0 + t.nchunks > ncm;  // malformed: keep it behind the wait
-            for (uint64_t c = c0; !reloc && c < c0 + t.nchunks; ++c) reloc = cmeta[c] != 0;
-            (reloc ? rest : plain).push_back(t);
-        }
-        if (!plain.empty() && !rest.empty()) {
-            plain.insert(plain.end(), rest.begin(), rest.end());
-            s.planned_tiles = DeviceBuffer(dev, plain.size() * sizeof(fdt_tile));
-            cuda_check(cudaMemcpyAsync(s.planned_tiles.data(), plain.data(), plain.size() * sizeof(fdt_tile),
-                                       cudaMemcpyHostToDevice, dev.stream()),
-                       "cudaMemcpyAsync(tile plan H2D)");
-            cuda_check(cudaStreamSynchronize(dev.stream()), "cudaStreamSynchronize(tile plan)");
-            s.n_plain_tiles = static_cast<uint32_t>(h.n_tiles - rest.size());
-        }
-    }
+    require(h.n_plain_tiles <= h.n_tiles, Errc::archive_corruption,
+            "template store: more relocation-free tiles than tiles");
     return s;
 }
 
@@ -206,18 +182,41 @@ DeviceStore upload_store(Device& dev, const void* host_blob, size_t bytes) {
     DeviceBuffer buf(dev, bytes, /*shareable=*/true);  // fdy_store_export may hand it to peers
     cuda_check(cudaMemcpyAsync(buf.data(), host_blob, bytes, cudaMemcpyHostToDevice, dev.stream()),
                "cudaMemcpyAsync(store H2D)");
-    DeviceStore s = adopt_store(dev, buf.data(), bytes, h, host_blob);
+    DeviceStore s = adopt_store(dev, buf.data(), bytes, h);
     s.blob = std::move(buf);
     return s;
 }
 
+void check_store_sources(const fdt_header& h, const Manifest& manifest) {
+    const auto slots = manifest.file_digests.find("comm_slots.bin");
+    require(h.source_graphs_crc == manifest.file_digests.at("graphs.bin") &&
+                h.source_patch_crc == manifest.file_digests.at("patch.bin"),
+            Errc::archive_corruption, "template store was packed from a different graphs.bin/patch.bin");
+    require(h.source_slots_crc == (slots == manifest.file_digests.end() ? 0ull : slots->second),
+            Errc::archive_corruption, "template store was packed from a different comm_slots.bin");
+    if (h.n_rank_ops > 0)
+        require(manifest.comm_real_hash != 0, Errc::unresolved_kernel,
+                "archive carries comm patches but no real comm binary");
+}
+
 void launch_materialize(Device& dev, const DeviceStore& store, const MaterializeRequest& req,
-                        unsigned char* out, MaterializeTiming* timing, int grid_override,
-                        const uint64_t* d_values) {
+                        unsigned char* out, MaterializeTiming* timing, int grid_override) {
     const fdt_header& h = store.header;
     require(req.world >= 1 && req.rank < req.world, Errc::invalid_argument,
             "rank " + std::to_string(req.rank) + " is outside world size " + std::to_string(req.world));
+    require(req.values.size() >= h.n_values, Errc::invalid_argument,
+            "the archive's comm slots read " + std::to_string(h.n_values) + " per-rank values, " +
+                std::to_string(req.values.size()) + " given (LoadOptions::comm_values)");
     dev.make_current();
+    const uint64_t* d_values = nullptr;
+    if (!req.values.empty()) {
+        const size_t vb = req.values.size() * sizeof(uint64_t);
+        if (store.values.size() < vb) store.values = DeviceBuffer(dev, vb);
+        cuda_check(cudaMemcpyAsync(store.values.data(), req.values.data(), vb, cudaMemcpyHostToDevice,
+                                   dev.stream()),
+                   "cudaMemcpyAsync(value table)");
+        d_values = reinterpret_cast<const uint64_t*>(store.values.data());
+    }
     FdyMaterializeArgs a{};
     const unsigned char* b = store.data;
     a.store = b;
@@ -238,10 +237,7 @@ void launch_materialize(Device& dev, const DeviceStore& store, const Materialize
     a.rank = req.rank;
     a.world = req.world;
     a.n_tiles = h.n_tiles;
-    if (store.planned_tiles.data() != nullptr && a.delta != 0) {
-        a.tiles = reinterpret_cast<const fdt_tile*>(store.planned_tiles.data());
-        a.n_plain = store.n_plain_tiles;
-    }
+    a.n_plain = h.n_plain_tiles;  // the packer stored the relocation-free tiles first
     // the kernel reads template chunks at tsrc + tile.src_off (a store offset)
     a.tsrc = a.delta && a.rtimg ? reinterpret_cast<const unsigned char*>(
                                       reinterpret_cast<uintptr_t>(a.rtimg) - a.timage_base)

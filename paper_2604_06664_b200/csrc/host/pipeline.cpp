@@ -903,8 +903,9 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
                                I.view->header());
     } else {
         try {
-            I.inline_store = pack_template_store(I.file_host("graphs.bin"), I.file_host("patch.bin"),
-                                                 I.manifest, opts.prepare_lanes);
+            I.inline_store = pack_template_store(
+                I.file_host("graphs.bin"), I.file_host("patch.bin"), I.manifest, opts.prepare_lanes, nullptr,
+                I.staged->has("comm_slots.bin") ? I.file_host("comm_slots.bin") : std::span<const uint8_t>{});
         } catch (const Error&) {
             rethrow_in_step("template construction");
         }
@@ -914,12 +915,10 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
         I.t.h2d_bytes += I.inline_store.size();
     }
     const fdt_header& H = I.view->header();
-    require(H.source_graphs_crc == I.manifest.file_digests.at("graphs.bin") &&
-                H.source_patch_crc == I.manifest.file_digests.at("patch.bin"),
-            Errc::archive_corruption, "template store was packed from a different graphs.bin/patch.bin");
-    if (H.n_rank_ops > 0)
-        require(I.manifest.comm_real_hash != 0, Errc::unresolved_kernel,
-                "archive carries comm patches but no real comm binary");
+    check_store_sources(H, I.manifest);
+    require(opts.comm_values.size() >= H.n_values, Errc::invalid_argument,
+            "the archive's comm slots read " + std::to_string(H.n_values) + " per-rank values, " +
+                std::to_string(opts.comm_values.size()) + " given (LoadOptions::comm_values)");
 
     // 3. restore binaries (cuLibraryLoadData)
     t0 = Clock::now();
@@ -953,6 +952,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     MaterializeRequest req;
     req.rank = opts.rank;
     req.world = opts.world;
+    req.values = opts.comm_values;
     const uint64_t new_base = I.ctx->region_base();
     req.new_base = (opts.relocate && new_base != I.manifest.allocator.base) ? new_base : 0;
     I.t.relocation_delta = req.new_base ? req.new_base - I.manifest.allocator.base : 0;

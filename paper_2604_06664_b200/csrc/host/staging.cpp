@@ -480,24 +480,15 @@ struct Launched {
     uint64_t bytes = 0;
 };
 
-void launch_from_store(Device& dev, const Manifest& manifest, DeviceStore& store, uint32_t rank, uint32_t world,
-                       uint64_t new_base, void* host_out, uint64_t cap, Launched& L) {
+void launch_from_store(Device& dev, const Manifest& manifest, DeviceStore& store, const MaterializeRequest& req,
+                       void* host_out, uint64_t cap, Launched& L) {
     const fdt_header& H = store.header;
-    require(H.source_graphs_crc == manifest.file_digests.at("graphs.bin") &&
-                H.source_patch_crc == manifest.file_digests.at("patch.bin"),
-            Errc::archive_corruption, "template store was packed from a different graphs.bin/patch.bin");
-    if (H.n_rank_ops > 0)
-        require(manifest.comm_real_hash != 0, Errc::unresolved_kernel,
-                "archive carries comm patches but no real comm binary");
+    check_store_sources(H, manifest);
     if (host_out)
         require(cap >= H.members_image_bytes, Errc::invalid_argument,
                 "output buffer holds " + std::to_string(cap) + " bytes, the member images need " +
                     std::to_string(H.members_image_bytes));
     L.out = DeviceBuffer(dev, std::max<uint64_t>(H.members_image_bytes, 16));
-    MaterializeRequest req;
-    req.rank = rank;
-    req.world = world;
-    req.new_base = new_base;
     L.mt.gate = false;  // part of a pipeline: no stream hold for the events
     launch_materialize(dev, store, req, L.out.data(), &L.mt);
     L.t2 = Clock::now();
@@ -515,7 +506,7 @@ void launch_from_store(Device& dev, const Manifest& manifest, DeviceStore& store
 static uint64_t materialize_archive_early(Device& dev, const fs::path& root, const Manifest& manifest,
                                           std::unique_ptr<StagedArchive> early,
                                           std::future<std::unique_ptr<StagedArchive>> rest_future, StageTimings& st,
-                                          Clock::time_point t_all, uint32_t rank, uint32_t world, uint64_t new_base,
+                                          Clock::time_point t_all, const MaterializeRequest& req,
                                           void* host_out, uint64_t cap, ArchiveMaterializeTimings* t) {
     std::unique_ptr<StagedArchive> rest;
     auto others = [&]() -> StagedArchive& {
@@ -545,7 +536,7 @@ static uint64_t materialize_archive_early(Device& dev, const fs::path& root, con
     const StoreView view(host);
     early->order_after("templates.fdt", dev.stream());
     DeviceStore store = adopt_store(dev, early->device("templates.fdt"), host.size(), view.header());
-    launch_from_store(dev, manifest, store, rank, world, new_base, host_out, cap, L);
+    launch_from_store(dev, manifest, store, req, host_out, cap, L);
     trace_point("kernel launched", t_all);
     try {
         const auto tv = Clock::now();
@@ -577,12 +568,11 @@ static uint64_t materialize_archive_early(Device& dev, const fs::path& root, con
     return L.bytes;
 }
 
-uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, uint32_t world,
-                             uint64_t new_base, unsigned lanes, void* host_out, uint64_t cap,
-                             ArchiveMaterializeTimings* t) {
+uint64_t materialize_archive(Device& dev, const fs::path& root, const MaterializeRequest& req, unsigned lanes,
+                             void* host_out, uint64_t cap, ArchiveMaterializeTimings* t) {
     const auto t_all = Clock::now();
-    require(world >= 1 && rank < world, Errc::invalid_argument,
-            "rank " + std::to_string(rank) + " is outside world size " + std::to_string(world));
+    require(req.world >= 1 && req.rank < req.world, Errc::invalid_argument,
+            "rank " + std::to_string(req.rank) + " is outside world size " + std::to_string(req.world));
     ArchivePaths paths{root};
     StageTimings st;
     // The store and graphs.bin (the largest file, hashed only) start streaming
@@ -637,8 +627,8 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
     const Manifest manifest = parse_manifest(std::string(mb.begin(), mb.end()));
     trace_point("manifest parsed", t_all);
     if (early && manifest.file_digests.count("templates.fdt"))
-        return materialize_archive_early(dev, root, manifest, std::move(early), std::move(rest), st, t_all, rank,
-                                         world, new_base, host_out, cap, t);
+        return materialize_archive_early(dev, root, manifest, std::move(early), std::move(rest), st, t_all, req,
+                                         host_out, cap, t);
     if (rest.valid()) {
         try {
             rest.get();
@@ -661,7 +651,10 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
         first = plan.device;
     } else {
         first = {"graphs.bin", "patch.bin"};
-        plan.keep_host = [](const std::string& rel) { return rel == "graphs.bin" || rel == "patch.bin"; };
+        if (manifest.file_digests.count("comm_slots.bin")) first.push_back("comm_slots.bin");
+        plan.keep_host = [](const std::string& rel) {
+            return rel == "graphs.bin" || rel == "patch.bin" || rel == "comm_slots.bin";
+        };
     }
     try {
         staged = std::make_unique<StagedArchive>(dev, root, manifest, lanes, &st, plan);
@@ -682,7 +675,9 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
     } else {
         try {
             packed = pack_template_store(staged->host("graphs.bin"), staged->host("patch.bin"), manifest,
-                                         lanes);
+                                         lanes, nullptr,
+                                         staged->has("comm_slots.bin") ? staged->host("comm_slots.bin")
+                                                                       : std::span<const uint8_t>{});
         } catch (const Error&) {
             rethrow_in_step("template construction");
         }
@@ -690,21 +685,12 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, uint32_t rank, u
         st.h2d_bytes += packed.size();
     }
     const fdt_header& H = store.header;
-    require(H.source_graphs_crc == manifest.file_digests.at("graphs.bin") &&
-                H.source_patch_crc == manifest.file_digests.at("patch.bin"),
-            Errc::archive_corruption, "template store was packed from a different graphs.bin/patch.bin");
-    if (H.n_rank_ops > 0)
-        require(manifest.comm_real_hash != 0, Errc::unresolved_kernel,
-                "archive carries comm patches but no real comm binary");
+    check_store_sources(H, manifest);
     if (host_out)
         require(cap >= H.members_image_bytes, Errc::invalid_argument,
                 "output buffer holds " + std::to_string(cap) + " bytes, the member images need " +
                     std::to_string(H.members_image_bytes));
     DeviceBuffer out(dev, std::max<uint64_t>(H.members_image_bytes, 16));
-    MaterializeRequest req;
-    req.rank = rank;
-    req.world = world;
-    req.new_base = new_base;
     MaterializeTiming mt;
     mt.gate = false;  // part of a pipeline: no stream hold for the events
     launch_materialize(dev, store, req, out.data(), &mt);

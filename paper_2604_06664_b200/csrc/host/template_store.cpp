@@ -156,10 +156,15 @@ uint64_t put_section(Sink& s, fdt_header& h, int id, const T* data, size_t count
 // depends on: the stub -> real kernel swap is rank-independent, so it is
 // written into g's image here (and so lands in the template / diffs); the
 // rank and world writes become rank ops, in table order.
-void patch_graph(const CapturedGraph& g, const PatchTable& patches, const GroupLayout& L,
-                 const KernelTable& kt, uint64_t comm_real_hash, std::vector<uint8_t>& img,
-                 std::vector<fdt_rank_op>* rops) {
+// Comm slots (archive.hpp) follow the rank/world writes as value ops, with
+// the checks apply_comm_slots performs.
+void patch_graph(const CapturedGraph& g, const PatchTable& patches, const CommSlotTable& slots,
+                 const GroupLayout& L, const KernelTable& kt, uint64_t comm_real_hash,
+                 std::vector<uint8_t>& img, std::vector<fdt_rank_op>* rops) {
     auto pit = patches.per_graph.find(g.label);
+    auto sit = slots.per_graph.find(g.label);
+    require(sit == slots.per_graph.end() || pit != patches.per_graph.end(), Errc::archive_corruption,
+            "comm slot table lists graph " + std::to_string(g.label) + ", which has no comm patches");
     if (pit == patches.per_graph.end()) return;
     for (const CommPatchEntry& e : pit->second) {
         // the checks apply_rank_patches performs (rank_forge.cpp:136-150)
@@ -185,6 +190,20 @@ void patch_graph(const CapturedGraph& g, const PatchTable& patches, const GroupL
             if (rops) emit_write(*rops, blob + off, 8, FDT_ROP_WORLD, 0);
         }
     }
+    if (sit != slots.per_graph.end()) {
+        for (const CommSlot& c : sit->second) {
+            bool stub = false;
+            for (const CommPatchEntry& e : pit->second) stub = stub || e.node_id == c.node_id;
+            require(stub && c.node_id < g.nodes.size() && g.nodes[c.node_id].type == NodeType::Kernel,
+                    Errc::archive_corruption,
+                    "comm slot references node " + std::to_string(c.node_id) + ", which is not a patched comm node");
+            require(uint64_t(c.offset) + c.width <= g.nodes[c.node_id].kernel_params().arg_buffer.size(),
+                    Errc::invalid_argument, "comm slot offset outside the argument buffer");
+            if (rops)
+                emit_write(*rops, L.desc_bytes() + L.blob_off[c.node_id] + c.offset, c.width, FDT_ROP_VALUE,
+                           c.value_index);
+        }
+    }
     if (rops)
         std::stable_sort(rops->begin(), rops->end(),
                          [](const fdt_rank_op& a, const fdt_rank_op& b) { return a.chunk < b.chunk; });
@@ -195,8 +214,9 @@ void patch_graph(const CapturedGraph& g, const PatchTable& patches, const GroupL
 std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
                                          std::span<const uint8_t> patch_bin,
                                          const Manifest& manifest, unsigned threads,
-                                         PackStats* stats) {
+                                         PackStats* stats, std::span<const uint8_t> slots_bin) {
     const PatchTable patches = parse_patch_table(patch_bin);
+    const CommSlotTable slots = slots_bin.empty() ? CommSlotTable{} : parse_comm_slots(slots_bin);
     KernelTable kt;
     const bool has_patches = !patches.empty();
     if (has_patches) {
@@ -291,7 +311,7 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
 
         std::vector<uint8_t> timg, tmeta;
         build_image(T, L, kt, timg, tmeta);
-        patch_graph(T, patches, L, kt, manifest.comm_real_hash, timg, nullptr);
+        patch_graph(T, patches, slots, L, kt, manifest.comm_real_hash, timg, nullptr);
         timages.align(16);
         G.timage_off = timages.size();  // rebased onto the section below
         timages.raw(timg);
@@ -304,7 +324,7 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
             MemberOut& o = outs[i];
             std::vector<uint8_t> img, meta;
             build_image(g, L, kt, img, meta);
-            patch_graph(g, patches, L, kt, manifest.comm_real_hash, img, &o.rops);
+            patch_graph(g, patches, slots, L, kt, manifest.comm_real_hash, img, &o.rops);
             // every 8-byte lane whose bytes or relocation flag differ from the
             // template's becomes a diff entry (store_format.h)
             const uint64_t nlanes = img.size() / 8;
@@ -376,6 +396,21 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
         groups.push_back(G);
     }
 
+    // tiles whose template chunks hold no relocatable lane go first (stable)
+    uint32_t n_plain = 0;
+    {
+        std::vector<fdt_tile> plain, rest;
+        for (const fdt_tile& t : tiles) {
+            const uint64_t c0 = t.src_off / 16;  // TIMAGES-relative until rebased below
+            bool reloc = false;
+            for (uint64_t c = c0; !reloc && c < c0 + t.nchunks; ++c) reloc = cmeta[c] != 0;
+            (reloc ? rest : plain).push_back(t);
+        }
+        n_plain = static_cast<uint32_t>(plain.size());
+        plain.insert(plain.end(), rest.begin(), rest.end());
+        tiles = std::move(plain);
+    }
+
     // kernel table + strings
     std::vector<fdt_kernel> kernels(kt.size());
     std::string strings;
@@ -405,6 +440,9 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
     h.real_comm_hash = manifest.comm_real_hash;
     h.members_image_bytes = out_off;
     h.total_nodes = total_nodes;
+    h.n_plain_tiles = n_plain;
+    h.n_values = slots.empty() ? 0u : slots.n_values;
+    h.source_slots_crc = slots_bin.empty() ? 0ull : crc64(slots_bin);
 
     Sink s;
     s.zeros(sizeof(fdt_header));
@@ -445,12 +483,27 @@ PackStats pack_archive_store(const std::filesystem::path& archive, unsigned thre
     Manifest m = parse_manifest(std::string(mtext.begin(), mtext.end()));
     const auto graphs = slurp(paths.graphs());
     const auto patch = slurp(paths.patch_table());
+    const bool has_slots = m.file_digests.count("comm_slots.bin") != 0;
+    const auto slots = has_slots ? slurp(paths.comm_slots()) : std::vector<uint8_t>{};
     PackStats st;
-    const auto store = pack_template_store(graphs, patch, m, threads, &st);
+    const auto store = pack_template_store(graphs, patch, m, threads, &st, slots);
     spit(paths.template_store(), store);
     m.file_digests["templates.fdt"] = crc64(store);
     spit(paths.manifest(), serialize_manifest(m));
     return st;
+}
+
+void write_comm_slots(const std::filesystem::path& archive, const CommSlotTable& table) {
+    ArchivePaths paths{archive};
+    const auto mtext = slurp(paths.manifest());
+    Manifest m = parse_manifest(std::string(mtext.begin(), mtext.end()));
+    const auto bytes = serialize_comm_slots(table);
+    // validate against the graphs it patches before touching the archive
+    (void)pack_template_store(slurp(paths.graphs()), slurp(paths.patch_table()), m, 0, nullptr, bytes);
+    spit(paths.comm_slots(), bytes);
+    m.file_digests["comm_slots.bin"] = crc64(bytes);
+    spit(paths.manifest(), serialize_manifest(m));
+    if (m.file_digests.count("templates.fdt")) pack_archive_store(archive);
 }
 
 // ------------------------------------------------------------------ StoreView

@@ -114,6 +114,7 @@ struct ArchivePaths {
     std::filesystem::path cubin(uint64_t hash) const {
         return binaries() / (hex16(hash) + ".sm_100a.cubin");
     }
+    std::filesystem::path comm_slots() const { return root / "comm_slots.bin"; }
 };
 
 // ------------------------------------------------------------ FNDB images
@@ -182,6 +183,44 @@ struct PatchTable {
 
 std::vector<uint8_t> serialize_patch_table(const PatchTable& t);
 PatchTable parse_patch_table(std::span<const uint8_t> bytes);
+
+// ------------------------------------------------------------ comm slots
+// Per-rank communication state beyond rank/world (B200 addition, "comm_slots.bin",
+// listed in the manifest digests so the reference loader only CRCs it). The
+// stub layer authors the argument layout of every comm stub
+// (rank_forge.cpp:18-22: rank@0 world@8 buf@16 payload@24) and so knows which
+// bytes hold deployment state; a slot says "after apply_rank_patches, bytes
+// [offset, offset + width) of node node_id's argument buffer := the low
+// `width` bytes (little endian) of value table entry value_index". The value
+// table (comm handles, peer buffer addresses, ...) is per rank and supplied at
+// LOAD (LoadOptions::comm_values). Slots may only target nodes the patch table
+// lists for the same graph (opaque compute kernels are never patched), are
+// applied in table order after the rank/world writes, and may straddle
+// 16-byte chunks. Format (little endian):
+//   "FNDS" u16 version=1 u32 n_values u32 n_graphs
+//   per graph: u32 label u32 count, per slot: u32 node_id u32 offset u32 value_index u8 width
+struct CommSlot {
+    uint32_t node_id = 0;
+    uint32_t offset = 0;
+    uint32_t value_index = 0;
+    uint8_t width = 8;  // 1..8
+    bool operator==(const CommSlot&) const = default;
+};
+
+struct CommSlotTable {
+    uint32_t n_values = 0;  // value-table entries every rank must supply
+    std::map<uint32_t, std::vector<CommSlot>> per_graph;  // keyed by batch label
+    bool empty() const { return per_graph.empty(); }
+    bool operator==(const CommSlotTable&) const = default;
+};
+
+std::vector<uint8_t> serialize_comm_slots(const CommSlotTable& t);
+CommSlotTable parse_comm_slots(std::span<const uint8_t> bytes);
+
+// The slot writes of one graph (host statement of the K3 value ops; the
+// checks the packer performs): graph must already be rank-patched.
+void apply_comm_slots(CapturedGraph& graph, std::span<const CommSlot> slots,
+                      std::span<const CommPatchEntry> patches, std::span<const uint64_t> values);
 
 // Host reference of the K3 rewrite (reference rank_forge.cpp:132-152), kept for
 // the drop-in C++ surface; LOAD itself patches on the GPU.

@@ -9,6 +9,7 @@
 #include <span>
 #include <vector>
 
+#include "foundry/archive.hpp"
 #include "foundry/errors.hpp"
 #include "foundry/store_format.h"
 
@@ -105,19 +106,19 @@ struct DeviceStore {
     // Relocated template images of the launch in flight (delta != 0); one per
     // store, so materializations of a store are ordered on its device stream.
     DeviceBuffer rtimages;
-    // Tile order of the launch (adopt_store with the host blob): tiles whose
-    // template chunks hold no relocatable lane first, so with delta != 0 the
-    // member grid's first tiles read the store itself and do not wait for the
-    // relocation grid. Empty = the store's own order.
-    DeviceBuffer planned_tiles;
-    uint32_t n_plain_tiles = 0;
+    // The per-rank value table of the launch in flight (FDT_ROP_VALUE ops).
+    mutable DeviceBuffer values;
 };
+
+// The store's source digests must be the archive's (graphs.bin, patch.bin,
+// comm_slots.bin when present); a store with rank ops needs a real comm binary.
+void check_store_sources(const fdt_header& h, const Manifest& manifest);
 
 struct MaterializeRequest {
     uint32_t rank = 0;
     uint32_t world = 1;
     uint64_t new_base = 0;  // 0 = keep the captured base
-    std::vector<uint64_t> values;  // FDT_ROP_VALUE table
+    std::vector<uint64_t> values;  // FDT_ROP_VALUE table (>= header.n_values entries)
 };
 
 struct MaterializeTiming {
@@ -132,15 +133,14 @@ struct MaterializeTiming {
 
 // Checks a device-resident store blob's header (host copy) and prepares pointers.
 DeviceStore adopt_store(Device& dev, const unsigned char* d_blob, size_t bytes,
-                        const fdt_header& host_header,
-                        const void* host_blob = nullptr);
+                        const fdt_header& host_header);
 DeviceStore upload_store(Device& dev, const void* host_blob, size_t bytes);
 
 // Launches K2+K1+K3 into `out` (must hold header.members_image_bytes bytes).
 // Asynchronous on dev.stream(); timing (if non-null) is filled after a sync.
+// req.values is copied to the store's value scratch first (stream ordered).
 void launch_materialize(Device& dev, const DeviceStore& store, const MaterializeRequest& req,
-                        unsigned char* out, MaterializeTiming* timing, int grid_override = 0,
-                        const uint64_t* d_values = nullptr);
+                        unsigned char* out, MaterializeTiming* timing, int grid_override = 0);
 
 struct Segment {
     uint64_t offset = 0;  // within the device buffer

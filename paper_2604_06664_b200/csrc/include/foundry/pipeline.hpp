@@ -71,6 +71,10 @@ struct LoadOptions {
     // memset nodes (and any node whose function, block or shared memory would
     // change) go through the host. Excludes share_execs.
     bool device_updates = false;
+    // This rank's communication state for the archive's comm slots
+    // (comm_slots.bin, archive.hpp: comm handles, peer buffer addresses, ...);
+    // at least the store's n_values entries when the archive carries slots.
+    std::vector<uint64_t> comm_values;
 };
 
 // Wall/kernel time of each LOAD phase (milliseconds) and the DMA volume.

@@ -158,8 +158,7 @@ struct ArchiveMaterializeTimings {
 // new_base) -> member images copied to host_out (if non-null; cap bytes).
 // The GPU-native equivalent of the reference's verify_archive_integrity +
 // PrepareFn over every member. Returns the member-image bytes.
-uint64_t materialize_archive(Device& dev, const std::filesystem::path& root, uint32_t rank,
-                             uint32_t world, uint64_t new_base, unsigned lanes, void* host_out,
-                             uint64_t cap, ArchiveMaterializeTimings* timings);
+uint64_t materialize_archive(Device& dev, const std::filesystem::path& root, const MaterializeRequest& req,
+                             unsigned lanes, void* host_out, uint64_t cap, ArchiveMaterializeTimings* timings);
 
 }  // namespace foundry

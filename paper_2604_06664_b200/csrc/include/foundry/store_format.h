@@ -36,13 +36,19 @@
  * The kernel works tile by tile: a tile is up to tile_chunks consecutive
  * 16-byte chunks of one member image; the packer precomputes each tile's
  * diff and rank-op ranges so a CTA needs one descriptor load to start.
+ * Tiles whose template chunks hold no relocatable lane are stored first
+ * (n_plain_tiles of them): with delta != 0 they read the store directly
+ * while the relocation grid is still running.
+ * Comm slots (comm_slots.bin, archive.hpp) become FDT_ROP_VALUE ops after the
+ * rank/world ops of the same chunk; the kernel reads values[aux] from the
+ * caller's per-rank table of n_values entries.
  */
 #ifndef FOUNDRY_STORE_FORMAT_H
 #define FOUNDRY_STORE_FORMAT_H
 
 #include <stdint.h>
 
-#define FDT_VERSION 3u
+#define FDT_VERSION 4u
 #define FDT_TILE_CHUNKS 1024u /* 16 KiB of member image per tile */
 
 enum fdt_section_id {
@@ -85,6 +91,11 @@ typedef struct {
     uint64_t real_comm_hash;
     uint64_t members_image_bytes; /* sum of member image sizes = output arena */
     uint64_t total_nodes;         /* sum over members of node counts */
+    /* v4 */
+    uint32_t n_plain_tiles;    /* the first n_plain_tiles tiles read no relocatable
+                                  template lane (they need not wait for K1's grid) */
+    uint32_t n_values;         /* per-rank value-table entries FDT_ROP_VALUE ops read */
+    uint64_t source_slots_crc; /* comm_slots.bin digest (0: no comm slots) */
     fdt_section sec[FDT_NSEC];
 } fdt_header;
 

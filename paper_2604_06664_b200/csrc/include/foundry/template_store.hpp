@@ -31,15 +31,23 @@ struct PackStats {
     uint64_t store_bytes = 0;
 };
 
+// slots_bin: the archive's comm_slots.bin (empty: none).
 std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
                                          std::span<const uint8_t> patch_bin,
                                          const Manifest& manifest, unsigned threads = 0,
-                                         PackStats* stats = nullptr);
+                                         PackStats* stats = nullptr,
+                                         std::span<const uint8_t> slots_bin = {});
 
 // Packs an archive directory in place: writes templates.fdt and records its
 // digest in the manifest (the archive stays loadable by the reference build,
 // which only verifies the extra file's digest).
 PackStats pack_archive_store(const std::filesystem::path& archive, unsigned threads = 0);
+
+// The stub layer's authoring step for per-rank comm state (archive.hpp
+// CommSlotTable): writes comm_slots.bin, records its digest in the manifest
+// and re-packs templates.fdt when the archive has one. The table is validated
+// against graphs.bin + patch.bin first (the packer's checks).
+void write_comm_slots(const std::filesystem::path& archive, const CommSlotTable& table);
 
 class StoreView {
 public:

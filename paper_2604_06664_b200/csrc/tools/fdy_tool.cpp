@@ -142,6 +142,7 @@ static int cmd_load(int argc, char** argv) {
     if (argc > 3) o.rank = static_cast<uint32_t>(std::stoul(argv[3]));
     if (argc > 4) o.world = static_cast<uint32_t>(std::stoul(argv[4]));
     if (argc > 5) o.relocate = std::string(argv[5]) == "1";
+    if (argc > 6) o.share_execs = std::string(argv[6]) == "share";
     ServingContext sc = load(argv[2], o);
     const auto& t = sc.timings();
     std::fprintf(stderr, "loaded: total %.3f ms restore %.3f instantiate %.3f build %.3f\n", t.total_ms,
@@ -205,12 +206,209 @@ static int cmd_restorebench(int argc, char** argv) {
         std::printf("%-40s threads %2d: %8.3f ms for %zu libraries\n", label, threads, ms, bins.size());
         for (CUlibrary l : libs) api.cuLibraryUnload(l);
     };
+    // function loads alone: every library loaded and every kernel resolved
+    // first, then cuKernelGetFunction + cuFuncLoad of every entry from T threads
+    auto run_funcs = [&](int threads) {
+        std::vector<CUlibrary> libs(bins.size(), nullptr);
+        std::vector<CUkernel> ks;
+        for (size_t i = 0; i < bins.size(); ++i) {
+            cu_check(api.cuLibraryLoadData(&libs[i], bins[i].cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
+                     "load");
+            for (const auto& n : bins[i].names) {
+                CUkernel k;
+                cu_check(api.cuLibraryGetKernel(&k, libs[i], n.c_str()), "getkernel");
+                ks.push_back(k);
+            }
+        }
+        std::atomic<size_t> next{0};
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (int t = 0; t < threads; ++t)
+            pool.emplace_back([&] {
+                dev.make_current();
+                for (size_t i; (i = next.fetch_add(64)) < ks.size();)
+                    for (size_t j = i; j < std::min(ks.size(), i + 64); ++j) {
+                        CUfunction f;
+                        cu_check(api.cuKernelGetFunction(&f, ks[j]), "getfunction");
+                        cu_check(api.cuFuncLoad(f), "funcload");
+                    }
+            });
+        for (auto& t : pool) t.join();
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        std::printf("%-40s threads %2d: %8.3f ms for %zu functions (%.2f us each)\n", "function loads only", threads,
+                    ms, ks.size(), 1e3 * ms / ks.size());
+        for (CUlibrary l : libs) api.cuLibraryUnload(l);
+    };
     run("warm-up", 2, 1);
+    for (int threads : {1, 2, 4, 8, 16, 1}) run_funcs(threads);
     for (int threads : {1, 4, 16}) {
         run("cuLibraryLoadData", 0, threads);
         run("+ cuLibraryGetKernel", 1, threads);
         run("+ cuKernelGetFunction", 2, threads);
         run("+ cuFuncLoad", 3, threads);
+    }
+    return 0;
+}
+
+// overlapbench <archive>: which driver operations overlap across host threads:
+// (a) cuGraphInstantiate of a template-0-shaped graph alone, (b) function loads
+// of half the catalog alone, (c) both at once on two threads; then the same
+// with library loads (cuLibraryLoadData) against function loads.
+static int cmd_overlapbench(int argc, char** argv) {
+    (void)argc;
+    ArchivePaths paths{argv[2]};
+    Device dev(0);
+    const DriverApi& api = driver();
+    const Catalog cat = parse_catalog(slurp(paths.catalog()));
+    struct Bin {
+        std::vector<uint8_t> cubin;
+        std::vector<std::string> names;
+        CUlibrary lib = nullptr;
+        std::vector<CUkernel> ks;
+    };
+    std::vector<Bin> bins;
+    for (const auto& [hash, rec] : cat.binaries) {
+        Bin b;
+        b.cubin = slurp(paths.cubin(hash));
+        for (const auto& e : parse_kernel_image(slurp(paths.binary(hash))).entrypoints) b.names.push_back(e.name);
+        bins.push_back(std::move(b));
+    }
+    using clk = std::chrono::steady_clock;
+    auto ms_since = [](clk::time_point t) {
+        return std::chrono::duration<double, std::milli>(clk::now() - t).count();
+    };
+    auto load_libs = [&](size_t lo, size_t hi, int threads) {
+        std::atomic<size_t> next{lo};
+        std::vector<std::thread> pool;
+        for (int t = 0; t < threads; ++t)
+            pool.emplace_back([&] {
+                dev.make_current();
+                for (size_t i; (i = next.fetch_add(1)) < hi;) {
+                    cu_check(api.cuLibraryLoadData(&bins[i].lib, bins[i].cubin.data(), nullptr, nullptr, 0, nullptr,
+                                                   nullptr, 0), "load");
+                    bins[i].ks.clear();
+                    for (const auto& n : bins[i].names) {
+                        CUkernel k;
+                        cu_check(api.cuLibraryGetKernel(&k, bins[i].lib, n.c_str()), "getkernel");
+                        bins[i].ks.push_back(k);
+                    }
+                }
+            });
+        for (auto& t : pool) t.join();
+    };
+    auto unload = [&] {
+        for (auto& b : bins)
+            if (b.lib) api.cuLibraryUnload(b.lib), b.lib = nullptr;
+    };
+    auto load_funcs = [&](size_t lo, size_t hi) {
+        dev.make_current();
+        size_t n = 0;
+        for (size_t i = lo; i < hi; ++i)
+            for (CUkernel k : bins[i].ks) {
+                CUfunction f;
+                cu_check(api.cuKernelGetFunction(&f, k), "getfunction");
+                cu_check(api.cuFuncLoad(f), "funcload");
+                ++n;
+            }
+        return n;
+    };
+    // template-0 topology with one (loaded) function per node
+    const auto tstore = slurp(paths.root / "templates.fdt");
+    const StoreView tview(tstore);
+    const fdt_group& TG = tview.group(0);
+    const auto TE = tview.edges(0);
+    std::vector<uint8_t> blob(4096, 0);
+    auto make_graph = [&](CUfunction fn) {
+        CUgraph g;
+        cu_check(api.cuGraphCreate(&g, 0), "create");
+        std::vector<CUgraphNode> ns(TG.n_nodes);
+        for (uint32_t i = 0; i < TG.n_nodes; ++i) {
+            size_t size = 32;
+            void* extra[5] = {CU_LAUNCH_PARAM_BUFFER_POINTER, blob.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &size,
+                              CU_LAUNCH_PARAM_END};
+            CUDA_KERNEL_NODE_PARAMS p;
+            std::memset(&p, 0, sizeof p);
+            p.func = fn;
+            p.gridDimX = p.gridDimY = p.gridDimZ = 1;
+            p.blockDimX = 32;
+            p.blockDimY = p.blockDimZ = 1;
+            p.extra = extra;
+            cu_check(api.cuGraphAddKernelNode(&ns[i], g, nullptr, 0, &p), "add");
+        }
+        std::vector<CUgraphNode> from(TG.n_edges), to(TG.n_edges);
+        for (uint32_t i = 0; i < TG.n_edges; ++i) from[i] = ns[TE[2 * i]], to[i] = ns[TE[2 * i + 1]];
+        cu_check(api.cuGraphAddDependencies(g, from.data(), to.data(), TG.n_edges), "deps");
+        return g;
+    };
+    const size_t half = bins.size() / 2;
+    for (int rep = 0; rep < 3; ++rep) {
+        load_libs(0, bins.size(), 4);
+        CUfunction fn;
+        size_t stub = 0;
+        for (size_t i = 0; i < bins.size(); ++i)
+            for (size_t j = 0; j < bins[i].names.size(); ++j)  // a 32-byte-argument entry (comm stub)
+                if (!stub && bins[i].names[j].find("allreduce") != std::string::npos) stub = i + 1;
+        (void)stub;
+        cu_check(api.cuKernelGetFunction(&fn, bins[0].ks[0]), "fn");
+        cu_check(api.cuFuncLoad(fn), "fn load");
+        CUgraph g0 = make_graph(fn), g1 = make_graph(fn);
+        CUgraphExec x0, x1;
+        auto t0 = clk::now();
+        cu_check(api.cuGraphInstantiate(&x0, g0, 0), "inst");
+        const double inst = ms_since(t0);
+        t0 = clk::now();
+        const size_t nf = load_funcs(0, half);
+        const double funcs = ms_since(t0);
+        t0 = clk::now();
+        double inst_b = 0, funcs_b = 0;
+        size_t nf_b = 0;
+        std::thread a([&] {
+            dev.make_current();
+            const auto ta = clk::now();
+            cu_check(api.cuGraphInstantiate(&x1, g1, 0), "inst");
+            inst_b = ms_since(ta);
+        });
+        std::thread b([&] {
+            const auto tb = clk::now();
+            nf_b = load_funcs(half, bins.size());
+            funcs_b = ms_since(tb);
+        });
+        a.join();
+        b.join();
+        const double both = ms_since(t0);
+        std::printf("rep %d: instantiate alone %.2f ms | %zu function loads alone %.2f ms | together: wall %.2f ms "
+                    "(instantiate %.2f, %zu function loads %.2f)\n",
+                    rep, inst, nf, funcs, both, inst_b, nf_b, funcs_b);
+        api.cuGraphExecDestroy(x0);
+        api.cuGraphExecDestroy(x1);
+        api.cuGraphDestroy(g0);
+        api.cuGraphDestroy(g1);
+        unload();
+        // library loads (4 threads) of the second half || function loads of the first half
+        load_libs(0, half, 4);
+        t0 = clk::now();
+        load_libs(half, bins.size(), 4);
+        const double libs_alone = ms_since(t0);
+        unload();
+        load_libs(0, half, 4);
+        t0 = clk::now();
+        double fl = 0, ll = 0;
+        std::thread c([&] {
+            const auto tc = clk::now();
+            load_funcs(0, half);
+            fl = ms_since(tc);
+        });
+        std::thread d([&] {
+            const auto td = clk::now();
+            load_libs(half, bins.size(), 4);
+            ll = ms_since(td);
+        });
+        c.join();
+        d.join();
+        std::printf("rep %d: library loads (half, 4 threads) alone %.2f ms | with function loads of the other half: "
+                    "wall %.2f ms (libraries %.2f, functions %.2f)\n",
+                    rep, libs_alone, ms_since(t0), ll, fl);
+        unload();
     }
     return 0;
 }
@@ -508,6 +706,7 @@ int main(int argc, char** argv) {
         if (cmd == "save") return cmd_save(argc, argv);
         if (cmd == "load") return cmd_load(argc, argv);
         if (cmd == "instbench") return cmd_instbench(argc, argv);
+        if (cmd == "overlapbench") return cmd_overlapbench(argc, argv);
         if (cmd == "cuda-init") {  // fresh-process floor: create the device context, nothing else
             fdy_device* d = nullptr;
             if (fdy_device_open(argc > 2 ? std::atoi(argv[2]) : 0, &d)) return 1;

@@ -182,3 +182,30 @@ def write_container(graph_list, version: int, crc64) -> tuple[bytes, list]:
         at += len(r)
     head = b"FNDG" + struct.pack("<HI", version, len(recs))
     return head + b"".join(struct.pack("<IQQQ", *l) for l in locs) + b"".join(recs), locs
+
+
+def patch_nodes(buf: bytes) -> dict:
+    """FNDP patch table (rank_forge.cpp:43-102) -> {label: [node_id, ...]}."""
+    assert buf[:4] == b"FNDP"
+    at = 4 + 2 + 8
+    (graphs,) = struct.unpack_from("<I", buf, at)
+    at += 4
+    out = {}
+    for _ in range(graphs):
+        label, count = struct.unpack_from("<II", buf, at)
+        at += 8
+        nodes = []
+        for _ in range(count):
+            (node,) = struct.unpack_from("<I", buf, at)
+            at += 4 + 8
+            for _ in range(2):  # stub name, real name
+                (n,) = struct.unpack_from("<I", buf, at)
+                at += 4 + n
+            for _ in range(2):  # rank offsets, world offsets
+                (n,) = struct.unpack_from("<I", buf, at)
+                at += 4 + 4 * n
+            at += 1  # patch_width
+            nodes.append(node)
+        out[label] = nodes
+    assert at == len(buf)
+    return out

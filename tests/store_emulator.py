@@ -28,7 +28,8 @@ def parse_header(blob: bytes) -> dict:
                   "n_kernels", "n_tiles", "tile_chunks", "n_diffs", "n_rank_ops"], f))
     (h["source_graphs_crc"], h["source_patch_crc"], h["old_base"], h["final_offset"],
      h["real_comm_hash"], h["members_image_bytes"], h["total_nodes"]) = struct.unpack_from("<7Q", blob, 40)
-    secs = struct.unpack_from("<%dQ" % (2 * len(SEC_NAMES)), blob, 96)
+    h["n_plain_tiles"], h["n_values"], h["source_slots_crc"] = struct.unpack_from("<IIQ", blob, 96)
+    secs = struct.unpack_from("<%dQ" % (2 * len(SEC_NAMES)), blob, 112)
     h["sec"] = {n: (secs[2 * i], secs[2 * i + 1]) for i, n in enumerate(SEC_NAMES)}
     return h
 

@@ -213,7 +213,7 @@ def test_ipc_fanout_between_two_processes(foundry, oracle, archives, tmp_path):
     procs = []
     for rank in range(2):
         env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
-                   WORLD_SIZE="2", LOCAL_RANK="0")
+                   WORLD_SIZE="2", LOCAL_RANK=str(rank))
         procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "ipc_worker.py"), arch,
                                        str(tmp_path)], env=env))
     for p in procs:

@@ -158,3 +158,94 @@ def test_manifest_fast_reader_agrees_or_defers(foundry, archives):
     assert agrees(variants[-1]) == 1
     for v in variants[:8]:
         assert agrees(v) == -1
+
+
+# ------------------------------------------------------------------ comm slots
+
+def _with_slots(foundry, archives, tmp_path, table_fn, name="moe-spmd"):
+    import shutil
+
+    import comm_slots
+    arch, _ = archives(name)
+    copy = str(tmp_path / (name + "-slots"))
+    shutil.copytree(arch, copy)
+    foundry.write_comm_slots(copy, comm_slots.N_VALUES, table_fn(copy))
+    return copy
+
+
+def test_comm_slots_store_expansion_equals_oracle(foundry, oracle, archives, tmp_path):
+    """K3 value ops (comm handles, peer buffers): every rank of W=8 gets its own
+    value table; writes straddle 16-byte chunks, overlap the rank/world bytes
+    (slots apply after them) and use 1/4/8-byte widths."""
+    import comm_slots
+    from paper_2604_06664_b200 import capi
+    arch = _with_slots(foundry, archives, tmp_path, comm_slots.stress_table)
+    h = capi.store_header(open(os.path.join(arch, "templates.fdt"), "rb").read())
+    m = manifest(arch)
+    assert h["n_values"] == comm_slots.N_VALUES
+    assert h["source_slots_crc"] == m["files"]["comm_slots.bin"]
+    blob = open(os.path.join(arch, "templates.fdt"), "rb").read()
+    off, n = h["sec"]["rops"]
+    rops = np.frombuffer(blob, emu.ROP_DT, n // emu.ROP_DT.itemsize, off)
+    assert (rops["kind"] == 3).any()  # FDT_ROP_VALUE
+    outs = set()
+    for rank, delta in [(0, 0), (3, 0x10000), (7, 0x10000000000)]:
+        vals = comm_slots.rank_values(rank)
+        want, _ = oracle.materialize_archive(arch, rank, 8, delta, values=vals)
+        assert emulate(foundry, arch, rank, 8, delta, vals) == want, rank
+        outs.add(want)
+    assert len(outs) == 3
+
+
+def test_comm_slots_oracle_differs_from_the_reference_only_at_slot_bytes(foundry, oracle, archives, tmp_path,
+                                                                       ref_tool):
+    """Pin of the slot rule: the oracle with comm slots equals the reference's
+    own PrepareFn output (ref_tool prepare) except at exactly the slot bytes,
+    which hold the rank's values little-endian."""
+    import subprocess
+
+    import comm_slots
+    import fndg
+    arch = _with_slots(foundry, archives, tmp_path, comm_slots.stress_table)
+    rank, vals = 5, comm_slots.rank_values(5)
+    got, _ = oracle.materialize_archive(arch, rank, 8, values=vals)
+    ref = str(tmp_path / "ref.fndg")
+    subprocess.run([ref_tool, "prepare", arch, str(rank), "8", ref], check=True)
+    want = {g.label: g for g in fndg.graphs(open(ref, "rb").read())}
+    table = comm_slots.stress_table(arch)
+    touched = 0
+    for g in fndg.graphs(got):
+        r = want[g.label]
+        expect = {n.id: bytearray(n.args) for n in r.nodes}
+        for node, off, idx, width in table.get(g.label, []):
+            expect[node][off:off + width] = vals[idx].to_bytes(8, "little")[:width]
+            touched += 1
+        for a, b in zip(g.nodes, r.nodes):
+            assert (a.type, a.grid, a.block, a.hash, a.name) == (b.type, b.grid, b.block, b.hash, b.name)
+            assert a.args == bytes(expect[a.id]), (g.label, a.id)
+    assert touched > 0
+
+
+def test_comm_slots_are_validated(foundry, archives, tmp_path):
+    """Slots may only name patched comm nodes, must fit the argument buffer,
+    and index the value table (archive-corruption / invalid-argument)."""
+    import shutil
+
+    import fndg
+    arch, _ = archives("moe-spmd")
+    copy = str(tmp_path / "bad")
+    shutil.copytree(arch, copy)
+    nodes = fndg.patch_nodes(open(os.path.join(copy, "patch.bin"), "rb").read())
+    label, ids = next(iter(nodes.items()))
+    compute = next(i for i in range(1, 50) if i not in ids)
+    with pytest.raises(foundry.FoundryError, match="not a patched comm node"):
+        foundry.write_comm_slots(copy, 2, {label: [(compute, 0, 0, 8)]})
+    with pytest.raises(foundry.FoundryError, match="outside the argument buffer"):
+        foundry.write_comm_slots(copy, 2, {label: [(ids[0], 30, 0, 8)]})
+    with pytest.raises(foundry.FoundryError, match="value index 2 is outside"):
+        foundry.write_comm_slots(copy, 2, {label: [(ids[0], 16, 2, 8)]})
+    with pytest.raises(foundry.FoundryError, match="width 9"):
+        foundry.write_comm_slots(copy, 2, {label: [(ids[0], 16, 0, 9)]})
+    # nothing was written by the failed calls
+    assert not os.path.exists(os.path.join(copy, "comm_slots.bin"))
+    assert "comm_slots.bin" not in manifest(copy)["files"]
