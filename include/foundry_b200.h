@@ -32,6 +32,11 @@
  *       fdy_store_fanout      GPU -> GPU copy of a resident store (NVLink P2P)
  *       fdy_materialize       K2 diff expansion + K1 relocation + K3 rank patch
  *       fdy_members_download  HBM -> host copy of member images
+ *       fdy_members_record    one member as the FNDG record the reference PrepareFn
+ *                             returns (encode_graph_record, graph_model.cpp:205-218)
+ *       fdy_load_members      the PrepareFn replacement for a whole archive:
+ *                             integrity + fused kernel, result kept in HBM
+ *                             (pipeline.cpp:411-417 + :506-514)
  *       fdy_crc64_segments    CRC-64/XZ of byte ranges, computed on the GPU
  *       fdy_sync, fdy_last_error
  *
@@ -124,6 +129,17 @@ int fdy_materialize_timed_split(fdy_device* dev, const fdy_store* store, const f
 size_t fdy_members_bytes(const fdy_members* members);
 int fdy_members_download(fdy_members* members, void* host_dst, size_t offset, size_t bytes);
 void fdy_members_free(fdy_members* members);
+/* One member graph of a materialized set as the FNDG record the reference's
+ * encode_graph_record writes (graph_model.cpp:205-218) — i.e. what the
+ * reference PrepareFn returns for `label` (pipeline.cpp:506-514), ready for its
+ * own parse_graph_at(record, GraphLocator{label, 0, *len, *crc})
+ * (graph_model.cpp:295-303). *len (and *crc, the record's CRC-64/XZ) are always
+ * set; the bytes are written only when cap >= *len (query with buf NULL, then
+ * copy: the second call reuses the first decode). invalid-argument for a label
+ * outside the set. Thread-safe per call (prepare lanes may call concurrently). */
+int fdy_members_record(fdy_members* members, uint32_t label, unsigned char* buf, size_t cap,
+                       size_t* len, uint64_t* crc);
+
 
 /* CRC-64/XZ of n byte ranges of a host buffer, computed on the GPU after one
  * H2D copy (ranges need not be aligned). digests receives n values. */
@@ -150,6 +166,14 @@ typedef struct {
 int fdy_prepare_archive(fdy_device* dev, const char* archive, const fdy_materialize_desc* desc,
                         uint32_t lanes, void* host_out, size_t cap, size_t* out_len,
                         fdy_prepare_timings* timings);
+/* The GPU PrepareFn in one call, result kept in HBM: the archive's files are
+ * staged and integrity-checked (GPU CRC of the store, host CRC of the rest,
+ * verify_archive_integrity pipeline.cpp:411-417), the fused K2+K1+K3 kernel
+ * materializes every member for desc, and the returned fdy_members serves
+ * fdy_members_record / fdy_members_download. A reference-written archive (no
+ * templates.fdt) is packed on the host first. */
+int fdy_load_members(fdy_device* dev, const char* archive, const fdy_materialize_desc* desc, uint32_t lanes,
+                     fdy_members** out, fdy_prepare_timings* timings);
 
 /* Pinned host memory usable as host_out (released with fdy_host_free). */
 void* fdy_host_alloc(fdy_device* dev, size_t bytes);

@@ -25,6 +25,8 @@
 //        integrity CRC of every file + PrepareFn of every member, timed.
 //   time-serve <archive> <rank> <world> <lanes> <reps>
 //        serve + replay of every batch after one load (pipeline.cpp:876-889).
+//   load-traces <archive> <rank> <world> <traces-out>
+//        foundry::load + replay of every batch, traces_to_text.
 //   crc <file>   CRC-64/XZ (hash.cpp:53-69) of a file, hex.
 //   diff <a.fndg> <b.fndg>   reference diff() text per graph pair.
 #include <atomic>
@@ -157,6 +159,21 @@ static int cmd_time_load(int argc, char** argv) {
     return 0;
 }
 
+// load-traces <archive> <rank> <world> <traces-out>
+//   the reference's own load() (pipeline.cpp:447-557) + replay of every batch
+//   (pipeline.cpp:566-569), as traces_to_text.
+static int cmd_load_traces(int argc, char** argv) {
+    if (argc < 6) return usage();
+    LoadOptions options;
+    options.rank = static_cast<uint32_t>(std::stoul(argv[3]));
+    options.world = static_cast<uint32_t>(std::stoul(argv[4]));
+    ServingContext sc = load(argv[2], options);
+    std::map<uint32_t, LaunchTrace> traces;
+    for (uint32_t b : sc.batches()) traces.emplace(b, sc.replay(b));
+    write_file(argv[5], traces_to_text(traces));
+    return 0;
+}
+
 // time-serve <archive> <rank> <world> <lanes> <reps>
 //   one foundry::load, then `reps` sweeps of ServingContext::replay over every
 //   batch in label order (= ServingSet::serve + the simulated launch,
@@ -280,6 +297,7 @@ int main(int argc, char** argv) {
         if (cmd == "time-load") return cmd_time_load(argc, argv);
         if (cmd == "time-materialize") return cmd_time_materialize(argc, argv);
         if (cmd == "time-serve") return cmd_time_serve(argc, argv);
+        if (cmd == "load-traces") return cmd_load_traces(argc, argv);
         if (cmd == "crc") return cmd_crc(argc, argv);
         if (cmd == "diff") return cmd_diff(argc, argv);
     } catch (const Error& e) {

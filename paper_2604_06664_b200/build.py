@@ -108,9 +108,12 @@ def _write_ninja() -> Path:
         "rule embed",
         f"  command = {sys.executable} {CSRC}/tools/embed_ptx.py $in $out",
         "  description = EMBED $in",
+        # -Bsymbolic: the library's own C++ symbols (namespace foundry, the
+        # reference's names) bind inside it, so a process that also links the
+        # reference cannot interpose them
         "rule link",
         f"  command = $cxx -shared -o $out $in {cudart} {CUDA}/lib64/libcudadevrt.a -ldl -lrt -lpthread "
-        "-Wl,-soname,libfoundry_b200.so",
+        "-Wl,-soname,libfoundry_b200.so -Wl,-Bsymbolic",
         "  description = LINK $out",
         "rule pymod",
         f"  command = $cxx $cxxflags -shared -I{py_inc} -I{pybind11.get_include()} $in "

@@ -1,5 +1,7 @@
 // C-ABI, kernel layer (declarations and reference anchors: include/foundry_b200.h).
+#include <atomic>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -7,7 +9,10 @@
 
 #include "capi_common.hpp"
 #include "foundry/device.hpp"
+#include "foundry/graph_model.hpp"
+#include "foundry/hash.hpp"
 #include "foundry/staging.hpp"
+#include "foundry/template_store.hpp"
 #include "foundry_b200.h"
 
 using namespace foundry;
@@ -19,12 +24,39 @@ struct fdy_device {
 struct fdy_store {
     fdy_device* owner = nullptr;
     DeviceStore store;
+    // host copy of the blob, fetched from HBM on first decode (its host
+    // sections turn member images back into graphs)
+    std::mutex mu;
+    std::vector<uint8_t> host;
+    std::unique_ptr<StoreView> view;
+
+    const StoreView& host_view() {
+        std::lock_guard lock(mu);
+        if (!view) {
+            host.resize(store.bytes);
+            owner->dev->make_current();
+            cuda_check(cudaMemcpy(host.data(), store.data, store.bytes, cudaMemcpyDeviceToHost), "store D2H");
+            view = std::make_unique<StoreView>(host);
+        }
+        return *view;
+    }
 };
 
 struct fdy_members {
     fdy_device* owner = nullptr;
     DeviceBuffer out;
+    fdy_store* store = nullptr;  // the store the images were materialized from
+    // fdy_load_members: the archive's own store, kept with its images
+    std::vector<uint8_t> store_host;
+    std::unique_ptr<StoreView> own_view;
+    uint64_t generation = 0;     // bumped whenever the arena is rewritten
+
+    const StoreView& view() { return own_view ? *own_view : store->host_view(); }
 };
+
+namespace {
+std::atomic<uint64_t> g_generation{1};
+}
 
 extern "C" {
 
@@ -133,6 +165,22 @@ size_t fdy_store_members_bytes(const fdy_store* store) {
     return store ? store->store.header.members_image_bytes : 0;
 }
 
+static void copy_timings(const ArchiveMaterializeTimings& t, fdy_prepare_timings* timings) {
+    if (!timings) return;
+    timings->total_ms = t.total_ms;
+    timings->read_ms = t.read_ms;
+    timings->integrity_ms = t.integrity_ms;
+    timings->materialize_ms = t.materialize_ms;
+    timings->d2h_ms = t.d2h_ms;
+    timings->crc_kernel_ms = t.crc_kernel_ms;
+    timings->kernel_ms = t.kernel_ms;
+    timings->h2d_bytes = t.h2d_bytes;
+    timings->d2h_bytes = t.d2h_bytes;
+    timings->member_bytes = t.member_bytes;
+    timings->graphs = t.graphs;
+    timings->nodes = t.nodes;
+}
+
 // The request a descriptor describes; the value table (FDT_ROP_VALUE ops) is
 // part of it on every entry point.
 static MaterializeRequest request_of(const fdy_materialize_desc* desc) {
@@ -151,6 +199,9 @@ static void materialize_into(fdy_device* dev, const fdy_store* store,
                              const fdy_materialize_desc* desc, fdy_members* m, float* kernel_ms) {
     require(dev && store && desc && m, Errc::invalid_argument, "fdy_materialize: null argument");
     require(store->owner == dev, Errc::invalid_argument, "fdy_materialize: store lives on another device");
+    m->store = const_cast<fdy_store*>(store);
+    m->own_view.reset();
+    m->generation = g_generation.fetch_add(1);
     const MaterializeRequest req = request_of(desc);
     MaterializeTiming t;
     launch_materialize(*dev->dev, store->store, req, m->out.data(), kernel_ms ? &t : nullptr, desc->grid);
@@ -187,6 +238,9 @@ int fdy_materialize_timed_split(fdy_device* dev, const fdy_store* store, const f
         require(m->out.size() >= store->store.header.members_image_bytes, Errc::invalid_argument,
                 "fdy_materialize_timed_split: arena too small for this store");
         const MaterializeRequest req = request_of(desc);
+        m->store = const_cast<fdy_store*>(store);
+        m->own_view.reset();
+        m->generation = g_generation.fetch_add(1);
         MaterializeTiming t;
         t.split = true;
         launch_materialize(*dev->dev, store->store, req, m->out.data(), &t, desc->grid);
@@ -213,6 +267,57 @@ int fdy_members_download(fdy_members* m, void* host_dst, size_t offset, size_t b
 
 void fdy_members_free(fdy_members* m) { delete m; }
 
+int fdy_members_record(fdy_members* m, uint32_t label, unsigned char* buf, size_t cap, size_t* len,
+                       uint64_t* crc) {
+    return fdy_guard([&] {
+        require(m != nullptr, Errc::invalid_argument, "fdy_members_record: null members");
+        require(m->own_view || m->store, Errc::invalid_argument, "fdy_members_record: arena holds no materialization");
+        // the last record this thread decoded: the size query and the copy are one decode
+        thread_local struct {
+            uint64_t generation = 0;
+            uint32_t label = 0;
+            std::vector<uint8_t> rec;
+            uint64_t crc = 0;
+        } last;
+        if (last.generation != m->generation || last.label != label || last.rec.empty()) {
+            const StoreView& v = m->view();
+            const int64_t mi = v.member_of(label);
+            require(mi >= 0, Errc::invalid_argument,
+                    "label " + std::to_string(label) + " is not a member of the materialized graph set");
+            const fdt_member& M = v.member(static_cast<uint32_t>(mi));
+            std::vector<uint8_t> image(v.group(M.group).image_bytes);
+            m->owner->dev->make_current();
+            cuda_check(cudaMemcpy(image.data(), m->out.data() + M.out_off, image.size(), cudaMemcpyDeviceToHost),
+                       "cudaMemcpy(member image D2H)");
+            last.rec = encode_graph_record(v.image_to_graph(static_cast<uint32_t>(mi), image));
+            last.crc = crc64(last.rec);
+            last.generation = m->generation;
+            last.label = label;
+        }
+        if (len) *len = last.rec.size();
+        if (crc) *crc = last.crc;
+        if (buf && cap >= last.rec.size()) std::memcpy(buf, last.rec.data(), last.rec.size());
+    });
+}
+
+int fdy_load_members(fdy_device* dev, const char* archive, const fdy_materialize_desc* desc, uint32_t lanes,
+                     fdy_members** out, fdy_prepare_timings* timings) {
+    return fdy_guard([&] {
+        require(dev && archive && desc && out, Errc::invalid_argument, "fdy_load_members: null argument");
+        auto m = std::make_unique<fdy_members>();
+        m->owner = dev;
+        MaterializedArchive keep;
+        ArchiveMaterializeTimings t;
+        materialize_archive(*dev->dev, archive, request_of(desc), lanes ? lanes : 4, nullptr, 0, &t, &keep);
+        m->out = std::move(keep.images);
+        m->store_host = std::move(keep.store_host);
+        m->own_view = std::make_unique<StoreView>(m->store_host);
+        m->generation = g_generation.fetch_add(1);
+        copy_timings(t, timings);
+        *out = m.release();
+    });
+}
+
 int fdy_prepare_archive(fdy_device* dev, const char* archive, const fdy_materialize_desc* desc,
                         uint32_t lanes, void* host_out, size_t cap, size_t* out_len,
                         fdy_prepare_timings* timings) {
@@ -222,20 +327,7 @@ int fdy_prepare_archive(fdy_device* dev, const char* archive, const fdy_material
         const MaterializeRequest req = request_of(desc);
         const uint64_t n = materialize_archive(*dev->dev, archive, req, lanes ? lanes : 4, host_out, cap, &t);
         if (out_len) *out_len = n;
-        if (timings) {
-            timings->total_ms = t.total_ms;
-            timings->read_ms = t.read_ms;
-            timings->integrity_ms = t.integrity_ms;
-            timings->materialize_ms = t.materialize_ms;
-            timings->d2h_ms = t.d2h_ms;
-            timings->crc_kernel_ms = t.crc_kernel_ms;
-            timings->kernel_ms = t.kernel_ms;
-            timings->h2d_bytes = t.h2d_bytes;
-            timings->d2h_bytes = t.d2h_bytes;
-            timings->member_bytes = t.member_bytes;
-            timings->graphs = t.graphs;
-            timings->nodes = t.nodes;
-        }
+        copy_timings(t, timings);
     });
 }
 

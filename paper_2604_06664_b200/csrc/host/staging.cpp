@@ -507,7 +507,8 @@ static uint64_t materialize_archive_early(Device& dev, const fs::path& root, con
                                           std::unique_ptr<StagedArchive> early,
                                           std::future<std::unique_ptr<StagedArchive>> rest_future, StageTimings& st,
                                           Clock::time_point t_all, const MaterializeRequest& req,
-                                          void* host_out, uint64_t cap, ArchiveMaterializeTimings* t) {
+                                          void* host_out, uint64_t cap, ArchiveMaterializeTimings* t,
+                                          MaterializedArchive* keep) {
     std::unique_ptr<StagedArchive> rest;
     auto others = [&]() -> StagedArchive& {
         if (!rest) rest = rest_future.get();  // rethrows a listing / staging error
@@ -551,6 +552,10 @@ static uint64_t materialize_archive_early(Device& dev, const fs::path& root, con
     }
     cuda_check(cudaStreamSynchronize(dev.stream()), "cudaStreamSynchronize");
     trace_point("member images on the host", t_all);
+    if (keep) {
+        keep->images = std::move(L.out);
+        keep->store_host.assign(host.begin(), host.end());
+    }
     if (t) {
         t->read_ms = st.read_ms;
         t->integrity_ms = st.integrity_ms;
@@ -569,7 +574,7 @@ static uint64_t materialize_archive_early(Device& dev, const fs::path& root, con
 }
 
 uint64_t materialize_archive(Device& dev, const fs::path& root, const MaterializeRequest& req, unsigned lanes,
-                             void* host_out, uint64_t cap, ArchiveMaterializeTimings* t) {
+                             void* host_out, uint64_t cap, ArchiveMaterializeTimings* t, MaterializedArchive* keep) {
     const auto t_all = Clock::now();
     require(req.world >= 1 && req.rank < req.world, Errc::invalid_argument,
             "rank " + std::to_string(req.rank) + " is outside world size " + std::to_string(req.world));
@@ -628,7 +633,7 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
     trace_point("manifest parsed", t_all);
     if (early && manifest.file_digests.count("templates.fdt"))
         return materialize_archive_early(dev, root, manifest, std::move(early), std::move(rest), st, t_all, req,
-                                         host_out, cap, t);
+                                         host_out, cap, t, keep);
     if (rest.valid()) {
         try {
             rest.get();
@@ -711,6 +716,11 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
     }
     cuda_check(cudaStreamSynchronize(dev.stream()), "cudaStreamSynchronize");
     trace_point("member images on the host", t_all);
+    if (keep) {
+        keep->images = std::move(out);
+        const auto host = has_store ? staged->host("templates.fdt") : std::span<const uint8_t>(packed);
+        keep->store_host.assign(host.begin(), host.end());
+    }
     if (t) {
         t->read_ms = st.read_ms;
         t->integrity_ms = st.integrity_ms;

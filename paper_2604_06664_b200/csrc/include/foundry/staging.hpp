@@ -158,7 +158,15 @@ struct ArchiveMaterializeTimings {
 // new_base) -> member images copied to host_out (if non-null; cap bytes).
 // The GPU-native equivalent of the reference's verify_archive_integrity +
 // PrepareFn over every member. Returns the member-image bytes.
+// What a caller may keep of the materialization: the member images in HBM and
+// a host copy of the store (its host sections decode the images).
+struct MaterializedArchive {
+    DeviceBuffer images;
+    std::vector<uint8_t> store_host;
+};
+
 uint64_t materialize_archive(Device& dev, const std::filesystem::path& root, const MaterializeRequest& req,
-                             unsigned lanes, void* host_out, uint64_t cap, ArchiveMaterializeTimings* timings);
+                             unsigned lanes, void* host_out, uint64_t cap, ArchiveMaterializeTimings* timings,
+                             MaterializedArchive* keep = nullptr);
 
 }  // namespace foundry
