@@ -84,6 +84,9 @@ void load_all() {
     FDY_RESOLVE(cuLaunchKernelEx);
     resolve(g_api.cuFuncLoad, "cuFuncLoad", 12040);
     FDY_RESOLVE(cuGraphUpload);
+    resolve(g_api.cuLibraryGetKernelCount, "cuLibraryGetKernelCount", 12040);
+    resolve(g_api.cuLibraryEnumerateKernels, "cuLibraryEnumerateKernels", 12040);
+    resolve(g_api.cuKernelGetName, "cuKernelGetName", 12040);
 #undef FDY_RESOLVE
 }
 

@@ -2,6 +2,9 @@
 #include "foundry/gpu_context.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 
 #include <cuda_runtime.h>
@@ -9,6 +12,18 @@
 namespace foundry {
 
 namespace {
+// FOUNDRY_DEBUG driver-call accounting: total ns and calls per kind
+enum StatKind { kGetFunction, kFuncLoad, kSetAttribute, kLibraryLoad, kGetKernel, kStatKinds };
+std::atomic<uint64_t> g_stat_ns[kStatKinds], g_stat_n[kStatKinds];
+struct StatScope {
+    StatKind k;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit StatScope(StatKind kind) : k(kind) {}
+    ~StatScope() {
+        g_stat_ns[k] += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+        g_stat_n[k] += 1;
+    }
+};
 uint64_t align_down(uint64_t v, uint64_t a) { return v / a * a; }
 uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 std::string key_of(uint64_t hash, std::string_view name) { return hex16(hash) + "|" + std::string(name); }
@@ -38,6 +53,21 @@ GpuContext::~GpuContext() {
     if (va_) api->cuMemAddressFree(va_, va_bytes_);
 }
 
+std::string driver_call_stats(bool reset) {
+    static const char* names[kStatKinds] = {"cuKernelGetFunction", "cuFuncLoad", "cuFuncSetAttribute",
+                                            "cuLibraryLoadData", "cuLibraryGet*"};
+    std::string out;
+    char line[160];
+    for (int k = 0; k < kStatKinds; ++k) {
+        const uint64_t n = reset ? g_stat_n[k].exchange(0) : g_stat_n[k].load();
+        const uint64_t ns = reset ? g_stat_ns[k].exchange(0) : g_stat_ns[k].load();
+        std::snprintf(line, sizeof line, "%s %llu calls %.3f ms (%.2f us each); ", names[k], (unsigned long long)n,
+                      ns * 1e-6, n ? ns * 1e-3 / n : 0.0);
+        out += line;
+    }
+    return out;
+}
+
 // ------------------------------------------------------------------ libraries
 
 GpuContext::OpenedLibrary GpuContext::open_library(const KernelImage& image,
@@ -45,8 +75,12 @@ GpuContext::OpenedLibrary GpuContext::open_library(const KernelImage& image,
     const DriverApi& api = driver();
     dev_.make_current();
     OpenedLibrary o;
-    cu_check(api.cuLibraryLoadData(&o.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
-             "cuLibraryLoadData");
+    {
+        StatScope st(kLibraryLoad);
+        cu_check(api.cuLibraryLoadData(&o.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
+                 "cuLibraryLoadData");
+    }
+    StatScope st(kGetKernel);
     try {
         size_t sz = 0;
         cu_check(api.cuLibraryGetGlobal(&o.ctx_global, &sz, o.lib, "fdy_trace_context"),
@@ -74,6 +108,7 @@ CUfunction GpuContext::function(const Kernel& k) const {
     std::lock_guard lock(fn_mu_);
     if (!k.fn) {
         dev_.make_current();
+        StatScope st(kGetFunction);
         cu_check(driver().cuKernelGetFunction(&k.fn, k.kern), "cuKernelGetFunction");
     }
     return k.fn;
@@ -83,26 +118,46 @@ void GpuContext::ensure_loaded(const Kernel& k) const {
     const CUfunction f = function(k);
     std::lock_guard lock(fn_mu_);
     if (k.loaded) return;
+    StatScope st(kFuncLoad);
     if (driver().cuFuncLoad) cu_check(driver().cuFuncLoad(f), "cuFuncLoad");
     k.loaded = true;
 }
 
+// Launch limits go on the kernel's function in THIS context
+// (cuFuncSetAttribute, ~0.1 us) rather than on the context-independent
+// CUkernel (cuKernelSetAttribute, 10-40 us and serialized in the driver:
+// 5358 calls cost 50-200 ms of LOAD on the headline set; tools/gpu_restore_study.sh).
+// Graph nodes and launches use that function, so the limit applies to them.
 void GpuContext::set_kernel_attribute(const Kernel& k, CUfunction_attribute attr, int value) const {
-    cu_check(driver().cuKernelSetAttribute(attr, value, k.kern, cu_device_), "cuKernelSetAttribute");
+    const CUfunction f = function(k);
+    StatScope st(kSetAttribute);
+    cu_check(driver().cuFuncSetAttribute(f, attr, value), "cuFuncSetAttribute");
 }
 
 void GpuContext::require_dynamic_smem(const Kernel& k, int bytes) const {
-    std::lock_guard lock(fn_mu_);
-    if (bytes <= k.max_dynamic_smem) return;
+    {
+        std::lock_guard lock(fn_mu_);
+        if (bytes <= k.max_dynamic_smem) return;
+    }
     set_kernel_attribute(k, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, bytes);
-    k.max_dynamic_smem = bytes;
+    std::lock_guard lock(fn_mu_);
+    k.max_dynamic_smem = std::max(k.max_dynamic_smem, bytes);
 }
 
 void GpuContext::set_carveout(const Kernel& k, int percent) const {
-    std::lock_guard lock(fn_mu_);
-    if (percent == k.carveout) return;
+    {
+        std::lock_guard lock(fn_mu_);
+        if (percent == k.carveout) return;
+    }
     set_kernel_attribute(k, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, percent);
+    std::lock_guard lock(fn_mu_);
     k.carveout = percent;
+}
+
+int GpuContext::function_attribute(const Kernel& k, CUfunction_attribute attr) const {
+    int v = 0;
+    cu_check(driver().cuFuncGetAttribute(&v, attr, function(k)), "cuFuncGetAttribute");
+    return v;
 }
 
 uint32_t GpuContext::register_library(uint64_t hash, const KernelImage& image, OpenedLibrary&& o,

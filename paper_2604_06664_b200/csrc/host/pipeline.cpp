@@ -191,7 +191,8 @@ void ServingContext::Impl::restore_binaries() {
         if (ctx->has_library(hash)) continue;  // a second restore is a no-op
         items.push_back(Item{hash, &rec, ord, {}, {}});
     }
-    const unsigned lanes = std::max(1u, std::min(opts.prepare_lanes, 8u));
+    unsigned lanes = std::max(1u, std::min(opts.prepare_lanes, 8u));
+    if (const char* env = std::getenv("FOUNDRY_RESTORE_LANES")) lanes = std::max(1, std::atoi(env));
     std::vector<std::exception_ptr> failed(items.size());
     parallel_for(items.size(), lanes, [&](size_t i) {
         try {
@@ -200,6 +201,7 @@ void ServingContext::Impl::restore_binaries() {
             failed[i] = std::current_exception();
         }
     });
+    debug_phase("restore: libraries opened");
     // the first failure in catalog order is the one reported, as sequentially
     for (size_t i = 0; i < items.size(); ++i) {
         if (!failed[i]) continue;
@@ -260,7 +262,7 @@ void ServingContext::Impl::kernel_params(const fdt_node& d, const uint8_t* blob,
                                          const GpuContext::Kernel& K, CUDA_KERNEL_NODE_PARAMS& p,
                                          void** extra, size_t* size) const {
     std::memset(&p, 0, sizeof p);
-    p.kern = K.kern;  // func = null: the driver resolves the kernel in the current context
+    p.func = ctx->function(K);  // this context's function: it carries the launch limits set at LOAD
     p.gridDimX = d.grid[0];
     p.gridDimY = d.grid[1];
     p.gridDimZ = d.grid[2];
@@ -982,11 +984,13 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     // (the driver loads each kernel's function lazily when its first node is
     // added; a separate loader thread ahead of the builder measured no gain:
     // function loads and instantiation serialize inside the driver)
+    debug_phase("templates downloaded");
     if (opts.share_execs) {  // one exec per graph shape; the first group of a shape owns it
         std::map<std::string, uint32_t> first_of_shape;
         I.owner.resize(H.n_groups);
         for (uint32_t g = 0; g < H.n_groups; ++g)
             I.owner[g] = first_of_shape.emplace(I.shape_key(g), g).first->second;
+        debug_phase("shape keys");
     }
     std::thread builder([&] {
         try {
@@ -999,6 +1003,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
                 // served through the owner's exec: its functions are loaded now, as
                 // a build would (every template is servable when LOAD returns)
                 const auto tf = Clock::now();
+                debug_phase("function loads of a shared-exec template");
                 I.prepare_kernels(gi, I.view->group(gi).first_member, /*load_functions=*/true);
                 std::lock_guard lock(I.stats_mu);
                 I.t.function_load_ms += ms_since(tf);
@@ -1061,6 +1066,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     I.t.templates = H.n_groups;
     I.t.total_ms = ms_since(t_all);
     debug_phase("load returns");
+    if (std::getenv("FOUNDRY_DEBUG")) std::fprintf(stderr, "[foundry] driver calls: %s\n", driver_call_stats(true).c_str());
     return ServingContext(std::move(impl));
 }
 

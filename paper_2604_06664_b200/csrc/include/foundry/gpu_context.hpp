@@ -36,6 +36,10 @@
 
 namespace foundry {
 
+// Summed wall time and count of the driver calls GpuContext issues per kind
+// (thread time: concurrent calls add up); diagnostics for FOUNDRY_DEBUG.
+std::string driver_call_stats(bool reset);
+
 using CounterSnapshot = std::map<std::string, uint64_t>;
 
 class GpuContext {
@@ -91,6 +95,8 @@ public:
     // limit only ever grows (every node of the kernel must fit).
     void require_dynamic_smem(const Kernel& k, int bytes) const;
     void set_carveout(const Kernel& k, int percent) const;
+    // cuFuncGetAttribute of the kernel's function in this context
+    int function_attribute(const Kernel& k, CUfunction_attribute attr) const;
     void run_device_init(uint32_t library);
     bool library_device_inited(uint32_t library) const;
     bool library_requires_init(uint32_t library) const;

@@ -157,6 +157,34 @@ static int cmd_load(int argc, char** argv) {
     return 0;
 }
 
+// loadbench <archive> <rank> <world> <reps> [share] [lanes]: warm-process LOAD
+// (one device, `reps` loads back to back), one JSON line of phase times per
+// load; FOUNDRY_DEBUG=1 adds the phase timeline on stderr.
+static int cmd_loadbench(int argc, char** argv) {
+    if (argc < 6) return 64;
+    LoadOptions o;
+    o.rank = static_cast<uint32_t>(std::stoul(argv[3]));
+    o.world = static_cast<uint32_t>(std::stoul(argv[4]));
+    const int reps = std::stoi(argv[5]);
+    o.share_execs = argc > 6 && std::string(argv[6]) == "share";
+    o.prepare_lanes = argc > 7 ? static_cast<unsigned>(std::stoul(argv[7])) : std::thread::hardware_concurrency();
+    Device dev(0);
+    for (int i = 0; i < reps; ++i) {
+        const auto t0 = std::chrono::steady_clock::now();
+        ServingContext sc = load(dev, argv[2], o);
+        const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        const auto& t = sc.timings();
+        std::printf("{\"rep\": %d, \"wall_ms\": %.3f, \"total_ms\": %.3f, \"stage_ms\": %.3f, "
+                    "\"integrity_ms\": %.3f, \"restore_ms\": %.3f, \"region_ms\": %.3f, \"materialize_ms\": %.3f, "
+                    "\"download_ms\": %.3f, \"build_ms\": %.3f, \"function_load_ms\": %.3f, "
+                    "\"instantiate_ms\": %.3f, \"foreground_ms\": %.3f}\n",
+                    i, wall, t.total_ms, t.stage_ms, t.integrity_ms, t.restore_ms, t.region_ms, t.materialize_ms,
+                    t.download_ms, t.build_ms, t.function_load_ms, t.instantiate_ms, t.foreground_ms);
+        std::fflush(stdout);
+    }
+    return 0;
+}
+
 // restorebench <archive>: where the binary-restore time goes (driver-cost
 // study): cuLibraryLoadData alone, + cuLibraryGetKernel, + cuKernelGetFunction,
 // sequential and from T host threads.
@@ -239,7 +267,85 @@ static int cmd_restorebench(int argc, char** argv) {
                     ms, ks.size(), 1e3 * ms / ks.size());
         for (CUlibrary l : libs) api.cuLibraryUnload(l);
     };
+    // per-call costs from T threads, every library loaded first:
+    //   getkernel    cuLibraryGetKernel by name for every entry
+    //   enumerate    cuLibraryGetKernelCount + cuLibraryEnumerateKernels + cuKernelGetName
+    //   setattr      cuKernelSetAttribute(MAX_DYNAMIC_SHARED_SIZE_BYTES, 64 KiB) per kernel
+    //   getfunction  cuKernelGetFunction (the function load) per kernel
+    //   funcattr     cuFuncSetAttribute(MAX_DYNAMIC_SHARED_SIZE_BYTES, 72 KiB) per loaded function
+    auto run_calls = [&](const char* what, int threads) {
+        std::vector<CUlibrary> libs(bins.size(), nullptr);
+        std::vector<std::vector<CUkernel>> ks(bins.size());
+        for (size_t i = 0; i < bins.size(); ++i)
+            cu_check(api.cuLibraryLoadData(&libs[i], bins[i].cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
+                     "load");
+        const std::string w = what;
+        auto get_kernels = [&](size_t i) {
+            ks[i].resize(bins[i].names.size());
+            for (size_t j = 0; j < ks[i].size(); ++j)
+                cu_check(api.cuLibraryGetKernel(&ks[i][j], libs[i], bins[i].names[j].c_str()), "getkernel");
+        };
+        if (w != "getkernel" && w != "enumerate")
+            for (size_t i = 0; i < bins.size(); ++i) get_kernels(i);
+        std::vector<std::vector<CUfunction>> fs(bins.size());
+        if (w == "funcattr")
+            for (size_t i = 0; i < bins.size(); ++i)
+                for (CUkernel k : ks[i]) {
+                    CUfunction f;
+                    cu_check(api.cuKernelGetFunction(&f, k), "getfunction");
+                    fs[i].push_back(f);
+                }
+        std::atomic<size_t> next{0};
+        std::atomic<size_t> calls{0};
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (int t = 0; t < threads; ++t)
+            pool.emplace_back([&] {
+                dev.make_current();
+                for (size_t i; (i = next.fetch_add(1)) < bins.size();) {
+                    if (w == "getkernel") {
+                        get_kernels(i);
+                        calls += ks[i].size();
+                    } else if (w == "enumerate") {
+                        unsigned n = 0;
+                        cu_check(api.cuLibraryGetKernelCount(&n, libs[i]), "count");
+                        ks[i].resize(n);
+                        cu_check(api.cuLibraryEnumerateKernels(ks[i].data(), n, libs[i]), "enumerate");
+                        for (CUkernel k : ks[i]) {
+                            const char* nm = nullptr;
+                            cu_check(api.cuKernelGetName(&nm, k), "name");
+                        }
+                        calls += n;
+                    } else if (w == "setattr") {
+                        CUdevice d;
+                        api.cuCtxGetDevice(&d);
+                        for (CUkernel k : ks[i])
+                            cu_check(api.cuKernelSetAttribute(CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 65536, k, d),
+                                     "setattr");
+                        calls += ks[i].size();
+                    } else if (w == "getfunction") {
+                        for (CUkernel k : ks[i]) {
+                            CUfunction f;
+                            cu_check(api.cuKernelGetFunction(&f, k), "getfunction");
+                        }
+                        calls += ks[i].size();
+                    } else if (w == "funcattr") {
+                        for (CUfunction f : fs[i])
+                            cu_check(api.cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 73728),
+                                     "funcattr");
+                        calls += fs[i].size();
+                    }
+                }
+            });
+        for (auto& t : pool) t.join();
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        std::printf("%-12s threads %2d: %8.3f ms for %zu calls (%.2f us per call, wall)\n", what, threads, ms,
+                    calls.load(), 1e3 * ms / std::max<size_t>(1, calls.load()));
+        for (CUlibrary l : libs) api.cuLibraryUnload(l);
+    };
     run("warm-up", 2, 1);
+    for (const char* w : {"getkernel", "enumerate", "setattr", "getfunction", "funcattr"})
+        for (int threads : {1, 4, 8}) run_calls(w, threads);
     for (int threads : {1, 2, 4, 8, 16, 1}) run_funcs(threads);
     for (int threads : {1, 4, 16}) {
         run("cuLibraryLoadData", 0, threads);
@@ -707,6 +813,7 @@ int main(int argc, char** argv) {
         if (cmd == "load") return cmd_load(argc, argv);
         if (cmd == "instbench") return cmd_instbench(argc, argv);
         if (cmd == "overlapbench") return cmd_overlapbench(argc, argv);
+        if (cmd == "loadbench") return cmd_loadbench(argc, argv);
         if (cmd == "cuda-init") {  // fresh-process floor: create the device context, nothing else
             fdy_device* d = nullptr;
             if (fdy_device_open(argc > 2 ? std::atoi(argv[2]) : 0, &d)) return 1;

@@ -351,3 +351,21 @@ def test_device_updates_random_serve_order(foundry, load, oracle, archives):
             h.serve(b)
             h.serve(b)               # no-op: already applied
         assert h.replay(b) == want[b], "step %d batch %d" % (i, b)
+
+
+@pytest.mark.parametrize("share", [False, True])
+def test_restored_shared_memory_limits_allow_large_launches(foundry, load, oracle, archives, tmp_path, share):
+    """Function attributes recorded at capture are restored at LOAD: every
+    kernel node launches with as much dynamic shared memory as its recorded
+    MAX_DYNAMIC_SHARED_SIZE_BYTES allows (> 48 KiB), which the device accepts
+    only if the limit was applied to the function the graph launches."""
+    import tier_s
+    src, _ = archives("moe-spmd")
+    arch = tier_s.make_big_smem(src, str(tmp_path / "big"), oracle.crc64)
+    foundry._foundry._pack_store(arch)
+    h = load(arch, rank=1, world=4, share_execs=share)
+    want = expected_traces(oracle, arch, 1, 4)
+    for b in h.batches()[::17] + [h.batches()[-1]]:
+        assert h.replay(b) == want[b], "batch %d" % b
+    import re
+    assert max(int(x) for x in re.findall(r"shmem=(\d+)", want[h.batches()[-1]])) > 48 * 1024

@@ -60,3 +60,35 @@ def make_tier_s(src: str, dst: str, crc64, seed: int = 7) -> str:
     os.remove(os.path.join(dst, "templates.fdt"))
     json.dump(m, open(os.path.join(dst, "manifest"), "w"))
     return dst
+
+
+def make_big_smem(src: str, dst: str, crc64) -> str:
+    """Every kernel node whose recorded function attribute allows more than
+    48 KiB of dynamic shared memory launches with exactly that much (the
+    attribute's value). Such a launch is only valid if LOAD restored the
+    function's MAX_DYNAMIC_SHARED_SIZE_BYTES on this device."""
+    shutil.copytree(src, dst)
+    m = json.load(open(os.path.join(dst, "manifest")))
+    raw = open(os.path.join(dst, "graphs.bin"), "rb").read()
+    (version,) = struct.unpack_from("<H", raw, 4)
+    graphs = fndg.graphs(raw)
+    big = 0
+    for g in graphs:
+        for n in g.nodes:
+            if n.type == 0:
+                (limit,) = struct.unpack_from("<i", n.fattrs, 0)
+                if limit > 48 * 1024:
+                    n.shmem = limit
+                    big += 1
+    assert big > 0
+    data, locs = fndg.write_container(graphs, version, crc64)
+    open(os.path.join(dst, "graphs.bin"), "wb").write(data)
+    by_label = {l[0]: l for l in locs}
+    for grp in m["grouping"]["groups"]:
+        grp["locators"] = [list(by_label[l[0]]) for l in grp["locators"]]
+    m["files"]["graphs.bin"] = crc64(data)
+    m["files"].pop("templates.fdt", None)
+    if os.path.exists(os.path.join(dst, "templates.fdt")):
+        os.remove(os.path.join(dst, "templates.fdt"))
+    json.dump(m, open(os.path.join(dst, "manifest"), "w"))
+    return dst
