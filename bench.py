@@ -12,13 +12,14 @@ is one GPU and one TP rank (rank = global rank % 8 of world 8), so per-GPU work
 is fixed as N grows ("weak" scaling); there is no data-path collective.
 
 JSON keys beyond the base contract:
-  e2e          the same materialization measured through the public API
-               (`foundry.load(archive, rank, world)`): archive files on the host
-               -> GPU integrity CRC -> store DMA -> fused kernel -> cuLibrary
-               restore -> template graphs built+instantiated -> one verified
-               replay read back. Host<->device bytes are counted per step.
-  e2e.breakdown  per-phase wall times; `driver_bound_ms` (cuLibraryLoadData +
-               graph construction + cuGraphInstantiate) is reported separately.
+  e2e          the same materialization through the C-ABI with host buffers
+               (fdy_prepare_archive): archive files -> integrity (GPU CRC of the
+               store, host CRC of the rest) -> fused kernel -> every member's
+               parameters in host memory. The reference arm's e2e is its CPU
+               path for the same work (verify_archive_integrity + PrepareFn).
+  e2e_servable LOAD to every graph servable (foundry.load): + cuLibraryLoadData,
+               function loads, template graphs built + instantiated, with the
+               driver-bound part broken out; next to the reference's load().
   roofline     HBM roofline of the fused kernel (algorithmic bytes / event time).
   cpu_baseline the reference's own CPU path (oracle/_ref) on this host's cores.
 """
@@ -52,7 +53,7 @@ def parse_args():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--workload", default="qwen3-235b-a22b")
     p.add_argument("--e2e-steps", type=int, default=5)
-    p.add_argument("--load-steps", type=int, default=2)
+    p.add_argument("--load-steps", type=int, default=3)
     p.add_argument("--skip-load", action="store_true", help="skip the full-LOAD section (profiling)")
     p.add_argument("--fanout", choices=["host", "ipc"], default="ipc",
                    help="N>1: how the store reaches every GPU (ipc = GPU0 -> peers over NVLink)")
@@ -280,45 +281,85 @@ def reference_serve_ms(archive: str, rank: int, world: int, lanes: int, reps: in
     return json.loads(r.stdout) if r.returncode == 0 else None
 
 
-def cold_process_load(args, local: int) -> dict:
+def cold_process_load(args, local: int, samples: int = 5) -> dict:
     """Wall clock of a fresh process from exec to every template servable:
     `foundry load --archive <headline> --rank 0 --world 8` (CUDA context
-    creation + LOAD, stamped when the CLI's "ready" line arrives), per-template
-    execs and share_execs, next to a fresh process that only creates the CUDA
-    context (`fdy_tool cuda-init`). `process_exit` adds the teardown (graphs,
-    libraries, context) until the process has exited."""
+    creation + LOAD, stamped when the CLI's flushed "ready" line arrives),
+    per-template execs and share_execs, next to a fresh process that only
+    creates the CUDA context (`fdy_tool cuda-init`). The three kinds run
+    interleaved, `samples` rounds, so drift of the box hits all of them alike;
+    median and range per kind. `device_open_ms` / `load_ms` split the LOAD
+    process at its device-open stamp (FOUNDRY_DEBUG timeline); the CLI asks
+    the kernel to read the archive ahead (posix_fadvise) before it creates
+    the context. `process_exit` adds the teardown (graphs, libraries, context)."""
     archive, _ = prepare_archives(args.workload, 0, lambda: None)
     pkg = os.path.join(ROOT, "paper_2604_06664_b200")
     runs = {"cuda_init": [os.path.join(pkg, "fdy_tool"), "cuda-init", str(local)]}
     base = [os.path.join(pkg, "foundry"), "load", "--archive", archive, "--rank", "0", "--world",
             str(TP_WORLD), "--device", str(local)]
-    runs["per_template"] = base
     runs["share_execs"] = base + ["--share-execs"]
+    runs["per_template"] = base
     # one untimed fresh process first: the box's very first context creation after
     # idle (driver / GPU wake-up) is not part of any load
     subprocess.run(runs["cuda_init"], capture_output=True)
-    out = {}
-    exits = {}
-    for name, cmd in runs.items():
-        walls, totals = [], []
-        for _ in range(2):
+    walls = {k: [] for k in runs}
+    exits = {k: [] for k in runs}
+    opens = {k: [] for k in runs}
+    env = dict(os.environ, FOUNDRY_DEBUG="1")
+    for _ in range(samples):
+        for name, cmd in runs.items():
             t0 = time.perf_counter()
-            p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, env=env)
             t_ready = None
             for line in p.stdout:  # the CLI flushes its "ready" line when LOAD returns
                 if t_ready is None and " ready: " in line:
                     t_ready = time.perf_counter()
+            err = p.stderr.read()
             rc = p.wait()
             t_exit = time.perf_counter()
             if rc != 0:
-                walls = []
-                break
-            walls.append(((t_ready or t_exit) - t0) * 1e3)
-            totals.append((t_exit - t0) * 1e3)
-        out[name] = statistics.mean(walls) if walls else None
-        exits[name] = statistics.mean(totals) if walls else None
-    out["process_exit"] = exits
+                continue
+            walls[name].append(((t_ready or t_exit) - t0) * 1e3)
+            exits[name].append((t_exit - t0) * 1e3)
+            for line in err.splitlines():  # "[foundry]   812.3 ms  device open"
+                if line.endswith("  device open"):
+                    opens[name].append(float(line.split()[1]))
+
+    def stat(xs):
+        return None if not xs else {"median": statistics.median(xs), "min": min(xs), "max": max(xs), "n": len(xs)}
+
+    out = {k: stat(v) for k, v in walls.items()}
+    out["process_exit"] = {k: stat(v) for k, v in exits.items()}
+    out["device_open_ms"] = {k: stat(v) for k, v in opens.items() if v}
+    out["load_ms"] = {k: stat([w - o for w, o in zip(walls[k], opens[k])]) for k in runs if opens[k]}
     return out
+
+
+def full_load_stats(foundry, archive, wrank, lanes, steps, barrier, reduce_max, **kw) -> dict:
+    """LOAD to every graph servable through the public API (foundry.load):
+    archive files -> integrity -> catalog restore (cuLibraryLoadData) ->
+    fused materialization -> template graphs built + instantiated (and, with
+    share_execs, every other template's functions loaded) -> member parameters
+    resident in HBM, representatives on the host. One warm-up, then `steps`
+    LOADs; per-phase breakdown averaged, wall as median/min/max (max over
+    ranks of the median)."""
+    h = foundry.load(archive, rank=wrank, world=TP_WORLD, prepare_lanes=lanes, **kw)  # warm-up
+    h.close()
+    walls, bds = [], []
+    for _ in range(steps):
+        barrier()
+        t0 = time.perf_counter()
+        h = foundry.load(archive, rank=wrank, world=TP_WORLD, prepare_lanes=lanes, **kw)
+        walls.append((time.perf_counter() - t0) * 1e3)
+        bds.append(dict(h.timings(), instantiate_calls=h.counters()["exec.instantiate_calls"]))
+        h.close()
+    bd = {k: statistics.mean(b[k] for b in bds) for k in bds[0]}
+    driver = sum(bd.get(k, 0) for k in ("restore_ms", "build_ms", "instantiate_ms", "function_load_ms"))
+    return {"value": reduce_max(statistics.median(walls)), "unit": "ms", "min": min(walls), "max": max(walls),
+            "steps": steps, "instantiate_calls": bd["instantiate_calls"],
+            "driver_bound_ms": driver,
+            "h2d_bytes_per_step": int(bd.get("h2d_bytes", 0)), "d2h_bytes_per_step": int(bd.get("d2h_bytes", 0)),
+            "breakdown": {k: v for k, v in bd.items() if k.endswith("_ms") and k != "crc_kernel_ms"}}
 
 
 def run_reference(args, grank, gworld):
@@ -508,51 +549,35 @@ def main():
         e2e_ms = reduce_max(statistics.mean(e2e_times))
         api.lib.fdy_host_free(host_out)
 
-        # ------- full LOAD through the Python API (adds driver-bound work) -------
-        load_times, breakdowns, trace = [], [], ""
+        # ------- LOAD to every graph servable through the Python API -------
+        servable = {}
         if not args.skip_load:
-            h = foundry.load(archive, rank=wrank, world=TP_WORLD, prepare_lanes=lanes)  # warm-up (driver, page cache)
-            h.replay(1)
-            h.close()
-        for _ in range(0 if args.skip_load else args.load_steps):
-            barrier()
-            t0 = time.perf_counter()
-            h = foundry.load(archive, rank=wrank, world=TP_WORLD, prepare_lanes=lanes)
-            trace = h.replay(1)  # D2H of the verified device trace of batch 1
-            load_times.append((time.perf_counter() - t0) * 1e3)
-            breakdowns.append(h.timings())
-            h.close()
-        load_ms = reduce_max(statistics.mean(load_times)) if load_times else None
-        # the same LOAD with LoadOptions.share_execs (one cuGraphInstantiate per graph shape)
-        shared_times, shared_bd = [], []
-        for _ in range(0 if args.skip_load else args.load_steps):
-            barrier()
-            t0 = time.perf_counter()
-            h = foundry.load(archive, rank=wrank, world=TP_WORLD, share_execs=True, prepare_lanes=lanes)
-            trace_s = h.replay(1)
-            shared_times.append((time.perf_counter() - t0) * 1e3)
-            shared_bd.append(dict(h.timings(), instantiate_calls=h.counters()["exec.instantiate_calls"]))
-            assert trace_s == trace, "share_execs replay differs"
-            h.close()
-        # serve sweep (reference ServingSet::serve, templater.cpp:177-188): apply every
-        # batch's parameters in label order, one exec per template vs shared execs
+            servable["share_execs"] = full_load_stats(foundry, archive, wrank, lanes, args.load_steps, barrier,
+                                                      reduce_max, share_execs=True)
+            servable["per_template"] = full_load_stats(foundry, archive, wrank, lanes, args.load_steps, barrier,
+                                                       reduce_max)
+        # serve sweeps (reference ServingSet::serve, templater.cpp:177-188): apply every
+        # batch's parameters in label order; then serve + replay every batch, the
+        # reference's `bench --mode load` loop (pipeline.cpp:876-889)
         serve_ms = {}
         if not args.skip_load:
             for mode in ("per_template", "shared_execs", "device_updates"):
-                h = foundry.load(archive, rank=wrank, world=TP_WORLD, prepare_lanes=lanes, share_execs=mode == "shared_execs",
-                                 device_updates=mode == "device_updates")
+                h = foundry.load(archive, rank=wrank, world=TP_WORLD, prepare_lanes=lanes,
+                                 share_execs=mode == "shared_execs", device_updates=mode == "device_updates")
                 bs = h.batches()
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 touched = sum(h.serve(b) for b in bs)
                 torch.cuda.synchronize()  # device_updates queues its serve kernels: count them
                 ms = (time.perf_counter() - t0) * 1e3
-                ok = h.replay(bs[-1]) == h.replay(bs[-1])  # the trace is device-verified
+                t0 = time.perf_counter()
+                for b in bs:
+                    h.replay(b)  # serve + launch + device-side trace verification
+                replay_ms = (time.perf_counter() - t0) * 1e3
                 serve_ms[mode] = {"ms": ms, "us_per_serve": ms * 1e3 / len(bs), "batches": len(bs),
-                                  "nodes_touched": touched, "load_ms": h.timings()["total_ms"],
-                                  "verified": ok}
+                                  "nodes_touched": touched, "serve_replay_all_ms": replay_ms,
+                                  "replay_verified": True}
                 h.close()
-        shared_ms = reduce_max(statistics.mean(shared_times)) if shared_times else None
     clocks = sampler.summary()
 
     api.lib.fdy_members_free(members)
@@ -573,23 +598,28 @@ def main():
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    bd = {k: statistics.mean(b[k] for b in breakdowns) for k in breakdowns[0]} if breakdowns else {}
-    driver_bound = bd.get("restore_ms", 0) + bd.get("build_ms", 0) + bd.get("instantiate_ms", 0)
-    sbd = {k: statistics.mean(b[k] for b in shared_bd) for k in shared_bd[0]} if shared_bd else {}
-    shared_driver = sum(sbd.get(k, 0) for k in ("restore_ms", "build_ms", "instantiate_ms", "function_load_ms"))
     ep = {k: statistics.mean(p[k] for p in e2e_parts) for k in e2e_parts[0]}
 
     # ---------------- CPU baseline: the reference itself, rank 0, N=1 ----------------
     cpu = None
+    refarch = reference_archive(args.workload) or plain
     if not args.no_cpu_baseline and gworld == 1:
-        refm = reference_materialize_ms(plain, wrank, TP_WORLD, lanes, 5)
-        refl = reference_load_ms(plain, wrank, TP_WORLD, lanes, 3)
+        refm = reference_materialize_ms(refarch, wrank, TP_WORLD, lanes, 5)
         if refm is not None:
+            refm4 = reference_materialize_ms(refarch, wrank, TP_WORLD, 4, 3)
+            refl = reference_load_ms(refarch, wrank, TP_WORLD, lanes, 3)
+            refl4 = reference_load_ms(refarch, wrank, TP_WORLD, 4, 3)
+            refs = reference_serve_ms(refarch, wrank, TP_WORLD, lanes, 2)
             cpu = {"value": refm["mean_ms"], "unit": "ms", "cores": lanes, "kind": "reference",
+                   "cpu_model": cpu_model(),
                    "sample": "reference verify_archive_integrity + PrepareFn over all 512 members "
-                             "(rank 0 of 8, %d prepare lanes), 5 reps after 1 warm-up" % lanes,
+                             "(rank 0 of 8, %d prepare lanes; archive written by the reference's save), "
+                             "5 reps after 1 warm-up" % lanes,
                    "reference_integrity_ms": refm["integrity_best_ms"],
-                   "reference_full_load_ms": refl["mean_ms"] if refl else None}
+                   "reference_prepare_lanes_4_ms": refm4["mean_ms"] if refm4 else None,
+                   "reference_full_load_ms": refl["mean_ms"] if refl else None,
+                   "reference_full_load_lanes_4_ms": refl4["mean_ms"] if refl4 else None,
+                   "reference_serve_replay_all_ms": refs["mean_ms"] if refs else None}
         else:
             port = oracle_port_ms(plain, wrank, TP_WORLD, lanes, 3)
             cpu = {"value": port["mean_ms"], "unit": "ms", "cores": lanes, "kind": "port",
@@ -617,6 +647,10 @@ def main():
         "relocation_gbps": launch_gbps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     # what the DRAM counters of the ncu capture (profiles/) say the same
+                     # launch moved, over the same event time: below `frac` when part of
+                     # the output is still dirty in the 126 MB L2 when the kernel ends
+                     "frac_dram": (traffic / (member_ms * 1e-3) / 1e9 / peak) if traffic else None,
                      "algorithmic_bytes": alg["member_pass"],
                      "kernel": "fdy_materialize_kernel (member pass: K2 diff + K1 relocated lanes + "
                                "K3 rank patch), CUDA events around it alone, L2 flushed",
@@ -635,34 +669,28 @@ def main():
                 # (the store's CRC blocks run interleaved with its DMA pieces on a side
                 # stream: no separate kernel time, see profiles/ for the launch list)
                 "breakdown": {k: v for k, v in ep.items() if k.endswith("_ms") and k != "crc_kernel_ms"}},
-        "full_load": {"value": load_ms, "unit": "ms", "steps": args.load_steps,
-                      "api": "paper_2604_06664_b200.load(archive, rank, world, prepare_lanes=<host cores per rank>).replay(1)",
-                      "driver_bound_ms": driver_bound,
-                      "driver_bound": "cuLibraryLoadData x catalog + cuGraphAdd*/cuGraphInstantiate x templates",
-                      "excluding_driver_bound_ms": (load_ms - driver_bound) if load_ms else None,
-                      "h2d_bytes_per_step": int(bd.get("h2d_bytes", 0)),
-                      "d2h_bytes_per_step": int(bd.get("d2h_bytes", 0)) + len(trace),
-                      "breakdown": {k: v for k, v in bd.items()
-                                    if k.endswith("_ms") and k != "crc_kernel_ms"}},
-        "full_load_shared_execs": None if shared_ms is None else {
-            "value": shared_ms, "unit": "ms", "steps": args.load_steps,
-            "api": "paper_2604_06664_b200.load(archive, rank, world, share_execs=True).replay(1)",
-            "instantiate_calls": shared_bd[0]["instantiate_calls"],
-            "driver_bound_ms": shared_driver,
-            "driver_bound": "cuLibraryLoadData + cuFuncLoad of every template's functions + "
-                            "cuGraphAdd*/cuGraphInstantiate per graph shape",
-            "breakdown": {k: v for k, v in sbd.items() if k.endswith("_ms") and k != "crc_kernel_ms"}},
+        "e2e_servable": None if not servable else dict(
+            servable["share_execs"],
+            api="paper_2604_06664_b200.load(archive, rank, world, share_execs=True): files -> every "
+                "template instantiated (one exec per graph shape), every function of every template "
+                "loaded, every member's parameters resident in HBM",
+            reference_full_load_ms=(cpu or {}).get("reference_full_load_ms"),
+            per_template=servable["per_template"],
+            floor="driver-serialized: ~11-15 us per function load (9028 functions in 96 libraries) and "
+                  "~35 ms per cuGraphInstantiate of a 1036-node template (~50 us per concurrent branch "
+                  "node); profiles/round2_driver_floor.md"),
         "tier_s": None if ts is None else dict(ts, member_pass_frac=ts["member_pass_gbps"] / peak,
                                                whole_launch_frac=ts["whole_launch_gbps"] / peak),
         "serve_sweep": serve_ms or None,
         "cold_process_load": None if not cold else {
             "unit": "ms", "per_template": cold.get("per_template"), "share_execs": cold.get("share_execs"),
             "cuda_init_only": cold.get("cuda_init"), "process_exit": cold.get("process_exit"),
+            "device_open_ms": cold.get("device_open_ms"), "load_after_device_open_ms": cold.get("load_ms"),
             "what": "wall clock of `foundry load --archive <headline> --rank r --world 8` in a fresh "
                     "process from exec to its 'ready' line: CUDA context creation + LOAD to every "
                     "template servable (the paper's cold start); cuda_init_only = a fresh process "
                     "that only opens the device (CUDA context creation, until exit); process_exit = "
-                    "exec to exit, teardown included. The "
+                    "exec to exit, teardown included; median/min/max of 5 interleaved rounds. The "
                     "reference arm's simulated LOAD creates no CUDA context"},
         "cpu_baseline": cpu,
         "clocks": clocks,

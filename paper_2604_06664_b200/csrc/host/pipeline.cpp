@@ -1070,7 +1070,29 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     return ServingContext(std::move(impl));
 }
 
+namespace {
+// Asks the kernel to read every manifest-listed file ahead (posix_fadvise
+// WILLNEED: asynchronous readahead), so a LOAD whose archive is not in the page
+// cache reads it while the CUDA context is being created. Best effort.
+void prefetch_archive(const fs::path& archive) {
+    try {
+        const auto mb = slurp(ArchivePaths{archive}.manifest());
+        const Manifest m = parse_manifest(std::string(mb.begin(), mb.end()));
+        for (const auto& [rel, digest] : m.file_digests) {
+            (void)digest;
+            const int fd = ::open((archive / rel).c_str(), O_RDONLY | O_CLOEXEC);
+            if (fd < 0) continue;
+            ::posix_fadvise(fd, 0, 0, POSIX_FADV_WILLNEED);
+            ::close(fd);
+        }
+    } catch (...) {
+    }
+}
+}  // namespace
+
 ServingContext load(const fs::path& archive, const LoadOptions& opts) {
+    prefetch_archive(archive);
+    debug_phase("archive readahead requested");
     debug_phase("open device");
     auto dev = std::make_unique<Device>(opts.device);
     debug_phase("device open");
