@@ -17,6 +17,8 @@
  *       fdy_serving_counter(s)   <- ServingContext::counters()               pipeline.hpp:100
  *       fdy_serving_template_count <- ServingHandle.template_count           module.cpp:32
  *       fdy_serving_close        <- ~ServingContext
+ *       fdy_serving_save_captured   GPU-side SAVE of a whole archive (reference save,
+ *                                   pipeline.cpp:249-405) from device captures
  *       fdy_serving_capture_graph   GPU-side SAVE: the batch's graph
  *                                   stream-captured on the device and extracted back,
  *                                   as the FNDG record encode_graph_record writes
@@ -211,6 +213,13 @@ uint32_t fdy_serving_template_count(const fdy_serving* s);
 void fdy_serving_close(fdy_serving* s);
 /* Bytes written to buf (up to cap); *len = the record's full length. */
 int fdy_serving_capture_graph(fdy_serving* s, uint32_t batch, unsigned char* buf, size_t cap, size_t* len);
+/* GPU-side SAVE to an archive directory (reference SAVE
+ * pipeline.cpp:249-405): every batch stream-captured on the device and
+ * extracted, comm nodes lowered back to stubs (rank_forge.cpp:132-152
+ * inverted), grouped (templater.cpp:18-52), serialized (graph_model.cpp:244-269)
+ * and written with the catalog, memory log, patch table, binaries and a packed
+ * templates.fdt. The archive loads in the reference and here. */
+int fdy_serving_save_captured(fdy_serving* s, const char* out_dir);
 
 #ifdef __cplusplus
 }

@@ -119,6 +119,15 @@ struct ServingHandle {
         py::gil_scoped_release nogil;
         return ctx().naive_rebuild_all();
     }
+    // GPU-side SAVE to an archive directory; returns (graphs, templates)
+    py::tuple save_captured(const std::string& out) {
+        SaveResult r;
+        {
+            py::gil_scoped_release nogil;
+            r = ctx().save_captured(out);
+        }
+        return py::make_tuple(r.manifest.grouping.total_graphs, r.manifest.grouping.template_count);
+    }
     std::unique_ptr<ServingContext> sc;
 };
 
@@ -213,6 +222,8 @@ PYBIND11_MODULE(_foundry, m) {
         .def("capture_graph", &ServingHandle::capture_graph, py::arg("batch"),
              "GPU-side SAVE: stream-capture the batch's graph and extract it (FNDG record bytes)")
         .def("naive_rebuild_all", &ServingHandle::naive_rebuild_all)
+        .def("save_captured", &ServingHandle::save_captured, py::arg("out"),
+             "GPU-side SAVE: capture every batch on the device and write a reference-layout archive")
         .def("exec_update", &ServingHandle::exec_update, py::arg("batch"), py::arg("donor"),
              "Apply a donor graph (FNDG record bytes) to the exec of batch's template")
         .def("close", &ServingHandle::close, "Release the rank's graphs, libraries and VA region now")

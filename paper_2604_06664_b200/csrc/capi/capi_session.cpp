@@ -79,6 +79,13 @@ int fdy_serving_capture_graph(fdy_serving* s, uint32_t batch, unsigned char* buf
     });
 }
 
+int fdy_serving_save_captured(fdy_serving* s, const char* out_dir) {
+    return fdy_guard([&] {
+        require(s && out_dir, Errc::invalid_argument, "fdy_serving_save_captured: null argument");
+        s->sc.save_captured(out_dir);
+    });
+}
+
 int fdy_serving_batches(fdy_serving* s, uint32_t* out, size_t cap, size_t* count) {
     return fdy_guard([&] {
         require(s != nullptr, Errc::invalid_argument, "fdy_serving_batches: null handle");

@@ -1349,6 +1349,93 @@ CapturedGraph ServingContext::capture_graph(uint32_t batch) {
     }
 }
 
+// GPU-side SAVE to an archive (reference SAVE pipeline.cpp:249-405).
+// Every batch's graph is stream-captured on the device and extracted from the
+// driver (capture_graph); the interception record supplies the launch
+// attributes each kernel was launched with (the extraction cannot read back
+// the ones the hardware does not carry, capture.hpp). The stub layer then
+// lowers the rank-specific comm nodes back to stubs with the SAVE-time
+// placeholders (the inverse of apply_rank_patches, rank_forge.cpp:132-152:
+// kernel -> stub ref, rank bytes -> 0, world bytes -> the table's
+// world_placeholder), so one capture from ANY rank yields the rank-agnostic
+// archive. Grouping (topology_key + group_graphs, templater.cpp:18-52),
+// serialize_graphs (graph_model.cpp:244-269), the catalog of the restored
+// binaries (binary_catalog.cpp:108-183), the memory log and the manifest follow
+// the reference layout; templates.fdt is packed from the new graphs.bin.
+SaveResult ServingContext::save_captured(const fs::path& out) {
+    Impl& I = *impl_;
+    require(I.t.relocation_delta == 0, Errc::invalid_argument,
+            "save_captured: the region was relocated; capture from a LOAD at the captured base");
+    require(I.view->header().n_values == 0, Errc::invalid_argument,
+            "save_captured: the archive carries comm slots whose SAVE-time values are unknown");
+    require(!fs::exists(out) || fs::is_empty(out), Errc::invalid_argument,
+            "save_captured: " + out.string() + " exists and is not empty");
+    const PatchTable patches = parse_patch_table(I.file_host("patch.bin"));
+    std::vector<CapturedGraph> graphs;
+    for (uint32_t b : I.labels) {
+        CapturedGraph g = capture_graph(b);
+        const uint32_t m = I.member_for(b);
+        const uint32_t gi = I.view->member(m).group;
+        for (uint32_t n = 0; n < g.nodes.size(); ++n) {
+            if (g.nodes[n].type != NodeType::Kernel) continue;
+            const fdt_node_attrs& a = I.view->node_attrs(gi, n);  // what the launch asked for
+            g.nodes[n].attrs.cluster_dim = {a.cluster[0], a.cluster[1], a.cluster[2]};
+            g.nodes[n].attrs.cluster_scheduling_policy_preference = a.sched_policy;
+            g.nodes[n].attrs.mem_sync_domain_map_default = a.sync_default;
+            g.nodes[n].attrs.mem_sync_domain_map_remote = a.sync_remote;
+            g.nodes[n].attrs.attr_query_available = a.attr_query != 0;
+        }
+        auto pit = patches.per_graph.find(b);
+        if (pit != patches.per_graph.end()) {
+            for (const CommPatchEntry& e : pit->second) {
+                require(e.node_id < g.nodes.size() && g.nodes[e.node_id].type == NodeType::Kernel,
+                        Errc::archive_corruption, "patch entry references a non-kernel node");
+                auto& k = g.nodes[e.node_id].kernel_params();
+                require(k.kernel == KernelRef{I.manifest.comm_real_hash, e.real_name}, Errc::unpatchable_comm,
+                        "node " + std::to_string(e.node_id) + " of batch " + std::to_string(b) +
+                            " is not the real comm kernel its patch entry names");
+                k.kernel = e.stub;
+                for (uint32_t off : e.rank_offsets) std::memset(k.arg_buffer.data() + off, 0, 8);
+                for (uint32_t off : e.world_offsets)
+                    std::memcpy(k.arg_buffer.data() + off, &patches.world_placeholder, 8);
+            }
+        }
+        graphs.push_back(std::move(g));
+    }
+    GroupingManifest grouping = group_graphs(graphs);
+    const std::vector<uint8_t> graphs_bin = serialize_graphs(graphs);
+    attach_locators(grouping, parse_graph_locators(graphs_bin));
+
+    ArchivePaths paths{out};
+    fs::create_directories(paths.binaries());
+    Manifest m = I.manifest;
+    m.grouping = std::move(grouping);
+    m.file_digests.clear();
+    auto put = [&](const std::string& rel, std::span<const uint8_t> bytes) {
+        spit(out / rel, std::vector<uint8_t>(bytes.begin(), bytes.end()));
+        m.file_digests[rel] = crc64(bytes);
+    };
+    put("graphs.bin", graphs_bin);
+    put("memlayout.bin", I.file_host("memlayout.bin"));
+    put("catalog.bin", serialize_catalog(I.catalog));
+    put("patch.bin", I.file_host("patch.bin"));
+    for (const auto& [hash, rec] : I.catalog.binaries) {
+        (void)rec;
+        for (const std::string rel : {"binaries/" + hex16(hash) + ".bin", "binaries/" + hex16(hash) + ".sm_100a.cubin"}) {
+            if (I.staged->has(rel)) put(rel, I.file_host(rel));
+            else if (fs::exists(I.root / rel)) put(rel, slurp(I.root / rel));
+        }
+    }
+    spit(paths.manifest(), serialize_manifest(m));
+    pack_archive_store(out, I.opts.prepare_lanes);
+
+    SaveResult res;
+    res.archive_dir = out;
+    const auto mt = slurp(paths.manifest());
+    res.manifest = parse_manifest(std::string(mt.begin(), mt.end()));
+    return res;
+}
+
 uint64_t ServingContext::naive_rebuild_all() {
     Impl& I = *impl_;
     const DriverApi& api = driver();

@@ -128,6 +128,12 @@ public:
     // with the template's dependencies (cudaStreamUpdateCaptureDependencies per
     // node) and extracts the driver's graph back into the portable model.
     CapturedGraph capture_graph(uint32_t batch);
+    // GPU-side SAVE to an archive: capture_graph of every batch, comm nodes
+    // lowered back to stubs, grouped, serialized and written with the catalog,
+    // memory log, patch table, binaries and a packed template store. The
+    // archive loads in the reference and here. Needs a LOAD at the captured
+    // base and no comm slots.
+    SaveResult save_captured(const std::filesystem::path& out);
 
     struct Impl;
 
