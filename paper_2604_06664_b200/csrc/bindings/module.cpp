@@ -156,7 +156,7 @@ ServingHandle do_load(const std::string& archive, uint32_t rank, uint32_t world,
                       int device, bool relocate, unsigned prepare_lanes, bool skip_binary_restore,
                       bool skip_device_init, int64_t base_shift_granules, bool extra_prewindow_alloc,
                       bool verify_replay, bool share_execs, bool device_updates,
-                      std::vector<uint64_t> comm_values) {
+                      std::vector<uint64_t> comm_values, bool fail_device_serve) {
     LoadOptions o;
     o.rank = rank;
     o.world = world;
@@ -172,6 +172,7 @@ ServingHandle do_load(const std::string& archive, uint32_t rank, uint32_t world,
     o.faults.skip_device_init = skip_device_init;
     o.faults.base_shift_granules = base_shift_granules;
     o.faults.extra_prewindow_alloc = extra_prewindow_alloc;
+    o.faults.fail_device_serve = fail_device_serve;
     py::gil_scoped_release nogil;
     return ServingHandle(load(archive, o));
 }
@@ -243,7 +244,7 @@ PYBIND11_MODULE(_foundry, m) {
           py::arg("skip_device_init") = false, py::arg("base_shift_granules") = 0,
           py::arg("extra_prewindow_alloc") = false, py::arg("verify_replay") = true,
           py::arg("share_execs") = false, py::arg("device_updates") = false,
-          py::arg("comm_values") = std::vector<uint64_t>{});
+          py::arg("comm_values") = std::vector<uint64_t>{}, py::arg("fail_device_serve") = false);
     // The stub layer's comm-slot authoring (archive.hpp CommSlotTable): writes
     // comm_slots.bin, records its digest in the manifest and re-packs the
     // template store if the archive has one.

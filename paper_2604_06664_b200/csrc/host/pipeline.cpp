@@ -96,7 +96,12 @@ struct ServingContext::Impl {
     std::vector<uint8_t> serve_member_host;           // per member: host path needed
     std::vector<uint32_t> serve_memop_base;           // per member: first slot in serve_plan_records
     std::vector<std::array<uint64_t, 3>> serve_plan_records;
+    // device updates that failed since the last check (host-mapped; the serve
+    // kernel writes them, replay() reads them): u32 "any" word, then one flag
+    // byte per member
+    PinnedBuffer serve_error;
     void build_serve_plan();
+    bool recover_device_serve(uint32_t gi);
     uint64_t serve_on_device(uint32_t gi, uint32_t m);
     std::vector<Group> groups;
     // share_execs: the group whose graph/exec serves group g (itself otherwise)
@@ -568,6 +573,8 @@ void ServingContext::Impl::build_serve_plan() {
     a.n_members = nm;
     cuda_check(fdy_launch_serve_plan(&a, dev->stream()), "serve plan launch");
     serve_member_host.assign(nm, 1);
+    serve_error = PinnedBuffer(*dev, sizeof(uint32_t) + nm);
+    std::memset(serve_error.data(), 0, sizeof(uint32_t) + nm);
     serve_plan_records.assign(slots, {0, 0, 0});
     if (nm) cuda_check(cudaMemcpyAsync(serve_member_host.data(), a.member_host, nm, cudaMemcpyDeviceToHost,
                                        dev->stream()), "serve plan D2H");
@@ -592,6 +599,10 @@ uint64_t ServingContext::Impl::serve_on_device(uint32_t gi, uint32_t m) {
     a.nodes = reinterpret_cast<const FdyServeNode*>(grp.d_serve_nodes.data());
     a.image = d_members.data() + view->member(m).out_off;
     a.n_nodes = G.n_nodes;  // host_flags / host_records null: nothing comes back
+    a.member = m;
+    a.error_word = reinterpret_cast<uint32_t*>(serve_error.data());
+    a.member_failed = serve_error.data() + sizeof(uint32_t);
+    a.inject_failure = opts.faults.fail_device_serve ? 1u : 0u;
     cuda_check(fdy_launch_serve(&a, dev->stream()), "serve kernel launch");
     uint64_t touched = grp.n_kernel_nodes;
     for (uint32_t k = 0; k < grp.memop_nodes.size(); ++k) {
@@ -614,6 +625,31 @@ uint64_t ServingContext::Impl::serve_on_device(uint32_t gi, uint32_t m) {
         ++touched;
     }
     return touched;
+}
+
+// Called with the device stream synchronized. A failed device update marks its
+// member for the host path (every later serve of it goes through the host) and,
+// if its exec still holds that member, forgets it, so the next apply
+// re-applies every node on the host. True when the exec of group gi was
+// affected.
+bool ServingContext::Impl::recover_device_serve(uint32_t gi) {
+    if (serve_error.size() == 0) return false;
+    volatile uint32_t* any = reinterpret_cast<volatile uint32_t*>(serve_error.data());
+    if (*any == 0) return false;
+    *any = 0;
+    volatile uint8_t* failed = serve_error.data() + sizeof(uint32_t);
+    bool mine = false;
+    for (uint32_t m = 0; m < serve_member_host.size(); ++m) {
+        if (!failed[m]) continue;
+        failed[m] = 0;
+        serve_member_host[m] = 1;
+        for (Group& g : groups) {
+            if (g.applied != m) continue;
+            g.applied = kNoMember;
+            mine = mine || &g == &exec_of(gi);
+        }
+    }
+    return mine;
 }
 
 uint64_t ServingContext::Impl::apply_member(uint32_t gi, uint32_t m) {
@@ -771,10 +807,11 @@ LaunchTrace ServingContext::Impl::replay(uint32_t batch) {
     ctx->reset_trace();
     cu_check(api.cuGraphLaunch(exec_of(gi).exec, dev->stream()), "cuGraphLaunch");
     ctx->c_replay.fetch_add(1);
-    if (!opts.verify_replay) {
-        dev->sync();
-        return trace;
-    }
+    dev->sync();
+    // a device serve that failed left its exec with stale parameters: re-apply
+    // that member on the host and, if it is this batch's, launch again
+    if (recover_device_serve(gi)) return replay(batch);
+    if (!opts.verify_replay) return trace;
     const std::vector<uint8_t> recs = ctx->read_trace();
     // index the expected launches by (entry id, parameter bytes)
     std::multimap<std::pair<uint32_t, uint64_t>, const Expect*> want;

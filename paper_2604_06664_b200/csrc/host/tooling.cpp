@@ -304,8 +304,12 @@ void unpack_archive_file(const fs::path& file, const fs::path& dir) {
         std::string rel;
         uint64_t offset, length, checksum;
     };
-    std::vector<Entry> entries(r.u32());
-    for (Entry& e : entries) {
+    // entries are appended one at a time (as the reference reads them), so a
+    // corrupt count fails as a cursor overrun rather than a huge allocation
+    const uint32_t count = r.u32();
+    std::vector<Entry> entries;
+    for (uint32_t i = 0; i < count; ++i) {
+        Entry& e = entries.emplace_back();
         e.rel = r.str();
         e.offset = r.u64();
         e.length = r.u64();

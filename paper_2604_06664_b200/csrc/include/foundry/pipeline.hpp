@@ -46,6 +46,9 @@ struct FaultInjection {
     bool skip_device_init = false;
     int64_t base_shift_granules = 0;
     bool extra_prewindow_alloc = false;
+    // B200 addition: the device serve kernel reports every update as failed
+    // (exercises the error word replay() checks; device_updates only)
+    bool fail_device_serve = false;
 };
 
 struct LoadOptions {

@@ -65,7 +65,11 @@ struct FdyServeArgs {
     const unsigned char* image;     // member image in HBM (descriptors + pool)
     uint8_t* host_flags;            // host-mapped: 0 applied on device, 1 memop, 2 host path
     uint64_t* host_records;         // host-mapped: 3 x u64 per node (memop records)
+    uint32_t* error_word;           // host-mapped: set to 1 when any device update fails, and
+    uint8_t* member_failed;         //   member_failed[member] = 1 (per-member flags)
     uint32_t n_nodes;
+    uint32_t member;
+    uint32_t inject_failure;        // FaultInjection::fail_device_serve
 };
 
 struct FdyCrcBlock {

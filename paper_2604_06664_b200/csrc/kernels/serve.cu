@@ -43,7 +43,17 @@ fdy_serve_kernel(const FdyServeArgs a) {
         for (uint32_t off = 16 * lane; off < s.param_bytes; off += 16 * 32)
             ok &= cudaGraphKernelNodeSetParam(node, off, blob + off, min(16u, s.param_bytes - off)) == cudaSuccess;
         if (lane == 0) ok &= cudaGraphKernelNodeSetGridDim(node, dim3(d.grid[0], d.grid[1], d.grid[2])) == cudaSuccess;
-        if (!__all_sync(0xFFFFFFFFu, ok)) flag = 2;  // the host re-applies the whole member
+        if (a.inject_failure) ok = false;
+        if (!__all_sync(0xFFFFFFFFu, ok)) {
+            flag = 2;  // the host re-applies the whole member
+            // nothing waits for this kernel: the word is checked at the next
+            // synchronization point (replay), which re-applies on the host
+            if (lane == 0 && a.error_word) {
+                a.member_failed[a.member] = 1;
+                __threadfence_system();
+                atomicOr(a.error_word, 1u);
+            }
+        }
     } else if (d.type == 1 || d.type == 2) {
         flag = 1;  // memop: host SetParams from the record below
         if (lane < 3 && a.host_records) a.host_records[3ull * n + lane] = reinterpret_cast<const uint64_t*>(blob)[lane];

@@ -333,13 +333,17 @@ def test_replay_equivalence_at_world_four(foundry, load, oracle, archives, name)
         assert h.replay(b) == want[b], "batch %d" % b
 
 
-def test_device_updates_random_serve_order(foundry, load, oracle, archives):
+@pytest.mark.parametrize("fail", [False, True])
+def test_device_updates_random_serve_order(foundry, load, oracle, archives, fail):
     """Asynchronous device serves in a random order, interleaved with serves
     that are not replayed (queued updates overwritten by later ones) and
-    with repeated batches: every replay still matches the oracle."""
+    with repeated batches: every replay still matches the oracle. With
+    fail=True every device update reports failure (FaultInjection
+    fail_device_serve): replay() finds the error flags at its synchronization
+    point, re-applies the failed members on the host and launches again."""
     import random
     arch, _ = archives("moe-spmd")
-    h = load(arch, rank=2, world=8, device_updates=True)
+    h = load(arch, rank=2, world=8, device_updates=True, fail_device_serve=fail)
     want = expected_traces(oracle, arch, 2, 8)
     rng = random.Random(11)
     bs = h.batches()
