@@ -39,6 +39,7 @@ HOST_SRCS = [
     "host/graph_model.cpp",
     "host/archive.cpp",
     "host/template_store.cpp",
+    "host/device_pack.cpp",
     "host/device.cpp",
     "host/workload.cpp",
     "host/save.cpp",
@@ -53,7 +54,7 @@ HOST_SRCS = [
     "capi/capi_kernels.cpp",
     "capi/capi_session.cpp",
 ]
-CU_SRCS = ["kernels/materialize.cu", "kernels/crc64.cu"]
+CU_SRCS = ["kernels/materialize.cu", "kernels/crc64.cu", "kernels/pack.cu"]
 RDC_SRCS = ["kernels/serve.cu"]  # device runtime (graph device updates): -rdc + device link
 
 

@@ -10,6 +10,7 @@
 #include <chrono>
 
 #include "foundry/bytes.hpp"
+#include "foundry/device_pack.hpp"
 #include "foundry/pipeline.hpp"
 #include "foundry/save.hpp"
 #include "foundry/template_store.hpp"
@@ -66,6 +67,7 @@ struct ServingHandle {
         d["download_ms"] = t.download_ms;
         d["build_ms"] = t.build_ms;
         d["function_load_ms"] = t.function_load_ms;
+        d["pack_ms"] = t.pack_ms;
         d["instantiate_ms"] = t.instantiate_ms;
         d["foreground_ms"] = t.foreground_ms;
         d["crc_kernel_ms"] = t.crc_kernel_ms;
@@ -300,6 +302,32 @@ PYBIND11_MODULE(_foundry, m) {
                                                {"rank_ops", st.rank_ops},
                                                {"member_image_bytes", st.member_image_bytes}};
     });
+    // The template store of an archive as bytes, packed on the host
+    // (pack_template_store) or on the GPU (pack_template_store_device, from a
+    // device copy of graphs.bin); with the GPU packer's phase timings.
+    m.def("_pack_store_bytes", [](const std::string& archive, bool gpu, int device) {
+        ArchivePaths paths{archive};
+        std::vector<uint8_t> out;
+        std::map<std::string, double> t;
+        {
+            py::gil_scoped_release nogil;
+            if (!gpu) {
+                const auto mtext = slurp(paths.manifest());
+                const Manifest man = parse_manifest(std::string(mtext.begin(), mtext.end()));
+                const bool has_slots = man.file_digests.count("comm_slots.bin") != 0;
+                out = pack_template_store(slurp(paths.graphs()), slurp(paths.patch_table()), man, 0, nullptr,
+                                          has_slots ? slurp(paths.comm_slots()) : std::vector<uint8_t>{});
+            } else {
+                Device dev(device);
+                DevicePackTimings tm;
+                out = pack_archive_store_device(dev, archive, &tm);
+                t = {{"prep_ms", tm.prep_ms}, {"pass1_ms", tm.pass1_ms}, {"host1_ms", tm.host1_ms}, {"pass2_ms", tm.pass2_ms},
+                     {"host2_ms", tm.host2_ms}, {"pass3_ms", tm.pass3_ms}, {"total_ms", tm.total_ms},
+                     {"kernel_keys", double(tm.kernel_keys)}, {"retries", double(tm.retries)}};
+            }
+        }
+        return py::make_tuple(py::bytes(reinterpret_cast<const char*>(out.data()), out.size()), t);
+    }, py::arg("archive"), py::arg("gpu") = true, py::arg("device") = 0);
     // member-image arena (the kernel's output layout) -> FNDG container in
     // graphs.bin locator order
     m.def("_decode_member_images", [](const std::string& archive, py::bytes arena_bytes) {

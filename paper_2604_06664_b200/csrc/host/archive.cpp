@@ -701,6 +701,68 @@ PatchTable parse_patch_table(std::span<const uint8_t> bytes) {
     return t;
 }
 
+uint32_t PatchEntryView::rank_offset(uint32_t i) const {
+    uint32_t v;
+    std::memcpy(&v, rank_offsets + 4ull * i, 4);
+    return v;
+}
+uint32_t PatchEntryView::world_offset(uint32_t i) const {
+    uint32_t v;
+    std::memcpy(&v, world_offsets + 4ull * i, 4);
+    return v;
+}
+
+PatchView parse_patch_view(std::span<const uint8_t> bytes) {
+    Cursor c(bytes, Errc::archive_corruption);
+    c.magic("FNDP");
+    const uint16_t version = c.u16();
+    require(version == 1, Errc::archive_corruption,
+            "unsupported patch table version " + std::to_string(version));
+    PatchView t;
+    t.world_placeholder = c.u64();
+    const uint32_t ng = c.u32();
+    t.graphs.reserve(std::min<size_t>(ng, bytes.size() / 8));
+    for (uint32_t g = 0; g < ng; ++g) {
+        const uint32_t label = c.u32();
+        const uint32_t n = c.u32();
+        const uint32_t first = static_cast<uint32_t>(t.entries.size());
+        for (uint32_t i = 0; i < n; ++i) {
+            PatchEntryView e;
+            e.node_id = c.u32();
+            e.stub_hash = c.u64();
+            e.stub_name = c.str_view();
+            e.real_name = c.str_view();
+            e.n_rank = c.u32();
+            e.rank_offsets = c.take(4ull * e.n_rank);
+            e.n_world = c.u32();
+            e.world_offsets = c.take(4ull * e.n_world);
+            e.patch_width = c.u8();
+            t.entries.push_back(e);
+        }
+        t.graphs.push_back({label, first, n});
+    }
+    require(c.at_end(), Errc::archive_corruption, "trailing bytes in patch table");
+    std::stable_sort(t.graphs.begin(), t.graphs.end(),
+                     [](const auto& a, const auto& b) { return a[0] < b[0]; });
+    t.graphs.erase(std::unique(t.graphs.begin(), t.graphs.end(),
+                               [](const auto& a, const auto& b) { return a[0] == b[0]; }),
+                   t.graphs.end());
+    return t;
+}
+
+std::span<const PatchEntryView> PatchView::find(uint32_t label) const {
+    auto it = std::lower_bound(graphs.begin(), graphs.end(), label,
+                               [](const std::array<uint32_t, 3>& g, uint32_t l) { return g[0] < l; });
+    if (it == graphs.end() || (*it)[0] != label) return {};
+    return {entries.data() + (*it)[1], (*it)[2]};
+}
+
+bool PatchView::has(uint32_t label) const {
+    auto it = std::lower_bound(graphs.begin(), graphs.end(), label,
+                               [](const std::array<uint32_t, 3>& g, uint32_t l) { return g[0] < l; });
+    return it != graphs.end() && (*it)[0] == label;
+}
+
 void apply_rank_patches(CapturedGraph& graph, std::span<const CommPatchEntry> entries,
                         uint64_t real_comm_hash, uint32_t rank, uint32_t world) {
     auto put = [](std::vector<uint8_t>& buf, uint32_t off, uint64_t v) {

@@ -294,7 +294,6 @@ std::vector<uint64_t> crc64_device(Device& dev, const unsigned char* d_base,
             b.segment = static_cast<uint32_t>(s);
             b.length = static_cast<uint32_t>(std::min<uint64_t>(kCrcBlockBytes, segments[s].length - off));
             b.offset = segments[s].offset + off;
-            require(b.offset % 16 == 0, Errc::invalid_argument, "CRC segment must be 16-byte aligned");
             blocks.push_back(b);
         }
         count[s] = static_cast<uint32_t>(blocks.size()) - first[s];

@@ -1,0 +1,753 @@
+// Host side of the GPU packer (kernels/pack.cu; format: store_format.h).
+//
+// The offline packer (template_store.cpp pack_template_store) decodes every
+// member with parse_graph_at on host threads; here the members stay in HBM and
+// the kernels decode, validate, lay out, diff and compact them. The host works
+// on what is per group or per kernel and on patch.bin:
+//   pass 1 (GPU)  node walk, validation, topology, slot capacities, kernel keys
+//   host          error checks in the offline packer's order, kernel table
+//                 (first-occurrence order), group layouts, stub swaps, rank ops
+//   pass 2 (GPU)  member images + relocation meta, diff counts per tile
+//   host          tile table (relocation-free tiles first), host sections
+//   pass 3 (GPU)  diff streams (ballot / scan compaction), template images
+// The result is byte-identical to pack_template_store's (tests/test_gpu_pack.py).
+#include "foundry/device_pack.hpp"
+
+#include <algorithm>
+#include <array>
+#include <exception>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <unordered_map>
+
+#include "../kernels/fdy_kernels.h"
+#include "foundry/bytes.hpp"
+#include "foundry/hash.hpp"
+#include "foundry/parallel.hpp"
+
+namespace foundry {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double ms_of(Clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+constexpr uint32_t kNoKernel = 0xFFFFFFFFu;
+constexpr size_t kSectionAlign = 256;
+
+uint32_t rd32(const uint8_t* p) {
+    uint32_t v;
+    std::memcpy(&v, p, 4);
+    return v;
+}
+uint64_t rd64(const uint8_t* p) {
+    uint64_t v;
+    std::memcpy(&v, p, 8);
+    return v;
+}
+
+// Bump allocator over one device allocation (256-byte aligned pieces).
+class Scratch {
+public:
+    Scratch(Device& dev, size_t bytes) : buf_(dev, bytes + 256) {}
+    template <typename T>
+    T* take(size_t count) {
+        at_ = (at_ + 255) / 256 * 256;
+        T* p = reinterpret_cast<T*>(buf_.data() + at_);
+        at_ += count * sizeof(T);
+        return p;
+    }
+    static size_t need(std::initializer_list<size_t> sizes) {
+        size_t n = 0;
+        for (size_t s : sizes) n += (s + 255) / 256 * 256;
+        return n;
+    }
+
+private:
+    DeviceBuffer buf_;
+    size_t at_ = 0;
+};
+
+template <typename T>
+void h2d(T* dst, const std::vector<T>& src, cudaStream_t st) {
+    if (!src.empty())
+        cuda_check(cudaMemcpyAsync(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st),
+                   "GPU pack H2D");
+}
+template <typename T>
+void d2h(std::vector<T>& dst, const T* src, size_t count, cudaStream_t st) {
+    dst.resize(count);
+    if (count)
+        cuda_check(cudaMemcpyAsync(dst.data(), src, count * sizeof(T), cudaMemcpyDeviceToHost, st), "GPU pack D2H");
+}
+
+// KernelTable key bytes (template_store.cpp): binary hash | FuncAttrs | name.
+std::string kernel_key(uint64_t hash, const uint8_t* fattrs, std::string_view name) {
+    std::string k(8 + 24, '\0');
+    std::memcpy(k.data(), &hash, 8);
+    std::memcpy(k.data() + 8, fattrs, 24);
+    k.append(name);
+    return k;
+}
+
+struct NodeView {  // a kernel node's fields, read from the host copy
+    const uint8_t* q;
+    uint32_t name_len() const { return rd32(q + 62); }
+    std::string_view name() const { return {reinterpret_cast<const char*>(q + 66), name_len()}; }
+    uint64_t hash() const { return rd64(q + 54); }
+    const uint8_t* fattrs() const { return q + 66 + name_len(); }
+    uint32_t arg_size() const { return rd32(q + 90 + name_len()); }
+};
+
+}  // namespace
+
+DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t> graphs_host,
+                                            const unsigned char* d_graphs, std::span<const uint8_t> patch_bin,
+                                            const Manifest& manifest, std::span<const uint8_t> slots_bin,
+                                            PackStats* stats, DevicePackTimings* timings) {
+    const auto t_all = Clock::now();
+    DevicePackTimings tm;
+    const PatchView patches = parse_patch_view(patch_bin);
+    const CommSlotTable slots = slots_bin.empty() ? CommSlotTable{} : parse_comm_slots(slots_bin);
+    if (!patches.empty())
+        require(manifest.comm_real_hash != 0, Errc::unresolved_kernel,
+                "archive carries comm patches but no real comm binary");
+    dev.make_current();
+    cudaStream_t st = dev.stream();
+    const uint8_t* G = graphs_host.data();
+    const uint64_t gsize = graphs_host.size();
+
+    // ------------------------------------------------ members, group-major
+    const auto& groups_in = manifest.grouping.groups;
+    const uint32_t n_groups = static_cast<uint32_t>(groups_in.size());
+    std::vector<uint64_t> rec_off, rec_len;
+    std::vector<uint32_t> node_base, n_nodes, n_edges, member_group, group_rep, group_first;
+    std::vector<const GraphLocator*> loc_of;
+    std::vector<uint8_t> suspect;  // the host already sees the record is malformed
+    uint64_t total_nodes = 0;
+    for (uint32_t g = 0; g < n_groups; ++g) {
+        const TemplateGroup& grp = groups_in[g];
+        require(grp.locators.size() == grp.members.size() && !grp.members.empty(), Errc::invalid_argument,
+                "grouping manifest is missing member locators");
+        group_first.push_back(static_cast<uint32_t>(rec_off.size()));
+        size_t rep = 0;  // the offline packer keeps the last member whose label is the representative
+        for (size_t i = 0; i < grp.locators.size(); ++i)
+            if (grp.locators[i].label == grp.representative) rep = i;
+        group_rep.push_back(group_first.back() + static_cast<uint32_t>(rep));
+        for (const GraphLocator& l : grp.locators) {
+            require(l.offset <= gsize && l.length <= gsize - l.offset, Errc::binary_format,
+                    "graph record for label " + std::to_string(l.label) + " overruns the container");
+            require(l.length < (1ull << 32), Errc::invalid_argument, "graph record exceeds 4 GiB");
+            uint32_t nn = 0, ne = 0;
+            bool bad = l.length < 12;
+            if (!bad) {
+                const uint8_t* r = G + l.offset;
+                nn = rd32(r + 4);
+                ne = rd32(r + 8);
+                bad = rd32(r) != l.label || nn > l.length - 12 || ne > (l.length - 12) / 8;
+            }
+            if (bad) nn = ne = 0;
+            rec_off.push_back(l.offset);
+            rec_len.push_back(l.length);
+            node_base.push_back(static_cast<uint32_t>(total_nodes));
+            n_nodes.push_back(nn);
+            n_edges.push_back(ne);
+            member_group.push_back(g);
+            loc_of.push_back(&l);
+            suspect.push_back(bad ? 1 : 0);
+            total_nodes += nn;
+        }
+    }
+    const uint32_t nm = static_cast<uint32_t>(rec_off.size());
+    require(total_nodes < (1ull << 31), Errc::invalid_argument, "graph set exceeds 2^31 nodes");
+    const uint32_t TN = static_cast<uint32_t>(total_nodes);
+    std::vector<uint32_t> gnode_base(n_groups + 1, 0);
+    for (uint32_t g = 0; g < n_groups; ++g) gnode_base[g + 1] = gnode_base[g] + n_nodes[group_rep[g]];
+    const uint32_t GN = gnode_base[n_groups];
+    uint32_t tslots = 1024;
+    while (tslots < 2ull * TN) tslots <<= 1;
+
+    // ------------------------------------------------ pass 1
+    tm.prep_ms = ms_of(t_all);
+    auto t0 = Clock::now();
+    Scratch s1(dev, Scratch::need({8ull * nm, 8ull * nm, 4ull * nm, 4ull * nm, 4ull * nm, 4ull * nm, 4ull * nm,
+                                   4ull * n_groups, 4ull * n_groups, 4ull * TN, 4ull * TN, 4ull * TN, 4ull * GN,
+                                   sizeof(fdt_node_attrs) * GN, 8ull * tslots, 8ull * tslots, 4ull * tslots,
+                                   8ull * tslots, 8ull * tslots, 16}));
+    FdyPackArgs a{};
+    a.graphs = d_graphs;
+    a.graphs_bytes = gsize;
+    auto* d_rec_off = s1.take<uint64_t>(nm);
+    auto* d_rec_len = s1.take<uint64_t>(nm);
+    auto* d_node_base = s1.take<uint32_t>(nm);
+    auto* d_n_nodes = s1.take<uint32_t>(nm);
+    auto* d_n_edges = s1.take<uint32_t>(nm);
+    auto* d_member_group = s1.take<uint32_t>(nm);
+    auto* d_status = s1.take<uint32_t>(nm);
+    auto* d_group_rep = s1.take<uint32_t>(n_groups);
+    auto* d_gnode_base = s1.take<uint32_t>(n_groups);
+    a.node_off = s1.take<uint32_t>(TN);
+    a.node_member = s1.take<uint32_t>(TN);
+    a.node_slot = s1.take<uint32_t>(TN);
+    a.cap = s1.take<uint32_t>(GN);
+    a.rep_attrs = s1.take<fdt_node_attrs>(GN);
+    a.tkey = s1.take<unsigned long long>(tslots);
+    a.tpos = s1.take<unsigned long long>(tslots);
+    a.tuniq = s1.take<uint32_t>(tslots);
+    a.upos = s1.take<unsigned long long>(tslots);
+    a.uoff = s1.take<uint64_t>(tslots);
+    auto* d_small = s1.take<uint32_t>(4);  // ucount, flags
+    a.rec_off = d_rec_off;
+    a.rec_len = d_rec_len;
+    a.node_base = d_node_base;
+    a.n_nodes = d_n_nodes;
+    a.n_edges = d_n_edges;
+    a.member_group = d_member_group;
+    a.group_rep = d_group_rep;
+    a.gnode_base = d_gnode_base;
+    a.status = d_status;
+    a.ucount = d_small;
+    a.flags = d_small + 1;
+    a.tmask = tslots - 1;
+    a.n_members = nm;
+    a.total_nodes = TN;
+    h2d(d_rec_off, rec_off, st);
+    h2d(d_rec_len, rec_len, st);
+    h2d(d_node_base, node_base, st);
+    h2d(d_n_nodes, n_nodes, st);
+    h2d(d_n_edges, n_edges, st);
+    h2d(d_member_group, member_group, st);
+    h2d(d_group_rep, group_rep, st);
+    {
+        std::vector<uint32_t> gb(gnode_base.begin(), gnode_base.end() - 1);
+        h2d(d_gnode_base, gb, st);
+    }
+    // record CRCs (parse_graph_at's per-record check) and the whole file's
+    // digest (the store header's source_graphs_crc), on the GPU
+    std::vector<Segment> segs;
+    segs.push_back({0, gsize});
+    for (uint32_t m = 0; m < nm; ++m) segs.push_back({rec_off[m], rec_len[m]});
+
+    std::vector<uint32_t> status, small;
+    std::vector<unsigned long long> upos;
+    std::vector<uint64_t> uoff, digests;
+    for (uint32_t attempt = 0;; ++attempt) {
+        a.seed = 0x46445450ull + 0x9E3779B97F4A7C15ull * attempt;  // "FDTP"
+        cuda_check(cudaMemsetAsync(d_status, 0, 4ull * nm, st), "GPU pack memset");
+        cuda_check(cudaMemsetAsync(a.node_member, 0xFF, 4ull * TN, st), "GPU pack memset");
+        cuda_check(cudaMemsetAsync(a.cap, 0, 4ull * GN, st), "GPU pack memset");
+        cuda_check(cudaMemsetAsync(a.tkey, 0, 8ull * tslots, st), "GPU pack memset");
+        cuda_check(cudaMemsetAsync(a.tpos, 0xFF, 8ull * tslots, st), "GPU pack memset");
+        cuda_check(cudaMemsetAsync(d_small, 0, 16, st), "GPU pack memset");
+        cuda_check(fdy_launch_pack_pass1(&a, st), "GPU pack pass 1");
+        d2h(small, d_small, 2, st);
+        cuda_check(cudaStreamSynchronize(st), "GPU pack pass 1");
+        if (small[1] == 0) break;
+        require(attempt < 4, Errc::cuda_error, "GPU pack: kernel key fingerprints keep colliding");
+        ++tm.retries;
+    }
+    const uint32_t nu = small[0];
+    tm.kernel_keys = nu;
+    d2h(status, d_status, nm, st);
+    d2h(upos, a.upos, nu, st);
+    d2h(uoff, a.uoff, nu, st);
+    std::vector<uint32_t> cap, node_off;
+    std::vector<fdt_node_attrs> rep_attrs;
+    d2h(cap, a.cap, GN, st);
+    d2h(rep_attrs, a.rep_attrs, GN, st);
+    d2h(node_off, a.node_off, TN, st);
+    digests = crc64_device(dev, d_graphs, segs);  // synchronizes the stream
+    tm.pass1_ms = ms_of(t0);
+
+    // ------------------------------------------------ host: checks, kernel table, layout
+    t0 = Clock::now();
+    auto node_ptr = [&](uint32_t m, uint32_t n) { return G + rec_off[m] + node_off[node_base[m] + n]; };
+    // errors in the offline packer's order: group by group, decode, topology, patches
+    auto decode_error = [&](uint32_t m) {
+        const bool crc_bad = digests[1 + m] != loc_of[m]->checksum;
+        return suspect[m] || crc_bad || (status[m] & FDY_PACK_DECODE);
+    };
+    for (uint32_t g = 0; g < n_groups; ++g) {
+        const uint32_t f = group_first[g], e = g + 1 < n_groups ? group_first[g + 1] : nm;
+        for (uint32_t m = f; m < e; ++m) {
+            if (!decode_error(m)) continue;
+            (void)parse_graph_at(graphs_host, *loc_of[m]);  // raises the reference's message
+            raise(Errc::binary_format, "graph record for label " + std::to_string(loc_of[m]->label) +
+                                           " failed to decode on the GPU");
+        }
+        for (uint32_t m = f; m < e; ++m) {
+            if (!(status[m] & FDY_PACK_TOPO)) continue;
+            const TopologyKey k = topology_key(parse_graph_at(graphs_host, *loc_of[m]));
+            const TopologyKey want = topology_key(parse_graph_at(graphs_host, *loc_of[group_rep[g]]));
+            require(k == want, Errc::topology_mismatch,
+                    "donor topology " + k.hex() + " does not match exec topology " + want.hex());
+        }
+    }
+
+    // kernel table: every distinct (hash, func attrs, name) in first-occurrence
+    // order, where a graph's patch entries' real comm kernels follow its nodes
+    struct KeyAt {
+        unsigned long long pos;
+        int64_t gpu;  // compacted GPU index, or -1 (a patch entry's real kernel)
+        uint64_t hash;
+        const uint8_t* fattrs;
+        std::string_view name;
+    };
+    std::vector<KeyAt> keys;
+    keys.reserve(nu + 64);
+    for (uint32_t u = 0; u < nu; ++u) {
+        const NodeView v{G + uoff[u]};
+        keys.push_back({upos[u], u, v.hash(), v.fattrs(), v.name()});
+    }
+    // real comm kernels: few distinct (name, func attrs); the first position of each
+    struct RealKey {
+        std::array<uint8_t, 24> fattrs;
+        uint32_t kidx;
+    };
+    std::unordered_map<std::string_view, std::vector<RealKey>> real_keys;
+    auto real_slot = [&](std::string_view name, const uint8_t* fa) -> RealKey* {  // lookup only
+        auto it = real_keys.find(name);
+        if (it == real_keys.end()) return nullptr;
+        for (RealKey& r : it->second)
+            if (std::memcmp(r.fattrs.data(), fa, 24) == 0) return &r;
+        return nullptr;
+    };
+    if (!patches.empty()) {
+        for (uint32_t m = 0; m < nm; ++m) {
+            const auto entries = patches.find(loc_of[m]->label);
+            for (size_t j = 0; j < entries.size(); ++j) {
+                const PatchEntryView& e = entries[j];
+                if (e.node_id >= n_nodes[m] || node_ptr(m, e.node_id)[0] != 0) continue;
+                const NodeView v{node_ptr(m, e.node_id)};
+                if (real_slot(e.real_name, v.fattrs())) continue;
+                RealKey r{};
+                std::memcpy(r.fattrs.data(), v.fattrs(), 24);
+                r.kidx = kNoKernel;
+                real_keys[e.real_name].push_back(r);
+                keys.push_back({(uint64_t(m) << 32) | (n_nodes[m] + j), -1, manifest.comm_real_hash,
+                                v.fattrs(), e.real_name});
+            }
+        }
+    }
+    std::sort(keys.begin(), keys.end(), [](const KeyAt& x, const KeyAt& y) { return x.pos < y.pos; });
+    std::unordered_map<std::string, uint32_t> kindex;
+    kindex.reserve(keys.size() * 2);
+    std::vector<fdt_kernel> kernels;
+    std::string strings;
+    std::vector<uint32_t> ukidx(nu, kNoKernel);
+    for (const KeyAt& k : keys) {
+        auto [it, fresh] = kindex.try_emplace(kernel_key(k.hash, k.fattrs, k.name),
+                                              static_cast<uint32_t>(kernels.size()));
+        if (fresh) {
+            fdt_kernel K{};
+            K.binary_hash = k.hash;
+            K.name_off = static_cast<uint32_t>(strings.size());
+            K.name_len = static_cast<uint32_t>(k.name.size());
+            std::memcpy(K.func_attrs, k.fattrs, 24);
+            kernels.push_back(K);
+            strings.append(k.name);
+        }
+        if (k.gpu >= 0) ukidx[k.gpu] = it->second;
+        else real_slot(k.name, k.fattrs)->kidx = it->second;
+    }
+
+    // group layouts: slot capacity = group-wide maximum (round16), in node order
+    std::vector<uint32_t> blob_off(GN);
+    std::vector<uint64_t> g_image(n_groups), g_desc(n_groups);
+    for (uint32_t g = 0; g < n_groups; ++g) {
+        uint64_t pool = 0;
+        for (uint32_t i = gnode_base[g]; i < gnode_base[g + 1]; ++i) {
+            blob_off[i] = static_cast<uint32_t>(pool);
+            pool += cap[i];
+        }
+        g_desc[g] = 48ull * n_nodes[group_rep[g]];
+        g_image[g] = g_desc[g] + pool;
+    }
+    std::vector<uint64_t> out_off(nm);
+    std::vector<uint32_t> tile_base(nm), tile_member;
+    uint64_t arena_bytes = 0;
+    for (uint32_t m = 0; m < nm; ++m) {
+        const uint64_t img = g_image[member_group[m]];
+        out_off[m] = arena_bytes;
+        arena_bytes += img;
+        const uint64_t ntiles = (img / 16 + FDT_TILE_CHUNKS - 1) / FDT_TILE_CHUNKS;
+        require(ntiles <= UINT32_MAX && img / 8 <= UINT32_MAX, Errc::invalid_argument,
+                "graph image exceeds the store's 32 GiB limit");
+        tile_base[m] = static_cast<uint32_t>(tile_member.size());
+        tile_member.insert(tile_member.end(), ntiles, m);
+    }
+    const uint32_t n_tiles = static_cast<uint32_t>(tile_member.size());
+
+    // stub swaps + rank ops (apply_rank_patches split as in patch_graph),
+    // checked as the offline packer checks them: per group, representative
+    // first, then members in order (members run on host threads; the first
+    // error in that order is raised)
+    std::vector<std::vector<uint32_t>> swaps_of(nm);
+    std::vector<std::vector<fdt_rank_op>> rops_of(nm);
+    auto patch_member = [&](uint32_t m) {
+        const uint32_t label = loc_of[m]->label;
+        const uint32_t gi0 = gnode_base[member_group[m]];
+        const uint64_t desc = g_desc[member_group[m]];
+        const bool patched = patches.has(label);
+        auto sit = slots.per_graph.find(label);
+        require(sit == slots.per_graph.end() || patched, Errc::archive_corruption,
+                "comm slot table lists graph " + std::to_string(label) + ", which has no comm patches");
+        if (!patched) return;
+        const auto entries = patches.find(label);
+        auto& ops = rops_of[m];
+        auto& sw = swaps_of[m];
+        for (const PatchEntryView& e : entries) {
+            require(e.node_id < n_nodes[m], Errc::archive_corruption, "patch entry references missing node");
+            const uint8_t* q = node_ptr(m, e.node_id);
+            require(q[0] == 0, Errc::archive_corruption, "patch entry references a non-kernel node");
+            const NodeView v{q};
+            require(v.hash() == e.stub_hash && v.name() == e.stub_name, Errc::archive_corruption,
+                    "node " + std::to_string(e.node_id) + " is not the recorded stub " +
+                        KernelRef{e.stub_hash, std::string(e.stub_name)}.describe());
+            RealKey* r = real_slot(e.real_name, v.fattrs());
+            require(r != nullptr && r->kidx != kNoKernel, Errc::invalid_argument, "kernel table: missing entry");
+            sw.push_back(node_base[m] + e.node_id);
+            sw.push_back(r->kidx);
+            const uint64_t blob = desc + blob_off[gi0 + e.node_id];
+            for (uint32_t i = 0; i < e.n_rank; ++i) {
+                const uint32_t off = e.rank_offset(i);
+                require(uint64_t(off) + 8 <= v.arg_size(), Errc::invalid_argument,
+                        "patch offset outside the argument buffer");
+                store_detail::emit_write(ops, blob + off, 8, FDT_ROP_RANK, 0);
+            }
+            for (uint32_t i = 0; i < e.n_world; ++i) {
+                const uint32_t off = e.world_offset(i);
+                require(uint64_t(off) + 8 <= v.arg_size(), Errc::invalid_argument,
+                        "patch offset outside the argument buffer");
+                store_detail::emit_write(ops, blob + off, 8, FDT_ROP_WORLD, 0);
+            }
+        }
+        if (sit != slots.per_graph.end()) {
+            for (const CommSlot& c : sit->second) {
+                bool stub = false;
+                for (const PatchEntryView& e : entries) stub = stub || e.node_id == c.node_id;
+                require(stub && c.node_id < n_nodes[m] && node_ptr(m, c.node_id)[0] == 0, Errc::archive_corruption,
+                        "comm slot references node " + std::to_string(c.node_id) +
+                            ", which is not a patched comm node");
+                require(uint64_t(c.offset) + c.width <= NodeView{node_ptr(m, c.node_id)}.arg_size(),
+                        Errc::invalid_argument, "comm slot offset outside the argument buffer");
+                store_detail::emit_write(ops, desc + blob_off[gi0 + c.node_id] + c.offset, c.width, FDT_ROP_VALUE,
+                                         c.value_index);
+            }
+        }
+        std::stable_sort(ops.begin(), ops.end(),
+                         [](const fdt_rank_op& x, const fdt_rank_op& y) { return x.chunk < y.chunk; });
+    };
+    if (!patches.empty() || !slots.empty()) {
+        std::vector<std::exception_ptr> err(nm);
+        parallel_for(nm, 0, [&](size_t m) {
+            try {
+                patch_member(static_cast<uint32_t>(m));
+            } catch (...) {
+                err[m] = std::current_exception();
+            }
+        });
+        for (uint32_t g = 0; g < n_groups; ++g) {
+            const uint32_t f = group_first[g], e = g + 1 < n_groups ? group_first[g + 1] : nm;
+            if (err[group_rep[g]]) std::rethrow_exception(err[group_rep[g]]);
+            for (uint32_t m = f; m < e; ++m)
+                if (err[m]) std::rethrow_exception(err[m]);
+        }
+    }
+    std::vector<uint32_t> swap_node, swap_kidx;
+    for (const auto& sw : swaps_of)
+        for (size_t i = 0; i < sw.size(); i += 2) {
+            swap_node.push_back(sw[i]);
+            swap_kidx.push_back(sw[i + 1]);
+        }
+    tm.host1_ms = ms_of(t0);
+
+    // ------------------------------------------------ pass 2
+    t0 = Clock::now();
+    const uint32_t nsw = static_cast<uint32_t>(swap_node.size());
+    Scratch s2(dev, Scratch::need({4ull * GN, 8ull * nm, 4ull * nm, 8ull * n_groups, 4ull * std::max(nu, 1u),
+                                   4ull * nsw, 4ull * nsw, 4ull * n_tiles, 4ull * n_tiles, n_tiles, 4ull * n_tiles,
+                                   arena_bytes, arena_bytes / 16}));
+    auto* d_blob_off = s2.take<uint32_t>(GN);
+    auto* d_out_off = s2.take<uint64_t>(nm);
+    auto* d_tile_base = s2.take<uint32_t>(nm);
+    auto* d_g_image = s2.take<uint64_t>(n_groups);
+    auto* d_ukidx = s2.take<uint32_t>(std::max(nu, 1u));
+    auto* d_swap_node = s2.take<uint32_t>(nsw);
+    auto* d_swap_kidx = s2.take<uint32_t>(nsw);
+    auto* d_tile_member = s2.take<uint32_t>(n_tiles);
+    a.tile_count = s2.take<uint32_t>(n_tiles);
+    a.tile_reloc = s2.take<uint8_t>(n_tiles);
+    auto* d_diff_lo = s2.take<uint32_t>(n_tiles);
+    a.arena = s2.take<unsigned char>(arena_bytes);
+    a.meta = s2.take<uint8_t>(arena_bytes / 16);
+    a.blob_off = d_blob_off;
+    a.out_off = d_out_off;
+    a.tile_base = d_tile_base;
+    a.g_image = d_g_image;
+    a.ukidx = d_ukidx;
+    a.swap_node = d_swap_node;
+    a.swap_kidx = d_swap_kidx;
+    a.n_swaps = nsw;
+    a.tile_member = d_tile_member;
+    a.diff_lo = d_diff_lo;
+    a.n_tiles = n_tiles;
+    h2d(d_blob_off, blob_off, st);
+    h2d(d_out_off, out_off, st);
+    h2d(d_tile_base, tile_base, st);
+    h2d(d_g_image, g_image, st);
+    h2d(d_ukidx, ukidx, st);
+    h2d(d_swap_node, swap_node, st);
+    h2d(d_swap_kidx, swap_kidx, st);
+    h2d(d_tile_member, tile_member, st);
+    cuda_check(fdy_launch_pack_pass2(&a, st), "GPU pack pass 2");
+    std::vector<uint32_t> tile_count;
+    std::vector<uint8_t> tile_reloc;
+    d2h(tile_count, a.tile_count, n_tiles, st);
+    d2h(tile_reloc, a.tile_reloc, n_tiles, st);
+    cuda_check(cudaStreamSynchronize(st), "GPU pack pass 2");
+    tm.pass2_ms = ms_of(t0);
+
+    // ------------------------------------------------ host: tables and sections
+    t0 = Clock::now();
+    std::vector<uint32_t> diff_lo(n_tiles);
+    uint64_t n_diffs = 0;
+    for (uint32_t t = 0; t < n_tiles; ++t) {
+        diff_lo[t] = static_cast<uint32_t>(n_diffs);
+        n_diffs += tile_count[t];
+    }
+    require(n_diffs < (1ull << 32), Errc::invalid_argument, "template store exceeds 2^32 diff entries");
+    std::vector<fdt_group> groups(n_groups);
+    std::vector<fdt_member> members(nm);
+    std::vector<fdt_tile> tiles;
+    tiles.reserve(n_tiles);
+    std::vector<fdt_rank_op> rops;
+    std::vector<uint32_t> edges;
+    std::vector<fdt_node_attrs> attrs;
+    uint64_t timages_bytes = 0;
+    for (uint32_t g = 0; g < n_groups; ++g) {
+        const uint32_t rep = group_rep[g], N = n_nodes[rep], E = n_edges[rep];
+        fdt_group& Gp = groups[g];
+        Gp.image_bytes = g_image[g];
+        Gp.n_nodes = N;
+        Gp.n_edges = E;
+        Gp.first_member = group_first[g];
+        Gp.n_members = (g + 1 < n_groups ? group_first[g + 1] : nm) - group_first[g];
+        Gp.representative = groups_in[g].representative;
+        Gp.attrs_first = static_cast<uint32_t>(attrs.size());
+        Gp.edges_off = edges.size() * sizeof(uint32_t);
+        attrs.insert(attrs.end(), rep_attrs.begin() + gnode_base[g], rep_attrs.begin() + gnode_base[g + 1]);
+        const uint8_t* etab = G + rec_off[rep] + rec_len[rep] - 8ull * E;
+        const size_t e0 = edges.size();
+        edges.resize(e0 + 2ull * E);
+        std::memcpy(edges.data() + e0, etab, 8ull * E);
+        // topology key of the representative (topology_key, graph_model.cpp)
+        Sink k;
+        k.u64(N);
+        for (uint32_t n = 0; n < N; ++n) {
+            const uint8_t t = node_ptr(rep, n)[0];
+            k.u8(t);
+            if (t == 0) {
+                const fdt_node_attrs& at = rep_attrs[gnode_base[g] + n];
+                k.u32(at.cluster[0]);
+                k.u32(at.cluster[1]);
+                k.u32(at.cluster[2]);
+                k.i32(at.sched_policy);
+                k.i32(at.sync_default);
+                k.i32(at.sync_remote);
+                k.u8(at.attr_query ? 1 : 0);
+            }
+        }
+        k.u64(E);
+        k.raw(etab, 8ull * E);
+        const Digest128 key = murmur3_x64_128(k.bytes().data(), k.size(), 0x464E4447ull);
+        Gp.key_hi = key.hi;
+        Gp.key_lo = key.lo;
+        timages_bytes = (timages_bytes + 15) / 16 * 16;
+        Gp.timage_off = timages_bytes;  // TIMAGES-relative until rebased
+        timages_bytes += g_image[g];
+
+        // members' tiles; rank-op ranges shared per (group, tile index)
+        std::vector<std::map<std::string, std::pair<uint32_t, uint32_t>>> shared_ops;
+        for (uint32_t m = Gp.first_member; m < Gp.first_member + Gp.n_members; ++m) {
+            fdt_member& M = members[m];
+            M.label = loc_of[m]->label;
+            M.group = g;
+            M.out_off = out_off[m];
+            M.n_nodes = N;
+            M.first_tile = tile_base[m];
+            const uint64_t nchunks = g_image[g] / 16;
+            const uint32_t ntiles = static_cast<uint32_t>((nchunks + FDT_TILE_CHUNKS - 1) / FDT_TILE_CHUNKS);
+            M.n_tiles = ntiles;
+            shared_ops.resize(std::max<size_t>(shared_ops.size(), ntiles));
+            const auto& ops = rops_of[m];
+            size_t rpos = 0;
+            for (uint32_t t = 0; t < ntiles; ++t) {
+                const uint64_t cb = uint64_t(t) * FDT_TILE_CHUNKS;
+                const uint64_t ce = std::min<uint64_t>(nchunks, cb + FDT_TILE_CHUNKS);
+                fdt_tile T{};
+                T.src_off = Gp.timage_off + 16 * cb;
+                T.dst_off = out_off[m] + 16 * cb;
+                T.nchunks = static_cast<uint32_t>(ce - cb);
+                T.member = m;
+                T.chunk_base = static_cast<uint32_t>(cb);
+                T.diff_lo = diff_lo[tile_base[m] + t];
+                T.diff_hi = T.diff_lo + tile_count[tile_base[m] + t];
+                const size_t r_begin = rpos;
+                while (rpos < ops.size() && ops[rpos].chunk < ce) ++rpos;
+                const std::string key(reinterpret_cast<const char*>(ops.data() + r_begin),
+                                      (rpos - r_begin) * sizeof(fdt_rank_op));
+                auto [it, fresh] = shared_ops[t].try_emplace(key);
+                if (fresh) {
+                    it->second.first = static_cast<uint32_t>(rops.size());
+                    rops.insert(rops.end(), ops.begin() + static_cast<long>(r_begin),
+                                ops.begin() + static_cast<long>(rpos));
+                    it->second.second = static_cast<uint32_t>(rops.size());
+                }
+                T.rop_lo = it->second.first;
+                T.rop_hi = it->second.second;
+                tiles.push_back(T);
+            }
+        }
+    }
+    // relocation-free template tiles first (stable), as the offline packer orders them
+    uint32_t n_plain = 0;
+    {
+        std::vector<fdt_tile> plain, rest;
+        for (uint32_t t = 0; t < n_tiles; ++t) (tile_reloc[t] ? rest : plain).push_back(tiles[t]);
+        n_plain = static_cast<uint32_t>(plain.size());
+        plain.insert(plain.end(), rest.begin(), rest.end());
+        tiles = std::move(plain);
+    }
+
+    fdt_header h{};
+    std::memcpy(h.magic, "FNDT", 4);
+    h.version = FDT_VERSION;
+    h.header_bytes = sizeof(fdt_header);
+    h.n_groups = n_groups;
+    h.n_members = nm;
+    h.n_kernels = static_cast<uint32_t>(kernels.size());
+    h.n_tiles = n_tiles;
+    h.tile_chunks = FDT_TILE_CHUNKS;
+    h.n_diffs = static_cast<uint32_t>(n_diffs);
+    h.n_rank_ops = static_cast<uint32_t>(rops.size());
+    h.source_graphs_crc = digests[0];
+    h.source_patch_crc = crc64(patch_bin);
+    h.old_base = manifest.allocator.base;
+    h.final_offset = manifest.final_offset;
+    h.real_comm_hash = manifest.comm_real_hash;
+    h.members_image_bytes = arena_bytes;
+    h.total_nodes = total_nodes;
+    h.n_plain_tiles = n_plain;
+    h.n_values = slots.empty() ? 0u : slots.n_values;
+    h.source_slots_crc = slots_bin.empty() ? 0ull : crc64(slots_bin);
+
+    // section layout, in the offline packer's order
+    uint64_t at = sizeof(fdt_header);
+    auto place = [&](int id, uint64_t bytes) {
+        at = (at + kSectionAlign - 1) / kSectionAlign * kSectionAlign;
+        h.sec[id] = {at, bytes};
+        at += bytes;
+    };
+    place(FDT_SEC_TIMAGES, timages_bytes);
+    const uint64_t timg_base = h.sec[FDT_SEC_TIMAGES].offset;
+    for (auto& Gp : groups) Gp.timage_off += timg_base;
+    for (auto& T : tiles) T.src_off += timg_base;
+    place(FDT_SEC_GROUPS, groups.size() * sizeof(fdt_group));
+    place(FDT_SEC_CMETA, timages_bytes / 16);
+    place(FDT_SEC_MEMBERS, members.size() * sizeof(fdt_member));
+    place(FDT_SEC_TILES, tiles.size() * sizeof(fdt_tile));
+    place(FDT_SEC_DIDX, n_diffs * sizeof(uint16_t));
+    place(FDT_SEC_DDATA, n_diffs * sizeof(uint64_t));
+    place(FDT_SEC_ROPS, rops.size() * sizeof(fdt_rank_op));
+    place(FDT_SEC_KERNELS, kernels.size() * sizeof(fdt_kernel));
+    place(FDT_SEC_NODEATTRS, attrs.size() * sizeof(fdt_node_attrs));
+    place(FDT_SEC_EDGES, edges.size() * sizeof(uint32_t));
+    place(FDT_SEC_STRINGS, strings.size());
+    const uint64_t blob_bytes = (at + kSectionAlign - 1) / kSectionAlign * kSectionAlign;
+
+    DevicePackResult out;
+    out.host.assign(blob_bytes, 0);
+    uint8_t* hb = out.host.data();
+    std::memcpy(hb, &h, sizeof h);
+    auto put = [&](int id, const void* src) {
+        if (h.sec[id].bytes) std::memcpy(hb + h.sec[id].offset, src, h.sec[id].bytes);
+    };
+    put(FDT_SEC_GROUPS, groups.data());
+    put(FDT_SEC_MEMBERS, members.data());
+    put(FDT_SEC_TILES, tiles.data());
+    put(FDT_SEC_ROPS, rops.data());
+    put(FDT_SEC_KERNELS, kernels.data());
+    put(FDT_SEC_NODEATTRS, attrs.data());
+    put(FDT_SEC_EDGES, edges.data());
+    put(FDT_SEC_STRINGS, strings.data());
+    tm.host2_ms = ms_of(t0);
+
+    // ------------------------------------------------ pass 3: device sections
+    t0 = Clock::now();
+    out.blob = DeviceBuffer(dev, blob_bytes);
+    unsigned char* db = out.blob.data();
+    cuda_check(cudaMemsetAsync(db, 0, blob_bytes, st), "GPU pack memset");
+    // the host-built sections (header .. strings, without the device ones)
+    cuda_check(cudaMemcpyAsync(db, hb, sizeof h, cudaMemcpyHostToDevice, st), "GPU pack H2D");
+    for (int id : {FDT_SEC_GROUPS, FDT_SEC_MEMBERS, FDT_SEC_TILES, FDT_SEC_ROPS, FDT_SEC_KERNELS,
+                   FDT_SEC_NODEATTRS, FDT_SEC_EDGES, FDT_SEC_STRINGS})
+        if (h.sec[id].bytes)
+            cuda_check(cudaMemcpyAsync(db + h.sec[id].offset, hb + h.sec[id].offset, h.sec[id].bytes,
+                                       cudaMemcpyHostToDevice, st),
+                       "GPU pack H2D");
+    a.didx = reinterpret_cast<uint16_t*>(db + h.sec[FDT_SEC_DIDX].offset);
+    a.ddata = reinterpret_cast<uint64_t*>(db + h.sec[FDT_SEC_DDATA].offset);
+    h2d(d_diff_lo, diff_lo, st);
+    cuda_check(fdy_launch_pack_pass3(&a, st), "GPU pack pass 3");
+    // template images = the representatives' pack images (+ their relocation meta)
+    for (uint32_t g = 0; g < n_groups; ++g) {
+        const uint64_t src = out_off[group_rep[g]];
+        const uint64_t dst = groups[g].timage_off;  // blob-relative now
+        cuda_check(cudaMemcpyAsync(db + dst, a.arena + src, g_image[g], cudaMemcpyDeviceToDevice, st),
+                   "GPU pack template image");
+        cuda_check(cudaMemcpyAsync(db + h.sec[FDT_SEC_CMETA].offset + (dst - timg_base) / 16, a.meta + src / 16,
+                                   g_image[g] / 16, cudaMemcpyDeviceToDevice, st),
+                   "GPU pack template meta");
+    }
+    for (int id : {FDT_SEC_TIMAGES, FDT_SEC_CMETA, FDT_SEC_DIDX, FDT_SEC_DDATA})
+        if (h.sec[id].bytes)
+            cuda_check(cudaMemcpyAsync(hb + h.sec[id].offset, db + h.sec[id].offset, h.sec[id].bytes,
+                                       cudaMemcpyDeviceToHost, st),
+                       "GPU pack D2H");
+    cuda_check(cudaStreamSynchronize(st), "GPU pack pass 3");
+    tm.pass3_ms = ms_of(t0);
+
+    if (stats) {
+        stats->template_bytes = timages_bytes;
+        stats->diff_entries = n_diffs;
+        stats->rank_ops = rops.size();
+        stats->member_image_bytes = arena_bytes;
+        stats->store_bytes = blob_bytes;
+    }
+    tm.total_ms = ms_of(t_all);
+    if (timings) *timings = tm;
+    return out;
+}
+
+std::vector<uint8_t> pack_archive_store_device(Device& dev, const std::filesystem::path& archive,
+                                               DevicePackTimings* timings) {
+    ArchivePaths paths{archive};
+    const auto mtext = slurp(paths.manifest());
+    const Manifest man = parse_manifest(std::string(mtext.begin(), mtext.end()));
+    const auto graphs = slurp(paths.graphs());
+    const auto patch = slurp(paths.patch_table());
+    const bool has_slots = man.file_digests.count("comm_slots.bin") != 0;
+    const auto slots = has_slots ? slurp(paths.comm_slots()) : std::vector<uint8_t>{};
+    dev.make_current();
+    DeviceBuffer d(dev, std::max<size_t>(graphs.size(), 16));
+    cuda_check(cudaMemcpyAsync(d.data(), graphs.data(), graphs.size(), cudaMemcpyHostToDevice, dev.stream()),
+               "cudaMemcpyAsync(graphs.bin)");
+    DevicePackResult r = pack_template_store_device(dev, graphs, d.data(), patch, man, slots, nullptr, timings);
+    return std::move(r.host);
+}
+
+}  // namespace foundry

@@ -1,5 +1,6 @@
 // LOAD orchestration on B200 (phase map and reference anchors: pipeline.hpp).
 #include "foundry/pipeline.hpp"
+#include "foundry/device_pack.hpp"
 
 #include <fcntl.h>
 #include <unistd.h>
@@ -913,7 +914,9 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     try {
         StagePlan plan;
         const bool has_store = I.manifest.file_digests.count("templates.fdt") != 0;
-        if (has_store) plan.device = {"templates.fdt"};
+        // the store goes to HBM; a reference-written archive's graphs.bin goes
+        // there instead, for the GPU packer
+        plan.device = {has_store ? "templates.fdt" : "graphs.bin"};
         plan.keep_host = [has_store](const std::string& rel) { return !(has_store && rel == "graphs.bin"); };
         I.staged = std::make_unique<StagedArchive>(device, archive, I.manifest, opts.prepare_lanes, &st, plan);
         I.staged->verify(I.manifest, &st);
@@ -930,28 +933,34 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     require(spec.digest() == I.manifest.workload_digest, Errc::archive_corruption,
             "embedded workload text does not match its recorded digest");
     I.catalog = parse_catalog(I.file_host("catalog.bin"));
-    (void)parse_patch_table(I.file_host("patch.bin"));  // format check; the store carries the ops
+    (void)parse_patch_view(I.file_host("patch.bin"));  // format check; the store carries the ops
     const MemoryEventLog log = parse_event_log(I.file_host("memlayout.bin"));
 
     // template store: packed offline (templates.fdt) or, for a reference-written
-    // archive, packed now from graphs.bin + patch.bin
+    // archive, packed now on the GPU from graphs.bin (in HBM) + patch.bin
     if (I.staged->has("templates.fdt")) {
         I.store_host = I.file_host("templates.fdt");
         I.view = std::make_unique<StoreView>(I.store_host);
         I.dstore = adopt_store(device, I.staged->device("templates.fdt"), I.store_host.size(),
                                I.view->header());
     } else {
+        const auto t_pack = Clock::now();
+        DevicePackResult packed;
         try {
-            I.inline_store = pack_template_store(
-                I.file_host("graphs.bin"), I.file_host("patch.bin"), I.manifest, opts.prepare_lanes, nullptr,
+            I.staged->order_after("graphs.bin", device.stream());
+            packed = pack_template_store_device(
+                device, I.file_host("graphs.bin"), I.staged->device("graphs.bin"), I.file_host("patch.bin"),
+                I.manifest,
                 I.staged->has("comm_slots.bin") ? I.file_host("comm_slots.bin") : std::span<const uint8_t>{});
         } catch (const Error&) {
             rethrow_in_step("template construction");
         }
+        I.inline_store = std::move(packed.host);
         I.store_host = I.inline_store;
         I.view = std::make_unique<StoreView>(I.store_host);
-        I.dstore = upload_store(device, I.inline_store.data(), I.inline_store.size());
-        I.t.h2d_bytes += I.inline_store.size();
+        I.dstore = adopt_store(device, packed.blob.data(), I.inline_store.size(), I.view->header());
+        I.dstore.blob = std::move(packed.blob);
+        I.t.pack_ms = ms_since(t_pack);
     }
     const fdt_header& H = I.view->header();
     check_store_sources(H, I.manifest);
@@ -1458,7 +1467,7 @@ SaveResult ServingContext::save_captured(const fs::path& out) {
     put("patch.bin", I.file_host("patch.bin"));
     for (const auto& [hash, rec] : I.catalog.binaries) {
         (void)rec;
-        for (const std::string rel : {"binaries/" + hex16(hash) + ".bin", "binaries/" + hex16(hash) + ".sm_100a.cubin"}) {
+        for (const std::string& rel : {"binaries/" + hex16(hash) + ".bin", "binaries/" + hex16(hash) + ".sm_100a.cubin"}) {
             if (I.staged->has(rel)) put(rel, I.file_host(rel));
             else if (fs::exists(I.root / rel)) put(rel, slurp(I.root / rel));
         }

@@ -1,5 +1,6 @@
 // Archive staging with overlapped reads + DMA, pinned pool, GPU integrity.
 #include "foundry/staging.hpp"
+#include "foundry/device_pack.hpp"
 
 #include <fcntl.h>
 #include <sys/resource.h>
@@ -654,12 +655,11 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
     if (has_store) {
         plan.device = {"templates.fdt"};
         first = plan.device;
-    } else {
+    } else {  // graphs.bin to HBM for the GPU packer
+        plan.device = {"graphs.bin"};
         first = {"graphs.bin", "patch.bin"};
         if (manifest.file_digests.count("comm_slots.bin")) first.push_back("comm_slots.bin");
-        plan.keep_host = [](const std::string& rel) {
-            return rel == "graphs.bin" || rel == "patch.bin" || rel == "comm_slots.bin";
-        };
+        plan.keep_host = [](const std::string& rel) { return rel == "patch.bin" || rel == "comm_slots.bin"; };
     }
     try {
         staged = std::make_unique<StagedArchive>(dev, root, manifest, lanes, &st, plan);
@@ -670,7 +670,7 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
         rethrow_in_step("archive integrity");
     }
     const auto t1 = Clock::now();
-    std::vector<uint8_t> packed;  // reference-written archive: pack now
+    std::vector<uint8_t> packed;  // reference-written archive: packed now, on the GPU
     DeviceStore store;
     if (has_store) {
         const auto host = staged->host("templates.fdt");
@@ -678,16 +678,19 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
         staged->order_after("templates.fdt", dev.stream());
         store = adopt_store(dev, staged->device("templates.fdt"), host.size(), view.header());
     } else {
+        DevicePackResult gpu;
         try {
-            packed = pack_template_store(staged->host("graphs.bin"), staged->host("patch.bin"), manifest,
-                                         lanes, nullptr,
-                                         staged->has("comm_slots.bin") ? staged->host("comm_slots.bin")
-                                                                       : std::span<const uint8_t>{});
+            staged->order_after("graphs.bin", dev.stream());
+            gpu = pack_template_store_device(dev, staged->host("graphs.bin"), staged->device("graphs.bin"),
+                                             staged->host("patch.bin"), manifest,
+                                             staged->has("comm_slots.bin") ? staged->host("comm_slots.bin")
+                                                                           : std::span<const uint8_t>{});
         } catch (const Error&) {
             rethrow_in_step("template construction");
         }
-        store = upload_store(dev, packed.data(), packed.size());
-        st.h2d_bytes += packed.size();
+        packed = std::move(gpu.host);
+        store = adopt_store(dev, gpu.blob.data(), packed.size(), StoreView(packed).header());
+        store.blob = std::move(gpu.blob);
     }
     const fdt_header& H = store.header;
     check_store_sources(H, manifest);

@@ -124,6 +124,10 @@ bool lane_flag(const std::vector<uint8_t>& meta, uint64_t lane) {
     return (meta[lane / 2] >> (lane % 2)) & 1u;
 }
 
+}  // namespace
+
+namespace store_detail {
+
 // Splits a little-endian write of `width` bytes at image byte offset `at`
 // into per-chunk ops.
 void emit_write(std::vector<fdt_rank_op>& ops, uint64_t at, uint32_t width, uint8_t kind,
@@ -142,6 +146,12 @@ void emit_write(std::vector<fdt_rank_op>& ops, uint64_t at, uint32_t width, uint
         b = end;
     }
 }
+
+}  // namespace store_detail
+
+namespace {
+
+using store_detail::emit_write;
 
 template <typename T>
 uint64_t put_section(Sink& s, fdt_header& h, int id, const T* data, size_t count) {

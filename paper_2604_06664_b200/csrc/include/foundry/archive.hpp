@@ -8,7 +8,9 @@
 // kernel_image.hpp:11-61, kernel_image.cpp:14-117; templater.hpp:15-38).
 #pragma once
 
+#include <array>
 #include <cstdint>
+#include <string_view>
 #include <filesystem>
 #include <map>
 #include <optional>
@@ -182,6 +184,32 @@ struct PatchTable {
 };
 
 std::vector<uint8_t> serialize_patch_table(const PatchTable& t);
+
+// Zero-copy view of a patch table (same validation, same errors as
+// parse_patch_table): entries point into the bytes, which must outlive it.
+// LOAD reads the table through this (no per-entry allocations).
+struct PatchEntryView {
+    uint32_t node_id = 0;
+    uint64_t stub_hash = 0;
+    std::string_view stub_name, real_name;
+    const uint8_t* rank_offsets = nullptr;  // n_rank little-endian u32
+    const uint8_t* world_offsets = nullptr;
+    uint32_t n_rank = 0, n_world = 0;
+    uint8_t patch_width = 8;
+    uint32_t rank_offset(uint32_t i) const;
+    uint32_t world_offset(uint32_t i) const;
+};
+struct PatchView {
+    uint64_t world_placeholder = 1;
+    std::vector<PatchEntryView> entries;
+    // label -> [first, first + count) in entries, sorted by label; the first
+    // occurrence of a label wins (parse_patch_table's map emplace)
+    std::vector<std::array<uint32_t, 3>> graphs;
+    bool empty() const { return graphs.empty(); }
+    std::span<const PatchEntryView> find(uint32_t label) const;  // empty span: none
+    bool has(uint32_t label) const;
+};
+PatchView parse_patch_view(std::span<const uint8_t> bytes);
 PatchTable parse_patch_table(std::span<const uint8_t> bytes);
 
 // ------------------------------------------------------------ comm slots

@@ -1,0 +1,50 @@
+// GPU packer (kernels/pack.cu + host/device_pack.cpp): the FNDT template
+// store that pack_template_store (template_store.hpp) writes offline, built on
+// the device from an archive's graphs.bin already resident in HBM, for
+// archives written by the reference (no templates.fdt).
+#pragma once
+
+#include <cstdint>
+#include <span>
+#include <vector>
+
+#include "foundry/archive.hpp"
+#include "foundry/device.hpp"
+#include "foundry/template_store.hpp"
+
+namespace foundry {
+
+struct DevicePackTimings {
+    double prep_ms = 0;   // patch table view, member / group tables
+    double pass1_ms = 0;  // upload + walk/fields/edges/verify/compact + record CRCs
+    double host1_ms = 0;  // checks, kernel table, layout, rank ops
+    double pass2_ms = 0;  // images + diff counts
+    double host2_ms = 0;  // tile table, host sections
+    double pass3_ms = 0;  // diff writes + template images + D2H of the device sections
+    double total_ms = 0;
+    uint32_t kernel_keys = 0;  // distinct kernel keys the GPU table found
+    uint32_t retries = 0;      // fingerprint collisions resolved by a reseed
+};
+
+struct DevicePackResult {
+    std::vector<uint8_t> host;  // the store, byte-identical to pack_template_store's
+    DeviceBuffer blob;          // the same bytes in HBM
+};
+
+// graphs_host / d_graphs: graphs.bin on the host and in HBM (the device copy
+// is read by the kernels; the host copy only for per-group and per-kernel
+// metadata and, on error paths, to re-derive the reference's exact message for
+// the failing record). Asynchronous work runs on dev.stream(); returns after a
+// synchronize.
+DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t> graphs_host,
+                                            const unsigned char* d_graphs, std::span<const uint8_t> patch_bin,
+                                            const Manifest& manifest, std::span<const uint8_t> slots_bin = {},
+                                            PackStats* stats = nullptr, DevicePackTimings* timings = nullptr);
+
+// The same for an archive directory: reads and uploads graphs.bin, packs it on
+// the GPU, returns the store bytes (the tests compare them with the offline
+// packer's; LOAD and fdy_prepare_archive use the staged path above).
+std::vector<uint8_t> pack_archive_store_device(Device& dev, const std::filesystem::path& archive,
+                                               DevicePackTimings* timings = nullptr);
+
+}  // namespace foundry

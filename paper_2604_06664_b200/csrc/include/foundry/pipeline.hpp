@@ -85,7 +85,8 @@ struct LoadTimings {
     double total_ms = 0, manifest_ms = 0, stage_ms = 0, integrity_ms = 0, restore_ms = 0,
            region_ms = 0, materialize_ms = 0, download_ms = 0, build_ms = 0, instantiate_ms = 0,
            foreground_ms = 0,
-           function_load_ms = 0;  // share_execs: loading the functions of exec-sharing templates
+           function_load_ms = 0,  // share_execs: loading the functions of exec-sharing templates
+           pack_ms = 0;           // reference-written archive: the GPU packer (graphs.bin -> store)
     float crc_kernel_ms = 0, materialize_kernel_ms = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0, member_bytes = 0, store_bytes = 0;
     uint64_t graphs = 0, nodes = 0, templates = 0;

@@ -49,6 +49,12 @@ PackStats pack_archive_store(const std::filesystem::path& archive, unsigned thre
 // against graphs.bin + patch.bin first (the packer's checks).
 void write_comm_slots(const std::filesystem::path& archive, const CommSlotTable& table);
 
+// The packer's rank-op emitter (shared with the GPU packer): a little-endian
+// write of `width` bytes at image byte offset `at`, split into per-chunk ops.
+namespace store_detail {
+void emit_write(std::vector<fdt_rank_op>& ops, uint64_t at, uint32_t width, uint8_t kind, uint32_t aux);
+}
+
 class StoreView {
 public:
     explicit StoreView(std::span<const uint8_t> blob);

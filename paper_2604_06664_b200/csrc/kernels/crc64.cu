@@ -122,7 +122,7 @@ crc_blocks_kernel(const unsigned char* __restrict__ base, const FdyCrcBlock* __r
 
     for (uint32_t b = blockIdx.x; b < n_blocks; b += gridDim.x) {
         const FdyCrcBlock blk = blocks[b];
-        if (blk.length == kCrcBlockBytes) {  // uniform per CTA
+        if (blk.length == kCrcBlockBytes && (blk.offset & 15u) == 0) {  // uniform per CTA
             // Braid: warp w owns the block's 8 KiB region w; lane l takes its
             // 16-byte chunks j = 32 k + l (each warp load is 512 contiguous
             // bytes) and runs Horner with the 512-byte advance:
@@ -145,14 +145,19 @@ crc_blocks_kernel(const unsigned char* __restrict__ base, const FdyCrcBlock* __r
                     out_len[b] = blk.length;
                 }
             }
-        } else {  // a segment's short last block: 256 contiguous bytes per thread,
-                  // weighted by generic mulmod, plain XOR reduction
+        } else {  // a segment's short last block, or any block of a segment that is
+                  // not 16-byte aligned (graph records inside graphs.bin): 256
+                  // contiguous bytes per thread, weighted by generic mulmod,
+                  // plain XOR reduction
             const uint32_t lo = umin(blk.length, tid * kBytesPerThread);
             const uint32_t hi = umin(blk.length, lo + kBytesPerThread);
             const unsigned char* p = base + blk.offset + lo;
             uint64_t c = 0;
             uint32_t i = 0;
             const uint32_t n = hi - lo;
+            // bytewise up to the first 16-byte boundary (the linear CRC state
+            // takes bytes and words alike)
+            for (; i < n && (reinterpret_cast<uintptr_t>(p + i) & 15u); ++i) c = crc_byte_bitwise(c, p[i]);
             for (; i + 16 <= n; i += 16) {
                 const uint4 v = __ldg(reinterpret_cast<const uint4*>(p + i));
                 c = mulc(A8, c ^ ((uint64_t(v.y) << 32) | v.x));

@@ -72,6 +72,69 @@ struct FdyServeArgs {
     uint32_t inject_failure;        // FaultInjection::fail_device_serve
 };
 
+// GPU packer (kernels/pack.cu): a reference-written archive's graphs.bin, in
+// HBM, becomes the same FNDT template store the offline packer writes
+// (host/template_store.cpp), decoded, diffed and compacted on the device.
+// Members are numbered group-major in manifest order (the packer's order).
+enum : uint32_t {
+    FDY_PACK_DECODE = 1u,  // record fails to decode or validate: the host re-parses it for the message
+    FDY_PACK_TOPO = 2u,    // topology differs from the group representative's
+};
+
+struct FdyPackArgs {
+    const unsigned char* graphs;  // graphs.bin in HBM
+    uint64_t graphs_bytes;
+    // per member
+    const uint64_t* rec_off;      // record offset / length in graphs.bin (locator)
+    const uint64_t* rec_len;
+    const uint32_t* node_base;    // first global node index
+    const uint32_t* n_nodes;      // node / edge counts from the record header (0 if unusable)
+    const uint32_t* n_edges;
+    const uint32_t* member_group;
+    const uint64_t* out_off;      // pass 2: member image offset in the pack arena
+    const uint32_t* tile_base;    // pass 2: first natural-order tile
+    // per group
+    const uint32_t* group_rep;    // member index of the representative
+    const uint32_t* gnode_base;   // first per-(group, node) slot
+    const uint64_t* g_image;      // pass 2: image bytes
+    // per global node
+    uint32_t* node_off;           // record-relative node offset (walk)
+    uint32_t* node_member;        // member of the node (walk; ~0u = not decoded)
+    uint32_t* node_slot;          // kernel-table slot (kernel nodes)
+    // per (group, node)
+    uint32_t* cap;                // max over the group of round16(blob length)
+    const uint32_t* blob_off;     // pass 2: slot offset in the pool
+    fdt_node_attrs* rep_attrs;    // the representative's launch attributes
+    // kernel table: open addressing over 64-bit key fingerprints
+    unsigned long long* tkey;     // 0 = empty slot
+    unsigned long long* tpos;     // min over the key's nodes of (member << 32 | node)
+    uint32_t* tuniq;              // slot -> compacted index
+    uint32_t tmask;
+    uint32_t n_members;
+    uint64_t seed;
+    unsigned long long* upos;     // compacted: first position of each key
+    uint64_t* uoff;               //            absolute graphs.bin offset of that node
+    uint32_t* ucount;
+    const uint32_t* ukidx;        // pass 2: compacted index -> store kernel index
+    const uint32_t* swap_node;    // pass 2: global node -> real comm kernel (stub swap)
+    const uint32_t* swap_kidx;
+    uint32_t n_swaps;
+    uint32_t total_nodes;
+    uint32_t* status;             // per member: FDY_PACK_* bits
+    uint32_t* flags;              // [0]: fingerprint collision
+    // pass 2
+    unsigned char* arena;         // member pack images (captured state + stub swaps)
+    uint8_t* meta;                // FDT_CMETA_* per 16-byte chunk of arena
+    const uint32_t* tile_member;  // per natural tile
+    uint32_t* tile_count;         // diff entries per natural tile
+    uint8_t* tile_reloc;          // 1: the tile's template chunks hold a relocatable lane
+    const uint32_t* diff_lo;      // first diff entry per natural tile
+    uint16_t* didx;               // store FDT_SEC_DIDX / FDT_SEC_DDATA
+    uint64_t* ddata;
+    uint32_t n_tiles;
+    uint32_t pad_;
+};
+
 struct FdyCrcBlock {
     uint32_t segment;
     uint32_t length;   // <= kCrcBlockBytes
@@ -90,6 +153,15 @@ cudaError_t fdy_launch_materialize_split(const FdyMaterializeArgs* args, int gri
 // delta == 0: one grid. Otherwise the template relocation grid, then the
 // member grid under programmatic dependent launch (both on `stream`).
 cudaError_t fdy_launch_materialize(const FdyMaterializeArgs* args, int grid, cudaStream_t stream);
+
+// GPU packer passes (pack.cu), in stream order. Pass 1: walk (node offsets,
+// record structure), fields (validation, topology, slot capacities, kernel
+// keys), edges, verify (fingerprint collisions), compact (distinct keys).
+// Pass 2 (after the host lays out groups and the kernel table): images, swaps,
+// diff counts; pass 3: diff writes.
+cudaError_t fdy_launch_pack_pass1(const FdyPackArgs* args, cudaStream_t stream);
+cudaError_t fdy_launch_pack_pass2(const FdyPackArgs* args, cudaStream_t stream);
+cudaError_t fdy_launch_pack_pass3(const FdyPackArgs* args, cudaStream_t stream);
 
 // per device: x^(2^k) mod P and the constant-multiplier nibble tables built from them
 cudaError_t fdy_crc64_set_constants(const uint64_t* x2k64);

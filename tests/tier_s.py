@@ -57,7 +57,8 @@ def make_tier_s(src: str, dst: str, crc64, seed: int = 7) -> str:
         grp["locators"] = [list(by_label[l[0]]) for l in grp["locators"]]
     m["files"]["graphs.bin"] = crc64(data)
     m["files"].pop("templates.fdt", None)
-    os.remove(os.path.join(dst, "templates.fdt"))
+    if os.path.exists(os.path.join(dst, "templates.fdt")):
+        os.remove(os.path.join(dst, "templates.fdt"))
     json.dump(m, open(os.path.join(dst, "manifest"), "w"))
     return dst
 
