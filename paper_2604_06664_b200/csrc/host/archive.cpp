@@ -722,6 +722,7 @@ PatchView parse_patch_view(std::span<const uint8_t> bytes) {
     t.world_placeholder = c.u64();
     const uint32_t ng = c.u32();
     t.graphs.reserve(std::min<size_t>(ng, bytes.size() / 8));
+    t.entries.reserve(bytes.size() / 29);  // an entry is at least 29 bytes: no regrowth
     for (uint32_t g = 0; g < ng; ++g) {
         const uint32_t label = c.u32();
         const uint32_t n = c.u32();

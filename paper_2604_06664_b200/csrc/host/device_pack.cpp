@@ -107,10 +107,12 @@ struct NodeView {  // a kernel node's fields, read from the host copy
 DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t> graphs_host,
                                             const unsigned char* d_graphs, std::span<const uint8_t> patch_bin,
                                             const Manifest& manifest, std::span<const uint8_t> slots_bin,
-                                            PackStats* stats, DevicePackTimings* timings) {
+                                            PackStats* stats, DevicePackTimings* timings, bool full_host_copy,
+                                            const uint64_t* verified_graphs_crc) {
     const auto t_all = Clock::now();
     DevicePackTimings tm;
     const PatchView patches = parse_patch_view(patch_bin);
+    tm.patch_parse_ms = ms_of(t_all);
     const CommSlotTable slots = slots_bin.empty() ? CommSlotTable{} : parse_comm_slots(slots_bin);
     if (!patches.empty())
         require(manifest.comm_real_hash != 0, Errc::unresolved_kernel,
@@ -167,8 +169,104 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     std::vector<uint32_t> gnode_base(n_groups + 1, 0);
     for (uint32_t g = 0; g < n_groups; ++g) gnode_base[g + 1] = gnode_base[g] + n_nodes[group_rep[g]];
     const uint32_t GN = gnode_base[n_groups];
+
+    // patch entries, flattened in member order (apply_rank_patches' table);
+    // names interned (a handful of distinct stub / real comm names)
+    std::vector<uint32_t> pe_node, pe_stub_name, pe_real_name, pe_need, entry_base(nm + 1, 0);
+    std::vector<uint64_t> pe_stub_hash;
+    std::vector<uint8_t> patch_bad(nm, 0);  // the host already sees a patch / slot problem
+    std::vector<std::string_view> name_list;
+    std::string name_bytes;
+    std::vector<uint32_t> name_off, name_len;
+    auto intern = [&](std::string_view n) -> uint32_t {
+        for (uint32_t i = 0; i < name_list.size(); ++i)
+            if (name_list[i].size() == n.size() && std::memcmp(name_list[i].data(), n.data(), n.size()) == 0) return i;
+        name_list.push_back(n);
+        name_off.push_back(static_cast<uint32_t>(name_bytes.size()));
+        name_len.push_back(static_cast<uint32_t>(n.size()));
+        name_bytes.append(n);
+        return static_cast<uint32_t>(name_list.size() - 1);
+    };
+    if (!patches.empty() || !slots.empty()) {
+        // entry ranges per member, then the entries filled on host threads
+        std::vector<std::span<const PatchEntryView>> entries_of(nm);
+        uint32_t ne = 0;
+        for (uint32_t m = 0; m < nm; ++m) {
+            entries_of[m] = patches.find(loc_of[m]->label);
+            entry_base[m] = ne;
+            ne += static_cast<uint32_t>(entries_of[m].size());
+        }
+        pe_node.resize(ne);
+        pe_stub_hash.resize(ne);
+        pe_stub_name.resize(ne);
+        pe_real_name.resize(ne);
+        pe_need.resize(ne);
+        for (uint32_t m = 0; m < nm; ++m)  // the distinct names, in first-use order
+            for (const PatchEntryView& e : entries_of[m].first(std::min<size_t>(entries_of[m].size(), 64))) {
+                intern(e.stub_name);
+                intern(e.real_name);
+            }
+        // the name table is frozen during the parallel fill: a name the scan
+        // above did not see leaves the member for a sequential fix-up
+        std::vector<uint8_t> unnamed(nm, 0);
+        parallel_for(nm, 0, [&](size_t mi) {
+            const uint32_t m = static_cast<uint32_t>(mi);
+            const uint32_t label = loc_of[m]->label;
+            const auto entries = entries_of[m];
+            uint32_t last_stub = 0, last_real = 0;
+            auto id_of = [&](std::string_view n, uint32_t& last) {
+                if (last < name_list.size() && name_list[last] == n) return last;
+                for (uint32_t i = 0; i < name_list.size(); ++i)
+                    if (name_list[i] == n) return last = i;
+                unnamed[m] = 1;
+                return kNoKernel;
+            };
+            for (uint32_t j = 0; j < entries.size(); ++j) {
+                const PatchEntryView& e = entries[j];
+                const uint32_t i = entry_base[m] + j;
+                const bool in = e.node_id < n_nodes[m];
+                if (!in) patch_bad[m] = 1;
+                pe_node[i] = in ? node_base[m] + e.node_id : kNoKernel;
+                pe_stub_hash[i] = e.stub_hash;
+                pe_stub_name[i] = id_of(e.stub_name, last_stub);
+                pe_real_name[i] = id_of(e.real_name, last_real);
+                uint64_t need = 0;
+                for (uint32_t k = 0; k < e.n_rank; ++k) need = std::max<uint64_t>(need, e.rank_offset(k) + 8ull);
+                for (uint32_t k = 0; k < e.n_world; ++k) need = std::max<uint64_t>(need, e.world_offset(k) + 8ull);
+                if (need > UINT32_MAX) patch_bad[m] = 1;
+                pe_need[i] = static_cast<uint32_t>(std::min<uint64_t>(need, UINT32_MAX));
+            }
+            auto sit = slots.per_graph.find(label);
+            if (sit == slots.per_graph.end()) return;
+            if (!patches.has(label)) {
+                patch_bad[m] = 1;
+                return;
+            }
+            std::vector<std::pair<uint32_t, uint32_t>> by_node;  // (node id, entry)
+            for (uint32_t j = 0; j < entries.size(); ++j) by_node.push_back({entries[j].node_id, entry_base[m] + j});
+            std::sort(by_node.begin(), by_node.end());
+            for (const CommSlot& c : sit->second) {
+                auto it = std::lower_bound(by_node.begin(), by_node.end(), std::make_pair(c.node_id, 0u));
+                const uint64_t end = uint64_t(c.offset) + c.width;
+                if (it == by_node.end() || it->first != c.node_id || end > UINT32_MAX) {
+                    patch_bad[m] = 1;
+                    continue;
+                }
+                pe_need[it->second] = std::max<uint32_t>(pe_need[it->second], static_cast<uint32_t>(end));
+            }
+        });
+        for (uint32_t m = 0; m < nm; ++m) {
+            if (!unnamed[m]) continue;
+            for (uint32_t j = 0; j < entries_of[m].size(); ++j) {
+                pe_stub_name[entry_base[m] + j] = intern(entries_of[m][j].stub_name);
+                pe_real_name[entry_base[m] + j] = intern(entries_of[m][j].real_name);
+            }
+        }
+        entry_base[nm] = ne;
+    }
+    const uint32_t NE = entry_base[nm];
     uint32_t tslots = 1024;
-    while (tslots < 2ull * TN) tslots <<= 1;
+    while (tslots < 2ull * (uint64_t(TN) + NE)) tslots <<= 1;
 
     // ------------------------------------------------ pass 1
     tm.prep_ms = ms_of(t_all);
@@ -176,7 +274,9 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     Scratch s1(dev, Scratch::need({8ull * nm, 8ull * nm, 4ull * nm, 4ull * nm, 4ull * nm, 4ull * nm, 4ull * nm,
                                    4ull * n_groups, 4ull * n_groups, 4ull * TN, 4ull * TN, 4ull * TN, 4ull * GN,
                                    sizeof(fdt_node_attrs) * GN, 8ull * tslots, 8ull * tslots, 4ull * tslots,
-                                   8ull * tslots, 8ull * tslots, 16}));
+                                   8ull * tslots, 8ull * tslots, 16, 4ull * NE, 8ull * NE, 4ull * NE, 4ull * NE,
+                                   4ull * NE, 4ull * NE, 4ull * (nm + 1), name_bytes.size() + 1,
+                                   4ull * name_off.size(), 4ull * name_len.size()}));
     FdyPackArgs a{};
     a.graphs = d_graphs;
     a.graphs_bytes = gsize;
@@ -200,6 +300,38 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     a.upos = s1.take<unsigned long long>(tslots);
     a.uoff = s1.take<uint64_t>(tslots);
     auto* d_small = s1.take<uint32_t>(4);  // ucount, flags
+    auto* d_pe_node = s1.take<uint32_t>(NE);
+    auto* d_pe_stub_hash = s1.take<uint64_t>(NE);
+    auto* d_pe_stub_name = s1.take<uint32_t>(NE);
+    auto* d_pe_real_name = s1.take<uint32_t>(NE);
+    auto* d_pe_need = s1.take<uint32_t>(NE);
+    a.pe_slot = s1.take<uint32_t>(NE);
+    auto* d_entry_base = s1.take<uint32_t>(nm + 1);
+    auto* d_names = s1.take<unsigned char>(name_bytes.size() + 1);
+    auto* d_name_off = s1.take<uint32_t>(name_off.size());
+    auto* d_name_len = s1.take<uint32_t>(name_len.size());
+    a.pe_node = d_pe_node;
+    a.pe_stub_hash = d_pe_stub_hash;
+    a.pe_stub_name = d_pe_stub_name;
+    a.pe_real_name = d_pe_real_name;
+    a.pe_need = d_pe_need;
+    a.entry_base = d_entry_base;
+    a.names = d_names;
+    a.name_off = d_name_off;
+    a.name_len = d_name_len;
+    a.comm_real_hash = manifest.comm_real_hash;
+    a.n_entries = NE;
+    h2d(d_pe_node, pe_node, st);
+    h2d(d_pe_stub_hash, pe_stub_hash, st);
+    h2d(d_pe_stub_name, pe_stub_name, st);
+    h2d(d_pe_real_name, pe_real_name, st);
+    h2d(d_pe_need, pe_need, st);
+    h2d(d_entry_base, entry_base, st);
+    h2d(d_name_off, name_off, st);
+    h2d(d_name_len, name_len, st);
+    if (!name_bytes.empty())
+        cuda_check(cudaMemcpyAsync(d_names, name_bytes.data(), name_bytes.size(), cudaMemcpyHostToDevice, st),
+                   "GPU pack H2D");
     a.rec_off = d_rec_off;
     a.rec_len = d_rec_len;
     a.node_base = d_node_base;
@@ -227,8 +359,9 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     }
     // record CRCs (parse_graph_at's per-record check) and the whole file's
     // digest (the store header's source_graphs_crc), on the GPU
+    // (the whole file only when the caller has not already verified it)
     std::vector<Segment> segs;
-    segs.push_back({0, gsize});
+    segs.push_back({0, verified_graphs_crc ? 0 : gsize});
     for (uint32_t m = 0; m < nm; ++m) segs.push_back({rec_off[m], rec_len[m]});
 
     std::vector<uint32_t> status, small;
@@ -265,7 +398,44 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     // ------------------------------------------------ host: checks, kernel table, layout
     t0 = Clock::now();
     auto node_ptr = [&](uint32_t m, uint32_t n) { return G + rec_off[m] + node_off[node_base[m] + n]; };
-    // errors in the offline packer's order: group by group, decode, topology, patches
+    // apply_rank_patches' checks with the reference's messages, reading the
+    // node bytes on the host: only run for a group whose entries the GPU (or
+    // the host's table scan) rejected
+    auto check_patches_exact = [&](uint32_t m) {
+        const uint32_t label = loc_of[m]->label;
+        const bool patched = patches.has(label);
+        auto sit = slots.per_graph.find(label);
+        require(sit == slots.per_graph.end() || patched, Errc::archive_corruption,
+                "comm slot table lists graph " + std::to_string(label) + ", which has no comm patches");
+        if (!patched) return;
+        const auto entries = patches.find(label);
+        for (const PatchEntryView& e : entries) {
+            require(e.node_id < n_nodes[m], Errc::archive_corruption, "patch entry references missing node");
+            const uint8_t* q = node_ptr(m, e.node_id);
+            require(q[0] == 0, Errc::archive_corruption, "patch entry references a non-kernel node");
+            const NodeView v{q};
+            require(v.hash() == e.stub_hash && v.name() == e.stub_name, Errc::archive_corruption,
+                    "node " + std::to_string(e.node_id) + " is not the recorded stub " +
+                        KernelRef{e.stub_hash, std::string(e.stub_name)}.describe());
+            for (uint32_t i = 0; i < e.n_rank; ++i)
+                require(uint64_t(e.rank_offset(i)) + 8 <= v.arg_size(), Errc::invalid_argument,
+                        "patch offset outside the argument buffer");
+            for (uint32_t i = 0; i < e.n_world; ++i)
+                require(uint64_t(e.world_offset(i)) + 8 <= v.arg_size(), Errc::invalid_argument,
+                        "patch offset outside the argument buffer");
+        }
+        if (sit == slots.per_graph.end()) return;
+        for (const CommSlot& c : sit->second) {
+            bool stub = false;
+            for (const PatchEntryView& e : entries) stub = stub || e.node_id == c.node_id;
+            require(stub && c.node_id < n_nodes[m] && node_ptr(m, c.node_id)[0] == 0, Errc::archive_corruption,
+                    "comm slot references node " + std::to_string(c.node_id) + ", which is not a patched comm node");
+            require(uint64_t(c.offset) + c.width <= NodeView{node_ptr(m, c.node_id)}.arg_size(),
+                    Errc::invalid_argument, "comm slot offset outside the argument buffer");
+        }
+    };
+    // errors in the offline packer's order: group by group, decode, topology,
+    // patches (representative first)
     auto decode_error = [&](uint32_t m) {
         const bool crc_bad = digests[1 + m] != loc_of[m]->checksum;
         return suspect[m] || crc_bad || (status[m] & FDY_PACK_DECODE);
@@ -285,73 +455,40 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
             require(k == want, Errc::topology_mismatch,
                     "donor topology " + k.hex() + " does not match exec topology " + want.hex());
         }
+        bool patch_error = false;
+        for (uint32_t m = f; m < e; ++m) patch_error |= patch_bad[m] || (status[m] & FDY_PACK_PATCH);
+        if (!patch_error) continue;
+        check_patches_exact(group_rep[g]);
+        for (uint32_t m = f; m < e; ++m)
+            if (m != group_rep[g]) check_patches_exact(m);
+        raise(Errc::archive_corruption, "a patch entry of group " + std::to_string(g) + " was rejected on the GPU");
     }
 
     // kernel table: every distinct (hash, func attrs, name) in first-occurrence
     // order, where a graph's patch entries' real comm kernels follow its nodes
-    struct KeyAt {
-        unsigned long long pos;
-        int64_t gpu;  // compacted GPU index, or -1 (a patch entry's real kernel)
-        uint64_t hash;
-        const uint8_t* fattrs;
-        std::string_view name;
-    };
-    std::vector<KeyAt> keys;
-    keys.reserve(nu + 64);
-    for (uint32_t u = 0; u < nu; ++u) {
-        const NodeView v{G + uoff[u]};
-        keys.push_back({upos[u], u, v.hash(), v.fattrs(), v.name()});
-    }
-    // real comm kernels: few distinct (name, func attrs); the first position of each
-    struct RealKey {
-        std::array<uint8_t, 24> fattrs;
-        uint32_t kidx;
-    };
-    std::unordered_map<std::string_view, std::vector<RealKey>> real_keys;
-    auto real_slot = [&](std::string_view name, const uint8_t* fa) -> RealKey* {  // lookup only
-        auto it = real_keys.find(name);
-        if (it == real_keys.end()) return nullptr;
-        for (RealKey& r : it->second)
-            if (std::memcmp(r.fattrs.data(), fa, 24) == 0) return &r;
-        return nullptr;
-    };
-    if (!patches.empty()) {
-        for (uint32_t m = 0; m < nm; ++m) {
-            const auto entries = patches.find(loc_of[m]->label);
-            for (size_t j = 0; j < entries.size(); ++j) {
-                const PatchEntryView& e = entries[j];
-                if (e.node_id >= n_nodes[m] || node_ptr(m, e.node_id)[0] != 0) continue;
-                const NodeView v{node_ptr(m, e.node_id)};
-                if (real_slot(e.real_name, v.fattrs())) continue;
-                RealKey r{};
-                std::memcpy(r.fattrs.data(), v.fattrs(), 24);
-                r.kidx = kNoKernel;
-                real_keys[e.real_name].push_back(r);
-                keys.push_back({(uint64_t(m) << 32) | (n_nodes[m] + j), -1, manifest.comm_real_hash,
-                                v.fattrs(), e.real_name});
-            }
-        }
-    }
-    std::sort(keys.begin(), keys.end(), [](const KeyAt& x, const KeyAt& y) { return x.pos < y.pos; });
-    std::unordered_map<std::string, uint32_t> kindex;
-    kindex.reserve(keys.size() * 2);
-    std::vector<fdt_kernel> kernels;
+    // (the GPU table holds both; positions order them)
+    std::vector<uint32_t> order(nu);
+    for (uint32_t u = 0; u < nu; ++u) order[u] = u;
+    std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return upos[x] < upos[y]; });
+    std::vector<fdt_kernel> kernels(nu);
     std::string strings;
     std::vector<uint32_t> ukidx(nu, kNoKernel);
-    for (const KeyAt& k : keys) {
-        auto [it, fresh] = kindex.try_emplace(kernel_key(k.hash, k.fattrs, k.name),
-                                              static_cast<uint32_t>(kernels.size()));
-        if (fresh) {
-            fdt_kernel K{};
-            K.binary_hash = k.hash;
-            K.name_off = static_cast<uint32_t>(strings.size());
-            K.name_len = static_cast<uint32_t>(k.name.size());
-            std::memcpy(K.func_attrs, k.fattrs, 24);
-            kernels.push_back(K);
-            strings.append(k.name);
+    for (uint32_t k = 0; k < nu; ++k) {
+        const uint32_t u = order[k];
+        const uint32_t m = uint32_t(upos[u] >> 32), local = uint32_t(upos[u]);
+        const NodeView v{G + uoff[u]};  // the node, or the stub node of a real comm kernel
+        fdt_kernel& K = kernels[k];
+        std::string_view name = v.name();
+        K.binary_hash = v.hash();
+        if (local >= n_nodes[m]) {
+            name = name_list[pe_real_name[entry_base[m] + (local - n_nodes[m])]];
+            K.binary_hash = manifest.comm_real_hash;
         }
-        if (k.gpu >= 0) ukidx[k.gpu] = it->second;
-        else real_slot(k.name, k.fattrs)->kidx = it->second;
+        K.name_off = static_cast<uint32_t>(strings.size());
+        K.name_len = static_cast<uint32_t>(name.size());
+        std::memcpy(K.func_attrs, v.fattrs(), 24);
+        strings.append(name);
+        ukidx[u] = k;
     }
 
     // group layouts: slot capacity = group-wide maximum (round16), in node order
@@ -381,103 +518,45 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     }
     const uint32_t n_tiles = static_cast<uint32_t>(tile_member.size());
 
-    // stub swaps + rank ops (apply_rank_patches split as in patch_graph),
-    // checked as the offline packer checks them: per group, representative
-    // first, then members in order (members run on host threads; the first
-    // error in that order is raised)
-    std::vector<std::vector<uint32_t>> swaps_of(nm);
+    // rank ops (apply_rank_patches' rank / world writes, then comm slots as
+    // value ops), per member in table order, stably sorted by chunk; the stub
+    // -> real kernel swap is the GPU's (pack_swaps_kernel)
     std::vector<std::vector<fdt_rank_op>> rops_of(nm);
-    auto patch_member = [&](uint32_t m) {
-        const uint32_t label = loc_of[m]->label;
-        const uint32_t gi0 = gnode_base[member_group[m]];
-        const uint64_t desc = g_desc[member_group[m]];
-        const bool patched = patches.has(label);
-        auto sit = slots.per_graph.find(label);
-        require(sit == slots.per_graph.end() || patched, Errc::archive_corruption,
-                "comm slot table lists graph " + std::to_string(label) + ", which has no comm patches");
-        if (!patched) return;
-        const auto entries = patches.find(label);
-        auto& ops = rops_of[m];
-        auto& sw = swaps_of[m];
-        for (const PatchEntryView& e : entries) {
-            require(e.node_id < n_nodes[m], Errc::archive_corruption, "patch entry references missing node");
-            const uint8_t* q = node_ptr(m, e.node_id);
-            require(q[0] == 0, Errc::archive_corruption, "patch entry references a non-kernel node");
-            const NodeView v{q};
-            require(v.hash() == e.stub_hash && v.name() == e.stub_name, Errc::archive_corruption,
-                    "node " + std::to_string(e.node_id) + " is not the recorded stub " +
-                        KernelRef{e.stub_hash, std::string(e.stub_name)}.describe());
-            RealKey* r = real_slot(e.real_name, v.fattrs());
-            require(r != nullptr && r->kidx != kNoKernel, Errc::invalid_argument, "kernel table: missing entry");
-            sw.push_back(node_base[m] + e.node_id);
-            sw.push_back(r->kidx);
-            const uint64_t blob = desc + blob_off[gi0 + e.node_id];
-            for (uint32_t i = 0; i < e.n_rank; ++i) {
-                const uint32_t off = e.rank_offset(i);
-                require(uint64_t(off) + 8 <= v.arg_size(), Errc::invalid_argument,
-                        "patch offset outside the argument buffer");
-                store_detail::emit_write(ops, blob + off, 8, FDT_ROP_RANK, 0);
+    if (NE || !slots.empty()) {
+        parallel_for(nm, 0, [&](size_t mi) {
+            const uint32_t m = static_cast<uint32_t>(mi);
+            const uint32_t label = loc_of[m]->label;
+            const uint32_t gi0 = gnode_base[member_group[m]];
+            const uint64_t desc = g_desc[member_group[m]];
+            auto& ops = rops_of[m];
+            for (const PatchEntryView& e : patches.find(label)) {
+                const uint64_t blob = desc + blob_off[gi0 + e.node_id];
+                for (uint32_t i = 0; i < e.n_rank; ++i)
+                    store_detail::emit_write(ops, blob + e.rank_offset(i), 8, FDT_ROP_RANK, 0);
+                for (uint32_t i = 0; i < e.n_world; ++i)
+                    store_detail::emit_write(ops, blob + e.world_offset(i), 8, FDT_ROP_WORLD, 0);
             }
-            for (uint32_t i = 0; i < e.n_world; ++i) {
-                const uint32_t off = e.world_offset(i);
-                require(uint64_t(off) + 8 <= v.arg_size(), Errc::invalid_argument,
-                        "patch offset outside the argument buffer");
-                store_detail::emit_write(ops, blob + off, 8, FDT_ROP_WORLD, 0);
-            }
-        }
-        if (sit != slots.per_graph.end()) {
-            for (const CommSlot& c : sit->second) {
-                bool stub = false;
-                for (const PatchEntryView& e : entries) stub = stub || e.node_id == c.node_id;
-                require(stub && c.node_id < n_nodes[m] && node_ptr(m, c.node_id)[0] == 0, Errc::archive_corruption,
-                        "comm slot references node " + std::to_string(c.node_id) +
-                            ", which is not a patched comm node");
-                require(uint64_t(c.offset) + c.width <= NodeView{node_ptr(m, c.node_id)}.arg_size(),
-                        Errc::invalid_argument, "comm slot offset outside the argument buffer");
-                store_detail::emit_write(ops, desc + blob_off[gi0 + c.node_id] + c.offset, c.width, FDT_ROP_VALUE,
-                                         c.value_index);
-            }
-        }
-        std::stable_sort(ops.begin(), ops.end(),
-                         [](const fdt_rank_op& x, const fdt_rank_op& y) { return x.chunk < y.chunk; });
-    };
-    if (!patches.empty() || !slots.empty()) {
-        std::vector<std::exception_ptr> err(nm);
-        parallel_for(nm, 0, [&](size_t m) {
-            try {
-                patch_member(static_cast<uint32_t>(m));
-            } catch (...) {
-                err[m] = std::current_exception();
-            }
+            auto sit = slots.per_graph.find(label);
+            if (sit != slots.per_graph.end())
+                for (const CommSlot& c : sit->second)
+                    store_detail::emit_write(ops, desc + blob_off[gi0 + c.node_id] + c.offset, c.width,
+                                             FDT_ROP_VALUE, c.value_index);
+            std::stable_sort(ops.begin(), ops.end(),
+                             [](const fdt_rank_op& x, const fdt_rank_op& y) { return x.chunk < y.chunk; });
         });
-        for (uint32_t g = 0; g < n_groups; ++g) {
-            const uint32_t f = group_first[g], e = g + 1 < n_groups ? group_first[g + 1] : nm;
-            if (err[group_rep[g]]) std::rethrow_exception(err[group_rep[g]]);
-            for (uint32_t m = f; m < e; ++m)
-                if (err[m]) std::rethrow_exception(err[m]);
-        }
     }
-    std::vector<uint32_t> swap_node, swap_kidx;
-    for (const auto& sw : swaps_of)
-        for (size_t i = 0; i < sw.size(); i += 2) {
-            swap_node.push_back(sw[i]);
-            swap_kidx.push_back(sw[i + 1]);
-        }
     tm.host1_ms = ms_of(t0);
 
     // ------------------------------------------------ pass 2
     t0 = Clock::now();
-    const uint32_t nsw = static_cast<uint32_t>(swap_node.size());
     Scratch s2(dev, Scratch::need({4ull * GN, 8ull * nm, 4ull * nm, 8ull * n_groups, 4ull * std::max(nu, 1u),
-                                   4ull * nsw, 4ull * nsw, 4ull * n_tiles, 4ull * n_tiles, n_tiles, 4ull * n_tiles,
-                                   arena_bytes, arena_bytes / 16}));
+                                   4ull * n_tiles, 4ull * n_tiles, n_tiles, 4ull * n_tiles, arena_bytes,
+                                   arena_bytes / 16}));
     auto* d_blob_off = s2.take<uint32_t>(GN);
     auto* d_out_off = s2.take<uint64_t>(nm);
     auto* d_tile_base = s2.take<uint32_t>(nm);
     auto* d_g_image = s2.take<uint64_t>(n_groups);
     auto* d_ukidx = s2.take<uint32_t>(std::max(nu, 1u));
-    auto* d_swap_node = s2.take<uint32_t>(nsw);
-    auto* d_swap_kidx = s2.take<uint32_t>(nsw);
     auto* d_tile_member = s2.take<uint32_t>(n_tiles);
     a.tile_count = s2.take<uint32_t>(n_tiles);
     a.tile_reloc = s2.take<uint8_t>(n_tiles);
@@ -489,9 +568,6 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     a.tile_base = d_tile_base;
     a.g_image = d_g_image;
     a.ukidx = d_ukidx;
-    a.swap_node = d_swap_node;
-    a.swap_kidx = d_swap_kidx;
-    a.n_swaps = nsw;
     a.tile_member = d_tile_member;
     a.diff_lo = d_diff_lo;
     a.n_tiles = n_tiles;
@@ -500,8 +576,6 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     h2d(d_tile_base, tile_base, st);
     h2d(d_g_image, g_image, st);
     h2d(d_ukidx, ukidx, st);
-    h2d(d_swap_node, swap_node, st);
-    h2d(d_swap_kidx, swap_kidx, st);
     h2d(d_tile_member, tile_member, st);
     cuda_check(fdy_launch_pack_pass2(&a, st), "GPU pack pass 2");
     std::vector<uint32_t> tile_count;
@@ -571,7 +645,8 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
         timages_bytes += g_image[g];
 
         // members' tiles; rank-op ranges shared per (group, tile index)
-        std::vector<std::map<std::string, std::pair<uint32_t, uint32_t>>> shared_ops;
+        // per tile index: the distinct op slices stored so far, as ranges of rops
+        std::vector<std::vector<std::pair<uint32_t, uint32_t>>> shared_ops;
         for (uint32_t m = Gp.first_member; m < Gp.first_member + Gp.n_members; ++m) {
             fdt_member& M = members[m];
             M.label = loc_of[m]->label;
@@ -598,17 +673,23 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
                 T.diff_hi = T.diff_lo + tile_count[tile_base[m] + t];
                 const size_t r_begin = rpos;
                 while (rpos < ops.size() && ops[rpos].chunk < ce) ++rpos;
-                const std::string key(reinterpret_cast<const char*>(ops.data() + r_begin),
-                                      (rpos - r_begin) * sizeof(fdt_rank_op));
-                auto [it, fresh] = shared_ops[t].try_emplace(key);
-                if (fresh) {
-                    it->second.first = static_cast<uint32_t>(rops.size());
+                const size_t n_ops = rpos - r_begin;
+                const std::pair<uint32_t, uint32_t>* hit = nullptr;
+                for (const auto& c : shared_ops[t])
+                    if (c.second - c.first == n_ops &&
+                        std::memcmp(rops.data() + c.first, ops.data() + r_begin, n_ops * sizeof(fdt_rank_op)) == 0) {
+                        hit = &c;
+                        break;
+                    }
+                if (!hit) {
+                    const uint32_t lo = static_cast<uint32_t>(rops.size());
                     rops.insert(rops.end(), ops.begin() + static_cast<long>(r_begin),
                                 ops.begin() + static_cast<long>(rpos));
-                    it->second.second = static_cast<uint32_t>(rops.size());
+                    shared_ops[t].push_back({lo, static_cast<uint32_t>(rops.size())});
+                    hit = &shared_ops[t].back();
                 }
-                T.rop_lo = it->second.first;
-                T.rop_hi = it->second.second;
+                T.rop_lo = hit->first;
+                T.rop_hi = hit->second;
                 tiles.push_back(T);
             }
         }
@@ -623,6 +704,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
         tiles = std::move(plain);
     }
 
+    tm.tiles_ms = ms_of(t0);
     fdt_header h{};
     std::memcpy(h.magic, "FNDT", 4);
     h.version = FDT_VERSION;
@@ -634,7 +716,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     h.tile_chunks = FDT_TILE_CHUNKS;
     h.n_diffs = static_cast<uint32_t>(n_diffs);
     h.n_rank_ops = static_cast<uint32_t>(rops.size());
-    h.source_graphs_crc = digests[0];
+    h.source_graphs_crc = verified_graphs_crc ? *verified_graphs_crc : digests[0];
     h.source_patch_crc = crc64(patch_bin);
     h.old_base = manifest.allocator.base;
     h.final_offset = manifest.final_offset;
@@ -670,8 +752,22 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     const uint64_t blob_bytes = (at + kSectionAlign - 1) / kSectionAlign * kSectionAlign;
 
     DevicePackResult out;
-    out.host.assign(blob_bytes, 0);
-    uint8_t* hb = out.host.data();
+    out.host_bytes.reset(new uint8_t[blob_bytes]);  // not zeroed: every byte is written below
+    out.host_size = blob_bytes;
+    out.host_complete = full_host_copy;
+    uint8_t* hb = out.host_bytes.get();
+    {  // zero padding between sections; device sections are filled by the D2H (or left out)
+        uint64_t at0 = sizeof h;
+        std::vector<int> by_offset(FDT_NSEC);
+        for (int i = 0; i < FDT_NSEC; ++i) by_offset[i] = i;
+        std::sort(by_offset.begin(), by_offset.end(),
+                  [&](int x, int y) { return h.sec[x].offset < h.sec[y].offset; });
+        for (int id : by_offset) {
+            std::memset(hb + at0, 0, h.sec[id].offset - at0);
+            at0 = h.sec[id].offset + h.sec[id].bytes;
+        }
+        std::memset(hb + at0, 0, blob_bytes - at0);
+    }
     std::memcpy(hb, &h, sizeof h);
     auto put = [&](int id, const void* src) {
         if (h.sec[id].bytes) std::memcpy(hb + h.sec[id].offset, src, h.sec[id].bytes);
@@ -714,7 +810,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
                    "GPU pack template meta");
     }
     for (int id : {FDT_SEC_TIMAGES, FDT_SEC_CMETA, FDT_SEC_DIDX, FDT_SEC_DDATA})
-        if (h.sec[id].bytes)
+        if (h.sec[id].bytes && full_host_copy)
             cuda_check(cudaMemcpyAsync(hb + h.sec[id].offset, db + h.sec[id].offset, h.sec[id].bytes,
                                        cudaMemcpyDeviceToHost, st),
                        "GPU pack D2H");
@@ -747,7 +843,8 @@ std::vector<uint8_t> pack_archive_store_device(Device& dev, const std::filesyste
     cuda_check(cudaMemcpyAsync(d.data(), graphs.data(), graphs.size(), cudaMemcpyHostToDevice, dev.stream()),
                "cudaMemcpyAsync(graphs.bin)");
     DevicePackResult r = pack_template_store_device(dev, graphs, d.data(), patch, man, slots, nullptr, timings);
-    return std::move(r.host);
+    const auto h = r.host();
+    return std::vector<uint8_t>(h.begin(), h.end());
 }
 
 }  // namespace foundry

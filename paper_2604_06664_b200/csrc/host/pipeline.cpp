@@ -68,7 +68,9 @@ struct ServingContext::Impl {
 
     std::unique_ptr<StagedArchive> staged;  // every listed file, in pinned host memory and HBM
 
-    std::vector<uint8_t> inline_store;  // reference archives without templates.fdt
+    // reference archives without templates.fdt: the GPU packer's host copy
+    // (header + host sections; the device-only sections stay in HBM)
+    std::unique_ptr<uint8_t[]> inline_store;
     std::span<const uint8_t> store_host;
     std::unique_ptr<StoreView> view;
     DeviceStore dstore;
@@ -951,14 +953,15 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
             packed = pack_template_store_device(
                 device, I.file_host("graphs.bin"), I.staged->device("graphs.bin"), I.file_host("patch.bin"),
                 I.manifest,
-                I.staged->has("comm_slots.bin") ? I.file_host("comm_slots.bin") : std::span<const uint8_t>{});
+                I.staged->has("comm_slots.bin") ? I.file_host("comm_slots.bin") : std::span<const uint8_t>{},
+                nullptr, nullptr, /*full_host_copy=*/false, &I.manifest.file_digests.at("graphs.bin"));
         } catch (const Error&) {
             rethrow_in_step("template construction");
         }
-        I.inline_store = std::move(packed.host);
-        I.store_host = I.inline_store;
+        I.inline_store = std::move(packed.host_bytes);
+        I.store_host = {I.inline_store.get(), packed.host_size};
         I.view = std::make_unique<StoreView>(I.store_host);
-        I.dstore = adopt_store(device, packed.blob.data(), I.inline_store.size(), I.view->header());
+        I.dstore = adopt_store(device, packed.blob.data(), packed.host_size, I.view->header());
         I.dstore.blob = std::move(packed.blob);
         I.t.pack_ms = ms_since(t_pack);
     }

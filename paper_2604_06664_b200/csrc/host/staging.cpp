@@ -670,7 +670,8 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
         rethrow_in_step("archive integrity");
     }
     const auto t1 = Clock::now();
-    std::vector<uint8_t> packed;  // reference-written archive: packed now, on the GPU
+    DevicePackResult gpu;              // reference-written archive: packed now, on the GPU
+    std::span<const uint8_t> packed;   // its host copy
     DeviceStore store;
     if (has_store) {
         const auto host = staged->host("templates.fdt");
@@ -678,17 +679,19 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
         staged->order_after("templates.fdt", dev.stream());
         store = adopt_store(dev, staged->device("templates.fdt"), host.size(), view.header());
     } else {
-        DevicePackResult gpu;
         try {
             staged->order_after("graphs.bin", dev.stream());
+            // keep: the caller gets the whole store on the host (fdy_load_members)
             gpu = pack_template_store_device(dev, staged->host("graphs.bin"), staged->device("graphs.bin"),
                                              staged->host("patch.bin"), manifest,
                                              staged->has("comm_slots.bin") ? staged->host("comm_slots.bin")
-                                                                           : std::span<const uint8_t>{});
+                                                                           : std::span<const uint8_t>{},
+                                             nullptr, nullptr, /*full_host_copy=*/keep != nullptr,
+                                             &manifest.file_digests.at("graphs.bin"));
         } catch (const Error&) {
             rethrow_in_step("template construction");
         }
-        packed = std::move(gpu.host);
+        packed = gpu.host();
         store = adopt_store(dev, gpu.blob.data(), packed.size(), StoreView(packed).header());
         store.blob = std::move(gpu.blob);
     }

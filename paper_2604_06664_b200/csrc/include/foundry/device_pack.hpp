@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <span>
 #include <vector>
 
@@ -15,11 +16,13 @@
 namespace foundry {
 
 struct DevicePackTimings {
-    double prep_ms = 0;   // patch table view, member / group tables
+    double prep_ms = 0;   // patch table view, member / group / entry tables
+    double patch_parse_ms = 0;  // of which: the patch table view
     double pass1_ms = 0;  // upload + walk/fields/edges/verify/compact + record CRCs
     double host1_ms = 0;  // checks, kernel table, layout, rank ops
     double pass2_ms = 0;  // images + diff counts
     double host2_ms = 0;  // tile table, host sections
+    double tiles_ms = 0;  // of which: the tile table and shared rank-op ranges
     double pass3_ms = 0;  // diff writes + template images + D2H of the device sections
     double total_ms = 0;
     uint32_t kernel_keys = 0;  // distinct kernel keys the GPU table found
@@ -27,10 +30,20 @@ struct DevicePackTimings {
 };
 
 struct DevicePackResult {
-    std::vector<uint8_t> host;  // the store, byte-identical to pack_template_store's
-    DeviceBuffer blob;          // the same bytes in HBM
+    // The store on the host, byte-identical to pack_template_store's when
+    // host_complete; otherwise the device-only sections (template images, chunk
+    // meta, diff streams: what only the kernels read) are not copied back and
+    // their host bytes are unspecified. Host-side readers (StoreView) only use
+    // the header and the host sections.
+    std::unique_ptr<uint8_t[]> host_bytes;
+    size_t host_size = 0;
+    bool host_complete = false;
+    DeviceBuffer blob;  // the whole store in HBM
+    std::span<const uint8_t> host() const { return {host_bytes.get(), host_size}; }
 };
 
+// verified_graphs_crc: graphs.bin's digest when the caller has already checked
+// it (LOAD's integrity pass); otherwise the GPU computes it for the header.
 // graphs_host / d_graphs: graphs.bin on the host and in HBM (the device copy
 // is read by the kernels; the host copy only for per-group and per-kernel
 // metadata and, on error paths, to re-derive the reference's exact message for
@@ -39,7 +52,9 @@ struct DevicePackResult {
 DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t> graphs_host,
                                             const unsigned char* d_graphs, std::span<const uint8_t> patch_bin,
                                             const Manifest& manifest, std::span<const uint8_t> slots_bin = {},
-                                            PackStats* stats = nullptr, DevicePackTimings* timings = nullptr);
+                                            PackStats* stats = nullptr, DevicePackTimings* timings = nullptr,
+                                            bool full_host_copy = true,
+                                            const uint64_t* verified_graphs_crc = nullptr);
 
 // The same for an archive directory: reads and uploads graphs.bin, packs it on
 // the GPU, returns the store bytes (the tests compare them with the offline

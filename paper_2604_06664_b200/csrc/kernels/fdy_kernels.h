@@ -79,6 +79,7 @@ struct FdyServeArgs {
 enum : uint32_t {
     FDY_PACK_DECODE = 1u,  // record fails to decode or validate: the host re-parses it for the message
     FDY_PACK_TOPO = 2u,    // topology differs from the group representative's
+    FDY_PACK_PATCH = 4u,   // a patch entry / comm slot fails apply_rank_patches' checks
 };
 
 struct FdyPackArgs {
@@ -116,9 +117,19 @@ struct FdyPackArgs {
     uint64_t* uoff;               //            absolute graphs.bin offset of that node
     uint32_t* ucount;
     const uint32_t* ukidx;        // pass 2: compacted index -> store kernel index
-    const uint32_t* swap_node;    // pass 2: global node -> real comm kernel (stub swap)
-    const uint32_t* swap_kidx;
-    uint32_t n_swaps;
+    // patch entries (apply_rank_patches), flattened in member order
+    const uint32_t* pe_node;      // global node of the stub (~0u: node id out of range)
+    const uint64_t* pe_stub_hash;
+    const uint32_t* pe_stub_name; // name ids into names / name_off / name_len
+    const uint32_t* pe_real_name;
+    const uint32_t* pe_need;      // argument bytes the entry's offsets and slots need
+    uint32_t* pe_slot;            // kernel-table slot of the real comm kernel
+    const uint32_t* entry_base;   // per member: first entry
+    const unsigned char* names;
+    const uint32_t* name_off;
+    const uint32_t* name_len;
+    uint64_t comm_real_hash;
+    uint32_t n_entries;
     uint32_t total_nodes;
     uint32_t* status;             // per member: FDY_PACK_* bits
     uint32_t* flags;              // [0]: fingerprint collision

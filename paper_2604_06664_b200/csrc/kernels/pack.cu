@@ -28,7 +28,10 @@
 //            first position (atomicMin) as the key's order.
 //   edges    one CTA per record: canonical order, bounds, equality with the
 //            representative's edges.
-//   verify   one thread per kernel node: its key bytes equal the first
+//   entries  one thread per patch entry: apply_rank_patches' checks (stub
+//            node, offsets inside its arguments), then the real comm kernel's
+//            key into the table at the entry's position.
+//   verify   one thread per kernel node / entry: its key bytes equal the first
 //            occurrence's (a fingerprint collision is reported, never merged).
 //   compact  warp-ballot / popc compaction of the occupied table slots.
 // Pass 2
@@ -71,17 +74,15 @@ __device__ __forceinline__ uint64_t mix64(uint64_t h) {
     return h;
 }
 
-// Kernel key of a kernel node at q: (binary hash, func attrs, name), the
-// offline packer's KernelTable key.
-__device__ uint64_t key_fingerprint(const unsigned char* q, uint64_t seed) {
-    const uint32_t nl = ld32(q + 62);
+// Kernel key (binary hash, func attrs, name): the offline packer's
+// KernelTable key, for a kernel node or a patch entry's real comm kernel.
+__device__ uint64_t key_fingerprint(uint64_t hash, const unsigned char* fa, const unsigned char* name, uint32_t nl,
+                                    uint64_t seed) {
     uint64_t h = mix64(seed ^ (uint64_t(nl) << 1));
-    h = mix64(h ^ ld64(q + 54));
-    const unsigned char* fa = q + 66 + nl;
+    h = mix64(h ^ hash);
     h = mix64(h ^ ld64(fa));
     h = mix64(h ^ ld64(fa + 8));
     h = mix64(h ^ ld64(fa + 16));
-    const unsigned char* name = q + 66;
     uint32_t i = 0;
     for (; i + 8 <= nl; i += 8) h = mix64(h ^ ld64(name + i));
     uint64_t tail = 0;
@@ -90,8 +91,61 @@ __device__ uint64_t key_fingerprint(const unsigned char* q, uint64_t seed) {
     return h ? h : 1;
 }
 
+struct KeyParts {
+    uint64_t hash;
+    const unsigned char* fa;
+    const unsigned char* name;
+    uint32_t nl;
+};
+
+__device__ __forceinline__ KeyParts node_key(const unsigned char* q) {
+    const uint32_t nl = ld32(q + 62);
+    return {ld64(q + 54), q + 66 + nl, q + 66, nl};
+}
+
 __device__ __forceinline__ const unsigned char* node_at(const FdyPackArgs& a, uint32_t m, uint32_t n) {
     return a.graphs + a.rec_off[m] + a.node_off[a.node_base[m] + n];
+}
+
+__device__ __forceinline__ const unsigned char* gnode_at(const FdyPackArgs& a, uint32_t gn) {
+    return a.graphs + a.rec_off[a.node_member[gn]] + a.node_off[gn];
+}
+
+// Patch entry e's real comm kernel key: (comm_real_hash, the stub node's func
+// attrs, real name).
+__device__ __forceinline__ KeyParts entry_key(const FdyPackArgs& a, uint32_t e) {
+    const unsigned char* q = gnode_at(a, a.pe_node[e]);
+    const uint32_t r = a.pe_real_name[e];
+    return {a.comm_real_hash, q + 66 + ld32(q + 62), a.names + a.name_off[r], a.name_len[r]};
+}
+
+// The key at a table position: a node (local < its member's node count) or
+// the member's patch entry local - nodes.
+__device__ __forceinline__ KeyParts key_at(const FdyPackArgs& a, unsigned long long pos) {
+    const uint32_t m = uint32_t(pos >> 32), local = uint32_t(pos);
+    if (local < a.n_nodes[m]) return node_key(node_at(a, m, local));
+    return entry_key(a, a.entry_base[m] + (local - a.n_nodes[m]));
+}
+
+__device__ __forceinline__ bool same_key(const KeyParts& x, const KeyParts& y) {
+    if (x.hash != y.hash || x.nl != y.nl) return false;
+    for (uint32_t i = 0; i < 24; ++i)
+        if (x.fa[i] != y.fa[i]) return false;
+    for (uint32_t i = 0; i < x.nl; ++i)
+        if (x.name[i] != y.name[i]) return false;
+    return true;
+}
+
+__device__ __forceinline__ uint32_t table_insert(const FdyPackArgs& a, uint64_t fp, unsigned long long pos) {
+    uint32_t s = uint32_t(fp >> 20) & a.tmask;
+    for (;;) {
+        const unsigned long long old = atomicCAS(&a.tkey[s], 0ull, fp);
+        if (old == 0ull || old == fp) {
+            atomicMin(&a.tpos[s], pos);
+            return s;
+        }
+        s = (s + 1) & a.tmask;
+    }
 }
 
 // ------------------------------------------------------------------- pass 1
@@ -207,18 +261,9 @@ __global__ void __launch_bounds__(kThreads) pack_fields_kernel(const FdyPackArgs
             bool valid = blob_len != 0;  // CapturedGraph::validate
             for (int i = 0; i < 6; ++i) valid &= ld32(q + 26 + 4 * i) != 0;
             if (!valid) atomicOr(&a.status[m], FDY_PACK_DECODE);
-            const uint64_t fp = key_fingerprint(q, a.seed);
-            const unsigned long long pos = (uint64_t(m) << 32) | n;
-            uint32_t s = uint32_t(fp >> 20) & a.tmask;
-            for (;;) {
-                const unsigned long long old = atomicCAS(&a.tkey[s], 0ull, fp);
-                if (old == 0ull || old == fp) {
-                    atomicMin(&a.tpos[s], pos);
-                    a.node_slot[gn] = s;
-                    break;
-                }
-                s = (s + 1) & a.tmask;
-            }
+            const KeyParts k = node_key(q);
+            a.node_slot[gn] = table_insert(a, key_fingerprint(k.hash, k.fa, k.name, k.nl, a.seed),
+                                           (uint64_t(m) << 32) | n);
         }
         if (!rep_ok) continue;
         const uint32_t gi = a.gnode_base[g] + n;
@@ -266,19 +311,59 @@ __global__ void __launch_bounds__(kThreads) pack_edges_kernel(const FdyPackArgs 
     if (!same_shape && m != rep && threadIdx.x == 0) atomicOr(&a.status[m], FDY_PACK_TOPO);
 }
 
-__global__ void __launch_bounds__(kThreads) pack_verify_kernel(const FdyPackArgs a) {
-    for (uint32_t gn = blockIdx.x * kThreads + threadIdx.x; gn < a.total_nodes; gn += gridDim.x * kThreads) {
+// apply_rank_patches' checks (rank_forge.cpp:136-150) per patch entry: the
+// node is a kernel node carrying the recorded stub, and its argument buffer
+// holds every rank / world offset and comm slot; then the real comm kernel's
+// key goes into the table at the entry's position (after its graph's nodes).
+__global__ void __launch_bounds__(kThreads) pack_entries_kernel(const FdyPackArgs a) {
+    for (uint32_t e = blockIdx.x * kThreads + threadIdx.x; e < a.n_entries; e += gridDim.x * kThreads) {
+        const uint32_t gn = a.pe_node[e];
+        if (gn == kNone) continue;  // the host saw the node id out of range
         const uint32_t m = a.node_member[gn];
         if (!member_ok(a, m)) continue;
-        const unsigned char* q = a.graphs + a.rec_off[m] + a.node_off[gn];
-        if (q[0] != 0) continue;
-        const unsigned long long pos = a.tpos[a.node_slot[gn]];
-        const unsigned char* r = node_at(a, uint32_t(pos >> 32), uint32_t(pos));
-        if (r == q) continue;
-        const uint32_t nl = ld32(q + 62);
-        bool same = r[0] == 0 && ld32(r + 62) == nl && ld64(r + 54) == ld64(q + 54);
-        for (uint32_t i = 0; same && i < nl + 24; ++i) same = q[66 + i] == r[66 + i];  // name, func attrs
-        if (!same) atomicOr(&a.flags[0], 1u);
+        const unsigned char* q = gnode_at(a, gn);
+        bool ok = q[0] == 0;
+        if (ok) {
+            const KeyParts k = node_key(q);
+            const uint32_t sn = a.pe_stub_name[e];
+            ok = k.hash == a.pe_stub_hash[e] && k.nl == a.name_len[sn] && ld32(q + 90 + k.nl) >= a.pe_need[e];
+            for (uint32_t i = 0; ok && i < k.nl; ++i) ok = k.name[i] == a.names[a.name_off[sn] + i];
+        }
+        if (!ok) {
+            atomicOr(&a.status[m], FDY_PACK_PATCH);
+            continue;
+        }
+        const KeyParts k = entry_key(a, e);
+        const uint32_t local = a.n_nodes[m] + (e - a.entry_base[m]);
+        a.pe_slot[e] = table_insert(a, key_fingerprint(k.hash, k.fa, k.name, k.nl, a.seed),
+                                    (uint64_t(m) << 32) | local);
+    }
+}
+
+// Every key equals its slot's first occurrence byte for byte (a fingerprint
+// collision is reported, never merged). Threads [0, total_nodes) take nodes,
+// the rest patch entries.
+__global__ void __launch_bounds__(kThreads) pack_verify_kernel(const FdyPackArgs a) {
+    const uint32_t n_items = a.total_nodes + a.n_entries;
+    for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < n_items; i += gridDim.x * kThreads) {
+        KeyParts k;
+        uint32_t slot;
+        if (i < a.total_nodes) {
+            const uint32_t m = a.node_member[i];
+            if (!member_ok(a, m)) continue;
+            const unsigned char* q = a.graphs + a.rec_off[m] + a.node_off[i];
+            if (q[0] != 0) continue;
+            k = node_key(q);
+            slot = a.node_slot[i];
+        } else {
+            const uint32_t e = i - a.total_nodes;
+            const uint32_t gn = a.pe_node[e];
+            if (gn == kNone || !member_ok(a, a.node_member[gn]) || (a.status[a.node_member[gn]] & FDY_PACK_PATCH))
+                continue;
+            k = entry_key(a, e);
+            slot = a.pe_slot[e];
+        }
+        if (!same_key(k, key_at(a, a.tpos[slot]))) atomicOr(&a.flags[0], 1u);
     }
 }
 
@@ -296,8 +381,11 @@ __global__ void __launch_bounds__(kThreads) pack_compact_kernel(const FdyPackArg
             const uint32_t u = first + __popc(ballot & ((1u << lane) - 1u));
             const unsigned long long pos = a.tpos[s];
             const uint32_t m = uint32_t(pos >> 32), n = uint32_t(pos);
+            // the node, or for a real comm kernel the stub node it replaces
+            const uint32_t gn = n < a.n_nodes[m] ? a.node_base[m] + n
+                                                 : a.pe_node[a.entry_base[m] + (n - a.n_nodes[m])];
             a.upos[u] = pos;
-            a.uoff[u] = a.rec_off[m] + a.node_off[a.node_base[m] + n];
+            a.uoff[u] = a.rec_off[m] + a.node_off[gn];
             a.tuniq[s] = u;
         }
     }
@@ -380,13 +468,16 @@ __global__ void __launch_bounds__(kThreads) pack_images_kernel(const FdyPackArgs
     }
 }
 
+// apply_rank_patches' kernel swap: each entry's stub node gets the real comm
+// kernel's store index.
 __global__ void __launch_bounds__(kThreads) pack_swaps_kernel(const FdyPackArgs a) {
-    const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
-    if (i >= a.n_swaps) return;
-    const uint32_t gn = a.swap_node[i];
+    const uint32_t e = blockIdx.x * kThreads + threadIdx.x;
+    if (e >= a.n_entries) return;
+    const uint32_t gn = a.pe_node[e];
     const uint32_t m = a.node_member[gn];
     const uint32_t n = gn - a.node_base[m];
-    *reinterpret_cast<uint32_t*>(a.arena + a.out_off[m] + 48ull * n + offsetof(fdt_node, kernel)) = a.swap_kidx[i];
+    *reinterpret_cast<uint32_t*>(a.arena + a.out_off[m] + 48ull * n + offsetof(fdt_node, kernel)) =
+        a.ukidx[a.tuniq[a.pe_slot[e]]];
 }
 
 struct TileRef {
@@ -502,8 +593,9 @@ extern "C" cudaError_t fdy_launch_pack_pass1(const FdyPackArgs* args, cudaStream
         pack_fields_kernel<<<grid_for(a.total_nodes, kThreads), kThreads, 0, stream>>>(a);
     }
     pack_edges_kernel<<<a.n_members, kThreads, 0, stream>>>(a);
-    if (a.total_nodes) {
-        pack_verify_kernel<<<grid_for(a.total_nodes, kThreads), kThreads, 0, stream>>>(a);
+    if (a.n_entries) pack_entries_kernel<<<grid_for(a.n_entries, kThreads), kThreads, 0, stream>>>(a);
+    if (a.total_nodes + a.n_entries) {
+        pack_verify_kernel<<<grid_for(a.total_nodes + a.n_entries, kThreads), kThreads, 0, stream>>>(a);
     }
     pack_compact_kernel<<<grid_for(a.tmask + 1, kThreads), kThreads, 0, stream>>>(a);
     return cudaGetLastError();
@@ -512,7 +604,7 @@ extern "C" cudaError_t fdy_launch_pack_pass1(const FdyPackArgs* args, cudaStream
 extern "C" cudaError_t fdy_launch_pack_pass2(const FdyPackArgs* args, cudaStream_t stream) {
     const FdyPackArgs& a = *args;
     if (a.total_nodes) pack_images_kernel<<<grid_for(a.total_nodes, kThreads / 32), kThreads, 0, stream>>>(a);
-    if (a.n_swaps) pack_swaps_kernel<<<(a.n_swaps + kThreads - 1) / kThreads, kThreads, 0, stream>>>(a);
+    if (a.n_entries) pack_swaps_kernel<<<(a.n_entries + kThreads - 1) / kThreads, kThreads, 0, stream>>>(a);
     if (a.n_tiles) pack_count_kernel<<<a.n_tiles, kThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
