@@ -57,7 +57,7 @@ def parse_args():
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--load-steps", type=int, default=3)
     p.add_argument("--skip-load", action="store_true", help="skip the full-LOAD section (profiling)")
-    p.add_argument("--fanout", choices=["host", "ipc"], default="ipc",
+    p.add_argument("--fanout", choices=["host", "ipc", "chain"], default="ipc",
                    help="N>1: how the store reaches every GPU (ipc = GPU0 -> peers over NVLink)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--skip-tier-s", action="store_true", help="skip the model-shaped arena measurement")

@@ -103,6 +103,27 @@ int fdy_store_fanout(const fdy_store* src, fdy_device* dst_dev, fdy_store** out)
 int fdy_store_export(const fdy_store* store, unsigned char handle[64], uint64_t* bytes);
 int fdy_store_import(fdy_device* dev, const unsigned char handle[64], uint64_t bytes,
                      fdy_store** out);
+/* Pipelined chain fan-out (SURVEY §8(e) option ii), one process: dsts[0]
+ * pulls the store from src chunk by chunk, dsts[i] from dsts[i-1] as each
+ * chunk lands on it (per-chunk events, peer copies over NVLink), so the store
+ * crosses each link once instead of src's egress carrying n copies.
+ * chunk_bytes 0 = 2 MiB. outs[i] receives dsts[i]'s store. */
+int fdy_store_fanout_chain(const fdy_store* src, fdy_device* const* dsts, uint32_t n, uint64_t chunk_bytes,
+                           fdy_store** outs);
+/* The same across processes (one per GPU): every link creates its buffer and
+ * exports its handle (fdy_chain_create), the handles are exchanged (any
+ * plumbing), then the head seeds from host memory and every other link pulls
+ * from its predecessor; chunk k moves as soon as the predecessor published it
+ * (a progress word in the predecessor's HBM, polled by the GPU: no host round
+ * trip per chunk). fdy_chain_finish waits and returns the store; keep it alive
+ * until the next link has finished (a barrier). */
+typedef struct fdy_chain fdy_chain;
+int fdy_chain_create(fdy_device* dev, uint64_t bytes, uint64_t chunk_bytes, fdy_chain** out,
+                     unsigned char handle[64]);
+int fdy_chain_seed(fdy_chain* chain, const void* host_blob);
+int fdy_chain_pull(fdy_chain* chain, const unsigned char upstream[64]);
+int fdy_chain_finish(fdy_chain* chain, fdy_store** out);
+void fdy_chain_free(fdy_chain* chain);
 void fdy_store_free(fdy_store* store);
 size_t fdy_store_members_bytes(const fdy_store* store);
 

@@ -54,7 +54,7 @@ HOST_SRCS = [
     "capi/capi_kernels.cpp",
     "capi/capi_session.cpp",
 ]
-CU_SRCS = ["kernels/materialize.cu", "kernels/crc64.cu", "kernels/pack.cu"]
+CU_SRCS = ["kernels/materialize.cu", "kernels/crc64.cu", "kernels/pack.cu", "kernels/fanout.cu"]
 RDC_SRCS = ["kernels/serve.cu"]  # device runtime (graph device updates): -rdc + device link
 
 

@@ -93,6 +93,13 @@ class CApi:
         L.fdy_store_free.argtypes = [P]
         L.fdy_store_export.argtypes = [P, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64)]
         L.fdy_store_import.argtypes = [P, ctypes.c_char_p, ctypes.c_uint64, ctypes.POINTER(P)]
+        L.fdy_store_fanout_chain.argtypes = [P, ctypes.POINTER(P), ctypes.c_uint32, ctypes.c_uint64,
+                                             ctypes.POINTER(P)]
+        L.fdy_chain_create.argtypes = [P, ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(P), ctypes.c_char_p]
+        L.fdy_chain_seed.argtypes = [P, ctypes.c_void_p]
+        L.fdy_chain_pull.argtypes = [P, ctypes.c_char_p]
+        L.fdy_chain_finish.argtypes = [P, ctypes.POINTER(P)]
+        L.fdy_chain_free.argtypes = [P]
         L.fdy_store_members_bytes.argtypes = [P]
         L.fdy_store_members_bytes.restype = ctypes.c_size_t
         L.fdy_materialize.argtypes = [P, P, ctypes.POINTER(MaterializeDesc), ctypes.POINTER(P),
@@ -174,6 +181,32 @@ class CApi:
         handle, nbytes = exported
         h = ctypes.c_void_p()
         self.check(self.lib.fdy_store_import(dev, handle, nbytes, ctypes.byref(h)))
+        return h
+
+    def store_fanout_chain(self, src, devs, chunk_bytes: int = 0) -> list:
+        """In-process pipelined chain: devs[0] pulls from src, devs[i] from devs[i-1]."""
+        n = len(devs)
+        arr = (ctypes.c_void_p * n)(*[d.value if isinstance(d, ctypes.c_void_p) else d for d in devs])
+        outs = (ctypes.c_void_p * n)()
+        self.check(self.lib.fdy_store_fanout_chain(src, arr, n, chunk_bytes, outs))
+        return [ctypes.c_void_p(o) for o in outs]
+
+    def chain_create(self, dev, nbytes: int, chunk_bytes: int = 0):
+        h = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        self.check(self.lib.fdy_chain_create(dev, nbytes, chunk_bytes, ctypes.byref(h), handle))
+        return h, handle.raw
+
+    def chain_seed(self, chain, blob: bytes) -> None:
+        self.check(self.lib.fdy_chain_seed(chain, blob))
+
+    def chain_pull(self, chain, upstream: bytes) -> None:
+        self.check(self.lib.fdy_chain_pull(chain, upstream))
+
+    def chain_finish(self, chain):
+        h = ctypes.c_void_p()
+        self.check(self.lib.fdy_chain_finish(chain, ctypes.byref(h)))
+        self.lib.fdy_chain_free(chain)
         return h
 
     @staticmethod

@@ -1,4 +1,5 @@
 // C-ABI, kernel layer (declarations and reference anchors: include/foundry_b200.h).
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -8,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include "capi_common.hpp"
+#include "../kernels/fdy_kernels.h"
 #include "foundry/device.hpp"
 #include "foundry/graph_model.hpp"
 #include "foundry/hash.hpp"
@@ -118,6 +120,188 @@ int fdy_store_fanout(const fdy_store* src, fdy_device* dst_dev, fdy_store** out)
         *out = o.release();
     });
 }
+
+namespace {
+
+constexpr uint64_t kChainChunk = 2ull << 20;
+
+void enable_peer(Device& d, Device& s) {
+    if (d.ordinal() == s.ordinal()) return;
+    int can = 0;
+    cuda_check(cudaDeviceCanAccessPeer(&can, d.ordinal(), s.ordinal()), "cudaDeviceCanAccessPeer");
+    if (!can) return;
+    d.make_current();
+    const cudaError_t e = cudaDeviceEnablePeerAccess(s.ordinal(), 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else cuda_check(e, "cudaDeviceEnablePeerAccess");
+}
+
+}  // namespace
+
+int fdy_store_fanout_chain(const fdy_store* src, fdy_device* const* dsts, uint32_t n, uint64_t chunk_bytes,
+                           fdy_store** outs) {
+    return fdy_guard([&] {
+        require(src && (dsts || n == 0) && (outs || n == 0), Errc::invalid_argument,
+                "fdy_store_fanout_chain: null argument");
+        for (uint32_t i = 0; i < n; ++i)
+            require(dsts[i] != nullptr, Errc::invalid_argument, "fdy_store_fanout_chain: null device");
+        const uint64_t bytes = src->store.bytes;
+        const uint64_t chunk = chunk_bytes ? chunk_bytes : kChainChunk;
+        const uint64_t nchunks = (bytes + chunk - 1) / chunk;
+        src->owner->dev->sync();  // the head's bytes have landed
+        std::vector<DeviceBuffer> bufs;
+        bufs.reserve(n);
+        for (uint32_t i = 0; i < n; ++i) {
+            Device& d = *dsts[i]->dev;
+            Device& up = i == 0 ? *src->owner->dev : *dsts[i - 1]->dev;
+            enable_peer(d, up);
+            d.make_current();
+            bufs.emplace_back(d, bytes, /*shareable=*/true);
+        }
+        // events[i * nchunks + k]: chunk k has landed on dsts[i]
+        std::vector<cudaEvent_t> events(size_t(n) * nchunks, nullptr);
+        auto cleanup = [&] {
+            for (cudaEvent_t e : events)
+                if (e) cudaEventDestroy(e);
+        };
+        try {
+            for (uint32_t i = 0; i < n; ++i) {
+                dsts[i]->dev->make_current();
+                for (uint64_t k = 0; k < nchunks; ++k)
+                    cuda_check(cudaEventCreateWithFlags(&events[i * nchunks + k], cudaEventDisableTiming),
+                               "cudaEventCreate");
+            }
+            for (uint64_t k = 0; k < nchunks; ++k) {
+                const uint64_t off = k * chunk, len = std::min(chunk, bytes - off);
+                for (uint32_t i = 0; i < n; ++i) {
+                    Device& d = *dsts[i]->dev;
+                    d.make_current();
+                    const unsigned char* from = i == 0 ? src->store.data : bufs[i - 1].data();
+                    const int from_dev = i == 0 ? src->owner->dev->ordinal() : dsts[i - 1]->dev->ordinal();
+                    if (i > 0)
+                        cuda_check(cudaStreamWaitEvent(d.stream(), events[(i - 1) * nchunks + k], 0),
+                                   "cudaStreamWaitEvent");
+                    cuda_check(cudaMemcpyPeerAsync(bufs[i].data() + off, d.ordinal(), from + off, from_dev, len,
+                                                   d.stream()),
+                               "cudaMemcpyPeerAsync(chain fan-out)");
+                    cuda_check(cudaEventRecord(events[i * nchunks + k], d.stream()), "cudaEventRecord");
+                }
+            }
+            for (uint32_t i = 0; i < n; ++i) dsts[i]->dev->sync();
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+        for (uint32_t i = 0; i < n; ++i) {
+            auto o = std::make_unique<fdy_store>();
+            o->owner = dsts[i];
+            o->store = adopt_store(*dsts[i]->dev, bufs[i].data(), bytes, src->store.header);
+            o->store.blob = std::move(bufs[i]);
+            outs[i] = o.release();
+        }
+    });
+}
+
+// Cross-process chain link: the store bytes, then a progress word (chunks
+// landed), in one shareable allocation whose IPC handle the next link opens.
+struct fdy_chain {
+    fdy_device* dev = nullptr;
+    DeviceBuffer buf;
+    uint64_t bytes = 0, chunk = 0, progress_off = 0;
+    uint32_t nchunks = 0;
+    void* upstream = nullptr;  // opened IPC mapping of the previous link
+    bool fed = false;
+    uint32_t* progress() { return reinterpret_cast<uint32_t*>(buf.data() + progress_off); }
+    ~fdy_chain() {
+        if (upstream) {
+            dev->dev->make_current();
+            cudaIpcCloseMemHandle(upstream);
+        }
+    }
+};
+
+int fdy_chain_create(fdy_device* dev, uint64_t bytes, uint64_t chunk_bytes, fdy_chain** out,
+                     unsigned char handle[64]) {
+    return fdy_guard([&] {
+        require(dev && out && handle && bytes >= sizeof(fdt_header), Errc::invalid_argument,
+                "fdy_chain_create: null argument or store smaller than its header");
+        auto c = std::make_unique<fdy_chain>();
+        c->dev = dev;
+        c->bytes = bytes;
+        c->chunk = chunk_bytes ? chunk_bytes : kChainChunk;
+        c->nchunks = static_cast<uint32_t>((bytes + c->chunk - 1) / c->chunk);
+        c->progress_off = (bytes + 255) / 256 * 256;
+        Device& d = *dev->dev;
+        d.make_current();
+        c->buf = DeviceBuffer(d, c->progress_off + 256, /*shareable=*/true);
+        // zeroed before the handle leaves this process: a link never sees a stale count
+        cuda_check(cudaMemset(c->progress(), 0, 256), "cudaMemset(chain progress)");
+        cudaIpcMemHandle_t h;
+        cuda_check(cudaIpcGetMemHandle(&h, c->buf.data()), "cudaIpcGetMemHandle");
+        std::memcpy(handle, &h, sizeof h);
+        *out = c.release();
+    });
+}
+
+int fdy_chain_seed(fdy_chain* c, const void* host_blob) {
+    return fdy_guard([&] {
+        require(c && host_blob && !c->fed, Errc::invalid_argument, "fdy_chain_seed: null argument or fed twice");
+        Device& d = *c->dev->dev;
+        d.make_current();
+        const auto* src = static_cast<const unsigned char*>(host_blob);
+        for (uint32_t k = 0; k < c->nchunks; ++k) {
+            const uint64_t off = uint64_t(k) * c->chunk, len = std::min(c->chunk, c->bytes - off);
+            cuda_check(cudaMemcpyAsync(c->buf.data() + off, src + off, len, cudaMemcpyHostToDevice, d.stream()),
+                       "cudaMemcpyAsync(chain seed)");
+            cuda_check(fdy_launch_chain_publish(c->progress(), k + 1, d.stream()), "chain publish");
+        }
+        c->fed = true;
+    });
+}
+
+int fdy_chain_pull(fdy_chain* c, const unsigned char upstream[64]) {
+    return fdy_guard([&] {
+        require(c && upstream && !c->fed, Errc::invalid_argument, "fdy_chain_pull: null argument or fed twice");
+        Device& d = *c->dev->dev;
+        d.make_current();
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, upstream, sizeof h);
+        cuda_check(cudaIpcOpenMemHandle(&c->upstream, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        const auto* up = static_cast<const unsigned char*>(c->upstream);
+        const auto* up_progress = reinterpret_cast<const uint32_t*>(up + c->progress_off);
+        for (uint32_t k = 0; k < c->nchunks; ++k) {
+            const uint64_t off = uint64_t(k) * c->chunk, len = std::min(c->chunk, c->bytes - off);
+            cuda_check(fdy_launch_chain_wait(up_progress, k + 1, d.stream()), "chain wait");
+            cuda_check(cudaMemcpyAsync(c->buf.data() + off, up + off, len, cudaMemcpyDeviceToDevice, d.stream()),
+                       "cudaMemcpyAsync(chain link)");
+            cuda_check(fdy_launch_chain_publish(c->progress(), k + 1, d.stream()), "chain publish");
+        }
+        c->fed = true;
+    });
+}
+
+int fdy_chain_finish(fdy_chain* c, fdy_store** out) {
+    return fdy_guard([&] {
+        require(c && out && c->fed, Errc::invalid_argument, "fdy_chain_finish: null argument or nothing fed");
+        Device& d = *c->dev->dev;
+        d.make_current();
+        cuda_check(cudaStreamSynchronize(d.stream()), "chain fan-out");
+        if (c->upstream) {
+            cuda_check(cudaIpcCloseMemHandle(c->upstream), "cudaIpcCloseMemHandle");
+            c->upstream = nullptr;
+        }
+        fdt_header hdr;
+        cuda_check(cudaMemcpy(&hdr, c->buf.data(), sizeof hdr, cudaMemcpyDeviceToHost), "store header D2H");
+        auto o = std::make_unique<fdy_store>();
+        o->owner = c->dev;
+        o->store = adopt_store(d, c->buf.data(), c->bytes, hdr);
+        o->store.blob = std::move(c->buf);  // the next link may still be reading it: free after a barrier
+        *out = o.release();
+    });
+}
+
+void fdy_chain_free(fdy_chain* c) { delete c; }
 
 int fdy_store_export(const fdy_store* store, unsigned char handle[64], uint64_t* bytes) {
     return fdy_guard([&] {

@@ -8,6 +8,12 @@ one-time broadcast of the read-only template store:
 * `ipc`  — rank 0 DMAs the store from host into HBM and exports it (CUDA IPC);
            every other rank pulls it GPU->GPU over NVLink (fdy_store_import).
 * `host` — every rank DMAs the store from (shared, page-cached) host memory.
+* `chain` — pipelined chain over the ranks of a node (SURVEY §8e ii): local
+           rank 0 seeds its copy from host memory chunk by chunk, rank r pulls
+           each chunk from rank r-1 as soon as it landed there (fdy_chain_*:
+           a progress word in HBM polled by the GPU), so the store crosses
+           every NVLink hop once, pipelined, instead of rank 0's egress
+           carrying N-1 copies.
 
 torch.distributed is plumbing only: barriers, the handle broadcast and the
 max-over-ranks timing reduction. No collective touches the data path.
@@ -100,9 +106,13 @@ def distribute_store(group: RankGroup, api, dev, blob: bytes | None, mode: str =
     mode "host": each rank uploads `blob` itself (blob must be given on every rank).
     mode "ipc":  local rank 0 of every node uploads and exports; the other ranks of
                  that node import it over NVLink (CUDA IPC handles are node-local).
+    mode "chain": local rank 0 of every node seeds a pipelined chain through the
+                 node's ranks in global-rank order (blob needed on local rank 0).
     """
     if mode == "host" or group.world == 1:
         return api.store_upload(dev, blob)
+    if mode == "chain":
+        return _chain(group, api, dev, blob)
     leader = node_leader(group)
     if group.rank == leader:
         store = api.store_upload(dev, blob)
@@ -118,3 +128,23 @@ def distribute_store(group: RankGroup, api, dev, blob: bytes | None, mode: str =
             store = api.store_import(dev, mine[0][1])
     group.barrier()  # every peer has finished pulling before a leader may free
     return store
+
+
+def _chain(group: RankGroup, api, dev, blob: bytes | None):
+    """mode "chain": the node's ranks in global-rank order form the chain; the
+    node leader is its head. Every rank needs the store's size (blob or the
+    leader's broadcast)."""
+    leader = node_leader(group)
+    size = group.all_gather_object(len(blob) if group.rank == leader else None)[leader]
+    chain, handle = api.chain_create(dev, size)
+    links = group.all_gather_object((leader, group.rank, handle))
+    if group.rank == leader:
+        api.chain_seed(chain, blob)
+    else:
+        upstream = [h for (l, r, h) in links if l == leader and r == group.rank - 1]
+        assert upstream, "chain fan-out: no predecessor on this node"
+        api.chain_pull(chain, upstream[0])
+    store = api.chain_finish(chain)
+    group.barrier()  # every link has finished reading its predecessor
+    return store
+

@@ -1,7 +1,7 @@
-"""Worker of test_gpu_capi.py::test_ipc_fanout_between_two_processes (one
-process per rank, both on cuda:0; gloo carries the exported handle).
+"""Worker of the multi-process fan-out tests in test_gpu_capi.py (one process
+per rank, all on cuda:0; gloo carries the exported handles).
 
-    RANK=r WORLD_SIZE=2 MASTER_ADDR=127.0.0.1 MASTER_PORT=p python ipc_worker.py <archive> <outdir>
+    RANK=r WORLD_SIZE=n MASTER_ADDR=127.0.0.1 MASTER_PORT=p python ipc_worker.py <archive> <outdir> [ipc|chain]
 """
 from __future__ import annotations
 
@@ -15,6 +15,7 @@ sys.path.insert(0, ROOT)
 
 def main() -> None:
     arch, outdir = sys.argv[1], sys.argv[2]
+    mode = sys.argv[3] if len(sys.argv) > 3 else "ipc"
     import paper_2604_06664_b200 as foundry
     from paper_2604_06664_b200 import capi
     from paper_2604_06664_b200.multirank import RankGroup, distribute_store
@@ -24,7 +25,7 @@ def main() -> None:
     api = capi.CApi()
     dev = api.device_open(0)
     blob = open(os.path.join(arch, "templates.fdt"), "rb").read() if g.rank == 0 else None
-    store = distribute_store(g, api, dev, blob, "ipc")
+    store = distribute_store(g, api, dev, blob, mode)
     base = json.load(open(os.path.join(arch, "manifest")))["allocator"]["base"]
     tp = 2 + g.rank
     members, _ = api.materialize(dev, store, tp, 8, base + 0x10000 * (g.rank + 1))

@@ -224,6 +224,56 @@ def test_ipc_fanout_between_two_processes(foundry, oracle, archives, tmp_path):
         assert got == want, rank
 
 
+def test_chain_fanout_between_three_processes(foundry, oracle, archives, tmp_path):
+    """SURVEY §8(e) option ii across processes: rank 0 seeds a pipelined chain
+    from host memory, rank 1 pulls every chunk from rank 0 and rank 2 from
+    rank 1 as each lands (GPU-polled progress words over CUDA IPC); each rank
+    materializes its own TP rank from its copy and must equal the oracle."""
+    arch, _ = archives("moe-spmd")
+    port = _free_port()
+    procs = []
+    for rank in range(3):
+        env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                   WORLD_SIZE="3", LOCAL_RANK=str(rank))
+        procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "ipc_worker.py"), arch,
+                                       str(tmp_path), "chain"], env=env))
+    for p in procs:
+        assert p.wait(timeout=600) == 0
+    for rank in range(3):
+        got = (tmp_path / ("rank%d.fndg" % rank)).read_bytes()
+        want, _ = oracle.materialize_archive(arch, 2 + rank, 8, 0x10000 * (rank + 1))
+        assert got == want, rank
+
+
+@pytest.mark.parametrize("chunk", [0, 4096 + 16])
+def test_chain_fanout_in_one_process(foundry, oracle, archives, api, dev, chunk):
+    """fdy_store_fanout_chain through three device handles (one GPU here, so
+    each hop is a device-to-device copy on its own stream, ordered by the
+    per-chunk events exactly as across GPUs); every link's store materializes
+    like the oracle. chunk = 4112 bytes: many chunks, ragged last one."""
+    arch, _ = archives("moe-spmd")
+    blob = open(os.path.join(arch, "templates.fdt"), "rb").read()
+    devs = [api.device_open(0) for _ in range(3)]
+    src = api.store_upload(dev, blob)
+    outs = api.store_fanout_chain(src, devs, chunk)
+    base = manifest(arch)["allocator"]["base"]
+    try:
+        for i, (d, st) in enumerate(zip(devs, outs)):
+            members, _ = api.materialize(d, st, i + 1, 4, base)
+            try:
+                got = decode(foundry, arch, api.members_download(members))
+            finally:
+                api.lib.fdy_members_free(members)
+            want, _ = oracle.materialize_archive(arch, i + 1, 4, 0)
+            assert got == want, i
+    finally:
+        for st in outs:
+            api.lib.fdy_store_free(st)
+        api.lib.fdy_store_free(src)
+        for d in devs:
+            api.lib.fdy_device_close(d)
+
+
 def test_session_layer_load_replay_and_capture(foundry, oracle, archives, api):
     """The reference's LOAD surface through the C-ABI (fdy_load ->
     fdy_serving_replay / fdy_serving_capture_graph): traces equal the oracle's,

@@ -139,3 +139,71 @@ def test_ipc_fanout_has_one_exporter_per_node():
     assert got[2] == [("upload", 64), ("export",)], got
     assert got[1] == [("import", "handle-of-0")], got
     assert got[3] == [("import", "handle-of-2")], got
+
+
+class _FileChainApi:
+    """Stand-in for the chain C-ABI (fdy_chain_*) with files as links: a
+    link's 'HBM' is a file named after its handle; pull waits for the
+    predecessor's file. Exercises the orchestration only (who seeds, who pulls
+    from whom, across two nodes)."""
+
+    def __init__(self, workdir: str, rank: int):
+        self.dir, self.rank = workdir, rank
+
+    def chain_create(self, dev, nbytes, chunk_bytes=0):
+        return {"size": nbytes, "path": os.path.join(self.dir, "link%d" % self.rank)}, b"link%d" % self.rank
+
+    def chain_seed(self, chain, blob):
+        assert len(blob) == chain["size"]
+        open(chain["path"], "wb").write(blob)
+
+    def chain_pull(self, chain, upstream):
+        import time
+        src = os.path.join(self.dir, upstream.decode())
+        for _ in range(6000):
+            if os.path.exists(src) and os.path.getsize(src) == chain["size"]:
+                break
+            time.sleep(0.01)
+        data = open(src, "rb").read()
+        chain["pulled_from"] = upstream.decode()
+        open(chain["path"], "wb").write(data)
+
+    def chain_finish(self, chain):
+        return (open(chain["path"], "rb").read(), chain.get("pulled_from"))
+
+
+def _chain_worker(rank: int, world: int, local: int, port: int, workdir: str, queue) -> None:
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(local))
+    sys.path.insert(0, ROOT)
+    try:
+        from paper_2604_06664_b200.multirank import RankGroup, distribute_store
+
+        g = RankGroup.from_env()
+        g.init("gloo")
+        blob = bytes(range(256)) * 1000 if local == 0 else None
+        data, pulled_from = distribute_store(g, _FileChainApi(workdir, rank), None, blob, "chain")
+        queue.put((rank, data == bytes(range(256)) * 1000, pulled_from))
+        g.close()
+    except Exception as exc:
+        queue.put((rank, repr(exc), None))
+
+
+def test_chain_fanout_orchestration_over_gloo(tmp_path, native_build):
+    """Four processes on two 'nodes' (local ranks 0,1,2 and 0): each node's
+    leader seeds its own chain, every other rank pulls from the rank before it
+    on its node, and every rank ends with the store's bytes."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    locals_ = [0, 1, 2, 0]
+    procs = [ctx.Process(target=_chain_worker, args=(r, 4, locals_[r], port, str(tmp_path), q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert [r[1] for r in results] == [True] * 4, results
+    assert [r[2] for r in results] == [None, "link0", "link1", None]
