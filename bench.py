@@ -573,6 +573,9 @@ def main():
                                                       reduce_max, share_execs=True)
             servable["per_template"] = full_load_stats(foundry, archive, wrank, lanes, args.load_steps, barrier,
                                                        reduce_max)
+            # the archive as the reference writes it: the store is packed on the GPU at LOAD
+            servable["reference_written"] = full_load_stats(foundry, plain, wrank, lanes, args.load_steps,
+                                                            barrier, reduce_max, share_execs=True)
         # serve sweeps (reference ServingSet::serve, templater.cpp:177-188): apply every
         # batch's parameters in label order; then serve + replay every batch, the
         # reference's `bench --mode load` loop (pipeline.cpp:876-889)
@@ -704,6 +707,10 @@ def main():
                 "loaded, every member's parameters resident in HBM",
             reference_full_load_ms=(cpu or {}).get("reference_full_load_ms"),
             per_template=servable["per_template"],
+            reference_written_archive=dict(servable["reference_written"],
+                                           note="same LOAD (share_execs) of the archive the reference's "
+                                                "save writes (no templates.fdt): graphs.bin to HBM and the "
+                                                "GPU packer first (breakdown pack_ms)"),
             floor="driver-serialized: ~11-15 us per function load (9028 functions in 96 libraries) and "
                   "~35 ms per cuGraphInstantiate of a 1036-node template (~50 us per concurrent branch "
                   "node); profiles/round2_driver_floor.md"),
