@@ -3,4 +3,4 @@
 # (max 5.8), 16/10 4.42-5.14, 12/10 4.29-4.47, 16/19 4.19-4.31 (max 4.4-5.2) -> 16/19 shipped.
 cd "$(dirname "$0")/.."
 python bench.py --steps 3 --warmup 3 --e2e-steps 1 --skip-load --no-cpu-baseline > /dev/null 2>&1
-for i in 1 2; do REPS=12 TAG="shipped" python tools/_exp_e2e.py; done
+for i in 1 2; do REPS=12 TAG="shipped" python tools/experiments/e2e.py; done

@@ -51,9 +51,9 @@ def main() -> None:
     out = {"workload": name, "n": n}
 
     # one LOAD alone (warm process)
-    foundry.load(arch, rank=0, world=8, share_execs=True).close()
+    foundry.load(arch, rank=0, world=8, share_execs=True, relocate=True).close()
     t0 = time.perf_counter()
-    foundry.load(arch, rank=0, world=8, share_execs=True).close()
+    foundry.load(arch, rank=0, world=8, share_execs=True, relocate=True).close()
     out["alone_ms"] = (time.perf_counter() - t0) * 1e3
 
     # N threads of this process
