@@ -35,6 +35,21 @@ namespace fs = std::filesystem;
 namespace {
 
 using Clock = std::chrono::steady_clock;
+
+// Driver lane: the reference serializes driver mutation, instantiation and
+// update on one lane (sim_driver.hpp:213-215). The CUDA driver does too,
+// behind process-wide locks, and concurrent LOADs (or teardowns) from several
+// threads of one process convoy on them (profiles/round2_thread_vs_process.md).
+// Even with only the driver-bound phases on one lane, another LOAD's staging
+// (allocations, copies, CRC launches) stretched a concurrent cuGraphInstantiate
+// by up to 15x. So a LOAD and a context's teardown hold one process-wide lane:
+// LOADs of one process run one after another (N x one LOAD); parallel LOADs
+// are one process per GPU (bench.py, tools/verify_tp8.py).
+std::mutex& driver_lane() {
+    static std::mutex m;
+    return m;
+}
+
 double ms_since(Clock::time_point t0) {
     return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
 }
@@ -116,6 +131,7 @@ struct ServingContext::Impl {
     CUcontext cu_ctx = nullptr;
 
     ~Impl() {
+        std::lock_guard lane(driver_lane());
         try {
             const DriverApi& api = driver();
             if (dev) dev->make_current();
@@ -887,6 +903,9 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     require(opts.world >= 1 && opts.rank < opts.world, Errc::invalid_argument,
             "rank " + std::to_string(opts.rank) + " is outside world size " + std::to_string(opts.world));
     auto impl = std::make_unique<ServingContext::Impl>();
+    // one LOAD at a time per process (see driver_lane()); declared after the
+    // context, so on an exception the lane is released before ~Impl takes it
+    std::unique_lock lane(driver_lane());
     auto& I = *impl;
     I.dev = &device;
     I.opts = opts;
@@ -1107,6 +1126,7 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
         arena = std::max<uint64_t>(arena, I.view->group(g).image_bytes + 64ull * I.view->group(g).n_nodes);
     I.ctx->ensure_trace_arena(arena);
     I.ctx->sync_trace_state();
+    lane.unlock();
 
     for (uint32_t m = 0; m < H.n_members; ++m) I.labels.push_back(I.view->member(m).label);
     std::sort(I.labels.begin(), I.labels.end());
