@@ -108,10 +108,11 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
                                             const unsigned char* d_graphs, std::span<const uint8_t> patch_bin,
                                             const Manifest& manifest, std::span<const uint8_t> slots_bin,
                                             PackStats* stats, DevicePackTimings* timings, bool full_host_copy,
-                                            const uint64_t* verified_graphs_crc) {
+                                            const uint64_t* verified_graphs_crc,
+                                            std::future<PatchView>* patch_view) {
     const auto t_all = Clock::now();
     DevicePackTimings tm;
-    const PatchView patches = parse_patch_view(patch_bin);
+    const PatchView patches = patch_view ? patch_view->get() : parse_patch_view(patch_bin);
     tm.patch_parse_ms = ms_of(t_all);
     const CommSlotTable slots = slots_bin.empty() ? CommSlotTable{} : parse_comm_slots(slots_bin);
     if (!patches.empty())
@@ -643,16 +644,24 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
         timages_bytes = (timages_bytes + 15) / 16 * 16;
         Gp.timage_off = timages_bytes;  // TIMAGES-relative until rebased
         timages_bytes += g_image[g];
-
-        // members' tiles; rank-op ranges shared per (group, tile index)
-        // per tile index: the distinct op slices stored so far, as ranges of rops
+    }
+    // members' tiles, group by group on host threads: rank-op ranges are shared
+    // per (group, tile index), so each group builds its own op list, which are
+    // then concatenated in group order (the offline packer's single list)
+    tiles.resize(n_tiles);
+    std::vector<std::vector<fdt_rank_op>> grops(n_groups);
+    parallel_for(n_groups, 0, [&](size_t gi) {
+        const uint32_t g = static_cast<uint32_t>(gi);
+        const fdt_group& Gp = groups[g];
+        std::vector<fdt_rank_op>& gops = grops[g];
+        // per tile index: the distinct op slices stored so far, as ranges of gops
         std::vector<std::vector<std::pair<uint32_t, uint32_t>>> shared_ops;
         for (uint32_t m = Gp.first_member; m < Gp.first_member + Gp.n_members; ++m) {
             fdt_member& M = members[m];
             M.label = loc_of[m]->label;
             M.group = g;
             M.out_off = out_off[m];
-            M.n_nodes = N;
+            M.n_nodes = Gp.n_nodes;
             M.first_tile = tile_base[m];
             const uint64_t nchunks = g_image[g] / 16;
             const uint32_t ntiles = static_cast<uint32_t>((nchunks + FDT_TILE_CHUNKS - 1) / FDT_TILE_CHUNKS);
@@ -663,7 +672,8 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
             for (uint32_t t = 0; t < ntiles; ++t) {
                 const uint64_t cb = uint64_t(t) * FDT_TILE_CHUNKS;
                 const uint64_t ce = std::min<uint64_t>(nchunks, cb + FDT_TILE_CHUNKS);
-                fdt_tile T{};
+                fdt_tile& T = tiles[tile_base[m] + t];
+                T = fdt_tile{};
                 T.src_off = Gp.timage_off + 16 * cb;
                 T.dst_off = out_off[m] + 16 * cb;
                 T.nchunks = static_cast<uint32_t>(ce - cb);
@@ -677,21 +687,32 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
                 const std::pair<uint32_t, uint32_t>* hit = nullptr;
                 for (const auto& c : shared_ops[t])
                     if (c.second - c.first == n_ops &&
-                        std::memcmp(rops.data() + c.first, ops.data() + r_begin, n_ops * sizeof(fdt_rank_op)) == 0) {
+                        std::memcmp(gops.data() + c.first, ops.data() + r_begin, n_ops * sizeof(fdt_rank_op)) == 0) {
                         hit = &c;
                         break;
                     }
                 if (!hit) {
-                    const uint32_t lo = static_cast<uint32_t>(rops.size());
-                    rops.insert(rops.end(), ops.begin() + static_cast<long>(r_begin),
+                    const uint32_t lo = static_cast<uint32_t>(gops.size());
+                    gops.insert(gops.end(), ops.begin() + static_cast<long>(r_begin),
                                 ops.begin() + static_cast<long>(rpos));
-                    shared_ops[t].push_back({lo, static_cast<uint32_t>(rops.size())});
+                    shared_ops[t].push_back({lo, static_cast<uint32_t>(gops.size())});
                     hit = &shared_ops[t].back();
                 }
-                T.rop_lo = hit->first;
+                T.rop_lo = hit->first;  // group-relative until the lists are joined
                 T.rop_hi = hit->second;
-                tiles.push_back(T);
             }
+        }
+    });
+    for (uint32_t g = 0; g < n_groups; ++g) {
+        const uint32_t base = static_cast<uint32_t>(rops.size());
+        rops.insert(rops.end(), grops[g].begin(), grops[g].end());
+        const fdt_group& Gp = groups[g];
+        if (Gp.n_members == 0) continue;
+        const uint32_t t0g = tile_base[Gp.first_member];
+        const uint32_t last = Gp.first_member + Gp.n_members - 1;
+        for (uint32_t t = t0g; t < tile_base[last] + members[last].n_tiles; ++t) {
+            tiles[t].rop_lo += base;
+            tiles[t].rop_hi += base;
         }
     }
     // relocation-free template tiles first (stable), as the offline packer orders them

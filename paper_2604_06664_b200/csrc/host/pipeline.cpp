@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <future>
 #include <mutex>
 #include <thread>
 
@@ -932,14 +933,20 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
     //    lands); files LOAD parses stay in host memory; graphs.bin is only
     //    hashed when the store replaces it
     StageTimings st;
+    std::future<PatchView> patch_view;  // reference-written archive: parsed while the rest streams
     try {
         StagePlan plan;
         const bool has_store = I.manifest.file_digests.count("templates.fdt") != 0;
         // the store goes to HBM; a reference-written archive's graphs.bin goes
-        // there instead, for the GPU packer
+        // there instead, for the GPU packer, with patch.bin read first
         plan.device = {has_store ? "templates.fdt" : "graphs.bin"};
+        if (!has_store) plan.host_first = {"patch.bin"};
         plan.keep_host = [has_store](const std::string& rel) { return !(has_store && rel == "graphs.bin"); };
         I.staged = std::make_unique<StagedArchive>(device, archive, I.manifest, opts.prepare_lanes, &st, plan);
+        if (!has_store && I.staged->has("patch.bin")) {
+            StagedArchive* staged = I.staged.get();  // its errors surface in the packer, after integrity
+            patch_view = std::async(std::launch::async, [staged] { return parse_patch_view(staged->host("patch.bin")); });
+        }
         I.staged->verify(I.manifest, &st);
     } catch (const Error&) {
         rethrow_in_step("archive integrity");
@@ -973,7 +980,8 @@ ServingContext load(Device& device, const fs::path& archive, const LoadOptions& 
                 device, I.file_host("graphs.bin"), I.staged->device("graphs.bin"), I.file_host("patch.bin"),
                 I.manifest,
                 I.staged->has("comm_slots.bin") ? I.file_host("comm_slots.bin") : std::span<const uint8_t>{},
-                nullptr, nullptr, /*full_host_copy=*/false, &I.manifest.file_digests.at("graphs.bin"));
+                nullptr, nullptr, /*full_host_copy=*/false, &I.manifest.file_digests.at("graphs.bin"),
+                patch_view.valid() ? &patch_view : nullptr);
         } catch (const Error&) {
             rethrow_in_step("template construction");
         }

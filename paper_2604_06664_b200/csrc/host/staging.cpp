@@ -191,6 +191,8 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const std::vecto
         f.placement = plan.keep_host && plan.keep_host(rel) ? Placement::host : Placement::hash;
         files_[rel] = f;
     }
+    for (const auto& rel : plan.host_first)
+        if (files_.count(rel) && files_.at(rel).placement == Placement::host) order_.push_back(&files_.at(rel));
     for (const auto& rel : plan.device)
         if (files_.count(rel) && files_.at(rel).placement != Placement::device) {
             files_.at(rel).placement = Placement::device;
@@ -198,7 +200,8 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const std::vecto
         }
     for (Placement pl : {Placement::host, Placement::hash})
         for (const auto& [rel, f] : files_)
-            if (f.placement == pl) order_.push_back(&f);
+            if (f.placement == pl && std::find(order_.begin(), order_.end(), &f) == order_.end())
+                order_.push_back(&f);
 
     // layout: device + host files in staging memory; device files' CRC plan
     std::vector<FdyCrcBlock> blocks;
@@ -655,15 +658,21 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
     if (has_store) {
         plan.device = {"templates.fdt"};
         first = plan.device;
-    } else {  // graphs.bin to HBM for the GPU packer
+    } else {  // graphs.bin to HBM for the GPU packer; patch.bin first, parsed while graphs.bin streams
         plan.device = {"graphs.bin"};
+        plan.host_first = {"patch.bin"};
         first = {"graphs.bin", "patch.bin"};
         if (manifest.file_digests.count("comm_slots.bin")) first.push_back("comm_slots.bin");
         plan.keep_host = [](const std::string& rel) { return rel == "patch.bin" || rel == "comm_slots.bin"; };
     }
+    std::future<PatchView> patch_view;
     try {
         staged = std::make_unique<StagedArchive>(dev, root, manifest, lanes, &st, plan);
         trace_point("staging started", t_all);
+        if (!has_store && staged->has("patch.bin")) {
+            // parse errors surface when the packer consumes it, after integrity
+            patch_view = std::async(std::launch::async, [&staged] { return parse_patch_view(staged->host("patch.bin")); });
+        }
         for (const auto& rel : first) staged->verify_file(manifest, rel, &st);
         trace_point("store verified", t_all);
     } catch (const Error&) {
@@ -687,7 +696,8 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
                                              staged->has("comm_slots.bin") ? staged->host("comm_slots.bin")
                                                                            : std::span<const uint8_t>{},
                                              nullptr, nullptr, /*full_host_copy=*/keep != nullptr,
-                                             &manifest.file_digests.at("graphs.bin"));
+                                             &manifest.file_digests.at("graphs.bin"),
+                                             patch_view.valid() ? &patch_view : nullptr);
         } catch (const Error&) {
             rethrow_in_step("template construction");
         }

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <future>
 #include <memory>
 #include <span>
 #include <vector>
@@ -42,6 +43,8 @@ struct DevicePackResult {
     std::span<const uint8_t> host() const { return {host_bytes.get(), host_size}; }
 };
 
+// patch_view: patch_bin already being parsed (parse_patch_view) on another
+// thread while graphs.bin streamed in; its errors surface here.
 // verified_graphs_crc: graphs.bin's digest when the caller has already checked
 // it (LOAD's integrity pass); otherwise the GPU computes it for the header.
 // graphs_host / d_graphs: graphs.bin on the host and in HBM (the device copy
@@ -54,7 +57,8 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
                                             const Manifest& manifest, std::span<const uint8_t> slots_bin = {},
                                             PackStats* stats = nullptr, DevicePackTimings* timings = nullptr,
                                             bool full_host_copy = true,
-                                            const uint64_t* verified_graphs_crc = nullptr);
+                                            const uint64_t* verified_graphs_crc = nullptr,
+                                            std::future<PatchView>* patch_view = nullptr);
 
 // The same for an archive directory: reads and uploads graphs.bin, packs it on
 // the GPU, returns the store bytes (the tests compare them with the offline

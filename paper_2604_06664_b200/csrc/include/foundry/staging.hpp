@@ -59,6 +59,8 @@ struct StagePlan {
     std::function<bool(const std::string&)> keep_host;  // Placement::host files (others: hash)
     int lane_nice = 0;  // > 0: lanes run at this lower CPU priority (they yield to a concurrent
                         // critical-path stager when the host's cores are oversubscribed)
+    std::vector<std::string> host_first;  // Placement::host files staged before the device files
+                                          // (small inputs a consumer parses while the rest streams)
 };
 
 struct StagedFile {
