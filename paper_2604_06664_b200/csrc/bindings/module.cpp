@@ -328,6 +328,37 @@ PYBIND11_MODULE(_foundry, m) {
         }
         return py::make_tuple(py::bytes(reinterpret_cast<const char*>(out.data()), out.size()), t);
     }, py::arg("archive"), py::arg("gpu") = true, py::arg("device") = 0);
+    // parse_patch_view against parse_patch_table: the same entries (or the same
+    // error) for a patch.bin's bytes
+    m.def("_patch_view_matches_table", [](py::bytes raw) {
+        const std::string b = raw;
+        const std::span<const uint8_t> bytes(reinterpret_cast<const uint8_t*>(b.data()), b.size());
+        const PatchTable t = parse_patch_table(bytes);  // raises like the reference
+        const PatchView v = parse_patch_view(bytes);
+        if (v.world_placeholder != t.world_placeholder || v.graphs.size() != t.per_graph.size()) return false;
+        for (const auto& [label, entries] : t.per_graph) {
+            if (!v.has(label)) return false;
+            const auto got = v.find(label);
+            if (got.size() != entries.size()) return false;
+            for (size_t i = 0; i < entries.size(); ++i) {
+                const CommPatchEntry& e = entries[i];
+                const PatchEntryView& g = got[i];
+                if (g.node_id != e.node_id || g.stub_hash != e.stub.binary_hash || g.stub_name != e.stub.name ||
+                    g.real_name != e.real_name || g.n_rank != e.rank_offsets.size() ||
+                    g.n_world != e.world_offsets.size() || g.patch_width != e.patch_width)
+                    return false;
+                for (uint32_t k = 0; k < g.n_rank; ++k)
+                    if (g.rank_offset(k) != e.rank_offsets[k]) return false;
+                for (uint32_t k = 0; k < g.n_world; ++k)
+                    if (g.world_offset(k) != e.world_offsets[k]) return false;
+            }
+        }
+        return true;
+    });
+    m.def("_parse_patch_view", [](py::bytes raw) {
+        const std::string b = raw;
+        (void)parse_patch_view({reinterpret_cast<const uint8_t*>(b.data()), b.size()});
+    });
     // member-image arena (the kernel's output layout) -> FNDG container in
     // graphs.bin locator order
     m.def("_decode_member_images", [](const std::string& archive, py::bytes arena_bytes) {

@@ -249,3 +249,20 @@ def test_comm_slots_are_validated(foundry, archives, tmp_path):
     # nothing was written by the failed calls
     assert not os.path.exists(os.path.join(copy, "comm_slots.bin"))
     assert "comm_slots.bin" not in manifest(copy)["files"]
+
+
+def test_patch_view_equals_the_patch_table(foundry, archives):
+    """The zero-copy patch-table view LOAD and the GPU packer read
+    (parse_patch_view) yields exactly parse_patch_table's entries, and the same
+    error for every truncation of the bytes (reference rank_forge.cpp:43-102)."""
+    arch, _ = archives("moe-spmd")
+    raw = open(os.path.join(arch, "patch.bin"), "rb").read()
+    assert foundry._foundry._patch_view_matches_table(raw)
+    for cut in (0, 3, 5, 13, 17, 40, len(raw) // 2, len(raw) - 1):
+        with pytest.raises(foundry.FoundryError) as table:
+            foundry._foundry._patch_view_matches_table(raw[:cut])
+        with pytest.raises(foundry.FoundryError) as view:
+            foundry._foundry._parse_patch_view(raw[:cut])
+        assert str(table.value) == str(view.value), cut
+    with pytest.raises(foundry.FoundryError, match="trailing bytes in patch table"):
+        foundry._foundry._parse_patch_view(raw + b"\0")
