@@ -361,9 +361,17 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     // record CRCs (parse_graph_at's per-record check) and the whole file's
     // digest (the store header's source_graphs_crc), on the GPU
     // (the whole file only when the caller has not already verified it)
+    // A record rarely starts on a 16-byte boundary: its head (up to 15 bytes)
+    // and its aligned body are CRCed as two segments, so the body takes the
+    // kernel's vectorized path, and the host combines them
+    // (crc(A||B) = crc64_combine(crc(A), crc(B), |B|)).
     std::vector<Segment> segs;
     segs.push_back({0, verified_graphs_crc ? 0 : gsize});
-    for (uint32_t m = 0; m < nm; ++m) segs.push_back({rec_off[m], rec_len[m]});
+    for (uint32_t m = 0; m < nm; ++m) {
+        const uint64_t head = std::min<uint64_t>(rec_len[m], (16 - rec_off[m] % 16) % 16);
+        segs.push_back({rec_off[m], head});
+        segs.push_back({rec_off[m] + head, rec_len[m] - head});
+    }
 
     std::vector<uint32_t> status, small;
     std::vector<unsigned long long> upos;
@@ -393,7 +401,13 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     d2h(cap, a.cap, GN, st);
     d2h(rep_attrs, a.rep_attrs, GN, st);
     d2h(node_off, a.node_off, TN, st);
-    digests = crc64_device(dev, d_graphs, segs);  // synchronizes the stream
+    {
+        const auto parts = crc64_device(dev, d_graphs, segs);  // synchronizes the stream
+        digests.assign(1 + nm, 0);
+        digests[0] = parts[0];
+        for (uint32_t m = 0; m < nm; ++m)
+            digests[1 + m] = crc64_combine(parts[1 + 2 * m], parts[2 + 2 * m], segs[2 + 2 * m].length);
+    }
     tm.pass1_ms = ms_of(t0);
 
     // ------------------------------------------------ host: checks, kernel table, layout
