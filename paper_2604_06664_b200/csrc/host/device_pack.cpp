@@ -25,6 +25,7 @@
 #include "foundry/bytes.hpp"
 #include "foundry/hash.hpp"
 #include "foundry/parallel.hpp"
+#include "foundry/staging.hpp"
 
 namespace foundry {
 
@@ -69,6 +70,40 @@ public:
 private:
     DeviceBuffer buf_;
     size_t at_ = 0;
+};
+
+// Host arrays bound for one contiguous device range, gathered into one pinned
+// buffer and sent with one copy (each pageable copy blocks the host for
+// ~10-20 us). The gaps between the arrays are alignment padding only.
+class Upload {
+public:
+    template <typename T>
+    void add(T* dst, const T* src, size_t count) {
+        if (count) items_.push_back({reinterpret_cast<unsigned char*>(dst), src, count * sizeof(T)});
+    }
+    template <typename T>
+    void add(T* dst, const std::vector<T>& v) { add(dst, v.data(), v.size()); }
+    void send(Device& dev, cudaStream_t st) {
+        if (items_.empty()) return;
+        unsigned char* lo = items_[0].dst;
+        unsigned char* hi = lo;
+        for (const Item& it : items_) {
+            lo = std::min(lo, it.dst);
+            hi = std::max(hi, it.dst + it.bytes);
+        }
+        lease_ = PinnedLease(dev, size_t(hi - lo));
+        for (const Item& it : items_) std::memcpy(lease_.data() + (it.dst - lo), it.src, it.bytes);
+        cuda_check(cudaMemcpyAsync(lo, lease_.data(), size_t(hi - lo), cudaMemcpyHostToDevice, st), "GPU pack H2D");
+    }
+
+private:
+    struct Item {
+        unsigned char* dst;
+        const void* src;
+        size_t bytes;
+    };
+    std::vector<Item> items_;
+    PinnedLease lease_;  // alive until the owner has synchronized the stream
 };
 
 template <typename T>
@@ -281,36 +316,39 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     FdyPackArgs a{};
     a.graphs = d_graphs;
     a.graphs_bytes = gsize;
+    // uploaded arrays first (one contiguous range, one copy), then the results
+    // read back (one contiguous range), then the device-only scratch
     auto* d_rec_off = s1.take<uint64_t>(nm);
     auto* d_rec_len = s1.take<uint64_t>(nm);
     auto* d_node_base = s1.take<uint32_t>(nm);
     auto* d_n_nodes = s1.take<uint32_t>(nm);
     auto* d_n_edges = s1.take<uint32_t>(nm);
     auto* d_member_group = s1.take<uint32_t>(nm);
-    auto* d_status = s1.take<uint32_t>(nm);
     auto* d_group_rep = s1.take<uint32_t>(n_groups);
     auto* d_gnode_base = s1.take<uint32_t>(n_groups);
-    a.node_off = s1.take<uint32_t>(TN);
-    a.node_member = s1.take<uint32_t>(TN);
-    a.node_slot = s1.take<uint32_t>(TN);
+    auto* d_pe_node = s1.take<uint32_t>(NE);
+    auto* d_pe_stub_hash = s1.take<uint64_t>(NE);
+    auto* d_pe_stub_name = s1.take<uint32_t>(NE);
+    auto* d_pe_real_name = s1.take<uint32_t>(NE);
+    auto* d_pe_need = s1.take<uint32_t>(NE);
+    auto* d_entry_base = s1.take<uint32_t>(nm + 1);
+    auto* d_names = s1.take<unsigned char>(name_bytes.size() + 1);
+    auto* d_name_off = s1.take<uint32_t>(name_off.size());
+    auto* d_name_len = s1.take<uint32_t>(name_len.size());
+    auto* d_status = s1.take<uint32_t>(nm);
     a.cap = s1.take<uint32_t>(GN);
     a.rep_attrs = s1.take<fdt_node_attrs>(GN);
+    a.node_off = s1.take<uint32_t>(TN);
+    unsigned char* const back_end = reinterpret_cast<unsigned char*>(a.node_off + TN);
+    a.node_member = s1.take<uint32_t>(TN);
+    a.node_slot = s1.take<uint32_t>(TN);
     a.tkey = s1.take<unsigned long long>(tslots);
     a.tpos = s1.take<unsigned long long>(tslots);
     a.tuniq = s1.take<uint32_t>(tslots);
     a.upos = s1.take<unsigned long long>(tslots);
     a.uoff = s1.take<uint64_t>(tslots);
     auto* d_small = s1.take<uint32_t>(4);  // ucount, flags
-    auto* d_pe_node = s1.take<uint32_t>(NE);
-    auto* d_pe_stub_hash = s1.take<uint64_t>(NE);
-    auto* d_pe_stub_name = s1.take<uint32_t>(NE);
-    auto* d_pe_real_name = s1.take<uint32_t>(NE);
-    auto* d_pe_need = s1.take<uint32_t>(NE);
     a.pe_slot = s1.take<uint32_t>(NE);
-    auto* d_entry_base = s1.take<uint32_t>(nm + 1);
-    auto* d_names = s1.take<unsigned char>(name_bytes.size() + 1);
-    auto* d_name_off = s1.take<uint32_t>(name_off.size());
-    auto* d_name_len = s1.take<uint32_t>(name_len.size());
     a.pe_node = d_pe_node;
     a.pe_stub_hash = d_pe_stub_hash;
     a.pe_stub_name = d_pe_stub_name;
@@ -322,17 +360,6 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     a.name_len = d_name_len;
     a.comm_real_hash = manifest.comm_real_hash;
     a.n_entries = NE;
-    h2d(d_pe_node, pe_node, st);
-    h2d(d_pe_stub_hash, pe_stub_hash, st);
-    h2d(d_pe_stub_name, pe_stub_name, st);
-    h2d(d_pe_real_name, pe_real_name, st);
-    h2d(d_pe_need, pe_need, st);
-    h2d(d_entry_base, entry_base, st);
-    h2d(d_name_off, name_off, st);
-    h2d(d_name_len, name_len, st);
-    if (!name_bytes.empty())
-        cuda_check(cudaMemcpyAsync(d_names, name_bytes.data(), name_bytes.size(), cudaMemcpyHostToDevice, st),
-                   "GPU pack H2D");
     a.rec_off = d_rec_off;
     a.rec_len = d_rec_len;
     a.node_base = d_node_base;
@@ -347,17 +374,25 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     a.tmask = tslots - 1;
     a.n_members = nm;
     a.total_nodes = TN;
-    h2d(d_rec_off, rec_off, st);
-    h2d(d_rec_len, rec_len, st);
-    h2d(d_node_base, node_base, st);
-    h2d(d_n_nodes, n_nodes, st);
-    h2d(d_n_edges, n_edges, st);
-    h2d(d_member_group, member_group, st);
-    h2d(d_group_rep, group_rep, st);
-    {
-        std::vector<uint32_t> gb(gnode_base.begin(), gnode_base.end() - 1);
-        h2d(d_gnode_base, gb, st);
-    }
+    Upload up1;
+    up1.add(d_rec_off, rec_off);
+    up1.add(d_rec_len, rec_len);
+    up1.add(d_node_base, node_base);
+    up1.add(d_n_nodes, n_nodes);
+    up1.add(d_n_edges, n_edges);
+    up1.add(d_member_group, member_group);
+    up1.add(d_group_rep, group_rep);
+    up1.add(d_gnode_base, gnode_base.data(), n_groups);
+    up1.add(d_pe_node, pe_node);
+    up1.add(d_pe_stub_hash, pe_stub_hash);
+    up1.add(d_pe_stub_name, pe_stub_name);
+    up1.add(d_pe_real_name, pe_real_name);
+    up1.add(d_pe_need, pe_need);
+    up1.add(d_entry_base, entry_base);
+    up1.add(d_names, reinterpret_cast<const unsigned char*>(name_bytes.data()), name_bytes.size());
+    up1.add(d_name_off, name_off);
+    up1.add(d_name_len, name_len);
+    up1.send(dev, st);
     // record CRCs (parse_graph_at's per-record check) and the whole file's
     // digest (the store header's source_graphs_crc), on the GPU
     // (the whole file only when the caller has not already verified it)
@@ -373,7 +408,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
         segs.push_back({rec_off[m] + head, rec_len[m] - head});
     }
 
-    std::vector<uint32_t> status, small;
+    std::vector<uint32_t> small;
     std::vector<unsigned long long> upos;
     std::vector<uint64_t> uoff, digests;
     for (uint32_t attempt = 0;; ++attempt) {
@@ -393,14 +428,18 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     }
     const uint32_t nu = small[0];
     tm.kernel_keys = nu;
-    d2h(status, d_status, nm, st);
     d2h(upos, a.upos, nu, st);
     d2h(uoff, a.uoff, nu, st);
-    std::vector<uint32_t> cap, node_off;
-    std::vector<fdt_node_attrs> rep_attrs;
-    d2h(cap, a.cap, GN, st);
-    d2h(rep_attrs, a.rep_attrs, GN, st);
-    d2h(node_off, a.node_off, TN, st);
+    // status | cap | rep_attrs | node_off: one copy into pinned memory
+    unsigned char* const back_lo = reinterpret_cast<unsigned char*>(d_status);
+    PinnedLease back(dev, size_t(back_end - back_lo));
+    cuda_check(cudaMemcpyAsync(back.data(), back_lo, size_t(back_end - back_lo), cudaMemcpyDeviceToHost, st),
+               "GPU pack D2H");
+    auto host_of = [&](const void* d) { return back.data() + (static_cast<const unsigned char*>(d) - back_lo); };
+    const uint32_t* status = reinterpret_cast<const uint32_t*>(host_of(d_status));
+    const uint32_t* cap = reinterpret_cast<const uint32_t*>(host_of(a.cap));
+    const fdt_node_attrs* rep_attrs = reinterpret_cast<const fdt_node_attrs*>(host_of(a.rep_attrs));
+    const uint32_t* node_off = reinterpret_cast<const uint32_t*>(host_of(a.node_off));
     {
         const auto parts = crc64_device(dev, d_graphs, segs);  // synchronizes the stream
         digests.assign(1 + nm, 0);
@@ -479,6 +518,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
         raise(Errc::archive_corruption, "a patch entry of group " + std::to_string(g) + " was rejected on the GPU");
     }
 
+    tm.checks_ms = ms_of(t0);
     // kernel table: every distinct (hash, func attrs, name) in first-occurrence
     // order, where a graph's patch entries' real comm kernels follow its nodes
     // (the GPU table holds both; positions order them)
@@ -506,6 +546,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
         ukidx[u] = k;
     }
 
+    tm.kernel_table_ms = ms_of(t0) - tm.checks_ms;
     // group layouts: slot capacity = group-wide maximum (round16), in node order
     std::vector<uint32_t> blob_off(GN);
     std::vector<uint64_t> g_image(n_groups), g_desc(n_groups);
@@ -533,6 +574,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     }
     const uint32_t n_tiles = static_cast<uint32_t>(tile_member.size());
 
+    const double before_rops = ms_of(t0);
     // rank ops (apply_rank_patches' rank / world writes, then comm slots as
     // value ops), per member in table order, stably sorted by chunk; the stub
     // -> real kernel swap is the GPU's (pack_swaps_kernel)
@@ -561,6 +603,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
         });
     }
     tm.host1_ms = ms_of(t0);
+    tm.rank_ops_ms = tm.host1_ms - before_rops;
 
     // ------------------------------------------------ pass 2
     t0 = Clock::now();
@@ -628,7 +671,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
         Gp.representative = groups_in[g].representative;
         Gp.attrs_first = static_cast<uint32_t>(attrs.size());
         Gp.edges_off = edges.size() * sizeof(uint32_t);
-        attrs.insert(attrs.end(), rep_attrs.begin() + gnode_base[g], rep_attrs.begin() + gnode_base[g + 1]);
+        attrs.insert(attrs.end(), rep_attrs + gnode_base[g], rep_attrs + gnode_base[g + 1]);
         const uint8_t* etab = G + rec_off[rep] + rec_len[rep] - 8ull * E;
         const size_t e0 = edges.size();
         edges.resize(e0 + 2ull * E);

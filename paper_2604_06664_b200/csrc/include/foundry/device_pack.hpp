@@ -21,6 +21,7 @@ struct DevicePackTimings {
     double patch_parse_ms = 0;  // of which: the patch table view
     double pass1_ms = 0;  // upload + walk/fields/edges/verify/compact + record CRCs
     double host1_ms = 0;  // checks, kernel table, layout, rank ops
+    double checks_ms = 0, kernel_table_ms = 0, rank_ops_ms = 0;  // of which
     double pass2_ms = 0;  // images + diff counts
     double host2_ms = 0;  // tile table, host sections
     double tiles_ms = 0;  // of which: the tile table and shared rank-op ranges
