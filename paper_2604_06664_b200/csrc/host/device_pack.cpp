@@ -917,7 +917,7 @@ std::vector<uint8_t> pack_archive_store_device(Device& dev, const std::filesyste
     const bool has_slots = man.file_digests.count("comm_slots.bin") != 0;
     const auto slots = has_slots ? slurp(paths.comm_slots()) : std::vector<uint8_t>{};
     dev.make_current();
-    DeviceBuffer d(dev, std::max<size_t>(graphs.size(), 16));
+    DeviceBuffer d(dev, (graphs.size() + 256) / 256 * 256);  // kernels read whole 16-byte units
     cuda_check(cudaMemcpyAsync(d.data(), graphs.data(), graphs.size(), cudaMemcpyHostToDevice, dev.stream()),
                "cudaMemcpyAsync(graphs.bin)");
     DevicePackResult r = pack_template_store_device(dev, graphs, d.data(), patch, man, slots, nullptr, timings);

@@ -17,10 +17,11 @@
 // memset: type + 3 x u64 (25 bytes). Empty: 1 byte. Nothing is aligned.
 //
 // Pass 1
-//   walk     one CTA per record: the record streams through a 32 KiB shared
-//            window and one thread hops node to node (a node's length is only
-//            known from its own name and argument sizes); emits node offsets,
-//            checks tags, bounds and the edge-table size.
+//   walk     one thread per record hops node to node (a node's length is only
+//            known from its own name and argument sizes) through a ring of
+//            8 KiB shared-memory windows that TMA bulk copies keep filled
+//            ahead of it; emits node offsets, checks tags, bounds and the
+//            edge-table size.
 //   fields   one thread per node: launch-dim / argument validation, topology
 //            against the representative's node, slot capacity (atomicMax per
 //            group node), kernel key (binary hash, func attrs, name) into an
@@ -51,8 +52,9 @@
 
 namespace {
 
-constexpr uint32_t kWalkThreads = 256;
-constexpr uint32_t kWalkWindow = 32768;
+constexpr uint32_t kWalkWin = 8192;                  // walk: TMA window
+constexpr uint32_t kWalkWins = 4;                    //       windows in the ring
+constexpr uint32_t kWalkRing = kWalkWin * kWalkWins; //       (a power of two)
 constexpr uint32_t kThreads = 256;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
@@ -150,84 +152,111 @@ __device__ __forceinline__ uint32_t table_insert(const FdyPackArgs& a, uint64_t 
 
 // ------------------------------------------------------------------- pass 1
 
-__global__ void __launch_bounds__(kWalkThreads) pack_walk_kernel(const FdyPackArgs a) {
-    __shared__ __align__(16) unsigned char win[kWalkWindow];
-    __shared__ uint64_t s_need;
-    __shared__ int s_done;  // 1 ok, 2 malformed
+__device__ __forceinline__ uint32_t smem_u32addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// One thread per record walks it node to node. The record streams through a
+// ring of kWalkWins 8 KiB windows in shared memory, filled by TMA bulk copies
+// (cp.async.bulk + mbarrier complete_tx) issued as far ahead as the ring
+// allows, so the walk's reads (type byte, name length, argument size: the
+// only fields a node's length depends on) hit shared memory and the next
+// windows are already in flight. Window k of the record holds bytes
+// [w0 + k * kWalkWin, ...) at ring offset (k mod kWalkWins) * kWalkWin.
+__global__ void __launch_bounds__(32) pack_walk_kernel(const FdyPackArgs a) {
+    __shared__ __align__(128) unsigned char ring[kWalkRing];
+    __shared__ __align__(8) unsigned long long bar[kWalkWins];
+    if (threadIdx.x != 0) return;
     const uint32_t m = blockIdx.x;
     const uint64_t rb = a.rec_off[m], rl = a.rec_len[m];
     const uint32_t N = a.n_nodes[m], E = a.n_edges[m], nb = a.node_base[m];
-    const uint64_t lim = rb + rl;  // the host checked it is inside graphs.bin
-    const uint64_t vec_end = a.graphs_bytes & ~15ull;
-    uint64_t p = 12;  // thread 0's cursor (record-relative) and node state
-    uint32_t n = 0, nl = 0;
-    int stage = 0;
-    if (threadIdx.x == 0) {
-        s_need = rb + 12;
-        s_done = rl < 12 ? 2 : 0;
+    if (rl < 12) {
+        atomicOr(&a.status[m], FDY_PACK_DECODE);
+        return;
     }
-    __syncthreads();
-    while (!s_done) {
-        const uint64_t ws = s_need & ~15ull;
-        const uint64_t we = u64min(ws + kWalkWindow, lim);
-        for (uint64_t o = uint64_t(threadIdx.x) * 16; ws + o < we; o += kWalkThreads * 16) {
-            if (ws + o + 16 <= vec_end) {
-                *reinterpret_cast<uint4*>(win + o) = __ldg(reinterpret_cast<const uint4*>(a.graphs + ws + o));
-            } else {
-                for (uint32_t k = 0; k < 16; ++k)
-                    win[o + k] = ws + o + k < a.graphs_bytes ? a.graphs[ws + o + k] : 0;
+    const uint64_t w0 = rb & ~15ull;                 // windows start 16-byte aligned
+    const uint64_t span = rb + rl - w0;              // bytes of the record's windows
+    const uint32_t n_wins = uint32_t((span + kWalkWin - 1) / kWalkWin);
+    for (uint32_t i = 0; i < kWalkWins; ++i)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32addr(&bar[i])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    uint32_t issued = 0, waited = 0;  // windows [0, issued) requested, [0, waited) landed
+    auto issue = [&](uint32_t k) {
+        const uint32_t slot = k % kWalkWins;
+        const uint64_t off = uint64_t(k) * kWalkWin;
+        // whole 16-byte units; the staged buffer is padded past every file
+        const uint32_t bytes = uint32_t((u64min(kWalkWin, span - off) + 15) & ~15ull);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32addr(&bar[slot])),
+                     "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32addr(ring + slot * kWalkWin)),
+            "l"(a.graphs + w0 + off), "r"(bytes), "r"(smem_u32addr(&bar[slot]))
+            : "memory");
+    };
+    auto wait = [&](uint32_t k) {
+        const uint32_t slot = k % kWalkWins, parity = (k / kWalkWins) & 1u;
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "WALK_WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra WALK_WAIT_%=;\n}" ::"r"(smem_u32addr(&bar[slot])),
+            "r"(parity)
+            : "memory");
+    };
+    // bytes [x, x + n) of the record (record-relative) are in shared memory
+    // once this returns; the ring is refilled ahead of x as far as it reaches
+    auto ensure = [&](uint64_t x, uint32_t n) {
+        const uint64_t ax = rb + x - w0;
+        const uint32_t lo = uint32_t(ax / kWalkWin), hi = uint32_t((ax + n - 1) / kWalkWin);
+        while (issued < n_wins && issued < lo + kWalkWins) {
+            if (issued >= kWalkWins && waited <= issued - kWalkWins) {  // its slot's last window
+                wait(waited);
+                ++waited;
             }
+            issue(issued++);
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            auto w32 = [&](uint64_t at) {
-                const unsigned char* s = win + (at - ws);
-                return uint32_t(s[0]) | uint32_t(s[1]) << 8 | uint32_t(s[2]) << 16 | uint32_t(s[3]) << 24;
-            };
-            uint64_t need = 0;
-            int done = 0;
-            while (!done && !need) {
-                if (n == N) {  // the edge table must end the record exactly
-                    done = p + 8ull * E == rl ? 1 : 2;
-                    break;
-                }
-                const uint64_t q = rb + p;
-                if (stage == 0) {
-                    if (p + 1 > rl) { done = 2; break; }
-                    if (q >= we) { need = q; break; }
-                    const uint8_t t = win[q - ws];
-                    if (t == 0) { stage = 1; continue; }
-                    if (t > 3) { done = 2; break; }
-                    const uint32_t len = t == 3 ? 1u : 25u;
-                    if (p + len > rl) { done = 2; break; }
-                    a.node_off[nb + n] = uint32_t(p);
-                    a.node_member[nb + n] = m;
-                    ++n;
-                    p += len;
-                } else if (stage == 1) {  // name length
-                    if (p + 66 > rl) { done = 2; break; }
-                    if (q + 66 > we) { need = q + 62; break; }
-                    nl = w32(q + 62);
-                    stage = 2;
-                } else {  // argument size
-                    if (p + 94 + uint64_t(nl) > rl) { done = 2; break; }
-                    const uint64_t f = q + 90 + nl;
-                    if (f < ws || f + 4 > we) { need = f; break; }
-                    const uint64_t len = 94ull + nl + w32(f);
-                    if (p + len > rl) { done = 2; break; }
-                    a.node_off[nb + n] = uint32_t(p);
-                    a.node_member[nb + n] = m;
-                    ++n;
-                    p += len;
-                    stage = 0;
-                }
-            }
-            if (done) s_done = done;
-            else s_need = need;
+        while (waited <= hi) {
+            wait(waited);
+            ++waited;
         }
-        __syncthreads();
+    };
+    auto byte_at = [&](uint64_t x) -> uint32_t { return ring[(rb + x - w0) & (kWalkRing - 1)]; };
+    auto u32_at = [&](uint64_t x) {
+        return byte_at(x) | byte_at(x + 1) << 8 | byte_at(x + 2) << 16 | byte_at(x + 3) << 24;
+    };
+    uint64_t p = 12;
+    bool bad = false;
+    for (uint32_t n = 0; n < N && !bad; ++n) {
+        if (p + 1 > rl) { bad = true; break; }
+        ensure(p, 1);
+        const uint32_t t = byte_at(p);
+        uint64_t len;
+        if (t == 0) {
+            if (p + 66 > rl) { bad = true; break; }
+            ensure(p + 62, 4);
+            const uint32_t nl = u32_at(p + 62);
+            if (p + 94 + uint64_t(nl) > rl) { bad = true; break; }
+            ensure(p + 90 + nl, 4);
+            len = 94ull + nl + u32_at(p + 90 + nl);
+        } else if (t <= 3) {
+            len = t == 3 ? 1u : 25u;
+        } else {
+            bad = true;
+            break;
+        }
+        if (p + len > rl) { bad = true; break; }
+        a.node_off[nb + n] = uint32_t(p);
+        a.node_member[nb + n] = m;
+        p += len;
     }
-    if (threadIdx.x == 0 && s_done == 2) atomicOr(&a.status[m], FDY_PACK_DECODE);
+    // the edge table must end the record exactly
+    if (bad || p + 8ull * E != rl) atomicOr(&a.status[m], FDY_PACK_DECODE);
+    while (waited < issued) {  // no bulk copy may still target this CTA's shared memory
+        wait(waited);
+        ++waited;
+    }
 }
 
 __device__ __forceinline__ bool member_ok(const FdyPackArgs& a, uint32_t m) {
@@ -588,7 +617,7 @@ int grid_for(uint32_t items, uint32_t per_cta) {
 extern "C" cudaError_t fdy_launch_pack_pass1(const FdyPackArgs* args, cudaStream_t stream) {
     const FdyPackArgs& a = *args;
     if (a.n_members == 0) return cudaSuccess;
-    pack_walk_kernel<<<a.n_members, kWalkThreads, 0, stream>>>(a);
+    pack_walk_kernel<<<a.n_members, 32, 0, stream>>>(a);
     if (a.total_nodes) {
         pack_fields_kernel<<<grid_for(a.total_nodes, kThreads), kThreads, 0, stream>>>(a);
     }
