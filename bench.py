@@ -463,6 +463,21 @@ def main():
     t_fan = time.perf_counter()
     store = distribute_store(group, api, dev, blob, args.fanout)  # the one exchange step
     fanout_ms = (time.perf_counter() - t_fan) * 1e3
+    # N > 1: the three SURVEY §8(e) exchange options on the same ranks, each
+    # twice after the one above (wall clock from a barrier to the store being
+    # resident on this rank, max over ranks)
+    fanout_modes = {}
+    if gworld > 1:
+        for mode in ("ipc", "chain", "host"):
+            times = []
+            for _ in range(2):
+                barrier()
+                t_m = time.perf_counter()
+                extra = distribute_store(group, api, dev, blob, mode)
+                times.append((time.perf_counter() - t_m) * 1e3)
+                barrier()  # no rank frees a store a peer may still read
+                api.lib.fdy_store_free(extra)
+            fanout_modes[mode] = reduce_max(min(times))
     members, _ = api.materialize(dev, store, wrank, TP_WORLD, base + delta)
     flush_w = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # each > 126 MB L2
     flush_r = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
@@ -738,6 +753,7 @@ def main():
         # submitted (its hold ends before the start event), the relocation grid, the member grid
         "gpu_launches": args.steps * (3 if delta else 2),
         "fanout": {"mode": args.fanout if gworld > 1 else "none", "ms": fanout_ms,
+                   "modes_ms": fanout_modes or None,
                    "store_bytes": len(blob)},
     }
     print(json.dumps(line), flush=True)

@@ -42,3 +42,5 @@ def test_bench_n_ranks(native_build, fanout, n):
     assert d["n_gpus"] == n and d["scaling"] == "weak" and d["value"] > 0
     assert d["roofline"]["achieved"] > 0 and d["e2e"]["value"] > 0
     assert d["fanout"]["mode"] == fanout
+    assert set(d["fanout"]["modes_ms"]) == {"ipc", "chain", "host"}  # all three options
+    assert all(v > 0 for v in d["fanout"]["modes_ms"].values())
