@@ -321,7 +321,7 @@ PYBIND11_MODULE(_foundry, m) {
                 Device dev(device);
                 DevicePackTimings tm;
                 out = pack_archive_store_device(dev, archive, &tm);
-                t = {{"prep_ms", tm.prep_ms}, {"patch_parse_ms", tm.patch_parse_ms}, {"tiles_ms", tm.tiles_ms}, {"checks_ms", tm.checks_ms},
+                t = {{"prep_ms", tm.prep_ms}, {"patch_parse_ms", tm.patch_parse_ms}, {"tiles_ms", tm.tiles_ms}, {"layout_ms", tm.layout_ms}, {"checks_ms", tm.checks_ms},
                      {"kernel_table_ms", tm.kernel_table_ms}, {"rank_ops_ms", tm.rank_ops_ms}, {"pass1_ms", tm.pass1_ms}, {"host1_ms", tm.host1_ms}, {"pass2_ms", tm.pass2_ms},
                      {"host2_ms", tm.host2_ms}, {"pass3_ms", tm.pass3_ms}, {"total_ms", tm.total_ms},
                      {"kernel_keys", double(tm.kernel_keys)}, {"retries", double(tm.retries)}};

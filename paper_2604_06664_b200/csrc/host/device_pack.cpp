@@ -312,7 +312,8 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
                                    sizeof(fdt_node_attrs) * GN, 8ull * tslots, 8ull * tslots, 4ull * tslots,
                                    8ull * tslots, 8ull * tslots, 16, 4ull * NE, 8ull * NE, 4ull * NE, 4ull * NE,
                                    4ull * NE, 4ull * NE, 4ull * (nm + 1), name_bytes.size() + 1,
-                                   4ull * name_off.size(), 4ull * name_len.size()}));
+                                   4ull * name_off.size(), 4ull * name_len.size(),
+                                   size_t(std::min<uint64_t>(tslots, uint64_t(TN) + NE + 1)) * FDY_PACK_KEY_BYTES}));
     FdyPackArgs a{};
     a.graphs = d_graphs;
     a.graphs_bytes = gsize;
@@ -347,6 +348,8 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     a.tuniq = s1.take<uint32_t>(tslots);
     a.upos = s1.take<unsigned long long>(tslots);
     a.uoff = s1.take<uint64_t>(tslots);
+    const uint32_t key_cap = std::min<uint32_t>(tslots, TN + NE + 1);  // distinct keys <= key uses
+    a.ukey = s1.take<unsigned char>(size_t(key_cap) * FDY_PACK_KEY_BYTES);
     auto* d_small = s1.take<uint32_t>(4);  // ucount, flags
     a.pe_slot = s1.take<uint32_t>(NE);
     a.pe_node = d_pe_node;
@@ -430,6 +433,10 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     tm.kernel_keys = nu;
     d2h(upos, a.upos, nu, st);
     d2h(uoff, a.uoff, nu, st);
+    PinnedLease ukeys(dev, std::max<size_t>(size_t(nu) * FDY_PACK_KEY_BYTES, 16));
+    if (nu)
+        cuda_check(cudaMemcpyAsync(ukeys.data(), a.ukey, size_t(nu) * FDY_PACK_KEY_BYTES, cudaMemcpyDeviceToHost, st),
+                   "GPU pack D2H");
     // status | cap | rep_attrs | node_off: one copy into pinned memory
     unsigned char* const back_lo = reinterpret_cast<unsigned char*>(d_status);
     PinnedLease back(dev, size_t(back_end - back_lo));
@@ -530,18 +537,19 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     std::vector<uint32_t> ukidx(nu, kNoKernel);
     for (uint32_t k = 0; k < nu; ++k) {
         const uint32_t u = order[k];
-        const uint32_t m = uint32_t(upos[u] >> 32), local = uint32_t(upos[u]);
-        const NodeView v{G + uoff[u]};  // the node, or the stub node of a real comm kernel
+        const uint8_t* r = ukeys.data() + size_t(u) * FDY_PACK_KEY_BYTES;  // hash | fattrs | nl | name
         fdt_kernel& K = kernels[k];
-        std::string_view name = v.name();
-        K.binary_hash = v.hash();
-        if (local >= n_nodes[m]) {
-            name = name_list[pe_real_name[entry_base[m] + (local - n_nodes[m])]];
-            K.binary_hash = manifest.comm_real_hash;
+        const uint32_t nl = rd32(r + 32);
+        std::string_view name(reinterpret_cast<const char*>(r + 36), std::min<uint32_t>(nl, FDY_PACK_KEY_NAME));
+        if (nl > FDY_PACK_KEY_NAME) {  // a long name: from the host copy (node) or the name table (entry)
+            const uint32_t m = uint32_t(upos[u] >> 32), local = uint32_t(upos[u]);
+            name = local < n_nodes[m] ? NodeView{G + uoff[u]}.name()
+                                      : name_list[pe_real_name[entry_base[m] + (local - n_nodes[m])]];
         }
+        K.binary_hash = rd64(r);
         K.name_off = static_cast<uint32_t>(strings.size());
         K.name_len = static_cast<uint32_t>(name.size());
-        std::memcpy(K.func_attrs, v.fattrs(), 24);
+        std::memcpy(K.func_attrs, r + 8, 24);
         strings.append(name);
         ukidx[u] = k;
     }
@@ -586,7 +594,9 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
             const uint32_t gi0 = gnode_base[member_group[m]];
             const uint64_t desc = g_desc[member_group[m]];
             auto& ops = rops_of[m];
-            for (const PatchEntryView& e : patches.find(label)) {
+            const auto entries = patches.find(label);
+            ops.reserve(entries.size() * 4);
+            for (const PatchEntryView& e : entries) {
                 const uint64_t blob = desc + blob_off[gi0 + e.node_id];
                 for (uint32_t i = 0; i < e.n_rank; ++i)
                     store_detail::emit_write(ops, blob + e.rank_offset(i), 8, FDT_ROP_RANK, 0);
@@ -598,8 +608,9 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
                 for (const CommSlot& c : sit->second)
                     store_detail::emit_write(ops, desc + blob_off[gi0 + c.node_id] + c.offset, c.width,
                                              FDT_ROP_VALUE, c.value_index);
-            std::stable_sort(ops.begin(), ops.end(),
-                             [](const fdt_rank_op& x, const fdt_rank_op& y) { return x.chunk < y.chunk; });
+            const auto by_chunk = [](const fdt_rank_op& x, const fdt_rank_op& y) { return x.chunk < y.chunk; };
+            if (!std::is_sorted(ops.begin(), ops.end(), by_chunk))  // entries usually come in node order
+                std::stable_sort(ops.begin(), ops.end(), by_chunk);
         });
     }
     tm.host1_ms = ms_of(t0);
@@ -795,7 +806,15 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     h.n_diffs = static_cast<uint32_t>(n_diffs);
     h.n_rank_ops = static_cast<uint32_t>(rops.size());
     h.source_graphs_crc = verified_graphs_crc ? *verified_graphs_crc : digests[0];
-    h.source_patch_crc = crc64(patch_bin);
+    // a caller that verified graphs.bin verified every input against the manifest
+    const auto digest_of = [&](const char* rel, std::span<const uint8_t> bytes) {
+        if (verified_graphs_crc) {
+            auto it = manifest.file_digests.find(rel);
+            if (it != manifest.file_digests.end()) return it->second;
+        }
+        return crc64(bytes);
+    };
+    h.source_patch_crc = digest_of("patch.bin", patch_bin);
     h.old_base = manifest.allocator.base;
     h.final_offset = manifest.final_offset;
     h.real_comm_hash = manifest.comm_real_hash;
@@ -803,7 +822,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     h.total_nodes = total_nodes;
     h.n_plain_tiles = n_plain;
     h.n_values = slots.empty() ? 0u : slots.n_values;
-    h.source_slots_crc = slots_bin.empty() ? 0ull : crc64(slots_bin);
+    h.source_slots_crc = slots_bin.empty() ? 0ull : digest_of("comm_slots.bin", slots_bin);
 
     // section layout, in the offline packer's order
     uint64_t at = sizeof(fdt_header);
@@ -829,6 +848,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     place(FDT_SEC_STRINGS, strings.size());
     const uint64_t blob_bytes = (at + kSectionAlign - 1) / kSectionAlign * kSectionAlign;
 
+    tm.layout_ms = ms_of(t0) - tm.tiles_ms;
     DevicePackResult out;
     out.host_bytes.reset(new uint8_t[blob_bytes]);  // not zeroed: every byte is written below
     out.host_size = blob_bytes;

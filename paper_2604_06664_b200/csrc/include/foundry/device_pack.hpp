@@ -25,6 +25,7 @@ struct DevicePackTimings {
     double pass2_ms = 0;  // images + diff counts
     double host2_ms = 0;  // tile table, host sections
     double tiles_ms = 0;  // of which: the tile table and shared rank-op ranges
+    double layout_ms = 0; //           header and section layout
     double pass3_ms = 0;  // diff writes + template images + D2H of the device sections
     double total_ms = 0;
     uint32_t kernel_keys = 0;  // distinct kernel keys the GPU table found
@@ -47,7 +48,8 @@ struct DevicePackResult {
 // patch_view: patch_bin already being parsed (parse_patch_view) on another
 // thread while graphs.bin streamed in; its errors surface here.
 // verified_graphs_crc: graphs.bin's digest when the caller has already checked
-// it (LOAD's integrity pass); otherwise the GPU computes it for the header.
+// it and the other inputs against the manifest (LOAD's integrity pass); the
+// header then takes the manifest digests; otherwise they are computed.
 // graphs_host / d_graphs: graphs.bin on the host and in HBM (the device copy
 // is read by the kernels; the host copy only for per-group and per-kernel
 // metadata and, on error paths, to re-derive the reference's exact message for

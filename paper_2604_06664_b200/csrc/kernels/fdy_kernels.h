@@ -82,6 +82,12 @@ enum : uint32_t {
     FDY_PACK_PATCH = 4u,   // a patch entry / comm slot fails apply_rank_patches' checks
 };
 
+// A compacted kernel key as the host reads it back: binary hash u64 @0, func
+// attrs 6 x i32 @8, name length u32 @32, name bytes @36 (only the first
+// FDY_PACK_KEY_NAME bytes; longer names are read from the host copy).
+#define FDY_PACK_KEY_BYTES 128u
+#define FDY_PACK_KEY_NAME (FDY_PACK_KEY_BYTES - 36u)
+
 struct FdyPackArgs {
     const unsigned char* graphs;  // graphs.bin in HBM
     uint64_t graphs_bytes;
@@ -115,6 +121,7 @@ struct FdyPackArgs {
     uint64_t seed;
     unsigned long long* upos;     // compacted: first position of each key
     uint64_t* uoff;               //            absolute graphs.bin offset of that node
+    unsigned char* ukey;          //            its key bytes, FDY_PACK_KEY_BYTES each (see below)
     uint32_t* ucount;
     const uint32_t* ukidx;        // pass 2: compacted index -> store kernel index
     // patch entries (apply_rank_patches), flattened in member order

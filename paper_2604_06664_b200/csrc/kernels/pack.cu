@@ -416,6 +416,14 @@ __global__ void __launch_bounds__(kThreads) pack_compact_kernel(const FdyPackArg
             a.upos[u] = pos;
             a.uoff[u] = a.rec_off[m] + a.node_off[gn];
             a.tuniq[s] = u;
+            // the key's bytes, so the host builds the kernel table from one
+            // contiguous read-back instead of 9,000 scattered ones
+            const KeyParts k = key_at(a, pos);
+            unsigned char* r = a.ukey + uint64_t(u) * FDY_PACK_KEY_BYTES;
+            *reinterpret_cast<uint64_t*>(r) = k.hash;
+            for (int i = 0; i < 24; ++i) r[8 + i] = k.fa[i];
+            *reinterpret_cast<uint32_t*>(r + 32) = k.nl;
+            for (uint32_t i = 0; i < k.nl && i < FDY_PACK_KEY_NAME; ++i) r[36 + i] = k.name[i];
         }
     }
 }
