@@ -222,3 +222,47 @@ def test_errors_match_the_offline_packer(foundry, load, oracle, archives, tmp_pa
     locs = fndg.locators(bytes(raw))
     _commit(arch, m, bytes(raw), locs, crc)
     assert "checksum failure in graph record for label %d" % victim in _errors(foundry, load, arch)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_gpu_pack_randomized_members(foundry, archives, oracle, tmp_path, seed):
+    """Randomized rewrites of every member of a moe-spmd archive (topology kept):
+    kernel names of 5..305 characters (keys longer than the GPU's 92-byte key
+    record take the host path; node headers straddle the walk's 8 KiB
+    windows), argument blocks of 1 B .. 40 KB (ragged, with u64 lanes inside
+    and outside the captured VA range), grids, shared memory, func attrs and
+    memcpy / memset records varied per member; patch-entry stubs untouched.
+    The GPU-built store equals the offline packer's byte for byte."""
+    import random
+    src, _ = archives("moe-spmd", b200=False)
+    m = manifest(src)
+    base, span = m["allocator"]["base"], m["allocator"]["final_offset"]
+    stubs = fndg.patch_nodes(open(os.path.join(src, "patch.bin"), "rb").read())
+    r = random.Random(seed)
+    names = ["k%d_%s" % (i, "n" * r.choice([0, 3, 40, 86, 87, 88, 300])) for i in range(48)]
+
+    def edit(graphs):
+        for g in graphs:
+            keep = set(stubs.get(g.label, []))
+            for n in g.nodes:
+                if n.type == 0 and n.id not in keep:
+                    if r.random() < 0.5:
+                        n.name = r.choice(names)
+                    if r.random() < 0.5:
+                        size = r.choice([1, 7, 8, 9, 16, 24, 100, 416, 1720, 3001] + [40000] * (r.random() < 0.01))
+                        b = bytearray(r.randbytes(size))
+                        for off in range(0, size - 7, 8):
+                            if r.random() < 0.3:
+                                struct.pack_into("<Q", b, off, base + r.randrange(0, span, 8))
+                        n.args = bytes(b)
+                    if r.random() < 0.3:
+                        n.grid = (r.randint(1, 9), r.randint(1, 9), 1)
+                    if r.random() < 0.2:
+                        n.shmem = r.randint(0, 99999)
+                    if r.random() < 0.2:
+                        n.fattrs = struct.pack("<6i", *[r.randint(-1, 9) for _ in range(6)])
+                elif n.type in (1, 2) and r.random() < 0.3:
+                    n.mem = (base + r.randrange(0, span, 16), r.randrange(0, 1 << 64), r.randint(1, 4096))
+
+    arch = _rewrite(src, str(tmp_path / "random"), oracle.crc64, edit)
+    _same_store(foundry, arch)
