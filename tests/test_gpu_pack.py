@@ -232,7 +232,8 @@ def test_gpu_pack_randomized_members(foundry, archives, oracle, tmp_path, seed):
     windows), argument blocks of 1 B .. 40 KB (ragged, with u64 lanes inside
     and outside the captured VA range), grids, shared memory, func attrs and
     memcpy / memset records varied per member; patch-entry stubs untouched.
-    The GPU-built store equals the offline packer's byte for byte."""
+    The GPU-built store equals the offline packer's byte for byte, and the
+    fused kernel over it equals the oracle for a random (rank, world, delta)."""
     import random
     src, _ = archives("moe-spmd", b200=False)
     m = manifest(src)
@@ -266,3 +267,25 @@ def test_gpu_pack_randomized_members(foundry, archives, oracle, tmp_path, seed):
 
     arch = _rewrite(src, str(tmp_path / "random"), oracle.crc64, edit)
     _same_store(foundry, arch)
+    # and the fused kernel over that store (random rank / world / relocation)
+    # equals the oracle's PrepareFn + relocation for every member
+    from paper_2604_06664_b200 import capi
+    blob, _ = foundry._foundry._pack_store_bytes(arch, True)
+    open(os.path.join(arch, "templates.fdt"), "wb").write(blob)  # read by the decoder only
+    api = capi.CApi()
+    dev = api.device_open(0)
+    store = api.store_upload(dev, blob)
+    try:
+        world = r.choice([1, 2, 4, 8])
+        rank = r.randrange(world)
+        delta = r.choice([0, 0x10000, 0x10000000000, 0x10000 * r.randrange(1, 1 << 20)])
+        members, _ = api.materialize(dev, store, rank, world, base + delta if delta else 0)
+        try:
+            got = foundry._foundry._decode_member_images(arch, api.members_download(members))
+        finally:
+            api.lib.fdy_members_free(members)
+        want, _ = oracle.materialize_archive(arch, rank, world, delta)
+        assert got == want, (rank, world, hex(delta))
+    finally:
+        api.lib.fdy_store_free(store)
+        api.lib.fdy_device_close(dev)
