@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <array>
 #include <exception>
+#include <future>
 #include <chrono>
 #include <cstring>
 #include <map>
@@ -586,8 +587,12 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     // rank ops (apply_rank_patches' rank / world writes, then comm slots as
     // value ops), per member in table order, stably sorted by chunk; the stub
     // -> real kernel swap is the GPU's (pack_swaps_kernel)
+    // They need only the layouts, so they run on host threads while pass 2
+    // runs on the GPU.
     std::vector<std::vector<fdt_rank_op>> rops_of(nm);
-    if (NE || !slots.empty()) {
+    std::future<void> rops_done = std::async(std::launch::async, [&] {
+        const auto t_r = Clock::now();
+        if (!NE && slots.empty()) return;
         parallel_for(nm, 0, [&](size_t mi) {
             const uint32_t m = static_cast<uint32_t>(mi);
             const uint32_t label = loc_of[m]->label;
@@ -612,22 +617,23 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
             if (!std::is_sorted(ops.begin(), ops.end(), by_chunk))  // entries usually come in node order
                 std::stable_sort(ops.begin(), ops.end(), by_chunk);
         });
-    }
+        tm.rank_ops_ms = ms_of(t_r);
+    });
     tm.host1_ms = ms_of(t0);
-    tm.rank_ops_ms = tm.host1_ms - before_rops;
+    (void)before_rops;
 
     // ------------------------------------------------ pass 2
     t0 = Clock::now();
     Scratch s2(dev, Scratch::need({4ull * GN, 8ull * nm, 4ull * nm, 8ull * n_groups, 4ull * std::max(nu, 1u),
                                    4ull * n_tiles, 4ull * n_tiles, n_tiles, 4ull * n_tiles, arena_bytes,
                                    arena_bytes / 16}));
-    auto* d_blob_off = s2.take<uint32_t>(GN);
+    auto* d_blob_off = s2.take<uint32_t>(GN);  // uploaded: one contiguous range
     auto* d_out_off = s2.take<uint64_t>(nm);
     auto* d_tile_base = s2.take<uint32_t>(nm);
     auto* d_g_image = s2.take<uint64_t>(n_groups);
     auto* d_ukidx = s2.take<uint32_t>(std::max(nu, 1u));
     auto* d_tile_member = s2.take<uint32_t>(n_tiles);
-    a.tile_count = s2.take<uint32_t>(n_tiles);
+    a.tile_count = s2.take<uint32_t>(n_tiles);  // read back: one contiguous range
     a.tile_reloc = s2.take<uint8_t>(n_tiles);
     auto* d_diff_lo = s2.take<uint32_t>(n_tiles);
     a.arena = s2.take<unsigned char>(arena_bytes);
@@ -640,18 +646,24 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     a.tile_member = d_tile_member;
     a.diff_lo = d_diff_lo;
     a.n_tiles = n_tiles;
-    h2d(d_blob_off, blob_off, st);
-    h2d(d_out_off, out_off, st);
-    h2d(d_tile_base, tile_base, st);
-    h2d(d_g_image, g_image, st);
-    h2d(d_ukidx, ukidx, st);
-    h2d(d_tile_member, tile_member, st);
+    Upload up2;
+    up2.add(d_blob_off, blob_off);
+    up2.add(d_out_off, out_off);
+    up2.add(d_tile_base, tile_base);
+    up2.add(d_g_image, g_image);
+    up2.add(d_ukidx, ukidx);
+    up2.add(d_tile_member, tile_member);
+    up2.send(dev, st);
     cuda_check(fdy_launch_pack_pass2(&a, st), "GPU pack pass 2");
-    std::vector<uint32_t> tile_count;
-    std::vector<uint8_t> tile_reloc;
-    d2h(tile_count, a.tile_count, n_tiles, st);
-    d2h(tile_reloc, a.tile_reloc, n_tiles, st);
+    const auto* back2_lo = reinterpret_cast<const unsigned char*>(a.tile_count);
+    const size_t back2_bytes = size_t(reinterpret_cast<const unsigned char*>(a.tile_reloc + n_tiles) - back2_lo);
+    PinnedLease back2(dev, std::max<size_t>(back2_bytes, 16));
+    if (n_tiles)
+        cuda_check(cudaMemcpyAsync(back2.data(), back2_lo, back2_bytes, cudaMemcpyDeviceToHost, st), "GPU pack D2H");
     cuda_check(cudaStreamSynchronize(st), "GPU pack pass 2");
+    const uint32_t* tile_count = reinterpret_cast<const uint32_t*>(back2.data());
+    const uint8_t* tile_reloc = back2.data() + (reinterpret_cast<const unsigned char*>(a.tile_reloc) - back2_lo);
+    rops_done.get();  // rank ops (host threads) joined: they ran alongside pass 2
     tm.pass2_ms = ms_of(t0);
 
     // ------------------------------------------------ host: tables and sections
