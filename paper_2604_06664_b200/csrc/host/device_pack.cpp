@@ -310,7 +310,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     auto t0 = Clock::now();
     Scratch s1(dev, Scratch::need({8ull * nm, 8ull * nm, 4ull * nm, 4ull * nm, 4ull * nm, 4ull * nm, 4ull * nm,
                                    4ull * n_groups, 4ull * n_groups, 4ull * TN, 4ull * TN, 4ull * TN, 4ull * GN,
-                                   sizeof(fdt_node_attrs) * GN, 8ull * tslots, 8ull * tslots, 4ull * tslots,
+                                   sizeof(fdt_node_attrs) * GN, GN, 8ull * tslots, 8ull * tslots, 4ull * tslots,
                                    8ull * tslots, 8ull * tslots, 16, 4ull * NE, 8ull * NE, 4ull * NE, 4ull * NE,
                                    4ull * NE, 4ull * NE, 4ull * (nm + 1), name_bytes.size() + 1,
                                    4ull * name_off.size(), 4ull * name_len.size(),
@@ -340,6 +340,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     auto* d_status = s1.take<uint32_t>(nm);
     a.cap = s1.take<uint32_t>(GN);
     a.rep_attrs = s1.take<fdt_node_attrs>(GN);
+    a.rep_type = s1.take<uint8_t>(GN);
     a.node_off = s1.take<uint32_t>(TN);
     unsigned char* const back_end = reinterpret_cast<unsigned char*>(a.node_off + TN);
     a.node_member = s1.take<uint32_t>(TN);
@@ -448,6 +449,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     const uint32_t* cap = reinterpret_cast<const uint32_t*>(host_of(a.cap));
     const fdt_node_attrs* rep_attrs = reinterpret_cast<const fdt_node_attrs*>(host_of(a.rep_attrs));
     const uint32_t* node_off = reinterpret_cast<const uint32_t*>(host_of(a.node_off));
+    const uint8_t* rep_type = host_of(a.rep_type);
     {
         const auto parts = crc64_device(dev, d_graphs, segs);  // synchronizes the stream
         digests.assign(1 + nm, 0);
@@ -703,7 +705,7 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
         Sink k;
         k.u64(N);
         for (uint32_t n = 0; n < N; ++n) {
-            const uint8_t t = node_ptr(rep, n)[0];
+            const uint8_t t = rep_type[gnode_base[g] + n];  // read back with the attributes
             k.u8(t);
             if (t == 0) {
                 const fdt_node_attrs& at = rep_attrs[gnode_base[g] + n];

@@ -112,6 +112,7 @@ struct FdyPackArgs {
     uint32_t* cap;                // max over the group of round16(blob length)
     const uint32_t* blob_off;     // pass 2: slot offset in the pool
     fdt_node_attrs* rep_attrs;    // the representative's launch attributes
+    uint8_t* rep_type;            // the representative's node types
     // kernel table: open addressing over 64-bit key fingerprints
     unsigned long long* tkey;     // 0 = empty slot
     unsigned long long* tpos;     // min over the key's nodes of (member << 32 | node)

@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(kThreads) pack_fields_kernel(const FdyPackArgs
                 at.attr_query = q[25] != 0;
             }
             a.rep_attrs[gi] = at;
+            a.rep_type[gi] = t;
         }
     }
 }
