@@ -1,6 +1,7 @@
 // C-ABI, kernel layer (declarations and reference anchors: include/foundry_b200.h).
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -124,6 +125,12 @@ int fdy_store_fanout(const fdy_store* src, fdy_device* dst_dev, fdy_store** out)
 namespace {
 
 constexpr uint64_t kChainChunk = 2ull << 20;
+// a link gives up on a predecessor that publishes nothing for this long (per
+// chunk; FOUNDRY_CHAIN_TIMEOUT_MS overrides, for tests)
+uint64_t chain_timeout_ns() {
+    if (const char* v = std::getenv("FOUNDRY_CHAIN_TIMEOUT_MS")) return std::strtoull(v, nullptr, 10) * 1000000ull;
+    return 60ull * 1000 * 1000 * 1000;
+}
 
 void enable_peer(Device& d, Device& s) {
     if (d.ordinal() == s.ordinal()) return;
@@ -213,6 +220,7 @@ struct fdy_chain {
     void* upstream = nullptr;  // opened IPC mapping of the previous link
     bool fed = false;
     uint32_t* progress() { return reinterpret_cast<uint32_t*>(buf.data() + progress_off); }
+    uint32_t* failed() { return progress() + 1; }  // set by a wait that timed out
     ~fdy_chain() {
         if (upstream) {
             dev->dev->make_current();
@@ -270,9 +278,11 @@ int fdy_chain_pull(fdy_chain* c, const unsigned char upstream[64]) {
         cuda_check(cudaIpcOpenMemHandle(&c->upstream, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
         const auto* up = static_cast<const unsigned char*>(c->upstream);
         const auto* up_progress = reinterpret_cast<const uint32_t*>(up + c->progress_off);
+        const uint64_t timeout = chain_timeout_ns();
         for (uint32_t k = 0; k < c->nchunks; ++k) {
             const uint64_t off = uint64_t(k) * c->chunk, len = std::min(c->chunk, c->bytes - off);
-            cuda_check(fdy_launch_chain_wait(up_progress, k + 1, d.stream()), "chain wait");
+            cuda_check(fdy_launch_chain_wait(up_progress, k + 1, timeout, c->failed(), d.stream()),
+                       "chain wait");
             cuda_check(cudaMemcpyAsync(c->buf.data() + off, up + off, len, cudaMemcpyDeviceToDevice, d.stream()),
                        "cudaMemcpyAsync(chain link)");
             cuda_check(fdy_launch_chain_publish(c->progress(), k + 1, d.stream()), "chain publish");
@@ -291,6 +301,10 @@ int fdy_chain_finish(fdy_chain* c, fdy_store** out) {
             cuda_check(cudaIpcCloseMemHandle(c->upstream), "cudaIpcCloseMemHandle");
             c->upstream = nullptr;
         }
+        uint32_t failed = 0;
+        cuda_check(cudaMemcpy(&failed, c->failed(), sizeof failed, cudaMemcpyDeviceToHost), "chain status D2H");
+        require(failed == 0, Errc::cuda_error,
+                "chain fan-out: the predecessor published no progress within the timeout (did its process exit?)");
         fdt_header hdr;
         cuda_check(cudaMemcpy(&hdr, c->buf.data(), sizeof hdr, cudaMemcpyDeviceToHost), "store header D2H");
         auto o = std::make_unique<fdy_store>();

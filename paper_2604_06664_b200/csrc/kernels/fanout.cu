@@ -19,11 +19,21 @@ __global__ void chain_publish_kernel(uint32_t* progress, uint32_t value) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(progress), "r"(value) : "memory");
 }
 
-__global__ void chain_wait_kernel(const uint32_t* progress, uint32_t value) {
+// Gives up after timeout_ns (a predecessor that died must not hang this GPU's
+// stream): it then sets *failed, and the link's finish reports it.
+__global__ void chain_wait_kernel(const uint32_t* progress, uint32_t value, uint64_t timeout_ns,
+                                  uint32_t* failed) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     uint32_t v = 0;
     for (;;) {
         asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(progress) : "memory");
         if (v >= value) break;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > timeout_ns) {
+            atomicExch(failed, 1u);
+            break;
+        }
         __nanosleep(256);
     }
 }
@@ -35,7 +45,8 @@ extern "C" cudaError_t fdy_launch_chain_publish(uint32_t* progress, uint32_t val
     return cudaGetLastError();
 }
 
-extern "C" cudaError_t fdy_launch_chain_wait(const uint32_t* progress, uint32_t value, cudaStream_t stream) {
-    chain_wait_kernel<<<1, 1, 0, stream>>>(progress, value);
+extern "C" cudaError_t fdy_launch_chain_wait(const uint32_t* progress, uint32_t value, uint64_t timeout_ns,
+                                             uint32_t* failed, cudaStream_t stream) {
+    chain_wait_kernel<<<1, 1, 0, stream>>>(progress, value, timeout_ns, failed);
     return cudaGetLastError();
 }

@@ -186,7 +186,9 @@ cudaError_t fdy_launch_pack_pass3(const FdyPackArgs* args, cudaStream_t stream);
 // system scope) after everything before it on `stream`; hold `stream` until a
 // (possibly peer-mapped) progress word reaches `value`.
 cudaError_t fdy_launch_chain_publish(uint32_t* progress, uint32_t value, cudaStream_t stream);
-cudaError_t fdy_launch_chain_wait(const uint32_t* progress, uint32_t value, cudaStream_t stream);
+// (gives up after timeout_ns, setting *failed)
+cudaError_t fdy_launch_chain_wait(const uint32_t* progress, uint32_t value, uint64_t timeout_ns,
+                                  uint32_t* failed, cudaStream_t stream);
 
 // per device: x^(2^k) mod P and the constant-multiplier nibble tables built from them
 cudaError_t fdy_crc64_set_constants(const uint64_t* x2k64);
