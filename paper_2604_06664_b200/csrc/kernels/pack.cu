@@ -480,16 +480,29 @@ __global__ void __launch_bounds__(kThreads) pack_images_kernel(const FdyPackArgs
         const uint64_t pool = 48ull * N + boff;
         const uint32_t chunks = cap / 16;
         for (uint32_t j = lane; j < chunks; j += 32) {
-            uint32_t w[4];
+            // the chunk's 16 source bytes start anywhere: five aligned 32-bit
+            // loads and funnel shifts (lanes read consecutive words), bytes
+            // past the blob zeroed; the buffer is padded, so the last word may
+            // run past the record
+            uint32_t w[4] = {0u, 0u, 0u, 0u};
+            if (16 * j < blob_len) {
+                const uintptr_t at = reinterpret_cast<uintptr_t>(src + 16 * j);
+                const uint32_t* wp = reinterpret_cast<const uint32_t*>(at & ~uintptr_t(3));
+                const uint32_t sh = uint32_t(at & 3u) * 8u;
+                uint32_t r[5];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                uint32_t v = 0;
+                for (int k = 0; k < 5; ++k) r[k] = __ldg(wp + k);
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const uint32_t at = 16 * j + 4 * k + b;
-                    if (at < blob_len) v |= uint32_t(src[at]) << (8 * b);
+                for (int k = 0; k < 4; ++k) w[k] = __funnelshift_r(r[k], r[k + 1], sh);
+                const uint32_t valid = blob_len - 16 * j;  // bytes of this chunk inside the blob
+                if (valid < 16) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t lo = 4u * k;
+                        if (valid <= lo) w[k] = 0u;
+                        else if (valid < lo + 4) w[k] &= (1u << (8 * (valid - lo))) - 1u;
+                    }
                 }
-                w[k] = v;
             }
             *reinterpret_cast<uint4*>(img + pool + 16ull * j) = make_uint4(w[0], w[1], w[2], w[3]);
             uint8_t f = 0;
