@@ -585,7 +585,6 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
     }
     const uint32_t n_tiles = static_cast<uint32_t>(tile_member.size());
 
-    const double before_rops = ms_of(t0);
     // rank ops (apply_rank_patches' rank / world writes, then comm slots as
     // value ops), per member in table order, stably sorted by chunk; the stub
     // -> real kernel swap is the GPU's (pack_swaps_kernel)
@@ -622,7 +621,6 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
         tm.rank_ops_ms = ms_of(t_r);
     });
     tm.host1_ms = ms_of(t0);
-    (void)before_rops;
 
     // ------------------------------------------------ pass 2
     t0 = Clock::now();
