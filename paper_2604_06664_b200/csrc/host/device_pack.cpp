@@ -238,11 +238,15 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
         pe_stub_name.resize(ne);
         pe_real_name.resize(ne);
         pe_need.resize(ne);
-        for (uint32_t m = 0; m < nm; ++m)  // the distinct names, in first-use order
-            for (const PatchEntryView& e : entries_of[m].first(std::min<size_t>(entries_of[m].size(), 64))) {
+        // the distinct names (a handful), seen on the first few patched members;
+        // any other name goes through the fix-up below
+        for (uint32_t m = 0, seen = 0; m < nm && seen < 4; ++m) {
+            for (const PatchEntryView& e : entries_of[m]) {
                 intern(e.stub_name);
                 intern(e.real_name);
             }
+            seen += entries_of[m].empty() ? 0 : 1;
+        }
         // the name table is frozen during the parallel fill: a name the scan
         // above did not see leaves the member for a sequential fix-up
         std::vector<uint8_t> unnamed(nm, 0);
