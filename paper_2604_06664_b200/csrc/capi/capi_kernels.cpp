@@ -262,7 +262,7 @@ int fdy_chain_seed(fdy_chain* c, const void* host_blob) {
             const uint64_t off = uint64_t(k) * c->chunk, len = std::min(c->chunk, c->bytes - off);
             cuda_check(cudaMemcpyAsync(c->buf.data() + off, src + off, len, cudaMemcpyHostToDevice, d.stream()),
                        "cudaMemcpyAsync(chain seed)");
-            cuda_check(fdy_launch_chain_publish(c->progress(), k + 1, d.stream()), "chain publish");
+            cuda_check(fdy_launch_chain_publish(c->progress(), k + 1, nullptr, d.stream()), "chain publish");
         }
         c->fed = true;
     });
@@ -285,7 +285,7 @@ int fdy_chain_pull(fdy_chain* c, const unsigned char upstream[64]) {
                        "chain wait");
             cuda_check(cudaMemcpyAsync(c->buf.data() + off, up + off, len, cudaMemcpyDeviceToDevice, d.stream()),
                        "cudaMemcpyAsync(chain link)");
-            cuda_check(fdy_launch_chain_publish(c->progress(), k + 1, d.stream()), "chain publish");
+            cuda_check(fdy_launch_chain_publish(c->progress(), k + 1, c->failed(), d.stream()), "chain publish");
         }
         c->fed = true;
     });

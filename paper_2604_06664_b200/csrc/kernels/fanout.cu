@@ -14,7 +14,10 @@
 
 namespace {
 
-__global__ void chain_publish_kernel(uint32_t* progress, uint32_t value) {
+// A link whose wait gave up (failed set) publishes nothing more, so the links
+// after it give up too instead of forwarding what it never received.
+__global__ void chain_publish_kernel(uint32_t* progress, uint32_t value, const uint32_t* failed) {
+    if (failed && *reinterpret_cast<const volatile uint32_t*>(failed)) return;
     __threadfence_system();
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(progress), "r"(value) : "memory");
 }
@@ -23,6 +26,7 @@ __global__ void chain_publish_kernel(uint32_t* progress, uint32_t value) {
 // stream): it then sets *failed, and the link's finish reports it.
 __global__ void chain_wait_kernel(const uint32_t* progress, uint32_t value, uint64_t timeout_ns,
                                   uint32_t* failed) {
+    if (*reinterpret_cast<volatile uint32_t*>(failed)) return;  // an earlier chunk already gave up
     uint64_t t0, t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     uint32_t v = 0;
@@ -40,8 +44,9 @@ __global__ void chain_wait_kernel(const uint32_t* progress, uint32_t value, uint
 
 }  // namespace
 
-extern "C" cudaError_t fdy_launch_chain_publish(uint32_t* progress, uint32_t value, cudaStream_t stream) {
-    chain_publish_kernel<<<1, 1, 0, stream>>>(progress, value);
+extern "C" cudaError_t fdy_launch_chain_publish(uint32_t* progress, uint32_t value, const uint32_t* failed,
+                                                cudaStream_t stream) {
+    chain_publish_kernel<<<1, 1, 0, stream>>>(progress, value, failed);
     return cudaGetLastError();
 }
 

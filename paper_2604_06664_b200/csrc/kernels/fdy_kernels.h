@@ -185,7 +185,9 @@ cudaError_t fdy_launch_pack_pass3(const FdyPackArgs* args, cudaStream_t stream);
 // Chain fan-out (fanout.cu): publish `value` to a progress word (release,
 // system scope) after everything before it on `stream`; hold `stream` until a
 // (possibly peer-mapped) progress word reaches `value`.
-cudaError_t fdy_launch_chain_publish(uint32_t* progress, uint32_t value, cudaStream_t stream);
+// (not when *failed is set: a link that gave up stops forwarding; failed may be null)
+cudaError_t fdy_launch_chain_publish(uint32_t* progress, uint32_t value, const uint32_t* failed,
+                                     cudaStream_t stream);
 // (gives up after timeout_ns, setting *failed)
 cudaError_t fdy_launch_chain_wait(const uint32_t* progress, uint32_t value, uint64_t timeout_ns,
                                   uint32_t* failed, cudaStream_t stream);

@@ -1,8 +1,9 @@
 """Worker of test_gpu_capi.py::test_chain_link_times_out_on_a_silent_predecessor:
-rank 0 creates a chain link and never seeds it; rank 1 pulls from it with a
-short timeout and must get the timeout error from fdy_chain_finish.
+rank 0 creates a chain link and never seeds it; rank r > 0 pulls from rank
+r - 1 with a short timeout, and every one of them must get the timeout error
+from fdy_chain_finish (a link that gave up does not forward).
 
-    RANK=r WORLD_SIZE=2 MASTER_ADDR=127.0.0.1 MASTER_PORT=p python chain_timeout_worker.py
+    RANK=r WORLD_SIZE=n MASTER_ADDR=127.0.0.1 MASTER_PORT=p python chain_timeout_worker.py
 """
 from __future__ import annotations
 
@@ -24,15 +25,15 @@ def main() -> int:
     chain, handle = api.chain_create(dev, 1 << 20)
     handles = g.all_gather_object(handle)
     rc = 0
-    if g.rank == 1:
+    if g.rank > 0:
         os.environ["FOUNDRY_CHAIN_TIMEOUT_MS"] = "1500"
-        api.chain_pull(chain, handles[0])
+        api.chain_pull(chain, handles[g.rank - 1])
         try:
             api.chain_finish(chain)
             rc = 3  # should have timed out
         except capi.CApiError as e:
             rc = 0 if "no progress" in str(e) else 4
-    g.barrier()  # rank 0 keeps its (never seeded) link alive until rank 1 is done
+    g.barrier()  # every link stays alive until its successor is done
     if g.rank == 0:
         api.lib.fdy_chain_free(chain)
     api.lib.fdy_device_close(dev)

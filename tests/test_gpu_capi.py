@@ -248,15 +248,16 @@ def test_chain_fanout_between_three_processes(foundry, oracle, archives, tmp_pat
 def test_chain_link_times_out_on_a_silent_predecessor(tmp_path):
     """A chain link whose predecessor never publishes gives up after the
     timeout (the GPU's wait kernel stops polling) and fdy_chain_finish raises,
-    instead of hanging its GPU's stream."""
+    instead of hanging its GPU's stream; the link after it gives up as well
+    (a link that gave up forwards nothing)."""
     port = _free_port()
     procs = []
-    for rank in range(2):
+    for rank in range(3):
         env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
-                   WORLD_SIZE="2", LOCAL_RANK=str(rank))
+                   WORLD_SIZE="3", LOCAL_RANK=str(rank))
         procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "chain_timeout_worker.py")],
                                       env=env))
-    assert [p.wait(timeout=300) for p in procs] == [0, 0]
+    assert [p.wait(timeout=300) for p in procs] == [0, 0, 0]
 
 
 @pytest.mark.parametrize("chunk", [0, 4096 + 16])
