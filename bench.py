@@ -294,8 +294,9 @@ def cold_process_load(args, local: int, samples: int = 5) -> dict:
     creation + LOAD, stamped when the CLI's flushed "ready" line arrives),
     per-template execs and share_execs, next to a fresh process that only
     creates the CUDA context (`fdy_tool cuda-init`). The three kinds run
-    interleaved, `samples` rounds, so drift of the box hits all of them alike;
-    median and range per kind. `device_open_ms` / `load_ms` split the LOAD
+    interleaved, `samples` rounds in a rotating order with a 1 s settle before
+    each process, so drift of the box and the previous process's teardown hit
+    all of them alike; median and range per kind. `device_open_ms` / `load_ms` split the LOAD
     process at its device-open stamp (FOUNDRY_DEBUG timeline); the CLI asks
     the kernel to read the archive ahead (posix_fadvise) before it creates
     the context. `process_exit` adds the teardown (graphs, libraries, context)."""
@@ -313,8 +314,14 @@ def cold_process_load(args, local: int, samples: int = 5) -> dict:
     exits = {k: [] for k in runs}
     opens = {k: [] for k in runs}
     env = dict(os.environ, FOUNDRY_DEBUG="1")
-    for _ in range(samples):
-        for name, cmd in runs.items():
+    names = list(runs)
+    for r in range(samples):
+        # rotate the order each round and let the driver finish tearing down
+        # the previous process first: a context created right after a heavy
+        # process exits is slower, whichever kind it belongs to
+        for name in names[r % len(names):] + names[:r % len(names)]:
+            cmd = runs[name]
+            time.sleep(1.0)
             t0 = time.perf_counter()
             p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, env=env)
             t_ready = None
