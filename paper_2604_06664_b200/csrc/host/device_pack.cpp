@@ -1057,7 +1057,14 @@ DevicePackResult pack_template_store_device(Device& dev, std::span<const uint8_t
                                             std::future<PatchView>* patch_view) {
     DevicePacker packer(dev, graphs_host, d_graphs, patch_bin, manifest, slots_bin, full_host_copy,
                         verified_graphs_crc, patch_view);
-    return packer.run(stats, timings);
+    try {
+        return packer.run(stats, timings);
+    } catch (...) {
+        // copies into the packer's pinned leases may still be in flight: they
+        // must land before the leases go back to the pool
+        cudaStreamSynchronize(dev.stream());
+        throw;
+    }
 }
 
 std::vector<uint8_t> pack_archive_store_device(Device& dev, const std::filesystem::path& archive,
