@@ -28,6 +28,7 @@ JSON keys beyond the base contract:
 from __future__ import annotations
 
 import argparse
+import ctypes
 import hashlib
 import json
 import os
@@ -522,6 +523,19 @@ def main():
         barrier()
         reloc_ms = reduce_max(statistics.mean(r for r, _ in split))
         member_ms = reduce_max(statistics.mean(m for _, m in split))
+        # what writing an output of this size alone takes on this GPU (the
+        # member pass is write-dominated: 147 MB written, ~17 MB read), same
+        # protocol (L2 flushed, CUDA events): a plain st.global.v4 fill of the
+        # same arena (fdy_members_write_probe, measurement only); the arena is
+        # re-materialized afterwards
+        fill_times = []
+        for _ in range(args.steps):
+            flush_l2()
+            fms = ctypes.c_float()
+            api.check(api.lib.fdy_members_write_probe(members, ctypes.byref(fms)))
+            fill_times.append(fms.value)
+        write_ceiling_ms = reduce_max(statistics.mean(fill_times))
+        api.materialize(dev, store, wrank, TP_WORLD, base + delta, members)
 
         # the same on a model-shaped (tier-S) arena of the headline set: 1720-byte
         # GEMM-like argument blocks make the member images ~330 MB (SURVEY §8(d):
@@ -698,6 +712,11 @@ def main():
                      # launch moved, over the same event time: below `frac` when part of
                      # the output is still dirty in the 126 MB L2 when the kernel ends
                      "frac_dram": (traffic / (member_ms * 1e-3) / 1e9 / peak) if traffic else None,
+                     # a plain fill of the member-image size on the same GPU, same
+                     # protocol: the write-only floor of a launch this size
+                     "write_ceiling": {"ms": write_ceiling_ms, "bytes": hdr["members_image_bytes"],
+                                       "gbps": hdr["members_image_bytes"] / (write_ceiling_ms * 1e-3) / 1e9,
+                                       "member_pass_over_write_floor": member_ms / write_ceiling_ms},
                      "algorithmic_bytes": alg["member_pass"],
                      "kernel": "fdy_materialize_kernel (member pass: K2 diff + K1 relocated lanes + "
                                "K3 rank patch), CUDA events around it alone, L2 flushed",

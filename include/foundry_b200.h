@@ -149,6 +149,11 @@ int fdy_materialize_into(fdy_device* dev, const fdy_store* store,
  * events on the device stream; blocks). Same output. */
 int fdy_materialize_timed_split(fdy_device* dev, const fdy_store* store, const fdy_materialize_desc* desc,
                                 fdy_members* members, float* reloc_ms, float* member_ms);
+/* Measurement only (bench.py's roofline): overwrites the arena with a plain
+ * st.global.v4 fill and returns its CUDA-event duration — the floor a kernel
+ * writing this many bytes reaches on this GPU. The arena holds no member
+ * images afterwards. */
+int fdy_members_write_probe(fdy_members* members, float* ms);
 size_t fdy_members_bytes(const fdy_members* members);
 int fdy_members_download(fdy_members* members, void* host_dst, size_t offset, size_t bytes);
 void fdy_members_free(fdy_members* members);

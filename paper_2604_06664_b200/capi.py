@@ -106,6 +106,7 @@ class CApi:
                                       ctypes.POINTER(ctypes.c_float)]
         L.fdy_materialize_into.argtypes = [P, P, ctypes.POINTER(MaterializeDesc), P,
                                            ctypes.POINTER(ctypes.c_float)]
+        L.fdy_members_write_probe.argtypes = [P, ctypes.POINTER(ctypes.c_float)]
         L.fdy_members_bytes.argtypes = [P]
         L.fdy_members_bytes.restype = ctypes.c_size_t
         L.fdy_members_download.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t]

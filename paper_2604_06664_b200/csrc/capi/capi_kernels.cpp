@@ -447,6 +447,25 @@ int fdy_materialize_timed_split(fdy_device* dev, const fdy_store* store, const f
     });
 }
 
+int fdy_members_write_probe(fdy_members* m, float* ms) {
+    return fdy_guard([&] {
+        require(m && ms, Errc::invalid_argument, "fdy_members_write_probe: null argument");
+        Device& d = *m->owner->dev;
+        d.make_current();
+        m->generation = g_generation.fetch_add(1);  // the arena no longer holds member images
+        cudaEvent_t e0, e1;
+        cuda_check(cudaEventCreate(&e0), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&e1), "cudaEventCreate");
+        cuda_check(cudaEventRecord(e0, d.stream()), "cudaEventRecord");
+        cuda_check(fdy_launch_write_probe(m->out.data(), m->out.size(), d.stream()), "write probe launch");
+        cuda_check(cudaEventRecord(e1, d.stream()), "cudaEventRecord");
+        cuda_check(cudaEventSynchronize(e1), "cudaEventSynchronize");
+        cuda_check(cudaEventElapsedTime(ms, e0, e1), "cudaEventElapsedTime");
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    });
+}
+
 size_t fdy_members_bytes(const fdy_members* m) { return m ? m->out.size() : 0; }
 
 int fdy_members_download(fdy_members* m, void* host_dst, size_t offset, size_t bytes) {

@@ -165,6 +165,8 @@ size_t fdy_materialize_smem_bytes();
 // A one-thread kernel that holds `stream` for `ns` ns (see materialize.cu).
 cudaError_t fdy_launch_gate(cudaStream_t stream, uint64_t ns);
 cudaError_t fdy_materialize_occupancy(int* blocks_per_sm);
+// Measurement only: st.global.v4 fill of `bytes` at out (SMs x 8 CTAs).
+cudaError_t fdy_launch_write_probe(unsigned char* out, uint64_t bytes, cudaStream_t stream);
 // Measurement variant: relocation grid, then `between` recorded, then the member
 // grid as an ordinary launch (events time the member pass alone).
 cudaError_t fdy_launch_materialize_split(const FdyMaterializeArgs* args, int grid, cudaStream_t stream,

@@ -345,6 +345,15 @@ __global__ void fdy_gate_kernel(uint64_t ns) {
     } while (t - t0 < ns);
 }
 
+// Measurement only: a plain st.global.v4 fill of an output buffer, the floor
+// any kernel writing that many bytes reaches on this GPU (the member pass is
+// write-dominated). Not used on any product path.
+__global__ void __launch_bounds__(256) fdy_write_probe_kernel(uint4* out, uint64_t n) {
+    const uint4 v = make_uint4(0x46445750u, 1u, 2u, 3u);
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = v;
+}
+
 cudaError_t set_smem_attribute_once() {
     static std::once_flag once[64];
     static cudaError_t result[64];
@@ -367,6 +376,14 @@ extern "C" cudaError_t fdy_launch_gate(cudaStream_t stream, uint64_t ns) {
 }
 
 extern "C" size_t fdy_materialize_smem_bytes() { return sizeof(Smem); }
+
+extern "C" cudaError_t fdy_launch_write_probe(unsigned char* out, uint64_t bytes, cudaStream_t stream) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (bytes >= 16) fdy_write_probe_kernel<<<sms * 8, 256, 0, stream>>>(reinterpret_cast<uint4*>(out), bytes / 16);
+    return cudaGetLastError();
+}
 
 extern "C" cudaError_t fdy_launch_materialize(const FdyMaterializeArgs* args, int grid,
                                               cudaStream_t stream) {
