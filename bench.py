@@ -294,7 +294,8 @@ def cold_process_load(args, local: int, samples: int = 5) -> dict:
     `foundry load --archive <headline> --rank 0 --world 8` (CUDA context
     creation + LOAD, stamped when the CLI's flushed "ready" line arrives),
     per-template execs and share_execs, next to a fresh process that only
-    creates the CUDA context (`fdy_tool cuda-init`). The three kinds run
+    creates the CUDA context (`fdy_tool cuda-init`, stamped at its own 'ready'
+    line once the context exists, like the LOAD processes). The three kinds run
     interleaved, `samples` rounds in a rotating order with a 1 s settle before
     each process, so drift of the box and the previous process's teardown hit
     all of them alike; median and range per kind. `device_open_ms` / `load_ms` split the LOAD

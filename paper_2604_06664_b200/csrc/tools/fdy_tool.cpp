@@ -817,6 +817,10 @@ int main(int argc, char** argv) {
         if (cmd == "cuda-init") {  // fresh-process floor: create the device context, nothing else
             fdy_device* d = nullptr;
             if (fdy_device_open(argc > 2 ? std::atoi(argv[2]) : 0, &d)) return 1;
+            // stamped like the CLI's LOAD (bench.py cold_process_load): the context
+            // exists here; the teardown after it is process exit
+            std::printf("cuda-init ready: device open\n");
+            std::fflush(stdout);
             fdy_device_close(d);
             return 0;
         }
