@@ -115,6 +115,51 @@ PinnedLease& PinnedLease::operator=(PinnedLease&& o) noexcept {
     return *this;
 }
 
+// ------------------------------------------------------------------ pageable pool
+
+namespace {
+std::mutex g_pageable_mu;
+std::vector<std::pair<unsigned char*, size_t>> g_pageable;
+}  // namespace
+
+PageableLease::PageableLease(size_t bytes) {
+    {
+        std::lock_guard lock(g_pageable_mu);
+        size_t best = g_pageable.size();
+        for (size_t i = 0; i < g_pageable.size(); ++i)
+            if (g_pageable[i].second >= bytes && (best == g_pageable.size() || g_pageable[i].second < g_pageable[best].second))
+                best = i;
+        if (best < g_pageable.size()) {
+            p_ = g_pageable[best].first;
+            cap_ = g_pageable[best].second;
+            g_pageable.erase(g_pageable.begin() + static_cast<long>(best));
+            return;
+        }
+    }
+    cap_ = std::max<size_t>(bytes, 1 << 20);
+    p_ = new unsigned char[cap_];
+}
+
+PageableLease::~PageableLease() {
+    if (!p_) return;
+    std::lock_guard lock(g_pageable_mu);
+    g_pageable.push_back({p_, cap_});
+}
+
+PageableLease& PageableLease::operator=(PageableLease&& o) noexcept {
+    if (this != &o) {
+        if (p_) {
+            std::lock_guard lock(g_pageable_mu);
+            g_pageable.push_back({p_, cap_});
+        }
+        p_ = o.p_;
+        cap_ = o.cap_;
+        o.p_ = nullptr;
+        o.cap_ = 0;
+    }
+    return *this;
+}
+
 // ------------------------------------------------------------------ staging
 
 namespace {
@@ -210,9 +255,12 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const std::vecto
     for (size_t i = 0; i < order_.size(); ++i) {
         StagedFile& f = files_.at(order_[i]->rel);
         f.segment = static_cast<uint32_t>(i);
-        if (f.placement != Placement::hash) {
-            f.offset = total_;
-            total_ += (f.length + kAlign - 1) / kAlign * kAlign;
+        if (f.placement == Placement::device) {
+            f.offset = device_bytes_;
+            device_bytes_ += (f.length + kAlign - 1) / kAlign * kAlign;
+        } else if (f.placement == Placement::host) {
+            f.offset = host_bytes_;
+            host_bytes_ += (f.length + kAlign - 1) / kAlign * kAlign;
         }
         if (f.placement == Placement::device) {
             f.dseg = static_cast<uint32_t>(seg_first.size());
@@ -224,7 +272,6 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const std::vecto
             require(f.n_blocks <= kCrcMaxSegmentBlocks, Errc::invalid_argument, f.rel + ": longer than 64 GiB");
             seg_first.push_back(f.first_block);
             seg_count.push_back(f.n_blocks);
-            device_bytes_ = total_;
         } else {
             f.first_piece = n_pieces;
             f.n_pieces = static_cast<uint32_t>((f.length + kPiece - 1) / kPiece);
@@ -233,7 +280,9 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const std::vecto
     }
     const size_t nb = blocks.size(), nd = seg_first.size(), ns = order_.size();
     trace_point("  staging: layout", sh_->t0);
-    host_ = PinnedLease(dev, std::max<uint64_t>(total_, 16));
+    total_ = device_bytes_ + host_bytes_;
+    host_ = PinnedLease(dev, std::max<uint64_t>(device_bytes_, 16));  // only what the DMA reads is pinned
+    pageable_ = PageableLease(std::max<uint64_t>(host_bytes_, 16));
     device_ = DeviceBuffer(dev, std::max<uint64_t>(device_bytes_, 16));
     // GPU CRC scratch: block table | first | count | (align 8) crc | len | digests
     const size_t table = nb * sizeof(FdyCrcBlock), plan_bytes = table + 2 * nd * 4;
@@ -312,6 +361,7 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const std::vecto
     trace_point("  staging: buffers + CRC plan", sh_->t0);
     auto next = std::make_shared<std::atomic<size_t>>(0);
     unsigned char* hbase = host_.data();
+    unsigned char* pbase = pageable_.data();
     unsigned char* dbase = device_.data();
     const int ordinal = dev.ordinal();
     const fs::path dir = root;  // the lanes outlive this constructor
@@ -344,7 +394,7 @@ StagedArchive::StagedArchive(Device& dev, const fs::path& root, const std::vecto
                     ::close(fd);
                     piece_crc = c.value();
                 } else {
-                    unsigned char* h = hbase + f.offset + pc.off;
+                    unsigned char* h = (f.placement == Placement::device ? hbase : pbase) + f.offset + pc.off;
                     read_range(dir / f.rel, h, pc.off, pc.len);
                     if (f.placement == Placement::host) piece_crc = crc64(h, pc.len);
                 }
@@ -461,7 +511,7 @@ std::span<const uint8_t> StagedArchive::host(const std::string& rel) const {
     const StagedFile& f = file(rel);
     require(f.placement != Placement::hash, Errc::invalid_argument, rel + " was hashed, not kept in host memory");
     wait_ready(f);
-    return {host_.data() + f.offset, f.length};
+    return {(f.placement == Placement::device ? host_.data() : pageable_.data()) + f.offset, f.length};
 }
 
 const unsigned char* StagedArchive::device(const std::string& rel) const {

@@ -46,11 +46,27 @@ private:
     int device_ = -1;
 };
 
+// Pageable host memory leased from a per-process pool (the host-kept files'
+// staging: no pinning cost, no page faults once warm); returns on destruction.
+class PageableLease {
+public:
+    PageableLease() = default;
+    explicit PageableLease(size_t bytes);
+    ~PageableLease();
+    PageableLease(PageableLease&& o) noexcept { *this = std::move(o); }
+    PageableLease& operator=(PageableLease&& o) noexcept;
+    unsigned char* data() const { return p_; }
+
+private:
+    unsigned char* p_ = nullptr;
+    size_t cap_ = 0;
+};
+
 // Where a staged file goes. Every file is CRC-64/XZ-checked against the
 // manifest; only the template store needs to be in HBM.
 enum class Placement : uint8_t {
     device,  // pinned host copy + DMA to HBM; CRC on the GPU as its pieces land
-    host,    // pinned host copy (the caller parses it); CRC on the host per piece
+    host,    // pageable host copy (the caller parses it); CRC on the host per piece
     hash,    // not kept: read through a per-lane scratch, CRC on the host
 };
 
@@ -65,7 +81,7 @@ struct StagePlan {
 
 struct StagedFile {
     std::string rel;
-    uint64_t offset = 0;  // in host staging and in device staging (device / host files)
+    uint64_t offset = 0;  // device files: in pinned and device staging; host files: in pageable staging
     uint64_t length = 0;
     uint32_t segment = 0;  // index in staging order
     Placement placement = Placement::hash;
@@ -140,12 +156,14 @@ private:
     Device& dev_;
     std::map<std::string, StagedFile> files_;
     std::vector<const StagedFile*> order_;  // staging order
-    PinnedLease host_;
+    PinnedLease host_;         // device files' pinned copies (the DMA source)
+    PageableLease pageable_;   // host files (never DMAed: no pinning)
     DeviceBuffer device_;
     DeviceBuffer crc_;  // block table | block crc | block len | seg first | seg count | digests
     PinnedLease digests_;
     uint64_t total_ = 0;         // staged (device + host) bytes
-    uint64_t device_bytes_ = 0;  // of which DMAed to HBM
+    uint64_t device_bytes_ = 0;  // of which DMAed to HBM (pinned)
+    uint64_t host_bytes_ = 0;    // of which host-kept (pageable)
     std::unique_ptr<Shared> sh_;
 };
 
