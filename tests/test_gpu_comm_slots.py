@@ -43,9 +43,9 @@ def dev(api):
     api.lib.fdy_device_close(d)
 
 
-def slotted(foundry, archives, tmp_path, table_fn, name="moe-spmd"):
-    arch, _ = archives(name)
-    copy = str(tmp_path / (name + "-slots"))
+def slotted(foundry, archives, tmp_path, table_fn, name="moe-spmd", b200=True):
+    arch, _ = archives(name, b200=b200)
+    copy = str(tmp_path / (name + ("-slots" if b200 else "-plain-slots")))
     shutil.copytree(arch, copy)
     foundry.write_comm_slots(copy, comm_slots.N_VALUES, table_fn(copy))
     return copy
@@ -101,12 +101,14 @@ def test_prepare_archive_applies_the_value_table(foundry, oracle, archives, api,
     assert got == want
 
 
-@pytest.mark.parametrize("share", [False, True])
-def test_load_with_comm_values_replays_like_the_oracle(foundry, load, oracle, archives, tmp_path, share):
+@pytest.mark.parametrize("share,b200", [(False, True), (True, True), (False, False)])
+def test_load_with_comm_values_replays_like_the_oracle(foundry, load, oracle, archives, tmp_path, share, b200):
     """LOAD with LoadOptions.comm_values: the deploy table puts a peer buffer
     (a mapped region address, so the device dereference succeeds) at buf@16 and
-    a comm handle over payload@24; every replayed trace equals the oracle's."""
-    arch = slotted(foundry, archives, tmp_path, comm_slots.deploy_table)
+    a comm handle over payload@24; every replayed trace equals the oracle's.
+    b200=False: the archive in the reference's layout plus comm_slots.bin, so
+    the GPU packer turns the slots into value ops at LOAD."""
+    arch = slotted(foundry, archives, tmp_path, comm_slots.deploy_table, b200=b200)
     base = manifest(arch)["allocator"]["base"]
     rank = 3
     vals = comm_slots.rank_values(rank, base)
