@@ -9,6 +9,7 @@
 
 #include "../kernels/fdy_kernels.h"
 #include "foundry/hash.hpp"
+#include "foundry/staging.hpp"
 
 namespace foundry {
 
@@ -340,6 +341,58 @@ std::vector<uint64_t> crc64_device(Device& dev, const unsigned char* d_base,
         cudaEventDestroy(e1);
     }
     return out;
+}
+
+void CrcJob::launch(Device& dev, const unsigned char* d_base, std::span<const Segment> segments) {
+    dev.make_current();
+    dev_ = &dev;
+    ns_ = segments.size();
+    size_t nb = 0;
+    for (const Segment& g : segments) nb += (g.length + kCrcBlockBytes - 1) / kCrcBlockBytes;
+    // plan in pinned memory (one async copy): block table | first | count
+    const size_t plan_bytes = nb * sizeof(FdyCrcBlock) + 8 * ns_;
+    plan_ = PinnedLease(dev, std::max<size_t>(plan_bytes, 16));
+    out_ = PinnedLease(dev, std::max<size_t>(8 * ns_, 16));
+    auto* blocks = reinterpret_cast<FdyCrcBlock*>(plan_.data());
+    auto* first = reinterpret_cast<uint32_t*>(plan_.data() + nb * sizeof(FdyCrcBlock));
+    auto* count = first + ns_;
+    uint32_t b = 0;
+    for (size_t s = 0; s < ns_; ++s) {
+        first[s] = b;
+        for (uint64_t off = 0; off < segments[s].length; off += kCrcBlockBytes) {
+            FdyCrcBlock& k = blocks[b++];
+            k = FdyCrcBlock{};
+            k.segment = static_cast<uint32_t>(s);
+            k.length = static_cast<uint32_t>(std::min<uint64_t>(kCrcBlockBytes, segments[s].length - off));
+            k.offset = segments[s].offset + off;
+        }
+        count[s] = b - first[s];
+        require(count[s] <= kCrcMaxSegmentBlocks, Errc::invalid_argument, "CRC segment longer than 64 GiB");
+    }
+    // device scratch: plan | crc | len | out
+    const size_t dev_bytes = (plan_bytes + 15) / 16 * 16 + 2 * nb * 8 + ns_ * 8 + 64;
+    scratch_ = DeviceBuffer(dev, dev_bytes);
+    unsigned char* p = scratch_.data();
+    auto* d_blocks = reinterpret_cast<FdyCrcBlock*>(p);
+    auto* d_first = reinterpret_cast<uint32_t*>(p + nb * sizeof(FdyCrcBlock));
+    auto* d_count = d_first + ns_;
+    p += (plan_bytes + 15) / 16 * 16;
+    auto* d_crc = reinterpret_cast<uint64_t*>(p);
+    auto* d_len = d_crc + nb;
+    auto* d_out = d_len + nb;
+    cudaStream_t st = dev.stream();
+    if (plan_bytes)
+        cuda_check(cudaMemcpyAsync(scratch_.data(), plan_.data(), plan_bytes, cudaMemcpyHostToDevice, st),
+                   "H2D crc plan");
+    cuda_check(fdy_launch_crc64(d_base, d_blocks, static_cast<uint32_t>(nb), d_first, d_count,
+                                static_cast<uint32_t>(ns_), d_crc, d_len, d_out, st),
+               "crc64 kernel launch");
+    if (ns_) cuda_check(cudaMemcpyAsync(out_.data(), d_out, ns_ * 8, cudaMemcpyDeviceToHost, st), "D2H crc");
+}
+
+std::span<const uint64_t> CrcJob::wait() {
+    if (dev_) cuda_check(cudaStreamSynchronize(dev_->stream()), "cudaStreamSynchronize(crc)");
+    return digests();
 }
 
 }  // namespace foundry

@@ -461,6 +461,11 @@ private:
             segs.push_back({rec_off_[m], head});
             segs.push_back({rec_off_[m] + head, rec_len_[m] - head});
         }
+        crc_.launch(dev_, d_graphs_, segs);  // ahead of pass 1 on the stream: one sync covers both
+        // status | cap | rep_attrs | rep_type | node_off: one copy into pinned memory,
+        // read back with the key count
+        unsigned char* const back_lo = reinterpret_cast<unsigned char*>(d_status);
+        back_ = PinnedLease(dev_, size_t(back_end - back_lo));
         std::vector<uint32_t> small;
         for (uint32_t attempt = 0;; ++attempt) {
             a.seed = 0x46445450ull + 0x9E3779B97F4A7C15ull * attempt;  // "FDTP"
@@ -472,6 +477,8 @@ private:
             cuda_check(cudaMemsetAsync(d_small, 0, 16, st_), "GPU pack memset");
             cuda_check(fdy_launch_pack_pass1(&a, st_), "GPU pack pass 1");
             d2h(small, d_small, 2, st_);
+            cuda_check(cudaMemcpyAsync(back_.data(), back_lo, size_t(back_end - back_lo), cudaMemcpyDeviceToHost, st_),
+                       "GPU pack D2H");
             cuda_check(cudaStreamSynchronize(st_), "GPU pack pass 1");
             if (small[1] == 0) break;
             require(attempt < 4, Errc::cuda_error, "GPU pack: kernel key fingerprints keep colliding");
@@ -486,11 +493,7 @@ private:
             cuda_check(cudaMemcpyAsync(ukeys_.data(), a.ukey, size_t(nu_) * FDY_PACK_KEY_BYTES,
                                        cudaMemcpyDeviceToHost, st_),
                        "GPU pack D2H");
-        // status | cap | rep_attrs | rep_type | node_off: one copy into pinned memory
-        unsigned char* const back_lo = reinterpret_cast<unsigned char*>(d_status);
-        back_ = PinnedLease(dev_, size_t(back_end - back_lo));
-        cuda_check(cudaMemcpyAsync(back_.data(), back_lo, size_t(back_end - back_lo), cudaMemcpyDeviceToHost, st_),
-                   "GPU pack D2H");
+        cuda_check(cudaStreamSynchronize(st_), "GPU pack pass 1 keys");
         auto host_of = [&](const void* d) {
             return back_.data() + (static_cast<const unsigned char*>(d) - back_lo);
         };
@@ -499,7 +502,7 @@ private:
         rep_attrs_ = reinterpret_cast<const fdt_node_attrs*>(host_of(a.rep_attrs));
         rep_type_ = host_of(a.rep_type);
         node_off_ = reinterpret_cast<const uint32_t*>(host_of(a.node_off));
-        const auto parts = crc64_device(dev_, d_graphs_, segs);  // synchronizes the stream
+        const auto parts = crc_.digests();  // launched ahead of pass 1: complete
         digests_.assign(1 + nm, 0);
         digests_[0] = parts[0];
         for (uint32_t m = 0; m < nm; ++m)
@@ -581,13 +584,14 @@ private:
     // order, where a graph's patch entries' real comm kernels follow its nodes
     // (the GPU table holds both; positions order them)
     void build_kernel_table() {
-        std::vector<uint32_t> order(nu_);
-        for (uint32_t u = 0; u < nu_; ++u) order[u] = u;
-        std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return upos_[x] < upos_[y]; });
+        std::vector<std::pair<unsigned long long, uint32_t>> order(nu_);  // positions are unique
+        for (uint32_t u = 0; u < nu_; ++u) order[u] = {upos_[u], u};
+        std::sort(order.begin(), order.end());
         kernels_.assign(nu_, fdt_kernel{});
         ukidx_.assign(nu_, kNoKernel);
+        strings_.reserve(size_t(nu_) * 48);
         for (uint32_t k = 0; k < nu_; ++k) {
-            const uint32_t u = order[k];
+            const uint32_t u = order[k].second;
             const uint8_t* r = ukeys_.data() + size_t(u) * FDY_PACK_KEY_BYTES;  // hash | fattrs | nl | name
             fdt_kernel& K = kernels_[k];
             const uint32_t nl = rd32(r + 32);
@@ -732,22 +736,35 @@ private:
         groups_.assign(n_groups_, fdt_group{});
         members_.assign(nm_, fdt_member{});
         const auto& groups_in = manifest_.grouping.groups;
+        // section offsets first (prefix sums), then every group's attributes, edges
+        // and topology key on host threads
+        size_t n_attrs = 0, n_edge_words = 0;
         for (uint32_t g = 0; g < n_groups_; ++g) {
-            const uint32_t rep = group_rep_[g], N = n_nodes_[rep], E = n_edges_[rep];
+            const uint32_t rep = group_rep_[g];
             fdt_group& Gp = groups_[g];
             Gp.image_bytes = g_image_[g];
-            Gp.n_nodes = N;
-            Gp.n_edges = E;
+            Gp.n_nodes = n_nodes_[rep];
+            Gp.n_edges = n_edges_[rep];
             Gp.first_member = group_first_[g];
             Gp.n_members = group_end(g) - group_first_[g];
             Gp.representative = groups_in[g].representative;
-            Gp.attrs_first = static_cast<uint32_t>(attrs_.size());
-            Gp.edges_off = edges_.size() * sizeof(uint32_t);
-            attrs_.insert(attrs_.end(), rep_attrs_ + gnode_base_[g], rep_attrs_ + gnode_base_[g + 1]);
+            Gp.attrs_first = static_cast<uint32_t>(n_attrs);
+            Gp.edges_off = n_edge_words * sizeof(uint32_t);
+            n_attrs += gnode_base_[g + 1] - gnode_base_[g];
+            n_edge_words += 2ull * Gp.n_edges;
+            timages_bytes_ = (timages_bytes_ + 15) / 16 * 16;
+            Gp.timage_off = timages_bytes_;  // TIMAGES-relative until rebased
+            timages_bytes_ += g_image_[g];
+        }
+        attrs_.resize(n_attrs);
+        edges_.resize(n_edge_words);
+        parallel_for(n_groups_, 0, [&](size_t gi) {
+            const uint32_t g = static_cast<uint32_t>(gi);
+            fdt_group& Gp = groups_[g];
+            const uint32_t rep = group_rep_[g], N = Gp.n_nodes, E = Gp.n_edges;
+            std::copy(rep_attrs_ + gnode_base_[g], rep_attrs_ + gnode_base_[g + 1], attrs_.begin() + Gp.attrs_first);
             const uint8_t* etab = G_ + rec_off_[rep] + rec_len_[rep] - 8ull * E;
-            const size_t e0 = edges_.size();
-            edges_.resize(e0 + 2ull * E);
-            std::memcpy(edges_.data() + e0, etab, 8ull * E);
+            if (E) std::memcpy(edges_.data() + Gp.edges_off / sizeof(uint32_t), etab, 8ull * E);
             // topology key of the representative (topology_key, graph_model.cpp)
             Sink k;
             k.u64(N);
@@ -770,10 +787,7 @@ private:
             const Digest128 key = murmur3_x64_128(k.bytes().data(), k.size(), 0x464E4447ull);
             Gp.key_hi = key.hi;
             Gp.key_lo = key.lo;
-            timages_bytes_ = (timages_bytes_ + 15) / 16 * 16;
-            Gp.timage_off = timages_bytes_;  // TIMAGES-relative until rebased
-            timages_bytes_ += g_image_[g];
-        }
+        });
         // members' tiles, group by group on host threads: rank-op ranges are shared
         // per (group, tile index), so each group builds its own op list, which are
         // then concatenated in group order (the offline packer's single list)
@@ -844,11 +858,12 @@ private:
             }
         }
         // relocation-free template tiles first (stable), as the offline packer orders them
-        std::vector<fdt_tile> plain, rest;
-        for (uint32_t t = 0; t < n_tiles_; ++t) (tile_reloc_[t] ? rest : plain).push_back(tiles_[t]);
-        n_plain_ = static_cast<uint32_t>(plain.size());
-        plain.insert(plain.end(), rest.begin(), rest.end());
-        tiles_ = std::move(plain);
+        uint32_t n_plain = 0;
+        for (uint32_t t = 0; t < n_tiles_; ++t) n_plain += tile_reloc_[t] ? 0 : 1;
+        std::vector<fdt_tile> ordered(n_tiles_);
+        for (uint32_t t = 0, p = 0, r = n_plain; t < n_tiles_; ++t) ordered[tile_reloc_[t] ? r++ : p++] = tiles_[t];
+        n_plain_ = n_plain;
+        tiles_ = std::move(ordered);
     }
 
     // the header and the section layout, in the offline packer's order
@@ -1017,6 +1032,7 @@ private:
     std::vector<unsigned long long> upos_;
     std::vector<uint64_t> uoff_, digests_;
     PinnedLease ukeys_, back_;
+    CrcJob crc_;
     const uint32_t *status_ = nullptr, *cap_ = nullptr, *node_off_ = nullptr;
     const fdt_node_attrs* rep_attrs_ = nullptr;
     const uint8_t* rep_type_ = nullptr;

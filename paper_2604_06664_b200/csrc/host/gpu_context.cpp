@@ -409,6 +409,10 @@ void GpuContext::sync_trace_state() {
         d_cursor_ = reinterpret_cast<unsigned long long*>(trace_meta_.data() + 64);
         d_bitmap_ = reinterpret_cast<uint64_t*>(trace_meta_.data() + 128);
         bitmap_dirty_ = true;
+        // pool memory is not zeroed: a path that launches before any reset_trace
+        // (naive_rebuild_all) must not start from a stale cursor
+        cuda_check(cudaMemsetAsync(trace_meta_.data(), 0, 128, dev_.stream()), "trace meta reset");
+        cuda_check(cudaStreamSynchronize(dev_.stream()), "trace meta reset");
     }
     if (bitmap_dirty_) {
         fdy_trace_ctx h{};

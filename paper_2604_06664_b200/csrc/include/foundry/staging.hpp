@@ -46,6 +46,23 @@ private:
     int device_ = -1;
 };
 
+// crc64_device split: launch() enqueues the plan upload, the kernel and the digests'
+// read-back on dev.stream() and returns; digests() is valid once that stream has
+// been synchronized past the launch (by the caller or by wait()).
+class CrcJob {
+public:
+    CrcJob() = default;
+    void launch(Device& dev, const unsigned char* d_base, std::span<const Segment> segments);
+    std::span<const uint64_t> wait();  // synchronizes dev.stream()
+    std::span<const uint64_t> digests() const { return {reinterpret_cast<const uint64_t*>(out_.data()), ns_}; }
+
+private:
+    Device* dev_ = nullptr;
+    DeviceBuffer scratch_;
+    PinnedLease plan_, out_;
+    size_t ns_ = 0;
+};
+
 // Pageable host memory leased from a per-process pool (the host-kept files'
 // staging: no pinning cost, no page faults once warm); returns on destruction.
 class PageableLease {
