@@ -322,7 +322,7 @@ PYBIND11_MODULE(_foundry, m) {
                 DevicePackTimings tm;
                 out = pack_archive_store_device(dev, archive, &tm);
                 t = {{"prep_ms", tm.prep_ms}, {"patch_parse_ms", tm.patch_parse_ms}, {"tiles_ms", tm.tiles_ms}, {"layout_ms", tm.layout_ms}, {"checks_ms", tm.checks_ms},
-                     {"kernel_table_ms", tm.kernel_table_ms}, {"rank_ops_ms", tm.rank_ops_ms}, {"pass1_ms", tm.pass1_ms}, {"host1_ms", tm.host1_ms}, {"pass2_ms", tm.pass2_ms},
+                     {"kernel_table_ms", tm.kernel_table_ms}, {"rank_ops_ms", tm.rank_ops_ms}, {"pass1_ms", tm.pass1_ms}, {"pass1_upload_ms", tm.pass1_upload_ms}, {"pass1_launch_ms", tm.pass1_launch_ms}, {"pass1_sync_ms", tm.pass1_sync_ms}, {"host1_ms", tm.host1_ms}, {"pass2_ms", tm.pass2_ms},
                      {"host2_ms", tm.host2_ms}, {"pass3_ms", tm.pass3_ms}, {"total_ms", tm.total_ms},
                      {"kernel_keys", double(tm.kernel_keys)}, {"retries", double(tm.retries)}};
             }

@@ -94,7 +94,10 @@ public:
             hi = std::max(hi, it.dst + it.bytes);
         }
         lease_ = PinnedLease(dev, size_t(hi - lo));
-        for (const Item& it : items_) std::memcpy(lease_.data() + (it.dst - lo), it.src, it.bytes);
+        // the patch-entry arrays are a few MB: gathered on host threads
+        parallel_for(items_.size(), size_t(hi - lo) > (1u << 20) ? 0u : 1u, [&](size_t i) {
+            std::memcpy(lease_.data() + (items_[i].dst - lo), items_[i].src, items_[i].bytes);
+        });
         cuda_check(cudaMemcpyAsync(lo, lease_.data(), size_t(hi - lo), cudaMemcpyHostToDevice, st), "GPU pack H2D");
     }
 
@@ -162,11 +165,13 @@ public:
         t0 = Clock::now();
         check_errors();
         tm_.checks_ms = ms_of(t0);
-        build_kernel_table();
-        tm_.kernel_table_ms = ms_of(t0) - tm_.checks_ms;
         layout();
-        // rank ops need only the layouts: host threads build them while pass 2 runs
+        // rank ops need only the layouts: host threads build them while the
+        // kernel table is assembled and pass 2 runs
         std::future<void> rops_done = std::async(std::launch::async, [this] { build_rank_ops(); });
+        const auto tk = Clock::now();
+        build_kernel_table();
+        tm_.kernel_table_ms = ms_of(tk);
         tm_.host1_ms = ms_of(t0);
 
         t0 = Clock::now();
@@ -355,6 +360,7 @@ private:
     // ------------------------------------------------ pass 1
     void pass1() {
         const uint32_t nm = nm_, TN = TN_, GN = GN_, NE = NE_, tslots = tslots_;
+        const auto tp = Clock::now();
         s1_.emplace(dev_, Scratch::need({8ull * nm, 8ull * nm, 4ull * nm, 4ull * nm, 4ull * nm, 4ull * nm, 4ull * nm,
                                          4ull * n_groups_, 4ull * n_groups_, 4ull * TN, 4ull * TN, 4ull * TN,
                                          4ull * GN, sizeof(fdt_node_attrs) * GN, GN, 8ull * tslots, 8ull * tslots,
@@ -447,6 +453,7 @@ private:
         up1.add(d_name_off, name_off_);
         up1.add(d_name_len, name_len_);
         up1.send(dev_, st_);
+        const double t_up = ms_of(tp);
         // record CRCs (parse_graph_at's per-record check) and the whole file's
         // digest (the store header's source_graphs_crc), on the GPU; the whole
         // file only when the caller has not already verified it. A record rarely
@@ -462,6 +469,7 @@ private:
             segs.push_back({rec_off_[m] + head, rec_len_[m] - head});
         }
         crc_.launch(dev_, d_graphs_, segs);  // ahead of pass 1 on the stream: one sync covers both
+        const double t_crc = ms_of(tp);
         // status | cap | rep_attrs | rep_type | node_off: one copy into pinned memory,
         // read back with the key count
         unsigned char* const back_lo = reinterpret_cast<unsigned char*>(d_status);
@@ -480,6 +488,7 @@ private:
             cuda_check(cudaMemcpyAsync(back_.data(), back_lo, size_t(back_end - back_lo), cudaMemcpyDeviceToHost, st_),
                        "GPU pack D2H");
             cuda_check(cudaStreamSynchronize(st_), "GPU pack pass 1");
+            tm_.pass1_sync_ms = ms_of(tp);
             if (small[1] == 0) break;
             require(attempt < 4, Errc::cuda_error, "GPU pack: kernel key fingerprints keep colliding");
             ++tm_.retries;
@@ -494,6 +503,8 @@ private:
                                        cudaMemcpyDeviceToHost, st_),
                        "GPU pack D2H");
         cuda_check(cudaStreamSynchronize(st_), "GPU pack pass 1 keys");
+        tm_.pass1_upload_ms = t_up;
+        tm_.pass1_launch_ms = t_crc;
         auto host_of = [&](const void* d) {
             return back_.data() + (static_cast<const unsigned char*>(d) - back_lo);
         };

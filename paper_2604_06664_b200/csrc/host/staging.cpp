@@ -717,7 +717,12 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
     }
     std::future<PatchView> patch_view;
     try {
-        staged = std::make_unique<StagedArchive>(dev, root, manifest, lanes, &st, plan);
+        // a reference-written archive streams 188 MB where the store is 18 MB: with
+        // every lane reading, the patch-table parse and the packer's host threads
+        // lose their cores (tools/experiments/e2e_plain_timeline.py, 16-core host:
+        // 16 lanes 14.7-17.7 ms, 8 lanes 13.9-14.9 ms; the stream is PCIe-bound)
+        const unsigned stage_lanes = has_store ? lanes : std::max(4u, lanes / 2);
+        staged = std::make_unique<StagedArchive>(dev, root, manifest, stage_lanes, &st, plan);
         trace_point("staging started", t_all);
         if (!has_store && staged->has("patch.bin")) {
             // parse errors surface when the packer consumes it, after integrity
@@ -730,6 +735,7 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
     }
     const auto t1 = Clock::now();
     DevicePackResult gpu;              // reference-written archive: packed now, on the GPU
+    DevicePackTimings pack_t;
     std::span<const uint8_t> packed;   // its host copy
     DeviceStore store;
     if (has_store) {
@@ -745,9 +751,17 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
                                              staged->host("patch.bin"), manifest,
                                              staged->has("comm_slots.bin") ? staged->host("comm_slots.bin")
                                                                            : std::span<const uint8_t>{},
-                                             nullptr, nullptr, /*full_host_copy=*/keep != nullptr,
+                                             nullptr, &pack_t, /*full_host_copy=*/keep != nullptr,
                                              &manifest.file_digests.at("graphs.bin"),
                                              patch_view.valid() ? &patch_view : nullptr);
+            if (std::getenv("FOUNDRY_DEBUG"))
+                std::fprintf(stderr,
+                             "[foundry] pack phases: patch wait %.3f, prep %.3f, pass1 %.3f (uploaded %.3f, CRC queued %.3f, "
+                             "synced %.3f), host1 %.3f, pass2 %.3f (rank ops %.3f), host2 %.3f (tiles %.3f), pass3 %.3f, "
+                             "total %.3f ms\n",
+                             pack_t.patch_parse_ms, pack_t.prep_ms, pack_t.pass1_ms, pack_t.pass1_upload_ms,
+                             pack_t.pass1_launch_ms, pack_t.pass1_sync_ms, pack_t.host1_ms, pack_t.pass2_ms,
+                             pack_t.rank_ops_ms, pack_t.host2_ms, pack_t.tiles_ms, pack_t.pass3_ms, pack_t.total_ms);
         } catch (const Error&) {
             rethrow_in_step("template construction");
         }

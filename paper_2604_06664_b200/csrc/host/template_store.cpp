@@ -140,7 +140,8 @@ void emit_write(std::vector<fdt_rank_op>& ops, uint64_t at, uint32_t width, uint
         op.chunk = static_cast<uint32_t>(chunk);
         op.kind = kind;
         op.shift = static_cast<int8_t>(int64_t(at) - int64_t(chunk * 16));
-        for (uint64_t j = b; j < end; ++j) op.mask |= uint16_t(1u << (j - chunk * 16));
+        // bytes [b, end) of the chunk (at most 16)
+        op.mask = static_cast<uint16_t>(((1u << (end - b)) - 1u) << (b - chunk * 16));
         op.aux = aux;
         ops.push_back(op);
         b = end;
