@@ -82,6 +82,30 @@ def test_materialize_into_reuses_the_arena(foundry, oracle, archives, api, dev):
         api.lib.fdy_store_free(store)
 
 
+@pytest.mark.parametrize("name,rank,world,delta", [("micro", 0, 1, 0), ("moe-spmd", 3, 4, DELTAS[3])])
+def test_member_pass_writes_every_arena_byte(archives, api, dev, name, rank, world, delta):
+    """The member pass writes the arena with TMA bulk stores, which
+    compute-sanitizer initcheck does not model (tools/initcheck.sh flags every
+    D2H of the arena). Raw bytes, padding included: an arena filled with a
+    pattern (fdy_members_write_probe) and materialized again must equal the
+    first materialization byte for byte."""
+    arch, _ = archives(name)
+    blob = open(os.path.join(arch, "templates.fdt"), "rb").read()
+    base = manifest(arch)["allocator"]["base"]
+    store = api.store_upload(dev, blob)
+    members, _ = api.materialize(dev, store, rank, world, base + delta if delta else 0)
+    try:
+        first = api.members_download(members)
+        ms = ctypes.c_float()
+        api.check(api.lib.fdy_members_write_probe(members, ctypes.byref(ms)))
+        assert api.members_download(members) != first  # the pattern landed
+        api.materialize(dev, store, rank, world, base + delta if delta else 0, members)
+        assert api.members_download(members) == first
+    finally:
+        api.lib.fdy_members_free(members)
+        api.lib.fdy_store_free(store)
+
+
 def test_rank_outside_world_is_invalid_argument(archives, api, dev):
     from paper_2604_06664_b200.capi import CApiError
     arch, _ = archives("micro")
