@@ -289,3 +289,39 @@ def test_gpu_pack_randomized_members(foundry, archives, oracle, tmp_path, seed):
     finally:
         api.lib.fdy_store_free(store)
         api.lib.fdy_device_close(dev)
+
+
+@pytest.mark.parametrize("name,seed", [("micro", 0), ("micro", 1), ("moe-spmd", 2), ("moe-spmd", 3)])
+def test_gpu_pack_byte_flip_fuzz(foundry, archives, oracle, tmp_path, name, seed):
+    """Random byte flips inside member records (record checksums, locators and
+    the file digest kept consistent, so only the decoder / packer can object):
+    the GPU packer either builds the offline packer's exact store or raises its
+    exact error, for every mutation."""
+    import random
+    src, _ = archives(name, b200=False)
+    raw = open(os.path.join(src, "graphs.bin"), "rb").read()
+    locs = fndg.locators(raw)
+    r = random.Random(1000 + seed + 7919 * int(os.environ.get("FOUNDRY_FUZZ_ROUND", "0")))
+    outcomes = {"store": 0, "error": 0}
+    for i in range(int(os.environ.get("FOUNDRY_FUZZ_N", "24"))):
+        label, _, length, _ = r.choice(locs)
+        flips = [(r.randrange(length), r.randrange(1, 256)) for _ in range(r.choice([1, 1, 2, 4]))]
+
+        def fn(rec, flips=flips):
+            for at, x in flips:
+                rec[at] ^= x
+
+        arch = _raw_edit(src, str(tmp_path / ("m%d" % i)), oracle.crc64, label, fn)
+        try:
+            cpu, _ = foundry._foundry._pack_store_bytes(arch, False)
+        except foundry.FoundryError as e:
+            with pytest.raises(foundry.FoundryError) as gpu:
+                foundry._foundry._pack_store_bytes(arch, True)
+            assert str(gpu.value) == str(e), (i, label, flips)
+            outcomes["error"] += 1
+        else:
+            gpu, _ = foundry._foundry._pack_store_bytes(arch, True)
+            assert gpu == cpu, (i, label, flips, _first_difference(gpu, cpu))
+            outcomes["store"] += 1
+        shutil.rmtree(arch)
+    assert outcomes["error"] > 0
