@@ -133,7 +133,7 @@ class CApi:
 
     def check(self, rc: int) -> None:
         if rc:
-            raise CApiError(rc, self.lib.fdy_last_error().decode())
+            raise CApiError(rc, self.lib.fdy_last_error().decode(errors="backslashreplace"))
 
     # ---- session layer (the reference's LOAD surface)
     def load(self, archive: str, rank: int = 0, world: int = 1, relocate: bool = False,
@@ -255,7 +255,7 @@ class CApi:
     def host_alloc(self, dev, nbytes: int):
         p = self.lib.fdy_host_alloc(dev, nbytes)
         if not p:
-            raise CApiError(1, self.lib.fdy_last_error().decode())
+            raise CApiError(1, self.lib.fdy_last_error().decode(errors="backslashreplace"))
         return p
 
     def members_download(self, members) -> bytes:

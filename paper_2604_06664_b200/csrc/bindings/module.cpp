@@ -3,6 +3,8 @@
 // the B200 runtime. Names, argument names/defaults and return shapes match the
 // reference; B200-only knobs are extra keyword arguments with defaults that
 // keep reference behaviour.
+#include <cstring>
+
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 #include <pybind11/stl/filesystem.h>
@@ -185,7 +187,20 @@ PYBIND11_MODULE(_foundry, m) {
     m.doc() = "B200-native LOAD of template-based CUDA graph archives (Foundry drop-in)";
     m.attr("__version__") = "0.1.0";
 
-    py::register_exception<Error>(m, "FoundryError");
+    // FoundryError carries e.what(); a message that quotes bytes from a corrupt
+    // archive (a kernel name) need not be UTF-8, so it is decoded with
+    // backslash escapes instead of failing the conversion
+    static PyObject* foundry_error = py::exception<Error>(m, "FoundryError").inc_ref().ptr();
+    py::register_exception_translator([](std::exception_ptr p) {
+        try {
+            if (p) std::rethrow_exception(p);
+        } catch (const Error& e) {
+            const char* w = e.what();
+            PyObject* msg = PyUnicode_DecodeUTF8(w, static_cast<Py_ssize_t>(std::strlen(w)), "backslashreplace");
+            PyErr_SetObject(foundry_error, msg);
+            Py_XDECREF(msg);
+        }
+    });
 
     py::class_<WorkloadSpec>(m, "WorkloadSpec")
         .def(py::init<>())

@@ -325,3 +325,37 @@ def test_gpu_pack_byte_flip_fuzz(foundry, archives, oracle, tmp_path, name, seed
             outcomes["store"] += 1
         shutil.rmtree(arch)
     assert outcomes["error"] > 0
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_gpu_pack_patch_table_fuzz(foundry, archives, oracle, tmp_path, seed):
+    """Random byte flips in patch.bin (manifest digest kept consistent): the GPU
+    packer (patch-table view, entries on the GPU) builds the offline packer's
+    exact store or raises its exact error."""
+    import random
+    src, _ = archives("moe-spmd", b200=False)
+    patch = open(os.path.join(src, "patch.bin"), "rb").read()
+    r = random.Random(2000 + seed + 7919 * int(os.environ.get("FOUNDRY_FUZZ_ROUND", "0")))
+    errors = 0
+    for i in range(int(os.environ.get("FOUNDRY_FUZZ_N", "24"))):
+        arch = str(tmp_path / ("p%d" % i))
+        shutil.copytree(src, arch)
+        mutated = bytearray(patch)
+        for _ in range(r.choice([1, 1, 2, 3])):
+            mutated[r.randrange(len(mutated))] ^= r.randrange(1, 256)
+        open(os.path.join(arch, "patch.bin"), "wb").write(bytes(mutated))
+        m = json.load(open(os.path.join(arch, "manifest")))
+        m["files"]["patch.bin"] = oracle.crc64(bytes(mutated))
+        json.dump(m, open(os.path.join(arch, "manifest"), "w"))
+        try:
+            cpu, _ = foundry._foundry._pack_store_bytes(arch, False)
+        except foundry.FoundryError as e:
+            with pytest.raises(foundry.FoundryError) as gpu:
+                foundry._foundry._pack_store_bytes(arch, True)
+            assert str(gpu.value) == str(e), i
+            errors += 1
+        else:
+            gpu, _ = foundry._foundry._pack_store_bytes(arch, True)
+            assert gpu == cpu, (i, _first_difference(gpu, cpu))
+        shutil.rmtree(arch)
+    assert errors > 0

@@ -89,6 +89,22 @@ def test_pack_rejects_a_patch_on_a_non_stub(foundry, archives, tmp_path):
         foundry._foundry._pack_store(str(bad))
 
 
+def test_error_quoting_non_utf8_bytes_is_a_foundry_error(foundry, archives, tmp_path):
+    """A corrupt stub name in patch.bin (bytes 0xff) reaches the error message;
+    FoundryError still carries it (backslash-escaped) instead of the binding
+    failing to decode it (found by tests/test_gpu_pack.py's patch-table fuzz)."""
+    import shutil
+    arch, _ = archives("moe-spmd", b200=False)
+    bad = tmp_path / "bad"
+    shutil.copytree(arch, bad)
+    patch = bytearray((bad / "patch.bin").read_bytes())
+    at = patch.index(b"stub_allreduce")
+    patch[at:at + 4] = b"\xff\xfe\xff\xfe"
+    (bad / "patch.bin").write_bytes(bytes(patch))
+    with pytest.raises(foundry.FoundryError, match=r"\\xff\\xfe"):
+        foundry._foundry._pack_store(str(bad))
+
+
 def test_crc64_host_matches_the_oracle_and_combines(foundry, oracle):
     import random
     rng = random.Random(3)
