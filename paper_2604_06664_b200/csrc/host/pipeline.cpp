@@ -157,6 +157,7 @@ struct ServingContext::Impl {
             cuda_check(cudaMemcpy(dst, d_members.data() + M.out_off, view->group(M.group).image_bytes,
                                   cudaMemcpyDeviceToHost),
                        "cudaMemcpy(member image D2H)");
+            view->check_image(m, dst);
             const_cast<Impl*>(this)->h_present[m] = 1;
             const_cast<Impl*>(this)->t.d2h_bytes += view->group(M.group).image_bytes;
         }

@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <optional>
 #include <thread>
 
 #include <cuda_runtime.h>
@@ -578,7 +579,20 @@ static uint64_t materialize_archive_early(Device& dev, const fs::path& root, con
         }
     };
     Launched L;
+    std::span<const uint8_t> host;
+    std::optional<StoreView> view;
+    std::exception_ptr bad_store;
     try {
+        // the store's tables are validated as soon as its host copy is complete,
+        // while its last pieces are still DMAed and CRCed; a validation error is
+        // reported only once the digest has matched (integrity errors come first)
+        host = early->host("templates.fdt");
+        try {
+            view.emplace(host);
+        } catch (const Error&) {
+            bad_store = std::current_exception();
+        }
+        trace_point("store tables validated", t_all);
         const auto ts = Clock::now();
         if (early->digest("templates.fdt") != manifest.file_digests.at("templates.fdt")) verify_all();
         st.integrity_ms += ms_since(ts);
@@ -586,11 +600,10 @@ static uint64_t materialize_archive_early(Device& dev, const fs::path& root, con
     } catch (const Error&) {
         rethrow_in_step("archive integrity");
     }
+    if (bad_store) std::rethrow_exception(bad_store);
     L.t1 = Clock::now();
-    const auto host = early->host("templates.fdt");
-    const StoreView view(host);
     early->order_after("templates.fdt", dev.stream());
-    DeviceStore store = adopt_store(dev, early->device("templates.fdt"), host.size(), view.header());
+    DeviceStore store = adopt_store(dev, early->device("templates.fdt"), host.size(), view->header());
     launch_from_store(dev, manifest, store, req, host_out, cap, L);
     trace_point("kernel launched", t_all);
     try {

@@ -542,10 +542,75 @@ StoreView::StoreView(std::span<const uint8_t> blob) : blob_(blob) {
     attrs_ = reinterpret_cast<const fdt_node_attrs*>(at(FDT_SEC_NODEATTRS));
     edges_ = at(FDT_SEC_EDGES);
     strings_ = reinterpret_cast<const char*>(at(FDT_SEC_STRINGS));
+    validate_tables();
     uint32_t max_label = 0;
     for (uint32_t m = 0; m < h_.n_members; ++m) max_label = std::max(max_label, members_[m].label);
-    by_label_.assign(size_t(max_label) + 1, -1);
-    for (uint32_t m = 0; m < h_.n_members; ++m) by_label_[members_[m].label] = int32_t(m);
+    if (max_label <= 4ull * h_.n_members + 4096) {  // batch labels: dense table
+        by_label_.assign(size_t(max_label) + 1, -1);
+        for (uint32_t m = 0; m < h_.n_members; ++m) by_label_[members_[m].label] = int32_t(m);
+    } else {  // sparse labels: sorted (label, member), the last member of a label wins as above
+        for (uint32_t m = 0; m < h_.n_members; ++m) sparse_labels_.push_back({members_[m].label, m});
+        std::stable_sort(sparse_labels_.begin(), sparse_labels_.end(),
+                         [](const auto& x, const auto& y) { return x.first < y.first; });
+    }
+}
+
+// Every index and range the kernels and the host readers follow, checked once:
+// a store whose digest matches but whose tables do not (a writer bug, a forged
+// file) fails here with archive-corruption instead of reading or writing out
+// of bounds on the device. Linear in groups + members + kernels + tiles + edges.
+void StoreView::validate_tables() const {
+    auto bad = [](const std::string& what) { raise(Errc::archive_corruption, "template store: " + what); };
+    const fdt_section& ti = h_.sec[FDT_SEC_TIMAGES];
+    const uint64_t n_attrs = h_.sec[FDT_SEC_NODEATTRS].bytes / sizeof(fdt_node_attrs);
+    const uint64_t edge_bytes = h_.sec[FDT_SEC_EDGES].bytes, string_bytes = h_.sec[FDT_SEC_STRINGS].bytes;
+    if (h_.tile_chunks != FDT_TILE_CHUNKS) bad("tile size disagrees with this build");
+    if (h_.sec[FDT_SEC_CMETA].bytes != ti.bytes / 16 || h_.sec[FDT_SEC_DIDX].bytes != uint64_t(h_.n_diffs) * 2 ||
+        h_.sec[FDT_SEC_DDATA].bytes != uint64_t(h_.n_diffs) * 8 ||
+        h_.sec[FDT_SEC_ROPS].bytes != uint64_t(h_.n_rank_ops) * sizeof(fdt_rank_op))
+        bad("section sizes disagree with the header");
+    if (h_.n_plain_tiles > h_.n_tiles) bad("more relocation-free tiles than tiles");
+    const auto in_timages = [&](uint64_t off, uint64_t bytes) {
+        return off % 16 == 0 && off >= ti.offset && bytes <= ti.bytes && off - ti.offset <= ti.bytes - bytes;
+    };
+    for (uint32_t g = 0; g < h_.n_groups; ++g) {
+        const fdt_group& G = groups_[g];
+        const std::string at = "group " + std::to_string(g) + ": ";
+        if (G.image_bytes % 16 || G.image_bytes < 48ull * G.n_nodes || !in_timages(G.timage_off, G.image_bytes))
+            bad(at + "template image outside its section");
+        if (uint64_t(G.attrs_first) + G.n_nodes > n_attrs) bad(at + "node attributes outside their section");
+        if (G.edges_off % 4 || G.edges_off > edge_bytes || 8ull * G.n_edges > edge_bytes - G.edges_off)
+            bad(at + "edges outside their section");
+        if (uint64_t(G.first_member) + G.n_members > h_.n_members) bad(at + "members outside the member table");
+        const uint8_t* e = edges_ + G.edges_off;
+        for (uint64_t i = 0; i < 2ull * G.n_edges; ++i) {
+            uint32_t v;
+            std::memcpy(&v, e + 4 * i, 4);
+            if (v >= G.n_nodes) bad(at + "edge endpoint " + std::to_string(v) + " is not a node");
+        }
+    }
+    for (uint32_t k = 0; k < h_.n_kernels; ++k)
+        if (kernels_[k].name_off > string_bytes || kernels_[k].name_len > string_bytes - kernels_[k].name_off)
+            bad("kernel " + std::to_string(k) + ": name outside the string section");
+    for (uint32_t m = 0; m < h_.n_members; ++m) {
+        const fdt_member& M = members_[m];
+        if (M.group >= h_.n_groups) bad("member " + std::to_string(m) + ": no such group");
+        const fdt_group& G = groups_[M.group];
+        if (M.n_nodes != G.n_nodes || M.out_off % 16 || M.out_off > h_.members_image_bytes ||
+            G.image_bytes > h_.members_image_bytes - M.out_off ||
+            uint64_t(M.first_tile) + M.n_tiles > h_.n_tiles)
+            bad("member " + std::to_string(m) + ": image or tiles outside the arena");
+    }
+    for (uint32_t t = 0; t < h_.n_tiles; ++t) {
+        fdt_tile T;
+        std::memcpy(&T, blob_.data() + h_.sec[FDT_SEC_TILES].offset + uint64_t(t) * sizeof T, sizeof T);
+        const uint64_t bytes = 16ull * T.nchunks;
+        if (T.nchunks == 0 || T.nchunks > FDT_TILE_CHUNKS || T.member >= h_.n_members ||
+            !in_timages(T.src_off, bytes) || T.dst_off % 16 || T.dst_off > h_.members_image_bytes ||
+            bytes > h_.members_image_bytes - T.dst_off || T.diff_lo > T.diff_hi || T.diff_hi > h_.n_diffs ||
+            T.rop_lo > T.rop_hi || T.rop_hi > h_.n_rank_ops)
+            bad("tile " + std::to_string(t) + " reaches outside the store or the arena");
+    }
 }
 
 std::string_view StoreView::kernel_name(uint32_t k) const {
@@ -572,13 +637,34 @@ std::span<const uint32_t> StoreView::edges(uint32_t g) const {
 }
 
 int64_t StoreView::member_of(uint32_t label) const {
-    return label < by_label_.size() ? by_label_[label] : -1;
+    if (sparse_labels_.empty()) return label < by_label_.size() ? by_label_[label] : -1;
+    auto it = std::upper_bound(sparse_labels_.begin(), sparse_labels_.end(), label,
+                               [](uint32_t l, const auto& p) { return l < p.first; });
+    return it != sparse_labels_.begin() && (it - 1)->first == label ? int64_t((it - 1)->second) : -1;
+}
+
+void StoreView::check_image(uint32_t m, const uint8_t* image) const {
+    const fdt_member& M = members_[m];
+    const fdt_group& G = groups_[M.group];
+    const uint64_t pool = G.image_bytes - 48ull * G.n_nodes;
+    for (uint32_t i = 0; i < G.n_nodes; ++i) {
+        fdt_node d;
+        std::memcpy(&d, image + 48ull * i, sizeof d);
+        const uint64_t need = d.type == 1 || d.type == 2 ? 24 : d.type == 0 ? d.blob_len : 0;
+        const bool dims = d.type != 0 || (d.grid[0] && d.grid[1] && d.grid[2] && d.block[0] && d.block[1] &&
+                                          d.block[2]);  // decode_node's "launch dims must be >= 1"
+        if (d.type > 3 || (d.type == 0 && d.kernel >= h_.n_kernels) || !dims || d.blob_off > pool ||
+            need > pool - d.blob_off)
+            raise(Errc::archive_corruption, "template store: member " + std::to_string(M.label) + " node " +
+                                                std::to_string(i) + ": descriptor outside its image");
+    }
 }
 
 CapturedGraph StoreView::image_to_graph(uint32_t m, std::span<const uint8_t> image) const {
     const fdt_member& M = members_[m];
     const fdt_group& G = groups_[M.group];
     require(image.size() >= G.image_bytes, Errc::invalid_argument, "member image too small");
+    check_image(m, image.data());
     CapturedGraph g;
     g.label = M.label;
     g.nodes.resize(G.n_nodes);

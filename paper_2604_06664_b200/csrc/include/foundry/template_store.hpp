@@ -76,10 +76,16 @@ public:
     // Member index for a batch label, or -1.
     int64_t member_of(uint32_t label) const;
 
+    // Node descriptors of a materialized member image stay inside the image
+    // (type, kernel index, argument / memop bytes); archive-corruption otherwise.
+    void check_image(uint32_t member, const uint8_t* image) const;
+
     // Decode a member image (the GPU's output layout) back to a graph.
     CapturedGraph image_to_graph(uint32_t member, std::span<const uint8_t> image) const;
 
 private:
+    void validate_tables() const;
+
     std::span<const uint8_t> blob_;
     fdt_header h_{};
     const fdt_group* groups_ = nullptr;
@@ -89,6 +95,7 @@ private:
     const uint8_t* edges_ = nullptr;
     const char* strings_ = nullptr;
     std::vector<int32_t> by_label_;
+    std::vector<std::pair<uint32_t, uint32_t>> sparse_labels_;  // (label, member) when labels are sparse
 };
 
 }  // namespace foundry

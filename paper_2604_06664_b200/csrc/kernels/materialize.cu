@@ -222,7 +222,10 @@ __device__ __forceinline__ void prefetch_tile(const FdyMaterializeArgs& a, const
 __device__ __forceinline__ void apply_diff(uint4* buf, uint32_t word, uint64_t v, bool relocating,
                                            const FdyMaterializeArgs& a) {
     if (relocating && (word & FDT_DIDX_RELOC) && v - a.old_base < a.span) v += a.delta;
-    reinterpret_cast<uint64_t*>(buf)[word & FDT_DIDX_LANE_MASK] = v;
+    // a lane index is < 2 x nchunks in every store the packer writes; the mask
+    // keeps a forged one inside this stage's 16 KiB (the tail past nchunks is
+    // never stored)
+    reinterpret_cast<uint64_t*>(buf)[word & (2u * FDT_TILE_CHUNKS - 1u)] = v;
 }
 
 // K1 over the template images, once per launch: store -> scratch.
@@ -314,6 +317,7 @@ fdy_materialize_kernel(const FdyMaterializeArgs a) {
             const fdt_rank_op first = op_at(i);
             if (i != 0 && op_at(i - 1).chunk == first.chunk) continue;
             const uint32_t c = first.chunk - T.chunk_base;
+            if (c >= T.nchunks) continue;  // not this tile's chunk: only a forged store has it
             uint4 v = buf[c];
             for (uint32_t j = i; j < nops; ++j) {
                 const fdt_rank_op op = op_at(j);

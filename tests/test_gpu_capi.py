@@ -7,6 +7,7 @@ patch), which test_oracle.py pins to the reference.
 from __future__ import annotations
 
 import ctypes
+import json
 import os
 import shutil
 import socket
@@ -104,6 +105,24 @@ def test_member_pass_writes_every_arena_byte(archives, api, dev, name, rank, wor
     finally:
         api.lib.fdy_members_free(members)
         api.lib.fdy_store_free(store)
+
+
+@pytest.mark.parametrize("name,seed", [("micro", 0), ("moe-spmd", 1)])
+def test_forged_store_is_rejected_or_contained(archives, tmp_path, name, seed):
+    """templates.fdt with random byte flips and a matching manifest digest
+    (tests/store_fuzz_worker.py): fdy_prepare_archive and LOAD + replay either
+    succeed or raise a non-CUDA FoundryError; the store's table validation
+    (StoreView), the member pass's lane / chunk clamps and the image
+    descriptor checks keep a forged store off the device's out-of-bounds
+    paths. Run in a subprocess so a device fault could not poison this one."""
+    arch, _ = archives(name)
+    n = os.environ.get("FOUNDRY_FUZZ_N", "24")
+    seed += 7919 * int(os.environ.get("FOUNDRY_FUZZ_ROUND", "0"))
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "store_fuzz_worker.py"), arch,
+                          str(tmp_path), str(seed), n], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["ok"] + res["rejected"] == int(n) and res["rejected"] > 0, res
 
 
 def test_rank_outside_world_is_invalid_argument(archives, api, dev):
