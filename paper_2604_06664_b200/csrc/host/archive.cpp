@@ -3,7 +3,11 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
+#include <new>
+#include <memory>
 #include <optional>
+#include <type_traits>
 #include <string_view>
 #include <unordered_map>
 #include <unordered_set>
@@ -11,6 +15,7 @@
 #include <json.hpp>
 
 #include "foundry/bytes.hpp"
+#include "foundry/parallel.hpp"
 
 namespace foundry {
 
@@ -712,7 +717,11 @@ uint32_t PatchEntryView::world_offset(uint32_t i) const {
     return v;
 }
 
-PatchView parse_patch_view(std::span<const uint8_t> bytes) {
+namespace {
+
+// The reference-order parse (one pass, Cursor bounds checks): the exact error
+// for a malformed table, and the parse itself for a small one.
+PatchView parse_patch_view_sequential(std::span<const uint8_t> bytes) {
     Cursor c(bytes, Errc::archive_corruption);
     c.magic("FNDP");
     const uint16_t version = c.u16();
@@ -743,6 +752,130 @@ PatchView parse_patch_view(std::span<const uint8_t> bytes) {
         t.graphs.push_back({label, first, n});
     }
     require(c.at_end(), Errc::archive_corruption, "trailing bytes in patch table");
+    return t;
+}
+
+uint32_t rd32le(const uint8_t* p) {
+    uint32_t v;
+    std::memcpy(&v, p, 4);
+    return v;
+}
+
+// Pooled storage for large PatchViews' entries (raw bytes; PatchEntryView is
+// trivially destructible, so a block is returned without running destructors).
+std::mutex g_entry_pool_mu;
+std::vector<std::pair<void*, size_t>> g_entry_pool;
+
+static_assert(std::is_trivially_destructible_v<PatchEntryView>, "pooled entries are released without destructors");
+
+std::shared_ptr<PatchEntryView> pooled_entries(size_t count) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(PatchEntryView);
+    void* p = nullptr;
+    size_t cap = 0;
+    {
+        std::lock_guard lock(g_entry_pool_mu);
+        for (size_t i = 0; i < g_entry_pool.size(); ++i)
+            if (g_entry_pool[i].second >= bytes && (!p || g_entry_pool[i].second < cap)) {
+                p = g_entry_pool[i].first;
+                cap = g_entry_pool[i].second;
+            }
+        if (p)
+            g_entry_pool.erase(std::find(g_entry_pool.begin(), g_entry_pool.end(), std::make_pair(p, cap)));
+    }
+    if (!p) {
+        cap = bytes;
+        p = ::operator new(cap);
+    }
+    return std::shared_ptr<PatchEntryView>(static_cast<PatchEntryView*>(p), [cap](PatchEntryView* q) {
+        std::lock_guard lock(g_entry_pool_mu);
+        g_entry_pool.push_back({q, cap});
+        if (g_entry_pool.size() > 2) {  // keep the two largest
+            std::sort(g_entry_pool.begin(), g_entry_pool.end(),
+                      [](const auto& a, const auto& b) { return a.second > b.second; });
+            ::operator delete(g_entry_pool.back().first);
+            g_entry_pool.pop_back();
+        }
+    });
+}
+
+}  // namespace
+
+// Large tables (10 MB, 144K entries on the headline set) parse in two passes: a
+// sequential walk over the entry sizes finds every graph's byte range, then the
+// graphs are decoded on the worker pool into a pre-sized entry array. Anything
+// the walk cannot account for falls back to the sequential parse, so a
+// malformed table raises exactly the reference-order error.
+PatchView parse_patch_view(std::span<const uint8_t> bytes) {
+    PatchView t;
+    const uint8_t* p = bytes.data();
+    const uint64_t n = bytes.size();
+    if (n < (256u << 10) || std::memcmp(p, "FNDP", 4) != 0 || p[4] != 1 || p[5] != 0) {
+        t = parse_patch_view_sequential(bytes);
+    } else {
+        std::memcpy(&t.world_placeholder, p + 6, 8);
+        const uint32_t ng = rd32le(p + 14);
+        struct Span {
+            uint64_t at;
+            uint32_t label, count, first;
+        };
+        std::vector<Span> spans;
+        spans.reserve(std::min<uint64_t>(ng, n / 8));
+        uint64_t at = 18, total = 0;
+        bool ok = true;
+        auto fits = [&](uint64_t k) { return k <= n - at; };
+        for (uint32_t g = 0; g < ng && ok; ++g) {
+            if (!fits(8)) { ok = false; break; }
+            Span sp{at + 8, rd32le(p + at), rd32le(p + at + 4), static_cast<uint32_t>(total)};
+            at += 8;
+            for (uint32_t i = 0; i < sp.count; ++i) {
+                // node_id u32, stub_hash u64, two names (u32 + bytes), two u32 lists, u8
+                if (!fits(16)) { ok = false; break; }
+                at += 12;
+                uint64_t k = rd32le(p + at);
+                at += 4;
+                if (!fits(k) || !fits(k + 4)) { ok = false; break; }
+                at += k;
+                k = rd32le(p + at);
+                at += 4;
+                if (!fits(k) || !fits(k + 4)) { ok = false; break; }
+                at += k;
+                k = 4ull * rd32le(p + at);
+                at += 4;
+                if (!fits(k) || !fits(k + 4)) { ok = false; break; }
+                at += k;
+                k = 4ull * rd32le(p + at);
+                at += 4;
+                if (!fits(k) || !fits(k + 1)) { ok = false; break; }
+                at += k + 1;
+            }
+            total += sp.count;
+            spans.push_back(sp);
+        }
+        if (!ok || at != n || total >= (1ull << 32)) {
+            t = parse_patch_view_sequential(bytes);  // raises the reference's error
+        } else {
+            t.pooled = pooled_entries(total);
+            PatchEntryView* const out = t.pooled.get();
+            parallel_for(spans.size(), spans.size() >= 64 ? 0u : 1u, [&](size_t g) {
+                const Span& sp = spans[g];
+                Cursor c(p + sp.at, n - sp.at, Errc::archive_corruption);
+                for (uint32_t i = 0; i < sp.count; ++i) {
+                    PatchEntryView& e = *new (out + sp.first + i) PatchEntryView;
+                    e.node_id = c.u32();
+                    e.stub_hash = c.u64();
+                    e.stub_name = c.str_view();
+                    e.real_name = c.str_view();
+                    e.n_rank = c.u32();
+                    e.rank_offsets = c.take(4ull * e.n_rank);
+                    e.n_world = c.u32();
+                    e.world_offsets = c.take(4ull * e.n_world);
+                    e.patch_width = c.u8();
+                }
+            });
+            t.graphs.reserve(spans.size());
+            for (const Span& sp : spans) t.graphs.push_back({sp.label, sp.first, sp.count});
+        }
+    }
     std::stable_sort(t.graphs.begin(), t.graphs.end(),
                      [](const auto& a, const auto& b) { return a[0] < b[0]; });
     t.graphs.erase(std::unique(t.graphs.begin(), t.graphs.end(),
@@ -755,7 +888,7 @@ std::span<const PatchEntryView> PatchView::find(uint32_t label) const {
     auto it = std::lower_bound(graphs.begin(), graphs.end(), label,
                                [](const std::array<uint32_t, 3>& g, uint32_t l) { return g[0] < l; });
     if (it == graphs.end() || (*it)[0] != label) return {};
-    return {entries.data() + (*it)[1], (*it)[2]};
+    return {entry_data() + (*it)[1], (*it)[2]};
 }
 
 bool PatchView::has(uint32_t label) const {

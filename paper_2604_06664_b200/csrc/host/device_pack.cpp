@@ -18,6 +18,7 @@
 #include <exception>
 #include <future>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <optional>
@@ -468,7 +469,13 @@ private:
             segs.push_back({rec_off_[m], head});
             segs.push_back({rec_off_[m] + head, rec_len_[m] - head});
         }
+        static const bool debug = std::getenv("FOUNDRY_DEBUG") != nullptr;
+        cudaEvent_t ev[3] = {};
+        if (debug)
+            for (auto& e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        if (debug) cuda_check(cudaEventRecord(ev[0], st_), "cudaEventRecord");
         crc_.launch(dev_, d_graphs_, segs);  // ahead of pass 1 on the stream: one sync covers both
+        if (debug) cuda_check(cudaEventRecord(ev[1], st_), "cudaEventRecord");
         const double t_crc = ms_of(tp);
         // status | cap | rep_attrs | rep_type | node_off: one copy into pinned memory,
         // read back with the key count
@@ -484,6 +491,7 @@ private:
             cuda_check(cudaMemsetAsync(a.tpos, 0xFF, 8ull * tslots, st_), "GPU pack memset");
             cuda_check(cudaMemsetAsync(d_small, 0, 16, st_), "GPU pack memset");
             cuda_check(fdy_launch_pack_pass1(&a, st_), "GPU pack pass 1");
+            if (debug) cuda_check(cudaEventRecord(ev[2], st_), "cudaEventRecord");
             d2h(small, d_small, 2, st_);
             cuda_check(cudaMemcpyAsync(back_.data(), back_lo, size_t(back_end - back_lo), cudaMemcpyDeviceToHost, st_),
                        "GPU pack D2H");
@@ -492,6 +500,14 @@ private:
             if (small[1] == 0) break;
             require(attempt < 4, Errc::cuda_error, "GPU pack: kernel key fingerprints keep colliding");
             ++tm_.retries;
+        }
+        if (debug) {
+            float crc = 0, all = 0;
+            cuda_check(cudaEventElapsedTime(&crc, ev[0], ev[1]), "cudaEventElapsedTime");
+            cuda_check(cudaEventElapsedTime(&all, ev[0], ev[2]), "cudaEventElapsedTime");
+            tm_.pass1_gpu_crc_ms = crc;
+            tm_.pass1_gpu_ms = all;
+            for (auto& e : ev) cudaEventDestroy(e);
         }
         nu_ = small[0];
         tm_.kernel_keys = nu_;
@@ -516,8 +532,10 @@ private:
         const auto parts = crc_.digests();  // launched ahead of pass 1: complete
         digests_.assign(1 + nm, 0);
         digests_[0] = parts[0];
-        for (uint32_t m = 0; m < nm; ++m)
+        // ~1 us per combine (GF(2) powers): 512 records on the worker pool
+        parallel_for(nm, nm >= 64 ? 0u : 1u, [&](size_t m) {
             digests_[1 + m] = crc64_combine(parts[1 + 2 * m], parts[2 + 2 * m], segs[2 + 2 * m].length);
+        });
     }
 
     // ------------------------------------------------ host: checks, kernel table, layout

@@ -739,7 +739,13 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
         trace_point("staging started", t_all);
         if (!has_store && staged->has("patch.bin")) {
             // parse errors surface when the packer consumes it, after integrity
-            patch_view = std::async(std::launch::async, [&staged] { return parse_patch_view(staged->host("patch.bin")); });
+            patch_view = std::async(std::launch::async, [&staged, t_all] {
+                const auto bytes = staged->host("patch.bin");
+                trace_point("patch.bin on the host", t_all);
+                PatchView v = parse_patch_view(bytes);
+                trace_point("patch table parsed", t_all);
+                return v;
+            });
         }
         for (const auto& rel : first) staged->verify_file(manifest, rel, &st);
         trace_point("store verified", t_all);
@@ -770,10 +776,11 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
             if (std::getenv("FOUNDRY_DEBUG"))
                 std::fprintf(stderr,
                              "[foundry] pack phases: patch wait %.3f, prep %.3f, pass1 %.3f (uploaded %.3f, CRC queued %.3f, "
-                             "synced %.3f), host1 %.3f, pass2 %.3f (rank ops %.3f), host2 %.3f (tiles %.3f), pass3 %.3f, "
-                             "total %.3f ms\n",
+                             "synced %.3f; device %.3f of which CRC %.3f), host1 %.3f, pass2 %.3f (rank ops %.3f), "
+                             "host2 %.3f (tiles %.3f), pass3 %.3f, total %.3f ms\n",
                              pack_t.patch_parse_ms, pack_t.prep_ms, pack_t.pass1_ms, pack_t.pass1_upload_ms,
-                             pack_t.pass1_launch_ms, pack_t.pass1_sync_ms, pack_t.host1_ms, pack_t.pass2_ms,
+                             pack_t.pass1_launch_ms, pack_t.pass1_sync_ms, pack_t.pass1_gpu_ms, pack_t.pass1_gpu_crc_ms,
+                             pack_t.host1_ms, pack_t.pass2_ms,
                              pack_t.rank_ops_ms, pack_t.host2_ms, pack_t.tiles_ms, pack_t.pass3_ms, pack_t.total_ms);
         } catch (const Error&) {
             rethrow_in_step("template construction");

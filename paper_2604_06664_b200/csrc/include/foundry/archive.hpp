@@ -13,6 +13,7 @@
 #include <string_view>
 #include <filesystem>
 #include <map>
+#include <memory>
 #include <optional>
 #include <span>
 #include <string>
@@ -201,7 +202,11 @@ struct PatchEntryView {
 };
 struct PatchView {
     uint64_t world_placeholder = 1;
-    std::vector<PatchEntryView> entries;
+    std::vector<PatchEntryView> entries;  // small tables (and the reference-order parse)
+    // large tables: the entries live in a pooled block (a fresh 11 MB array costs
+    // more in page faults than the parse; tools/experiments/patch_parse.py)
+    std::shared_ptr<PatchEntryView> pooled;
+    const PatchEntryView* entry_data() const { return pooled ? pooled.get() : entries.data(); }
     // label -> [first, first + count) in entries, sorted by label; the first
     // occurrence of a label wins (parse_patch_table's map emplace)
     std::vector<std::array<uint32_t, 3>> graphs;

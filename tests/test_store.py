@@ -282,3 +282,29 @@ def test_patch_view_equals_the_patch_table(foundry, archives):
         assert str(table.value) == str(view.value), cut
     with pytest.raises(foundry.FoundryError, match="trailing bytes in patch table"):
         foundry._foundry._parse_patch_view(raw + b"\0")
+
+
+def test_patch_view_fuzz_matches_the_patch_table(foundry, archives):
+    """Random byte flips of a patch table large enough for the two-pass parallel
+    view (sizes walked first, graphs decoded on the worker pool): the view
+    either equals parse_patch_table's result or raises its exact error."""
+    import random
+    arch, _ = archives("moe-spmd")
+    raw = open(os.path.join(arch, "patch.bin"), "rb").read()
+    assert len(raw) >= 256 << 10  # the parallel path
+    r = random.Random(7)
+    for i in range(200):
+        b = bytearray(raw)
+        for _ in range(r.choice([1, 2, 3])):
+            # length and count fields sit in the first bytes of every entry: aim some flips there
+            at = r.randrange(len(b)) if r.random() < 0.5 else r.randrange(min(len(b), 4096))
+            b[at] ^= r.randrange(1, 256)
+        b = bytes(b)
+        try:
+            same = foundry._foundry._patch_view_matches_table(b)
+        except foundry.FoundryError as e:
+            with pytest.raises(foundry.FoundryError) as view:
+                foundry._foundry._parse_patch_view(b)
+            assert str(view.value) == str(e), i
+        else:
+            assert same, i
