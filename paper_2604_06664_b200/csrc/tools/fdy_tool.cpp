@@ -824,6 +824,17 @@ int main(int argc, char** argv) {
             fdy_device_close(d);
             return 0;
         }
+        if (cmd == "cuda-hold") {  // keeps one context open until stdin closes (a resident
+                                   // serving process / persistence daemon stand-in)
+            fdy_device* d = nullptr;
+            if (fdy_device_open(argc > 2 ? std::atoi(argv[2]) : 0, &d)) return 1;
+            std::printf("cuda-hold ready: device open\n");
+            std::fflush(stdout);
+            while (std::fgetc(stdin) != EOF) {
+            }
+            fdy_device_close(d);
+            return 0;
+        }
         if (cmd == "restorebench") return cmd_restorebench(argc, argv);
         if (cmd == "naive") {
             ServingContext sc = load(argv[2], LoadOptions{});
