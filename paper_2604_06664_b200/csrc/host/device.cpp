@@ -343,9 +343,20 @@ std::vector<uint64_t> crc64_device(Device& dev, const unsigned char* d_base,
     return out;
 }
 
-void CrcJob::launch(Device& dev, const unsigned char* d_base, std::span<const Segment> segments) {
+CrcJob::~CrcJob() {
+    // side-stream work may still read the scratch / write the pinned digests
+    // (an error path between launch and join): let it finish before they go
+    if (dev_ && on_ && on_ != dev_->stream()) cudaStreamSynchronize(on_);
+    if (fork_) cudaEventDestroy(fork_);
+    if (done_) cudaEventDestroy(done_);
+}
+
+void CrcJob::launch(Device& dev, const unsigned char* d_base, std::span<const Segment> segments,
+                    cudaStream_t on) {
     dev.make_current();
+    if (dev_ && on_ && on_ != dev_->stream()) cuda_check(cudaStreamSynchronize(on_), "cudaStreamSynchronize(crc)");
     dev_ = &dev;
+    on_ = on ? on : dev.stream();
     ns_ = segments.size();
     size_t nb = 0;
     for (const Segment& g : segments) nb += (g.length + kCrcBlockBytes - 1) / kCrcBlockBytes;
@@ -380,7 +391,12 @@ void CrcJob::launch(Device& dev, const unsigned char* d_base, std::span<const Se
     auto* d_crc = reinterpret_cast<uint64_t*>(p);
     auto* d_len = d_crc + nb;
     auto* d_out = d_len + nb;
-    cudaStream_t st = dev.stream();
+    cudaStream_t st = on_;
+    if (st != dev.stream()) {  // the scratch (stream-ordered on dev.stream()) and the input first
+        if (!fork_) cuda_check(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventRecord(fork_, dev.stream()), "cudaEventRecord(crc fork)");
+        cuda_check(cudaStreamWaitEvent(st, fork_, 0), "cudaStreamWaitEvent(crc fork)");
+    }
     if (plan_bytes)
         cuda_check(cudaMemcpyAsync(scratch_.data(), plan_.data(), plan_bytes, cudaMemcpyHostToDevice, st),
                    "H2D crc plan");
@@ -388,10 +404,18 @@ void CrcJob::launch(Device& dev, const unsigned char* d_base, std::span<const Se
                                 static_cast<uint32_t>(ns_), d_crc, d_len, d_out, st),
                "crc64 kernel launch");
     if (ns_) cuda_check(cudaMemcpyAsync(out_.data(), d_out, ns_ * 8, cudaMemcpyDeviceToHost, st), "D2H crc");
+    if (st != dev.stream()) {
+        if (!done_) cuda_check(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventRecord(done_, st), "cudaEventRecord(crc done)");
+    }
+}
+
+void CrcJob::join(cudaStream_t st) {
+    if (dev_ && on_ != st && done_) cuda_check(cudaStreamWaitEvent(st, done_, 0), "cudaStreamWaitEvent(crc join)");
 }
 
 std::span<const uint64_t> CrcJob::wait() {
-    if (dev_) cuda_check(cudaStreamSynchronize(dev_->stream()), "cudaStreamSynchronize(crc)");
+    if (dev_) cuda_check(cudaStreamSynchronize(on_), "cudaStreamSynchronize(crc)");
     return digests();
 }
 

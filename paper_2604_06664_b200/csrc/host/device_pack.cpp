@@ -362,6 +362,12 @@ private:
     void pass1() {
         const uint32_t nm = nm_, TN = TN_, GN = GN_, NE = NE_, tslots = tslots_;
         const auto tp = Clock::now();
+        static const bool debug = std::getenv("FOUNDRY_DEBUG") != nullptr;
+        cudaEvent_t ev[6] = {};  // upload done, read-back done, pass-1 kernels done, CRC done, entry, scratch
+        if (debug) {
+            for (auto& e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+            cuda_check(cudaEventRecord(ev[4], dev_.stream()), "cudaEventRecord");
+        }
         s1_.emplace(dev_, Scratch::need({8ull * nm, 8ull * nm, 4ull * nm, 4ull * nm, 4ull * nm, 4ull * nm, 4ull * nm,
                                          4ull * n_groups_, 4ull * n_groups_, 4ull * TN, 4ull * TN, 4ull * TN,
                                          4ull * GN, sizeof(fdt_node_attrs) * GN, GN, 8ull * tslots, 8ull * tslots,
@@ -371,6 +377,7 @@ private:
                                          size_t(std::min<uint64_t>(tslots, uint64_t(TN) + NE + 1)) *
                                              FDY_PACK_KEY_BYTES}));
         Scratch& s1 = *s1_;
+        if (debug) cuda_check(cudaEventRecord(ev[5], dev_.stream()), "cudaEventRecord");
         FdyPackArgs& a = a_;
         a.graphs = d_graphs_;
         a.graphs_bytes = gsize_;
@@ -469,13 +476,11 @@ private:
             segs.push_back({rec_off_[m], head});
             segs.push_back({rec_off_[m] + head, rec_len_[m] - head});
         }
-        static const bool debug = std::getenv("FOUNDRY_DEBUG") != nullptr;
-        cudaEvent_t ev[3] = {};
-        if (debug)
-            for (auto& e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
         if (debug) cuda_check(cudaEventRecord(ev[0], st_), "cudaEventRecord");
-        crc_.launch(dev_, d_graphs_, segs);  // ahead of pass 1 on the stream: one sync covers both
-        if (debug) cuda_check(cudaEventRecord(ev[1], st_), "cudaEventRecord");
+        // on the side stream, concurrent with pass 1 (the record walk is latency
+        // bound, the CRC bandwidth bound); joined before the pass-1 sync
+        crc_.launch(dev_, d_graphs_, segs, dev_.side_stream());
+        if (debug) cuda_check(cudaEventRecord(ev[3], dev_.side_stream()), "cudaEventRecord");
         const double t_crc = ms_of(tp);
         // status | cap | rep_attrs | rep_type | node_off: one copy into pinned memory,
         // read back with the key count
@@ -491,10 +496,12 @@ private:
             cuda_check(cudaMemsetAsync(a.tpos, 0xFF, 8ull * tslots, st_), "GPU pack memset");
             cuda_check(cudaMemsetAsync(d_small, 0, 16, st_), "GPU pack memset");
             cuda_check(fdy_launch_pack_pass1(&a, st_), "GPU pack pass 1");
+            if (attempt == 0) crc_.join(st_);
             if (debug) cuda_check(cudaEventRecord(ev[2], st_), "cudaEventRecord");
             d2h(small, d_small, 2, st_);
             cuda_check(cudaMemcpyAsync(back_.data(), back_lo, size_t(back_end - back_lo), cudaMemcpyDeviceToHost, st_),
                        "GPU pack D2H");
+            if (debug) cuda_check(cudaEventRecord(ev[1], st_), "cudaEventRecord");
             cuda_check(cudaStreamSynchronize(st_), "GPU pack pass 1");
             tm_.pass1_sync_ms = ms_of(tp);
             if (small[1] == 0) break;
@@ -502,11 +509,18 @@ private:
             ++tm_.retries;
         }
         if (debug) {
-            float crc = 0, all = 0;
-            cuda_check(cudaEventElapsedTime(&crc, ev[0], ev[1]), "cudaEventElapsedTime");
+            float crc = 0, all = 0, pre = 0, tail = 0;
+            cuda_check(cudaEventElapsedTime(&pre, ev[4], ev[0]), "cudaEventElapsedTime");
+            float alloc = 0;
+            cuda_check(cudaEventElapsedTime(&alloc, ev[4], ev[5]), "cudaEventElapsedTime");
+            tm_.pass1_gpu_alloc_ms = alloc;
+            cuda_check(cudaEventElapsedTime(&crc, ev[0], ev[3]), "cudaEventElapsedTime");
             cuda_check(cudaEventElapsedTime(&all, ev[0], ev[2]), "cudaEventElapsedTime");
+            cuda_check(cudaEventElapsedTime(&tail, ev[2], ev[1]), "cudaEventElapsedTime");
             tm_.pass1_gpu_crc_ms = crc;
             tm_.pass1_gpu_ms = all;
+            tm_.pass1_gpu_pre_ms = pre;
+            tm_.pass1_gpu_tail_ms = tail;
             for (auto& e : ev) cudaEventDestroy(e);
         }
         nu_ = small[0];

@@ -730,11 +730,16 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
     }
     std::future<PatchView> patch_view;
     try {
-        // a reference-written archive streams 188 MB where the store is 18 MB: with
-        // every lane reading, the patch-table parse and the packer's host threads
-        // lose their cores (tools/experiments/e2e_plain_timeline.py, 16-core host:
-        // 16 lanes 14.7-17.7 ms, 8 lanes 13.9-14.9 ms; the stream is PCIe-bound)
-        const unsigned stage_lanes = has_store ? lanes : std::max(4u, lanes / 2);
+        // a reference-written archive streams 188 MB where the store is 18 MB; the
+        // stream is host-memory bound (page cache -> pinned at ~36 GB/s on 16
+        // lanes). Half the lanes used to be faster while the patch-table parse
+        // needed its cores for 5-7 ms; with the parse done by ~3 ms every lane
+        // streams (tools/experiments/plain_lanes.sh, 16-core host, median of 5:
+        // 8 lanes 14.7 / 16.0 ms, 12 lanes 14.6 / 13.9, 16 lanes 14.0 / 13.8).
+        // FOUNDRY_PLAIN_STAGE_LANES overrides it for such sweeps.
+        unsigned stage_lanes = lanes;
+        if (const char* env = std::getenv("FOUNDRY_PLAIN_STAGE_LANES"); env && !has_store)
+            stage_lanes = std::max(1, std::atoi(env));
         staged = std::make_unique<StagedArchive>(dev, root, manifest, stage_lanes, &st, plan);
         trace_point("staging started", t_all);
         if (!has_store && staged->has("patch.bin")) {
@@ -746,6 +751,10 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
                 trace_point("patch table parsed", t_all);
                 return v;
             });
+        }
+        if (!has_store && std::getenv("FOUNDRY_DEBUG")) {
+            (void)staged->host("graphs.bin");
+            trace_point("graphs.bin read", t_all);
         }
         for (const auto& rel : first) staged->verify_file(manifest, rel, &st);
         trace_point("store verified", t_all);
@@ -776,10 +785,12 @@ uint64_t materialize_archive(Device& dev, const fs::path& root, const Materializ
             if (std::getenv("FOUNDRY_DEBUG"))
                 std::fprintf(stderr,
                              "[foundry] pack phases: patch wait %.3f, prep %.3f, pass1 %.3f (uploaded %.3f, CRC queued %.3f, "
-                             "synced %.3f; device %.3f of which CRC %.3f), host1 %.3f, pass2 %.3f (rank ops %.3f), "
+                             "synced %.3f; device: entry->kernels %.3f (scratch %.3f), kernels %.3f, CRC %.3f, read-back %.3f), host1 %.3f, pass2 %.3f (rank ops %.3f), "
                              "host2 %.3f (tiles %.3f), pass3 %.3f, total %.3f ms\n",
                              pack_t.patch_parse_ms, pack_t.prep_ms, pack_t.pass1_ms, pack_t.pass1_upload_ms,
-                             pack_t.pass1_launch_ms, pack_t.pass1_sync_ms, pack_t.pass1_gpu_ms, pack_t.pass1_gpu_crc_ms,
+                             pack_t.pass1_launch_ms, pack_t.pass1_sync_ms, pack_t.pass1_gpu_pre_ms, pack_t.pass1_gpu_alloc_ms,
+                             pack_t.pass1_gpu_ms,
+                             pack_t.pass1_gpu_crc_ms, pack_t.pass1_gpu_tail_ms,
                              pack_t.host1_ms, pack_t.pass2_ms,
                              pack_t.rank_ops_ms, pack_t.host2_ms, pack_t.tiles_ms, pack_t.pass3_ms, pack_t.total_ms);
         } catch (const Error&) {

@@ -22,6 +22,7 @@ struct DevicePackTimings {
     double pass1_ms = 0;  // upload + walk/fields/edges/verify/compact + record CRCs
     double pass1_upload_ms = 0, pass1_launch_ms = 0, pass1_sync_ms = 0;  // stamps within pass 1
     double pass1_gpu_ms = 0, pass1_gpu_crc_ms = 0;  // device time of pass 1 / its CRCs (FOUNDRY_DEBUG)
+    double pass1_gpu_pre_ms = 0, pass1_gpu_tail_ms = 0, pass1_gpu_alloc_ms = 0;  // device: pass-1 entry -> kernels; kernels -> read-back done
     double host1_ms = 0;  // checks, kernel table, layout, rank ops
     double checks_ms = 0, kernel_table_ms = 0, rank_ops_ms = 0;  // of which
     double pass2_ms = 0;  // images + diff counts

@@ -49,15 +49,24 @@ private:
 // crc64_device split: launch() enqueues the plan upload, the kernel and the digests'
 // read-back on dev.stream() and returns; digests() is valid once that stream has
 // been synchronized past the launch (by the caller or by wait()).
+// With `on` = another stream (dev.side_stream()), the work runs there, after
+// everything already queued on dev.stream(); join(st) then makes `st` wait for it.
 class CrcJob {
 public:
     CrcJob() = default;
-    void launch(Device& dev, const unsigned char* d_base, std::span<const Segment> segments);
-    std::span<const uint64_t> wait();  // synchronizes dev.stream()
+    ~CrcJob();
+    CrcJob(const CrcJob&) = delete;
+    CrcJob& operator=(const CrcJob&) = delete;
+    void launch(Device& dev, const unsigned char* d_base, std::span<const Segment> segments,
+                cudaStream_t on = nullptr);
+    void join(cudaStream_t st);        // st waits for the launch (no-op on the launch stream)
+    std::span<const uint64_t> wait();  // synchronizes the launch stream
     std::span<const uint64_t> digests() const { return {reinterpret_cast<const uint64_t*>(out_.data()), ns_}; }
 
 private:
     Device* dev_ = nullptr;
+    cudaStream_t on_ = nullptr;
+    cudaEvent_t fork_ = nullptr, done_ = nullptr;
     DeviceBuffer scratch_;
     PinnedLease plan_, out_;
     size_t ns_ = 0;
