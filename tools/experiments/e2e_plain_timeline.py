@@ -3,7 +3,7 @@ sys.path.insert(0, os.getcwd())
 from paper_2604_06664_b200 import capi
 import paper_2604_06664_b200 as foundry
 root = "/tmp/foundry_bench_qwen3-235b-a22b"
-plain = root + "/plain"
+plain = root + "/" + os.environ.get("ARCHIVE", "plain")
 if not os.path.exists(plain + "/manifest"):  # the bench's archives, or fresh ones
     w = foundry.workload_from_text(open(foundry.workload_path("qwen3-235b-a22b")).read())
     foundry.save(w, root + "/b200")
