@@ -163,6 +163,26 @@ uint64_t put_section(Sink& s, fdt_header& h, int id, const T* data, size_t count
     return h.sec[id].offset;
 }
 
+// parallel_for whose failure is the lowest failing index's, not the first in
+// time: when several members of a group are bad, the store build reports the
+// same one on every run, in the order the GPU packer checks them (member order
+// within each phase). The reference's prepare lanes keep whichever failure
+// lands first (templater.cpp:100-116), so any one of them is a faithful
+// report; this build fixes which.
+template <typename Fn>
+void parallel_for_first_error(size_t n, unsigned threads, Fn&& fn) {
+    std::vector<std::exception_ptr> err(n);
+    parallel_for(n, threads, [&](size_t i) {
+        try {
+            fn(i);
+        } catch (...) {
+            err[i] = std::current_exception();
+        }
+    });
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+}
+
 // apply_rank_patches (rank_forge.cpp:132-152) for graph g, split by what it
 // depends on: the stub -> real kernel swap is rank-independent, so it is
 // written into g's image here (and so lands in the template / diffs); the
@@ -252,7 +272,7 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
                 Errc::invalid_argument, "grouping manifest is missing member locators");
         const size_t nm = grp.members.size();
         std::vector<CapturedGraph> graphs(nm);
-        parallel_for(nm, threads, [&](size_t i) {
+        parallel_for_first_error(nm, threads, [&](size_t i) {
             graphs[i] = parse_graph_at(graphs_bin, grp.locators[i]);
         });
         // representative = smallest label (templater.hpp:16); members ascending
@@ -261,7 +281,7 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
             if (graphs[i].label == grp.representative) rep = i;
         const CapturedGraph& T = graphs[rep];
         const TopologyKey tkey = topology_key(T);
-        parallel_for(nm, threads, [&](size_t i) {
+        parallel_for_first_error(nm, threads, [&](size_t i) {
             if (i == rep) return;
             const TopologyKey k = topology_key(graphs[i]);
             require(k == tkey, Errc::topology_mismatch,
@@ -330,7 +350,7 @@ std::vector<uint8_t> pack_template_store(std::span<const uint8_t> graphs_bin,
         std::copy(tmeta.begin(), tmeta.end(), cmeta.begin() + G.timage_off / 16);
 
         std::vector<MemberOut> outs(nm);
-        parallel_for(nm, threads, [&](size_t i) {
+        parallel_for_first_error(nm, threads, [&](size_t i) {
             const CapturedGraph& g = graphs[i];
             MemberOut& o = outs[i];
             std::vector<uint8_t> img, meta;

@@ -207,8 +207,11 @@ __global__ void __launch_bounds__(32) pack_walk_kernel(const FdyPackArgs a) {
     };
     // bytes [x, x + n) of the record (record-relative) are in shared memory
     // once this returns; the ring is refilled ahead of x as far as it reaches
+    uint64_t ready = 0;  // window-relative bytes [0, ready) have landed (the walk only moves forward,
+                         // and no window at or after the walker's is refilled before it moves on)
     auto ensure = [&](uint64_t x, uint32_t n) {
         const uint64_t ax = rb + x - w0;
+        if (ax + n <= ready) return;  // the common case: inside the windows already waited for
         const uint32_t lo = uint32_t(ax / kWalkWin), hi = uint32_t((ax + n - 1) / kWalkWin);
         while (issued < n_wins && issued < lo + kWalkWins) {
             if (issued >= kWalkWins && waited <= issued - kWalkWins) {  // its slot's last window
@@ -221,6 +224,7 @@ __global__ void __launch_bounds__(32) pack_walk_kernel(const FdyPackArgs a) {
             wait(waited);
             ++waited;
         }
+        ready = uint64_t(waited) * kWalkWin;
     };
     auto byte_at = [&](uint64_t x) -> uint32_t { return ring[(rb + x - w0) & (kWalkRing - 1)]; };
     auto u32_at = [&](uint64_t x) {

@@ -308,3 +308,34 @@ def test_patch_view_fuzz_matches_the_patch_table(foundry, archives):
             assert str(view.value) == str(e), i
         else:
             assert same, i
+
+
+def test_pack_error_is_the_first_failing_member_not_the_first_in_time(foundry, oracle, archives, tmp_path):
+    """Two members of a group with different patch errors: the offline packer used to
+    report whichever of its threads failed first, so it disagreed with the GPU packer
+    (which checks members in order) on some runs; found by the GPU packer's patch-table
+    fuzz (tests/test_gpu_pack.py, FOUNDRY_FUZZ_ROUND=5, seed 0, mutation 49). The
+    failure is now the lowest failing member's on every run."""
+    import json
+    import random
+    import shutil
+    src, _ = archives("moe-spmd", b200=False)
+    patch = open(os.path.join(src, "patch.bin"), "rb").read()
+    r = random.Random(2000 + 0 + 7919 * 5)  # the fuzz's draw sequence up to mutation 49
+    for _ in range(50):
+        mutated = bytearray(patch)
+        for _ in range(r.choice([1, 1, 2, 3])):
+            mutated[r.randrange(len(mutated))] ^= r.randrange(1, 256)
+    arch = str(tmp_path / "two-bad-members")
+    shutil.copytree(src, arch)
+    open(os.path.join(arch, "patch.bin"), "wb").write(bytes(mutated))
+    m = json.load(open(os.path.join(arch, "manifest")))
+    m["files"]["patch.bin"] = oracle.crc64(bytes(mutated))
+    json.dump(m, open(os.path.join(arch, "manifest"), "w"))
+    seen = set()
+    for _ in range(8):
+        with pytest.raises(foundry.FoundryError) as e:
+            foundry._foundry._pack_store_bytes(arch, False)
+        seen.add(str(e.value))
+    assert len(seen) == 1, seen
+    assert seen.pop().startswith("archive-corruption: node 29 is not the recorded stub")
